@@ -1,0 +1,252 @@
+/*
+ * evconv.h -- C ABI of libevconv.so, the sm_100a implementation of EvConv's
+ * incremental inference path (arXiv 2303.04670).
+ *
+ * The reference (evincr 0.1.0, /root/reference/pkg/src/evincr) is pure
+ * Python + numpy and has no FFI; its "operator API" is the set of Python
+ * functions in increment_ops.py / sparsify.py / tensors.py / events.py that
+ * Graph.incr_step (graph.py:573-630) dispatches to.  Each entry point below
+ * replaces one of those functions (cited per function); the Python package
+ * paper_2303_04670_b200 binds them with ctypes and keeps the reference names
+ * and signatures.  See INTEGRATION.md for the binding.
+ *
+ * Conventions
+ *  - Plain C types only: device pointers, int32/int64 sizes, cudaStream_t
+ *    (passed as void*).  No torch types cross this boundary.
+ *  - Every entry point is asynchronous on `stream`, never allocates, never
+ *    synchronises, and is safe to record into a CUDA graph.  Host-visible
+ *    results (FLOP meters, counts, norms) are written to device memory.
+ *  - Return 0 on success or a negative EVC_E* code; evc_last_error() returns
+ *    a thread-local message for the last failure.  Shape validation with the
+ *    reference's exception texts happens in Python before the call.
+ *  - Tensors are float32, channel-planar (C, H, W) exactly like the
+ *    reference (tensors.py:1-6), with a leading "session" index s for
+ *    batched independent streams.  Tile masks are uint8 (0/1) grids
+ *    (C, ceil(H/th), ceil(W/tw)) like TileMask.flags (tensors.py:65-90).
+ */
+#ifndef EVCONV_H
+#define EVCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVC_ABI_VERSION 1
+
+enum {
+  EVC_OK = 0,
+  EVC_EINVAL = -1, /* bad argument */
+  EVC_ECUDA = -2,  /* CUDA runtime error */
+  EVC_ENOSPC = -3  /* workspace too small */
+};
+
+/* A batch of S increment tensors (one per session) sharing one shape.
+ * value (s,c,h,w) lives at vals[s*vstride + (c*H + h)*W + w];
+ * flag  (s,c,i,j) lives at flags[s*fstride + (c*GH + i)*GW + j],
+ * GH = ceil(H/th), GW = ceil(W/tw).  vstride/fstride let a tensor be a
+ * channel slice of a larger concat buffer (zero-copy inc_concat). */
+typedef struct evc_tensor {
+  float* vals;
+  uint8_t* flags; /* NULL for dense (unmasked) tensors */
+  int64_t vstride;
+  int64_t fstride;
+  int32_t C, H, W;
+  int32_t th, tw;
+} evc_tensor;
+
+/* Static convolution geometry (ConvParams, increment_ops.py:58-77). */
+typedef struct evc_conv_geom {
+  int32_t c_in, c_out, kh, kw, stride, pad;
+  int32_t H, W, Ho, Wo;
+  int32_t th, tw;
+} evc_conv_geom;
+
+/* ---- library ---------------------------------------------------------- */
+int evc_version(void);
+const char* evc_last_error(void);
+/* Loads every kernel module and sets smem attributes (call once, outside
+ * graph capture). */
+int evc_init(void);
+
+/* ---- tile masks (tensors.py) ------------------------------------------ */
+
+/* step_increment (events.py:295-302) + make_tile_mask (tensors.py:93-107):
+ * out.vals = cur - prev, out.flags = exact per-tile any(!=0).
+ * prev/cur are dense batches with per-session stride `in_stride`. */
+int evc_diff_mask(const float* prev, const float* cur, int64_t in_stride,
+                  const evc_tensor* out, int32_t S, void* stream);
+
+/* make_tile_mask (tensors.py:93-107): recompute t.flags from t.vals. */
+int evc_make_tile_mask(const evc_tensor* t, int32_t S, void* stream);
+
+/* np.flatnonzero(flags) for n flags: ascending indices of nonzero bytes,
+ * count written to *count.  Warp-ballot + block prefix scan in two
+ * deterministic launches.  idx must hold n entries; scratch must hold
+ * evc_compact_scratch(n) int32 entries. */
+int64_t evc_compact_scratch(int64_t n);
+int evc_compact(const uint8_t* flags, int64_t n, int32_t* idx, int32_t* count,
+                int32_t* scratch, void* stream);
+
+/* Per-session count of True flags of t (TileMask.false_fraction,
+ * tensors.py:86-87; graph.py:632-636).  counts[s] (int32) is ACCUMULATED
+ * into -- zero it first. */
+int evc_count_flags(const evc_tensor* t, int32_t S, int32_t* counts, void* stream);
+
+/* integrate (tensors.py:167-174, graph.py:615-616): y_run += dx on live
+ * tiles.  y_run is a dense batch with stride y_stride. */
+int evc_integrate(float* y_run, int64_t y_stride, const evc_tensor* dx,
+                  int32_t S, void* stream);
+
+/* Copy a masked tensor (values on live-or-previously-live tiles, flags)
+ * into another (used when a concat part cannot be aliased). */
+int evc_copy_masked(const evc_tensor* src, const evc_tensor* dst, int32_t S,
+                    void* stream);
+
+/* Dense strided copy of S x (C,H,W) float blocks. */
+int evc_copy_dense(const float* src, int64_t src_stride, float* dst,
+                   int64_t dst_stride, int64_t n_per_session, int32_t S,
+                   void* stream);
+
+/* Graph.drift (graph.py:646-654): out[s] = max|a - b| (float32 bits kept
+ * exact).  out must be zeroed first. */
+int evc_max_abs_diff(const float* a, int64_t a_stride, const float* b,
+                     int64_t b_stride, int64_t n_per_session, int32_t S,
+                     float* out, void* stream);
+
+/* ---- convolution (increment_ops.py:126-194, tensors.py:205-228) ------- */
+
+/* Host helper: length (int32 entries) of the static per-layer table used
+ * by the mask/meter and gather kernels, and its contents.  Upload the
+ * table to device memory once per layer. */
+int64_t evc_conv_table_len(const evc_conv_geom* g);
+int evc_conv_table_fill(const evc_conv_geom* g, int32_t* host_table);
+
+/* Mask propagation + FLOP meter of inc_conv2d for a batch:
+ *  - in_true[s]  : number of True input flags (from evc_count_flags)
+ *  - writes out.flags (broadcast over C_out, increment_ops.py:193-194),
+ *    zeroes output tiles that were live last step and are dead now,
+ *  - tile_active[s*T + t] (uint8, T = output tiles per session),
+ *  - meter[s] += performed FLOPs (int64, exact reference meter incl. the
+ *    all-true / all-false shortcuts at increment_ops.py:148-154).
+ * `table` is the device copy of evc_conv_table_fill's output. */
+int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
+                  const evc_tensor* out, const int32_t* table,
+                  const int32_t* in_true, uint8_t* tile_active,
+                  int64_t* meter, int32_t S, void* stream);
+
+/* Workspace floats needed by evc_conv_gemm for `max_tiles` active output
+ * tiles and `splits` K-splits. */
+int64_t evc_conv_workspace(const evc_conv_geom* g, int64_t max_tiles, int32_t splits);
+
+/* Gather -> GEMM -> scatter over active output tiles.
+ * tile_list/tile_count: ascending (s*T + t) entries (evc_compact output);
+ * tile_list == NULL means every tile of every session (dense pass).
+ * weight: (C_out, C_in, KH, KW) fp32 as stored by the reference
+ * (graph.py:457-467); bias may be NULL (increments drop it).
+ * splits > 1 uses the fp32 workspace and a deterministic reduction. */
+int evc_conv_gemm(const evc_conv_geom* g, const evc_tensor* in,
+                  const float* weight, const float* bias, const evc_tensor* out,
+                  const int32_t* table, const int32_t* tile_list,
+                  const int32_t* tile_count, int32_t S, int32_t splits,
+                  float* workspace, void* stream);
+
+/* ---- nonlinearities / elementwise (increment_ops.py:226-310) ---------- */
+
+enum { EVC_ACT_RELU = 0, EVC_ACT_SIGMOID = 1, EVC_ACT_TANH = 2, EVC_ACT_LEAKY = 3 };
+
+/* inc_activation (increment_ops.py:232-238): y = f(acc+dx) - f(acc);
+ * acc += dx; y.flags = dx.flags.  acc is a dense batch (stride acc_stride). */
+int evc_act_delta(const evc_tensor* dx, float* acc, int64_t acc_stride,
+                  const evc_tensor* y, int32_t kind, float alpha, int32_t S,
+                  void* stream);
+
+/* Dense activation (graph.py:523-526): y = f(x); acc = x when acc != NULL. */
+int evc_act_dense(const float* x, int64_t x_stride, float* y, int64_t y_stride,
+                  float* acc, int64_t acc_stride, int64_t n_per_session,
+                  int32_t kind, float alpha, int32_t S, void* stream);
+
+/* sparsify_step (sparsify.py:54-78) for a batch.  k[s], norm_ema[s] are
+ * float64 device scalars (SparsifyState.k / .norm_ema); delta is the
+ * residual (dense batch); dlive (uint8, per tile) tracks tiles whose
+ * residual is nonzero.  partials (float64) receives per-block sums of
+ * corrected^2: partials[s*GH*C + c*GH + i]. */
+int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
+                 uint8_t* dlive, const evc_tensor* y, const double* k,
+                 double* partials, int32_t S, void* stream);
+
+/* Norm / EMA / k update (sparsify.py:72-76) after evc_sparsify, or the
+ * reset (sparsify.py:43-51) when reset != 0 (norm_ema = norm, and
+ * k = tp*norm if tp > 0).  n_partials per session. */
+int evc_sparsify_finalize(const double* partials, int64_t n_partials,
+                          double* norm_ema, double* k, double tp,
+                          double ema_decay, int32_t reset, int32_t S,
+                          void* stream);
+
+/* Per-session partial sums of x^2 for the dense reset norm:
+ * partials[s*n_blocks + b]; returns blocks used in *n_blocks_out (host). */
+int evc_sumsq_dense(const float* x, int64_t x_stride, int64_t n_per_session,
+                    double* partials, int32_t n_blocks, int32_t S, void* stream);
+
+/* inc_add (increment_ops.py:226-229). */
+int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y,
+            int32_t S, void* stream);
+
+/* inc_mul (increment_ops.py:241-254): y = (acc_a+a)*b + acc_b*a. */
+int evc_mul(const evc_tensor* a, const evc_tensor* b, float* acc_a,
+            float* acc_b, int64_t acc_stride, const evc_tensor* y, int32_t S,
+            void* stream);
+
+/* Dense elementwise for the dense pass: op 0 = add, 1 = mul (graph.py:530-537). */
+int evc_binary_dense(const float* a, int64_t a_stride, const float* b,
+                     int64_t b_stride, float* y, int64_t y_stride,
+                     int64_t n_per_session, int32_t op, int32_t S, void* stream);
+
+/* inc_upsample (increment_ops.py:271-285) / dense_upsample
+ * (tensors.py:259-282): mode 0 nearest, 1 bilinear.  When in->flags is
+ * NULL the call is the dense operator (no masks). */
+int evc_upsample(const evc_tensor* in, const evc_tensor* out, int32_t factor,
+                 int32_t mode, int32_t S, void* stream);
+
+/* inc_maxpool (increment_ops.py:288-310): y = pool(acc+dx) - pool(acc),
+ * then acc += dx.  Dense maxpool (tensors.py:242-256) when acc == NULL. */
+int evc_maxpool(const evc_tensor* in, float* acc, int64_t acc_stride,
+                const evc_tensor* out, int32_t wh, int32_t ww, int32_t stride,
+                int32_t S, void* stream);
+
+/* inc_linear + flatten_increment (increment_ops.py:197-223): runs of th*tw
+ * flat elements.  With in->flags == NULL run liveness is recomputed from the
+ * values (flatten_increment); otherwise `in` must be the (1,1,L) flattened
+ * increment with tile (1,run) and its flags are used.  y[f] = sum over live runs;
+ * meter[s] += 2*F*live_elements.  dense != 0 computes W@x + bias over all
+ * runs (dense_linear, tensors.py:231-239) and skips the meter.
+ * workspace: evc_linear_workspace() floats. */
+int64_t evc_linear_workspace(int32_t F, int64_t L, int32_t run, int32_t S);
+int evc_linear(const evc_tensor* in, const float* weight, const float* bias,
+               const evc_tensor* out, int32_t F, int32_t dense,
+               int64_t* meter, float* workspace, int32_t S, void* stream);
+
+/* ---- events (events.py:240-302) -------------------------------------- */
+
+enum { EVC_ENC_COUNT = 0, EVC_ENC_TIMESTAMP = 1, EVC_ENC_VOXEL = 2 };
+
+/* Workspace bytes for evc_bin_events with up to n_events in the window. */
+int64_t evc_bin_events_workspace(int64_t n_events, int32_t H, int32_t W, int32_t bins);
+
+/* encode (events.py:251-292), atomic-free and bit-exact: events
+ * [lo, hi) of the sorted stream are stable-radix-sorted by pixel key, then
+ * each pixel run is folded in time order (voxel: all lower-hat adds, then
+ * all upper-hat adds, each f32(f64(acc)+v)).  out is (C,H,W) float32 with
+ * C = 2 (count/timestamp) or bins (voxel). */
+int evc_bin_events(const uint64_t* t, const uint16_t* x, const uint16_t* y,
+                   const int8_t* p, int64_t lo, int64_t hi, int64_t tau,
+                   int64_t delta, int32_t H, int32_t W, int32_t kind,
+                   int32_t bins, float* out, void* workspace,
+                   int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EVCONV_H */

@@ -1,0 +1,130 @@
+// Shared helpers for libevconv (sm_100a).  Internal header.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/evconv.h"
+
+namespace evc {
+
+void set_error(const std::string& msg);
+
+#define EVC_CHECK_ARG(cond, msg)                 \
+  do {                                           \
+    if (!(cond)) {                               \
+      ::evc::set_error(std::string("evc: ") + (msg)); \
+      return EVC_EINVAL;                         \
+    }                                            \
+  } while (0)
+
+#define EVC_LAUNCH_CHECK(what)                                              \
+  do {                                                                      \
+    cudaError_t e__ = cudaGetLastError();                                   \
+    if (e__ != cudaSuccess) {                                               \
+      ::evc::set_error(std::string("evc: ") + (what) + ": " + cudaGetErrorString(e__)); \
+      return EVC_ECUDA;                                                     \
+    }                                                                       \
+  } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+static inline int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Geometry of a tile grid.
+struct Grid {
+  int C, H, W, th, tw, GH, GW;
+};
+
+static inline Grid grid_of(const evc_tensor& t) {
+  Grid g;
+  g.C = t.C;
+  g.H = t.H;
+  g.W = t.W;
+  g.th = t.th;
+  g.tw = t.tw;
+  g.GH = (t.H + t.th - 1) / t.th;
+  g.GW = (t.W + t.tw - 1) / t.tw;
+  return g;
+}
+
+// Device view of an evc_tensor (passed by value to kernels).
+struct TView {
+  float* v;
+  uint8_t* f;
+  int64_t vs, fs;
+  int C, H, W, th, tw, GH, GW;
+  __host__ __device__ __forceinline__ float* plane(int s, int c) const {
+    return v + (int64_t)s * vs + (int64_t)c * H * W;
+  }
+  __host__ __device__ __forceinline__ uint8_t* fplane(int s, int c) const {
+    return f + (int64_t)s * fs + (int64_t)c * GH * GW;
+  }
+};
+
+static inline TView view_of(const evc_tensor& t) {
+  TView r;
+  r.v = t.vals;
+  r.f = t.flags;
+  r.vs = t.vstride;
+  r.fs = t.fstride;
+  r.C = t.C;
+  r.H = t.H;
+  r.W = t.W;
+  r.th = t.th;
+  r.tw = t.tw;
+  r.GH = (t.H + t.th - 1) / t.th;
+  r.GW = (t.W + t.tw - 1) / t.tw;
+  return r;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum (blockDim.x multiple of 32, <= 1024).  Result valid in thread 0.
+template <typename T, typename F>
+__device__ __forceinline__ T block_sum(T v, F wsum) {
+  __shared__ T red[32];
+  v = wsum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  T r = 0;
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    r = lane < nw ? red[lane] : T(0);
+    r = wsum(r);
+  }
+  return r;
+}
+
+}  // namespace evc
+
+namespace evc {
+// Per-translation-unit module loaders (force lazy-loaded modules in before
+// any CUDA-graph capture).
+int init_masks();
+int init_conv();
+int init_elementwise();
+int init_linear_events();
+}  // namespace evc

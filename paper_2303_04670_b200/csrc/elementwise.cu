@@ -1,0 +1,514 @@
+// Increment-domain nonlinearities, sparsification, add/mul, upsample and
+// maxpool (increment_ops.py:226-310, sparsify.py:54-78).
+//
+// All masked kernels are "band" kernels (one CTA per session x channel x
+// tile-row) and process a tile when it is live in an input OR was live in the
+// output last step (old output flag).  Recomputing a previously-live tile from
+// all-zero inputs writes exact zeros, which keeps the invariant that values
+// under False flags are 0 (TileMask soundness, tensors.py:65-72) without a
+// separate clearing pass.  Float arithmetic uses explicit _rn intrinsics so no
+// FMA contraction changes the reference's float32 rounding sequence.
+
+#include "common.cuh"
+
+namespace evc {
+
+__device__ __forceinline__ float act_f(float x, int kind, float alpha) {
+  switch (kind) {
+    case EVC_ACT_RELU:
+      return fmaxf(x, 0.0f);
+    case EVC_ACT_SIGMOID:
+      return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+    case EVC_ACT_TANH:
+      return tanhf(x);
+    default:
+      return x > 0.0f ? x : __fmul_rn(alpha, x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// inc_activation (increment_ops.py:232-238)
+// ---------------------------------------------------------------------------
+__global__ void k_act_delta(TView d, float* __restrict__ acc, int64_t as, TView y, int kind, float alpha) {
+  extern __shared__ uint8_t s_proc[];
+  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
+  const uint8_t* fi = d.fplane(s, c) + (int64_t)i * d.GW;
+  uint8_t* fo = y.fplane(s, c) + (int64_t)i * y.GW;
+  bool any = false;
+  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) {
+    const uint8_t p = fi[j] | fo[j];
+    s_proc[j] = p;
+    any |= p != 0;
+  }
+  if (!__syncthreads_or(any)) return;
+  const float* dv = d.plane(s, c);
+  float* yv = y.plane(s, c);
+  float* av = acc + (int64_t)s * as + (int64_t)c * d.H * d.W;
+  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
+  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
+    if (!s_proc[x / d.tw]) continue;
+    for (int r = r0; r < r1; ++r) {
+      const int64_t e = (int64_t)r * d.W + x;
+      const float a0 = av[e];
+      const float a1 = __fadd_rn(a0, dv[e]);
+      yv[e] = __fsub_rn(act_f(a1, kind, alpha), act_f(a0, kind, alpha));
+      av[e] = a1;
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) fo[j] = fi[j];
+}
+
+__global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __restrict__ y, int64_t ys,
+                            float* __restrict__ acc, int64_t as, int64_t n, int kind, float alpha) {
+  const int s = blockIdx.y;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[(int64_t)s * xs + e];
+    y[(int64_t)s * ys + e] = act_f(v, kind, alpha);
+    if (acc) acc[(int64_t)s * as + e] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// sparsify_step (sparsify.py:54-78)
+// ---------------------------------------------------------------------------
+__global__ void k_sparsify(TView d, float* __restrict__ delta, int64_t ds, uint8_t* __restrict__ dlive, TView y,
+                           const double* __restrict__ kdev, double* __restrict__ partials) {
+  extern __shared__ uint8_t s_m[];  // proc | nz_y | nz_d   (3 x GW)
+  uint8_t* s_proc = s_m;
+  uint8_t* s_ny = s_m + d.GW;
+  uint8_t* s_nd = s_m + 2 * d.GW;
+  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
+  const uint8_t* fi = d.fplane(s, c) + (int64_t)i * d.GW;
+  uint8_t* fo = y.fplane(s, c) + (int64_t)i * y.GW;
+  uint8_t* dl = dlive + (int64_t)s * d.C * d.GH * d.GW + ((int64_t)c * d.GH + i) * d.GW;
+  bool any = false;
+  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) {
+    const uint8_t p = fi[j] | fo[j] | dl[j];
+    s_proc[j] = p;
+    s_ny[j] = 0;
+    s_nd[j] = 0;
+    any |= p != 0;
+  }
+  double* part = partials + (int64_t)s * d.C * d.GH + (int64_t)c * d.GH + i;
+  if (!__syncthreads_or(any)) {
+    if (threadIdx.x == 0) *part = 0.0;
+    return;
+  }
+  const double k = kdev[s];
+  const bool use_k = k > 0.0;
+  const float k32 = __double2float_rn(k);
+  const float* dv = d.plane(s, c);
+  float* yv = y.plane(s, c);
+  float* del = delta + (int64_t)s * ds + (int64_t)c * d.H * d.W;
+  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
+  double ss = 0.0;
+  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
+    const int j = x / d.tw;
+    if (!s_proc[j]) continue;
+    bool nzy = false, nzd = false;
+    for (int r = r0; r < r1; ++r) {
+      const int64_t e = (int64_t)r * d.W + x;
+      const float corr = __fadd_rn(del[e], dv[e]);
+      float out, nd;
+      if (use_k) {
+        const float q = floorf(__fadd_rn(0.5f, __fdiv_rn(corr, k32)));
+        out = __fmul_rn(k32, q);
+        nd = __fsub_rn(corr, out);
+      } else {
+        out = corr;
+        nd = 0.0f;
+      }
+      yv[e] = out;
+      del[e] = nd;
+      ss += (double)corr * (double)corr;
+      nzy |= out != 0.0f;
+      nzd |= nd != 0.0f;
+    }
+    if (nzy) s_ny[j] = 1;
+    if (nzd) s_nd[j] = 1;
+  }
+  ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
+  if (threadIdx.x == 0) *part = ss;
+  __syncthreads();
+  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) {
+    fo[j] = s_ny[j];
+    dl[j] = s_nd[j];
+  }
+}
+
+__global__ void k_sparsify_finalize(const double* __restrict__ partials, int64_t n, double* norm_ema, double* kdev,
+                                    double tp, double decay, int reset) {
+  const int s = blockIdx.x;
+  double sum = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) sum += partials[(int64_t)s * n + e];
+  sum = block_sum<double>(sum, [](double v) { return warp_sum_d(v); });
+  if (threadIdx.x == 0) {
+    // np.linalg.norm of float32 data returns float32 (sparsify.py:49,73)
+    const double norm = (double)__double2float_rn(sqrt(sum));
+    double ne;
+    if (reset) {
+      ne = norm;
+    } else {
+      ne = __dadd_rn(__dmul_rn(decay, norm_ema[s]), __dmul_rn(__dsub_rn(1.0, decay), norm));
+    }
+    norm_ema[s] = ne;
+    if (tp > 0.0) kdev[s] = __dmul_rn(tp, ne);
+  }
+}
+
+__global__ void k_sumsq(const float* __restrict__ x, int64_t xs, int64_t n, double* partials) {
+  const int s = blockIdx.y;
+  double ss = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[(int64_t)s * xs + e];
+    ss += v * v;
+  }
+  ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
+  if (threadIdx.x == 0) partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
+}
+
+// ---------------------------------------------------------------------------
+// inc_add / inc_mul (increment_ops.py:226-254)
+// ---------------------------------------------------------------------------
+template <bool MUL>
+__global__ void k_binary(TView a, TView b, float* __restrict__ sa, float* __restrict__ sb, int64_t ss, TView y) {
+  extern __shared__ uint8_t s_proc[];
+  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
+  const uint8_t* fa = a.fplane(s, c) + (int64_t)i * a.GW;
+  const uint8_t* fb = b.fplane(s, c) + (int64_t)i * b.GW;
+  uint8_t* fo = y.fplane(s, c) + (int64_t)i * y.GW;
+  bool any = false;
+  for (int j = threadIdx.x; j < a.GW; j += blockDim.x) {
+    const uint8_t p = fa[j] | fb[j] | fo[j];
+    s_proc[j] = p;
+    any |= p != 0;
+  }
+  if (!__syncthreads_or(any)) return;
+  const float* av = a.plane(s, c);
+  const float* bv = b.plane(s, c);
+  float* yv = y.plane(s, c);
+  const int64_t poff = (int64_t)s * ss + (int64_t)c * a.H * a.W;
+  const int r0 = i * a.th, r1 = min(a.H, r0 + a.th);
+  for (int x = threadIdx.x; x < a.W; x += blockDim.x) {
+    if (!s_proc[x / a.tw]) continue;
+    for (int r = r0; r < r1; ++r) {
+      const int64_t e = (int64_t)r * a.W + x;
+      const float va = av[e], vb = bv[e];
+      if (MUL) {
+        const float t1 = __fadd_rn(sa[poff + e], va);
+        yv[e] = __fadd_rn(__fmul_rn(t1, vb), __fmul_rn(sb[poff + e], va));
+        sa[poff + e] = t1;
+        sb[poff + e] = __fadd_rn(sb[poff + e], vb);
+      } else {
+        yv[e] = __fadd_rn(va, vb);
+      }
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < a.GW; j += blockDim.x) fo[j] = fa[j] | fb[j];
+}
+
+__global__ void k_binary_dense(const float* __restrict__ a, int64_t as, const float* __restrict__ b, int64_t bs,
+                               float* __restrict__ y, int64_t ys, int64_t n, int op) {
+  const int s = blockIdx.y;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const float va = a[(int64_t)s * as + e], vb = b[(int64_t)s * bs + e];
+    y[(int64_t)s * ys + e] = op ? __fmul_rn(va, vb) : __fadd_rn(va, vb);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// upsample (increment_ops.py:271-285, tensors.py:259-282)
+// ---------------------------------------------------------------------------
+struct Tap {
+  int i0, i1;
+  float w0, w1;
+};
+
+// half-pixel source taps of one output coordinate (tensors.py:259-266)
+__device__ __forceinline__ Tap bilinear_tap(int o, int n_in, int f) {
+  const float src = __fsub_rn(__fdiv_rn(__fadd_rn((float)o, 0.5f), (float)f), 0.5f);
+  const float fl = floorf(src);
+  const float frac = __fsub_rn(src, fl);
+  Tap t;
+  const int i0 = (int)fl;
+  t.i1 = min(max(i0 + 1, 0), n_in - 1);
+  t.i0 = min(max(i0, 0), n_in - 1);
+  t.w1 = frac;
+  t.w0 = __fsub_rn(1.0f, frac);
+  return t;
+}
+
+__global__ void k_upsample(TView in, TView out, int f, int mode) {
+  extern __shared__ uint8_t s_m[];  // proc | new (2 x GWo)
+  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
+  const bool masked = in.f != nullptr;
+  const int u0 = i * out.th, u1 = min(out.H, u0 + out.th);
+  uint8_t* s_proc = s_m;
+  uint8_t* s_new = s_m + out.GW;
+  uint8_t* fo = masked ? out.fplane(s, c) + (int64_t)i * out.GW : nullptr;
+  bool any = !masked;
+  if (masked) {
+    int rlo, rhi;
+    if (mode == 0) {
+      rlo = u0 / f;
+      rhi = (u1 - 1) / f;
+    } else {
+      rlo = bilinear_tap(u0, in.H, f).i0;
+      rhi = bilinear_tap(u1 - 1, in.H, f).i1;
+    }
+    const int alo = rlo / in.th, ahi = rhi / in.th;
+    const uint8_t* F = in.fplane(s, c);
+    for (int j = threadIdx.x; j < out.GW; j += blockDim.x) {
+      const int v0 = j * out.tw, v1 = min(out.W, v0 + out.tw);
+      int clo, chi;
+      if (mode == 0) {
+        clo = v0 / f;
+        chi = (v1 - 1) / f;
+      } else {
+        clo = bilinear_tap(v0, in.W, f).i0;
+        chi = bilinear_tap(v1 - 1, in.W, f).i1;
+      }
+      const int blo = clo / in.tw, bhi = chi / in.tw;
+      uint8_t nf = 0;
+      for (int a = alo; a <= ahi; ++a)
+        for (int b = blo; b <= bhi; ++b) nf |= F[a * in.GW + b];
+      nf = nf != 0;
+      s_new[j] = nf;
+      s_proc[j] = nf | fo[j];
+      any |= s_proc[j] != 0;
+    }
+  }
+  if (!__syncthreads_or(any)) return;
+  const float* xv = in.plane(s, c);
+  float* yv = out.plane(s, c);
+  for (int v = threadIdx.x; v < out.W; v += blockDim.x) {
+    if (masked && !s_proc[v / out.tw]) continue;
+    if (mode == 0) {
+      const int sx = v / f;
+      for (int u = u0; u < u1; ++u) yv[(int64_t)u * out.W + v] = xv[(int64_t)(u / f) * in.W + sx];
+    } else {
+      const Tap tc = bilinear_tap(v, in.W, f);
+      for (int u = u0; u < u1; ++u) {
+        const Tap tr = bilinear_tap(u, in.H, f);
+        const float* x0 = xv + (int64_t)tr.i0 * in.W;
+        const float* x1 = xv + (int64_t)tr.i1 * in.W;
+        const float ra = __fadd_rn(__fmul_rn(x0[tc.i0], tr.w0), __fmul_rn(x1[tc.i0], tr.w1));
+        const float rb = __fadd_rn(__fmul_rn(x0[tc.i1], tr.w0), __fmul_rn(x1[tc.i1], tr.w1));
+        yv[(int64_t)u * out.W + v] = __fadd_rn(__fmul_rn(ra, tc.w0), __fmul_rn(rb, tc.w1));
+      }
+    }
+  }
+  if (masked) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < out.GW; j += blockDim.x) fo[j] = s_new[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// maxpool (increment_ops.py:288-310, tensors.py:242-256)
+// ---------------------------------------------------------------------------
+// Does some pooling window of outputs [o0, o1) read a pixel of input tile a?
+__device__ __forceinline__ bool pool_covers(int a, int o0, int o1, int st, int win, int tile) {
+  for (int o = o0; o < o1; ++o) {
+    const int lo = o * st, hi = lo + win - 1;
+    if (lo / tile <= a && a <= hi / tile) return true;
+  }
+  return false;
+}
+
+__global__ void k_maxpool(TView in, const float* __restrict__ acc, int64_t as, TView out, int wh, int ww, int st) {
+  extern __shared__ uint8_t s_m[];
+  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
+  const bool masked = in.f != nullptr;
+  const int u0 = i * out.th, u1 = min(out.H, u0 + out.th);
+  uint8_t* s_proc = s_m;
+  uint8_t* s_new = s_m + out.GW;
+  uint8_t* fo = masked ? out.fplane(s, c) + (int64_t)i * out.GW : nullptr;
+  bool any = !masked;
+  if (masked) {
+    const int alo = (u0 * st) / in.th, ahi = ((u1 - 1) * st + wh - 1) / in.th;
+    const uint8_t* F = in.fplane(s, c);
+    for (int j = threadIdx.x; j < out.GW; j += blockDim.x) {
+      const int v0 = j * out.tw, v1 = min(out.W, v0 + out.tw);
+      const int blo = (v0 * st) / in.tw, bhi = ((v1 - 1) * st + ww - 1) / in.tw;
+      uint8_t nf = 0;
+      for (int a = alo; a <= ahi; ++a) {
+        if (!pool_covers(a, u0, u1, st, wh, in.th)) continue;  // stride > window leaves gaps
+        for (int b = blo; b <= bhi; ++b)
+          if (pool_covers(b, v0, v1, st, ww, in.tw)) nf |= F[a * in.GW + b];
+      }
+      nf = nf != 0;
+      s_new[j] = nf;
+      s_proc[j] = nf | fo[j];
+      any |= s_proc[j] != 0;
+    }
+  }
+  if (!__syncthreads_or(any)) return;
+  const float* xv = in.plane(s, c);
+  const float* av = acc ? acc + (int64_t)s * as + (int64_t)c * in.H * in.W : nullptr;
+  float* yv = out.plane(s, c);
+  for (int v = threadIdx.x; v < out.W; v += blockDim.x) {
+    if (masked && !s_proc[v / out.tw]) continue;
+    for (int u = u0; u < u1; ++u) {
+      float mb = -INFINITY, ma = -INFINITY;
+      for (int r = 0; r < wh; ++r)
+        for (int q = 0; q < ww; ++q) {
+          const int64_t e = (int64_t)(u * st + r) * in.W + v * st + q;
+          if (av) {
+            const float a0 = av[e];
+            mb = fmaxf(mb, a0);
+            ma = fmaxf(ma, __fadd_rn(a0, xv[e]));
+          } else {
+            ma = fmaxf(ma, xv[e]);
+          }
+        }
+      yv[(int64_t)u * out.W + v] = av ? __fsub_rn(ma, mb) : ma;
+    }
+  }
+  if (masked) {
+    __syncthreads();
+    for (int j = threadIdx.x; j < out.GW; j += blockDim.x) fo[j] = s_new[j];
+  }
+}
+
+// acc += dx on live input tiles (AccState.fold, increment_ops.py:93-94)
+__global__ void k_fold(TView d, float* __restrict__ acc, int64_t as) {
+  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
+  const uint8_t* f = d.fplane(s, c) + (int64_t)i * d.GW;
+  bool any = false;
+  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) any |= f[j] != 0;
+  if (!__syncthreads_or(any)) return;
+  const float* dv = d.plane(s, c);
+  float* av = acc + (int64_t)s * as + (int64_t)c * d.H * d.W;
+  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
+  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
+    if (!f[x / d.tw]) continue;
+    for (int r = r0; r < r1; ++r) {
+      const int64_t e = (int64_t)r * d.W + x;
+      av[e] = __fadd_rn(av[e], dv[e]);
+    }
+  }
+}
+
+static int bt(int W) { return W >= 192 ? 256 : (W >= 96 ? 128 : (W >= 48 ? 64 : 32)); }
+
+static int dense_blocks(int64_t n) {
+  int64_t b = cdiv64(n, 256 * 4);
+  if (b > 2048) b = 2048;
+  return (int)(b > 0 ? b : 1);
+}
+
+}  // namespace evc
+
+using namespace evc;
+
+extern "C" {
+
+int evc_act_delta(const evc_tensor* dx, float* acc, int64_t acc_stride, const evc_tensor* y, int32_t kind,
+                  float alpha, int32_t S, void* stream) {
+  EVC_CHECK_ARG(dx && y && acc && dx->flags && y->flags && S > 0, "act_delta: null argument");
+  EVC_CHECK_ARG(kind >= 0 && kind <= 3, "act_delta: unknown activation");
+  TView d = view_of(*dx), o = view_of(*y);
+  k_act_delta<<<dim3(d.GH, d.C, S), bt(d.W), d.GW, as_stream(stream)>>>(d, acc, acc_stride, o, kind, alpha);
+  EVC_LAUNCH_CHECK("act_delta");
+  return EVC_OK;
+}
+
+int evc_act_dense(const float* x, int64_t xs, float* y, int64_t ys, float* acc, int64_t as, int64_t n, int32_t kind,
+                  float alpha, int32_t S, void* stream) {
+  EVC_CHECK_ARG(x && y && S > 0, "act_dense: null argument");
+  k_act_dense<<<dim3(dense_blocks(n), S), 256, 0, as_stream(stream)>>>(x, xs, y, ys, acc, as, n, kind, alpha);
+  EVC_LAUNCH_CHECK("act_dense");
+  return EVC_OK;
+}
+
+int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y,
+                 const double* k, double* partials, int32_t S, void* stream) {
+  EVC_CHECK_ARG(dx && y && delta && dlive && k && partials && dx->flags && y->flags && S > 0,
+                "sparsify: null argument");
+  TView d = view_of(*dx), o = view_of(*y);
+  k_sparsify<<<dim3(d.GH, d.C, S), bt(d.W), 3 * d.GW, as_stream(stream)>>>(d, delta, ds, dlive, o, k, partials);
+  EVC_LAUNCH_CHECK("sparsify");
+  return EVC_OK;
+}
+
+int evc_sparsify_finalize(const double* partials, int64_t n, double* norm_ema, double* k, double tp, double decay,
+                          int32_t reset, int32_t S, void* stream) {
+  EVC_CHECK_ARG(partials && norm_ema && k && S > 0, "sparsify_finalize: null argument");
+  k_sparsify_finalize<<<S, 256, 0, as_stream(stream)>>>(partials, n, norm_ema, k, tp, decay, reset);
+  EVC_LAUNCH_CHECK("sparsify_finalize");
+  return EVC_OK;
+}
+
+int evc_sumsq_dense(const float* x, int64_t xs, int64_t n, double* partials, int32_t n_blocks, int32_t S,
+                    void* stream) {
+  EVC_CHECK_ARG(x && partials && n_blocks > 0 && S > 0, "sumsq_dense: null argument");
+  k_sumsq<<<dim3(n_blocks, S), 256, 0, as_stream(stream)>>>(x, xs, n, partials);
+  EVC_LAUNCH_CHECK("sumsq_dense");
+  return EVC_OK;
+}
+
+int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y, int32_t S, void* stream) {
+  EVC_CHECK_ARG(a && b && y && a->flags && b->flags && y->flags && S > 0, "add: null argument");
+  TView va = view_of(*a), vb = view_of(*b), vy = view_of(*y);
+  k_binary<false><<<dim3(va.GH, va.C, S), bt(va.W), va.GW, as_stream(stream)>>>(va, vb, nullptr, nullptr, 0, vy);
+  EVC_LAUNCH_CHECK("add");
+  return EVC_OK;
+}
+
+int evc_mul(const evc_tensor* a, const evc_tensor* b, float* acc_a, float* acc_b, int64_t acc_stride,
+            const evc_tensor* y, int32_t S, void* stream) {
+  EVC_CHECK_ARG(a && b && y && acc_a && acc_b && a->flags && b->flags && y->flags && S > 0, "mul: null argument");
+  TView va = view_of(*a), vb = view_of(*b), vy = view_of(*y);
+  k_binary<true><<<dim3(va.GH, va.C, S), bt(va.W), va.GW, as_stream(stream)>>>(va, vb, acc_a, acc_b, acc_stride, vy);
+  EVC_LAUNCH_CHECK("mul");
+  return EVC_OK;
+}
+
+int evc_binary_dense(const float* a, int64_t as, const float* b, int64_t bs, float* y, int64_t ys, int64_t n,
+                     int32_t op, int32_t S, void* stream) {
+  EVC_CHECK_ARG(a && b && y && S > 0, "binary_dense: null argument");
+  k_binary_dense<<<dim3(dense_blocks(n), S), 256, 0, as_stream(stream)>>>(a, as, b, bs, y, ys, n, op);
+  EVC_LAUNCH_CHECK("binary_dense");
+  return EVC_OK;
+}
+
+int evc_upsample(const evc_tensor* in, const evc_tensor* out, int32_t factor, int32_t mode, int32_t S,
+                 void* stream) {
+  EVC_CHECK_ARG(in && out && S > 0, "upsample: null argument");
+  EVC_CHECK_ARG(factor == 2 || factor == 4, "upsample: factor must be 2 or 4");
+  EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample: unknown mode");
+  EVC_CHECK_ARG((in->flags == nullptr) == (out->flags == nullptr), "upsample: masks on both or neither");
+  TView vi = view_of(*in), vo = view_of(*out);
+  k_upsample<<<dim3(vo.GH, vo.C, S), bt(vo.W), 2 * vo.GW, as_stream(stream)>>>(vi, vo, factor, mode);
+  EVC_LAUNCH_CHECK("upsample");
+  return EVC_OK;
+}
+
+int evc_maxpool(const evc_tensor* in, float* acc, int64_t acc_stride, const evc_tensor* out, int32_t wh, int32_t ww,
+                int32_t stride, int32_t S, void* stream) {
+  EVC_CHECK_ARG(in && out && S > 0 && wh > 0 && ww > 0 && stride > 0, "maxpool: bad argument");
+  EVC_CHECK_ARG((in->flags == nullptr) == (out->flags == nullptr), "maxpool: masks on both or neither");
+  EVC_CHECK_ARG(!acc || in->flags, "maxpool: incremental mode needs masks");
+  TView vi = view_of(*in), vo = view_of(*out);
+  cudaStream_t st = as_stream(stream);
+  k_maxpool<<<dim3(vo.GH, vo.C, S), bt(vo.W), 2 * vo.GW, st>>>(vi, acc, acc_stride, vo, wh, ww, stride);
+  EVC_LAUNCH_CHECK("maxpool");
+  if (acc) {
+    k_fold<<<dim3(vi.GH, vi.C, S), bt(vi.W), 0, st>>>(vi, acc, acc_stride);
+    EVC_LAUNCH_CHECK("maxpool_fold");
+  }
+  return EVC_OK;
+}
+
+}  // extern "C"
+
+namespace evc {
+int init_elementwise() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_sparsify) != cudaSuccess) return EVC_ECUDA;
+  return EVC_OK;
+}
+}  // namespace evc

@@ -1,0 +1,1032 @@
+"""Model specs, weights and the device-resident inference session (mirrors evincr/graph.py).
+
+``ModelSpec`` / ``NodeSpec`` / ``WeightManifest`` read and write the
+reference's YAML + raw little-endian float32 formats unchanged
+(graph.py:98-371).  ``Graph`` is the B200 session: every per-node buffer
+and state tensor is allocated once at build time in HBM, the whole
+``incr_step`` is one launch sequence of libevconv kernels that reads its
+data-dependent work counts from device memory, and that sequence is
+captured once into a CUDA graph and replayed per increment.  FLOP meters
+and false-tile fractions are device counters that ``FlopReport``
+materialises lazily.
+
+Engine-only knobs (never part of the spec): ``sessions`` runs S independent
+streams in lock-step over shared weights (one batched launch per node);
+``cuda_graph`` toggles capture.
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+import torch
+import yaml
+
+from . import _lib
+from .tensors import (
+    IncrementTensor,
+    TileMask,
+    TileShape,
+    as_bias,
+    as_matrix,
+    as_tensor,
+    choose_splits,
+    conv_geometry,
+    conv_output_hw,
+    grid_shape,
+)
+
+__all__ = [
+    "GraphError",
+    "CycleError",
+    "WeightError",
+    "ShapeError",
+    "NodeSpec",
+    "ModelSpec",
+    "WeightManifest",
+    "FlopReport",
+    "Graph",
+    "build",
+]
+
+ACTIVATION_KINDS = ("relu", "sigmoid", "tanh", "leaky_relu")
+NODE_KINDS = ACTIVATION_KINDS + ("conv", "linear", "add", "mul", "concat", "upsample", "maxpool", "sparsify")
+_ARITY = {"add": 2, "mul": 2}
+DEFAULT_REFRESH_INTERVAL = 64
+
+
+class GraphError(ValueError):
+    pass
+
+
+class CycleError(GraphError):
+    pass
+
+
+class WeightError(GraphError):
+    pass
+
+
+class ShapeError(GraphError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# specs  (graph.py:98-305)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class NodeSpec:
+    """One operator node (graph.py:98-120)."""
+
+    id: str
+    kind: str
+    inputs: list
+    attrs: dict = field(default_factory=dict)
+
+    def to_dict(self) -> dict:
+        d = {"id": self.id, "kind": self.kind, "inputs": list(self.inputs)}
+        d.update(self.attrs)
+        return d
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "NodeSpec":
+        d = dict(d)
+        return cls(id=str(d.pop("id")), kind=str(d.pop("kind")), inputs=[str(i) for i in d.pop("inputs")], attrs=d)
+
+
+@dataclass
+class ModelSpec:
+    """Operator DAG with a designated input and output (graph.py:123-263)."""
+
+    name: str
+    input_shape: tuple
+    nodes: list
+    output: str
+    aux_outputs: list = field(default_factory=list)
+    tile: TileShape = field(default_factory=TileShape)
+    input_id: str = "input"
+
+    def topo_order(self) -> list:
+        """Kahn's algorithm, ties broken by node id (graph.py:137-185)."""
+        by_id = {}
+        for n in self.nodes:
+            if n.id == self.input_id:
+                raise GraphError(f"node id {n.id!r} collides with the input id")
+            if n.id in by_id:
+                raise GraphError(f"duplicate node id {n.id!r}")
+            if n.kind not in NODE_KINDS:
+                raise GraphError(f"node {n.id!r}: unknown kind {n.kind!r}")
+            by_id[n.id] = n
+        indeg, users = {}, {}
+        for n in self.nodes:
+            want = _ARITY.get(n.kind)
+            if want is not None and len(n.inputs) != want:
+                raise GraphError(f"node {n.id!r}: {n.kind} takes {want} inputs, got {len(n.inputs)}")
+            if n.kind == "concat" and not n.inputs:
+                raise GraphError(f"node {n.id!r}: concat needs at least one input")
+            if n.kind not in ("add", "mul", "concat") and len(n.inputs) != 1:
+                raise GraphError(f"node {n.id!r}: {n.kind} takes 1 input, got {len(n.inputs)}")
+            deg = 0
+            for i in n.inputs:
+                if i == self.input_id:
+                    continue
+                if i not in by_id:
+                    raise GraphError(f"node {n.id!r} references unknown input {i!r}")
+                users.setdefault(i, []).append(n.id)
+                deg += 1
+            indeg[n.id] = deg
+        ready = sorted(k for k, d in indeg.items() if d == 0)
+        heapq.heapify(ready)
+        order = []
+        while ready:
+            nid = heapq.heappop(ready)
+            order.append(by_id[nid])
+            for u in users.get(nid, ()):
+                indeg[u] -= 1
+                if indeg[u] == 0:
+                    heapq.heappush(ready, u)
+        if len(order) != len(self.nodes):
+            stuck = sorted(set(indeg) - {n.id for n in order})
+            raise CycleError(f"cycle detected among nodes {stuck}")
+        for out in [self.output, *self.aux_outputs]:
+            if out not in by_id:
+                raise GraphError(f"designated output {out!r} is not a node")
+        return order
+
+    def infer_shapes(self) -> dict:
+        shapes = {self.input_id: tuple(self.input_shape)}
+        for n in self.topo_order():
+            shapes[n.id] = _node_out_shape(n, [shapes[i] for i in n.inputs])
+        return shapes
+
+    def _weight_specs(self, shapes) -> list:
+        specs = []
+        for n in self.nodes:
+            if n.kind == "conv":
+                c_in = shapes[n.inputs[0]][0]
+                kh, kw = n.attrs.get("kernel", [3, 3])
+                specs.append((f"{n.id}.weight", (int(n.attrs["out_channels"]), c_in, int(kh), int(kw))))
+                specs.append((f"{n.id}.bias", (int(n.attrs["out_channels"]),)))
+            elif n.kind == "linear":
+                c, h, w = shapes[n.inputs[0]]
+                f = int(n.attrs["out_features"])
+                specs.append((f"{n.id}.weight", (f, c * h * w)))
+                specs.append((f"{n.id}.bias", (f,)))
+        return specs
+
+    def weight_specs(self) -> list:
+        return self._weight_specs(self.infer_shapes())
+
+    def parameter_count(self) -> int:
+        return int(sum(np.prod(s) for _, s in self.weight_specs()))
+
+    def with_tp(self, tp: float) -> "ModelSpec":
+        nodes = []
+        for n in self.nodes:
+            attrs = dict(n.attrs)
+            if n.kind == "sparsify":
+                attrs["tp"] = float(tp)
+            nodes.append(NodeSpec(n.id, n.kind, list(n.inputs), attrs))
+        return ModelSpec(self.name, tuple(self.input_shape), nodes, self.output, list(self.aux_outputs), self.tile,
+                         self.input_id)
+
+    def to_dict(self) -> dict:
+        d = {"name": self.name, "input": {"id": self.input_id, "shape": list(self.input_shape)},
+             "tile": [self.tile.h, self.tile.w], "output": self.output, "nodes": [n.to_dict() for n in self.nodes]}
+        if self.aux_outputs:
+            d["aux_outputs"] = list(self.aux_outputs)
+        return d
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "ModelSpec":
+        inp = d.get("input", {})
+        tile = d.get("tile", [TileShape().h, TileShape().w])
+        return cls(name=str(d.get("name", "model")), input_shape=tuple(int(v) for v in inp["shape"]),
+                   nodes=[NodeSpec.from_dict(nd) for nd in d["nodes"]], output=str(d["output"]),
+                   aux_outputs=[str(a) for a in d.get("aux_outputs", [])], tile=TileShape(int(tile[0]), int(tile[1])),
+                   input_id=str(inp.get("id", "input")))
+
+    def save(self, path) -> None:
+        Path(path).write_text(yaml.safe_dump(self.to_dict(), sort_keys=False))
+
+    @classmethod
+    def load(cls, path) -> "ModelSpec":
+        return cls.from_dict(yaml.safe_load(Path(path).read_text()))
+
+
+def _node_out_shape(n: NodeSpec, ins: list) -> tuple:
+    """graph.py:266-305."""
+    kind = n.kind
+    if kind == "conv":
+        c, h, w = ins[0]
+        kh, kw = (int(v) for v in n.attrs.get("kernel", [3, 3]))
+        try:
+            ho, wo = conv_output_hw(h, w, kh, kw, int(n.attrs.get("stride", 1)), int(n.attrs.get("padding", 0)))
+        except ValueError as exc:
+            raise ShapeError(f"node {n.id!r}: {exc}") from exc
+        return (int(n.attrs["out_channels"]), ho, wo)
+    if kind == "linear":
+        return (int(n.attrs["out_features"]), 1, 1)
+    if kind in ACTIVATION_KINDS or kind == "sparsify":
+        return ins[0]
+    if kind in ("add", "mul"):
+        if ins[0] != ins[1]:
+            raise ShapeError(f"node {n.id!r}: {kind} inputs disagree: {ins[0]} vs {ins[1]}")
+        return ins[0]
+    if kind == "concat":
+        hw = ins[0][1:]
+        for s in ins[1:]:
+            if s[1:] != hw:
+                raise ShapeError(f"node {n.id!r}: concat spatial mismatch: {s} vs {ins[0]}")
+        return (sum(s[0] for s in ins), *hw)
+    if kind == "upsample":
+        c, h, w = ins[0]
+        f = int(n.attrs.get("factor", 2))
+        if f not in (2, 4):
+            raise ShapeError(f"node {n.id!r}: upsample factor must be 2 or 4")
+        return (c, h * f, w * f)
+    if kind == "maxpool":
+        c, h, w = ins[0]
+        wh, ww = (int(v) for v in n.attrs.get("window", [2, 2]))
+        stride = int(n.attrs.get("stride", 2))
+        if wh > h or ww > w:
+            raise ShapeError(f"node {n.id!r}: pool window {wh}x{ww} larger than input {h}x{w}")
+        return (c, (h - wh) // stride + 1, (w - ww) // stride + 1)
+    raise GraphError(f"node {n.id!r}: unknown kind {kind!r}")
+
+
+# ---------------------------------------------------------------------------
+# weights  (graph.py:313-371)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class WeightManifest:
+    """Named tensors at byte ranges of a raw little-endian float32 blob."""
+
+    blob_path: Path
+    entries: list
+
+    def to_dict(self) -> dict:
+        return {"blob": self.blob_path.name, "tensors": self.entries}
+
+    def save(self, path) -> None:
+        Path(path).write_text(yaml.safe_dump(self.to_dict(), sort_keys=False))
+
+    @classmethod
+    def load(cls, path) -> "WeightManifest":
+        path = Path(path)
+        d = yaml.safe_load(path.read_text())
+        return cls(blob_path=path.parent / d["blob"], entries=list(d["tensors"]))
+
+    def tensors(self) -> dict:
+        blob = self.blob_path.read_bytes()
+        out = {}
+        for e in self.entries:
+            name = str(e["name"])
+            if name in out:
+                raise WeightError(f"weight {name!r} appears more than once in the manifest")
+            shape = tuple(int(v) for v in e["shape"])
+            offset, length = int(e["offset"]), int(e["length"])
+            if length != int(np.prod(shape)) * 4:
+                raise WeightError(f"weight {name!r}: length {length} does not match shape {shape}")
+            if offset < 0 or offset + length > len(blob):
+                raise WeightError(f"weight {name!r}: byte range [{offset}, {offset + length}) exceeds blob")
+            out[name] = np.frombuffer(blob, dtype="<f4", count=length // 4, offset=offset).reshape(shape)
+        return out
+
+    @staticmethod
+    def random_tensors(spec: ModelSpec, seed: int) -> dict:
+        """The seeded He-normal / U(-0.1, 0.1) tensors of ``generate`` without touching disk."""
+        rng = np.random.default_rng(seed)
+        out = {}
+        for name, shape in spec.weight_specs():
+            if name.endswith(".bias"):
+                out[name] = rng.uniform(-0.1, 0.1, size=shape).astype(np.float32)
+            else:
+                fan_in = int(np.prod(shape[1:]))
+                out[name] = rng.normal(0.0, np.sqrt(2.0 / fan_in), size=shape).astype(np.float32)
+        return out
+
+    @classmethod
+    def generate(cls, spec: ModelSpec, seed: int, out_dir, stem: str = "weights") -> "WeightManifest":
+        out_dir = Path(out_dir)
+        out_dir.mkdir(parents=True, exist_ok=True)
+        blob_path = out_dir / f"{stem}.bin"
+        entries, chunks, offset = [], [], 0
+        for name, arr in cls.random_tensors(spec, seed).items():
+            data = arr.astype("<f4").tobytes()
+            entries.append({"name": name, "shape": list(arr.shape), "offset": offset, "length": len(data)})
+            chunks.append(data)
+            offset += len(data)
+        blob_path.write_bytes(b"".join(chunks))
+        manifest = cls(blob_path=blob_path, entries=entries)
+        manifest.save(out_dir / f"{stem}.yaml")
+        return manifest
+
+
+# ---------------------------------------------------------------------------
+# reports
+# ---------------------------------------------------------------------------
+
+
+class FlopReport:
+    """Per-node (performed, dense_equiv) pairs + false-tile fractions (graph.py:379-397).
+
+    Built either from host dicts or lazily from device counters: nothing is
+    copied to the host until a field is read.
+    """
+
+    def __init__(self, per_node=None, false_tile_frac=None, *, _lazy=None):
+        self._per_node = per_node
+        self._ff = false_tile_frac if false_tile_frac is not None else ({} if per_node is not None else None)
+        self._lazy = _lazy
+
+    def _resolve(self):
+        if self._lazy is not None:
+            ids, perf_dev, dense, ff_dev = self._lazy
+            perf = perf_dev.tolist()
+            ffv = ff_dev.tolist()
+            self._per_node = {nid: (int(perf[i]), int(dense[i])) for i, nid in enumerate(ids)}
+            self._ff = {nid: float(ffv[i]) for i, nid in enumerate(ids)}
+            self._lazy = None
+
+    @property
+    def per_node(self) -> dict:
+        self._resolve()
+        return self._per_node
+
+    @property
+    def false_tile_frac(self) -> dict:
+        self._resolve()
+        return self._ff
+
+    @property
+    def performed(self) -> int:
+        return sum(p for p, _ in self.per_node.values())
+
+    @property
+    def dense_equiv(self) -> int:
+        return sum(d for _, d in self.per_node.values())
+
+    @property
+    def reduction_pct(self) -> float:
+        d = self.dense_equiv
+        return 100.0 * (1.0 - self.performed / d) if d else 0.0
+
+
+# ---------------------------------------------------------------------------
+# device session
+# ---------------------------------------------------------------------------
+
+
+class _Slot:
+    """A node output inside a (possibly shared) batched storage."""
+
+    __slots__ = ("store", "coff", "C", "H", "W")
+
+    def __init__(self, store, coff, shape):
+        self.store, self.coff = store, coff
+        self.C, self.H, self.W = shape
+
+
+class _Store:
+    __slots__ = ("C", "H", "W", "vals", "flags", "GH", "GW")
+
+    def __init__(self, shape):
+        self.C, self.H, self.W = shape
+        self.vals = None
+        self.flags = None
+
+
+class _Node:
+    """Compiled node: spec + bound weights + state (graph.py:400-420)."""
+
+    def __init__(self, spec: NodeSpec, out_shape):
+        self.spec = spec
+        self.kind = spec.kind
+        self.out_shape = out_shape
+        self.weight = None
+        self.bias = None
+        self.conv = None  # (geom, table, splits)
+        self.acc = None
+        self.acc2 = None
+        self.delta = None
+        self.dlive = None
+        self.tp = 0.0
+        self.ema_decay = 0.9
+        self.act = None
+        self.meter_idx = -1
+        self.sp_idx = -1
+
+
+class Graph:
+    """Compiled inference session (graph.py:423-693) on one B200.
+
+    One Graph owns ``sessions`` independent streams that share the weights.
+    With the default ``sessions=1`` it is a drop-in for the reference
+    Graph: ``dense_pass``, ``incr_step``, ``refresh``, ``dense_oracle``,
+    ``drift``, ``flop_report``, ``reset_meters``, ``state_fingerprint``.
+    """
+
+    def __init__(self, spec: ModelSpec, weights, refresh_interval: int = DEFAULT_REFRESH_INTERVAL, *,
+                 sessions: int = 1, cuda_graph: bool = True, device=None):
+        self.lib = _lib.lib()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.spec = spec
+        self.tile = spec.tile
+        self.input_id = spec.input_id
+        self.input_shape = tuple(spec.input_shape)
+        self.output_ids = [spec.output, *spec.aux_outputs]
+        self.refresh_interval = int(refresh_interval) if refresh_interval else 0
+        self.S = int(sessions)
+        if self.S < 1:
+            raise ValueError("sessions must be >= 1")
+        self.use_cuda_graph = bool(cuda_graph)
+        self.shapes = spec.infer_shapes()
+        order = spec.topo_order()
+        if isinstance(weights, WeightManifest):
+            weights = weights.tensors()
+        weights = dict(weights or {})
+        self.nodes = []
+        for ns in order:
+            node = _Node(ns, self.shapes[ns.id])
+            self._bind(node, weights)
+            self.nodes.append(node)
+        self._by_id = {n.spec.id: n for n in self.nodes}
+        self.step_count = 0
+        self.refresh_due = False
+        self._initialized = False
+        self._plan()
+        self._graph = None
+
+    # -- construction ---------------------------------------------------------
+
+    def _bind(self, node: _Node, weights: dict) -> None:
+        ns = node.spec
+        in_shape = self.shapes[ns.inputs[0]] if ns.inputs else None
+        dev = self.device
+        if ns.kind == "conv":
+            kh, kw = (int(v) for v in ns.attrs.get("kernel", [3, 3]))
+            c_out = int(ns.attrs["out_channels"])
+            st, pad = int(ns.attrs.get("stride", 1)), int(ns.attrs.get("padding", 0))
+            node.weight = as_matrix(self._take(weights, f"{ns.id}.weight", (c_out, in_shape[0], kh, kw)), dev)
+            b = self._take(weights, f"{ns.id}.bias", (c_out,), required=False)
+            node.bias = None if b is None else as_bias(b, c_out, dev)
+            c, h, w = in_shape
+            g, tab = conv_geometry(c, c_out, kh, kw, st, pad, h, w, self.tile.h, self.tile.w)
+            ho, wo = int(g.Ho), int(g.Wo)
+            tiles = grid_shape((c_out, ho, wo), self.tile)
+            T = tiles[1] * tiles[2]
+            splits = choose_splits(self.S * T * self.tile.h * self.tile.w, c_out, c * kh * kw)
+            node.conv = (g, tab, splits, T, 2 * kh * kw * c * c_out * ho * wo)
+        elif ns.kind == "linear":
+            f = int(ns.attrs["out_features"])
+            length = int(np.prod(in_shape))
+            node.weight = as_matrix(self._take(weights, f"{ns.id}.weight", (f, length)), dev)
+            b = self._take(weights, f"{ns.id}.bias", (f,), required=False)
+            node.bias = None if b is None else as_bias(b, f, dev)
+        elif ns.kind in ACTIVATION_KINDS:
+            node.act = (_lib.ACT[ns.kind], float(np.float32(ns.attrs.get("alpha", 0.01))))
+        elif ns.kind == "sparsify":
+            node.tp = float(ns.attrs.get("tp", 0.0))
+            node.ema_decay = float(ns.attrs.get("ema_decay", 0.9))
+            if node.tp < 0:
+                raise ValueError("threshold parameter must be >= 0")
+            if not (0.0 < node.ema_decay < 1.0):
+                raise ValueError("ema_decay must lie in (0, 1)")
+
+    @staticmethod
+    def _take(weights, name, shape, required: bool = True):
+        arr = weights.get(name)
+        if arr is None:
+            if required:
+                raise WeightError(f"missing weight {name!r}")
+            return None
+        shp = tuple(arr.shape)
+        if shp != tuple(shape):
+            raise WeightError(f"weight {name!r} has shape {shp}, expected {tuple(shape)}")
+        return arr
+
+    def _plan(self) -> None:
+        """Place every node output in HBM (concat parts alias into the concat
+        buffer), allocate state, counters and workspaces once."""
+        S, dev, tile = self.S, self.device, self.tile
+        slots = {}
+        parent = {}  # node -> (concat id, channel offset)
+        copies = {}  # concat id -> [(part id, offset)]
+        for node in self.nodes:
+            if node.kind != "concat":
+                continue
+            off = 0
+            ins = node.spec.inputs
+            for p in ins:
+                if p not in parent and ins.count(p) == 1:
+                    parent[p] = (node.spec.id, off)
+                else:
+                    copies.setdefault(node.spec.id, []).append((p, off))
+                off += self.shapes[p][0]
+
+        def root(nid):
+            off = 0
+            while nid in parent:
+                nid, o = parent[nid]
+                off += o
+            return nid, off
+
+        stores = {}
+        for nid in [self.input_id, *[n.spec.id for n in self.nodes]]:
+            r, off = root(nid)
+            if r not in stores:
+                stores[r] = _Store(self.shapes[r])
+            slots[nid] = _Slot(stores[r], off, self.shapes[nid])
+        for st in stores.values():
+            _, st.GH, st.GW = grid_shape((st.C, st.H, st.W), tile)
+            st.vals = torch.zeros((S, st.C, st.H, st.W), dtype=torch.float32, device=dev)
+            st.flags = torch.zeros((S, st.C, st.GH, st.GW), dtype=torch.uint8, device=dev)
+        self._stores = list(stores.values())
+        self._slots = slots
+        self._copies = copies
+        self.hbm_bytes = sum(s.vals.numel() * 4 + s.flags.numel() for s in self._stores)
+
+        # state
+        meter_ids = []
+        sp_nodes = []
+        max_ws = 0
+        max_T = 1
+        max_part = 1
+        lin_ws = 1
+        for node in self.nodes:
+            k = node.kind
+            ish = self.shapes[node.spec.inputs[0]] if node.spec.inputs else None
+            if k in ACTIVATION_KINDS or k == "maxpool":
+                node.acc = torch.zeros((S, *ish), dtype=torch.float32, device=dev)
+            elif k == "mul":
+                node.acc = torch.zeros((S, *ish), dtype=torch.float32, device=dev)
+                node.acc2 = torch.zeros((S, *self.shapes[node.spec.inputs[1]]), dtype=torch.float32, device=dev)
+            elif k == "sparsify":
+                node.delta = torch.zeros((S, *ish), dtype=torch.float32, device=dev)
+                node.dlive = torch.zeros((S, *grid_shape(ish, tile)), dtype=torch.uint8, device=dev)
+                node.sp_idx = len(sp_nodes)
+                sp_nodes.append(node)
+                max_part = max(max_part, ish[0] * grid_shape(ish, tile)[1])
+            if k in ("conv", "linear"):
+                node.meter_idx = len(meter_ids)
+                meter_ids.append(node.spec.id)
+            if k == "conv":
+                g, tab, splits, T, _ = node.conv
+                max_T = max(max_T, S * T)
+                if splits > 1:
+                    max_ws = max(max_ws, int(self.lib.evc_conv_workspace(g, S * T, splits)))
+            if k == "linear":
+                f = int(node.spec.attrs["out_features"])
+                lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
+                                                                       self.tile.h * self.tile.w, S)))
+        nm = max(len(meter_ids), 1)
+        self._meter_ids = meter_ids
+        self._meter_nodes = [self._by_id[i] for i in meter_ids]
+        self._perf_step = torch.zeros((nm, S), dtype=torch.int64, device=dev)
+        self._perf_cum = torch.zeros((nm, S), dtype=torch.int64, device=dev)
+        self._cnt_step = torch.zeros((nm, S), dtype=torch.int32, device=dev)
+        self._ff_last = torch.zeros((nm, S), dtype=torch.float64, device=dev)
+        self._ff_sum = torch.zeros((nm, S), dtype=torch.float64, device=dev)
+        self._ff_n = 0
+        self._flag_size = torch.tensor(
+            [float(np.prod(grid_shape(self.shapes[self._by_id[i].spec.inputs[0]], tile))) for i in meter_ids] or [1.0],
+            dtype=torch.float64, device=dev).reshape(-1, 1)
+        self._dense_static = [self._dense_equiv(self._by_id[i]) for i in meter_ids]
+        self._perf_host = [0] * len(meter_ids)   # dense-pass contributions (host ints)
+        self._dense_host = [0] * len(meter_ids)
+        self._sp_nodes = sp_nodes
+        nsp = max(len(sp_nodes), 1)
+        self._norm = torch.zeros((nsp, S), dtype=torch.float64, device=dev)
+        self._k = torch.zeros((nsp, S), dtype=torch.float64, device=dev)
+        self._partials = torch.zeros(S * max(max_part, 64), dtype=torch.float64, device=dev)
+        self._tile_active = torch.zeros(max_T, dtype=torch.uint8, device=dev)
+        self._tile_list = torch.zeros(max_T, dtype=torch.int32, device=dev)
+        self._tile_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._compact_scratch = torch.zeros(int(self.lib.evc_compact_scratch(max_T)), dtype=torch.int32, device=dev)
+        self._conv_ws = torch.zeros(max(max_ws, 1), dtype=torch.float32, device=dev)
+        self._lin_ws = torch.zeros(lin_ws, dtype=torch.float32, device=dev)
+        self._y_run = {o: torch.zeros((S, *self.shapes[o]), dtype=torch.float32, device=dev) for o in self.output_ids}
+        self._baseline = {o: torch.zeros((S, *self.shapes[o]), dtype=torch.float32, device=dev) for o in self.output_ids}
+        self._drift_buf = torch.zeros(S, dtype=torch.float32, device=dev)
+        self._program = self._build_incr_program()
+
+    def _dense_equiv(self, node) -> int:
+        if node.kind == "conv":
+            return node.conv[4]
+        f = int(node.spec.attrs["out_features"])
+        return 2 * f * int(np.prod(self.shapes[node.spec.inputs[0]]))
+
+    # -- descriptors ------------------------------------------------------------
+
+    def _desc(self, nid, masked=True, tile=None):
+        sl = self._slots[nid]
+        st = sl.store
+        t = tile or self.tile
+        hw = st.H * st.W
+        vals = st.vals.data_ptr() + 4 * sl.coff * hw
+        flags = None
+        if masked:
+            flags = st.flags.data_ptr() + sl.coff * st.GH * st.GW
+        return _lib.tdesc(vals, flags, st.C * hw, st.C * st.GH * st.GW, sl.C, sl.H, sl.W, t.h, t.w)
+
+    def _vptr(self, nid):
+        sl = self._slots[nid]
+        return sl.store.vals.data_ptr() + 4 * sl.coff * sl.store.H * sl.store.W, sl.store.C * sl.store.H * sl.store.W
+
+    def _slot_view(self, nid):
+        sl = self._slots[nid]
+        return sl.store.vals[:, sl.coff:sl.coff + sl.C], sl.store.flags[:, sl.coff:sl.coff + sl.C]
+
+    # -- incremental program ------------------------------------------------------
+
+    def _build_incr_program(self):
+        """List of (ctypes fn, args-without-stream, name) for one incr_step."""
+        L, S = self.lib, self.S
+        prog = []
+        i32 = self._cnt_step
+        for node in self.nodes:
+            ns, k = node.spec, node.kind
+            nid = ns.id
+            if k == "conv":
+                g, tab, splits, T, _ = node.conv
+                mi = node.meter_idx
+                din, dout = self._desc(ns.inputs[0]), self._desc(nid)
+                cnt_ptr = i32.data_ptr() + 4 * mi * S
+                perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
+                prog.append((L.evc_count_flags, (din, S, cnt_ptr), "count_flags"))
+                prog.append((L.evc_conv_mask, (g, din, dout, tab.data_ptr(), cnt_ptr, self._tile_active.data_ptr(),
+                                               perf_ptr, S), "conv_mask"))
+                prog.append((L.evc_compact, (self._tile_active.data_ptr(), S * T, self._tile_list.data_ptr(),
+                                             self._tile_count.data_ptr(), self._compact_scratch.data_ptr()),
+                             "compact"))
+                prog.append((L.evc_conv_gemm, (g, din, node.weight.data_ptr(), None, dout, tab.data_ptr(),
+                                               self._tile_list.data_ptr(), self._tile_count.data_ptr(), S, splits,
+                                               self._conv_ws.data_ptr()), "conv_gemm"))
+            elif k == "linear":
+                mi = node.meter_idx
+                din = self._desc(ns.inputs[0])
+                f = int(ns.attrs["out_features"])
+                cnt_ptr = i32.data_ptr() + 4 * mi * S
+                perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
+                prog.append((L.evc_count_flags, (din, S, cnt_ptr), "count_flags"))
+                dflat = self._desc(ns.inputs[0], masked=False)
+                prog.append((L.evc_linear, (dflat, node.weight.data_ptr(), None, self._desc(nid), f, 0, perf_ptr,
+                                            self._lin_ws.data_ptr(), S), "linear"))
+            elif k in ACTIVATION_KINDS:
+                code, alpha = node.act
+                prog.append((L.evc_act_delta, (self._desc(ns.inputs[0]), node.acc.data_ptr(),
+                                               node.acc[0].numel(), self._desc(nid), code, alpha, S), "act_delta"))
+            elif k == "sparsify":
+                j = node.sp_idx
+                c, h, w = self.shapes[nid]
+                npart = c * grid_shape((c, h, w), self.tile)[1]
+                prog.append((L.evc_sparsify, (self._desc(ns.inputs[0]), node.delta.data_ptr(), node.delta[0].numel(),
+                                              node.dlive.data_ptr(), self._desc(nid),
+                                              self._k.data_ptr() + 8 * j * S, self._partials.data_ptr(), S),
+                             "sparsify"))
+                prog.append((L.evc_sparsify_finalize, (self._partials.data_ptr(), npart,
+                                                       self._norm.data_ptr() + 8 * j * S,
+                                                       self._k.data_ptr() + 8 * j * S, node.tp, node.ema_decay, 0, S),
+                             "sparsify_finalize"))
+            elif k == "add":
+                prog.append((L.evc_add, (self._desc(ns.inputs[0]), self._desc(ns.inputs[1]), self._desc(nid), S),
+                             "add"))
+            elif k == "mul":
+                prog.append((L.evc_mul, (self._desc(ns.inputs[0]), self._desc(ns.inputs[1]), node.acc.data_ptr(),
+                                         node.acc2.data_ptr(), node.acc[0].numel(), self._desc(nid), S), "mul"))
+            elif k == "concat":
+                for p, off in self._copies.get(nid, []):
+                    dst = self._concat_part_desc(nid, off, self.shapes[p][0])
+                    prog.append((L.evc_copy_masked, (self._desc(p), dst, S), "copy_masked"))
+            elif k == "upsample":
+                mode = 0 if ns.attrs.get("mode", "nearest") == "nearest" else 1
+                prog.append((L.evc_upsample, (self._desc(ns.inputs[0]), self._desc(nid),
+                                              int(ns.attrs.get("factor", 2)), mode, S), "upsample"))
+            elif k == "maxpool":
+                wh, ww = (int(v) for v in ns.attrs.get("window", [2, 2]))
+                prog.append((L.evc_maxpool, (self._desc(ns.inputs[0]), node.acc.data_ptr(), node.acc[0].numel(),
+                                             self._desc(nid), wh, ww, int(ns.attrs.get("stride", 2)), S), "maxpool"))
+            else:
+                raise GraphError(f"unhandled node kind {k!r}")
+        for o in self.output_ids:
+            prog.append((L.evc_integrate, (self._y_run[o].data_ptr(), self._y_run[o][0].numel(), self._desc(o), S),
+                         "integrate"))
+        return prog
+
+    def _concat_part_desc(self, cid, off, c):
+        sl = self._slots[cid]
+        st = sl.store
+        hw = st.H * st.W
+        coff = sl.coff + off
+        return _lib.tdesc(st.vals.data_ptr() + 4 * coff * hw, st.flags.data_ptr() + coff * st.GH * st.GW, st.C * hw,
+                          st.C * st.GH * st.GW, c, sl.H, sl.W, self.tile.h, self.tile.w)
+
+    def _run_program(self):
+        s = _lib.stream_ptr()
+        self._perf_step.zero_()
+        self._cnt_step.zero_()
+        for fn, args, name in self._program:
+            _lib.check(fn(*args, s), name)
+        # device-side meter bookkeeping (graph.py:620-629, 632-636)
+        self._perf_cum.add_(self._perf_step)
+        self._ff_last.copy_(1.0 - self._cnt_step.to(torch.float64) / self._flag_size)
+        self._ff_sum.add_(self._ff_last)
+
+    def kernel_launches_per_step(self) -> int:
+        """libevconv kernels launched by one incr_step (torch bookkeeping ops excluded)."""
+        n = 0
+        for fn, args, name in self._program:
+            n += 2 if name in ("compact", "maxpool", "linear") else 1
+            if name == "conv_gemm" and args[9] > 1:
+                n += 1
+        return n
+
+    # -- dense evaluation (graph.py:503-565) ----------------------------------------
+
+    def _dense_program(self, mutate: bool):
+        L, S, s = self.lib, self.S, _lib.stream_ptr()
+
+        def run(fn, *a):
+            _lib.check(fn(*a, s), fn.__name__)
+
+        for node in self.nodes:
+            ns, k, nid = node.spec, node.kind, node.spec.id
+            if k == "conv":
+                g, tab, splits, T, _ = node.conv
+                run(L.evc_conv_gemm, g, self._desc(ns.inputs[0], False), node.weight.data_ptr(),
+                    None if node.bias is None else node.bias.data_ptr(), self._desc(nid, False), tab.data_ptr(), None,
+                    None, S, splits, self._conv_ws.data_ptr())
+            elif k == "linear":
+                f = int(ns.attrs["out_features"])
+                run(L.evc_linear, self._desc(ns.inputs[0], False), node.weight.data_ptr(),
+                    None if node.bias is None else node.bias.data_ptr(), self._desc(nid, False), f, 1, None,
+                    self._lin_ws.data_ptr(), S)
+            elif k in ACTIVATION_KINDS:
+                code, alpha = node.act
+                xp, xs = self._vptr(ns.inputs[0])
+                yp, ys = self._vptr(nid)
+                run(L.evc_act_dense, xp, xs, yp, ys, node.acc.data_ptr() if mutate else None, node.acc[0].numel(),
+                    node.acc[0].numel(), code, alpha, S)
+            elif k == "sparsify":
+                xp, xs = self._vptr(ns.inputs[0])
+                yp, ys = self._vptr(nid)
+                n = int(np.prod(self.shapes[nid]))
+                run(L.evc_copy_dense, xp, xs, yp, ys, n, S)
+                if mutate:
+                    j = node.sp_idx
+                    nb = 64
+                    run(L.evc_sumsq_dense, xp, xs, n, self._partials.data_ptr(), nb, S)
+                    run(L.evc_sparsify_finalize, self._partials.data_ptr(), nb, self._norm.data_ptr() + 8 * j * S,
+                        self._k.data_ptr() + 8 * j * S, node.tp, node.ema_decay, 1, S)
+                    node.delta.zero_()
+                    node.dlive.zero_()
+            elif k in ("add", "mul"):
+                ap, as_ = self._vptr(ns.inputs[0])
+                bp, bs = self._vptr(ns.inputs[1])
+                yp, ys = self._vptr(nid)
+                n = int(np.prod(self.shapes[nid]))
+                run(L.evc_binary_dense, ap, as_, bp, bs, yp, ys, n, 1 if k == "mul" else 0, S)
+                if k == "mul" and mutate:
+                    run(L.evc_copy_dense, ap, as_, node.acc.data_ptr(), n, n, S)
+                    run(L.evc_copy_dense, bp, bs, node.acc2.data_ptr(), n, n, S)
+            elif k == "concat":
+                for p, off in self._copies.get(nid, []):
+                    pp, ps = self._vptr(p)
+                    dst = self._concat_part_desc(nid, off, self.shapes[p][0])
+                    n = int(np.prod(self.shapes[p]))
+                    run(L.evc_copy_dense, pp, ps, dst.vals, dst.vstride, n, S)
+            elif k == "upsample":
+                mode = 0 if ns.attrs.get("mode", "nearest") == "nearest" else 1
+                run(L.evc_upsample, self._desc(ns.inputs[0], False), self._desc(nid, False),
+                    int(ns.attrs.get("factor", 2)), mode, S)
+            elif k == "maxpool":
+                wh, ww = (int(v) for v in ns.attrs.get("window", [2, 2]))
+                run(L.evc_maxpool, self._desc(ns.inputs[0], False), None, 0, self._desc(nid, False), wh, ww,
+                    int(ns.attrs.get("stride", 2)), S)
+                if mutate:
+                    xp, xs = self._vptr(ns.inputs[0])
+                    run(L.evc_copy_dense, xp, xs, node.acc.data_ptr(), node.acc[0].numel(), node.acc[0].numel(), S)
+
+    def _load_input(self, x):
+        x = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        x = x.to(self.device, torch.float32)
+        if tuple(x.shape) == self.input_shape:
+            x = x.unsqueeze(0).expand(self.S, *self.input_shape)
+        if tuple(x.shape) != (self.S, *self.input_shape):
+            shp = tuple(x.shape) if self.S > 1 else tuple(x.shape)[-3:] if x.dim() > 3 else tuple(x.shape)
+            raise ShapeError(f"input shape {shp}, graph expects {self.input_shape}")
+        v, _ = self._slot_view(self.input_id)
+        v.copy_(x)
+
+    def _eval_dense(self, x, mutate: bool):
+        if self._initialized:
+            # dense pass reuses the increment buffers as scratch; keep nothing stale
+            pass
+        self._load_input(x)
+        self._dense_program(mutate)
+
+    def _clear_increments(self):
+        for st in self._stores:
+            st.vals.zero_()
+            st.flags.zero_()
+
+    def dense_oracle(self, x):
+        """Pure dense forward of the primary output; session state is untouched."""
+        self._check_input_shape(x)
+        self._eval_dense(x, mutate=False)
+        v, _ = self._slot_view(self.output_ids[0])
+        out = v.clone()
+        self._clear_increments()
+        return out[0] if self.S == 1 else out
+
+    def dense_pass(self, x):
+        """Full dense forward that re-seeds every accumulator and baseline."""
+        self._check_input_shape(x)
+        self._eval_dense(x, mutate=True)
+        for i, node in enumerate(self._meter_nodes):
+            de = self._dense_static[i]
+            self._perf_host[i] += de * self.S
+            self._dense_host[i] += de * self.S
+        for o in self.output_ids:
+            v, _ = self._slot_view(o)
+            self._baseline[o].copy_(v)
+            self._y_run[o].copy_(v)
+        out = self._y_run[self.output_ids[0]].clone()
+        self._clear_increments()
+        self.step_count = 0
+        self.refresh_due = False
+        self._initialized = True
+        return out[0] if self.S == 1 else out
+
+    def refresh(self, x):
+        """Dense reconstruction run; identical contract to dense_pass."""
+        return self.dense_pass(x)
+
+    def _check_input_shape(self, x):
+        shp = tuple(x.shape)
+        ok = shp == self.input_shape or shp == (self.S, *self.input_shape)
+        if not ok:
+            raise ShapeError(f"input shape {shp}, graph expects {self.input_shape}")
+
+    # -- incremental evaluation (graph.py:573-630) ------------------------------------
+
+    def _step(self):
+        if self.use_cuda_graph:
+            if self._graph is None:
+                self._capture()
+            self._graph.replay()
+        else:
+            self._run_program()
+        self._ff_n += 1
+        for i in range(len(self._meter_nodes)):
+            self._dense_host[i] += self._dense_static[i] * self.S
+        self.step_count += 1
+        if self.refresh_interval:
+            self.refresh_due = self.step_count >= self.refresh_interval
+
+    def _capture(self):
+        # warm the allocator-free program once outside capture on scratch copies?  Not needed:
+        # every kernel module was loaded by evc_init, and the program allocates nothing.
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        # capture records the launches without executing them
+        with torch.cuda.graph(g, stream=side):
+            self._run_program()
+        torch.cuda.current_stream().wait_stream(side)
+        self._graph = g
+
+    def input_slot(self):
+        """(values (S,C,H,W), flags (S,C,GH,GW)) device views of the graph input increment."""
+        return self._slot_view(self.input_id)
+
+    def step_from_encodings(self, prev, cur, in_stride=None):
+        """step_increment(prev, cur) written straight into the graph input, then incr_step.
+
+        prev/cur: (S, C, H, W) (or (C, H, W) for one session) device tensors.
+        Returns nothing; outputs stay on device (see integrated_output)."""
+        if not self._initialized:
+            raise GraphError("incr_step called before any dense_pass")
+        c, h, w = self.input_shape
+        stride = c * h * w if in_stride is None else in_stride
+        _lib.check(self.lib.evc_diff_mask(prev.data_ptr(), cur.data_ptr(), stride, self._desc(self.input_id), self.S,
+                                          _lib.stream_ptr()), "diff_mask")
+        self._step()
+
+    def incr_step(self, x_up: IncrementTensor):
+        """Propagate one input increment; returns (y_up, integrated y, step report)."""
+        if not self._initialized:
+            raise GraphError("incr_step called before any dense_pass")
+        if x_up.shape != self.input_shape:
+            raise ShapeError(f"increment shape {x_up.shape}, graph expects {self.input_shape}")
+        if x_up.tile != self.tile:
+            raise ShapeError(f"increment tile {x_up.tile} does not match graph tile {self.tile}")
+        v, f = self._slot_view(self.input_id)
+        v.copy_(x_up.values.unsqueeze(0).expand_as(v))
+        f.copy_(x_up.mask.u8.unsqueeze(0).expand_as(f))
+        self._step()
+        return self._outputs_and_report()
+
+    def incr_step_batch(self, values, flags):
+        """Batched incr_step over all sessions: values (S,C,H,W), flags (S,C,GH,GW)."""
+        if not self._initialized:
+            raise GraphError("incr_step called before any dense_pass")
+        v, f = self._slot_view(self.input_id)
+        v.copy_(values)
+        f.copy_(flags.view(torch.uint8) if flags.dtype == torch.bool else flags)
+        self._step()
+
+    def _outputs_and_report(self):
+        o = self.output_ids[0]
+        v, f = self._slot_view(o)
+        y_up = IncrementTensor(v[0].clone(), TileMask(f[0].clone(), self.tile)) if self.S == 1 else (v.clone(), f.clone())
+        y = self._y_run[o].clone()
+        report = self.step_report()
+        return y_up, (y[0] if self.S == 1 else y), report
+
+    def step_report(self, session: int = 0) -> FlopReport:
+        dense = [d for d in self._dense_static]
+        return FlopReport(_lazy=(self._meter_ids, self._perf_step[:, session].clone(), dense,
+                                 self._ff_last[:, session].clone()))
+
+    # -- reporting (graph.py:640-693) ---------------------------------------------------
+
+    def integrated_output(self, output_id: str | None = None, session: int = 0):
+        oid = output_id or self.output_ids[0]
+        if oid not in self._y_run or not self._initialized:
+            raise GraphError("no output available before a dense_pass")
+        return self._y_run[oid][session].clone()
+
+    def drift(self, oracle_y, session: int | None = None) -> float:
+        """Max-absolute deviation of the integrated output from a dense oracle output."""
+        if not self._initialized:
+            raise GraphError("drift requested before any dense_pass")
+        oy = oracle_y if isinstance(oracle_y, torch.Tensor) else torch.from_numpy(np.asarray(oracle_y, np.float32))
+        oy = oy.to(self.device, torch.float32)
+        y = self._y_run[self.output_ids[0]]
+        if tuple(oy.shape) == tuple(y.shape[1:]):
+            oy = oy.unsqueeze(0).expand_as(y)
+        if tuple(oy.shape) != tuple(y.shape):
+            raise ShapeError(f"oracle shape {tuple(oy.shape)}, output is {tuple(y.shape[1:])}")
+        oy = oy.contiguous()
+        self._drift_buf.zero_()
+        n = y[0].numel()
+        _lib.check(self.lib.evc_max_abs_diff(y.data_ptr(), n, oy.data_ptr(), n, n, self.S, self._drift_buf.data_ptr(),
+                                             _lib.stream_ptr()), "max_abs_diff")
+        d = self._drift_buf.tolist()
+        return float(d[0] if session is None and self.S == 1 else (max(d) if session is None else d[session]))
+
+    def flop_report(self, session: int | None = None) -> FlopReport:
+        """Cumulative counters since build or the last reset_meters() (summed over sessions by default)."""
+        perf = self._perf_cum.sum(dim=1) if session is None else self._perf_cum[:, session]
+        perf = perf.tolist()
+        scale = 1 if session is None else 1.0 / self.S
+        per_node = {}
+        for i, nid in enumerate(self._meter_ids):
+            ph = self._perf_host[i] if session is None else self._perf_host[i] // self.S
+            dh = self._dense_host[i] if session is None else self._dense_host[i] // self.S
+            per_node[nid] = (int(perf[i]) + int(ph), int(dh))
+        ffs = self._ff_sum[:, 0 if session is None else session].tolist()
+        ff = {nid: (ffs[i] / self._ff_n if self._ff_n else 0.0) for i, nid in enumerate(self._meter_ids)}
+        del scale
+        return FlopReport(per_node, ff)
+
+    def reset_meters(self) -> None:
+        self._perf_cum.zero_()
+        self._ff_sum.zero_()
+        self._ff_last.zero_()
+        self._ff_n = 0
+        self._perf_host = [0] * len(self._meter_ids)
+        self._dense_host = [0] * len(self._meter_ids)
+
+    def state_fingerprint(self, session: int = 0) -> dict:
+        """Copies of all mutable numeric state (graph.py:678-693), as numpy arrays."""
+        out = {}
+        for n in self.nodes:
+            nid = n.spec.id
+            if n.kind in ACTIVATION_KINDS or n.kind in ("maxpool", "mul"):
+                out[f"{nid}.acc"] = n.acc[session].cpu().numpy()
+            if n.kind == "mul":
+                out[f"{nid}.acc2"] = n.acc2[session].cpu().numpy()
+            if n.kind == "sparsify":
+                out[f"{nid}.delta"] = n.delta[session].cpu().numpy()
+                out[f"{nid}.norm"] = np.asarray([float(self._norm[n.sp_idx, session]),
+                                                 float(self._k[n.sp_idx, session])], dtype=np.float64)
+        if self._initialized:
+            for o in self.output_ids:
+                out[f"{o}.y_run"] = self._y_run[o][session].cpu().numpy()
+                out[f"{o}.baseline"] = self._baseline[o][session].cpu().numpy()
+        return out
+
+
+def build(spec: ModelSpec, weights, refresh_interval: int = DEFAULT_REFRESH_INTERVAL, **engine) -> Graph:
+    """Compile a ModelSpec against weights into a device session (graph.py:696-698)."""
+    return Graph(spec, weights, refresh_interval, **engine)

@@ -1,0 +1,370 @@
+"""Device tensors, tile masks and the dense operators (mirrors evincr/tensors.py).
+
+All activations are float32 CUDA tensors of shape (C, H, W), channel-planar
+like the reference (tensors.py:1-6).  A TileMask holds a per-channel uint8
+grid (C, ceil(H/h), ceil(W/w)) on the device; ``.flags`` exposes it as a
+bool view, the reference's dtype.  Numpy inputs are accepted at the edges
+and uploaded.  Every operator runs in libevconv.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = [
+    "TileShape",
+    "TileMask",
+    "IncrementTensor",
+    "as_tensor",
+    "grid_shape",
+    "make_tile_mask",
+    "all_true_mask",
+    "all_false_mask",
+    "mask_or",
+    "mask_to_pixels",
+    "integrate",
+    "conv_output_hw",
+    "dense_conv2d",
+    "dense_linear",
+    "dense_maxpool",
+    "dense_upsample",
+    "resolve_activation",
+]
+
+DEFAULT_TILE = (6, 6)
+DEV = "cuda"
+
+
+def _dev():
+    _lib.lib()
+    return torch.device(DEV, torch.cuda.current_device())
+
+
+def as_tensor(data) -> torch.Tensor:
+    """Coerce to a contiguous float32 (C, H, W) CUDA tensor (tensors.py:39-44)."""
+    if isinstance(data, torch.Tensor):
+        t = data.to(device=_dev(), dtype=torch.float32).contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).to(_dev())
+    if t.dim() != 3:
+        raise ValueError(f"expected a 3-D (C, H, W) tensor, got shape {tuple(t.shape)}")
+    return t
+
+
+@dataclass(frozen=True)
+class TileShape:
+    """Spatial extent of one mask tile, in pixels (tensors.py:47-56)."""
+
+    h: int = DEFAULT_TILE[0]
+    w: int = DEFAULT_TILE[1]
+
+    def __post_init__(self):
+        if self.h < 1 or self.w < 1:
+            raise ValueError(f"tile sides must be >= 1, got {self.h}x{self.w}")
+
+
+def grid_shape(shape, tile: TileShape):
+    """(C, ceil(H/h), ceil(W/w)) (tensors.py:59-62)."""
+    c, h, w = shape
+    return int(c), -(-int(h) // tile.h), -(-int(w) // tile.w)
+
+
+def _as_flags(flags) -> torch.Tensor:
+    if isinstance(flags, torch.Tensor):
+        f = flags.to(_dev())
+        if f.dtype == torch.bool:
+            f = f.view(torch.uint8)
+        elif f.dtype != torch.uint8:
+            f = (f != 0).view(torch.uint8)
+        return f.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(flags, dtype=bool)).view(np.uint8)).to(_dev())
+
+
+class TileMask:
+    """Per-channel tile grid; False marks a tile known to be all-zero (tensors.py:65-90)."""
+
+    __slots__ = ("_u8", "tile")
+
+    def __init__(self, flags, tile: TileShape = None):
+        u8 = _as_flags(flags)
+        if u8.dim() != 3:
+            raise ValueError(f"mask grid must be 3-D (C, gh, gw), got {tuple(u8.shape)}")
+        self._u8 = u8
+        self.tile = tile if tile is not None else TileShape()
+
+    @property
+    def flags(self) -> torch.Tensor:
+        return self._u8.view(torch.bool)
+
+    @property
+    def u8(self) -> torch.Tensor:
+        return self._u8
+
+    @property
+    def grid(self):
+        return tuple(self._u8.shape)
+
+    def false_fraction(self) -> float:
+        n = self._u8.numel()
+        return float(1.0 - int(self._u8.sum().item()) / n) if n else 0.0
+
+    def covers(self, shape) -> bool:
+        return self.grid == grid_shape(shape, self.tile)
+
+    def active_indices(self) -> torch.Tensor:
+        """Sorted active tile list == np.flatnonzero(flags), computed on device
+        by warp-ballot compaction (evc_compact)."""
+        n = self._u8.numel()
+        idx = torch.empty(max(n, 1), dtype=torch.int32, device=self._u8.device)
+        cnt = torch.zeros(1, dtype=torch.int32, device=self._u8.device)
+        scratch = torch.empty(int(_lib.lib().evc_compact_scratch(n)), dtype=torch.int32, device=self._u8.device)
+        _lib.check(_lib.lib().evc_compact(_lib.ptr(self._u8), n, _lib.ptr(idx), _lib.ptr(cnt), _lib.ptr(scratch),
+                                          _lib.stream_ptr()), "compact")
+        return idx[: int(cnt.item())].to(torch.int64)
+
+    def numpy(self) -> np.ndarray:
+        return self._u8.cpu().numpy().astype(bool)
+
+
+class IncrementTensor:
+    """Step-to-step difference tensor paired with a sound tile mask (tensors.py:133-164)."""
+
+    __slots__ = ("values", "mask")
+
+    def __init__(self, values, mask: TileMask):
+        self.values = as_tensor(values)
+        self.mask = mask
+        if not mask.covers(tuple(self.values.shape)):
+            raise ValueError(
+                f"mask grid {mask.grid} does not cover tensor {tuple(self.values.shape)} "
+                f"at tile {mask.tile.h}x{mask.tile.w}")
+
+    @property
+    def shape(self):
+        return tuple(self.values.shape)
+
+    @property
+    def tile(self) -> TileShape:
+        return self.mask.tile
+
+    @classmethod
+    def from_dense(cls, values, tile: TileShape) -> "IncrementTensor":
+        values = as_tensor(values)
+        return cls(values, make_tile_mask(values, tile))
+
+    @classmethod
+    def zeros(cls, shape, tile: TileShape) -> "IncrementTensor":
+        return cls(torch.zeros(shape, dtype=torch.float32, device=_dev()), all_false_mask(shape, tile))
+
+    def desc(self) -> _lib.EvcTensor:
+        c, h, w = self.shape
+        return _lib.tdesc(_lib.ptr(self.values), _lib.ptr(self.mask.u8), 0, 0, c, h, w, self.tile.h, self.tile.w)
+
+
+def make_tile_mask(t, tile: TileShape) -> TileMask:
+    """Exact mask: a tile is True iff it holds a nonzero (tensors.py:93-107)."""
+    t = as_tensor(t)
+    c, h, w = t.shape
+    flags = torch.empty(grid_shape((c, h, w), tile), dtype=torch.uint8, device=t.device)
+    d = _lib.tdesc(_lib.ptr(t), _lib.ptr(flags), 0, 0, c, h, w, tile.h, tile.w)
+    _lib.check(_lib.lib().evc_make_tile_mask(d, 1, _lib.stream_ptr()), "make_tile_mask")
+    return TileMask(flags, tile)
+
+
+def all_true_mask(shape, tile: TileShape) -> TileMask:
+    return TileMask(torch.ones(grid_shape(shape, tile), dtype=torch.uint8, device=_dev()), tile)
+
+
+def all_false_mask(shape, tile: TileShape) -> TileMask:
+    return TileMask(torch.zeros(grid_shape(shape, tile), dtype=torch.uint8, device=_dev()), tile)
+
+
+def mask_or(a: TileMask, b: TileMask) -> TileMask:
+    """Elementwise OR over the same grid (tensors.py:118-124)."""
+    if a.tile != b.tile:
+        raise ValueError(f"tile shape mismatch: {a.tile} vs {b.tile}")
+    if a.grid != b.grid:
+        raise ValueError(f"mask grid mismatch: {a.grid} vs {b.grid}")
+    return TileMask(a.u8 | b.u8, a.tile)
+
+
+def mask_to_pixels(mask: TileMask, h: int, w: int) -> torch.Tensor:
+    """Per-pixel bool (C, h, w) (tensors.py:127-130)."""
+    px = mask.flags.repeat_interleave(mask.tile.h, dim=1).repeat_interleave(mask.tile.w, dim=2)
+    return px[:, :h, :w]
+
+
+def integrate(dense, incr: IncrementTensor) -> torch.Tensor:
+    """dense + increment on live tiles (tensors.py:167-174)."""
+    dense = as_tensor(dense)
+    if tuple(dense.shape) != incr.shape:
+        raise ValueError(f"shape mismatch: {tuple(dense.shape)} vs {incr.shape}")
+    out = dense.clone()
+    _lib.check(_lib.lib().evc_integrate(_lib.ptr(out), 0, incr.desc(), 1, _lib.stream_ptr()), "integrate")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# dense operators
+# ---------------------------------------------------------------------------
+
+
+def conv_output_hw(h: int, w: int, kh: int, kw: int, stride: int, padding: int):
+    """tensors.py:194-202."""
+    h_out = (h + 2 * padding - kh) // stride + 1
+    w_out = (w + 2 * padding - kw) // stride + 1
+    if h_out < 1 or w_out < 1:
+        raise ValueError(
+            f"kernel {kh}x{kw} with stride {stride}, padding {padding} does not fit a {h}x{w} input")
+    return h_out, w_out
+
+
+_TABLES: dict = {}
+
+
+def conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw):
+    """(EvcConvGeom, device int32 table) for one conv layer, cached."""
+    key = (c_in, c_out, kh, kw, stride, pad, h, w, th, tw, torch.cuda.current_device())
+    hit = _TABLES.get(key)
+    if hit is not None:
+        return hit
+    ho, wo = conv_output_hw(h, w, kh, kw, stride, pad)
+    g = _lib.EvcConvGeom(c_in, c_out, kh, kw, stride, pad, h, w, ho, wo, th, tw)
+    lib = _lib.lib()
+    n = int(lib.evc_conv_table_len(g))
+    host = np.zeros(n, dtype=np.int32)
+    _lib.check(lib.evc_conv_table_fill(g, host.ctypes.data), "conv_table_fill")
+    tab = torch.from_numpy(host).to(_dev())
+    _TABLES[key] = (g, tab)
+    return g, tab
+
+
+def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148) -> int:
+    """K-splits so the worst-case grid still fills the B200 (148 SMs)."""
+    bm, bn = (128, 64) if c_out > 32 else ((128, 32) if c_out > 24 else (256, 16))
+    ctas = max(1, -(-max_sites // bm)) * max(1, -(-c_out // bn))
+    if ctas >= target_ctas:
+        return 1
+    s = -(-target_ctas // ctas)
+    return int(max(1, min(s, k // 64, 32)))
+
+
+def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> torch.Tensor:
+    """Cross-correlation with zero padding and optional bias (tensors.py:205-228)."""
+    x = as_tensor(x)
+    weight = as_matrix(weight, x.device)
+    if weight.dim() != 4:
+        raise ValueError(f"weight must be (C_out, C_in, K_h, K_w), got {tuple(weight.shape)}")
+    c_out, c_in, kh, kw = weight.shape
+    c, h, w = x.shape
+    if c != c_in:
+        raise ValueError(f"input has {c} channels but weight expects {c_in}")
+    ho, wo = conv_output_hw(h, w, kh, kw, stride, padding)
+    th, tw = (4, 32) if wo >= 32 else (8, max(1, wo))
+    g, tab = conv_geometry(c_in, c_out, kh, kw, stride, padding, h, w, th, tw)
+    y = torch.empty((c_out, ho, wo), dtype=torch.float32, device=x.device)
+    b = None if bias is None else as_bias(bias, c_out, x.device)
+    tiles = -(-ho // th) * -(-wo // tw)
+    splits = choose_splits(tiles * th * tw, c_out, c_in * kh * kw)
+    lib = _lib.lib()
+    ws = None
+    if splits > 1:
+        ws = torch.empty(int(lib.evc_conv_workspace(g, tiles, splits)), dtype=torch.float32, device=x.device)
+    din = _lib.tdesc(_lib.ptr(x), None, 0, 0, c, h, w, th, tw)
+    dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, c_out, ho, wo, th, tw)
+    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), _lib.ptr(b), dout, _lib.ptr(tab), None, None, 1, splits,
+                                 _lib.ptr(ws), _lib.stream_ptr()), "conv_gemm")
+    return y
+
+
+def as_bias(bias, n, device):
+    b = bias if isinstance(bias, torch.Tensor) else torch.from_numpy(np.asarray(bias, dtype=np.float32))
+    return b.to(device=device, dtype=torch.float32).reshape(n).contiguous()
+
+
+def as_matrix(m, device=None):
+    t = m if isinstance(m, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(m, dtype=np.float32))
+    return t.to(device=device or _dev(), dtype=torch.float32).contiguous()
+
+
+def dense_linear(x_flat, matrix, bias=None) -> torch.Tensor:
+    """matrix @ x (+ bias) (tensors.py:231-239)."""
+    x = x_flat if isinstance(x_flat, torch.Tensor) else torch.from_numpy(np.asarray(x_flat, dtype=np.float32))
+    x = x.to(_dev(), torch.float32).reshape(-1).contiguous()
+    matrix = as_matrix(matrix, x.device)
+    if matrix.dim() != 2 or matrix.shape[1] != x.shape[0]:
+        raise ValueError(f"matrix {tuple(matrix.shape)} does not apply to vector of length {x.shape[0]}")
+    f, length = matrix.shape
+    y = torch.empty(f, dtype=torch.float32, device=x.device)
+    b = None if bias is None else as_bias(bias, f, x.device)
+    lib = _lib.lib()
+    ws = torch.empty(int(lib.evc_linear_workspace(f, length, 1, 1)), dtype=torch.float32, device=x.device)
+    din = _lib.tdesc(_lib.ptr(x), None, 0, 0, 1, 1, length, 1, 1)
+    dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, f, 1, 1, 1, 1)
+    _lib.check(lib.evc_linear(din, _lib.ptr(matrix), _lib.ptr(b), dout, f, 1, None, _lib.ptr(ws), 1,
+                              _lib.stream_ptr()), "linear")
+    return y
+
+
+def dense_maxpool(x, window=(2, 2), stride: int = 2) -> torch.Tensor:
+    """No-padding max pooling (tensors.py:242-256)."""
+    x = as_tensor(x)
+    c, h, w = x.shape
+    wh, ww = window
+    if wh > h or ww > w:
+        raise ValueError(f"pool window {wh}x{ww} larger than input {h}x{w}")
+    ho, wo = (h - wh) // stride + 1, (w - ww) // stride + 1
+    y = torch.empty((c, ho, wo), dtype=torch.float32, device=x.device)
+    din = _lib.tdesc(_lib.ptr(x), None, 0, 0, c, h, w, 6, 6)
+    dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, c, ho, wo, 6, 6)
+    _lib.check(_lib.lib().evc_maxpool(din, None, 0, dout, wh, ww, stride, 1, _lib.stream_ptr()), "maxpool")
+    return y
+
+
+def dense_upsample(x, factor: int, mode: str = "nearest") -> torch.Tensor:
+    """Nearest / half-pixel bilinear upsampling (tensors.py:259-282)."""
+    x = as_tensor(x)
+    if factor not in (2, 4):
+        raise ValueError(f"upsample factor must be 2 or 4, got {factor}")
+    if mode not in ("nearest", "bilinear"):
+        raise ValueError(f"unknown upsample mode {mode!r}")
+    c, h, w = x.shape
+    y = torch.empty((c, h * factor, w * factor), dtype=torch.float32, device=x.device)
+    din = _lib.tdesc(_lib.ptr(x), None, 0, 0, c, h, w, 6, 6)
+    dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, c, h * factor, w * factor, 6, 6)
+    _lib.check(_lib.lib().evc_upsample(din, dout, factor, 0 if mode == "nearest" else 1, 1, _lib.stream_ptr()),
+               "upsample")
+    return y
+
+
+class Activation:
+    """Elementwise activation f (tensors.py:285-312); callable on device tensors."""
+
+    __slots__ = ("kind", "alpha", "code")
+
+    def __init__(self, kind: str, alpha: float = 0.01):
+        if kind not in _lib.ACT:
+            raise ValueError(f"unknown activation {kind!r}")
+        self.kind = kind
+        self.alpha = float(np.float32(alpha))
+        self.code = _lib.ACT[kind]
+
+    def __call__(self, x):
+        x = as_tensor(x)
+        y = torch.empty_like(x)
+        _lib.check(_lib.lib().evc_act_dense(_lib.ptr(x), 0, _lib.ptr(y), 0, None, 0, x.numel(), self.code,
+                                            self.alpha, 1, _lib.stream_ptr()), "act_dense")
+        return y
+
+    def __repr__(self):
+        return f"Activation({self.kind!r}, alpha={self.alpha})"
+
+
+def resolve_activation(kind: str, alpha: float = 0.01) -> Activation:
+    """Map an activation name to its elementwise function (tensors.py:303-312)."""
+    return Activation(kind, alpha)

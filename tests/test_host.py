@@ -1,0 +1,153 @@
+"""CPU-only checks of the host side: the C-ABI library, specs, weights, streams."""
+
+import hashlib
+import json
+import re
+import tempfile
+
+import numpy as np
+import pytest
+
+import paper_2303_04670_b200 as evc
+from paper_2303_04670_b200 import _lib, configs
+from oracle import evincr_np as O
+from evc_testutil import GOLDEN, ROOT
+
+
+def header_symbols():
+    text = (ROOT / "include" / "evconv.h").read_text()
+    return sorted(set(re.findall(r"\b(evc_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load(require_cuda=False)
+    syms = header_symbols()
+    assert len(syms) >= 30
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.EXPORTED)
+    assert lib.evc_version() == _lib.ABI_VERSION
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(_lib.LIB_PATH)],
+                         capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_conv_table_host_helper():
+    lib = _lib.load(require_cuda=False)
+    g = _lib.EvcConvGeom(3, 4, 3, 3, 2, 1, 13, 17, 7, 9, 6, 6)
+    n = lib.evc_conv_table_len(g)
+    tab = np.zeros(n, np.int32)
+    assert lib.evc_conv_table_fill(g, tab.ctypes.data) == 0
+    ho, wo, kh, kw, K, rows, cols, kdec = tab[:8]
+    assert (ho, wo, kh, kw, K) == (7, 9, 3, 3, 27)
+    # in-bounds tap counts per output row equal the oracle's
+    L, inb = O.conv_live_taps(np.ones((1, 3, 3), bool), 6, 6, 13, 17, 3, 3, 2, 1)
+    inr = tab[rows:rows + 7 * 6].reshape(7, 6)[:, 2]
+    inc = tab[cols:cols + 9 * 6].reshape(9, 6)[:, 2]
+    assert np.array_equal(np.outer(inr, inc), inb)
+
+
+def _specs():
+    return json.loads((GOLDEN / "graph_specs.json").read_text())
+
+
+@pytest.mark.parametrize("name", ["plain", "plain_tp", "unet", "delayed", "custom"])
+def test_spec_roundtrip_and_topo(name):
+    d = _specs()[name]
+    spec = evc.ModelSpec.from_dict(d)
+    assert spec.to_dict() == d
+    assert [n.id for n in spec.topo_order()] == [n["id"] for n in O.topo_order(d)]
+    with tempfile.TemporaryDirectory() as td:
+        spec.save(f"{td}/m.yaml")
+        assert evc.ModelSpec.load(f"{td}/m.yaml").to_dict() == d
+
+
+def test_builders_match_reference_specs():
+    s = _specs()
+    assert evc.build_plain_cnn(depth=3, channels=6, tp=0.0, in_shape=(2, 24, 30), pool_every=2).to_dict() == s["plain"]
+    assert evc.build_unet(evc.UNetConfig(levels=3, base_channels=4, in_shape=(2, 24, 32), tp=0.0,
+                                         upsample_mode="bilinear")).to_dict() == s["unet"]
+    assert evc.build_delayed_unet(evc.UNetConfig(levels=3, base_channels=4, in_shape=(5, 16, 24),
+                                                 tp=0.0)).to_dict() == s["delayed"]
+
+
+def test_spec_errors():
+    N = evc.NodeSpec
+    cyc = evc.ModelSpec("c", (1, 8, 8), [N("a", "relu", ["b"]), N("b", "relu", ["a"])], "a")
+    with pytest.raises(evc.CycleError):
+        cyc.topo_order()
+    bad = evc.ModelSpec("c", (1, 8, 8), [N("a", "conv", ["input"], {"out_channels": 2, "kernel": [9, 9]})], "a")
+    with pytest.raises(evc.ShapeError):
+        bad.infer_shapes()
+    with pytest.raises(evc.GraphError):
+        evc.ModelSpec("c", (1, 8, 8), [N("a", "add", ["input"])], "a").topo_order()
+    with pytest.raises(evc.GraphError):
+        evc.ModelSpec("c", (1, 8, 8), [N("a", "nope", ["input"])], "a").topo_order()
+
+
+def test_weight_generation_matches_reference():
+    dig = json.loads((GOLDEN / "host_digests.json").read_text())["weights"]
+    specs = {"plain": evc.build_plain_cnn(3, 6, 0.0, (2, 24, 30)),
+             "unet": evc.build_unet(evc.UNetConfig(levels=3, base_channels=4, in_shape=(2, 24, 32)))}
+    for name, spec in specs.items():
+        with tempfile.TemporaryDirectory() as td:
+            man = evc.WeightManifest.generate(spec, seed=3, out_dir=td)
+            assert hashlib.sha256(man.blob_path.read_bytes()).hexdigest() == dig[name]["sha256"]
+            assert man.entries == dig[name]["entries"]
+            t = evc.WeightManifest.load(f"{td}/weights.yaml").tensors()
+            r = evc.WeightManifest.random_tensors(spec, 3)
+            assert all(np.array_equal(t[k], r[k]) for k in r)
+
+
+def test_weight_manifest_errors():
+    spec = evc.build_plain_cnn(1, 2, 0.0, (1, 8, 8))
+    with tempfile.TemporaryDirectory() as td:
+        man = evc.WeightManifest.generate(spec, seed=0, out_dir=td)
+        man.entries[0]["length"] += 4
+        with pytest.raises(evc.WeightError):
+            man.tensors()
+
+
+def test_generate_events_matches_reference():
+    dig = json.loads((GOLDEN / "host_digests.json").read_text())["synth"]
+    for key, ref in dig.items():
+        seed, dur, rate, nobj, hw = key.split("_")
+        h, w = (int(v) for v in hw.split("x"))
+        s = evc.generate_events(int(seed), int(dur), float(rate), int(nobj), (h, w))
+        hsh = hashlib.sha256()
+        for a in (s.t, s.x, s.y, s.p):
+            hsh.update(np.ascontiguousarray(a).tobytes())
+        assert len(s) == ref["n"] and hsh.hexdigest() == ref["sha256"], key
+
+
+def test_event_io_roundtrip():
+    s = evc.generate_events(1, 20_000, 2e5, 2, (30, 40))
+    with tempfile.TemporaryDirectory() as td:
+        evc.write_events(s, f"{td}/a.evb")
+        evc.write_events(s, f"{td}/a.csv")
+        assert evc.read_events(f"{td}/a.evb") == s
+        assert evc.read_events(f"{td}/a.csv", sensor_size=(30, 40)) == s
+
+
+def test_slice_window_matches_oracle():
+    s = evc.generate_events(2, 60_000, 2e5, 3, (20, 20))
+    for tau in (0, 10, 50_000, 55_500, 60_000, 90_000):
+        w = evc.slice_window(s, tau, 50_000)
+        assert (w.lo, w.hi) == O.slice_window(s.t, tau, 50_000)
+
+
+def test_config_specs():
+    c1 = configs.evflownet_spec()
+    assert len(c1.nodes) == 58 and c1.parameter_count() == 3_535_128
+    assert c1.infer_shapes()[c1.output] == (2, 256, 256)
+    c3 = configs.resnet18_spec()
+    assert len(c3.nodes) == 67
+    sh = c3.infer_shapes()
+    assert sh["stem_pool"] == (64, 44, 59) and sh["s3b1_act"] == (512, 6, 8) and sh["fc"] == (101, 1, 1)
+    c2 = configs.unet_e2depth_spec()
+    assert len(c2.nodes) == 47

@@ -124,18 +124,24 @@ int evc_max_abs_diff(const float* a, int64_t a_stride, const float* b,
 int64_t evc_conv_table_len(const evc_conv_geom* g);
 int evc_conv_table_fill(const evc_conv_geom* g, int32_t* host_table);
 
-/* Mask propagation + FLOP meter of inc_conv2d for a batch:
- *  - in_true[s]  : number of True input flags (from evc_count_flags)
- *  - writes out.flags (broadcast over C_out, increment_ops.py:193-194),
+/* Mask propagation + FLOP meter of inc_conv2d for a batch (two launches):
+ *  - in_true[s] += number of True input flags (TileMask.false_fraction and
+ *    the all-false / all-true shortcuts, increment_ops.py:148-154),
+ *  - writes out.flags (broadcast over C_out, increment_ops.py:193-194) and
  *    zeroes output tiles that were live last step and are dead now,
- *  - tile_active[s*T + t] (uint8, T = output tiles per session),
- *  - meter[s] += performed FLOPs (int64, exact reference meter incl. the
- *    all-true / all-false shortcuts at increment_ops.py:148-154).
- * `table` is the device copy of evc_conv_table_fill's output. */
+ *  - appends every live output tile (s*T + t, T = output tiles per session)
+ *    to tile_list and counts them in *tile_count (work list of
+ *    evc_conv_gemm; the GEMM result does not depend on list order),
+ *  - meter[s] += performed FLOPs (int64, the exact reference meter).
+ * scratch (evc_conv_mask_scratch int32 entries), in_true and tile_count
+ * must be zeroed before the call.  `table` is the device copy of
+ * evc_conv_table_fill's output. */
+int64_t evc_conv_mask_scratch(const evc_conv_geom* g, int32_t S);
 int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
                   const evc_tensor* out, const int32_t* table,
-                  const int32_t* in_true, uint8_t* tile_active,
-                  int64_t* meter, int32_t S, void* stream);
+                  int32_t* scratch, int32_t* in_true, int32_t* tile_list,
+                  int32_t* tile_count, int64_t* meter, int32_t S,
+                  void* stream);
 
 /* Workspace floats needed by evc_conv_gemm for `max_tiles` active output
  * tiles and `splits` K-splits. */

@@ -60,7 +60,8 @@ _PROTOS = {
     "evc_max_abs_diff": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P]),
     "evc_conv_table_len": (_I64, [_G]),
     "evc_conv_table_fill": (_I32, [_G, _P]),
-    "evc_conv_mask": (_I32, [_G, _T, _T, _P, _P, _P, _P, _I32, _P]),
+    "evc_conv_mask_scratch": (_I64, [_G, _I32]),
+    "evc_conv_mask": (_I32, [_G, _T, _T, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
     "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
     "evc_act_delta": (_I32, [_T, _P, _I64, _T, _I32, _F, _I32, _P]),

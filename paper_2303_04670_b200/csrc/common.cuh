@@ -125,6 +125,7 @@ namespace evc {
 // any CUDA-graph capture).
 int init_masks();
 int init_conv();
+int init_conv_mask();
 int init_elementwise();
 int init_linear_events();
 }  // namespace evc

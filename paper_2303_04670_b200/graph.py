@@ -590,9 +590,22 @@ class Graph:
         nm = max(len(meter_ids), 1)
         self._meter_ids = meter_ids
         self._meter_nodes = [self._by_id[i] for i in meter_ids]
+        # per-step scratch zeroed by ONE memset at the start of every step:
+        # int32 [flag counts (nm x S) | per conv: tile count (2) + mask scratch]
+        z32 = nm * S + (nm * S) % 2
+        conv_off = []
+        for node in self.nodes:
+            if node.kind == "conv":
+                n = int(self.lib.evc_conv_mask_scratch(node.conv[0], S))
+                conv_off.append((node, z32, z32 + 2))
+                z32 += 2 + n + n % 2
+        self._z32 = torch.zeros(z32, dtype=torch.int32, device=dev)
+        base = self._z32.data_ptr()
+        for node, c_off, s_off in conv_off:
+            node.mask_scratch = (base + 4 * c_off, base + 4 * s_off)
+        self._cnt_step = self._z32[: nm * S].view(nm, S)
         self._perf_step = torch.zeros((nm, S), dtype=torch.int64, device=dev)
         self._perf_cum = torch.zeros((nm, S), dtype=torch.int64, device=dev)
-        self._cnt_step = torch.zeros((nm, S), dtype=torch.int32, device=dev)
         self._ff_last = torch.zeros((nm, S), dtype=torch.float64, device=dev)
         self._ff_sum = torch.zeros((nm, S), dtype=torch.float64, device=dev)
         self._ff_n = 0
@@ -607,10 +620,7 @@ class Graph:
         self._norm = torch.zeros((nsp, S), dtype=torch.float64, device=dev)
         self._k = torch.zeros((nsp, S), dtype=torch.float64, device=dev)
         self._partials = torch.zeros(S * max(max_part, 64), dtype=torch.float64, device=dev)
-        self._tile_active = torch.zeros(max_T, dtype=torch.uint8, device=dev)
         self._tile_list = torch.zeros(max_T, dtype=torch.int32, device=dev)
-        self._tile_count = torch.zeros(1, dtype=torch.int32, device=dev)
-        self._compact_scratch = torch.zeros(int(self.lib.evc_compact_scratch(max_T)), dtype=torch.int32, device=dev)
         self._conv_ws = torch.zeros(max(max_ws, 1), dtype=torch.float32, device=dev)
         self._lin_ws = torch.zeros(lin_ws, dtype=torch.float32, device=dev)
         self._y_run = {o: torch.zeros((S, *self.shapes[o]), dtype=torch.float32, device=dev) for o in self.output_ids}
@@ -661,14 +671,11 @@ class Graph:
                 din, dout = self._desc(ns.inputs[0]), self._desc(nid)
                 cnt_ptr = i32.data_ptr() + 4 * mi * S
                 perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
-                prog.append((L.evc_count_flags, (din, S, cnt_ptr), "count_flags"))
-                prog.append((L.evc_conv_mask, (g, din, dout, tab.data_ptr(), cnt_ptr, self._tile_active.data_ptr(),
-                                               perf_ptr, S), "conv_mask"))
-                prog.append((L.evc_compact, (self._tile_active.data_ptr(), S * T, self._tile_list.data_ptr(),
-                                             self._tile_count.data_ptr(), self._compact_scratch.data_ptr()),
-                             "compact"))
+                count_ptr, scratch_ptr = node.mask_scratch
+                prog.append((L.evc_conv_mask, (g, din, dout, tab.data_ptr(), scratch_ptr, cnt_ptr,
+                                               self._tile_list.data_ptr(), count_ptr, perf_ptr, S), "conv_mask"))
                 prog.append((L.evc_conv_gemm, (g, din, node.weight.data_ptr(), None, dout, tab.data_ptr(),
-                                               self._tile_list.data_ptr(), self._tile_count.data_ptr(), S, splits,
+                                               self._tile_list.data_ptr(), count_ptr, S, splits,
                                                self._conv_ws.data_ptr()), "conv_gemm"))
             elif k == "linear":
                 mi = node.meter_idx
@@ -732,7 +739,7 @@ class Graph:
     def _run_program(self):
         s = _lib.stream_ptr()
         self._perf_step.zero_()
-        self._cnt_step.zero_()
+        self._z32.zero_()
         for fn, args, name in self._program:
             _lib.check(fn(*args, s), name)
         # device-side meter bookkeeping (graph.py:620-629, 632-636)
@@ -744,7 +751,7 @@ class Graph:
         """libevconv kernels launched by one incr_step (torch bookkeeping ops excluded)."""
         n = 0
         for fn, args, name in self._program:
-            n += 2 if name in ("compact", "maxpool", "linear") else 1
+            n += 2 if name in ("conv_mask", "maxpool", "linear") else 1
             if name == "conv_gemm" and args[9] > 1:
                 n += 1
         return n

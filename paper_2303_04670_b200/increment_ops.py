@@ -138,18 +138,14 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     yv, yf = _zeros_incr((c_out, ho, wo), tile, dev)
     T = yf.shape[1] * yf.shape[2]
     i32 = torch.zeros(2, dtype=torch.int32, device=dev)  # [in_true, tile_count]
-    active = torch.empty(T, dtype=torch.uint8, device=dev)
     tiles = torch.empty(T, dtype=torch.int32, device=dev)
-    scratch = torch.empty(int(lib.evc_compact_scratch(T)), dtype=torch.int32, device=dev)
+    scratch = torch.zeros(int(lib.evc_conv_mask_scratch(g, 1)), dtype=torch.int32, device=dev)
     perf = torch.zeros(1, dtype=torch.int64, device=dev)
     s = _lib.stream_ptr()
     din = x.desc()
     dout = _desc(yv, yf, tile)
-    _lib.check(lib.evc_count_flags(din, 1, _lib.ptr(i32), s), "count_flags")
-    _lib.check(lib.evc_conv_mask(g, din, dout, _lib.ptr(tab), _lib.ptr(i32), _lib.ptr(active), _lib.ptr(perf), 1,
-                                 s), "conv_mask")
-    _lib.check(lib.evc_compact(_lib.ptr(active), T, _lib.ptr(tiles), _lib.ptr(i32) + 4, _lib.ptr(scratch), s),
-               "compact")
+    _lib.check(lib.evc_conv_mask(g, din, dout, _lib.ptr(tab), _lib.ptr(scratch), _lib.ptr(i32), _lib.ptr(tiles),
+                                 _lib.ptr(i32) + 4, _lib.ptr(perf), 1, s), "conv_mask")
     splits = choose_splits(T * tile.h * tile.w, c_out, c_in * kh * kw)
     ws = None
     if splits > 1:

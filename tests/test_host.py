@@ -43,13 +43,59 @@ def test_conv_table_host_helper():
     n = lib.evc_conv_table_len(g)
     tab = np.zeros(n, np.int32)
     assert lib.evc_conv_table_fill(g, tab.ctypes.data) == 0
-    ho, wo, kh, kw, K, rows, cols, kdec = tab[:8]
-    assert (ho, wo, kh, kw, K) == (7, 9, 3, 3, 27)
+    ho, wo, kh, kw, K, ghi, gwi, gho, gwo, rows, cols, kdec, rt, ct, boxr, boxc = tab[:16]
+    assert (ho, wo, kh, kw, K, ghi, gwi, gho, gwo) == (7, 9, 3, 3, 27, 3, 3, 2, 2)
     # in-bounds tap counts per output row equal the oracle's
     L, inb = O.conv_live_taps(np.ones((1, 3, 3), bool), 6, 6, 13, 17, 3, 3, 2, 1)
     inr = tab[rows:rows + 7 * 6].reshape(7, 6)[:, 2]
     inc = tab[cols:cols + 9 * 6].reshape(9, 6)[:, 2]
     assert np.array_equal(np.outer(inr, inc), inb)
+
+
+def _table(c_in, c_out, k, st, pad, h, w, th, tw):
+    lib = _lib.load(require_cuda=False)
+    ho, wo = O.conv_out_hw(h, w, k, k, st, pad)
+    g = _lib.EvcConvGeom(c_in, c_out, k, k, st, pad, h, w, ho, wo, th, tw)
+    tab = np.zeros(lib.evc_conv_table_len(g), np.int32)
+    assert lib.evc_conv_table_fill(g, tab.ctypes.data) == 0
+    return tab
+
+
+def _meter_from_table(tab, flags, c_out):
+    """The split used by the conv_mask kernels: weighted live count + border padding term."""
+    ho, wo, kh, kw, K, ghi, gwi, gho, gwo, rows, cols, kdec, rt, ct, boxr, boxc = (int(v) for v in tab[:16])
+    R = tab[rows:rows + ho * (3 + kh)].reshape(ho, 3 + kh)
+    Cc = tab[cols:cols + wo * (3 + kw)].reshape(wo, 3 + kw)
+    RT, CT = tab[rt:rt + ghi].astype(np.int64), tab[ct:ct + gwi].astype(np.int64)
+    c_in = flags.shape[0]
+    if not flags.any():
+        return 0
+    if flags.all():
+        return 2 * kh * kw * c_in * c_out * ho * wo
+    term1 = int((flags.astype(np.int64) * RT[None, :, None] * CT[None, None, :]).sum())
+    border = 0
+    for u in range(ho):
+        for v in range(wo):
+            d = kh * kw - R[u, 2] * Cc[v, 2]
+            if d == 0 or R[u, 1] == 0 or Cc[v, 1] == 0:
+                continue
+            box = flags[:, R[u, 0]:R[u, 0] + R[u, 1], Cc[v, 0]:Cc[v, 0] + Cc[v, 1]]
+            border += d * int(box.reshape(c_in, -1).any(axis=1).sum())
+    return 2 * c_out * (term1 + border)
+
+
+def test_meter_decomposition_matches_reference(golden):
+    """The weighted-count + border-term meter equals the reference's per-channel
+    loop on every golden conv case (pinned on CPU, no GPU needed)."""
+    from evc_testutil import unpack
+    n = len({k.split("/")[1] for k in golden.conv.files})
+    for i in range(n):
+        c = unpack(golden.conv, f"conv/{i}")
+        th, tw = (int(v) for v in c["tile"])
+        cin, h, w = c["x"].shape
+        cout, _, k, _ = c["w"].shape
+        tab = _table(cin, cout, k, int(c["stride"]), int(c["pad"]), h, w, th, tw)
+        assert _meter_from_table(tab, c["flags"], cout) == int(c["performed"]), i
 
 
 def _specs():

@@ -177,14 +177,17 @@ int evc_act_dense(const float* x, int64_t x_stride, float* y, int64_t y_stride,
 /* sparsify_step (sparsify.py:54-78) for a batch.  k[s], norm_ema[s] are
  * float64 device scalars (SparsifyState.k / .norm_ema); delta is the
  * residual (dense batch); dlive (uint8, per tile) tracks tiles whose
- * residual is nonzero.  partials (float64) receives per-block sums of
- * corrected^2: partials[s*GH*C + c*GH + i]. */
+ * residual is nonzero.  partials (float64, S*C*GH) receives per-CTA sums of
+ * corrected^2; the last CTA to retire (ticket: zeroed int32) folds them into
+ * norm_ema / k in a fixed order (sparsify.py:72-76), so the whole step is
+ * one launch. */
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
-                 uint8_t* dlive, const evc_tensor* y, const double* k,
-                 double* partials, int32_t S, void* stream);
+                 uint8_t* dlive, const evc_tensor* y, double* k,
+                 double* norm_ema, double tp, double ema_decay,
+                 double* partials, int32_t* ticket, int32_t S, void* stream);
 
-/* Norm / EMA / k update (sparsify.py:72-76) after evc_sparsify, or the
- * reset (sparsify.py:43-51) when reset != 0 (norm_ema = norm, and
+/* Norm / EMA / k update from partial sums (one CTA, all S sessions), or
+ * the reset (sparsify.py:43-51) when reset != 0 (norm_ema = norm, and
  * k = tp*norm if tp > 0).  n_partials per session. */
 int evc_sparsify_finalize(const double* partials, int64_t n_partials,
                           double* norm_ema, double* k, double tp,

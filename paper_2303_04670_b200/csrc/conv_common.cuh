@@ -6,19 +6,22 @@
 namespace evc {
 
 // int32 table layout (all offsets in int32 entries from the table start):
-//   [0..15] header (TabHdr)
+//   [0..19] header (TabHdr)
 //   rows  : Ho  x (3 + kh)  a_first, n_a, inR, cnt[kh]   (input tile rows hit by output row u)
 //   cols  : Wo  x (3 + kw)  b_first, n_b, inC, cnt[kw]
 //   kdec  : K   x 2         c*H*W + r*W + q,  (r << 16) | q      (k = (c*kh + r)*kw + q)
 //   rt    : GHi             RT[a] = sum_u cnt(u, a)   (output-row/tap pairs landing in input tile row a)
 //   ct    : GWi             CT[b]
-//   boxr  : GHo x 3         A0, A1, has_border_row   (input tile-row box of output tile row i)
-//   boxc  : GWo x 3         B0, B1, has_border_col
+//   boxr  : GHo x 2         A0, A1   (input tile-row box of output tile row i; A1 < A0 if empty)
+//   boxc  : GWo x 2         B0, B1
+//   grp   : ngrp x 5        a0, na, b0, nb, sumD: border output sites with the same
+//                           input tile box, sumD = sum over them of (K^2 - inb) > 0
 struct TabHdr {
   int Ho, Wo, kh, kw, K, GHi, GWi, GHo, GWo;
-  int rows, cols, kdec, rt, ct, boxr, boxc;
+  int rows, cols, kdec, rt, ct, boxr, boxc, grp, ngrp, pad0, pad1;
 };
 
+// Header with every offset except the border groups (grp, ngrp filled by the host builder).
 static inline TabHdr tab_layout(const evc_conv_geom* g) {
   TabHdr h;
   h.Ho = g->Ho;
@@ -30,19 +33,17 @@ static inline TabHdr tab_layout(const evc_conv_geom* g) {
   h.GWi = (g->W + g->tw - 1) / g->tw;
   h.GHo = (g->Ho + g->th - 1) / g->th;
   h.GWo = (g->Wo + g->tw - 1) / g->tw;
-  h.rows = 16;
+  h.rows = 20;
   h.cols = h.rows + g->Ho * (3 + g->kh);
   h.kdec = h.cols + g->Wo * (3 + g->kw);
   h.rt = h.kdec + 2 * h.K;
   h.ct = h.rt + h.GHi;
   h.boxr = h.ct + h.GWi;
-  h.boxc = h.boxr + 3 * h.GHo;
+  h.boxc = h.boxr + 2 * h.GHo;
+  h.grp = h.boxc + 2 * h.GWo;
+  h.ngrp = 0;
+  h.pad0 = h.pad1 = 0;
   return h;
-}
-
-static inline int64_t tab_len(const evc_conv_geom* g) {
-  const TabHdr h = tab_layout(g);
-  return h.boxc + 3 * h.GWo;
 }
 
 }  // namespace evc

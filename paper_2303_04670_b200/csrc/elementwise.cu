@@ -72,8 +72,28 @@ __global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __re
 // ---------------------------------------------------------------------------
 // sparsify_step (sparsify.py:54-78)
 // ---------------------------------------------------------------------------
+__device__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
+                                      double decay, int reset, int S);
+
+// Last-block-done: the CTA that retires last folds every session's partial sums
+// into norm_ema / k (sparsify.py:72-76) in a fixed order.
+__device__ __forceinline__ void sparsify_ticket(int* ticket, int nblocks, const double* partials, int64_t n,
+                                                double* norm_ema, double* kdev, double tp, double decay, int S) {
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1) == nblocks - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, 0, S);
+  }
+}
+
 __global__ void k_sparsify(TView d, float* __restrict__ delta, int64_t ds, uint8_t* __restrict__ dlive, TView y,
-                           const double* __restrict__ kdev, double* __restrict__ partials) {
+                           double* kdev, double* partials, double* norm_ema, double tp, double decay, int* ticket) {
   extern __shared__ uint8_t s_m[];  // proc | nz_y | nz_d   (3 x GW)
   uint8_t* s_proc = s_m;
   uint8_t* s_ny = s_m + d.GW;
@@ -90,9 +110,12 @@ __global__ void k_sparsify(TView d, float* __restrict__ delta, int64_t ds, uint8
     s_nd[j] = 0;
     any |= p != 0;
   }
-  double* part = partials + (int64_t)s * d.C * d.GH + (int64_t)c * d.GH + i;
+  const int64_t npart = (int64_t)d.C * d.GH;
+  const int nblocks = gridDim.x * gridDim.y * gridDim.z;
+  double* part = partials + (int64_t)s * npart + (int64_t)c * d.GH + i;
   if (!__syncthreads_or(any)) {
     if (threadIdx.x == 0) *part = 0.0;
+    sparsify_ticket(ticket, nblocks, partials, npart, norm_ema, kdev, tp, decay, gridDim.z);
     return;
   }
   const double k = kdev[s];
@@ -135,26 +158,32 @@ __global__ void k_sparsify(TView d, float* __restrict__ delta, int64_t ds, uint8
     fo[j] = s_ny[j];
     dl[j] = s_nd[j];
   }
+  sparsify_ticket(ticket, nblocks, partials, npart, norm_ema, kdev, tp, decay, gridDim.z);
+}
+
+// Sum each session's partials in a fixed order, then the EMA / k update
+// (sparsify.py:72-76) or the reset (sparsify.py:43-51).  One CTA does all S.
+__device__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
+                                      double decay, int reset, int S) {
+  for (int s = 0; s < S; ++s) {
+    double sum = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) sum += ((volatile const double*)partials)[(int64_t)s * n + e];
+    sum = block_sum<double>(sum, [](double v) { return warp_sum_d(v); });
+    if (threadIdx.x == 0) {
+      // np.linalg.norm of float32 data returns float32 (sparsify.py:49,73)
+      const double norm = (double)__double2float_rn(sqrt(sum));
+      const double ne =
+          reset ? norm : __dadd_rn(__dmul_rn(decay, norm_ema[s]), __dmul_rn(__dsub_rn(1.0, decay), norm));
+      norm_ema[s] = ne;
+      if (tp > 0.0) kdev[s] = __dmul_rn(tp, ne);
+    }
+    __syncthreads();
+  }
 }
 
 __global__ void k_sparsify_finalize(const double* __restrict__ partials, int64_t n, double* norm_ema, double* kdev,
-                                    double tp, double decay, int reset) {
-  const int s = blockIdx.x;
-  double sum = 0.0;
-  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) sum += partials[(int64_t)s * n + e];
-  sum = block_sum<double>(sum, [](double v) { return warp_sum_d(v); });
-  if (threadIdx.x == 0) {
-    // np.linalg.norm of float32 data returns float32 (sparsify.py:49,73)
-    const double norm = (double)__double2float_rn(sqrt(sum));
-    double ne;
-    if (reset) {
-      ne = norm;
-    } else {
-      ne = __dadd_rn(__dmul_rn(decay, norm_ema[s]), __dmul_rn(__dsub_rn(1.0, decay), norm));
-    }
-    norm_ema[s] = ne;
-    if (tp > 0.0) kdev[s] = __dmul_rn(tp, ne);
-  }
+                                    double tp, double decay, int reset, int S) {
+  sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, reset, S);
 }
 
 __global__ void k_sumsq(const float* __restrict__ x, int64_t xs, int64_t n, double* partials) {
@@ -424,12 +453,14 @@ int evc_act_dense(const float* x, int64_t xs, float* y, int64_t ys, float* acc, 
   return EVC_OK;
 }
 
-int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y,
-                 const double* k, double* partials, int32_t S, void* stream) {
-  EVC_CHECK_ARG(dx && y && delta && dlive && k && partials && dx->flags && y->flags && S > 0,
+int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
+                 double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, int32_t S,
+                 void* stream) {
+  EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && ticket && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   TView d = view_of(*dx), o = view_of(*y);
-  k_sparsify<<<dim3(d.GH, d.C, S), bt(d.W), 3 * d.GW, as_stream(stream)>>>(d, delta, ds, dlive, o, k, partials);
+  k_sparsify<<<dim3(d.GH, d.C, S), bt(d.W), 3 * d.GW, as_stream(stream)>>>(d, delta, ds, dlive, o, k, partials,
+                                                                           norm_ema, tp, ema_decay, ticket);
   EVC_LAUNCH_CHECK("sparsify");
   return EVC_OK;
 }
@@ -437,7 +468,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
 int evc_sparsify_finalize(const double* partials, int64_t n, double* norm_ema, double* k, double tp, double decay,
                           int32_t reset, int32_t S, void* stream) {
   EVC_CHECK_ARG(partials && norm_ema && k && S > 0, "sparsify_finalize: null argument");
-  k_sparsify_finalize<<<S, 256, 0, as_stream(stream)>>>(partials, n, norm_ema, k, tp, decay, reset);
+  k_sparsify_finalize<<<1, 256, 0, as_stream(stream)>>>(partials, n, norm_ema, k, tp, decay, reset, S);
   EVC_LAUNCH_CHECK("sparsify_finalize");
   return EVC_OK;
 }

@@ -594,15 +594,21 @@ class Graph:
         # int32 [flag counts (nm x S) | per conv: tile count (2) + mask scratch]
         z32 = nm * S + (nm * S) % 2
         conv_off = []
+        sp_off = []
         for node in self.nodes:
             if node.kind == "conv":
                 n = int(self.lib.evc_conv_mask_scratch(node.conv[0], S))
                 conv_off.append((node, z32, z32 + 2))
                 z32 += 2 + n + n % 2
+            elif node.kind == "sparsify":
+                sp_off.append((node, z32))
+                z32 += 2
         self._z32 = torch.zeros(z32, dtype=torch.int32, device=dev)
         base = self._z32.data_ptr()
         for node, c_off, s_off in conv_off:
             node.mask_scratch = (base + 4 * c_off, base + 4 * s_off)
+        for node, off in sp_off:
+            node.ticket = base + 4 * off
         self._cnt_step = self._z32[: nm * S].view(nm, S)
         self._perf_step = torch.zeros((nm, S), dtype=torch.int64, device=dev)
         self._perf_cum = torch.zeros((nm, S), dtype=torch.int64, device=dev)
@@ -697,12 +703,10 @@ class Graph:
                 npart = c * grid_shape((c, h, w), self.tile)[1]
                 prog.append((L.evc_sparsify, (self._desc(ns.inputs[0]), node.delta.data_ptr(), node.delta[0].numel(),
                                               node.dlive.data_ptr(), self._desc(nid),
-                                              self._k.data_ptr() + 8 * j * S, self._partials.data_ptr(), S),
+                                              self._k.data_ptr() + 8 * j * S, self._norm.data_ptr() + 8 * j * S,
+                                              node.tp, node.ema_decay, self._partials.data_ptr(), node.ticket, S),
                              "sparsify"))
-                prog.append((L.evc_sparsify_finalize, (self._partials.data_ptr(), npart,
-                                                       self._norm.data_ptr() + 8 * j * S,
-                                                       self._k.data_ptr() + 8 * j * S, node.tp, node.ema_decay, 0, S),
-                             "sparsify_finalize"))
+                del npart
             elif k == "add":
                 prog.append((L.evc_add, (self._desc(ns.inputs[0]), self._desc(ns.inputs[1]), self._desc(nid), S),
                              "add"))

@@ -68,10 +68,10 @@ def sparsify_step(x: IncrementTensor, state: SparsifyState) -> IncrementTensor:
     lib = _lib.lib()
     s = _lib.stream_ptr()
     dy = _lib.tdesc(_lib.ptr(yv), _lib.ptr(yf), 0, 0, c, h, w, tile.h, tile.w)
+    ticket = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.check(lib.evc_sparsify(x.desc(), _lib.ptr(state.delta), 0, _lib.ptr(dlive), dy, _lib.ptr(sc) + 8,
-                                _lib.ptr(part), 1, s), "sparsify")
-    _lib.check(lib.evc_sparsify_finalize(_lib.ptr(part), n_part, _lib.ptr(sc), _lib.ptr(sc) + 8, state.tp,
-                                         state.ema_decay, 0, 1, s), "sparsify_finalize")
+                                _lib.ptr(sc), state.tp, state.ema_decay, _lib.ptr(part), _lib.ptr(ticket), 1, s),
+               "sparsify")
     ne, k = sc.tolist()
     state.norm_ema = ne
     if state.tp > 0:

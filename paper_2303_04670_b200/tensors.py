@@ -251,7 +251,7 @@ def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148
     if ctas >= target_ctas:
         return 1
     s = -(-target_ctas // ctas)
-    return int(max(1, min(s, k // 256, 16)))
+    return int(max(1, min(s, k // 64, 32)))
 
 
 def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> torch.Tensor:

@@ -81,6 +81,12 @@ def _meter_from_table(tab, flags, c_out):
                 continue
             box = flags[:, R[u, 0]:R[u, 0] + R[u, 1], Cc[v, 0]:Cc[v, 0] + Cc[v, 1]]
             border += d * int(box.reshape(c_in, -1).any(axis=1).sum())
+    # the device sums the same border term over host-grouped boxes
+    grp, ngrp = int(tab[16]), int(tab[17])
+    G = tab[grp:grp + 5 * ngrp].reshape(ngrp, 5)
+    border_g = sum(int(d) * int(flags[:, a0:a0 + na, b0:b0 + nb].reshape(c_in, -1).any(axis=1).sum())
+                   for a0, na, b0, nb, d in G)
+    assert border_g == border
     return 2 * c_out * (term1 + border)
 
 

@@ -148,16 +148,25 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
 int64_t evc_conv_workspace(const evc_conv_geom* g, int64_t max_tiles, int32_t splits);
 
 /* Gather -> GEMM -> scatter over active output tiles.
- * tile_list/tile_count: ascending (s*T + t) entries (evc_compact output);
+ * tile_list/tile_count: (s*T + t) entries (evc_conv_mask output, any order);
  * tile_list == NULL means every tile of every session (dense pass).
- * weight: (C_out, C_in, KH, KW) fp32 as stored by the reference
- * (graph.py:457-467); bias may be NULL (increments drop it).
- * splits > 1 uses the fp32 workspace and a deterministic reduction. */
+ * wpack != NULL selects the tcgen05 tensor-core kernel (3xTF32 split, fp32
+ * TMEM accumulation) with weights pre-packed by evc_conv_tc_pack;
+ * otherwise `weight` ((C_out, C_in, KH, KW) fp32 as stored by the reference,
+ * graph.py:457-467) feeds the FFMA kernel.  bias may be NULL (increments
+ * drop it).  splits > 1 uses the fp32 workspace and a deterministic
+ * reduction. */
 int evc_conv_gemm(const evc_conv_geom* g, const evc_tensor* in,
-                  const float* weight, const float* bias, const evc_tensor* out,
-                  const int32_t* table, const int32_t* tile_list,
-                  const int32_t* tile_count, int32_t S, int32_t splits,
-                  float* workspace, void* stream);
+                  const float* weight, const float* wpack, const float* bias,
+                  const evc_tensor* out, const int32_t* table,
+                  const int32_t* tile_list, const int32_t* tile_count,
+                  int32_t S, int32_t splits, float* workspace, void* stream);
+
+/* Host helpers for the tensor-core path: pack (C_out, K) fp32 weights into
+ * the pre-split (hi = TF32 truncation, lo = w - hi), 128B-swizzled,
+ * K-major SMEM images streamed by cp.async.bulk (length in floats). */
+int64_t evc_conv_tc_pack_len(int32_t c_out, int64_t K);
+int evc_conv_tc_pack(const float* w, int32_t c_out, int64_t K, float* out);
 
 /* ---- nonlinearities / elementwise (increment_ops.py:226-310) ---------- */
 

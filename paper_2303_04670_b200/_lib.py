@@ -63,7 +63,9 @@ _PROTOS = {
     "evc_conv_mask_scratch": (_I64, [_G, _I32]),
     "evc_conv_mask": (_I32, [_G, _T, _T, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
-    "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
+    "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
+    "evc_conv_tc_pack_len": (_I64, [_I32, _I64]),
+    "evc_conv_tc_pack": (_I32, [_P, _I32, _I64, _P]),
     "evc_act_delta": (_I32, [_T, _P, _I64, _T, _I32, _F, _I32, _P]),
     "evc_act_dense": (_I32, [_P, _I64, _P, _I64, _P, _I64, _I64, _I32, _F, _I32, _P]),
     "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _I32, _P]),

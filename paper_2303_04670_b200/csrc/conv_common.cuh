@@ -46,4 +46,11 @@ static inline TabHdr tab_layout(const evc_conv_geom* g) {
   return h;
 }
 
+// tcgen05 path (conv_tc.cu): launches the tensor-core GEMM; returns the
+// effective number of K-splits (>= 1) or a negative EVC_E* code.
+int conv_tc_launch(const evc_conv_geom* g, const evc_tensor* in, const float* wpack, const float* bias,
+                   const evc_tensor* out, const int32_t* table, const int32_t* tile_list, const int32_t* tile_count,
+                   int32_t S, int32_t splits, float* workspace, cudaStream_t st);
+int init_conv_tc();
+
 }  // namespace evc

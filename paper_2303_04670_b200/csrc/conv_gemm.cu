@@ -222,10 +222,10 @@ int64_t evc_conv_workspace(const evc_conv_geom* g, int64_t max_tiles, int32_t sp
   return (int64_t)splits * max_tiles * g->th * g->tw * g->c_out;
 }
 
-int evc_conv_gemm(const evc_conv_geom* g, const evc_tensor* in, const float* weight, const float* bias,
-                  const evc_tensor* out, const int32_t* table, const int32_t* tile_list, const int32_t* tile_count,
-                  int32_t S, int32_t splits, float* workspace, void* stream) {
-  EVC_CHECK_ARG(g && in && out && weight && table && S > 0 && splits >= 1, "conv_gemm: null argument");
+int evc_conv_gemm(const evc_conv_geom* g, const evc_tensor* in, const float* weight, const float* wpack,
+                  const float* bias, const evc_tensor* out, const int32_t* table, const int32_t* tile_list,
+                  const int32_t* tile_count, int32_t S, int32_t splits, float* workspace, void* stream) {
+  EVC_CHECK_ARG(g && in && out && (weight || wpack) && table && S > 0 && splits >= 1, "conv_gemm: null argument");
   EVC_CHECK_ARG(!tile_list || tile_count, "conv_gemm: tile_count required with tile_list");
   EVC_CHECK_ARG(splits == 1 || workspace, "conv_gemm: workspace required for split-K");
   GemmArgs a;
@@ -252,16 +252,22 @@ int evc_conv_gemm(const evc_conv_geom* g, const evc_tensor* in, const float* wei
   const int64_t max_m = (int64_t)S * a.T * g->th * g->tw;
   a.mcap = max_m;
   cudaStream_t st = as_stream(stream);
-  if (g->c_out > 24 && g->c_out <= 32)
+  if (wpack) {  // tcgen05 3xTF32 path (conv_tc.cu)
+    const int eff = conv_tc_launch(g, in, wpack, bias, out, table, tile_list, tile_count, S, splits, workspace, st);
+    EVC_CHECK_ARG(eff >= 1, "conv_gemm: unsupported tensor-core geometry");
+    a.splits = eff;
+    EVC_LAUNCH_CHECK("conv_gemm_tc");
+  } else if (g->c_out > 24 && g->c_out <= 32) {
     launch_gemm<128, 32, 8, 4>(a, max_m, st);
-  else if (g->c_out > 32)
+  } else if (g->c_out > 32) {
     launch_gemm<128, 64, 8, 4>(a, max_m, st);
-  else if (g->c_out > 4)
+  } else if (g->c_out > 4) {
     launch_gemm<256, 16, 8, 4>(a, max_m, st);
-  else
+  } else {
     launch_gemm<256, 4, 4, 2>(a, max_m, st);
+  }
   EVC_LAUNCH_CHECK("conv_gemm");
-  if (splits > 1) {
+  if (a.splits > 1) {
     const int64_t work = max_m * g->c_out;
     const int blocks = (int)std::min<int64_t>(cdiv64(work, 256), 148 * 8);
     k_conv_splitk_reduce<<<blocks, 256, 0, st>>>(a);
@@ -276,6 +282,7 @@ namespace evc {
 int init_conv() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k_conv_splitk_reduce) != cudaSuccess) return EVC_ECUDA;
-  return init_conv_mask();
+  const int rc = init_conv_mask();
+  return rc ? rc : init_conv_tc();
 }
 }  // namespace evc

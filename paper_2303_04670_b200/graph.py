@@ -35,6 +35,7 @@ from .tensors import (
     as_tensor,
     choose_splits,
     conv_geometry,
+    pack_conv_weight,
     conv_output_hw,
     grid_shape,
 )
@@ -413,6 +414,7 @@ class _Node:
         self.out_shape = out_shape
         self.weight = None
         self.bias = None
+        self.wpack = None
         self.conv = None  # (geom, table, splits)
         self.acc = None
         self.acc2 = None
@@ -435,7 +437,7 @@ class Graph:
     """
 
     def __init__(self, spec: ModelSpec, weights, refresh_interval: int = DEFAULT_REFRESH_INTERVAL, *,
-                 sessions: int = 1, cuda_graph: bool = True, device=None):
+                 sessions: int = 1, cuda_graph: bool = True, device=None, conv_kernel: str | None = None):
         self.lib = _lib.lib()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.spec = spec
@@ -448,6 +450,11 @@ class Graph:
         if self.S < 1:
             raise ValueError("sessions must be >= 1")
         self.use_cuda_graph = bool(cuda_graph)
+        from . import tensors as _t
+
+        self.conv_kernel = conv_kernel or _t.CONV_KERNEL
+        if self.conv_kernel not in ("tc", "simt"):
+            raise ValueError(f"unknown conv kernel {self.conv_kernel!r}")
         self.shapes = spec.infer_shapes()
         order = spec.topo_order()
         if isinstance(weights, WeightManifest):
@@ -478,12 +485,14 @@ class Graph:
             node.weight = as_matrix(self._take(weights, f"{ns.id}.weight", (c_out, in_shape[0], kh, kw)), dev)
             b = self._take(weights, f"{ns.id}.bias", (c_out,), required=False)
             node.bias = None if b is None else as_bias(b, c_out, dev)
+            node.wpack = pack_conv_weight(node.weight) if self.conv_kernel == "tc" else None
             c, h, w = in_shape
             g, tab = conv_geometry(c, c_out, kh, kw, st, pad, h, w, self.tile.h, self.tile.w)
             ho, wo = int(g.Ho), int(g.Wo)
             tiles = grid_shape((c_out, ho, wo), self.tile)
             T = tiles[1] * tiles[2]
-            splits = choose_splits(self.S * T * self.tile.h * self.tile.w, c_out, c * kh * kw)
+            splits = choose_splits(self.S * T * self.tile.h * self.tile.w, c_out, c * kh * kw,
+                                   kernel=self.conv_kernel)
             node.conv = (g, tab, splits, T, 2 * kh * kw * c * c_out * ho * wo)
         elif ns.kind == "linear":
             f = int(ns.attrs["out_features"])
@@ -680,8 +689,8 @@ class Graph:
                 count_ptr, scratch_ptr = node.mask_scratch
                 prog.append((L.evc_conv_mask, (g, din, dout, tab.data_ptr(), scratch_ptr, cnt_ptr,
                                                self._tile_list.data_ptr(), count_ptr, perf_ptr, S), "conv_mask"))
-                prog.append((L.evc_conv_gemm, (g, din, node.weight.data_ptr(), None, dout, tab.data_ptr(),
-                                               self._tile_list.data_ptr(), count_ptr, S, splits,
+                prog.append((L.evc_conv_gemm, (g, din, node.weight.data_ptr(), _lib.ptr(node.wpack), None, dout,
+                                               tab.data_ptr(), self._tile_list.data_ptr(), count_ptr, S, splits,
                                                self._conv_ws.data_ptr()), "conv_gemm"))
             elif k == "linear":
                 mi = node.meter_idx
@@ -773,8 +782,8 @@ class Graph:
             if k == "conv":
                 g, tab, splits, T, _ = node.conv
                 run(L.evc_conv_gemm, g, self._desc(ns.inputs[0], False), node.weight.data_ptr(),
-                    None if node.bias is None else node.bias.data_ptr(), self._desc(nid, False), tab.data_ptr(), None,
-                    None, S, splits, self._conv_ws.data_ptr())
+                    _lib.ptr(node.wpack), None if node.bias is None else node.bias.data_ptr(), self._desc(nid, False),
+                    tab.data_ptr(), None, None, S, splits, self._conv_ws.data_ptr())
             elif k == "linear":
                 f = int(ns.attrs["out_features"])
                 run(L.evc_linear, self._desc(ns.inputs[0], False), node.weight.data_ptr(),

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, tensors
 from .tensors import (
     Activation,
     IncrementTensor,
@@ -30,6 +30,7 @@ from .tensors import (
     conv_output_hw,
     grid_shape,
     make_tile_mask,
+    pack_conv_weight,
 )
 
 __all__ = [
@@ -150,8 +151,9 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     ws = None
     if splits > 1:
         ws = torch.empty(int(lib.evc_conv_workspace(g, T, splits)), dtype=torch.float32, device=dev)
-    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), None, dout, _lib.ptr(tab), _lib.ptr(tiles),
-                                 _lib.ptr(i32) + 4, 1, splits, _lib.ptr(ws), s), "conv_gemm")
+    wpack = pack_conv_weight(weight) if tensors.CONV_KERNEL == "tc" else None
+    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), _lib.ptr(wpack), None, dout, _lib.ptr(tab),
+                                 _lib.ptr(tiles), _lib.ptr(i32) + 4, 1, splits, _lib.ptr(ws), s), "conv_gemm")
     meter.add(int(perf.item()), 0)
     return IncrementTensor(yv, TileMask(yf, tile))
 

@@ -9,6 +9,7 @@ and uploaded.  Every operator runs in libevconv.so; there is no CPU path.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -244,8 +245,28 @@ def conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw):
     return g, tab
 
 
-def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148) -> int:
+CONV_KERNEL = os.environ.get("EVC_CONV_KERNEL", "tc")  # "tc" (tcgen05 3xTF32) or "simt" (FFMA)
+
+
+def pack_conv_weight(weight: torch.Tensor):
+    """Pre-split (hi/lo) + 128B-swizzle a (C_out, C_in, KH, KW) weight for the tcgen05 kernel."""
+    c_out = int(weight.shape[0])
+    k = int(np.prod(weight.shape[1:]))
+    lib = _lib.lib()
+    host = np.ascontiguousarray(weight.detach().cpu().numpy().reshape(c_out, k), dtype=np.float32)
+    out = np.zeros(int(lib.evc_conv_tc_pack_len(c_out, k)), dtype=np.float32)
+    _lib.check(lib.evc_conv_tc_pack(host.ctypes.data, c_out, k, out.ctypes.data), "conv_tc_pack")
+    return torch.from_numpy(out).to(weight.device)
+
+
+def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148, kernel: str | None = None) -> int:
     """K-splits so the worst-case grid still fills the B200 (148 SMs)."""
+    if (kernel or CONV_KERNEL) == "tc":
+        ctas = max(1, -(-max_sites // 128)) * max(1, -(-c_out // 256))
+        if ctas >= 148:
+            return 1
+        nkb = -(-k // 32)
+        return int(max(1, min(-(-148 // ctas), nkb // 2, 64)))
     bm, bn = (128, 64) if c_out > 32 else ((128, 32) if c_out > 24 else (256, 16))
     ctas = max(1, -(-max_sites // bm)) * max(1, -(-c_out // bn))
     if ctas >= target_ctas:
@@ -277,8 +298,9 @@ def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> tor
         ws = torch.empty(int(lib.evc_conv_workspace(g, tiles, splits)), dtype=torch.float32, device=x.device)
     din = _lib.tdesc(_lib.ptr(x), None, 0, 0, c, h, w, th, tw)
     dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, c_out, ho, wo, th, tw)
-    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), _lib.ptr(b), dout, _lib.ptr(tab), None, None, 1, splits,
-                                 _lib.ptr(ws), _lib.stream_ptr()), "conv_gemm")
+    wpack = pack_conv_weight(weight) if CONV_KERNEL == "tc" else None
+    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), _lib.ptr(wpack), _lib.ptr(b), dout, _lib.ptr(tab), None,
+                                 None, 1, splits, _lib.ptr(ws), _lib.stream_ptr()), "conv_gemm")
     return y
 
 

@@ -48,10 +48,14 @@ def test_conv_golden(golden):
         assert np.array_equal(np_(y.mask.active_indices()), np.flatnonzero(c["yflags"])), i
 
 
+@pytest.mark.parametrize("kernel", ["tc", "simt"])
 @pytest.mark.parametrize("shape,k,st,pad,d", [((64, 120, 160), 3, 1, 1, 0.02), ((32, 64, 64), 3, 2, 1, 0.3),
                                               ((256, 16, 16), 3, 1, 1, 0.9), ((66, 64, 64), 3, 1, 1, 0.5),
-                                              ((16, 64, 64), 1, 1, 0, 0.7), ((2, 45, 61), 7, 2, 3, 0.4)])
-def test_conv_vs_oracle(shape, k, st, pad, d):
+                                              ((16, 64, 64), 1, 1, 0, 0.7), ((2, 45, 61), 7, 2, 3, 0.4),
+                                              ((512, 32, 32), 3, 1, 1, 1.0), ((130, 40, 44), 3, 1, 1, 0.6)])
+def test_conv_vs_oracle(shape, k, st, pad, d, kernel, monkeypatch):
+    from paper_2303_04670_b200 import tensors
+    monkeypatch.setattr(tensors, "CONV_KERNEL", kernel)
     rng = np.random.default_rng(7)
     c, h, w = shape
     gh, gw = -(-h // 6), -(-w // 6)

@@ -238,28 +238,19 @@ def conv_roofline(g, xs, args, evc):
     prog = g2._program
     gemm_ms, gemm_flops, step_ms = [], [], []
     nsteps = min(8, xs.shape[0] - 1)
+    conv_idx = [n.meter_idx for n in g2.nodes if n.kind == "conv"]
     for i in range(1, 1 + nsteps):
-        g2._perf_step.zero_()
-        g2._cnt_step.zero_()
         _lib.check(g2.lib.evc_diff_mask(xs[i - 1].data_ptr(), xs[i].data_ptr(), xs[0][0].numel(),
                                         g2._desc(g2.input_id), S, _lib.stream_ptr()), "diff")
-        pairs = []
+        timed = ({"conv_gemm"}, [])
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
-        for fn, a, name in prog:
-            if name == "conv_gemm":
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                _lib.check(fn(*a, _lib.stream_ptr()), name)
-                e1.record()
-                pairs.append((e0, e1))
-            else:
-                _lib.check(fn(*a, _lib.stream_ptr()), name)
+        g2._run_program(timed=timed)
         s1.record()
         torch.cuda.synchronize()
-        gemm_ms.append(sum(a.elapsed_time(b) for a, b in pairs))
+        gemm_ms.append(sum(a.elapsed_time(b) for _, a, b in timed[1]))
         step_ms.append(s0.elapsed_time(s1))
-        gemm_flops.append(int(g2._perf_step[[n.meter_idx for n in g2.nodes if n.kind == "conv"]].sum()))
+        gemm_flops.append(int(g2._perf_step[conv_idx].sum()))
     t = sum(gemm_ms) / len(gemm_ms) / 1e3
     f = sum(gemm_flops) / len(gemm_flops)
     achieved = f / t / 1e12

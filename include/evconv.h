@@ -133,15 +133,37 @@ int evc_conv_table_fill(const evc_conv_geom* g, int32_t* host_table);
  *    to tile_list and counts them in *tile_count (work list of
  *    evc_conv_gemm; the GEMM result does not depend on list order),
  *  - meter[s] += performed FLOPs (int64, the exact reference meter).
- * scratch (evc_conv_mask_scratch int32 entries), in_true and tile_count
- * must be zeroed before the call.  `table` is the device copy of
- * evc_conv_table_fill's output. */
+ * With region_flags != NULL it also sets region_flags[s][ri*RWn + rj] = 1
+ * for every 4x32 output region (evc_conv_region_grid) overlapping a live
+ * tile: the work list of evc_conv_gemm_region.  tile_list/tile_count may be
+ * NULL when only regions are wanted.
+ * scratch (evc_conv_mask_scratch int32 entries), in_true, tile_count and
+ * region_flags must be zeroed before the call.  `table` is the device copy
+ * of evc_conv_table_fill's output. */
 int64_t evc_conv_mask_scratch(const evc_conv_geom* g, int32_t S);
 int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
                   const evc_tensor* out, const int32_t* table,
                   int32_t* scratch, int32_t* in_true, int32_t* tile_list,
-                  int32_t* tile_count, int64_t* meter, int32_t S,
-                  void* stream);
+                  int32_t* tile_count, uint8_t* region_flags, int64_t* meter,
+                  int32_t S, void* stream);
+
+/* TMA-fed tensor-core GEMM for stride-1 convolutions over 4x32 output
+ * regions (conv_tma.cu): the im2col A operand is loaded as TMA boxes of
+ * the channel-planar input (zero padding = TMA out-of-bounds fill), the
+ * weights are packed by evc_conv_region_pack (K order: tap, then channel
+ * padded to 32).  region_flags == NULL computes every region (dense pass).
+ * Supported when stride == 1 and the input rows/planes are 16-byte
+ * aligned (evc_conv_region_supported). */
+int evc_conv_region_supported(const evc_conv_geom* g, int64_t vstride);
+int evc_conv_region_grid(const evc_conv_geom* g, int32_t* rh, int32_t* rw);
+int64_t evc_conv_region_pack_len(int32_t c_out, int32_t c_in, int32_t kh, int32_t kw);
+int evc_conv_region_pack(const float* w, int32_t c_out, int32_t c_in, int32_t kh,
+                         int32_t kw, float* out);
+int64_t evc_conv_region_workspace(const evc_conv_geom* g, int32_t S, int32_t splits);
+int evc_conv_gemm_region(const evc_conv_geom* g, const evc_tensor* in,
+                         const float* wpack, const float* bias,
+                         const evc_tensor* out, const uint8_t* region_flags,
+                         int32_t S, int32_t splits, float* workspace, void* stream);
 
 /* Workspace floats needed by evc_conv_gemm for `max_tiles` active output
  * tiles and `splits` K-splits. */

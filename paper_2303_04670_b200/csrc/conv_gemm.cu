@@ -282,7 +282,8 @@ namespace evc {
 int init_conv() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k_conv_splitk_reduce) != cudaSuccess) return EVC_ECUDA;
-  const int rc = init_conv_mask();
-  return rc ? rc : init_conv_tc();
+  int rc = init_conv_mask();
+  if (!rc) rc = init_conv_tc();
+  return rc ? rc : init_conv_tma();
 }
 }  // namespace evc

@@ -133,9 +133,10 @@ struct MaskArgs {
   int32_t* in_true;  // [S]            live input flags
   int32_t* list;
   int32_t* count;
+  uint8_t* regions;  // optional [S][RHn*RWn] flags of 4x32 output regions (TMA GEMM work)
   int64_t* meter;
   int64_t dense;  // 2*K^2*C_in*C_out*Ho*Wo
-  int c_in, c_out, nb_count;
+  int c_in, c_out, nb_count, RHn, RWn;
 };
 
 constexpr int kCountThreads = 256;
@@ -231,7 +232,16 @@ __global__ void __launch_bounds__(256) k_conv_flags(MaskArgs a) {
       a.out.plane(s, co)[(int64_t)(u0 + l / wd) * h.Wo + v0 + l % wd] = 0.0f;
     }
   }
-  if (nf && lane == 0) a.list[atomicAdd(a.count, 1)] = s * To + t;
+  if (nf && lane == 0) {
+    if (a.list) a.list[atomicAdd(a.count, 1)] = s * To + t;
+    if (a.regions) {  // mark the 4x32 output regions this tile overlaps (benign races: all store 1)
+      const int th = a.out.th, tw = a.out.tw;
+      const int ulast = min(h.Ho, (i + 1) * th) - 1, vlast = min(h.Wo, (j + 1) * tw) - 1;
+      for (int ri = (i * th) / 4; ri <= ulast / 4; ++ri)
+        for (int rj = (j * tw) / 32; rj <= vlast / 32; ++rj)
+          a.regions[((int64_t)s * a.RHn + ri) * a.RWn + rj] = 1;
+    }
+  }
 }
 
 }  // namespace evc
@@ -256,10 +266,10 @@ int64_t evc_conv_mask_scratch(const evc_conv_geom* g, int32_t S) {
 }
 
 int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in, const evc_tensor* out, const int32_t* table,
-                  int32_t* scratch, int32_t* in_true, int32_t* tile_list, int32_t* tile_count, int64_t* meter,
-                  int32_t S, void* stream) {
-  EVC_CHECK_ARG(g && in && out && table && scratch && in_true && tile_list && tile_count && meter && S > 0,
-                "conv_mask: null argument");
+                  int32_t* scratch, int32_t* in_true, int32_t* tile_list, int32_t* tile_count,
+                  uint8_t* region_flags, int64_t* meter, int32_t S, void* stream) {
+  EVC_CHECK_ARG(g && in && out && table && scratch && in_true && meter && S > 0, "conv_mask: null argument");
+  EVC_CHECK_ARG((tile_list != nullptr) == (tile_count != nullptr), "conv_mask: tile_list needs tile_count");
   EVC_CHECK_ARG(in->flags && out->flags, "conv_mask: masks required");
   const TabHdr h = tab_layout(g);
   // number of border groups is static per geometry; recompute it host-side
@@ -283,6 +293,9 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in, const evc_tensor
   a.in_true = in_true;
   a.list = tile_list;
   a.count = tile_count;
+  a.regions = region_flags;
+  a.RHn = (g->Ho + 3) / 4;
+  a.RWn = (g->Wo + 31) / 32;
   a.meter = meter;
   a.c_in = g->c_in;
   a.c_out = g->c_out;

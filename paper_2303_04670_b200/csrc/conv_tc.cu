@@ -111,7 +111,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// hi = x rounded to the nearest TF32 (ties away from zero), exactly representable
+// in TF32; lo = x - hi is exact in fp32 and |lo| <= 2^-11 |x|.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 // ---------------------------------------------------------------------------
 // kernel
@@ -417,7 +421,7 @@ int evc_conv_tc_pack(const float* w, int32_t c_out, int64_t K, float* out) {
           const float x = (n < c_out && k < K) ? w[n * K + k] : 0.0f;
           uint32_t bits;
           memcpy(&bits, &x, 4);
-          bits &= 0xFFFFE000u;
+          bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32, as tf32_hi()
           float h;
           memcpy(&h, &bits, 4);
           // 128B swizzle: 16-byte chunk j of row r lives at chunk (j ^ (r & 7))

@@ -27,15 +27,13 @@ import yaml
 
 from . import _lib
 from .tensors import (
+    ConvPlan,
     IncrementTensor,
     TileMask,
     TileShape,
     as_bias,
     as_matrix,
     as_tensor,
-    choose_splits,
-    conv_geometry,
-    pack_conv_weight,
     conv_output_hw,
     grid_shape,
 )
@@ -485,15 +483,7 @@ class Graph:
             node.weight = as_matrix(self._take(weights, f"{ns.id}.weight", (c_out, in_shape[0], kh, kw)), dev)
             b = self._take(weights, f"{ns.id}.bias", (c_out,), required=False)
             node.bias = None if b is None else as_bias(b, c_out, dev)
-            node.wpack = pack_conv_weight(node.weight) if self.conv_kernel == "tc" else None
-            c, h, w = in_shape
-            g, tab = conv_geometry(c, c_out, kh, kw, st, pad, h, w, self.tile.h, self.tile.w)
-            ho, wo = int(g.Ho), int(g.Wo)
-            tiles = grid_shape((c_out, ho, wo), self.tile)
-            T = tiles[1] * tiles[2]
-            splits = choose_splits(self.S * T * self.tile.h * self.tile.w, c_out, c * kh * kw,
-                                   kernel=self.conv_kernel)
-            node.conv = (g, tab, splits, T, 2 * kh * kw * c * c_out * ho * wo)
+            node.conv_attrs = (st, pad)  # the ConvPlan is made in _plan, once input placement is known
         elif ns.kind == "linear":
             f = int(ns.attrs["out_features"])
             length = int(np.prod(in_shape))
@@ -588,10 +578,12 @@ class Graph:
                 node.meter_idx = len(meter_ids)
                 meter_ids.append(node.spec.id)
             if k == "conv":
-                g, tab, splits, T, _ = node.conv
-                max_T = max(max_T, S * T)
-                if splits > 1:
-                    max_ws = max(max_ws, int(self.lib.evc_conv_workspace(g, S * T, splits)))
+                st_, pad_ = node.conv_attrs
+                src = self._slots[node.spec.inputs[0]].store
+                node.plan = ConvPlan(node.weight, st_, pad_, ish[1], ish[2], tile.h, tile.w, S,
+                                     vstride=src.C * src.H * src.W, kernel=self.conv_kernel)
+                max_T = max(max_T, S * node.plan.T)
+                max_ws = max(max_ws, node.plan.ws_floats)
             if k == "linear":
                 f = int(node.spec.attrs["out_features"])
                 lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
@@ -606,16 +598,17 @@ class Graph:
         sp_off = []
         for node in self.nodes:
             if node.kind == "conv":
-                n = int(self.lib.evc_conv_mask_scratch(node.conv[0], S))
-                conv_off.append((node, z32, z32 + 2))
-                z32 += 2 + n + n % 2
+                n = int(self.lib.evc_conv_mask_scratch(node.plan.g, S))
+                nreg = -(-(S * -(-int(node.plan.g.Ho) // 4) * -(-int(node.plan.g.Wo) // 32)) // 4)  # u8 -> int32
+                conv_off.append((node, z32, z32 + 2, z32 + 2 + n + n % 2))
+                z32 += 2 + n + n % 2 + nreg + nreg % 2
             elif node.kind == "sparsify":
                 sp_off.append((node, z32))
                 z32 += 2
         self._z32 = torch.zeros(z32, dtype=torch.int32, device=dev)
         base = self._z32.data_ptr()
-        for node, c_off, s_off in conv_off:
-            node.mask_scratch = (base + 4 * c_off, base + 4 * s_off)
+        for node, c_off, s_off, r_off in conv_off:
+            node.mask_scratch = (base + 4 * c_off, base + 4 * s_off, base + 4 * r_off)
         for node, off in sp_off:
             node.ticket = base + 4 * off
         self._cnt_step = self._z32[: nm * S].view(nm, S)
@@ -645,7 +638,7 @@ class Graph:
 
     def _dense_equiv(self, node) -> int:
         if node.kind == "conv":
-            return node.conv[4]
+            return node.plan.dense_flops
         f = int(node.spec.attrs["out_features"])
         return 2 * f * int(np.prod(self.shapes[node.spec.inputs[0]]))
 
@@ -681,17 +674,17 @@ class Graph:
             ns, k = node.spec, node.kind
             nid = ns.id
             if k == "conv":
-                g, tab, splits, T, _ = node.conv
+                plan = node.plan
                 mi = node.meter_idx
                 din, dout = self._desc(ns.inputs[0]), self._desc(nid)
                 cnt_ptr = i32.data_ptr() + 4 * mi * S
                 perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
-                count_ptr, scratch_ptr = node.mask_scratch
-                prog.append((L.evc_conv_mask, (g, din, dout, tab.data_ptr(), scratch_ptr, cnt_ptr,
-                                               self._tile_list.data_ptr(), count_ptr, perf_ptr, S), "conv_mask"))
-                prog.append((L.evc_conv_gemm, (g, din, node.weight.data_ptr(), _lib.ptr(node.wpack), None, dout,
-                                               tab.data_ptr(), self._tile_list.data_ptr(), count_ptr, S, splits,
-                                               self._conv_ws.data_ptr()), "conv_gemm"))
+                count_ptr, scratch_ptr, region_ptr = node.mask_scratch
+                tl = self._tile_list.data_ptr()
+                prog.append((L.evc_conv_mask, plan.mask_args(din, dout, scratch_ptr, cnt_ptr, tl, count_ptr,
+                                                             region_ptr, perf_ptr), "conv_mask"))
+                fn, args = plan.gemm(din, dout, None, (tl, count_ptr, region_ptr), self._conv_ws.data_ptr())
+                prog.append((fn, args, "conv_gemm"))
             elif k == "linear":
                 mi = node.meter_idx
                 din = self._desc(ns.inputs[0])
@@ -749,11 +742,21 @@ class Graph:
         return _lib.tdesc(st.vals.data_ptr() + 4 * coff * hw, st.flags.data_ptr() + coff * st.GH * st.GW, st.C * hw,
                           st.C * st.GH * st.GW, c, sl.H, sl.W, self.tile.h, self.tile.w)
 
-    def _run_program(self):
+    def _run_program(self, timed=None):
+        """One incr_step launch sequence.  ``timed``: optional (names, list) --
+        CUDA events are recorded around every launch whose name is in ``names``
+        (eager runs only; used by bench.py for per-kernel timing)."""
         s = _lib.stream_ptr()
         self._perf_step.zero_()
         self._z32.zero_()
         for fn, args, name in self._program:
+            if timed is not None and name in timed[0]:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                _lib.check(fn(*args, s), name)
+                e1.record()
+                timed[1].append((name, e0, e1))
+                continue
             _lib.check(fn(*args, s), name)
         # device-side meter bookkeeping (graph.py:620-629, 632-636)
         self._perf_cum.add_(self._perf_step)
@@ -765,8 +768,7 @@ class Graph:
         n = 0
         for fn, args, name in self._program:
             n += 2 if name in ("conv_mask", "maxpool", "linear") else 1
-            if name == "conv_gemm" and args[9] > 1:
-                n += 1
+        n += sum(1 for nd in self.nodes if nd.kind == "conv" and nd.plan.splits > 1)  # split-K reduce
         return n
 
     # -- dense evaluation (graph.py:503-565) ----------------------------------------
@@ -780,10 +782,9 @@ class Graph:
         for node in self.nodes:
             ns, k, nid = node.spec, node.kind, node.spec.id
             if k == "conv":
-                g, tab, splits, T, _ = node.conv
-                run(L.evc_conv_gemm, g, self._desc(ns.inputs[0], False), node.weight.data_ptr(),
-                    _lib.ptr(node.wpack), None if node.bias is None else node.bias.data_ptr(), self._desc(nid, False),
-                    tab.data_ptr(), None, None, S, splits, self._conv_ws.data_ptr())
+                fn, args = node.plan.gemm(self._desc(ns.inputs[0], False), self._desc(nid, False),
+                                          _lib.ptr(node.bias), None, self._conv_ws.data_ptr())
+                run(fn, *args)
             elif k == "linear":
                 f = int(ns.attrs["out_features"])
                 run(L.evc_linear, self._desc(ns.inputs[0], False), node.weight.data_ptr(),

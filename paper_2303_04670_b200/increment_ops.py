@@ -135,25 +135,23 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     tile = x.tile
     meter.add(0, 2 * kh * kw * c_in * c_out * ho * wo)
     lib = _lib.lib()
-    g, tab = conv_geometry(c_in, c_out, kh, kw, st, pad, h, w, tile.h, tile.w)
+    plan = tensors.ConvPlan(weight, st, pad, h, w, tile.h, tile.w)
     yv, yf = _zeros_incr((c_out, ho, wo), tile, dev)
     T = yf.shape[1] * yf.shape[2]
     i32 = torch.zeros(2, dtype=torch.int32, device=dev)  # [in_true, tile_count]
     tiles = torch.empty(T, dtype=torch.int32, device=dev)
-    scratch = torch.zeros(int(lib.evc_conv_mask_scratch(g, 1)), dtype=torch.int32, device=dev)
+    regions = torch.zeros(-(-ho // 4) * -(-wo // 32), dtype=torch.uint8, device=dev)
+    scratch = torch.zeros(int(lib.evc_conv_mask_scratch(plan.g, 1)), dtype=torch.int32, device=dev)
     perf = torch.zeros(1, dtype=torch.int64, device=dev)
     s = _lib.stream_ptr()
     din = x.desc()
     dout = _desc(yv, yf, tile)
-    _lib.check(lib.evc_conv_mask(g, din, dout, _lib.ptr(tab), _lib.ptr(scratch), _lib.ptr(i32), _lib.ptr(tiles),
-                                 _lib.ptr(i32) + 4, _lib.ptr(perf), 1, s), "conv_mask")
-    splits = choose_splits(T * tile.h * tile.w, c_out, c_in * kh * kw)
-    ws = None
-    if splits > 1:
-        ws = torch.empty(int(lib.evc_conv_workspace(g, T, splits)), dtype=torch.float32, device=dev)
-    wpack = pack_conv_weight(weight) if tensors.CONV_KERNEL == "tc" else None
-    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), _lib.ptr(wpack), None, dout, _lib.ptr(tab),
-                                 _lib.ptr(tiles), _lib.ptr(i32) + 4, 1, splits, _lib.ptr(ws), s), "conv_gemm")
+    _lib.check(lib.evc_conv_mask(*plan.mask_args(din, dout, _lib.ptr(scratch), _lib.ptr(i32), _lib.ptr(tiles),
+                                                 _lib.ptr(i32) + 4, _lib.ptr(regions), _lib.ptr(perf)), s),
+               "conv_mask")
+    ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=dev)
+    fn, args = plan.gemm(din, dout, None, (_lib.ptr(tiles), _lib.ptr(i32) + 4, _lib.ptr(regions)), ws.data_ptr())
+    _lib.check(fn(*args, s), "conv_gemm")
     meter.add(int(perf.item()), 0)
     return IncrementTensor(yv, TileMask(yf, tile))
 

@@ -259,6 +259,70 @@ def pack_conv_weight(weight: torch.Tensor):
     return torch.from_numpy(out).to(weight.device)
 
 
+class ConvPlan:
+    """Static launch plan of one conv layer: geometry table, kernel path, packed weights, K-splits.
+
+    path "region": stride-1 conv on 16-byte aligned planes -> TMA-fed tcgen05 GEMM over 4x32
+    output regions (evc_conv_gemm_region); path "tile": tcgen05 GEMM over gathered sites of the
+    active 6x6 output tiles (evc_conv_gemm with packed weights); path "simt": FFMA reference kernel.
+    """
+
+    def __init__(self, weight: torch.Tensor, stride, pad, h, w, th, tw, S=1, vstride=None, kernel=None):
+        lib = _lib.lib()
+        c_out, c_in, kh, kw = (int(v) for v in weight.shape)
+        self.g, self.table = conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw)
+        self.c_out, self.c_in, self.kh, self.kw, self.S = c_out, c_in, kh, kw, S
+        self.weight = weight
+        kernel = kernel or CONV_KERNEL
+        vs = c_in * h * w if vstride is None else int(vstride)
+        ho, wo = int(self.g.Ho), int(self.g.Wo)
+        T = -(-ho // th) * -(-wo // tw)
+        self.T = T
+        self.wpack = None
+        if kernel == "tc" and lib.evc_conv_region_supported(self.g, vs):
+            self.path = "region"
+            rh, rw = -(-ho // 4), -(-wo // 32)
+            self.n_regions = S * rh * rw
+            host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)
+            out = np.zeros(int(lib.evc_conv_region_pack_len(c_out, c_in, kh, kw)), dtype=np.float32)
+            _lib.check(lib.evc_conv_region_pack(host.ctypes.data, c_out, c_in, kh, kw, out.ctypes.data), "pack")
+            self.wpack = torch.from_numpy(out).to(weight.device)
+            bn = 256 if c_out >= 256 else max(16, -(-c_out // 16) * 16)
+            ctas = self.n_regions * -(-c_out // bn)
+            nkb = kh * kw * -(-c_in // 32)
+            self.splits = 1 if ctas >= 148 else int(max(1, min(-(-148 // ctas), nkb // 2, 64)))
+            self.ws_floats = int(lib.evc_conv_region_workspace(self.g, S, self.splits))
+        else:
+            self.path = "tile" if kernel == "tc" else "simt"
+            if self.path == "tile":
+                self.wpack = pack_conv_weight(weight)
+            self.splits = choose_splits(S * T * th * tw, c_out, c_in * kh * kw, kernel=kernel)
+            self.ws_floats = int(lib.evc_conv_workspace(self.g, S * T, self.splits))
+        self.dense_flops = 2 * kh * kw * c_in * c_out * ho * wo
+
+    def mask_args(self, din, dout, scratch, in_true, tile_list, tile_count, regions, meter):
+        """evc_conv_mask arguments (stream appended by the caller)."""
+        if self.path == "region":
+            tile_list = tile_count = None
+        else:
+            regions = None
+        return (self.g, din, dout, self.table.data_ptr(), scratch, in_true, tile_list, tile_count, regions, meter,
+                self.S)
+
+    def gemm(self, din, dout, bias_ptr, work, ws_ptr):
+        """(ctypes fn, args-without-stream) of the GEMM launch.
+
+        work = None for the dense pass (every tile / region), else the
+        (tile_list, tile_count, region_flags) device pointers from conv_mask."""
+        lib = _lib.lib()
+        tl, tc, rg = work if work is not None else (None, None, None)
+        if self.path == "region":
+            return lib.evc_conv_gemm_region, (self.g, din, _lib.ptr(self.wpack), bias_ptr, dout, rg, self.S,
+                                              self.splits, ws_ptr)
+        return lib.evc_conv_gemm, (self.g, din, self.weight.data_ptr(), _lib.ptr(self.wpack), bias_ptr, dout,
+                                   self.table.data_ptr(), tl, tc, self.S, self.splits, ws_ptr)
+
+
 def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148, kernel: str | None = None) -> int:
     """K-splits so the worst-case grid still fills the B200 (148 SMs)."""
     if (kernel or CONV_KERNEL) == "tc":
@@ -287,20 +351,14 @@ def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> tor
         raise ValueError(f"input has {c} channels but weight expects {c_in}")
     ho, wo = conv_output_hw(h, w, kh, kw, stride, padding)
     th, tw = (4, 32) if wo >= 32 else (8, max(1, wo))
-    g, tab = conv_geometry(c_in, c_out, kh, kw, stride, padding, h, w, th, tw)
+    plan = ConvPlan(weight, stride, padding, h, w, th, tw)
     y = torch.empty((c_out, ho, wo), dtype=torch.float32, device=x.device)
     b = None if bias is None else as_bias(bias, c_out, x.device)
-    tiles = -(-ho // th) * -(-wo // tw)
-    splits = choose_splits(tiles * th * tw, c_out, c_in * kh * kw)
-    lib = _lib.lib()
-    ws = None
-    if splits > 1:
-        ws = torch.empty(int(lib.evc_conv_workspace(g, tiles, splits)), dtype=torch.float32, device=x.device)
-    din = _lib.tdesc(_lib.ptr(x), None, 0, 0, c, h, w, th, tw)
-    dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, c_out, ho, wo, th, tw)
-    wpack = pack_conv_weight(weight) if CONV_KERNEL == "tc" else None
-    _lib.check(lib.evc_conv_gemm(g, din, _lib.ptr(weight), _lib.ptr(wpack), _lib.ptr(b), dout, _lib.ptr(tab), None,
-                                 None, 1, splits, _lib.ptr(ws), _lib.stream_ptr()), "conv_gemm")
+    ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=x.device)
+    din = _lib.tdesc(_lib.ptr(x), None, c * h * w, 0, c, h, w, th, tw)
+    dout = _lib.tdesc(_lib.ptr(y), None, c_out * ho * wo, 0, c_out, ho, wo, th, tw)
+    fn, args = plan.gemm(din, dout, _lib.ptr(b), None, ws.data_ptr())
+    _lib.check(fn(*args, _lib.stream_ptr()), "conv_gemm")
     return y
 
 

@@ -147,21 +147,24 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
                   int32_t* tile_count, uint8_t* region_flags, int64_t* meter,
                   int32_t S, void* stream);
 
-/* TMA-fed tensor-core GEMM for stride-1 convolutions over 4x32 output
- * regions (conv_tma.cu): the im2col A operand is loaded as TMA boxes of
- * the channel-planar input (zero padding = TMA out-of-bounds fill), the
- * weights are packed by evc_conv_region_pack (K order: tap, then channel
- * padded to 32).  region_flags == NULL computes every region (dense pass).
- * Supported when stride == 1 and the input rows/planes are 16-byte
- * aligned (evc_conv_region_supported). */
-int evc_conv_region_supported(const evc_conv_geom* g, int64_t vstride);
+/* TMA-fed tensor-core GEMM over 4x32 output regions (conv_tma.cu).  The
+ * conv input is first mirrored into a channels-innermost shadow
+ * (evc_to_hwc: element (s,y,x,c) at in_hwc[s*hwc_stride + (y*W + x)*cp + c],
+ * cp = evc_hwc_channels(C_in)); the im2col A operand is then exactly four TMA
+ * boxes per (tap, 32-channel) K-block, zero padding = TMA out-of-bounds fill.
+ * Weights are packed by evc_conv_region_pack (K order: tap, then channel
+ * padded to 32).  region_flags == NULL computes every region (dense pass). */
+int32_t evc_hwc_channels(int32_t c);
+int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp,
+               int32_t S, void* stream);
+int evc_conv_region_supported(const evc_conv_geom* g);
 int evc_conv_region_grid(const evc_conv_geom* g, int32_t* rh, int32_t* rw);
 int64_t evc_conv_region_pack_len(int32_t c_out, int32_t c_in, int32_t kh, int32_t kw);
 int evc_conv_region_pack(const float* w, int32_t c_out, int32_t c_in, int32_t kh,
                          int32_t kw, float* out);
 int64_t evc_conv_region_workspace(const evc_conv_geom* g, int32_t S, int32_t splits);
-int evc_conv_gemm_region(const evc_conv_geom* g, const evc_tensor* in,
-                         const float* wpack, const float* bias,
+int evc_conv_gemm_region(const evc_conv_geom* g, const float* in_hwc, int32_t cp,
+                         int64_t hwc_stride, const float* wpack, const float* bias,
                          const evc_tensor* out, const uint8_t* region_flags,
                          int32_t S, int32_t splits, float* workspace, void* stream);
 

@@ -62,12 +62,14 @@ _PROTOS = {
     "evc_conv_table_fill": (_I32, [_G, _P]),
     "evc_conv_mask_scratch": (_I64, [_G, _I32]),
     "evc_conv_mask": (_I32, [_G, _T, _T, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
-    "evc_conv_region_supported": (_I32, [_G, _I64]),
+    "evc_hwc_channels": (_I32, [_I32]),
+    "evc_to_hwc": (_I32, [_T, _P, _I64, _I32, _I32, _P]),
+    "evc_conv_region_supported": (_I32, [_G]),
     "evc_conv_region_grid": (_I32, [_G, _P, _P]),
     "evc_conv_region_pack_len": (_I64, [_I32, _I32, _I32, _I32]),
     "evc_conv_region_pack": (_I32, [_P, _I32, _I32, _I32, _I32, _P]),
     "evc_conv_region_workspace": (_I64, [_G, _I32, _I32]),
-    "evc_conv_gemm_region": (_I32, [_G, _T, _P, _P, _T, _P, _I32, _I32, _P, _P]),
+    "evc_conv_gemm_region": (_I32, [_G, _P, _I32, _I64, _P, _P, _T, _P, _I32, _I32, _P, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
     "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
     "evc_conv_tc_pack_len": (_I64, [_I32, _I64]),

@@ -1,24 +1,29 @@
-// TMA-fed tcgen05 implicit GEMM for stride-1 convolutions (decoders, residual
-// blocks, 1x1 heads: ~75 % of the EV-FlowNet FLOPs).
+// TMA-fed tcgen05 implicit GEMM for the incremental / dense convolution.
 //
-// M tile = a 4 x 32 region of output pixels.  For K order (tap r,s ; channel c)
-// one K-block is one tap and 32 channels, and its A operand is exactly four TMA
-// boxes of the channel-planar input, one per output row of the region:
-//   box = [32 pixels along W] x [1 row] x [32 channels] x [1 session]
-// at (x0 - pad + s, y0 + h - pad + r, c0, s).  TMA zero-fills out-of-range
-// coordinates, which *is* the convolution's zero padding (and the channel tail).
-// With SWIZZLE_128B each box lands as 32 K-rows of 128 B -> an MN-major canonical
-// UMMA operand (LBO = 4 KiB between the four 32-pixel M groups, SBO = 1 KiB
-// between 8-row K groups).  No per-element gathers, no index tables.
+// The conv input is mirrored into a channels-innermost ("HWC", channel count
+// padded to a multiple of 4) shadow buffer by k_to_hwc.  M tile = a 4 x 32
+// region of output pixels; one K-block = one tap (r, s) x 32 channels, and its
+// A operand is exactly four TMA boxes of the shadow, one per output row:
+//   box = [32 channels] x [32 pixels, traversal stride = conv stride] x [1 row] x [1 session]
+// at (c0, x0*st - pad + s, (y0 + h)*st - pad + r, session).  TMA zero-fills
+// out-of-range coordinates, which *is* the convolution's zero padding (and the
+// channel tail).  With SWIZZLE_128B each box lands as 32 pixel rows of 128 B =
+// the canonical K-major UMMA layout (8-row groups 1 KiB apart), so the four
+// boxes form the 128 x 32 A tile directly: no gathers, no index tables.  (The
+// channel start c0 is a multiple of 32, i.e. 128-byte aligned: TMA with a
+// swizzle mode traps on an unaligned innermost start, which rules out the
+// channel-planar layout for padded convs.)
 //
-// fp32 accuracy: 3xTF32 (hi*hi + hi*lo + lo*hi); four "split" warps turn each
-// landed fp32 box into hi (in place) and lo (second buffer) with plain linear
-// SMEM traffic -- the swizzle is layout-preserving, so no address math.
-// Weights are pre-split/pre-swizzled K-major images streamed by cp.async.bulk.
+// fp32 accuracy: 3xTF32 (hi*hi + hi*lo + lo*hi, fp32 TMEM accumulation); four
+// "split" warps turn each landed box into hi (in place, rounded to TF32) and
+// lo = x - hi (second buffer) with linear SMEM traffic -- the swizzle is
+// layout-preserving.  Weights are pre-split, pre-swizzled K-major images
+// streamed by cp.async.bulk.
 //
 // Roles (8 warps): warp 0 lane 0 = TMA producer; warp 1 = TMEM alloc + MMA
 // issuer (lane 0); warps 4-7 = hi/lo split, then epilogue (TMEM lane quadrant =
-// warp % 4 = output row of the region; lane = output column -> coalesced stores).
+// warp % 4 = output row of the region; lane = output column, so the CHW output
+// stores are coalesced).
 
 #include <cuda.h>
 
@@ -62,12 +67,12 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y, int c, int n,
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c, int x, int y, int n,
                                             uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
       "[%6];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(c), "r"(n), "r"(bar)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(x), "r"(y), "r"(n), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -81,13 +86,9 @@ __device__ __forceinline__ void commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-// SWIZZLE_128B operand descriptors (sm_100 version 1, layout type 2).
-__device__ __forceinline__ uint64_t desc_kmajor(uint32_t a) {  // B: K-major, SBO 1 KiB
+// K-major SWIZZLE_128B operand descriptor (sm_100 version 1, layout type 2, SBO 1 KiB).
+__device__ __forceinline__ uint64_t desc_k(uint32_t a) {
   return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
-__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t a) {  // A: MN-major, LBO 4 KiB, SBO 1 KiB
-  return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)(4096 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -121,7 +122,7 @@ struct Args {
   const uint8_t* region_flags;  // [S][RHn*RWn], nullptr = every region (dense pass)
   float* ws;
   int64_t mcap;
-  int c_in, c_out, kh, kw, pad, cchunks, nkb;
+  int c_in, c_out, kh, kw, stride, pad, cchunks, nkb;
   int Ho, Wo, RHn, RWn, S;
   int splits, kb_per_split;
 };
@@ -131,10 +132,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_tma(const __grid_constant__
   constexpr int NS = stages_of(BN);
   constexpr int STAGE = stage_bytes(BN);
   constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  // kind::tf32, fp32 accumulate, A MN-major (bit 15), B K-major, N = BN, M = 128
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | ((uint32_t)(BN >> 3) << 17) |
+  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
-  constexpr uint32_t A_BYTES = BM * 128;  // 4 boxes of 32 x 32 fp32
+  constexpr uint32_t A_BYTES = BM * 128;  // 4 boxes of 32 pixels x 32 channels
   constexpr uint32_t B_BYTES = 2 * BN * 128;
 
   const int R = a.RHn * a.RWn;
@@ -189,7 +190,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_tma(const __grid_constant__
         bar_arrive_tx(tma_bar(st), A_BYTES + B_BYTES);
 #pragma unroll
         for (int h = 0; h < RH; ++h)
-          tma_load_4d(abuf + h * 4096, &tmap, v0 - a.pad + q, u0 + h - a.pad + r, c0, s, tma_bar(st));
+          tma_load_4d(abuf + h * 4096, &tmap, c0, v0 * a.stride - a.pad + q, (u0 + h) * a.stride - a.pad + r, s,
+                      tma_bar(st));
         bulk_load(abuf + 2 * A_BYTES, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
       }
     }
@@ -204,10 +206,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_tma(const __grid_constant__
         const uint32_t bh = ah + 2 * A_BYTES, bl = bh + BN * 128;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint32_t ka = kk * 1024, kbo = kk * 32;  // K=8: next 8-row atom (A, MN-major) / +32 B (B, K-major)
-          mma(tmem, desc_mnmajor(ah + ka), desc_kmajor(bh + kbo), IDESC, (i | kk) ? 1u : 0u);
-          mma(tmem, desc_mnmajor(ah + ka), desc_kmajor(bl + kbo), IDESC, 1u);
-          mma(tmem, desc_mnmajor(al + ka), desc_kmajor(bh + kbo), IDESC, 1u);
+          const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
+          mma(tmem, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i | kk) ? 1u : 0u);
+          mma(tmem, desc_k(ah + ko), desc_k(bl + ko), IDESC, 1u);
+          mma(tmem, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
         }
         commit(empty_bar(st));
       }
@@ -295,6 +297,28 @@ __global__ void k_region_reduce(Args a) {
   }
 }
 
+// CHW -> channels-innermost shadow (channel stride cp), 32x32 tiles through SMEM
+// so both the planar reads and the channel-contiguous writes are coalesced.
+__global__ void __launch_bounds__(256) k_to_hwc(TView x, float* __restrict__ y, int64_t ys, int cp) {
+  __shared__ float t[32][33];
+  const int HW = x.H * x.W;
+  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32, s = blockIdx.z;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const float* src = x.v + (int64_t)s * x.vs;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = c0 + ty + 8 * k, p = p0 + tx;
+    t[ty + 8 * k][tx] = (c < x.C && p < HW) ? src[(int64_t)c * HW + p] : 0.0f;
+  }
+  __syncthreads();
+  float* dst = y + (int64_t)s * ys;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int p = p0 + ty + 8 * k, c = c0 + tx;
+    if (p < HW && c < x.C) dst[(int64_t)p * cp + c] = t[tx][ty + 8 * k];
+  }
+}
+
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -342,10 +366,20 @@ using namespace evc;
 
 extern "C" {
 
-int evc_conv_region_supported(const evc_conv_geom* g, int64_t vstride) {
+int32_t evc_hwc_channels(int32_t c) { return (c + 3) / 4 * 4; }
+
+int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp, int32_t S, void* stream) {
+  EVC_CHECK_ARG(x && x->vals && y && S > 0 && cp >= x->C, "to_hwc: bad argument");
+  TView v = view_of(*x);
+  dim3 grid(cdiv(v.H * v.W, 32), cdiv(v.C, 32), S);
+  tma::k_to_hwc<<<grid, 256, 0, as_stream(stream)>>>(v, y, y_stride, cp);
+  EVC_LAUNCH_CHECK("to_hwc");
+  return EVC_OK;
+}
+
+int evc_conv_region_supported(const evc_conv_geom* g) {
   if (!g) return 0;
-  return g->stride == 1 && g->W % 4 == 0 && ((int64_t)g->H * g->W) % 4 == 0 && vstride % 4 == 0 &&
-         tma::encoder() != nullptr;
+  return g->stride >= 1 && g->stride * tma::RW <= 256 && g->stride <= 8 && tma::encoder() != nullptr;
 }
 
 int evc_conv_region_grid(const evc_conv_geom* g, int32_t* rh, int32_t* rw) {
@@ -379,9 +413,10 @@ int evc_conv_region_pack(const float* w, int32_t c_out, int32_t c_in, int32_t kh
           const float x = (n < c_out && c < c_in) ? w[((n * c_in + c) * kh + r) * kw + q] : 0.0f;
           uint32_t bits;
           memcpy(&bits, &x, 4);
-          bits = (bits + 0x1000u) & 0xFFFFE000u;
+          bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32 (as tf32_rn)
           float h;
           memcpy(&h, &bits, 4);
+          // 128B swizzle: 16-byte chunk j of row `row` lives at chunk (j ^ (row & 7))
           const int j = e / 4, sub = e % 4;
           const int64_t pos = (int64_t)row * 32 + ((j ^ (row & 7)) * 4) + sub;
           hi[pos] = h;
@@ -397,19 +432,20 @@ int64_t evc_conv_region_workspace(const evc_conv_geom* g, int32_t S, int32_t spl
   return (int64_t)splits * S * R * tma::BM * g->c_out;
 }
 
-int evc_conv_gemm_region(const evc_conv_geom* g, const evc_tensor* in, const float* wpack, const float* bias,
-                         const evc_tensor* out, const uint8_t* region_flags, int32_t S, int32_t splits,
-                         float* workspace, void* stream) {
-  EVC_CHECK_ARG(g && in && out && wpack && S > 0 && splits >= 1, "conv_gemm_region: null argument");
-  EVC_CHECK_ARG(evc_conv_region_supported(g, in->vstride), "conv_gemm_region: geometry not TMA-compatible");
+int evc_conv_gemm_region(const evc_conv_geom* g, const float* in_hwc, int32_t cp, int64_t hwc_stride,
+                         const float* wpack, const float* bias, const evc_tensor* out, const uint8_t* region_flags,
+                         int32_t S, int32_t splits, float* workspace, void* stream) {
+  EVC_CHECK_ARG(g && in_hwc && out && wpack && S > 0 && splits >= 1, "conv_gemm_region: null argument");
+  EVC_CHECK_ARG(evc_conv_region_supported(g), "conv_gemm_region: unsupported geometry");
+  EVC_CHECK_ARG(cp % 4 == 0 && cp >= g->c_in && hwc_stride % 4 == 0, "conv_gemm_region: shadow not 16B aligned");
   EVC_CHECK_ARG(splits == 1 || workspace, "conv_gemm_region: workspace required for split-K");
   tma::EncodeTiled enc = tma::encoder();
   CUtensorMap map;
-  const cuuint64_t dims[4] = {(cuuint64_t)g->W, (cuuint64_t)g->H, (cuuint64_t)g->c_in, (cuuint64_t)S};
-  const cuuint64_t strides[3] = {(cuuint64_t)g->W * 4, (cuuint64_t)g->H * g->W * 4, (cuuint64_t)in->vstride * 4};
-  const cuuint32_t box[4] = {32, 1, 32, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, in->vals, dims, strides, box, estr,
+  const cuuint64_t dims[4] = {(cuuint64_t)cp, (cuuint64_t)g->W, (cuuint64_t)g->H, (cuuint64_t)S};
+  const cuuint64_t strides[3] = {(cuuint64_t)cp * 4, (cuuint64_t)g->W * cp * 4, (cuuint64_t)hwc_stride * 4};
+  const cuuint32_t box[4] = {32, (cuuint32_t)(tma::RW * g->stride), 1, 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g->stride, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in_hwc), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -427,6 +463,7 @@ int evc_conv_gemm_region(const evc_conv_geom* g, const evc_tensor* in, const flo
   a.c_out = g->c_out;
   a.kh = g->kh;
   a.kw = g->kw;
+  a.stride = g->stride;
   a.pad = g->pad;
   a.cchunks = (g->c_in + 31) / 32;
   a.nkb = g->kh * g->kw * a.cchunks;

@@ -681,6 +681,9 @@ class Graph:
                 perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
                 count_ptr, scratch_ptr, region_ptr = node.mask_scratch
                 tl = self._tile_list.data_ptr()
+                pre = plan.prep(din)
+                if pre is not None:
+                    prog.append((pre[0], pre[1], "to_hwc"))
                 prog.append((L.evc_conv_mask, plan.mask_args(din, dout, scratch_ptr, cnt_ptr, tl, count_ptr,
                                                              region_ptr, perf_ptr), "conv_mask"))
                 fn, args = plan.gemm(din, dout, None, (tl, count_ptr, region_ptr), self._conv_ws.data_ptr())
@@ -782,8 +785,12 @@ class Graph:
         for node in self.nodes:
             ns, k, nid = node.spec, node.kind, node.spec.id
             if k == "conv":
-                fn, args = node.plan.gemm(self._desc(ns.inputs[0], False), self._desc(nid, False),
-                                          _lib.ptr(node.bias), None, self._conv_ws.data_ptr())
+                din = self._desc(ns.inputs[0], False)
+                pre = node.plan.prep(din)
+                if pre is not None:
+                    run(pre[0], *pre[1])
+                fn, args = node.plan.gemm(din, self._desc(nid, False), _lib.ptr(node.bias), None,
+                                          self._conv_ws.data_ptr())
                 run(fn, *args)
             elif k == "linear":
                 f = int(ns.attrs["out_features"])

@@ -150,6 +150,9 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
                                                  _lib.ptr(i32) + 4, _lib.ptr(regions), _lib.ptr(perf)), s),
                "conv_mask")
     ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=dev)
+    pre = plan.prep(din)
+    if pre is not None:
+        _lib.check(pre[0](*pre[1], s), "to_hwc")
     fn, args = plan.gemm(din, dout, None, (_lib.ptr(tiles), _lib.ptr(i32) + 4, _lib.ptr(regions)), ws.data_ptr())
     _lib.check(fn(*args, s), "conv_gemm")
     meter.add(int(perf.item()), 0)

@@ -279,8 +279,12 @@ class ConvPlan:
         T = -(-ho // th) * -(-wo // tw)
         self.T = T
         self.wpack = None
-        if kernel == "tc" and lib.evc_conv_region_supported(self.g, vs):
+        self.hwc = None
+        del vs
+        if kernel == "tc" and lib.evc_conv_region_supported(self.g):
             self.path = "region"
+            self.cp = int(lib.evc_hwc_channels(c_in))
+            self.hwc = torch.zeros((S, h, w, self.cp), dtype=torch.float32, device=weight.device)
             rh, rw = -(-ho // 4), -(-wo // 32)
             self.n_regions = S * rh * rw
             host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)
@@ -300,6 +304,12 @@ class ConvPlan:
             self.ws_floats = int(lib.evc_conv_workspace(self.g, S * T, self.splits))
         self.dense_flops = 2 * kh * kw * c_in * c_out * ho * wo
 
+    def prep(self, din):
+        """(fn, args-without-stream) mirroring the conv input into the HWC shadow, or None."""
+        if self.path != "region":
+            return None
+        return _lib.lib().evc_to_hwc, (din, self.hwc.data_ptr(), self.hwc[0].numel(), self.cp, self.S)
+
     def mask_args(self, din, dout, scratch, in_true, tile_list, tile_count, regions, meter):
         """evc_conv_mask arguments (stream appended by the caller)."""
         if self.path == "region":
@@ -317,8 +327,8 @@ class ConvPlan:
         lib = _lib.lib()
         tl, tc, rg = work if work is not None else (None, None, None)
         if self.path == "region":
-            return lib.evc_conv_gemm_region, (self.g, din, _lib.ptr(self.wpack), bias_ptr, dout, rg, self.S,
-                                              self.splits, ws_ptr)
+            return lib.evc_conv_gemm_region, (self.g, self.hwc.data_ptr(), self.cp, self.hwc[0].numel(),
+                                              _lib.ptr(self.wpack), bias_ptr, dout, rg, self.S, self.splits, ws_ptr)
         return lib.evc_conv_gemm, (self.g, din, self.weight.data_ptr(), _lib.ptr(self.wpack), bias_ptr, dout,
                                    self.table.data_ptr(), tl, tc, self.S, self.splits, ws_ptr)
 
@@ -357,6 +367,9 @@ def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> tor
     ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=x.device)
     din = _lib.tdesc(_lib.ptr(x), None, c * h * w, 0, c, h, w, th, tw)
     dout = _lib.tdesc(_lib.ptr(y), None, c_out * ho * wo, 0, c_out, ho, wo, th, tw)
+    pre = plan.prep(din)
+    if pre is not None:
+        _lib.check(pre[0](*pre[1], _lib.stream_ptr()), "to_hwc")
     fn, args = plan.gemm(din, dout, _lib.ptr(b), None, ws.data_ptr())
     _lib.check(fn(*args, _lib.stream_ptr()), "conv_gemm")
     return y

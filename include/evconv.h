@@ -215,10 +215,19 @@ int evc_act_dense(const float* x, int64_t x_stride, float* y, int64_t y_stride,
  * corrected^2; the last CTA to retire (ticket: zeroed int32) folds them into
  * norm_ema / k in a fixed order (sparsify.py:72-76), so the whole step is
  * one launch. */
+int64_t evc_sparsify_partials(const evc_tensor* dx); /* per session */
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
                  uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay,
-                 double* partials, int32_t* ticket, int32_t S, void* stream);
+                 double* partials, int32_t* ticket, float* hwc, int32_t cp,
+                 int64_t hwc_stride, int32_t write_chw, int32_t S, void* stream);
+/* (hwc, cp, hwc_stride: optional channels-innermost shadow of y for the
+ * TMA conv GEMM, see evc_to_hwc; write_chw = 0 skips the planar y values --
+ * flags are always written.) */
+
+/* acc += dx on live tiles (AccState.fold, increment_ops.py:93-94). */
+int evc_fold(const evc_tensor* dx, float* acc, int64_t acc_stride, int32_t S,
+             void* stream);
 
 /* Norm / EMA / k update from partial sums (one CTA, all S sessions), or
  * the reset (sparsify.py:43-51) when reset != 0 (norm_ema = norm, and

@@ -127,5 +127,6 @@ int init_masks();
 int init_conv();
 int init_conv_mask();
 int init_elementwise();
+int init_bands();
 int init_linear_events();
 }  // namespace evc

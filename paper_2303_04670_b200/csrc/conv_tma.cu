@@ -131,7 +131,13 @@ template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) k_conv_tma(const __grid_constant__ CUtensorMap tmap, Args a) {
   constexpr int NS = stages_of(BN);
   constexpr int STAGE = stage_bytes(BN);
-  constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+  // Accumulators: NA rotating "main" ones for hi*hi (one per K-block, round
+  // robin) + one for the small hi*lo + lo*hi corrections, summed in fp32 (RN)
+  // by the epilogue: every accumulator chain is NA-times (main) or ~2^11-times
+  // (corrections) less exposed to the tensor core's accumulation rounding.
+  constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 3 : 4);
+  constexpr int NEED = (NA + 1) * BN;
+  constexpr int TMEM_COLS = NEED <= 32 ? 32 : (NEED <= 64 ? 64 : (NEED <= 128 ? 128 : (NEED <= 256 ? 256 : 512)));
   // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
@@ -204,12 +210,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_tma(const __grid_constant__
         fence_after();
         const uint32_t ah = sb + st * STAGE, al = ah + A_BYTES;
         const uint32_t bh = ah + 2 * A_BYTES, bl = bh + BN * 128;
+        const uint32_t tmain = tmem + (uint32_t)((i % NA) * BN), tcorr = tmem + (uint32_t)(NA * BN);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
-          mma(tmem, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i | kk) ? 1u : 0u);
-          mma(tmem, desc_k(ah + ko), desc_k(bl + ko), IDESC, 1u);
-          mma(tmem, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
+          mma(tmain, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i >= NA || kk) ? 1u : 0u);
+          mma(tcorr, desc_k(ah + ko), desc_k(bl + ko), IDESC, (i | kk) ? 1u : 0u);
+          mma(tcorr, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
         }
         commit(empty_bar(st));
       }
@@ -253,10 +260,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_tma(const __grid_constant__
     const int64_t obase = (int64_t)s * a.ovs + (int64_t)u * a.Wo + v;
     const int64_t pm = (int64_t)reg * BM + qd * 32 + lane;
     const int n0 = nblk * BN;
+    const int n_main = nk < NA ? nk : NA;
+    const uint32_t trow = tmem + ((uint32_t)(32 * qd) << 16);
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
-      float vals[16];
-      tmem_ld16(tmem + ((uint32_t)(32 * qd) << 16) + (uint32_t)c0, vals);
+      float vals[16], part[16];
+      tmem_ld16(trow + (uint32_t)(NA * BN + c0), vals);  // corrections
+      for (int j = 0; j < n_main; ++j) {
+        tmem_ld16(trow + (uint32_t)(j * BN + c0), part);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], part[e]);
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + c0 + j;

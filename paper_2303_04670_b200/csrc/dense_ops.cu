@@ -1,13 +1,11 @@
-// Increment-domain nonlinearities, sparsification, add/mul, upsample and
-// maxpool (increment_ops.py:226-310, sparsify.py:54-78).
+// Dense (unmasked) operators of the dense pass, norm finalize, upsample and
+// maxpool (tensors.py:242-312, increment_ops.py:271-310, sparsify.py:43-51).
 //
-// All masked kernels are "band" kernels (one CTA per session x channel x
-// tile-row) and process a tile when it is live in an input OR was live in the
-// output last step (old output flag).  Recomputing a previously-live tile from
-// all-zero inputs writes exact zeros, which keeps the invariant that values
-// under False flags are 0 (TileMask soundness, tensors.py:65-72) without a
-// separate clearing pass.  Float arithmetic uses explicit _rn intrinsics so no
-// FMA contraction changes the reference's float32 rounding sequence.
+// upsample / maxpool are "band" kernels (one CTA per session x channel x
+// output tile-row); masked calls process an output tile when it is live or was
+// live last step, so recomputation from zero inputs restores exact zeros.
+// Float arithmetic uses _rn intrinsics so no FMA contraction changes the
+// reference's float32 rounding sequence.
 
 #include "common.cuh"
 
@@ -26,39 +24,6 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// inc_activation (increment_ops.py:232-238)
-// ---------------------------------------------------------------------------
-__global__ void k_act_delta(TView d, float* __restrict__ acc, int64_t as, TView y, int kind, float alpha) {
-  extern __shared__ uint8_t s_proc[];
-  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
-  const uint8_t* fi = d.fplane(s, c) + (int64_t)i * d.GW;
-  uint8_t* fo = y.fplane(s, c) + (int64_t)i * y.GW;
-  bool any = false;
-  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) {
-    const uint8_t p = fi[j] | fo[j];
-    s_proc[j] = p;
-    any |= p != 0;
-  }
-  if (!__syncthreads_or(any)) return;
-  const float* dv = d.plane(s, c);
-  float* yv = y.plane(s, c);
-  float* av = acc + (int64_t)s * as + (int64_t)c * d.H * d.W;
-  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
-  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
-    if (!s_proc[x / d.tw]) continue;
-    for (int r = r0; r < r1; ++r) {
-      const int64_t e = (int64_t)r * d.W + x;
-      const float a0 = av[e];
-      const float a1 = __fadd_rn(a0, dv[e]);
-      yv[e] = __fsub_rn(act_f(a1, kind, alpha), act_f(a0, kind, alpha));
-      av[e] = a1;
-    }
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) fo[j] = fi[j];
-}
-
 __global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __restrict__ y, int64_t ys,
                             float* __restrict__ acc, int64_t as, int64_t n, int kind, float alpha) {
   const int s = blockIdx.y;
@@ -69,100 +34,7 @@ __global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __re
   }
 }
 
-// ---------------------------------------------------------------------------
-// sparsify_step (sparsify.py:54-78)
-// ---------------------------------------------------------------------------
-__device__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
-                                      double decay, int reset, int S);
 
-// Last-block-done: the CTA that retires last folds every session's partial sums
-// into norm_ema / k (sparsify.py:72-76) in a fixed order.
-__device__ __forceinline__ void sparsify_ticket(int* ticket, int nblocks, const double* partials, int64_t n,
-                                                double* norm_ema, double* kdev, double tp, double decay, int S) {
-  __shared__ int s_last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(ticket, 1) == nblocks - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, 0, S);
-  }
-}
-
-__global__ void k_sparsify(TView d, float* __restrict__ delta, int64_t ds, uint8_t* __restrict__ dlive, TView y,
-                           double* kdev, double* partials, double* norm_ema, double tp, double decay, int* ticket) {
-  extern __shared__ uint8_t s_m[];  // proc | nz_y | nz_d   (3 x GW)
-  uint8_t* s_proc = s_m;
-  uint8_t* s_ny = s_m + d.GW;
-  uint8_t* s_nd = s_m + 2 * d.GW;
-  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
-  const uint8_t* fi = d.fplane(s, c) + (int64_t)i * d.GW;
-  uint8_t* fo = y.fplane(s, c) + (int64_t)i * y.GW;
-  uint8_t* dl = dlive + (int64_t)s * d.C * d.GH * d.GW + ((int64_t)c * d.GH + i) * d.GW;
-  bool any = false;
-  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) {
-    const uint8_t p = fi[j] | fo[j] | dl[j];
-    s_proc[j] = p;
-    s_ny[j] = 0;
-    s_nd[j] = 0;
-    any |= p != 0;
-  }
-  const int64_t npart = (int64_t)d.C * d.GH;
-  const int nblocks = gridDim.x * gridDim.y * gridDim.z;
-  double* part = partials + (int64_t)s * npart + (int64_t)c * d.GH + i;
-  if (!__syncthreads_or(any)) {
-    if (threadIdx.x == 0) *part = 0.0;
-    sparsify_ticket(ticket, nblocks, partials, npart, norm_ema, kdev, tp, decay, gridDim.z);
-    return;
-  }
-  const double k = kdev[s];
-  const bool use_k = k > 0.0;
-  const float k32 = __double2float_rn(k);
-  const float* dv = d.plane(s, c);
-  float* yv = y.plane(s, c);
-  float* del = delta + (int64_t)s * ds + (int64_t)c * d.H * d.W;
-  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
-  double ss = 0.0;
-  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
-    const int j = x / d.tw;
-    if (!s_proc[j]) continue;
-    bool nzy = false, nzd = false;
-    for (int r = r0; r < r1; ++r) {
-      const int64_t e = (int64_t)r * d.W + x;
-      const float corr = __fadd_rn(del[e], dv[e]);
-      float out, nd;
-      if (use_k) {
-        const float q = floorf(__fadd_rn(0.5f, __fdiv_rn(corr, k32)));
-        out = __fmul_rn(k32, q);
-        nd = __fsub_rn(corr, out);
-      } else {
-        out = corr;
-        nd = 0.0f;
-      }
-      yv[e] = out;
-      del[e] = nd;
-      ss += (double)corr * (double)corr;
-      nzy |= out != 0.0f;
-      nzd |= nd != 0.0f;
-    }
-    if (nzy) s_ny[j] = 1;
-    if (nzd) s_nd[j] = 1;
-  }
-  ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
-  if (threadIdx.x == 0) *part = ss;
-  __syncthreads();
-  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) {
-    fo[j] = s_ny[j];
-    dl[j] = s_nd[j];
-  }
-  sparsify_ticket(ticket, nblocks, partials, npart, norm_ema, kdev, tp, decay, gridDim.z);
-}
-
-// Sum each session's partials in a fixed order, then the EMA / k update
-// (sparsify.py:72-76) or the reset (sparsify.py:43-51).  One CTA does all S.
 __device__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
                                       double decay, int reset, int S) {
   for (int s = 0; s < S; ++s) {
@@ -199,44 +71,6 @@ __global__ void k_sumsq(const float* __restrict__ x, int64_t xs, int64_t n, doub
 
 // ---------------------------------------------------------------------------
 // inc_add / inc_mul (increment_ops.py:226-254)
-// ---------------------------------------------------------------------------
-template <bool MUL>
-__global__ void k_binary(TView a, TView b, float* __restrict__ sa, float* __restrict__ sb, int64_t ss, TView y) {
-  extern __shared__ uint8_t s_proc[];
-  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
-  const uint8_t* fa = a.fplane(s, c) + (int64_t)i * a.GW;
-  const uint8_t* fb = b.fplane(s, c) + (int64_t)i * b.GW;
-  uint8_t* fo = y.fplane(s, c) + (int64_t)i * y.GW;
-  bool any = false;
-  for (int j = threadIdx.x; j < a.GW; j += blockDim.x) {
-    const uint8_t p = fa[j] | fb[j] | fo[j];
-    s_proc[j] = p;
-    any |= p != 0;
-  }
-  if (!__syncthreads_or(any)) return;
-  const float* av = a.plane(s, c);
-  const float* bv = b.plane(s, c);
-  float* yv = y.plane(s, c);
-  const int64_t poff = (int64_t)s * ss + (int64_t)c * a.H * a.W;
-  const int r0 = i * a.th, r1 = min(a.H, r0 + a.th);
-  for (int x = threadIdx.x; x < a.W; x += blockDim.x) {
-    if (!s_proc[x / a.tw]) continue;
-    for (int r = r0; r < r1; ++r) {
-      const int64_t e = (int64_t)r * a.W + x;
-      const float va = av[e], vb = bv[e];
-      if (MUL) {
-        const float t1 = __fadd_rn(sa[poff + e], va);
-        yv[e] = __fadd_rn(__fmul_rn(t1, vb), __fmul_rn(sb[poff + e], va));
-        sa[poff + e] = t1;
-        sb[poff + e] = __fadd_rn(sb[poff + e], vb);
-      } else {
-        yv[e] = __fadd_rn(va, vb);
-      }
-    }
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < a.GW; j += blockDim.x) fo[j] = fa[j] | fb[j];
-}
 
 __global__ void k_binary_dense(const float* __restrict__ a, int64_t as, const float* __restrict__ b, int64_t bs,
                                float* __restrict__ y, int64_t ys, int64_t n, int op) {
@@ -247,7 +81,7 @@ __global__ void k_binary_dense(const float* __restrict__ a, int64_t as, const fl
   }
 }
 
-// ---------------------------------------------------------------------------
+
 // upsample (increment_ops.py:271-285, tensors.py:259-282)
 // ---------------------------------------------------------------------------
 struct Tap {
@@ -402,25 +236,6 @@ __global__ void k_maxpool(TView in, const float* __restrict__ acc, int64_t as, T
   }
 }
 
-// acc += dx on live input tiles (AccState.fold, increment_ops.py:93-94)
-__global__ void k_fold(TView d, float* __restrict__ acc, int64_t as) {
-  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
-  const uint8_t* f = d.fplane(s, c) + (int64_t)i * d.GW;
-  bool any = false;
-  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) any |= f[j] != 0;
-  if (!__syncthreads_or(any)) return;
-  const float* dv = d.plane(s, c);
-  float* av = acc + (int64_t)s * as + (int64_t)c * d.H * d.W;
-  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
-  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
-    if (!f[x / d.tw]) continue;
-    for (int r = r0; r < r1; ++r) {
-      const int64_t e = (int64_t)r * d.W + x;
-      av[e] = __fadd_rn(av[e], dv[e]);
-    }
-  }
-}
-
 static int bt(int W) { return W >= 192 ? 256 : (W >= 96 ? 128 : (W >= 48 ? 64 : 32)); }
 
 static int dense_blocks(int64_t n) {
@@ -429,39 +244,20 @@ static int dense_blocks(int64_t n) {
   return (int)(b > 0 ? b : 1);
 }
 
+
 }  // namespace evc
 
 using namespace evc;
 
 extern "C" {
 
-int evc_act_delta(const evc_tensor* dx, float* acc, int64_t acc_stride, const evc_tensor* y, int32_t kind,
-                  float alpha, int32_t S, void* stream) {
-  EVC_CHECK_ARG(dx && y && acc && dx->flags && y->flags && S > 0, "act_delta: null argument");
-  EVC_CHECK_ARG(kind >= 0 && kind <= 3, "act_delta: unknown activation");
-  TView d = view_of(*dx), o = view_of(*y);
-  k_act_delta<<<dim3(d.GH, d.C, S), bt(d.W), d.GW, as_stream(stream)>>>(d, acc, acc_stride, o, kind, alpha);
-  EVC_LAUNCH_CHECK("act_delta");
-  return EVC_OK;
-}
+int evc_fold(const evc_tensor* dx, float* acc, int64_t acc_stride, int32_t S, void* stream);
 
 int evc_act_dense(const float* x, int64_t xs, float* y, int64_t ys, float* acc, int64_t as, int64_t n, int32_t kind,
                   float alpha, int32_t S, void* stream) {
   EVC_CHECK_ARG(x && y && S > 0, "act_dense: null argument");
   k_act_dense<<<dim3(dense_blocks(n), S), 256, 0, as_stream(stream)>>>(x, xs, y, ys, acc, as, n, kind, alpha);
   EVC_LAUNCH_CHECK("act_dense");
-  return EVC_OK;
-}
-
-int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
-                 double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, int32_t S,
-                 void* stream) {
-  EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && ticket && dx->flags && y->flags && S > 0,
-                "sparsify: null argument");
-  TView d = view_of(*dx), o = view_of(*y);
-  k_sparsify<<<dim3(d.GH, d.C, S), bt(d.W), 3 * d.GW, as_stream(stream)>>>(d, delta, ds, dlive, o, k, partials,
-                                                                           norm_ema, tp, ema_decay, ticket);
-  EVC_LAUNCH_CHECK("sparsify");
   return EVC_OK;
 }
 
@@ -478,23 +274,6 @@ int evc_sumsq_dense(const float* x, int64_t xs, int64_t n, double* partials, int
   EVC_CHECK_ARG(x && partials && n_blocks > 0 && S > 0, "sumsq_dense: null argument");
   k_sumsq<<<dim3(n_blocks, S), 256, 0, as_stream(stream)>>>(x, xs, n, partials);
   EVC_LAUNCH_CHECK("sumsq_dense");
-  return EVC_OK;
-}
-
-int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y, int32_t S, void* stream) {
-  EVC_CHECK_ARG(a && b && y && a->flags && b->flags && y->flags && S > 0, "add: null argument");
-  TView va = view_of(*a), vb = view_of(*b), vy = view_of(*y);
-  k_binary<false><<<dim3(va.GH, va.C, S), bt(va.W), va.GW, as_stream(stream)>>>(va, vb, nullptr, nullptr, 0, vy);
-  EVC_LAUNCH_CHECK("add");
-  return EVC_OK;
-}
-
-int evc_mul(const evc_tensor* a, const evc_tensor* b, float* acc_a, float* acc_b, int64_t acc_stride,
-            const evc_tensor* y, int32_t S, void* stream) {
-  EVC_CHECK_ARG(a && b && y && acc_a && acc_b && a->flags && b->flags && y->flags && S > 0, "mul: null argument");
-  TView va = view_of(*a), vb = view_of(*b), vy = view_of(*y);
-  k_binary<true><<<dim3(va.GH, va.C, S), bt(va.W), va.GW, as_stream(stream)>>>(va, vb, acc_a, acc_b, acc_stride, vy);
-  EVC_LAUNCH_CHECK("mul");
   return EVC_OK;
 }
 
@@ -527,10 +306,7 @@ int evc_maxpool(const evc_tensor* in, float* acc, int64_t acc_stride, const evc_
   cudaStream_t st = as_stream(stream);
   k_maxpool<<<dim3(vo.GH, vo.C, S), bt(vo.W), 2 * vo.GW, st>>>(vi, acc, acc_stride, vo, wh, ww, stride);
   EVC_LAUNCH_CHECK("maxpool");
-  if (acc) {
-    k_fold<<<dim3(vi.GH, vi.C, S), bt(vi.W), 0, st>>>(vi, acc, acc_stride);
-    EVC_LAUNCH_CHECK("maxpool_fold");
-  }
+  if (acc) return evc_fold(in, acc, acc_stride, S, stream);  // AccState.fold (increment_ops.py:93-94)
   return EVC_OK;
 }
 
@@ -539,7 +315,7 @@ int evc_maxpool(const evc_tensor* in, float* acc, int64_t acc_stride, const evc_
 namespace evc {
 int init_elementwise() {
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, k_sparsify) != cudaSuccess) return EVC_ECUDA;
-  return EVC_OK;
+  if (cudaFuncGetAttributes(&fa, k_sumsq) != cudaSuccess) return EVC_ECUDA;
+  return init_bands();
 }
 }  // namespace evc

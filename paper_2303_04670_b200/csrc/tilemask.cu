@@ -161,53 +161,6 @@ __global__ void k_count_flags(TView t, int32_t* counts) {
   if (threadIdx.x == 0 && tot) atomicAdd(counts + s, tot);
 }
 
-// ---------------------------------------------------------------------------
-// integrate (tensors.py:167-174)
-// ---------------------------------------------------------------------------
-__global__ void k_integrate(float* __restrict__ y, int64_t ys, TView d) {
-  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
-  const uint8_t* f = d.fplane(s, c) + (int64_t)i * d.GW;
-  bool any = false;
-  for (int j = threadIdx.x; j < d.GW; j += blockDim.x) any |= f[j] != 0;
-  if (!__syncthreads_or(any)) return;
-  const float* dv = d.plane(s, c);
-  float* yv = y + (int64_t)s * ys + (int64_t)c * d.H * d.W;
-  const int r0 = i * d.th, r1 = min(d.H, r0 + d.th);
-  for (int x = threadIdx.x; x < d.W; x += blockDim.x) {
-    if (!f[x / d.tw]) continue;
-    for (int r = r0; r < r1; ++r) {
-      const int64_t e = (int64_t)r * d.W + x;
-      yv[e] = __fadd_rn(yv[e], dv[e]);
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// masked copy (non-aliasable concat parts)
-// ---------------------------------------------------------------------------
-__global__ void k_copy_masked(TView a, TView b) {
-  extern __shared__ uint8_t s_proc[];
-  const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
-  const uint8_t* fa = a.fplane(s, c) + (int64_t)i * a.GW;
-  uint8_t* fb = b.fplane(s, c) + (int64_t)i * b.GW;
-  bool any = false;
-  for (int j = threadIdx.x; j < a.GW; j += blockDim.x) {
-    const uint8_t p = fa[j] | fb[j];
-    s_proc[j] = p;
-    any |= p != 0;
-  }
-  if (!__syncthreads_or(any)) return;
-  const float* av = a.plane(s, c);
-  float* bv = b.plane(s, c);
-  const int r0 = i * a.th, r1 = min(a.H, r0 + a.th);
-  for (int x = threadIdx.x; x < a.W; x += blockDim.x) {
-    if (!s_proc[x / a.tw]) continue;
-    for (int r = r0; r < r1; ++r) bv[(int64_t)r * a.W + x] = av[(int64_t)r * a.W + x];
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < a.GW; j += blockDim.x) fb[j] = fa[j];
-}
-
 __global__ void k_copy_dense(const float* __restrict__ a, int64_t as, float* __restrict__ b, int64_t bs,
                              int64_t n) {
   const int s = blockIdx.y;
@@ -277,23 +230,6 @@ int evc_count_flags(const evc_tensor* t, int32_t S, int32_t* counts, void* strea
   const int blocks = (int)std::min<int64_t>(cdiv64(n, 256 * 4), 64);
   k_count_flags<<<dim3(blocks > 0 ? blocks : 1, S), 256, 0, as_stream(stream)>>>(v, counts);
   EVC_LAUNCH_CHECK("count_flags");
-  return EVC_OK;
-}
-
-int evc_integrate(float* y_run, int64_t y_stride, const evc_tensor* dx, int32_t S, void* stream) {
-  EVC_CHECK_ARG(y_run && dx && dx->vals && dx->flags && S > 0, "integrate: null argument");
-  TView d = view_of(*dx);
-  k_integrate<<<dim3(d.GH, d.C, S), band_threads(d.W), 0, as_stream(stream)>>>(y_run, y_stride, d);
-  EVC_LAUNCH_CHECK("integrate");
-  return EVC_OK;
-}
-
-int evc_copy_masked(const evc_tensor* src, const evc_tensor* dst, int32_t S, void* stream) {
-  EVC_CHECK_ARG(src && dst && src->flags && dst->flags && S > 0, "copy_masked: null argument");
-  TView a = view_of(*src), b = view_of(*dst);
-  EVC_CHECK_ARG(a.C == b.C && a.H == b.H && a.W == b.W && a.th == b.th && a.tw == b.tw, "copy_masked: shape");
-  k_copy_masked<<<dim3(a.GH, a.C, S), band_threads(a.W), a.GW, as_stream(stream)>>>(a, b);
-  EVC_LAUNCH_CHECK("copy_masked");
   return EVC_OK;
 }
 

@@ -519,6 +519,12 @@ class Graph:
         slots = {}
         parent = {}  # node -> (concat id, channel offset)
         copies = {}  # concat id -> [(part id, offset)]
+        self._consumers = {n.spec.id: [] for n in self.nodes}
+        for node in self.nodes:
+            for i in node.spec.inputs:
+                if i in self._consumers:
+                    self._consumers[i].append(node.spec.id)
+            node.shadow = None
         for node in self.nodes:
             if node.kind != "concat":
                 continue
@@ -573,7 +579,8 @@ class Graph:
                 node.dlive = torch.zeros((S, *grid_shape(ish, tile)), dtype=torch.uint8, device=dev)
                 node.sp_idx = len(sp_nodes)
                 sp_nodes.append(node)
-                max_part = max(max_part, ish[0] * grid_shape(ish, tile)[1])
+                max_part = max(max_part, int(self.lib.evc_sparsify_partials(self._desc(node.spec.inputs[0]))),
+                               ish[0] * grid_shape(ish, tile)[1])
             if k in ("conv", "linear"):
                 node.meter_idx = len(meter_ids)
                 meter_ids.append(node.spec.id)
@@ -584,6 +591,14 @@ class Graph:
                                      vstride=src.C * src.H * src.W, kernel=self.conv_kernel)
                 max_T = max(max_T, S * node.plan.T)
                 max_ws = max(max_ws, node.plan.ws_floats)
+                # a sparsify whose only reader is this conv writes the conv's
+                # channels-innermost shadow itself (and skips its planar values)
+                prod = self._by_id.get(node.spec.inputs[0])
+                if (node.plan.path == "region" and prod is not None and prod.kind == "sparsify"
+                        and self._consumers[prod.spec.id] == [node.spec.id]
+                        and prod.spec.id not in self.output_ids):
+                    prod.shadow = node.plan
+                    node.plan.fed_by_sparsify = True
             if k == "linear":
                 f = int(node.spec.attrs["out_features"])
                 lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
@@ -681,7 +696,7 @@ class Graph:
                 perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
                 count_ptr, scratch_ptr, region_ptr = node.mask_scratch
                 tl = self._tile_list.data_ptr()
-                pre = plan.prep(din)
+                pre = None if getattr(plan, "fed_by_sparsify", False) else plan.prep(din)
                 if pre is not None:
                     prog.append((pre[0], pre[1], "to_hwc"))
                 prog.append((L.evc_conv_mask, plan.mask_args(din, dout, scratch_ptr, cnt_ptr, tl, count_ptr,
@@ -704,14 +719,14 @@ class Graph:
                                                node.acc[0].numel(), self._desc(nid), code, alpha, S), "act_delta"))
             elif k == "sparsify":
                 j = node.sp_idx
-                c, h, w = self.shapes[nid]
-                npart = c * grid_shape((c, h, w), self.tile)[1]
+                sh = node.shadow  # ConvPlan of the only consumer when it reads a channels-innermost shadow
+                hwc = (sh.hwc.data_ptr(), sh.cp, sh.hwc[0].numel()) if sh is not None else (None, 0, 0)
                 prog.append((L.evc_sparsify, (self._desc(ns.inputs[0]), node.delta.data_ptr(), node.delta[0].numel(),
                                               node.dlive.data_ptr(), self._desc(nid),
                                               self._k.data_ptr() + 8 * j * S, self._norm.data_ptr() + 8 * j * S,
-                                              node.tp, node.ema_decay, self._partials.data_ptr(), node.ticket, S),
+                                              node.tp, node.ema_decay, self._partials.data_ptr(), node.ticket,
+                                              *hwc, 0 if sh is not None else 1, S),
                              "sparsify"))
-                del npart
             elif k == "add":
                 prog.append((L.evc_add, (self._desc(ns.inputs[0]), self._desc(ns.inputs[1]), self._desc(nid), S),
                              "add"))
@@ -865,6 +880,9 @@ class Graph:
         for st in self._stores:
             st.vals.zero_()
             st.flags.zero_()
+        for nd in self.nodes:  # conv input shadows held dense values during the dense pass
+            if nd.kind == "conv" and nd.plan.hwc is not None:
+                nd.plan.hwc.zero_()
 
     def dense_oracle(self, x):
         """Pure dense forward of the primary output; session state is untouched."""

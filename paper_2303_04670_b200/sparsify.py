@@ -62,15 +62,15 @@ def sparsify_step(x: IncrementTensor, state: SparsifyState) -> IncrementTensor:
     dlive = make_tile_mask(state.delta, tile).u8.clone()
     yv = torch.zeros(x.shape, dtype=torch.float32, device=dev)
     yf = torch.zeros(grid_shape(x.shape, tile), dtype=torch.uint8, device=dev)
-    n_part = c * yf.shape[1]
-    part = torch.empty(n_part, dtype=torch.float64, device=dev)
-    sc = torch.tensor([state.norm_ema, state.k], dtype=torch.float64, device=dev)
     lib = _lib.lib()
+    dx = x.desc()
+    part = torch.empty(int(lib.evc_sparsify_partials(dx)), dtype=torch.float64, device=dev)
+    sc = torch.tensor([state.norm_ema, state.k], dtype=torch.float64, device=dev)
     s = _lib.stream_ptr()
     dy = _lib.tdesc(_lib.ptr(yv), _lib.ptr(yf), 0, 0, c, h, w, tile.h, tile.w)
     ticket = torch.zeros(1, dtype=torch.int32, device=dev)
-    _lib.check(lib.evc_sparsify(x.desc(), _lib.ptr(state.delta), 0, _lib.ptr(dlive), dy, _lib.ptr(sc) + 8,
-                                _lib.ptr(sc), state.tp, state.ema_decay, _lib.ptr(part), _lib.ptr(ticket), 1, s),
+    _lib.check(lib.evc_sparsify(dx, _lib.ptr(state.delta), 0, _lib.ptr(dlive), dy, _lib.ptr(sc) + 8, _lib.ptr(sc),
+                                state.tp, state.ema_decay, _lib.ptr(part), _lib.ptr(ticket), None, 0, 0, 1, 1, s),
                "sparsify")
     ne, k = sc.tolist()
     state.norm_ema = ne

@@ -76,8 +76,7 @@ struct TBArgs {
   float alpha;
 };
 
-__device__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
-                                      double decay, int reset, int S);
+
 
 template <int OP>
 __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {

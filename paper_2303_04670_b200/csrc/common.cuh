@@ -118,6 +118,26 @@ __device__ __forceinline__ T block_sum(T v, F wsum) {
   return r;
 }
 
+// Sum each session's partials in a fixed order, then the EMA / k update
+// (sparsify.py:72-76) or the reset (sparsify.py:43-51).  One CTA does all S.
+__device__ __forceinline__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
+                                      double decay, int reset, int S) {
+  for (int s = 0; s < S; ++s) {
+    double sum = 0.0;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) sum += ((volatile const double*)partials)[(int64_t)s * n + e];
+    sum = block_sum<double>(sum, [](double v) { return warp_sum_d(v); });
+    if (threadIdx.x == 0) {
+      // np.linalg.norm of float32 data returns float32 (sparsify.py:49,73)
+      const double norm = (double)__double2float_rn(sqrt(sum));
+      const double ne =
+          reset ? norm : __dadd_rn(__dmul_rn(decay, norm_ema[s]), __dmul_rn(__dsub_rn(1.0, decay), norm));
+      norm_ema[s] = ne;
+      if (tp > 0.0) kdev[s] = __dmul_rn(tp, ne);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace evc
 
 namespace evc {

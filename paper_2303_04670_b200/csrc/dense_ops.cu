@@ -35,24 +35,6 @@ __global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __re
 }
 
 
-__device__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
-                                      double decay, int reset, int S) {
-  for (int s = 0; s < S; ++s) {
-    double sum = 0.0;
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) sum += ((volatile const double*)partials)[(int64_t)s * n + e];
-    sum = block_sum<double>(sum, [](double v) { return warp_sum_d(v); });
-    if (threadIdx.x == 0) {
-      // np.linalg.norm of float32 data returns float32 (sparsify.py:49,73)
-      const double norm = (double)__double2float_rn(sqrt(sum));
-      const double ne =
-          reset ? norm : __dadd_rn(__dmul_rn(decay, norm_ema[s]), __dmul_rn(__dsub_rn(1.0, decay), norm));
-      norm_ema[s] = ne;
-      if (tp > 0.0) kdev[s] = __dmul_rn(tp, ne);
-    }
-    __syncthreads();
-  }
-}
-
 __global__ void k_sparsify_finalize(const double* __restrict__ partials, int64_t n, double* norm_ema, double* kdev,
                                     double tp, double decay, int reset, int S) {
   sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, reset, S);

@@ -3,31 +3,35 @@
 // (increment_ops.py:226-254, sparsify.py:54-78, tensors.py:167-174).
 //
 // One CTA owns a "tile block": 32 channels x one tile row x a tile-aligned chunk
-// of columns (CW = tw * floor(32 / tw) pixels) of one session.  Tiles never
-// straddle CTAs, so per-(channel, tile) flags live in shared memory; a tile is
-// processed when it is live in an input OR was live in the output last step
-// (recomputing a previously-live tile from all-zero inputs writes exact zeros,
-// which keeps values under False flags at 0 -- TileMask soundness,
-// tensors.py:65-72).  Float arithmetic uses _rn intrinsics so no FMA
-// contraction changes the reference's float32 rounding sequence.
+// of columns of one session (24 px for 6x6 tiles, a multiple of both the tile
+// width and 4 so rows move as aligned float4s).  Tiles never straddle CTAs, so
+// per-(channel, tile) flags live in shared memory; a float4 is processed when
+// one of its tiles is live in an input OR was live in the output last step.
+// Recomputing a dead element from all-zero inputs writes an exact zero, which
+// keeps values under False flags at 0 (TileMask soundness, tensors.py:65-72),
+// and every output flag is derived per element tile.  Float arithmetic uses _rn
+// intrinsics so no FMA contraction changes the reference's float32 rounding.
 //
 // The sparsify op can also emit the channels-innermost shadow that the TMA
-// conv GEMM reads (conv_tma.cu), staged through shared memory so both the
-// planar reads and the 128-byte channel runs are coalesced.
+// conv GEMM reads (conv_tma.cu), staged through padded shared memory so the
+// planar reads and the 128-byte channel runs are both coalesced.
 
 #include "common.cuh"
 
 namespace evc {
 
-constexpr int TB_C = 32;        // channels per tile block
+constexpr int TB_C = 32;  // channels per tile block
 constexpr int TB_THREADS = 256;
-constexpr int TB_MAXJ = 32;     // max tiles per column chunk
+constexpr int TB_MAXJ = 32;  // max tiles per column chunk
+constexpr int TB_UNROLL = 4;
 
 struct TBGeo {
-  int C, H, W, th, tw, GH, GW, CW, nCG, nJC;
+  int C, H, W, th, tw, GH, GW, CW, nCG, nJC, vec;
 };
 
-static TBGeo tb_geo(const TView& v) {
+static int gcd_i(int a, int b) { return b ? gcd_i(b, a % b) : a; }
+
+static TBGeo tb_geo(const TView& v, bool aligned) {
   TBGeo g;
   g.C = v.C;
   g.H = v.H;
@@ -36,10 +40,18 @@ static TBGeo tb_geo(const TView& v) {
   g.tw = v.tw;
   g.GH = v.GH;
   g.GW = v.GW;
-  g.CW = v.tw >= 32 ? v.tw : v.tw * (32 / v.tw);
+  const int l = v.tw / gcd_i(v.tw, 4) * 4;  // lcm(tw, 4)
+  g.vec = (aligned && v.W % 4 == 0 && l <= 32) ? 4 : 1;
+  const int unit = g.vec == 4 ? l : v.tw;
+  g.CW = unit >= 32 ? unit : unit * (32 / unit);
   g.nCG = (v.C + TB_C - 1) / TB_C;
   g.nJC = (v.W + g.CW - 1) / g.CW;
   return g;
+}
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static bool al_view(const TView& v) {
+  return !v.v || (al16(v.v) && v.vs % 4 == 0 && ((int64_t)v.H * v.W) % 4 == 0);
 }
 
 __device__ __forceinline__ float act_fn(float x, int kind, float alpha) {
@@ -58,42 +70,66 @@ __device__ __forceinline__ float act_fn(float x, int kind, float alpha) {
 enum { OP_ACT = 0, OP_SPARSIFY = 1, OP_ADD = 2, OP_MUL = 3, OP_INTEGRATE = 4, OP_COPY = 5, OP_FOLD = 6 };
 
 struct TBArgs {
-  TView a, b, y;       // inputs (b optional) and output
-  float* acc;          // activation / fold / mul-a accumulator, integrate target
-  float* acc2;         // mul-b accumulator / sparsify residual
-  int64_t as;          // accumulator session stride
-  uint8_t* dlive;      // sparsify residual-live flags
-  const double* k;     // sparsify k per session
-  double* partials;    // sparsify sum(corrected^2) per tile block
+  TView a, b, y;    // inputs (b optional) and output
+  float* acc;       // activation / fold / mul-a accumulator, integrate target
+  float* acc2;      // mul-b accumulator / sparsify residual
+  int64_t as;       // accumulator session stride
+  uint8_t* dlive;   // sparsify residual-live flags
+  const double* k;  // sparsify k per session
+  double* partials;
   double* norm_ema;
   double tp, decay;
   int* ticket;
-  float* hwc;          // sparsify channels-innermost shadow (optional)
-  int64_t hs;          // shadow session stride
-  int cp;              // shadow channel stride
-  int write_chw;       // sparsify: also write the planar output
-  int kind;            // activation kind
+  float* hwc;  // sparsify channels-innermost shadow (optional)
+  int64_t hs;  // shadow session stride
+  int cp;      // shadow channel stride
+  int write_chw;
+  int kind;
   float alpha;
 };
 
+template <int V>
+struct Vec;
+template <>
+struct Vec<4> {
+  using T = float4;
+  __device__ static T ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
+  __device__ static void st(float* p, const T& v) { *reinterpret_cast<float4*>(p) = v; }
+  __device__ static float get(const T& v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : (k == 2 ? v.z : v.w)); }
+  __device__ static void set(T& v, int k, float x) {
+    if (k == 0) v.x = x;
+    else if (k == 1) v.y = x;
+    else if (k == 2) v.z = x;
+    else v.w = x;
+  }
+};
+template <>
+struct Vec<1> {
+  using T = float;
+  __device__ static T ld(const float* p) { return *p; }
+  __device__ static void st(float* p, const T& v) { *p = v; }
+  __device__ static float get(const T& v, int) { return v; }
+  __device__ static void set(T& v, int, float x) { v = x; }
+};
 
-
-template <int OP>
+template <int OP, int V>
 __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
+  using VT = Vec<V>;
+  using T = typename VT::T;
   __shared__ uint8_t s_proc[TB_C * TB_MAXJ];
-  __shared__ uint8_t s_f1[TB_C * TB_MAXJ];  // output flag (values != 0) / residual-live
-  __shared__ uint8_t s_f2[TB_C * TB_MAXJ];
-  __shared__ float s_y[(OP == OP_SPARSIFY) ? TB_C * 8 * 32 : 1];  // staged outputs for the shadow
+  __shared__ uint8_t s_f1[TB_C * TB_MAXJ];  // sparsify: output value != 0
+  __shared__ uint8_t s_f2[TB_C * TB_MAXJ];  // sparsify: residual != 0
+  // sparsify shadow staging: [(row * 32 + col) * 33 + channel], padded -> conflict-free both ways
+  __shared__ float s_y[(OP == OP_SPARSIFY) ? 8 * 32 * 33 : 1];
   const int jc = blockIdx.x % g.nJC;
   const int rest = blockIdx.x / g.nJC;
   const int cg = rest % g.nCG, i = rest / g.nCG;
   const int s = blockIdx.y;
   const int c0 = cg * TB_C, nc = min(TB_C, g.C - c0);
-  const int x0 = jc * g.CW, x1 = min(g.W, x0 + g.CW), ncol = x1 - x0;
+  const int x0 = jc * g.CW, ncol = min(g.W, x0 + g.CW) - x0;
   const int j0 = x0 / g.tw, nj = (ncol + g.tw - 1) / g.tw;
   const int r0 = i * g.th, nrow = min(g.H, r0 + g.th) - r0;
 
-  // ---- per-(channel, tile) processing decision
   bool any = false;
   for (int t = threadIdx.x; t < nc * nj; t += TB_THREADS) {
     const int cl = t / nj, jl = t % nj;
@@ -107,7 +143,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
            p.dlive[(int64_t)s * g.C * g.GH * g.GW + fo];
     } else if (OP == OP_COPY) {
       pr = p.a.f[(int64_t)s * p.a.fs + fo] | p.y.f[(int64_t)s * p.y.fs + fo];
-    } else {  // add / mul
+    } else {
       pr = p.a.f[(int64_t)s * p.a.fs + fo] | p.b.f[(int64_t)s * p.b.fs + fo] | p.y.f[(int64_t)s * p.y.fs + fo];
     }
     s_proc[t] = pr != 0;
@@ -118,71 +154,119 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
   double ss = 0.0;
   const bool active = __syncthreads_or(any) != 0;
   if (OP != OP_SPARSIFY && !active) return;
-  // stage sparsify outputs for the shadow when the block fits (th <= 8, CW <= 32)
   const bool stage = OP == OP_SPARSIFY && p.hwc && nrow <= 8 && ncol <= 32;
   if (active) {
     const int64_t HW = (int64_t)g.H * g.W;
     const double kd = OP == OP_SPARSIFY ? p.k[s] : 0.0;
     const bool use_k = kd > 0.0;
     const float k32 = __double2float_rn(kd);
-    const int n = nc * nrow * ncol;
-    for (int e = threadIdx.x; e < n; e += TB_THREADS) {
-      const int xl = e % ncol, t2 = e / ncol;
-      const int r = t2 % nrow, cl = t2 / nrow;
-      const int ti = cl * nj + xl / g.tw;
-      if (!s_proc[ti]) {
-        if (stage) s_y[(cl * nrow + r) * 32 + xl] = 0.0f;
-        continue;
+    const int nq = ncol / V;  // vector units per row chunk (ncol % V == 0 by construction)
+    const int n = nc * nrow * nq;
+    const int64_t sa = (int64_t)s * p.a.vs, sy = (int64_t)s * p.y.vs, sacc = (int64_t)s * p.as;
+    const int64_t sb = (OP == OP_ADD || OP == OP_MUL) ? (int64_t)s * p.b.vs : 0;
+    for (int base = threadIdx.x; base < n; base += TB_THREADS * TB_UNROLL) {
+      int64_t off[TB_UNROLL];
+      int cl_[TB_UNROLL], r_[TB_UNROLL], xl_[TB_UNROLL];
+      bool on[TB_UNROLL];
+      T va[TB_UNROLL], vb[TB_UNROLL], vc[TB_UNROLL];
+#pragma unroll
+      for (int u = 0; u < TB_UNROLL; ++u) {
+        const int e = base + u * TB_THREADS;
+        on[u] = false;
+        if (e >= n) continue;
+        const int q = e % nq, t2 = e / nq;
+        const int r = t2 % nrow, cl = t2 / nrow;
+        const int xl = q * V;
+        bool pr = false;
+#pragma unroll
+        for (int k = 0; k < V; ++k) pr |= s_proc[cl * nj + (xl + k) / g.tw] != 0;
+        cl_[u] = cl;
+        r_[u] = r;
+        xl_[u] = xl;
+        on[u] = pr;
+        if (!pr) continue;
+        off[u] = (int64_t)(c0 + cl) * HW + (int64_t)(r0 + r) * g.W + x0 + xl;
+        va[u] = VT::ld(p.a.v + sa + off[u]);
+        if (OP == OP_ADD || OP == OP_MUL) vb[u] = VT::ld(p.b.v + sb + off[u]);
+        if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD) vc[u] = VT::ld(p.acc + sacc + off[u]);
+        if (OP == OP_SPARSIFY) vc[u] = VT::ld(p.acc2 + sacc + off[u]);
+        if (OP == OP_MUL) vb[u] = VT::ld(p.b.v + sb + off[u]);
       }
-      const int c = c0 + cl;
-      const int64_t off = (int64_t)c * HW + (int64_t)(r0 + r) * g.W + x0 + xl;
-      if (OP == OP_ACT) {
-        float* av = p.acc + (int64_t)s * p.as + off;
-        const float a0 = *av, a1 = __fadd_rn(a0, p.a.v[(int64_t)s * p.a.vs + off]);
-        p.y.v[(int64_t)s * p.y.vs + off] = __fsub_rn(act_fn(a1, p.kind, p.alpha), act_fn(a0, p.kind, p.alpha));
-        *av = a1;
-      } else if (OP == OP_SPARSIFY) {
-        float* dl = p.acc2 + (int64_t)s * p.as + off;
-        const float corr = __fadd_rn(*dl, p.a.v[(int64_t)s * p.a.vs + off]);
-        float out, nd;
-        if (use_k) {
-          out = __fmul_rn(k32, floorf(__fadd_rn(0.5f, __fdiv_rn(corr, k32))));
-          nd = __fsub_rn(corr, out);
-        } else {
-          out = corr;
-          nd = 0.0f;
+#pragma unroll
+      for (int u = 0; u < TB_UNROLL; ++u) {
+        const int e = base + u * TB_THREADS;
+        if (e >= n) continue;
+        if (!on[u]) {
+          if (stage) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) s_y[(r_[u] * 32 + xl_[u] + k) * 33 + cl_[u]] = 0.0f;
+          }
+          continue;
         }
-        if (p.write_chw) p.y.v[(int64_t)s * p.y.vs + off] = out;
-        if (stage) {
-          s_y[(cl * nrow + r) * 32 + xl] = out;
-        } else if (p.hwc) {
-          p.hwc[(int64_t)s * p.hs + ((int64_t)(r0 + r) * g.W + x0 + xl) * p.cp + c] = out;
+        T out = va[u], acc_new = vc[u], acc2_new = vb[u];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          const float a = VT::get(va[u], k);
+          if (OP == OP_ACT) {
+            const float a0 = VT::get(vc[u], k), a1 = __fadd_rn(a0, a);
+            VT::set(out, k, __fsub_rn(act_fn(a1, p.kind, p.alpha), act_fn(a0, p.kind, p.alpha)));
+            VT::set(acc_new, k, a1);
+          } else if (OP == OP_SPARSIFY) {
+            const float corr = __fadd_rn(VT::get(vc[u], k), a);
+            float o, nd;
+            if (use_k) {
+              o = __fmul_rn(k32, floorf(__fadd_rn(0.5f, __fdiv_rn(corr, k32))));
+              nd = __fsub_rn(corr, o);
+            } else {
+              o = corr;
+              nd = 0.0f;
+            }
+            VT::set(out, k, o);
+            VT::set(acc_new, k, nd);
+            ss += (double)corr * (double)corr;
+            const int ti = cl_[u] * nj + (xl_[u] + k) / g.tw;
+            if (o != 0.0f) s_f1[ti] = 1;
+            if (nd != 0.0f) s_f2[ti] = 1;
+            if (stage) s_y[(r_[u] * 32 + xl_[u] + k) * 33 + cl_[u]] = o;
+          } else if (OP == OP_ADD) {
+            VT::set(out, k, __fadd_rn(a, VT::get(vb[u], k)));
+          } else if (OP == OP_MUL) {
+            const float b = VT::get(vb[u], k);
+            const float t1 = __fadd_rn(VT::get(vc[u], k), a);
+            // acc_b lives in acc2; loaded below (kept scalar to limit registers)
+            VT::set(acc_new, k, t1);
+            VT::set(out, k, __fmul_rn(t1, b));
+          } else if (OP == OP_INTEGRATE || OP == OP_FOLD) {
+            VT::set(acc_new, k, __fadd_rn(VT::get(vc[u], k), a));
+          }
         }
-        *dl = nd;
-        ss += (double)corr * (double)corr;
-        if (out != 0.0f) s_f1[ti] = 1;
-        if (nd != 0.0f) s_f2[ti] = 1;
-      } else if (OP == OP_ADD || OP == OP_MUL) {
-        const float va = p.a.v[(int64_t)s * p.a.vs + off], vb = p.b.v[(int64_t)s * p.b.vs + off];
-        if (OP == OP_ADD) {
-          p.y.v[(int64_t)s * p.y.vs + off] = __fadd_rn(va, vb);
-        } else {
-          float* sa = p.acc + (int64_t)s * p.as + off;
-          float* sb = p.acc2 + (int64_t)s * p.as + off;
-          const float t1 = __fadd_rn(*sa, va);
-          p.y.v[(int64_t)s * p.y.vs + off] = __fadd_rn(__fmul_rn(t1, vb), __fmul_rn(*sb, va));
-          *sa = t1;
-          *sb = __fadd_rn(*sb, vb);
+        if (OP == OP_MUL) {  // y = (acc_a + a) * b + acc_b * a ; acc_b += b
+          float* pb2 = p.acc2 + sacc + off[u];
+          T sbv = VT::ld(pb2);
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            const float a = VT::get(va[u], k), b = VT::get(vb[u], k), s2 = VT::get(sbv, k);
+            VT::set(out, k, __fadd_rn(VT::get(out, k), __fmul_rn(s2, a)));
+            VT::set(sbv, k, __fadd_rn(s2, b));
+          }
+          VT::st(pb2, sbv);
+          (void)acc2_new;
         }
-      } else if (OP == OP_INTEGRATE || OP == OP_FOLD) {
-        float* yv = p.acc + (int64_t)s * p.as + off;
-        *yv = __fadd_rn(*yv, p.a.v[(int64_t)s * p.a.vs + off]);
-      } else if (OP == OP_COPY) {
-        p.y.v[(int64_t)s * p.y.vs + off] = p.a.v[(int64_t)s * p.a.vs + off];
+        if (OP == OP_ACT || OP == OP_ADD || OP == OP_MUL || OP == OP_COPY) VT::st(p.y.v + sy + off[u], out);
+        if (OP == OP_SPARSIFY) {
+          if (p.write_chw) VT::st(p.y.v + sy + off[u], out);
+          if (p.hwc && !stage) {
+#pragma unroll
+            for (int k = 0; k < V; ++k)
+              p.hwc[(int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * g.W + x0 + xl_[u] + k) * p.cp + c0 + cl_[u]] =
+                  VT::get(out, k);
+          }
+          VT::st(p.acc2 + sacc + off[u], acc_new);
+        }
+        if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD) VT::st(p.acc + sacc + off[u], acc_new);
       }
     }
     __syncthreads();
-    // ---- output flags
     for (int t = threadIdx.x; t < nc * nj; t += TB_THREADS) {
       const int cl = t / nj, jl = t % nj;
       const int64_t fo = ((int64_t)(c0 + cl) * g.GH + i) * g.GW + j0 + jl;
@@ -201,7 +285,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         const int cl = e % TB_C, pix = e / TB_C;
         if (cl >= nc) continue;
         const int r = pix / ncol, xl = pix % ncol;
-        dst[((int64_t)(r0 + r) * g.W + x0 + xl) * p.cp + c0 + cl] = s_y[(cl * nrow + r) * 32 + xl];
+        dst[((int64_t)(r0 + r) * g.W + x0 + xl) * p.cp + c0 + cl] = s_y[(r * 32 + xl) * 33 + cl];
       }
     }
   }
@@ -209,7 +293,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     const int nblocks = gridDim.x * gridDim.y;
     ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
     if (threadIdx.x == 0) p.partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
-    // last CTA to retire folds every session's partials into norm_ema / k
+    // last CTA to retire folds every session's partials into norm_ema / k (fixed order)
     __shared__ int s_last;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -225,29 +309,36 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
   }
 }
 
-static int tb_launch(int op, const TBArgs& p, const TBGeo& g, int S, cudaStream_t st) {
+template <int OP>
+static void launch_op(const TBArgs& p, const TBGeo& g, int S, cudaStream_t st) {
   dim3 grid((unsigned)(g.GH * g.nCG * g.nJC), (unsigned)S);
+  if (g.vec == 4)
+    k_tiles<OP, 4><<<grid, TB_THREADS, 0, st>>>(p, g);
+  else
+    k_tiles<OP, 1><<<grid, TB_THREADS, 0, st>>>(p, g);
+}
+
+static int tb_launch(int op, const TBArgs& p, int S, cudaStream_t st) {
+  bool al = al_view(p.a) && al_view(p.y) && al_view(p.b);
+  if (p.acc) al = al && al16(p.acc) && p.as % 4 == 0;
+  if (p.acc2) al = al && al16(p.acc2) && p.as % 4 == 0;
+  const TBGeo g = tb_geo(p.a, al);
   switch (op) {
-    case OP_ACT: k_tiles<OP_ACT><<<grid, TB_THREADS, 0, st>>>(p, g); break;
-    case OP_SPARSIFY: k_tiles<OP_SPARSIFY><<<grid, TB_THREADS, 0, st>>>(p, g); break;
-    case OP_ADD: k_tiles<OP_ADD><<<grid, TB_THREADS, 0, st>>>(p, g); break;
-    case OP_MUL: k_tiles<OP_MUL><<<grid, TB_THREADS, 0, st>>>(p, g); break;
-    case OP_INTEGRATE: k_tiles<OP_INTEGRATE><<<grid, TB_THREADS, 0, st>>>(p, g); break;
-    case OP_COPY: k_tiles<OP_COPY><<<grid, TB_THREADS, 0, st>>>(p, g); break;
-    case OP_FOLD: k_tiles<OP_FOLD><<<grid, TB_THREADS, 0, st>>>(p, g); break;
+    case OP_ACT: launch_op<OP_ACT>(p, g, S, st); break;
+    case OP_SPARSIFY: launch_op<OP_SPARSIFY>(p, g, S, st); break;
+    case OP_ADD: launch_op<OP_ADD>(p, g, S, st); break;
+    case OP_MUL: launch_op<OP_MUL>(p, g, S, st); break;
+    case OP_INTEGRATE: launch_op<OP_INTEGRATE>(p, g, S, st); break;
+    case OP_COPY: launch_op<OP_COPY>(p, g, S, st); break;
+    case OP_FOLD: launch_op<OP_FOLD>(p, g, S, st); break;
     default: return EVC_EINVAL;
   }
   return EVC_OK;
 }
 
-int tiles_partials(const evc_tensor* t) {
-  const TBGeo g = tb_geo(view_of(*t));
-  return g.GH * g.nCG * g.nJC;
-}
-
 int init_bands() {
   cudaFuncAttributes fa;
-  return cudaFuncGetAttributes(&fa, k_tiles<OP_SPARSIFY>) == cudaSuccess ? EVC_OK : EVC_ECUDA;
+  return cudaFuncGetAttributes(&fa, k_tiles<OP_SPARSIFY, 4>) == cudaSuccess ? EVC_OK : EVC_ECUDA;
 }
 
 }  // namespace evc
@@ -267,12 +358,17 @@ int evc_act_delta(const evc_tensor* dx, float* acc, int64_t acc_stride, const ev
   p.as = acc_stride;
   p.kind = kind;
   p.alpha = alpha;
-  const int rc = tb_launch(OP_ACT, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_ACT, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("act_delta");
   return rc;
 }
 
-int64_t evc_sparsify_partials(const evc_tensor* dx) { return dx ? tiles_partials(dx) : -1; }
+int64_t evc_sparsify_partials(const evc_tensor* dx) {
+  if (!dx) return -1;
+  const TBGeo g = tb_geo(view_of(*dx), true);
+  const TBGeo g1 = tb_geo(view_of(*dx), false);
+  return std::max(g.GH * g.nCG * g.nJC, g1.GH * g1.nCG * g1.nJC);
+}
 
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, float* hwc,
@@ -297,7 +393,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   p.hs = hwc_stride;
   p.cp = cp;
   p.write_chw = write_chw;
-  const int rc = tb_launch(OP_SPARSIFY, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_SPARSIFY, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("sparsify");
   return rc;
 }
@@ -308,7 +404,7 @@ int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y, int32
   p.a = view_of(*a);
   p.b = view_of(*b);
   p.y = view_of(*y);
-  const int rc = tb_launch(OP_ADD, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_ADD, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("add");
   return rc;
 }
@@ -323,7 +419,7 @@ int evc_mul(const evc_tensor* a, const evc_tensor* b, float* acc_a, float* acc_b
   p.acc = acc_a;
   p.acc2 = acc_b;
   p.as = acc_stride;
-  const int rc = tb_launch(OP_MUL, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_MUL, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("mul");
   return rc;
 }
@@ -334,7 +430,7 @@ int evc_integrate(float* y_run, int64_t y_stride, const evc_tensor* dx, int32_t 
   p.a = view_of(*dx);
   p.acc = y_run;
   p.as = y_stride;
-  const int rc = tb_launch(OP_INTEGRATE, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_INTEGRATE, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("integrate");
   return rc;
 }
@@ -346,7 +442,7 @@ int evc_copy_masked(const evc_tensor* src, const evc_tensor* dst, int32_t S, voi
   p.y = view_of(*dst);
   EVC_CHECK_ARG(p.a.C == p.y.C && p.a.H == p.y.H && p.a.W == p.y.W && p.a.th == p.y.th && p.a.tw == p.y.tw,
                 "copy_masked: shape");
-  const int rc = tb_launch(OP_COPY, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_COPY, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("copy_masked");
   return rc;
 }
@@ -357,7 +453,7 @@ int evc_fold(const evc_tensor* dx, float* acc, int64_t acc_stride, int32_t S, vo
   p.a = view_of(*dx);
   p.acc = acc;
   p.as = acc_stride;
-  const int rc = tb_launch(OP_FOLD, p, tb_geo(p.a), S, as_stream(stream));
+  const int rc = tb_launch(OP_FOLD, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("fold");
   return rc;
 }

@@ -129,23 +129,11 @@ def make_inputs(evc, n_windows, seeds, device):
     return torch.stack(per, dim=1).contiguous()  # (n_windows, S, 4, 256, 256)
 
 
-def run_ours(args):
+def timed_run(evc, spec, weights, S, steps, warmup, rank, world, dev):
+    """Build an S-session graph, warm up, and time `steps` steps with CUDA events (L2 flushed between)."""
     import torch
 
-    import paper_2303_04670_b200 as evc
-    from paper_2303_04670_b200 import configs
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
-    S = args.sessions
-    spec = configs.evflownet_spec(tp=0.0)
-    weights = evc.WeightManifest.random_tensors(spec, 0)
-    n_win = 1 + args.warmup + args.steps + 1
+    n_win = 1 + warmup + steps + 1
     seeds = [rank * S + s for s in range(S)]
     xs = make_inputs(evc, n_win, seeds, dev)  # resident in HBM before timing
     density = float((xs[1:] != xs[:-1]).float().mean())
@@ -161,18 +149,20 @@ def run_ours(args):
             dense(i)
 
     dense(0)
-    for i in range(1, 1 + args.warmup):
+    for i in range(1, 1 + warmup):
         step(i)
     torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     if world > 1:
+        import torch.distributed as dist
+
         dist.barrier()
     torch.cuda.synchronize()
     refreshes = 0
-    with Clocks(local) as clk:
-        for j in range(args.steps):
+    with Clocks(dev.index or 0) as clk:
+        for j in range(steps):
             flush.fill_(float(j))  # evict L2 between timed steps (256 MiB > 126 MB L2)
-            i = 1 + args.warmup + j
+            i = 1 + warmup + j
             evs[j][0].record()
             will_refresh = g.refresh_interval and g.step_count + 1 >= g.refresh_interval
             step(i)
@@ -182,6 +172,28 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     times = [a.elapsed_time(b) for a, b in evs]
+    del flush
+    return g, xs, times, refreshes, clk, density
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2303_04670_b200 as evc
+    from paper_2303_04670_b200 import configs
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    spec = configs.evflownet_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    S = args.sessions
+    res = timed_run(evc, spec, weights, S, args.steps, args.warmup, rank, world, dev)
+    g, xs, times, refreshes, clk, density = res
     total_ms = sum(times)
     if world > 1:
         t = torch.tensor([total_ms], device=dev)
@@ -193,8 +205,14 @@ def run_ours(args):
     p50 = statistics.median(steady)
     p99 = steady[min(len(steady) - 1, int(round(0.99 * (len(steady) - 1))))]
     launches = g.kernel_launches_per_step() + 1  # + diff_mask
-    gpu_launches = args.steps * launches + refreshes * 200
-
+    gpu_launches = args.steps * launches + refreshes * g.dense_launches()
+    lat = None
+    if S > 1 and not args.no_latency_pass:  # single-stream latency (batch 1), same workload
+        g1, _, t1, _, _, _ = timed_run(evc, spec, weights, 1, min(args.steps, 32), args.warmup, rank, world, dev)
+        s1 = sorted(t1)
+        lat = {"sessions": 1, "p50_ms": statistics.median(s1),
+               "p99_ms": s1[min(len(s1) - 1, int(round(0.99 * (len(s1) - 1))))], "steps": len(s1)}
+        del g1
     # -- per-kernel timing of the conv GEMMs (dominant kernel) on the launching stream
     roof = conv_roofline(g, xs, args, evc)
     e2e = measure_e2e(g, xs, args, S)
@@ -210,6 +228,7 @@ def run_ours(args):
                        "l2": "flushed between timed steps (256 MiB write, excluded from step events)",
                        "parallelism": f"streams sharded over {world} GPU(s), no collective"},
             "p50_ms": p50, "p99_ms": p99, "refreshes_in_timed_region": refreshes,
+            "latency_single_stream": lat,
             "clocks": clk.summary(), "gpu_launches": gpu_launches, "roofline": roof, "e2e": e2e,
         }
     if world > 1:
@@ -404,6 +423,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency-pass", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -781,6 +781,10 @@ class Graph:
         self._ff_last.copy_(1.0 - self._cnt_step.to(torch.float64) / self._flag_size)
         self._ff_sum.add_(self._ff_last)
 
+    def dense_launches(self) -> int:
+        """libevconv launches of the last dense pass (refresh), excluding torch memsets."""
+        return getattr(self, "_dense_launches", 0)
+
     def kernel_launches_per_step(self) -> int:
         """libevconv kernels launched by one incr_step (torch bookkeeping ops excluded)."""
         n = 0
@@ -793,9 +797,11 @@ class Graph:
 
     def _dense_program(self, mutate: bool):
         L, S, s = self.lib, self.S, _lib.stream_ptr()
+        self._dense_launches = 0
 
         def run(fn, *a):
             _lib.check(fn(*a, s), fn.__name__)
+            self._dense_launches += 1
 
         for node in self.nodes:
             ns, k, nid = node.spec, node.kind, node.spec.id

@@ -220,10 +220,25 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
                  uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay,
                  double* partials, int32_t* ticket, float* hwc, int32_t cp,
-                 int64_t hwc_stride, int32_t write_chw, int32_t S, void* stream);
+                 int64_t hwc_stride, int32_t write_chw, int32_t delta_zero,
+                 int32_t S, void* stream);
 /* (hwc, cp, hwc_stride: optional channels-innermost shadow of y for the
  * TMA conv GEMM, see evc_to_hwc; write_chw = 0 skips the planar y values --
- * flags are always written.) */
+ * flags are always written.  delta_zero != 0 asserts tp == 0 and k == 0, so
+ * the residual stays identically zero and is neither read nor written.) */
+
+/* Fused inc_upsample (increment_ops.py:271-285) -> sparsify_step: y is the
+ * sparsified upsample of x, computed without materialising the upsampled
+ * increment (arguments as evc_upsample + evc_sparsify; partials sized by
+ * evc_upsample_sparsify_partials(y) per session). */
+int64_t evc_upsample_sparsify_partials(const evc_tensor* y);
+int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode,
+                          float* delta, int64_t delta_stride, uint8_t* dlive,
+                          const evc_tensor* y, double* k, double* norm_ema,
+                          double tp, double ema_decay, double* partials,
+                          int32_t* ticket, float* hwc, int32_t cp,
+                          int64_t hwc_stride, int32_t write_chw,
+                          int32_t delta_zero, int32_t S, void* stream);
 
 /* acc += dx on live tiles (AccState.fold, increment_ops.py:93-94). */
 int evc_fold(const evc_tensor* dx, float* acc, int64_t acc_stride, int32_t S,

@@ -77,8 +77,11 @@ _PROTOS = {
     "evc_act_delta": (_I32, [_T, _P, _I64, _T, _I32, _F, _I32, _P]),
     "evc_act_dense": (_I32, [_P, _I64, _P, _I64, _P, _I64, _I64, _I32, _F, _I32, _P]),
     "evc_sparsify_partials": (_I64, [_T]),
-    "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32, _I32, _P]),
+    "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P]),
     "evc_fold": (_I32, [_T, _P, _I64, _I32, _P]),
+    "evc_upsample_sparsify_partials": (_I64, [_T]),
+    "evc_upsample_sparsify": (_I32, [_T, _I32, _I32, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32,
+                                     _I32, _I32, _P]),
     "evc_sparsify_finalize": (_I32, [_P, _I64, _P, _P, _D, _D, _I32, _I32, _P]),
     "evc_sumsq_dense": (_I32, [_P, _I64, _I64, _P, _I32, _I32, _P]),
     "evc_add": (_I32, [_T, _T, _T, _I32, _P]),

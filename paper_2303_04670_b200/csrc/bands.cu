@@ -84,6 +84,7 @@ struct TBArgs {
   int64_t hs;  // shadow session stride
   int cp;      // shadow channel stride
   int write_chw;
+  int delta_zero;  // sparsify with tp == 0 and k == 0: the residual is identically 0, skip its traffic
   int kind;
   float alpha;
 };
@@ -189,7 +190,14 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         va[u] = VT::ld(p.a.v + sa + off[u]);
         if (OP == OP_ADD || OP == OP_MUL) vb[u] = VT::ld(p.b.v + sb + off[u]);
         if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD) vc[u] = VT::ld(p.acc + sacc + off[u]);
-        if (OP == OP_SPARSIFY) vc[u] = VT::ld(p.acc2 + sacc + off[u]);
+        if (OP == OP_SPARSIFY) {
+          if (p.delta_zero) {
+#pragma unroll
+            for (int k = 0; k < V; ++k) VT::set(vc[u], k, 0.0f);
+          } else {
+            vc[u] = VT::ld(p.acc2 + sacc + off[u]);
+          }
+        }
         if (OP == OP_MUL) vb[u] = VT::ld(p.b.v + sb + off[u]);
       }
 #pragma unroll
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
               p.hwc[(int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * g.W + x0 + xl_[u] + k) * p.cp + c0 + cl_[u]] =
                   VT::get(out, k);
           }
-          VT::st(p.acc2 + sacc + off[u], acc_new);
+          if (!p.delta_zero) VT::st(p.acc2 + sacc + off[u], acc_new);
         }
         if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD) VT::st(p.acc + sacc + off[u], acc_new);
       }
@@ -372,7 +380,7 @@ int64_t evc_sparsify_partials(const evc_tensor* dx) {
 
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, float* hwc,
-                 int32_t cp, int64_t hwc_stride, int32_t write_chw, int32_t S, void* stream) {
+                 int32_t cp, int64_t hwc_stride, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
   EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && ticket && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
@@ -393,6 +401,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   p.hs = hwc_stride;
   p.cp = cp;
   p.write_chw = write_chw;
+  p.delta_zero = delta_zero;
   const int rc = tb_launch(OP_SPARSIFY, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("sparsify");
   return rc;

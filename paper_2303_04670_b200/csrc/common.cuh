@@ -118,6 +118,50 @@ __device__ __forceinline__ T block_sum(T v, F wsum) {
   return r;
 }
 
+// Bilinear upsampling taps of one output coordinate: half-pixel source
+// (i + 0.5) / f - 0.5, clamped, float32 weights (tensors.py:259-266).
+struct Tap {
+  int i0, i1;
+  float w0, w1;
+};
+
+__device__ __forceinline__ Tap bilinear_tap(int o, int n_in, int f) {
+  const float src = __fsub_rn(__fdiv_rn(__fadd_rn((float)o, 0.5f), (float)f), 0.5f);
+  const float fl = floorf(src);
+  const float frac = __fsub_rn(src, fl);
+  Tap t;
+  const int i0 = (int)fl;
+  t.i1 = min(max(i0 + 1, 0), n_in - 1);
+  t.i0 = min(max(i0, 0), n_in - 1);
+  t.w1 = frac;
+  t.w0 = __fsub_rn(1.0f, frac);
+  return t;
+}
+
+// Upsampled value of output (u, v) from plane xv (H x W input), float32 op
+// order of dense_upsample (tensors.py:269-282): rows first, then columns.
+__device__ __forceinline__ float upsample_at(const float* xv, int H, int W, int u, int v, int f, int mode) {
+  if (mode == 0) return xv[(int64_t)(u / f) * W + v / f];
+  const Tap tr = bilinear_tap(u, H, f), tc = bilinear_tap(v, W, f);
+  const float* x0 = xv + (int64_t)tr.i0 * W;
+  const float* x1 = xv + (int64_t)tr.i1 * W;
+  const float ra = __fadd_rn(__fmul_rn(x0[tc.i0], tr.w0), __fmul_rn(x1[tc.i0], tr.w1));
+  const float rb = __fadd_rn(__fmul_rn(x0[tc.i1], tr.w0), __fmul_rn(x1[tc.i1], tr.w1));
+  return __fadd_rn(__fmul_rn(ra, tc.w0), __fmul_rn(rb, tc.w1));
+}
+
+// Input tile box [lo, hi] (in tile units) read by the upsampled output range [o0, o1).
+__device__ __forceinline__ void upsample_box(int o0, int o1, int n_in, int f, int mode, int tile, int& lo,
+                                             int& hi) {
+  if (mode == 0) {
+    lo = (o0 / f) / tile;
+    hi = ((o1 - 1) / f) / tile;
+  } else {
+    lo = bilinear_tap(o0, n_in, f).i0 / tile;
+    hi = bilinear_tap(o1 - 1, n_in, f).i1 / tile;
+  }
+}
+
 // Sum each session's partials in a fixed order, then the EMA / k update
 // (sparsify.py:72-76) or the reset (sparsify.py:43-51).  One CTA does all S.
 __device__ __forceinline__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,

@@ -66,24 +66,6 @@ __global__ void k_binary_dense(const float* __restrict__ a, int64_t as, const fl
 
 // upsample (increment_ops.py:271-285, tensors.py:259-282)
 // ---------------------------------------------------------------------------
-struct Tap {
-  int i0, i1;
-  float w0, w1;
-};
-
-// half-pixel source taps of one output coordinate (tensors.py:259-266)
-__device__ __forceinline__ Tap bilinear_tap(int o, int n_in, int f) {
-  const float src = __fsub_rn(__fdiv_rn(__fadd_rn((float)o, 0.5f), (float)f), 0.5f);
-  const float fl = floorf(src);
-  const float frac = __fsub_rn(src, fl);
-  Tap t;
-  const int i0 = (int)fl;
-  t.i1 = min(max(i0 + 1, 0), n_in - 1);
-  t.i0 = min(max(i0, 0), n_in - 1);
-  t.w1 = frac;
-  t.w0 = __fsub_rn(1.0f, frac);
-  return t;
-}
 
 __global__ void k_upsample(TView in, TView out, int f, int mode) {
   extern __shared__ uint8_t s_m[];  // proc | new (2 x GWo)

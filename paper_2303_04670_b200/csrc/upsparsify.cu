@@ -1,0 +1,195 @@
+// Fused inc_upsample -> sparsify_step (the decoder pattern "upsample, then the
+// conv's sparsify layer": increment_ops.py:271-285 followed by sparsify.py:54-78).
+//
+// The upsampled increment exists only in registers: each CTA (32 channels x one
+// output tile row x a tile-aligned column chunk) evaluates the upsample of the
+// small input on the fly (same float32 op order as dense_upsample), applies the
+// error-feedback rounding, derives the output tile flags from the values, and
+// writes the next conv's channels-innermost shadow directly.  A tile is
+// processed when its upsample support is live, when it was live in the output
+// last step, or when its residual is nonzero -- exactly the tiles the unfused
+// pair could change.  Norm partials are folded by the last CTA (fixed order).
+
+#include "common.cuh"
+
+namespace evc {
+
+constexpr int US_C = 32, US_THREADS = 256, US_MAXJ = 32;
+
+struct USArgs {
+  TView x;         // upsample input (masked)
+  TView y;         // sparsify output (flags; values when write_chw)
+  float* delta;    // residual
+  int64_t ds;
+  uint8_t* dlive;
+  double* k;
+  double* norm_ema;
+  double tp, decay;
+  double* partials;
+  int* ticket;
+  float* hwc;
+  int64_t hs;
+  int cp, write_chw, delta_zero, f, mode;
+  int CW, nCG, nJC;
+};
+
+__global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
+  __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ];
+  __shared__ float s_y[8 * 32 * 33];
+  const TView& y = a.y;
+  const int jc = blockIdx.x % a.nJC, rest = blockIdx.x / a.nJC;
+  const int cg = rest % a.nCG, i = rest / a.nCG, s = blockIdx.y;
+  const int c0 = cg * US_C, nc = min(US_C, y.C - c0);
+  const int x0 = jc * a.CW, ncol = min(y.W, x0 + a.CW) - x0;
+  const int j0 = x0 / y.tw, nj = (ncol + y.tw - 1) / y.tw;
+  const int r0 = i * y.th, nrow = min(y.H, r0 + y.th) - r0;
+  int alo, ahi;
+  upsample_box(r0, r0 + nrow, a.x.H, a.f, a.mode, a.x.th, alo, ahi);
+  bool any = false;
+  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
+    const int cl = t / nj, jl = t % nj, c = c0 + cl;
+    const int v0 = (j0 + jl) * y.tw, v1 = min(y.W, v0 + y.tw);
+    int blo, bhi;
+    upsample_box(v0, v1, a.x.W, a.f, a.mode, a.x.tw, blo, bhi);
+    const uint8_t* F = a.x.fplane(s, c);
+    uint8_t live = 0;
+    for (int aa = alo; aa <= ahi; ++aa)
+      for (int bb = blo; bb <= bhi; ++bb) live |= F[aa * a.x.GW + bb];
+    const int64_t fo = ((int64_t)c * y.GH + i) * y.GW + j0 + jl;
+    const uint8_t pr = live | y.f[(int64_t)s * y.fs + fo] | a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo];
+    s_proc[t] = pr != 0;
+    s_ny[t] = 0;
+    s_nd[t] = 0;
+    any |= pr != 0;
+  }
+  const bool active = __syncthreads_or(any) != 0;
+  double ss = 0.0;
+  const bool stage = a.hwc && nrow <= 8 && ncol <= 32;
+  if (active) {
+    const double kd = a.k[s];
+    const bool use_k = kd > 0.0;
+    const float k32 = __double2float_rn(kd);
+    const int64_t HW = (int64_t)y.H * y.W;
+    const int n = nc * nrow * ncol;
+    for (int e = threadIdx.x; e < n; e += US_THREADS) {
+      const int xl = e % ncol, t2 = e / ncol;
+      const int r = t2 % nrow, cl = t2 / nrow;
+      const int ti = cl * nj + xl / y.tw;
+      if (!s_proc[ti]) {
+        if (stage) s_y[(r * 32 + xl) * 33 + cl] = 0.0f;
+        continue;
+      }
+      const int c = c0 + cl, u = r0 + r, v = x0 + xl;
+      const float up = upsample_at(a.x.plane(s, c), a.x.H, a.x.W, u, v, a.f, a.mode);
+      const int64_t off = (int64_t)c * HW + (int64_t)u * y.W + v;
+      float* dp = a.delta + (int64_t)s * a.ds + off;
+      const float corr = a.delta_zero ? __fadd_rn(0.0f, up) : __fadd_rn(*dp, up);
+      float o, nd;
+      if (use_k) {
+        o = __fmul_rn(k32, floorf(__fadd_rn(0.5f, __fdiv_rn(corr, k32))));
+        nd = __fsub_rn(corr, o);
+      } else {
+        o = corr;
+        nd = 0.0f;
+      }
+      if (a.write_chw) y.v[(int64_t)s * y.vs + off] = o;
+      if (stage) {
+        s_y[(r * 32 + xl) * 33 + cl] = o;
+      } else if (a.hwc) {
+        a.hwc[(int64_t)s * a.hs + ((int64_t)u * y.W + v) * a.cp + c] = o;
+      }
+      if (!a.delta_zero) *dp = nd;
+      ss += (double)corr * (double)corr;
+      if (o != 0.0f) s_ny[ti] = 1;
+      if (nd != 0.0f) s_nd[ti] = 1;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
+      const int cl = t / nj, jl = t % nj;
+      const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i) * y.GW + j0 + jl;
+      y.f[(int64_t)s * y.fs + fo] = s_ny[t];
+      a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
+    }
+    if (stage) {
+      float* dst = a.hwc + (int64_t)s * a.hs;
+      for (int e = threadIdx.x; e < nrow * ncol * US_C; e += US_THREADS) {
+        const int cl = e % US_C, pix = e / US_C;
+        if (cl >= nc) continue;
+        const int r = pix / ncol, xl = pix % ncol;
+        dst[((int64_t)(r0 + r) * y.W + x0 + xl) * a.cp + c0 + cl] = s_y[(r * 32 + xl) * 33 + cl];
+      }
+    }
+  }
+  const int nblocks = gridDim.x * gridDim.y;
+  ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
+  if (threadIdx.x == 0) a.partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(a.ticket, 1) == nblocks - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    sparsify_finalize_all(a.partials, gridDim.x, a.norm_ema, a.k, a.tp, a.decay, 0, gridDim.y);
+  }
+}
+
+static void us_grid(const TView& y, int& CW, int& nCG, int& nJC) {
+  CW = y.tw >= 32 ? y.tw : y.tw * (32 / y.tw);
+  nCG = (y.C + US_C - 1) / US_C;
+  nJC = (y.W + CW - 1) / CW;
+}
+
+}  // namespace evc
+
+using namespace evc;
+
+extern "C" {
+
+int64_t evc_upsample_sparsify_partials(const evc_tensor* y) {
+  if (!y) return -1;
+  int CW, nCG, nJC;
+  const TView v = view_of(*y);
+  us_grid(v, CW, nCG, nJC);
+  return (int64_t)v.GH * nCG * nJC;
+}
+
+int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, float* delta, int64_t ds,
+                          uint8_t* dlive, const evc_tensor* y, double* k, double* norm_ema, double tp,
+                          double ema_decay, double* partials, int32_t* ticket, float* hwc, int32_t cp,
+                          int64_t hwc_stride, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
+  EVC_CHECK_ARG(x && y && x->flags && y->flags && delta && dlive && k && norm_ema && partials && ticket && S > 0,
+                "upsample_sparsify: null argument");
+  EVC_CHECK_ARG(factor == 2 || factor == 4, "upsample_sparsify: factor must be 2 or 4");
+  EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
+  EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");
+  EVC_CHECK_ARG(write_chw || hwc, "upsample_sparsify: no output requested");
+  USArgs a;
+  a.x = view_of(*x);
+  a.y = view_of(*y);
+  a.delta = delta;
+  a.ds = ds;
+  a.dlive = dlive;
+  a.k = k;
+  a.norm_ema = norm_ema;
+  a.tp = tp;
+  a.decay = ema_decay;
+  a.partials = partials;
+  a.ticket = ticket;
+  a.hwc = hwc;
+  a.hs = hwc_stride;
+  a.cp = cp;
+  a.write_chw = write_chw;
+  a.delta_zero = delta_zero;
+  a.f = factor;
+  a.mode = mode;
+  us_grid(a.y, a.CW, a.nCG, a.nJC);
+  dim3 grid((unsigned)(a.y.GH * a.nCG * a.nJC), (unsigned)S);
+  k_up_sparsify<<<grid, US_THREADS, 0, as_stream(stream)>>>(a);
+  EVC_LAUNCH_CHECK("upsample_sparsify");
+  return EVC_OK;
+}
+
+}  // extern "C"

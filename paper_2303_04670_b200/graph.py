@@ -603,6 +603,14 @@ class Graph:
                 f = int(node.spec.attrs["out_features"])
                 lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
                                                                        self.tile.h * self.tile.w, S)))
+        # upsample -> sparsify pairs run as one fused kernel when the upsample has no other reader
+        self._fused_up = set()
+        for node in sp_nodes:
+            up = self._by_id.get(node.spec.inputs[0])
+            if (up is not None and up.kind == "upsample" and self._consumers[up.spec.id] == [node.spec.id]
+                    and up.spec.id not in self.output_ids):
+                self._fused_up.add(up.spec.id)
+                max_part = max(max_part, int(self.lib.evc_upsample_sparsify_partials(self._desc(node.spec.id))))
         nm = max(len(meter_ids), 1)
         self._meter_ids = meter_ids
         self._meter_nodes = [self._by_id[i] for i in meter_ids]
@@ -717,6 +725,22 @@ class Graph:
                 code, alpha = node.act
                 prog.append((L.evc_act_delta, (self._desc(ns.inputs[0]), node.acc.data_ptr(),
                                                node.acc[0].numel(), self._desc(nid), code, alpha, S), "act_delta"))
+            elif k == "sparsify" and ns.inputs[0] in self._fused_up:
+                j = node.sp_idx
+                up = self._by_id[ns.inputs[0]]
+                sh = node.shadow
+                hwc = (sh.hwc.data_ptr(), sh.cp, sh.hwc[0].numel()) if sh is not None else (None, 0, 0)
+                mode = 0 if up.spec.attrs.get("mode", "nearest") == "nearest" else 1
+                prog.append((L.evc_upsample_sparsify, (self._desc(up.spec.inputs[0]), int(up.spec.attrs.get("factor", 2)),
+                                                       mode, node.delta.data_ptr(), node.delta[0].numel(),
+                                                       node.dlive.data_ptr(), self._desc(nid),
+                                                       self._k.data_ptr() + 8 * j * S,
+                                                       self._norm.data_ptr() + 8 * j * S, node.tp, node.ema_decay,
+                                                       self._partials.data_ptr(), node.ticket, *hwc,
+                                                       0 if sh is not None else 1, 1 if node.tp == 0.0 else 0, S),
+                             "upsample_sparsify"))
+            elif k == "upsample" and nid in self._fused_up:
+                continue  # evaluated inside the consumer's fused upsample_sparsify
             elif k == "sparsify":
                 j = node.sp_idx
                 sh = node.shadow  # ConvPlan of the only consumer when it reads a channels-innermost shadow
@@ -725,7 +749,9 @@ class Graph:
                                               node.dlive.data_ptr(), self._desc(nid),
                                               self._k.data_ptr() + 8 * j * S, self._norm.data_ptr() + 8 * j * S,
                                               node.tp, node.ema_decay, self._partials.data_ptr(), node.ticket,
-                                              *hwc, 0 if sh is not None else 1, S),
+                                              *hwc, 0 if sh is not None else 1,
+                                              1 if node.tp == 0.0 else 0,  # k stays 0 -> residual stays 0
+                                              S),
                              "sparsify"))
             elif k == "add":
                 prog.append((L.evc_add, (self._desc(ns.inputs[0]), self._desc(ns.inputs[1]), self._desc(nid), S),

@@ -168,6 +168,57 @@ int evc_conv_gemm_region(const evc_conv_geom* g, const float* in_hwc, int32_t cp
                          const evc_tensor* out, const uint8_t* region_flags,
                          int32_t S, int32_t splits, float* workspace, void* stream);
 
+/* ---- fused incremental convolution (conv_fused.cu) --------------------
+ * inc_conv2d (increment_ops.py:126-194) in ONE launch: region test against the
+ * any-channel input tile map, output tile flags, the exact FLOP-meter terms,
+ * the TMA/tcgen05 3xTF32 GEMM over live RH x RW output regions, split-K over a
+ * thread-block cluster reduced deterministically through DSMEM, and optionally
+ * the activation delta of the following inc_activation (increment_ops.py:232-238)
+ * in the epilogue.  Launch configuration: */
+typedef struct evc_conv_cfg {
+  int32_t bn;     /* output channels per CTA: 16, 32, 64, 128 or 256 */
+  int32_t rh, rw; /* output region rows x cols, rh * rw = 128, rw in {8, 16, 32} */
+  int32_t splits; /* K-splits = cluster size along z, 1..16 */
+} evc_conv_cfg;
+
+/* 1 if the fused path handles this geometry (pad < kernel, stride <= 8). */
+int evc_conv_fused_supported(const evc_conv_geom* g);
+/* Heuristic launch configuration for S sessions (max_splits <= 0: 8). */
+int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits, evc_conv_cfg* cfg);
+/* Pre-split (TF32 hi / lo), 128B-swizzled, K-major weight images (floats). */
+int64_t evc_conv_fused_pack_len(const evc_conv_geom* g, const evc_conv_cfg* cfg);
+int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_cfg* cfg, float* out);
+/* Bytes of the persistent per-(session, region, channel block) "computed last
+ * step" state; zero it whenever the output increment buffers are zeroed. */
+int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg, int32_t S);
+/* in_hwc: channels-innermost shadow of the input (see evc_to_hwc).
+ * Incremental mode (dense == 0): `in` supplies the per-channel input flags,
+ * fany[s][tile] the any-channel map (evc_tile_any, or written by the producing
+ * sparsify), table = evc_conv_table_fill output; in_true[s] (int32) and bulk[s]
+ * (int64) are ACCUMULATED (zero them per step) and resolved by evc_meter_step.
+ * Output flags are written to act_out when act >= 0, else to out.
+ * out may be NULL when act >= 0 (the conv values are then not materialised).
+ * Dense mode (dense != 0): every region, bias added; with act >= 0 the
+ * activation y = f(x) is written to act_out and acc = x when acc != NULL. */
+int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
+                   int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
+                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int32_t* in_true,
+                   int64_t* bulk, const evc_tensor* out, int32_t act, float alpha, float* acc,
+                   int64_t acc_stride, const evc_tensor* act_out, int32_t dense, int32_t S,
+                   void* stream);
+/* fany[s][t] = OR over channels of x's flags (input of a fused conv whose
+ * producer does not emit the map). */
+int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream);
+/* Per-step meter bookkeeping for n meter nodes x S sessions (graph.py:620-636):
+ * mode[l] = C_out for a fused conv (performed = 0 / dense / 2*C_out*bulk by the
+ * live-flag count, increment_ops.py:148-154,191), 0 for a node whose
+ * perf_step is already final; then perf_cum += perf_step and the false-tile
+ * fraction ff_last = 1 - in_true / nflags, ff_sum += ff_last. */
+int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* bulk,
+                   const int64_t* nflags, const int64_t* dense, const int32_t* mode,
+                   int64_t* perf_step, int64_t* perf_cum, double* ff_last, double* ff_sum,
+                   void* stream);
+
 /* Workspace floats needed by evc_conv_gemm for `max_tiles` active output
  * tiles and `splits` K-splits. */
 int64_t evc_conv_workspace(const evc_conv_geom* g, int64_t max_tiles, int32_t splits);
@@ -220,10 +271,12 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
                  uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay,
                  double* partials, int32_t* ticket, float* hwc, int32_t cp,
-                 int64_t hwc_stride, int32_t write_chw, int32_t delta_zero,
-                 int32_t S, void* stream);
+                 int64_t hwc_stride, uint8_t* fany, int32_t write_chw,
+                 int32_t delta_zero, int32_t S, void* stream);
 /* (hwc, cp, hwc_stride: optional channels-innermost shadow of y for the
- * TMA conv GEMM, see evc_to_hwc; write_chw = 0 skips the planar y values --
+ * TMA conv GEMM, see evc_to_hwc; fany: optional any-channel tile map of y
+ * for evc_conv_fused, only ever set to 1 -- zero it per step;
+ * write_chw = 0 skips the planar y values --
  * flags are always written.  delta_zero != 0 asserts tp == 0 and k == 0, so
  * the residual stays identically zero and is neither read nor written.) */
 
@@ -237,7 +290,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode,
                           const evc_tensor* y, double* k, double* norm_ema,
                           double tp, double ema_decay, double* partials,
                           int32_t* ticket, float* hwc, int32_t cp,
-                          int64_t hwc_stride, int32_t write_chw,
+                          int64_t hwc_stride, uint8_t* fany, int32_t write_chw,
                           int32_t delta_zero, int32_t S, void* stream);
 
 /* acc += dx on live tiles (AccState.fold, increment_ops.py:93-94). */

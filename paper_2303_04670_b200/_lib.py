@@ -37,6 +37,10 @@ class EvcConvGeom(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("c_in", "c_out", "kh", "kw", "stride", "pad", "H", "W", "Ho", "Wo", "th", "tw")]
 
 
+class EvcConvCfg(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits")]
+
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -44,6 +48,7 @@ _F = C.c_float
 _D = C.c_double
 _T = C.POINTER(EvcTensor)
 _G = C.POINTER(EvcConvGeom)
+_CF = C.POINTER(EvcConvCfg)
 
 _PROTOS = {
     "evc_version": (_I32, []),
@@ -70,6 +75,15 @@ _PROTOS = {
     "evc_conv_region_pack": (_I32, [_P, _I32, _I32, _I32, _I32, _P]),
     "evc_conv_region_workspace": (_I64, [_G, _I32, _I32]),
     "evc_conv_gemm_region": (_I32, [_G, _P, _I32, _I64, _P, _P, _T, _P, _I32, _I32, _P, _P]),
+    "evc_conv_fused_supported": (_I32, [_G]),
+    "evc_conv_fused_config": (_I32, [_G, _I32, _I32, _CF]),
+    "evc_conv_fused_pack_len": (_I64, [_G, _CF]),
+    "evc_conv_fused_pack": (_I32, [_P, _G, _CF, _P]),
+    "evc_conv_fused_state_len": (_I64, [_G, _CF, _I32]),
+    "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
+                              _I32, _I32, _P]),
+    "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
+    "evc_meter_step": (_I32, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
     "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
     "evc_conv_tc_pack_len": (_I64, [_I32, _I64]),
@@ -77,10 +91,10 @@ _PROTOS = {
     "evc_act_delta": (_I32, [_T, _P, _I64, _T, _I32, _F, _I32, _P]),
     "evc_act_dense": (_I32, [_P, _I64, _P, _I64, _P, _I64, _I64, _I32, _F, _I32, _P]),
     "evc_sparsify_partials": (_I64, [_T]),
-    "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P]),
+    "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _P, _I32, _I32, _I32, _P]),
     "evc_fold": (_I32, [_T, _P, _I64, _I32, _P]),
     "evc_upsample_sparsify_partials": (_I64, [_T]),
-    "evc_upsample_sparsify": (_I32, [_T, _I32, _I32, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32,
+    "evc_upsample_sparsify": (_I32, [_T, _I32, _I32, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _P, _I32,
                                      _I32, _I32, _P]),
     "evc_sparsify_finalize": (_I32, [_P, _I64, _P, _P, _D, _D, _I32, _I32, _P]),
     "evc_sumsq_dense": (_I32, [_P, _I64, _I64, _P, _I32, _I32, _P]),

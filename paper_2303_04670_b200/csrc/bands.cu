@@ -83,6 +83,7 @@ struct TBArgs {
   float* hwc;  // sparsify channels-innermost shadow (optional)
   int64_t hs;  // shadow session stride
   int cp;      // shadow channel stride
+  uint8_t* fany;  // sparsify: optional any-channel tile map of the output (OR-accumulated, zeroed per step)
   int write_chw;
   int delta_zero;  // sparsify with tp == 0 and k == 0: the residual is identically 0, skip its traffic
   int kind;
@@ -283,6 +284,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
       } else if (OP == OP_SPARSIFY) {
         p.y.f[(int64_t)s * p.y.fs + fo] = s_f1[t];
         p.dlive[(int64_t)s * g.C * g.GH * g.GW + fo] = s_f2[t];
+        if (p.fany && s_f1[t]) p.fany[((int64_t)s * g.GH + i) * g.GW + j0 + jl] = 1;  // benign race: all store 1
       } else if (OP == OP_ADD || OP == OP_MUL) {
         p.y.f[(int64_t)s * p.y.fs + fo] = p.a.f[(int64_t)s * p.a.fs + fo] | p.b.f[(int64_t)s * p.b.fs + fo];
       }
@@ -380,7 +382,7 @@ int64_t evc_sparsify_partials(const evc_tensor* dx) {
 
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, float* hwc,
-                 int32_t cp, int64_t hwc_stride, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
+                 int32_t cp, int64_t hwc_stride, uint8_t* fany, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
   EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && ticket && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
@@ -400,6 +402,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   p.hwc = hwc;
   p.hs = hwc_stride;
   p.cp = cp;
+  p.fany = fany;
   p.write_chw = write_chw;
   p.delta_zero = delta_zero;
   const int rc = tb_launch(OP_SPARSIFY, p, S, as_stream(stream));

@@ -118,6 +118,21 @@ __device__ __forceinline__ T block_sum(T v, F wsum) {
   return r;
 }
 
+// Activation f of inc_activation (tensors.py:285-312), float32 ops with the
+// reference's rounding (no FMA contraction).
+__device__ __forceinline__ float act_apply(float x, int kind, float alpha) {
+  switch (kind) {
+    case EVC_ACT_RELU:
+      return fmaxf(x, 0.0f);
+    case EVC_ACT_SIGMOID:
+      return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-x)));
+    case EVC_ACT_TANH:
+      return tanhf(x);
+    default:
+      return x > 0.0f ? x : __fmul_rn(alpha, x);
+  }
+}
+
 // Bilinear upsampling taps of one output coordinate: half-pixel source
 // (i + 0.5) / f - 0.5, clamped, float32 weights (tensors.py:259-266).
 struct Tap {
@@ -190,6 +205,7 @@ namespace evc {
 int init_masks();
 int init_conv();
 int init_conv_mask();
+int init_conv_fused();
 int init_elementwise();
 int init_bands();
 int init_linear_events();

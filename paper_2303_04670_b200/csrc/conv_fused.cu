@@ -1,0 +1,790 @@
+// Fused incremental convolution: ONE launch per conv layer per step.
+//
+// Replaces the value path, the mask propagation and the FLOP meter of
+// inc_conv2d (increment_ops.py:126-194) -- and, when the conv's only reader is
+// an activation node, inc_activation (increment_ops.py:232-238) -- with a
+// single TMA-fed tcgen05 kernel:
+//
+//  * M tile = an RH x RW region of output pixels (RH * RW = 128; RW = 32, 16 or
+//    8 so narrow maps do not waste rows).  A CTA first decides whether its region
+//    can change this step: it ORs the any-channel input tile map `fany` (written
+//    by the producing sparsify kernel) over the region's receptive box.  Sites
+//    whose taps all read dead tiles are exactly zero (mask soundness), so a dead
+//    region is skipped -- or zeroed once when it was computed last step
+//    (`rstate`), which restores the exact-zero invariant of TileMask.
+//  * Live regions: K-block = one tap (r, s) x 32 channels; its A operand is RH TMA
+//    boxes of the channels-innermost shadow of the input (zero padding = TMA
+//    out-of-bounds fill).  3xTF32 (hi*hi + hi*lo + lo*hi, fp32 TMEM accumulation)
+//    keeps fp32-grade accuracy; weights are pre-split, pre-swizzled K-major images.
+//  * Split-K runs across a thread-block cluster (grid z = cluster z = splits):
+//    each CTA parks its fp32 partial tile in shared memory and CTA rank r sums
+//    channel slice r over all ranks through DSMEM in rank order -- deterministic,
+//    no workspace, no second launch.
+//  * The epilogue adds the bias (dense pass) and optionally applies the
+//    activation delta y = f(acc + dx) - f(acc), acc += dx in place.
+//  * Warps 2-3 of every CTA (idle in the GEMM pipeline) compute the output tile
+//    flags (live iff some input tile in the tile's receptive box is live in any
+//    channel) and the exact reference meter terms:
+//    the live-flag count and sum_c sum_ab F_c[a][b] RT[a] CT[b] + border padding
+//    term, accumulated with integer atomics.  evc_meter_step turns them into
+//    `performed` (with the all-false / all-true shortcuts, increment_ops.py:148-154).
+//
+// Roles (8 warps): warp 0 = region test + TMA producer (lane 0); warp 1 = TMEM
+// alloc + MMA issuer (lane 0); warps 2-3 = flags + meter; warps 4-7 = hi/lo
+// split of each landed A stage, then the epilogue.
+
+#include <cooperative_groups.h>
+#include <cuda.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "conv_common.cuh"
+
+namespace evc {
+
+namespace fz {
+
+constexpr int BM = 128;
+constexpr int THREADS = 256;
+
+__host__ __device__ constexpr int stages_of(int bn) { return bn <= 64 ? 4 : (bn <= 128 ? 3 : 2); }
+__host__ __device__ constexpr int stage_bytes(int bn) { return 2 * BM * 128 + 2 * bn * 128; }
+static inline int smem_bytes(int bn) { return stages_of(bn) * stage_bytes(bn) + 1024 + 256; }
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void bar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "EVC_FW:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra EVC_FW;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c, int x, int y, int n,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(x), "r"(y), "r"(n), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// K-major SWIZZLE_128B operand descriptor (sm_100 version 1, layout type 2, SBO 1 KiB).
+__device__ __forceinline__ uint64_t desc_k(uint32_t a) {
+  return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+struct Args {
+  int c_in, c_out, kh, kw, stride, pad, H, W, Ho, Wo, S;
+  int RH, RW, RHn, RWn, cchunks, nkb, splits, kb_per_split, bn;
+  int th, tw;
+  const float* wpack;
+  const float* bias;
+  // incremental mode (dense == 0)
+  const uint8_t* fany;  // [S][GHi*GWi]
+  const uint8_t* in_f;  // per-channel input flags
+  int64_t in_fs;
+  const int32_t* tab;
+  uint8_t* oflags;  // output flag planes (conv output, or the fused activation's output)
+  int64_t ofs;
+  uint8_t* rstate;  // [S*R][nb]
+  int32_t* in_true;
+  unsigned long long* bulk;
+  // outputs
+  float* out;  // conv values (nullable when the activation is fused and nothing else reads them)
+  int64_t ovs;
+  int act;  // -1 = none
+  float alpha;
+  float* acc;  // activation accumulator (nullable in dense mode = dense_oracle)
+  int64_t accs;
+  float* yact;
+  int64_t yvs;
+  int dense;
+};
+
+// Flags + meter share of one CTA (q of Qs CTAs of session s; t = thread 0..63).
+// 32-bit indices: every per-session count here is far below 2^31.
+__device__ __noinline__ void side_work(const Args& a, int s, int q, int Qs, int t) {
+  const TabHdr& h = *reinterpret_cast<const TabHdr*>(a.tab);
+  const int To = h.GHo * h.GWo, Ti = h.GHi * h.GWi, GWo = h.GWo, GWi = h.GWi;
+  const int nthr = Qs * 64, gid = q * 64 + t;
+  const uint8_t* fa = a.fany + (int64_t)s * Ti;
+  const int32_t* boxr = a.tab + h.boxr;
+  const int32_t* boxc = a.tab + h.boxc;
+  // output tile flags, (channel, tile) order -> coalesced byte stores
+  uint8_t* of = a.oflags + (int64_t)s * a.ofs;
+  const int nflag = a.c_out * To;
+  for (int e = gid; e < nflag; e += nthr) {
+    const int tt = e % To;
+    const int i = tt / GWo, j = tt - i * GWo;
+    const int r0 = boxr[2 * i], r1 = boxr[2 * i + 1], c0 = boxc[2 * j], c1 = boxc[2 * j + 1];
+    int nf = 0;
+    for (int r = r0; r <= r1; ++r)
+      for (int c = c0; c <= c1; ++c) nf |= fa[r * GWi + c];
+    of[e] = nf != 0;
+  }
+  // meter: live-flag count, weighted count and border padding term
+  int cnt = 0;
+  long long w = 0;
+  const uint8_t* F = a.in_f + (int64_t)s * a.in_fs;
+  const int32_t* rt = a.tab + h.rt;
+  const int32_t* ct = a.tab + h.ct;
+  const int nin = a.c_in * Ti;
+  for (int e = gid; e < nin; e += nthr) {
+    if (F[e]) {
+      const int tt = e % Ti;
+      const int i = tt / GWi;
+      ++cnt;
+      w += (long long)(rt[i] * ct[tt - i * GWi]);
+    }
+  }
+  const int nbd = h.ngrp * a.c_in;
+  for (int e = gid; e < nbd; e += nthr) {
+    const int g = e / a.c_in, c = e - g * a.c_in;
+    const int32_t* gp = a.tab + h.grp + 5 * g;
+    const uint8_t* Fc = F + (int64_t)c * Ti;
+    int live = 0;
+    for (int p = 0; p < gp[1]; ++p)
+      for (int qq = 0; qq < gp[3]; ++qq) live |= Fc[(gp[0] + p) * GWi + gp[2] + qq];
+    if (live) w += gp[4];
+  }
+  cnt = (int)warp_sum_ll(cnt);
+  w = warp_sum_ll(w);
+  if ((t & 31) == 0) {
+    if (cnt) atomicAdd(a.in_true + s, cnt);
+    if (w) atomicAdd(a.bulk + s, (unsigned long long)w);
+  }
+}
+
+__device__ __noinline__ float act_other(float x, int kind, float alpha) { return act_apply(x, kind, alpha); }
+
+// f of the fused activation: ReLU inline, the rest out of line (keeps the kernel small)
+__device__ __forceinline__ float act_f(float x, int kind, float alpha) {
+  return kind == EVC_ACT_RELU ? fmaxf(x, 0.0f) : act_other(x, kind, alpha);
+}
+
+// Final values of N channels (n0, n0 + step, ...) of output site m (region row-major):
+// every global load is issued before any store so the latencies overlap.
+template <int N>
+__device__ __forceinline__ void emit(const Args& a, int s, int u0, int v0, int m, int n0, int step, int cnt,
+                                     const float* vals) {
+  const int u = u0 + m / a.RW, x = v0 + m % a.RW;
+  if (u >= a.Ho || x >= a.Wo) return;
+  const int64_t plane = (int64_t)a.Ho * a.Wo;
+  const int64_t base = (int64_t)n0 * plane + (int64_t)u * a.Wo + x;
+  const int64_t dn = (int64_t)step * plane;
+  float v[N], acc0[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    v[j] = vals[j];
+    if (j < cnt && a.dense && a.bias) v[j] = __fadd_rn(v[j], __ldg(a.bias + n0 + j * step));
+  }
+  if (a.out) {
+    float* __restrict__ o = a.out + (int64_t)s * a.ovs + base;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (j < cnt) o[j * dn] = v[j];
+  }
+  if (a.act < 0) return;
+  float* __restrict__ ap = a.acc ? a.acc + (int64_t)s * a.accs + base : nullptr;
+  float* __restrict__ yp = a.yact + (int64_t)s * a.yvs + base;
+  if (!a.dense) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc0[j] = j < cnt ? ap[j * dn] : 0.0f;
+  }
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if (j >= cnt) continue;
+    if (a.dense) {
+      yp[j * dn] = act_f(v[j], a.act, a.alpha);
+      if (ap) ap[j * dn] = v[j];
+    } else {
+      const float a1 = __fadd_rn(acc0[j], v[j]);
+      yp[j * dn] = __fsub_rn(act_f(a1, a.act, a.alpha), act_f(acc0[j], a.act, a.alpha));
+      ap[j * dn] = a1;
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant__ CUtensorMap tmap,
+                                                           const __grid_constant__ Args a) {
+  constexpr int NS = stages_of(BN);
+  constexpr int STAGE = stage_bytes(BN);
+  // NA rotating "main" accumulators for hi*hi (one per K-block, round robin) + one
+  // for the small hi*lo + lo*hi corrections, summed in fp32 (RN) by the epilogue.
+  constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 3 : 4);
+  constexpr int NEED = (NA + 1) * BN;
+  constexpr int TMEM_COLS = NEED <= 32 ? 32 : (NEED <= 64 ? 64 : (NEED <= 128 ? 128 : (NEED <= 256 ? 256 : 512)));
+  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                             ((uint32_t)(BM >> 4) << 24);
+  constexpr uint32_t A_BYTES = BM * 128;
+  constexpr uint32_t B_BYTES = 2 * BN * 128;
+
+  const int R = a.RHn * a.RWn;
+  const int reg = blockIdx.x;  // s * R + region
+  const int s = reg / R, rr = reg % R;
+  const int u0 = (rr / a.RWn) * a.RH, v0 = (rr % a.RWn) * a.RW;
+  const int nblk = blockIdx.y, z = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t rs_idx = (int64_t)reg * gridDim.y + nblk;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[NS], split[NS], empty[NS], acc
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 1);
+  int* s_flag = reinterpret_cast<int*>(tslot + 1);  // [0] live, [1] computed last step
+  const uint32_t sb = su32(smem), b0 = su32(bars);
+  auto tma_bar = [&](int i) { return b0 + 8u * i; };
+  auto split_bar = [&](int i) { return b0 + 8u * (NS + i); };
+  auto empty_bar = [&](int i) { return b0 + 8u * (2 * NS + i); };
+  const uint32_t acc_bar = b0 + 8u * (3 * NS);
+
+  // ---- region test: OR of the any-channel input tile map over the receptive box
+  if (warp == 0) {
+    int live = 1;
+    if (!a.dense) {
+      const int y_lo = max(0, u0 * a.stride - a.pad);
+      const int y_hi = min(a.H - 1, (min(u0 + a.RH, a.Ho) - 1) * a.stride - a.pad + a.kh - 1);
+      const int x_lo = max(0, v0 * a.stride - a.pad);
+      const int x_hi = min(a.W - 1, (min(v0 + a.RW, a.Wo) - 1) * a.stride - a.pad + a.kw - 1);
+      live = 0;
+      if (y_lo <= y_hi && x_lo <= x_hi) {
+        const int GWi = (a.W + a.tw - 1) / a.tw, GHi = (a.H + a.th - 1) / a.th;
+        const int ra = y_lo / a.th, nr = y_hi / a.th - ra + 1;
+        const int ca = x_lo / a.tw, nc = x_hi / a.tw - ca + 1;
+        const uint8_t* fa = a.fany + (int64_t)s * GHi * GWi;
+        for (int e = lane; e < nr * nc; e += 32) live |= fa[(ra + e / nc) * GWi + ca + e % nc];
+      }
+      live = __any_sync(0xffffffffu, live);
+    }
+    if (lane == 0) {
+      s_flag[0] = live;
+      s_flag[1] = a.dense ? 0 : a.rstate[rs_idx];
+      if (live) {
+        for (int i = 0; i < NS; ++i) {
+          bar_init(tma_bar(i), 1);
+          bar_init(split_bar(i), 128);
+          bar_init(empty_bar(i), 1);
+        }
+        bar_init(acc_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      }
+    }
+  }
+  __syncthreads();
+  const bool live = s_flag[0] != 0;
+  const int Qs = R * gridDim.y * gridDim.z;
+  const int q = ((int)blockIdx.z * (int)gridDim.y + nblk) * R + rr;
+
+  if (!live) {
+    if (!a.dense && warp >= 2 && warp < 4) side_work(a, s, q, Qs, threadIdx.x - 64);
+    if (!a.dense && z == 0 && s_flag[1]) {  // computed last step, dead now: restore exact zeros
+      const int n0 = nblk * a.bn, nn = min(a.bn, a.c_out - n0);
+      for (int e = threadIdx.x; e < nn * BM; e += THREADS) {
+        const int n = n0 + e / BM, m = e % BM;
+        const int u = u0 + m / a.RW, x = v0 + m % a.RW;
+        if (u >= a.Ho || x >= a.Wo) continue;
+        const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
+        if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
+        if (a.act >= 0) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
+      }
+      if (threadIdx.x == 0) a.rstate[rs_idx] = 0;
+    }
+    return;
+  }
+  if (!a.dense && z == 0 && threadIdx.x == 0 && !s_flag[1]) a.rstate[rs_idx] = 1;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const int kb0 = z * a.kb_per_split, kb1 = min(a.nkb, kb0 + a.kb_per_split), nk = kb1 - kb0;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ TMA producer
+      const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
+      const uint32_t box_bytes = (uint32_t)a.RW * 128u;
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % NS;
+        bar_wait(empty_bar(st), ((i / NS) & 1) ^ 1);
+        const int kb = kb0 + i;
+        const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
+        const int r = tap / a.kw, qq = tap % a.kw;
+        const uint32_t abuf = sb + st * STAGE;
+        bar_arrive_tx(tma_bar(st), A_BYTES + B_BYTES);
+        for (int hh = 0; hh < a.RH; ++hh)
+          tma_load_4d(abuf + hh * box_bytes, &tmap, c0, v0 * a.stride - a.pad + qq, (u0 + hh) * a.stride - a.pad + r,
+                      s, tma_bar(st));
+        bulk_load(abuf + 2 * A_BYTES, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % NS;
+        bar_wait(split_bar(st), (i / NS) & 1);
+        fence_after();
+        const uint32_t ah = sb + st * STAGE, al = ah + A_BYTES;
+        const uint32_t bh = ah + 2 * A_BYTES, bl = bh + BN * 128;
+        const uint32_t tmain = tmem + (uint32_t)((i % NA) * BN), tcorr = tmem + (uint32_t)(NA * BN);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
+          mma(tmain, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i >= NA || kk) ? 1u : 0u);
+          mma(tcorr, desc_k(ah + ko), desc_k(bl + ko), IDESC, (i | kk) ? 1u : 0u);
+          mma(tcorr, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
+        }
+        commit(empty_bar(st));
+      }
+      commit(acc_bar);
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    if (!a.dense) {
+      if (a.act >= 0) {  // warm L2 with the accumulator rows the epilogue will read
+        const int per = (a.bn + a.splits - 1) / a.splits;
+        const int lo = a.splits > 1 ? z * per : 0, hi = a.splits > 1 ? min(a.bn, lo + per) : a.bn;
+        const int rows = min(a.RH, a.Ho - u0);
+        const int64_t plane = (int64_t)a.Ho * a.Wo;
+        for (int e = threadIdx.x - 64; e < (hi - lo) * rows * 2; e += 64) {
+          const int n = nblk * a.bn + lo + e / (rows * 2), r = (e / 2) % rows, half = e & 1;
+          if (n >= a.c_out) continue;
+          const float* p = a.acc + (int64_t)s * a.accs + n * plane + (int64_t)(u0 + r) * a.Wo + v0 +
+                           half * min(a.RW - 1, a.Wo - 1 - v0);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+      side_work(a, s, q, Qs, threadIdx.x - 64);
+    }
+  } else {
+    // ------------------------------------------------------------- hi/lo split
+    const int t = threadIdx.x - 128;  // 0..127
+    for (int i = 0; i < nk; ++i) {
+      const int st = i % NS;
+      bar_wait(tma_bar(st), (i / NS) & 1);
+      float4* ah = reinterpret_cast<float4*>(smem + st * STAGE);
+      float4* al = reinterpret_cast<float4*>(smem + st * STAGE + A_BYTES);
+#pragma unroll
+      for (int e = 0; e < (int)(A_BYTES / 16 / 128); ++e) {
+        const int idx = t + e * 128;
+        const float4 x = ah[idx];
+        float4 hv, lv;
+        hv.x = tf32_rn(x.x);
+        hv.y = tf32_rn(x.y);
+        hv.z = tf32_rn(x.z);
+        hv.w = tf32_rn(x.w);
+        lv.x = __fsub_rn(x.x, hv.x);
+        lv.y = __fsub_rn(x.y, hv.y);
+        lv.z = __fsub_rn(x.z, hv.z);
+        lv.w = __fsub_rn(x.w, hv.w);
+        ah[idx] = hv;
+        al[idx] = lv;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bar_arrive(split_bar(st));
+    }
+    // ------------------------------------------------------------- epilogue (TMEM -> values)
+    const int m = 32 * (warp & 3) + lane;  // TMEM lane = region site
+    bar_wait(acc_bar, 0);
+    fence_after();
+    const int n_main = nk < NA ? nk : NA;
+    const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    float* P = reinterpret_cast<float*>(smem);  // [BN][BM] partial tile (split-K only)
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float vals[16], part[16];
+      tmem_ld16(trow + (uint32_t)(NA * BN + c0), vals);  // corrections
+      for (int j = 0; j < n_main; ++j) {
+        tmem_ld16(trow + (uint32_t)(j * BN + c0), part);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], part[e]);
+      }
+      if (a.splits == 1) {
+        const int n0 = nblk * BN + c0;
+        emit<16>(a, s, u0, v0, m, n0, 1, min(16, a.c_out - n0), vals);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
+      }
+    }
+  }
+  if (a.splits > 1) {
+    // deterministic split-K: rank r sums channel slice r over all ranks in rank order
+    cluster_sync();
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    const int nsp = a.splits;
+    const int per = (BN + nsp - 1) / nsp;
+    const int rank = (int)cl.block_rank();
+    const int lo = rank * per, hi = min(BN, lo + per);
+    float* P = reinterpret_cast<float*>(smem);
+    const int m = threadIdx.x % BM, g = threadIdx.x / BM;  // 2 channel groups of 128 sites
+    constexpr int NB = 4;
+    for (int nl0 = lo + g; nl0 < hi; nl0 += 2 * NB) {
+      const int cnt = min(NB, (hi - nl0 + 1) / 2);
+      float sum[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) sum[j] = 0.0f;
+      for (int zz = 0; zz < nsp; ++zz) {
+        const float* R = cl.map_shared_rank(P, zz);
+        float t[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) t[j] = j < cnt ? R[(nl0 + 2 * j) * BM + m] : 0.0f;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) sum[j] = __fadd_rn(sum[j], t[j]);
+      }
+      const int n0 = nblk * BN + nl0;
+      emit<NB>(a, s, u0, v0, m, n0, 2, min(cnt, (a.c_out - n0 + 1) / 2), sum);
+    }
+    cluster_sync();
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+// any-channel tile map: fany[s][t] = OR_c flags[s][c][t]
+__global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
+  const int Ti = x.GH * x.GW;
+  const int s = blockIdx.y;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Ti; t += gridDim.x * blockDim.x) {
+    int any = 0;
+    for (int c = 0; c < x.C && !any; ++c) any |= x.fplane(s, c)[t];
+    fany[(int64_t)s * Ti + t] = any != 0;
+  }
+}
+
+// Meter + false-fraction bookkeeping of one step (graph.py:620-636) for n meter
+// nodes x S sessions: conv nodes (mode 1) resolve the reference shortcuts from
+// the live-flag count; linear nodes (mode 0) already hold `performed`.
+__global__ void k_meter_step(int n, int S, const int32_t* __restrict__ in_true, const long long* __restrict__ bulk,
+                             const long long* __restrict__ nflags, const long long* __restrict__ dense,
+                             const int32_t* __restrict__ mode, long long* perf_step, long long* perf_cum,
+                             double* ff_last, double* ff_sum) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * S) return;
+  const int l = e / S;
+  const long long cnt = in_true[e];
+  long long p = perf_step[e];
+  if (mode[l] > 0) {
+    p = cnt == 0 ? 0LL : (cnt == nflags[l] ? dense[l] : 2LL * mode[l] * bulk[e]);
+    perf_step[e] = p;
+  }
+  perf_cum[e] += p;
+  const double ff = __dsub_rn(1.0, __ddiv_rn((double)cnt, (double)nflags[l]));
+  ff_last[e] = ff;
+  ff_sum[e] = __dadd_rn(ff_sum[e], ff);
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  return fn;
+}
+
+template <int BN>
+static cudaError_t launch(const CUtensorMap& m, const Args& a, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.S * a.RHn * a.RWn), (unsigned)((a.c_out + BN - 1) / BN), (unsigned)a.splits);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem_bytes(BN);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = (unsigned)a.splits;
+  cfg.attrs = at;
+  cfg.numAttrs = a.splits > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_conv_fused<BN>, m, a);
+}
+
+template <int BN>
+static int attr() {
+  if (cudaFuncSetAttribute(k_conv_fused<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(BN)) !=
+      cudaSuccess)
+    return 1;
+  return cudaFuncSetAttribute(k_conv_fused<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess
+             ? 0
+             : 1;
+}
+
+static bool valid_bn(int bn) { return bn == 16 || bn == 32 || bn == 64 || bn == 128 || bn == 256; }
+
+}  // namespace fz
+
+int init_conv_fused() {
+  int rc = fz::attr<16>() | fz::attr<32>() | fz::attr<64>() | fz::attr<128>() | fz::attr<256>();
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, fz::k_tile_any) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_meter_step) != cudaSuccess) rc = 1;
+  return rc ? EVC_ECUDA : EVC_OK;
+}
+
+}  // namespace evc
+
+using namespace evc;
+
+extern "C" {
+
+int evc_conv_fused_supported(const evc_conv_geom* g) {
+  if (!g) return 0;
+  // pad >= K: the all-true shortcut (increment_ops.py:150-154) can mark tiles whose
+  // box holds only padding -- the unfused path keeps that corner exact.
+  return g->stride >= 1 && g->stride <= 8 && g->stride * 32 <= 256 && g->pad < g->kh && g->pad < g->kw &&
+         fz::encoder() != nullptr;
+}
+
+int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits, evc_conv_cfg* cfg) {
+  EVC_CHECK_ARG(g && cfg && S > 0, "conv_fused_config: null argument");
+  cfg->rw = g->Wo > 16 ? 32 : (g->Wo > 8 ? 16 : 8);
+  cfg->rh = 128 / cfg->rw;
+  const int64_t regions = (int64_t)S * ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw);
+  int bn = 16;
+  while (bn < g->c_out && bn < 256) bn *= 2;
+  const int msp = std::max(1, std::min<int>(max_splits > 0 ? max_splits : 8, 16));
+  while (bn > 64 && regions * ((g->c_out + bn - 1) / bn) * msp < 148) bn /= 2;
+  cfg->bn = bn;
+  const int nkb = g->kh * g->kw * ((g->c_in + 31) / 32);
+  const int64_t ctas = regions * ((g->c_out + bn - 1) / bn);
+  int sp = ctas >= 148 ? 1 : (int)std::min<int64_t>(msp, (148 + ctas - 1) / ctas);
+  sp = std::max(1, std::min(sp, nkb));
+  const int kbps = (nkb + sp - 1) / sp;
+  cfg->splits = (nkb + kbps - 1) / kbps;
+  return EVC_OK;
+}
+
+int64_t evc_conv_fused_pack_len(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
+  if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
+  const int64_t nb = (g->c_out + cfg->bn - 1) / cfg->bn, nkb = (int64_t)g->kh * g->kw * ((g->c_in + 31) / 32);
+  return nb * nkb * 2 * cfg->bn * 32;
+}
+
+int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_cfg* cfg, float* out) {
+  EVC_CHECK_ARG(w && g && cfg && out && fz::valid_bn(cfg->bn), "conv_fused_pack: bad argument");
+  const int bn = cfg->bn, c_out = g->c_out, c_in = g->c_in, kh = g->kh, kw = g->kw;
+  const int cch = (c_in + 31) / 32;
+  const int64_t nb = (c_out + bn - 1) / bn, nkb = (int64_t)kh * kw * cch;
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t kb = 0; kb < nkb; ++kb) {
+      const int tap = (int)(kb / cch), c0 = (int)(kb % cch) * 32;
+      const int r = tap / kw, q = tap % kw;
+      float* hi = out + ((b * nkb + kb) * 2) * bn * 32;
+      float* lo = hi + (int64_t)bn * 32;
+      for (int row = 0; row < bn; ++row)
+        for (int e = 0; e < 32; ++e) {
+          const int64_t n = b * bn + row;
+          const int c = c0 + e;
+          const float x = (n < c_out && c < c_in) ? w[((n * c_in + c) * kh + r) * kw + q] : 0.0f;
+          uint32_t bits;
+          memcpy(&bits, &x, 4);
+          bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32 (as tf32_rn)
+          float hv;
+          memcpy(&hv, &bits, 4);
+          // 128B swizzle: 16-byte chunk j of row `row` lives at chunk (j ^ (row & 7))
+          const int j = e / 4, sub = e % 4;
+          const int64_t pos = (int64_t)row * 32 + ((j ^ (row & 7)) * 4) + sub;
+          hi[pos] = hv;
+          lo[pos] = x - hv;
+        }
+    }
+  return EVC_OK;
+}
+
+int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg, int32_t S) {
+  if (!g || !cfg || cfg->rh <= 0 || cfg->rw <= 0 || cfg->bn <= 0) return -1;
+  return (int64_t)S * ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw) *
+         ((g->c_out + cfg->bn - 1) / cfg->bn);
+}
+
+int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
+                   int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
+                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int32_t* in_true, int64_t* bulk,
+                   const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
+                   const evc_tensor* act_out, int32_t dense, int32_t S, void* stream) {
+  EVC_CHECK_ARG(g && cfg && in_hwc && wpack && S > 0 && fz::valid_bn(cfg->bn), "conv_fused: null argument");
+  EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
+  EVC_CHECK_ARG(cfg->rh * cfg->rw == fz::BM && (cfg->rw == 32 || cfg->rw == 16 || cfg->rw == 8) &&
+                    cfg->rw * g->stride <= 256,
+                "conv_fused: bad region shape");
+  EVC_CHECK_ARG(cfg->splits >= 1 && cfg->splits <= 16, "conv_fused: splits must lie in [1, 16]");
+  EVC_CHECK_ARG(cp % 4 == 0 && cp >= g->c_in && hwc_stride % 4 == 0, "conv_fused: shadow not 16B aligned");
+  EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && act_out->vals && (acc || dense)), "conv_fused: activation");
+  EVC_CHECK_ARG(out || act >= 0, "conv_fused: no output");
+  EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && in_true && bulk &&
+                          ((act >= 0 ? act_out->flags : (out ? out->flags : nullptr)) != nullptr)),
+                "conv_fused: incremental mode needs masks, fany, table, rstate and counters");
+  fz::EncodeTiled enc = fz::encoder();
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {(cuuint64_t)cp, (cuuint64_t)g->W, (cuuint64_t)g->H, (cuuint64_t)S};
+  const cuuint64_t strides[3] = {(cuuint64_t)cp * 4, (cuuint64_t)g->W * cp * 4, (cuuint64_t)hwc_stride * 4};
+  const cuuint32_t box[4] = {32, (cuuint32_t)(cfg->rw * g->stride), 1, 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g->stride, 1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in_hwc), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("evc: conv_fused: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return EVC_ECUDA;
+  }
+  fz::Args a;
+  memset(&a, 0, sizeof(a));
+  a.c_in = g->c_in;
+  a.c_out = g->c_out;
+  a.kh = g->kh;
+  a.kw = g->kw;
+  a.stride = g->stride;
+  a.pad = g->pad;
+  a.H = g->H;
+  a.W = g->W;
+  a.Ho = g->Ho;
+  a.Wo = g->Wo;
+  a.S = S;
+  a.RH = cfg->rh;
+  a.RW = cfg->rw;
+  a.RHn = (g->Ho + cfg->rh - 1) / cfg->rh;
+  a.RWn = (g->Wo + cfg->rw - 1) / cfg->rw;
+  a.cchunks = (g->c_in + 31) / 32;
+  a.nkb = g->kh * g->kw * a.cchunks;
+  a.splits = std::max(1, std::min<int>(cfg->splits, a.nkb));
+  a.kb_per_split = (a.nkb + a.splits - 1) / a.splits;
+  a.splits = (a.nkb + a.kb_per_split - 1) / a.kb_per_split;
+  a.bn = cfg->bn;
+  a.th = g->th;
+  a.tw = g->tw;
+  a.wpack = wpack;
+  a.bias = bias;
+  a.dense = dense != 0;
+  if (!a.dense) {
+    const TView vin = view_of(*in);
+    a.fany = fany;
+    a.in_f = vin.f;
+    a.in_fs = vin.fs;
+    a.tab = table;
+    const evc_tensor* fo = act >= 0 ? act_out : out;
+    a.oflags = fo->flags;
+    a.ofs = fo->fstride;
+    a.rstate = rstate;
+    a.in_true = in_true;
+    a.bulk = reinterpret_cast<unsigned long long*>(bulk);
+  }
+  a.out = out ? out->vals : nullptr;
+  a.ovs = out ? out->vstride : 0;
+  a.act = act;
+  a.alpha = alpha;
+  a.acc = acc;
+  a.accs = acc_stride;
+  a.yact = act >= 0 ? act_out->vals : nullptr;
+  a.yvs = act >= 0 ? act_out->vstride : 0;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e;
+  switch (cfg->bn) {
+    case 16: e = fz::launch<16>(map, a, st); break;
+    case 32: e = fz::launch<32>(map, a, st); break;
+    case 64: e = fz::launch<64>(map, a, st); break;
+    case 128: e = fz::launch<128>(map, a, st); break;
+    default: e = fz::launch<256>(map, a, st); break;
+  }
+  if (e != cudaSuccess) {
+    set_error(std::string("evc: conv_fused launch: ") + cudaGetErrorString(e));
+    return EVC_ECUDA;
+  }
+  EVC_LAUNCH_CHECK("conv_fused");
+  return EVC_OK;
+}
+
+int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream) {
+  EVC_CHECK_ARG(x && x->flags && fany && S > 0, "tile_any: null argument");
+  TView v = view_of(*x);
+  const int Ti = v.GH * v.GW;
+  fz::k_tile_any<<<dim3(cdiv(Ti, 128), S), 128, 0, as_stream(stream)>>>(v, fany);
+  EVC_LAUNCH_CHECK("tile_any");
+  return EVC_OK;
+}
+
+int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* bulk, const int64_t* nflags,
+                   const int64_t* dense, const int32_t* mode, int64_t* perf_step, int64_t* perf_cum,
+                   double* ff_last, double* ff_sum, void* stream) {
+  EVC_CHECK_ARG(n > 0 && S > 0 && in_true && bulk && nflags && dense && mode && perf_step && perf_cum && ff_last &&
+                    ff_sum,
+                "meter_step: null argument");
+  const int tot = n * S;
+  fz::k_meter_step<<<cdiv(tot, 128), 128, 0, as_stream(stream)>>>(
+      n, S, in_true, reinterpret_cast<const long long*>(bulk), reinterpret_cast<const long long*>(nflags),
+      reinterpret_cast<const long long*>(dense), mode, reinterpret_cast<long long*>(perf_step),
+      reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum);
+  EVC_LAUNCH_CHECK("meter_step");
+  return EVC_OK;
+}
+
+}  // extern "C"

@@ -29,6 +29,7 @@ struct USArgs {
   int* ticket;
   float* hwc;
   int64_t hs;
+  uint8_t* fany;  // optional any-channel tile map of y (OR-accumulated, zeroed per step)
   int cp, write_chw, delta_zero, f, mode;
   int CW, nCG, nJC;
 };
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       const int cl = t / nj, jl = t % nj;
       const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i) * y.GW + j0 + jl;
       y.f[(int64_t)s * y.fs + fo] = s_ny[t];
+      if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i) * y.GW + fo % y.GW] = 1;  // benign race: all store 1
       a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage) {
@@ -159,7 +161,7 @@ int64_t evc_upsample_sparsify_partials(const evc_tensor* y) {
 int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, float* delta, int64_t ds,
                           uint8_t* dlive, const evc_tensor* y, double* k, double* norm_ema, double tp,
                           double ema_decay, double* partials, int32_t* ticket, float* hwc, int32_t cp,
-                          int64_t hwc_stride, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
+                          int64_t hwc_stride, uint8_t* fany, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
   EVC_CHECK_ARG(x && y && x->flags && y->flags && delta && dlive && k && norm_ema && partials && ticket && S > 0,
                 "upsample_sparsify: null argument");
   EVC_CHECK_ARG(factor == 2 || factor == 4, "upsample_sparsify: factor must be 2 or 4");
@@ -181,6 +183,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.hwc = hwc;
   a.hs = hwc_stride;
   a.cp = cp;
+  a.fany = fany;
   a.write_chw = write_chw;
   a.delta_zero = delta_zero;
   a.f = factor;

@@ -435,7 +435,8 @@ class Graph:
     """
 
     def __init__(self, spec: ModelSpec, weights, refresh_interval: int = DEFAULT_REFRESH_INTERVAL, *,
-                 sessions: int = 1, cuda_graph: bool = True, device=None, conv_kernel: str | None = None):
+                 sessions: int = 1, cuda_graph: bool = True, device=None, conv_kernel: str | None = None,
+                 max_splits: int = 0):
         self.lib = _lib.lib()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.spec = spec
@@ -448,6 +449,7 @@ class Graph:
         if self.S < 1:
             raise ValueError("sessions must be >= 1")
         self.use_cuda_graph = bool(cuda_graph)
+        self.max_splits = int(max_splits)  # K-split cap of the fused conv (0: library default)
         from . import tensors as _t
 
         self.conv_kernel = conv_kernel or _t.CONV_KERNEL
@@ -525,6 +527,7 @@ class Graph:
                 if i in self._consumers:
                     self._consumers[i].append(node.spec.id)
             node.shadow = None
+            node.fused_into = None
         for node in self.nodes:
             if node.kind != "concat":
                 continue
@@ -588,17 +591,26 @@ class Graph:
                 st_, pad_ = node.conv_attrs
                 src = self._slots[node.spec.inputs[0]].store
                 node.plan = ConvPlan(node.weight, st_, pad_, ish[1], ish[2], tile.h, tile.w, S,
-                                     vstride=src.C * src.H * src.W, kernel=self.conv_kernel)
+                                     vstride=src.C * src.H * src.W, kernel=self.conv_kernel,
+                                     max_splits=self.max_splits)
                 max_T = max(max_T, S * node.plan.T)
                 max_ws = max(max_ws, node.plan.ws_floats)
-                # a sparsify whose only reader is this conv writes the conv's
-                # channels-innermost shadow itself (and skips its planar values)
-                prod = self._by_id.get(node.spec.inputs[0])
-                if (node.plan.path == "region" and prod is not None and prod.kind == "sparsify"
-                        and self._consumers[prod.spec.id] == [node.spec.id]
-                        and prod.spec.id not in self.output_ids):
-                    prod.shadow = node.plan
-                    node.plan.fed_by_sparsify = True
+                node.fused_act = None
+                if node.plan.path == "fused":
+                    # a sparsify whose only reader is this conv writes the conv's channels-innermost
+                    # shadow and its any-channel tile map itself (and skips its planar values)
+                    prod = self._by_id.get(node.spec.inputs[0])
+                    node.plan.fed_by_sparsify = bool(
+                        prod is not None and prod.kind == "sparsify" and self._consumers[prod.spec.id] == [node.spec.id]
+                        and prod.spec.id not in self.output_ids)
+                    if node.plan.fed_by_sparsify:
+                        prod.shadow = node.plan
+                    # an activation that is the conv's only reader runs in the conv epilogue
+                    cons = self._consumers[node.spec.id]
+                    if (len(cons) == 1 and self._by_id[cons[0]].kind in ACTIVATION_KINDS
+                            and node.spec.id not in self.output_ids):
+                        node.fused_act = self._by_id[cons[0]]
+                        node.fused_act.fused_into = node
             if k == "linear":
                 f = int(node.spec.attrs["out_features"])
                 lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
@@ -614,36 +626,50 @@ class Graph:
         nm = max(len(meter_ids), 1)
         self._meter_ids = meter_ids
         self._meter_nodes = [self._by_id[i] for i in meter_ids]
-        # per-step scratch zeroed by ONE memset at the start of every step:
-        # int32 [flag counts (nm x S) | per conv: tile count (2) + mask scratch]
-        z32 = nm * S + (nm * S) % 2
-        conv_off = []
-        sp_off = []
+        # per-step scratch zeroed by ONE memset at the start of every step (byte arena):
+        # flag counts int32 (nm x S) | meter bulk int64 (nm x S) | performed int64 (nm x S) |
+        # per unfused conv: tile count + mask scratch | per fused conv: any-channel tile map |
+        # per sparsify: retire ticket
+        off = [0]
+
+        def take(nbytes, align=16):
+            o = -(-off[0] // align) * align
+            off[0] = o + int(nbytes)
+            return o
+
+        o_cnt, o_bulk, o_perf = take(4 * nm * S), take(8 * nm * S), take(8 * nm * S)
+        conv_off, fany_off, sp_off = [], [], []
         for node in self.nodes:
             if node.kind == "conv":
-                n = int(self.lib.evc_conv_mask_scratch(node.plan.g, S))
-                nreg = -(-(S * -(-int(node.plan.g.Ho) // 4) * -(-int(node.plan.g.Wo) // 32)) // 4)  # u8 -> int32
-                conv_off.append((node, z32, z32 + 2, z32 + 2 + n + n % 2))
-                z32 += 2 + n + n % 2 + nreg + nreg % 2
+                if node.plan.path == "fused":
+                    fany_off.append((node, take(S * node.plan.gi[0] * node.plan.gi[1])))
+                else:
+                    n = int(self.lib.evc_conv_mask_scratch(node.plan.g, S))
+                    conv_off.append((node, take(8), take(4 * n)))
             elif node.kind == "sparsify":
-                sp_off.append((node, z32))
-                z32 += 2
-        self._z32 = torch.zeros(z32, dtype=torch.int32, device=dev)
-        base = self._z32.data_ptr()
-        for node, c_off, s_off, r_off in conv_off:
-            node.mask_scratch = (base + 4 * c_off, base + 4 * s_off, base + 4 * r_off)
-        for node, off in sp_off:
-            node.ticket = base + 4 * off
-        self._cnt_step = self._z32[: nm * S].view(nm, S)
-        self._perf_step = torch.zeros((nm, S), dtype=torch.int64, device=dev)
+                sp_off.append((node, take(8)))
+        self._zero = torch.zeros(-(-off[0] // 16) * 16, dtype=torch.uint8, device=dev)
+        base = self._zero.data_ptr()
+        for node, c_off, s_off in conv_off:
+            node.mask_scratch = (base + c_off, base + s_off)
+        for node, o in fany_off:
+            node.plan.fany_ptr = base + o
+        for node, o in sp_off:
+            node.ticket = base + o
+        self._cnt_step = self._zero[o_cnt:o_cnt + 4 * nm * S].view(torch.int32).view(nm, S)
+        self._bulk_step = self._zero[o_bulk:o_bulk + 8 * nm * S].view(torch.int64).view(nm, S)
+        self._perf_step = self._zero[o_perf:o_perf + 8 * nm * S].view(torch.int64).view(nm, S)
         self._perf_cum = torch.zeros((nm, S), dtype=torch.int64, device=dev)
         self._ff_last = torch.zeros((nm, S), dtype=torch.float64, device=dev)
         self._ff_sum = torch.zeros((nm, S), dtype=torch.float64, device=dev)
         self._ff_n = 0
-        self._flag_size = torch.tensor(
-            [float(np.prod(grid_shape(self.shapes[self._by_id[i].spec.inputs[0]], tile))) for i in meter_ids] or [1.0],
-            dtype=torch.float64, device=dev).reshape(-1, 1)
+        nflags = [int(np.prod(grid_shape(self.shapes[self._by_id[i].spec.inputs[0]], tile))) for i in meter_ids]
         self._dense_static = [self._dense_equiv(self._by_id[i]) for i in meter_ids]
+        modes = [self._by_id[i].plan.c_out if self._by_id[i].kind == "conv" and self._by_id[i].plan.path == "fused"
+                 else 0 for i in meter_ids]
+        self._meter_static = (torch.tensor(nflags or [1], dtype=torch.int64, device=dev),
+                              torch.tensor(self._dense_static or [0], dtype=torch.int64, device=dev),
+                              torch.tensor(modes or [0], dtype=torch.int32, device=dev))
         self._perf_host = [0] * len(meter_ids)   # dense-pass contributions (host ints)
         self._dense_host = [0] * len(meter_ids)
         self._sp_nodes = sp_nodes
@@ -699,18 +725,32 @@ class Graph:
             if k == "conv":
                 plan = node.plan
                 mi = node.meter_idx
-                din, dout = self._desc(ns.inputs[0]), self._desc(nid)
+                din = self._desc(ns.inputs[0])
                 cnt_ptr = i32.data_ptr() + 4 * mi * S
                 perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
-                count_ptr, scratch_ptr, region_ptr = node.mask_scratch
-                tl = self._tile_list.data_ptr()
-                pre = None if getattr(plan, "fed_by_sparsify", False) else plan.prep(din)
-                if pre is not None:
-                    prog.append((pre[0], pre[1], "to_hwc"))
-                prog.append((L.evc_conv_mask, plan.mask_args(din, dout, scratch_ptr, cnt_ptr, tl, count_ptr,
-                                                             region_ptr, perf_ptr), "conv_mask"))
-                fn, args = plan.gemm(din, dout, None, (tl, count_ptr, region_ptr), self._conv_ws.data_ptr())
-                prog.append((fn, args, "conv_gemm"))
+                if plan.path == "fused":
+                    if not plan.fed_by_sparsify:
+                        pre = plan.prep(din)
+                        prog.append((pre[0], pre[1], "to_hwc"))
+                        prog.append((L.evc_tile_any, (din, plan.fany_ptr, S), "tile_any"))
+                    act = node.fused_act
+                    if act is not None:
+                        code, alpha = act.act
+                        fa = (code, alpha, act.acc.data_ptr(), act.acc[0].numel(), self._desc(act.spec.id))
+                        dout = None
+                    else:
+                        fa, dout = None, self._desc(nid)
+                    fn, args = plan.fused(din, dout, fany=plan.fany_ptr, in_true=cnt_ptr,
+                                          bulk=self._bulk_step.data_ptr() + 8 * mi * S, act=fa)
+                    prog.append((fn, args, "conv_fused"))
+                else:
+                    dout = self._desc(nid)
+                    count_ptr, scratch_ptr = node.mask_scratch
+                    tl = self._tile_list.data_ptr()
+                    prog.append((L.evc_conv_mask, plan.mask_args(din, dout, scratch_ptr, cnt_ptr, tl, count_ptr,
+                                                                 perf_ptr), "conv_mask"))
+                    fn, args = plan.gemm(din, dout, None, (tl, count_ptr), self._conv_ws.data_ptr())
+                    prog.append((fn, args, "conv_gemm"))
             elif k == "linear":
                 mi = node.meter_idx
                 din = self._desc(ns.inputs[0])
@@ -721,6 +761,8 @@ class Graph:
                 dflat = self._desc(ns.inputs[0], masked=False)
                 prog.append((L.evc_linear, (dflat, node.weight.data_ptr(), None, self._desc(nid), f, 0, perf_ptr,
                                             self._lin_ws.data_ptr(), S), "linear"))
+            elif k in ACTIVATION_KINDS and node.fused_into is not None:
+                continue  # evaluated in the producing conv's epilogue
             elif k in ACTIVATION_KINDS:
                 code, alpha = node.act
                 prog.append((L.evc_act_delta, (self._desc(ns.inputs[0]), node.acc.data_ptr(),
@@ -729,7 +771,7 @@ class Graph:
                 j = node.sp_idx
                 up = self._by_id[ns.inputs[0]]
                 sh = node.shadow
-                hwc = (sh.hwc.data_ptr(), sh.cp, sh.hwc[0].numel()) if sh is not None else (None, 0, 0)
+                hwc = (sh.hwc.data_ptr(), sh.cp, sh.hwc[0].numel(), sh.fany_ptr) if sh is not None else (None, 0, 0, None)
                 mode = 0 if up.spec.attrs.get("mode", "nearest") == "nearest" else 1
                 prog.append((L.evc_upsample_sparsify, (self._desc(up.spec.inputs[0]), int(up.spec.attrs.get("factor", 2)),
                                                        mode, node.delta.data_ptr(), node.delta[0].numel(),
@@ -744,7 +786,7 @@ class Graph:
             elif k == "sparsify":
                 j = node.sp_idx
                 sh = node.shadow  # ConvPlan of the only consumer when it reads a channels-innermost shadow
-                hwc = (sh.hwc.data_ptr(), sh.cp, sh.hwc[0].numel()) if sh is not None else (None, 0, 0)
+                hwc = (sh.hwc.data_ptr(), sh.cp, sh.hwc[0].numel(), sh.fany_ptr) if sh is not None else (None, 0, 0, None)
                 prog.append((L.evc_sparsify, (self._desc(ns.inputs[0]), node.delta.data_ptr(), node.delta[0].numel(),
                                               node.dlive.data_ptr(), self._desc(nid),
                                               self._k.data_ptr() + 8 * j * S, self._norm.data_ptr() + 8 * j * S,
@@ -791,8 +833,7 @@ class Graph:
         CUDA events are recorded around every launch whose name is in ``names``
         (eager runs only; used by bench.py for per-kernel timing)."""
         s = _lib.stream_ptr()
-        self._perf_step.zero_()
-        self._z32.zero_()
+        self._zero.zero_()
         for fn, args, name in self._program:
             if timed is not None and name in timed[0]:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -803,20 +844,22 @@ class Graph:
                 continue
             _lib.check(fn(*args, s), name)
         # device-side meter bookkeeping (graph.py:620-629, 632-636)
-        self._perf_cum.add_(self._perf_step)
-        self._ff_last.copy_(1.0 - self._cnt_step.to(torch.float64) / self._flag_size)
-        self._ff_sum.add_(self._ff_last)
+        nflags, dense, mode = self._meter_static
+        _lib.check(self.lib.evc_meter_step(len(self._meter_ids) or 1, self.S, self._cnt_step.data_ptr(),
+                                           self._bulk_step.data_ptr(), nflags.data_ptr(), dense.data_ptr(),
+                                           mode.data_ptr(), self._perf_step.data_ptr(), self._perf_cum.data_ptr(),
+                                           self._ff_last.data_ptr(), self._ff_sum.data_ptr(), s), "meter_step")
 
     def dense_launches(self) -> int:
         """libevconv launches of the last dense pass (refresh), excluding torch memsets."""
         return getattr(self, "_dense_launches", 0)
 
     def kernel_launches_per_step(self) -> int:
-        """libevconv kernels launched by one incr_step (torch bookkeeping ops excluded)."""
-        n = 0
+        """libevconv kernels launched by one incr_step (+ the scratch memset; diff_mask excluded)."""
+        n = 2  # memset of the per-step scratch + meter bookkeeping
         for fn, args, name in self._program:
             n += 2 if name in ("conv_mask", "maxpool", "linear") else 1
-        n += sum(1 for nd in self.nodes if nd.kind == "conv" and nd.plan.splits > 1)  # split-K reduce
+        n += sum(1 for nd in self.nodes if nd.kind == "conv" and nd.plan.path != "fused" and nd.plan.splits > 1)
         return n
 
     # -- dense evaluation (graph.py:503-565) ----------------------------------------
@@ -833,12 +876,25 @@ class Graph:
             ns, k, nid = node.spec, node.kind, node.spec.id
             if k == "conv":
                 din = self._desc(ns.inputs[0], False)
-                pre = node.plan.prep(din)
-                if pre is not None:
+                plan = node.plan
+                if plan.path == "fused":
+                    pre = plan.prep(din)
                     run(pre[0], *pre[1])
-                fn, args = node.plan.gemm(din, self._desc(nid, False), _lib.ptr(node.bias), None,
-                                          self._conv_ws.data_ptr())
-                run(fn, *args)
+                    act = node.fused_act
+                    if act is not None:
+                        code, alpha = act.act
+                        fa = (code, alpha, act.acc.data_ptr() if mutate else None, act.acc[0].numel(),
+                              self._desc(act.spec.id, False))
+                        fn, args = plan.fused(din, None, bias_ptr=_lib.ptr(node.bias), act=fa, dense=True)
+                    else:
+                        fn, args = plan.fused(din, self._desc(nid, False), bias_ptr=_lib.ptr(node.bias), dense=True)
+                    run(fn, *args)
+                else:
+                    fn, args = plan.gemm(din, self._desc(nid, False), _lib.ptr(node.bias), None,
+                                         self._conv_ws.data_ptr())
+                    run(fn, *args)
+            elif k in ACTIVATION_KINDS and node.fused_into is not None:
+                continue  # evaluated in the producing conv's epilogue
             elif k == "linear":
                 f = int(ns.attrs["out_features"])
                 run(L.evc_linear, self._desc(ns.inputs[0], False), node.weight.data_ptr(),
@@ -915,6 +971,8 @@ class Graph:
         for nd in self.nodes:  # conv input shadows held dense values during the dense pass
             if nd.kind == "conv" and nd.plan.hwc is not None:
                 nd.plan.hwc.zero_()
+            if nd.kind == "conv" and nd.plan.path == "fused":
+                nd.plan.rstate.zero_()  # no region holds a nonzero increment now
 
     def dense_oracle(self, x):
         """Pure dense forward of the primary output; session state is untouched."""

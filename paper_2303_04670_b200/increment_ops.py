@@ -137,23 +137,32 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     lib = _lib.lib()
     plan = tensors.ConvPlan(weight, st, pad, h, w, tile.h, tile.w)
     yv, yf = _zeros_incr((c_out, ho, wo), tile, dev)
-    T = yf.shape[1] * yf.shape[2]
-    i32 = torch.zeros(2, dtype=torch.int32, device=dev)  # [in_true, tile_count]
-    tiles = torch.empty(T, dtype=torch.int32, device=dev)
-    regions = torch.zeros(-(-ho // 4) * -(-wo // 32), dtype=torch.uint8, device=dev)
-    scratch = torch.zeros(int(lib.evc_conv_mask_scratch(plan.g, 1)), dtype=torch.int32, device=dev)
-    perf = torch.zeros(1, dtype=torch.int64, device=dev)
     s = _lib.stream_ptr()
     din = x.desc()
     dout = _desc(yv, yf, tile)
-    _lib.check(lib.evc_conv_mask(*plan.mask_args(din, dout, _lib.ptr(scratch), _lib.ptr(i32), _lib.ptr(tiles),
-                                                 _lib.ptr(i32) + 4, _lib.ptr(regions), _lib.ptr(perf)), s),
-               "conv_mask")
-    ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=dev)
-    pre = plan.prep(din)
-    if pre is not None:
+    if plan.path == "fused":
+        fany = torch.zeros(plan.gi[0] * plan.gi[1], dtype=torch.uint8, device=dev)
+        i32 = torch.zeros(2, dtype=torch.int32, device=dev)  # [in_true, pad]
+        bulk = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.check(lib.evc_tile_any(din, _lib.ptr(fany), 1, s), "tile_any")
+        pre = plan.prep(din)
         _lib.check(pre[0](*pre[1], s), "to_hwc")
-    fn, args = plan.gemm(din, dout, None, (_lib.ptr(tiles), _lib.ptr(i32) + 4, _lib.ptr(regions)), ws.data_ptr())
+        fn, args = plan.fused(din, dout, fany=_lib.ptr(fany), in_true=_lib.ptr(i32), bulk=_lib.ptr(bulk))
+        _lib.check(fn(*args, s), "conv_fused")
+        cnt, b = int(i32[0].item()), int(bulk.item())
+        n_flags = c_in * plan.gi[0] * plan.gi[1]
+        perf = 0 if cnt == 0 else (plan.dense_flops if cnt == n_flags else 2 * c_out * b)
+        meter.add(perf, 0)
+        return IncrementTensor(yv, TileMask(yf, tile))
+    T = yf.shape[1] * yf.shape[2]
+    i32 = torch.zeros(2, dtype=torch.int32, device=dev)  # [in_true, tile_count]
+    tiles = torch.empty(T, dtype=torch.int32, device=dev)
+    scratch = torch.zeros(int(lib.evc_conv_mask_scratch(plan.g, 1)), dtype=torch.int32, device=dev)
+    perf = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.check(lib.evc_conv_mask(*plan.mask_args(din, dout, _lib.ptr(scratch), _lib.ptr(i32), _lib.ptr(tiles),
+                                                 _lib.ptr(i32) + 4, _lib.ptr(perf)), s), "conv_mask")
+    ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=dev)
+    fn, args = plan.gemm(din, dout, None, (_lib.ptr(tiles), _lib.ptr(i32) + 4), ws.data_ptr())
     _lib.check(fn(*args, s), "conv_gemm")
     meter.add(int(perf.item()), 0)
     return IncrementTensor(yv, TileMask(yf, tile))

@@ -262,40 +262,41 @@ def pack_conv_weight(weight: torch.Tensor):
 class ConvPlan:
     """Static launch plan of one conv layer: geometry table, kernel path, packed weights, K-splits.
 
-    path "region": stride-1 conv on 16-byte aligned planes -> TMA-fed tcgen05 GEMM over 4x32
-    output regions (evc_conv_gemm_region); path "tile": tcgen05 GEMM over gathered sites of the
-    active 6x6 output tiles (evc_conv_gemm with packed weights); path "simt": FFMA reference kernel.
+    path "fused": TMA-fed tcgen05 GEMM over live RH x RW output regions with the mask
+    propagation, the FLOP meter, the split-K reduction (thread-block cluster) and an
+    optional activation delta in the same launch (evc_conv_fused); path "tile": tcgen05
+    GEMM over gathered sites of the active 6x6 output tiles after evc_conv_mask (geometries
+    the fused kernel does not take: padding >= kernel); path "simt": FFMA reference kernel.
     """
 
-    def __init__(self, weight: torch.Tensor, stride, pad, h, w, th, tw, S=1, vstride=None, kernel=None):
+    def __init__(self, weight: torch.Tensor, stride, pad, h, w, th, tw, S=1, vstride=None, kernel=None,
+                 max_splits: int = 0):
         lib = _lib.lib()
         c_out, c_in, kh, kw = (int(v) for v in weight.shape)
         self.g, self.table = conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw)
         self.c_out, self.c_in, self.kh, self.kw, self.S = c_out, c_in, kh, kw, S
         self.weight = weight
         kernel = kernel or CONV_KERNEL
-        vs = c_in * h * w if vstride is None else int(vstride)
         ho, wo = int(self.g.Ho), int(self.g.Wo)
         T = -(-ho // th) * -(-wo // tw)
         self.T = T
         self.wpack = None
         self.hwc = None
-        del vs
-        if kernel == "tc" and lib.evc_conv_region_supported(self.g):
-            self.path = "region"
+        self.gi = (-(-h // th), -(-w // tw))  # input tile grid
+        if kernel == "tc" and lib.evc_conv_fused_supported(self.g):
+            self.path = "fused"
             self.cp = int(lib.evc_hwc_channels(c_in))
             self.hwc = torch.zeros((S, h, w, self.cp), dtype=torch.float32, device=weight.device)
-            rh, rw = -(-ho // 4), -(-wo // 32)
-            self.n_regions = S * rh * rw
+            self.cfg = _lib.EvcConvCfg()
+            _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
             host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)
-            out = np.zeros(int(lib.evc_conv_region_pack_len(c_out, c_in, kh, kw)), dtype=np.float32)
-            _lib.check(lib.evc_conv_region_pack(host.ctypes.data, c_out, c_in, kh, kw, out.ctypes.data), "pack")
+            out = np.zeros(int(lib.evc_conv_fused_pack_len(self.g, self.cfg)), dtype=np.float32)
+            _lib.check(lib.evc_conv_fused_pack(host.ctypes.data, self.g, self.cfg, out.ctypes.data), "pack")
             self.wpack = torch.from_numpy(out).to(weight.device)
-            bn = 256 if c_out >= 256 else max(16, -(-c_out // 16) * 16)
-            ctas = self.n_regions * -(-c_out // bn)
-            nkb = kh * kw * -(-c_in // 32)
-            self.splits = 1 if ctas >= 148 else int(max(1, min(-(-148 // ctas), nkb // 2, 64)))
-            self.ws_floats = int(lib.evc_conv_region_workspace(self.g, S, self.splits))
+            self.rstate = torch.zeros(int(lib.evc_conv_fused_state_len(self.g, self.cfg, S)), dtype=torch.uint8,
+                                      device=weight.device)
+            self.splits = int(self.cfg.splits)
+            self.ws_floats = 0
         else:
             self.path = "tile" if kernel == "tc" else "simt"
             if self.path == "tile":
@@ -306,29 +307,33 @@ class ConvPlan:
 
     def prep(self, din):
         """(fn, args-without-stream) mirroring the conv input into the HWC shadow, or None."""
-        if self.path != "region":
+        if self.path != "fused":
             return None
         return _lib.lib().evc_to_hwc, (din, self.hwc.data_ptr(), self.hwc[0].numel(), self.cp, self.S)
 
-    def mask_args(self, din, dout, scratch, in_true, tile_list, tile_count, regions, meter):
-        """evc_conv_mask arguments (stream appended by the caller)."""
-        if self.path == "region":
-            tile_list = tile_count = None
-        else:
-            regions = None
-        return (self.g, din, dout, self.table.data_ptr(), scratch, in_true, tile_list, tile_count, regions, meter,
+    def mask_args(self, din, dout, scratch, in_true, tile_list, tile_count, meter):
+        """evc_conv_mask arguments of the unfused paths (stream appended by the caller)."""
+        return (self.g, din, dout, self.table.data_ptr(), scratch, in_true, tile_list, tile_count, None, meter,
                 self.S)
 
-    def gemm(self, din, dout, bias_ptr, work, ws_ptr):
-        """(ctypes fn, args-without-stream) of the GEMM launch.
+    def fused(self, din, dout, *, fany=None, in_true=None, bulk=None, bias_ptr=None, act=None, dense=False):
+        """(ctypes fn, args-without-stream) of evc_conv_fused.
 
-        work = None for the dense pass (every tile / region), else the
-        (tile_list, tile_count, region_flags) device pointers from conv_mask."""
+        act = (code, alpha, acc_ptr, acc_stride, act_desc) fuses the activation node;
+        dout may then be None (conv values not materialised)."""
+        code, alpha, acc, accs, adesc = act if act is not None else (-1, 0.0, None, 0, None)
+        return _lib.lib().evc_conv_fused, (self.g, self.cfg, self.hwc.data_ptr(), self.cp, self.hwc[0].numel(),
+                                           self.wpack.data_ptr(), bias_ptr, din, fany, self.table.data_ptr(),
+                                           self.rstate.data_ptr(), in_true, bulk, dout, code, alpha, acc, accs,
+                                           adesc, 1 if dense else 0, self.S)
+
+    def gemm(self, din, dout, bias_ptr, work, ws_ptr):
+        """(ctypes fn, args-without-stream) of the unfused GEMM launch (tile / simt paths).
+
+        work = None for the dense pass (every tile), else the (tile_list, tile_count)
+        device pointers from conv_mask."""
         lib = _lib.lib()
-        tl, tc, rg = work if work is not None else (None, None, None)
-        if self.path == "region":
-            return lib.evc_conv_gemm_region, (self.g, self.hwc.data_ptr(), self.cp, self.hwc[0].numel(),
-                                              _lib.ptr(self.wpack), bias_ptr, dout, rg, self.S, self.splits, ws_ptr)
+        tl, tc = work if work is not None else (None, None)
         return lib.evc_conv_gemm, (self.g, din, self.weight.data_ptr(), _lib.ptr(self.wpack), bias_ptr, dout,
                                    self.table.data_ptr(), tl, tc, self.S, self.splits, ws_ptr)
 
@@ -364,14 +369,18 @@ def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> tor
     plan = ConvPlan(weight, stride, padding, h, w, th, tw)
     y = torch.empty((c_out, ho, wo), dtype=torch.float32, device=x.device)
     b = None if bias is None else as_bias(bias, c_out, x.device)
-    ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=x.device)
     din = _lib.tdesc(_lib.ptr(x), None, c * h * w, 0, c, h, w, th, tw)
     dout = _lib.tdesc(_lib.ptr(y), None, c_out * ho * wo, 0, c_out, ho, wo, th, tw)
-    pre = plan.prep(din)
-    if pre is not None:
-        _lib.check(pre[0](*pre[1], _lib.stream_ptr()), "to_hwc")
+    s = _lib.stream_ptr()
+    if plan.path == "fused":
+        pre = plan.prep(din)
+        _lib.check(pre[0](*pre[1], s), "to_hwc")
+        fn, args = plan.fused(din, dout, bias_ptr=_lib.ptr(b), dense=True)
+        _lib.check(fn(*args, s), "conv_fused")
+        return y
+    ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=x.device)
     fn, args = plan.gemm(din, dout, _lib.ptr(b), None, ws.data_ptr())
-    _lib.check(fn(*args, _lib.stream_ptr()), "conv_gemm")
+    _lib.check(fn(*args, s), "conv_gemm")
     return y
 
 

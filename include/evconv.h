@@ -209,15 +209,28 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
 /* fany[s][t] = OR over channels of x's flags (input of a fused conv whose
  * producer does not emit the map). */
 int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream);
-/* Per-step meter bookkeeping for n meter nodes x S sessions (graph.py:620-636):
- * mode[l] = C_out for a fused conv (performed = 0 / dense / 2*C_out*bulk by the
- * live-flag count, increment_ops.py:148-154,191), 0 for a node whose
- * perf_step is already final; then perf_cum += perf_step and the false-tile
- * fraction ff_last = 1 - in_true / nflags, ff_sum += ff_last. */
+/* One sparsify node's deferred norm fold: partials[s*n + b] are the per-CTA sums
+ * of corrected^2 written by evc_sparsify / evc_upsample_sparsify called with
+ * ticket == NULL; norm_ema[s], k[s] as in evc_sparsify. */
+typedef struct evc_sp_node {
+  const double* partials;
+  int64_t n;
+  double* norm_ema;
+  double* k;
+  double tp, decay;
+} evc_sp_node;
+
+/* End-of-step bookkeeping in one launch (graph.py:617-636):
+ *  - n meter nodes x S sessions: mode[l] = C_out for a fused conv (performed =
+ *    0 / dense / 2*C_out*bulk by the live-flag count, increment_ops.py:148-154,191),
+ *    0 for a node whose perf_step is already final; then perf_cum += perf_step
+ *    and the false-tile fraction ff_last = 1 - in_true / nflags, ff_sum += ff_last;
+ *  - n_sp sparsify nodes (sp_nodes: DEVICE array): norm_ema / k update from the
+ *    deferred partial sums in a fixed order (sparsify.py:72-76). */
 int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* bulk,
                    const int64_t* nflags, const int64_t* dense, const int32_t* mode,
                    int64_t* perf_step, int64_t* perf_cum, double* ff_last, double* ff_sum,
-                   void* stream);
+                   const evc_sp_node* sp_nodes, int32_t n_sp, void* stream);
 
 /* Workspace floats needed by evc_conv_gemm for `max_tiles` active output
  * tiles and `splits` K-splits. */
@@ -265,7 +278,8 @@ int evc_act_dense(const float* x, int64_t x_stride, float* y, int64_t y_stride,
  * residual is nonzero.  partials (float64, S*C*GH) receives per-CTA sums of
  * corrected^2; the last CTA to retire (ticket: zeroed int32) folds them into
  * norm_ema / k in a fixed order (sparsify.py:72-76), so the whole step is
- * one launch. */
+ * one launch.  ticket == NULL leaves the fold to evc_meter_step (graph runtime:
+ * one end-of-step launch for every sparsify node). */
 int64_t evc_sparsify_partials(const evc_tensor* dx); /* per session */
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
                  uint8_t* dlive, const evc_tensor* y, double* k,

@@ -41,6 +41,11 @@ class EvcConvCfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits")]
 
 
+class EvcSpNode(C.Structure):
+    _fields_ = [("partials", C.c_void_p), ("n", C.c_int64), ("norm_ema", C.c_void_p), ("k", C.c_void_p),
+                ("tp", C.c_double), ("decay", C.c_double)]
+
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -83,7 +88,7 @@ _PROTOS = {
     "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
                               _I32, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
-    "evc_meter_step": (_I32, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "evc_meter_step": (_I32, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
     "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
     "evc_conv_tc_pack_len": (_I64, [_I32, _I64]),

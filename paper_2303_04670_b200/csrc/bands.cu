@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     const int nblocks = gridDim.x * gridDim.y;
     ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
     if (threadIdx.x == 0) p.partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
+    if (!p.ticket) return;  // norm / k folded later by evc_meter_step (one launch for every node)
     // last CTA to retire folds every session's partials into norm_ema / k (fixed order)
     __shared__ int s_last;
     __syncthreads();
@@ -383,7 +384,7 @@ int64_t evc_sparsify_partials(const evc_tensor* dx) {
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, float* hwc,
                  int32_t cp, int64_t hwc_stride, uint8_t* fany, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
-  EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && ticket && dx->flags && y->flags && S > 0,
+  EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
   EVC_CHECK_ARG(!hwc || cp >= dx->C, "sparsify: shadow channel stride too small");

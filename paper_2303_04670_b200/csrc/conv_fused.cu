@@ -513,26 +513,38 @@ __global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
   }
 }
 
-// Meter + false-fraction bookkeeping of one step (graph.py:620-636) for n meter
-// nodes x S sessions: conv nodes (mode 1) resolve the reference shortcuts from
-// the live-flag count; linear nodes (mode 0) already hold `performed`.
-__global__ void k_meter_step(int n, int S, const int32_t* __restrict__ in_true, const long long* __restrict__ bulk,
-                             const long long* __restrict__ nflags, const long long* __restrict__ dense,
-                             const int32_t* __restrict__ mode, long long* perf_step, long long* perf_cum,
-                             double* ff_last, double* ff_sum) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n * S) return;
-  const int l = e / S;
-  const long long cnt = in_true[e];
-  long long p = perf_step[e];
-  if (mode[l] > 0) {
-    p = cnt == 0 ? 0LL : (cnt == nflags[l] ? dense[l] : 2LL * mode[l] * bulk[e]);
-    perf_step[e] = p;
+// End-of-step bookkeeping (graph.py:617-636), one launch: block 0 resolves the
+// meters of n meter nodes x S sessions -- conv nodes (mode = C_out) apply the
+// reference shortcuts from the live-flag count, linear nodes (mode 0) already
+// hold `performed` -- and the false-tile fractions; block 1 + j folds sparsify
+// node j's per-CTA sums of squares into norm_ema / k (sparsify.py:72-76) in a
+// fixed order.  k is first read by the NEXT step's sparsify of that node, so
+// folding at the end of the step is exactly the reference's sequence.
+__global__ void __launch_bounds__(256) k_meter_step(int n, int S, const int32_t* __restrict__ in_true,
+                                                    const long long* __restrict__ bulk,
+                                                    const long long* __restrict__ nflags,
+                                                    const long long* __restrict__ dense,
+                                                    const int32_t* __restrict__ mode, long long* perf_step,
+                                                    long long* perf_cum, double* ff_last, double* ff_sum,
+                                                    const evc_sp_node* __restrict__ sp) {
+  if (blockIdx.x > 0) {
+    const evc_sp_node nd = sp[blockIdx.x - 1];
+    sparsify_finalize_all(nd.partials, nd.n, nd.norm_ema, nd.k, nd.tp, nd.decay, 0, S);
+    return;
   }
-  perf_cum[e] += p;
-  const double ff = __dsub_rn(1.0, __ddiv_rn((double)cnt, (double)nflags[l]));
-  ff_last[e] = ff;
-  ff_sum[e] = __dadd_rn(ff_sum[e], ff);
+  for (int e = threadIdx.x; e < n * S; e += blockDim.x) {
+    const int l = e / S;
+    const long long cnt = in_true[e];
+    long long p = perf_step[e];
+    if (mode[l] > 0) {
+      p = cnt == 0 ? 0LL : (cnt == nflags[l] ? dense[l] : 2LL * mode[l] * bulk[e]);
+      perf_step[e] = p;
+    }
+    perf_cum[e] += p;
+    const double ff = __dsub_rn(1.0, __ddiv_rn((double)cnt, (double)nflags[l]));
+    ff_last[e] = ff;
+    ff_sum[e] = __dadd_rn(ff_sum[e], ff);
+  }
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -774,15 +786,14 @@ int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream) {
 
 int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* bulk, const int64_t* nflags,
                    const int64_t* dense, const int32_t* mode, int64_t* perf_step, int64_t* perf_cum,
-                   double* ff_last, double* ff_sum, void* stream) {
+                   double* ff_last, double* ff_sum, const evc_sp_node* sp_nodes, int32_t n_sp, void* stream) {
   EVC_CHECK_ARG(n > 0 && S > 0 && in_true && bulk && nflags && dense && mode && perf_step && perf_cum && ff_last &&
-                    ff_sum,
+                    ff_sum && n_sp >= 0 && (n_sp == 0 || sp_nodes),
                 "meter_step: null argument");
-  const int tot = n * S;
-  fz::k_meter_step<<<cdiv(tot, 128), 128, 0, as_stream(stream)>>>(
+  fz::k_meter_step<<<1 + n_sp, 256, 0, as_stream(stream)>>>(
       n, S, in_true, reinterpret_cast<const long long*>(bulk), reinterpret_cast<const long long*>(nflags),
       reinterpret_cast<const long long*>(dense), mode, reinterpret_cast<long long*>(perf_step),
-      reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum);
+      reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum, sp_nodes);
   EVC_LAUNCH_CHECK("meter_step");
   return EVC_OK;
 }

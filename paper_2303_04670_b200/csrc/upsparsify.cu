@@ -37,6 +37,9 @@ struct USArgs {
 __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
   __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ];
   __shared__ float s_y[8 * 32 * 33];
+  // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
+  __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8];
+  __shared__ float s_cw0[32], s_cw1[32], s_rw0[8], s_rw1[8];
   const TView& y = a.y;
   const int jc = blockIdx.x % a.nJC, rest = blockIdx.x / a.nJC;
   const int cg = rest % a.nCG, i = rest / a.nCG, s = blockIdx.y;
@@ -63,6 +66,33 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     s_nd[t] = 0;
     any |= pr != 0;
   }
+  if (threadIdx.x < ncol) {
+    const int v = x0 + threadIdx.x;
+    if (a.mode == 0) {
+      s_ci0[threadIdx.x] = s_ci1[threadIdx.x] = v / a.f;
+      s_cw0[threadIdx.x] = 1.0f;
+      s_cw1[threadIdx.x] = 0.0f;
+    } else {
+      const Tap t = bilinear_tap(v, a.x.W, a.f);
+      s_ci0[threadIdx.x] = t.i0;
+      s_ci1[threadIdx.x] = t.i1;
+      s_cw0[threadIdx.x] = t.w0;
+      s_cw1[threadIdx.x] = t.w1;
+    }
+  } else if (threadIdx.x >= 32 && threadIdx.x < 32 + nrow) {
+    const int r = threadIdx.x - 32, u = r0 + r;
+    if (a.mode == 0) {
+      s_ri0[r] = s_ri1[r] = u / a.f;
+      s_rw0[r] = 1.0f;
+      s_rw1[r] = 0.0f;
+    } else {
+      const Tap t = bilinear_tap(u, a.x.H, a.f);
+      s_ri0[r] = t.i0;
+      s_ri1[r] = t.i1;
+      s_rw0[r] = t.w0;
+      s_rw1[r] = t.w1;
+    }
+  }
   const bool active = __syncthreads_or(any) != 0;
   double ss = 0.0;
   const bool stage = a.hwc && nrow <= 8 && ncol <= 32;
@@ -71,17 +101,34 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     const bool use_k = kd > 0.0;
     const float k32 = __double2float_rn(kd);
     const int64_t HW = (int64_t)y.H * y.W;
-    const int n = nc * nrow * ncol;
-    for (int e = threadIdx.x; e < n; e += US_THREADS) {
-      const int xl = e % ncol, t2 = e / ncol;
-      const int r = t2 % nrow, cl = t2 / nrow;
-      const int ti = cl * nj + xl / y.tw;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // lane = output column (ncol <= 32), warps stride over (channel, row) pairs
+    const bool col_ok = lane < ncol;
+    const int xl = lane, jl_lane = lane / y.tw;
+    const int ci0 = col_ok ? s_ci0[xl] : 0, ci1 = col_ok ? s_ci1[xl] : 0;
+    const float cw0 = col_ok ? s_cw0[xl] : 0.0f, cw1 = col_ok ? s_cw1[xl] : 0.0f;
+    const int npair = nc * nrow;
+    for (int pr = warp; pr < npair; pr += US_THREADS / 32) {
+      const int cl = pr / nrow, r = pr - cl * nrow;
+      if (!col_ok) continue;
+      const int ti = cl * nj + jl_lane;
       if (!s_proc[ti]) {
         if (stage) s_y[(r * 32 + xl) * 33 + cl] = 0.0f;
         continue;
       }
       const int c = c0 + cl, u = r0 + r, v = x0 + xl;
-      const float up = upsample_at(a.x.plane(s, c), a.x.H, a.x.W, u, v, a.f, a.mode);
+      const float* xp = a.x.plane(s, c);
+      float up;
+      if (a.mode == 0) {
+        up = xp[(int64_t)s_ri0[r] * a.x.W + ci0];
+      } else {  // same float32 op order as upsample_at (rows first, then columns)
+        const float* xr0 = xp + (int64_t)s_ri0[r] * a.x.W;
+        const float* xr1 = xp + (int64_t)s_ri1[r] * a.x.W;
+        const float rw0 = s_rw0[r], rw1 = s_rw1[r];
+        const float ra = __fadd_rn(__fmul_rn(xr0[ci0], rw0), __fmul_rn(xr1[ci0], rw1));
+        const float rb = __fadd_rn(__fmul_rn(xr0[ci1], rw0), __fmul_rn(xr1[ci1], rw1));
+        up = __fadd_rn(__fmul_rn(ra, cw0), __fmul_rn(rb, cw1));
+      }
       const int64_t off = (int64_t)c * HW + (int64_t)u * y.W + v;
       float* dp = a.delta + (int64_t)s * a.ds + off;
       const float corr = a.delta_zero ? __fadd_rn(0.0f, up) : __fadd_rn(*dp, up);
@@ -109,7 +156,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       const int cl = t / nj, jl = t % nj;
       const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i) * y.GW + j0 + jl;
       y.f[(int64_t)s * y.fs + fo] = s_ny[t];
-      if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i) * y.GW + fo % y.GW] = 1;  // benign race: all store 1
+      if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i) * y.GW + j0 + jl] = 1;  // benign race: all store 1
       a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage) {
@@ -117,14 +164,15 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       for (int e = threadIdx.x; e < nrow * ncol * US_C; e += US_THREADS) {
         const int cl = e % US_C, pix = e / US_C;
         if (cl >= nc) continue;
-        const int r = pix / ncol, xl = pix % ncol;
-        dst[((int64_t)(r0 + r) * y.W + x0 + xl) * a.cp + c0 + cl] = s_y[(r * 32 + xl) * 33 + cl];
+        const int r = pix / ncol, xq = pix % ncol;
+        dst[((int64_t)(r0 + r) * y.W + x0 + xq) * a.cp + c0 + cl] = s_y[(r * 32 + xq) * 33 + cl];
       }
     }
   }
-  const int nblocks = gridDim.x * gridDim.y;
   ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
   if (threadIdx.x == 0) a.partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
+  if (!a.ticket) return;  // norm / k folded later by evc_meter_step (one launch for every node)
+  const int nblocks = gridDim.x * gridDim.y;
   __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -162,8 +210,9 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
                           uint8_t* dlive, const evc_tensor* y, double* k, double* norm_ema, double tp,
                           double ema_decay, double* partials, int32_t* ticket, float* hwc, int32_t cp,
                           int64_t hwc_stride, uint8_t* fany, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
-  EVC_CHECK_ARG(x && y && x->flags && y->flags && delta && dlive && k && norm_ema && partials && ticket && S > 0,
+  EVC_CHECK_ARG(x && y && x->flags && y->flags && delta && dlive && k && norm_ema && partials && S > 0,
                 "upsample_sparsify: null argument");
+  EVC_CHECK_ARG(y->tw <= 32 && y->th <= 8, "upsample_sparsify: tiles wider than 32 or taller than 8");
   EVC_CHECK_ARG(factor == 2 || factor == 4, "upsample_sparsify: factor must be 2 or 4");
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
   EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");

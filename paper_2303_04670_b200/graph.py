@@ -620,16 +620,21 @@ class Graph:
         for node in sp_nodes:
             up = self._by_id.get(node.spec.inputs[0])
             if (up is not None and up.kind == "upsample" and self._consumers[up.spec.id] == [node.spec.id]
-                    and up.spec.id not in self.output_ids):
+                    and up.spec.id not in self.output_ids and tile.w <= 32 and tile.h <= 8):
                 self._fused_up.add(up.spec.id)
-                max_part = max(max_part, int(self.lib.evc_upsample_sparsify_partials(self._desc(node.spec.id))))
+                node.nparts = int(self.lib.evc_upsample_sparsify_partials(self._desc(node.spec.id)))
+            else:
+                node.nparts = int(self.lib.evc_sparsify_partials(self._desc(node.spec.inputs[0])))
+        # per-node partial sums of the sparsify norms, folded by the end-of-step kernel
+        tot = sum(S * nd.nparts for nd in sp_nodes)
+        self._sp_partials = torch.zeros(max(tot, 1), dtype=torch.float64, device=dev)
         nm = max(len(meter_ids), 1)
         self._meter_ids = meter_ids
         self._meter_nodes = [self._by_id[i] for i in meter_ids]
         # per-step scratch zeroed by ONE memset at the start of every step (byte arena):
         # flag counts int32 (nm x S) | meter bulk int64 (nm x S) | performed int64 (nm x S) |
         # per unfused conv: tile count + mask scratch | per fused conv: any-channel tile map |
-        # per sparsify: retire ticket
+        # (sparsify nodes fold their norms in the end-of-step kernel: no retire tickets)
         off = [0]
 
         def take(nbytes, align=16):
@@ -646,16 +651,12 @@ class Graph:
                 else:
                     n = int(self.lib.evc_conv_mask_scratch(node.plan.g, S))
                     conv_off.append((node, take(8), take(4 * n)))
-            elif node.kind == "sparsify":
-                sp_off.append((node, take(8)))
         self._zero = torch.zeros(-(-off[0] // 16) * 16, dtype=torch.uint8, device=dev)
         base = self._zero.data_ptr()
         for node, c_off, s_off in conv_off:
             node.mask_scratch = (base + c_off, base + s_off)
         for node, o in fany_off:
             node.plan.fany_ptr = base + o
-        for node, o in sp_off:
-            node.ticket = base + o
         self._cnt_step = self._zero[o_cnt:o_cnt + 4 * nm * S].view(torch.int32).view(nm, S)
         self._bulk_step = self._zero[o_bulk:o_bulk + 8 * nm * S].view(torch.int64).view(nm, S)
         self._perf_step = self._zero[o_perf:o_perf + 8 * nm * S].view(torch.int64).view(nm, S)
@@ -677,6 +678,15 @@ class Graph:
         self._norm = torch.zeros((nsp, S), dtype=torch.float64, device=dev)
         self._k = torch.zeros((nsp, S), dtype=torch.float64, device=dev)
         self._partials = torch.zeros(S * max(max_part, 64), dtype=torch.float64, device=dev)
+        recs = (_lib.EvcSpNode * max(len(sp_nodes), 1))()
+        po = 0
+        for j, nd in enumerate(sp_nodes):
+            nd.part_ptr = self._sp_partials.data_ptr() + 8 * po
+            po += S * nd.nparts
+            recs[j] = _lib.EvcSpNode(nd.part_ptr, nd.nparts, self._norm.data_ptr() + 8 * j * S,
+                                     self._k.data_ptr() + 8 * j * S, nd.tp, nd.ema_decay)
+        raw = np.frombuffer(bytes(recs), dtype=np.uint8).copy()
+        self._sp_table = torch.from_numpy(raw).to(dev)
         self._tile_list = torch.zeros(max_T, dtype=torch.int32, device=dev)
         self._conv_ws = torch.zeros(max(max_ws, 1), dtype=torch.float32, device=dev)
         self._lin_ws = torch.zeros(lin_ws, dtype=torch.float32, device=dev)
@@ -778,7 +788,7 @@ class Graph:
                                                        node.dlive.data_ptr(), self._desc(nid),
                                                        self._k.data_ptr() + 8 * j * S,
                                                        self._norm.data_ptr() + 8 * j * S, node.tp, node.ema_decay,
-                                                       self._partials.data_ptr(), node.ticket, *hwc,
+                                                       node.part_ptr, None, *hwc,
                                                        0 if sh is not None else 1, 1 if node.tp == 0.0 else 0, S),
                              "upsample_sparsify"))
             elif k == "upsample" and nid in self._fused_up:
@@ -790,7 +800,7 @@ class Graph:
                 prog.append((L.evc_sparsify, (self._desc(ns.inputs[0]), node.delta.data_ptr(), node.delta[0].numel(),
                                               node.dlive.data_ptr(), self._desc(nid),
                                               self._k.data_ptr() + 8 * j * S, self._norm.data_ptr() + 8 * j * S,
-                                              node.tp, node.ema_decay, self._partials.data_ptr(), node.ticket,
+                                              node.tp, node.ema_decay, node.part_ptr, None,
                                               *hwc, 0 if sh is not None else 1,
                                               1 if node.tp == 0.0 else 0,  # k stays 0 -> residual stays 0
                                               S),
@@ -848,7 +858,8 @@ class Graph:
         _lib.check(self.lib.evc_meter_step(len(self._meter_ids) or 1, self.S, self._cnt_step.data_ptr(),
                                            self._bulk_step.data_ptr(), nflags.data_ptr(), dense.data_ptr(),
                                            mode.data_ptr(), self._perf_step.data_ptr(), self._perf_cum.data_ptr(),
-                                           self._ff_last.data_ptr(), self._ff_sum.data_ptr(), s), "meter_step")
+                                           self._ff_last.data_ptr(), self._ff_sum.data_ptr(),
+                                           self._sp_table.data_ptr(), len(self._sp_nodes), s), "meter_step")
 
     def dense_launches(self) -> int:
         """libevconv launches of the last dense pass (refresh), excluding torch memsets."""

@@ -70,6 +70,10 @@ const char* evc_last_error(void);
 /* Loads every kernel module and sets smem attributes (call once, outside
  * graph capture). */
 int evc_init(void);
+/* Programmatic dependent launch for the step kernels (default on): each kernel
+ * may start while its predecessor on the stream drains and waits on the device
+ * (griddepcontrol.wait) before reading upstream results.  0 = plain launches. */
+int evc_set_pdl(int32_t on);
 
 /* ---- tile masks (tensors.py) ------------------------------------------ */
 
@@ -134,9 +138,8 @@ int evc_conv_table_fill(const evc_conv_geom* g, int32_t* host_table);
  *    evc_conv_gemm; the GEMM result does not depend on list order),
  *  - meter[s] += performed FLOPs (int64, the exact reference meter).
  * With region_flags != NULL it also sets region_flags[s][ri*RWn + rj] = 1
- * for every 4x32 output region (evc_conv_region_grid) overlapping a live
- * tile: the work list of evc_conv_gemm_region.  tile_list/tile_count may be
- * NULL when only regions are wanted.
+ * for every 4x32 output region (rows of 4, columns of 32) overlapping a live
+ * tile.  tile_list/tile_count may be NULL when only regions are wanted.
  * scratch (evc_conv_mask_scratch int32 entries), in_true, tile_count and
  * region_flags must be zeroed before the call.  `table` is the device copy
  * of evc_conv_table_fill's output. */
@@ -147,26 +150,12 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
                   int32_t* tile_count, uint8_t* region_flags, int64_t* meter,
                   int32_t S, void* stream);
 
-/* TMA-fed tensor-core GEMM over 4x32 output regions (conv_tma.cu).  The
- * conv input is first mirrored into a channels-innermost shadow
- * (evc_to_hwc: element (s,y,x,c) at in_hwc[s*hwc_stride + (y*W + x)*cp + c],
- * cp = evc_hwc_channels(C_in)); the im2col A operand is then exactly four TMA
- * boxes per (tap, 32-channel) K-block, zero padding = TMA out-of-bounds fill.
- * Weights are packed by evc_conv_region_pack (K order: tap, then channel
- * padded to 32).  region_flags == NULL computes every region (dense pass). */
+/* Channels-innermost shadow of the conv input (hwc.cu): element (s,y,x,c) at
+ * in_hwc[s*hwc_stride + (y*W + x)*cp + c], cp = evc_hwc_channels(C_in); the
+ * A operand of evc_conv_fused is RH TMA boxes of it per (tap, 32-channel) K-block. */
 int32_t evc_hwc_channels(int32_t c);
 int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp,
                int32_t S, void* stream);
-int evc_conv_region_supported(const evc_conv_geom* g);
-int evc_conv_region_grid(const evc_conv_geom* g, int32_t* rh, int32_t* rw);
-int64_t evc_conv_region_pack_len(int32_t c_out, int32_t c_in, int32_t kh, int32_t kw);
-int evc_conv_region_pack(const float* w, int32_t c_out, int32_t c_in, int32_t kh,
-                         int32_t kw, float* out);
-int64_t evc_conv_region_workspace(const evc_conv_geom* g, int32_t S, int32_t splits);
-int evc_conv_gemm_region(const evc_conv_geom* g, const float* in_hwc, int32_t cp,
-                         int64_t hwc_stride, const float* wpack, const float* bias,
-                         const evc_tensor* out, const uint8_t* region_flags,
-                         int32_t S, int32_t splits, float* workspace, void* stream);
 
 /* ---- fused incremental convolution (conv_fused.cu) --------------------
  * inc_conv2d (increment_ops.py:126-194) in ONE launch: region test against the
@@ -206,6 +195,9 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                    int64_t* bulk, const evc_tensor* out, int32_t act, float alpha, float* acc,
                    int64_t acc_stride, const evc_tensor* act_out, int32_t dense, int32_t S,
                    void* stream);
+/* Debug: subsequent evc_conv_fused launches record per-CTA phase clocks into
+ * buf (16 uint64 per CTA, CTA index (z*gy + y)*gx + x); NULL turns it off. */
+int evc_conv_trace(void* buf);
 /* fany[s][t] = OR over channels of x's flags (input of a fused conv whose
  * producer does not emit the map). */
 int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream);

@@ -59,6 +59,7 @@ _PROTOS = {
     "evc_version": (_I32, []),
     "evc_last_error": (C.c_char_p, []),
     "evc_init": (_I32, []),
+    "evc_set_pdl": (_I32, [_I32]),
     "evc_diff_mask": (_I32, [_P, _P, _I64, _T, _I32, _P]),
     "evc_make_tile_mask": (_I32, [_T, _I32, _P]),
     "evc_compact_scratch": (_I64, [_I64]),
@@ -74,12 +75,6 @@ _PROTOS = {
     "evc_conv_mask": (_I32, [_G, _T, _T, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_hwc_channels": (_I32, [_I32]),
     "evc_to_hwc": (_I32, [_T, _P, _I64, _I32, _I32, _P]),
-    "evc_conv_region_supported": (_I32, [_G]),
-    "evc_conv_region_grid": (_I32, [_G, _P, _P]),
-    "evc_conv_region_pack_len": (_I64, [_I32, _I32, _I32, _I32]),
-    "evc_conv_region_pack": (_I32, [_P, _I32, _I32, _I32, _I32, _P]),
-    "evc_conv_region_workspace": (_I64, [_G, _I32, _I32]),
-    "evc_conv_gemm_region": (_I32, [_G, _P, _I32, _I64, _P, _P, _T, _P, _I32, _I32, _P, _P]),
     "evc_conv_fused_supported": (_I32, [_G]),
     "evc_conv_fused_config": (_I32, [_G, _I32, _I32, _CF]),
     "evc_conv_fused_pack_len": (_I64, [_G, _CF]),
@@ -88,6 +83,7 @@ _PROTOS = {
     "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
                               _I32, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
+    "evc_conv_trace": (_I32, [_P]),
     "evc_meter_step": (_I32, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
     "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),

@@ -13,7 +13,7 @@
 // intrinsics so no FMA contraction changes the reference's float32 rounding.
 //
 // The sparsify op can also emit the channels-innermost shadow that the TMA
-// conv GEMM reads (conv_tma.cu), staged through padded shared memory so the
+// conv GEMM reads (conv_fused.cu), staged through padded shared memory so the
 // planar reads and the 128-byte channel runs are both coalesced.
 
 #include "common.cuh"
@@ -116,6 +116,8 @@ struct Vec<1> {
 
 template <int OP, int V>
 __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
+  pdl_wait();
+  pdl_trigger();
   using VT = Vec<V>;
   using T = typename VT::T;
   __shared__ uint8_t s_proc[TB_C * TB_MAXJ];
@@ -267,8 +269,8 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
           if (p.hwc && !stage) {
 #pragma unroll
             for (int k = 0; k < V; ++k)
-              p.hwc[(int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * g.W + x0 + xl_[u] + k) * p.cp + c0 + cl_[u]] =
-                  VT::get(out, k);
+              hwc_store(p.hwc + (int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * g.W + x0 + xl_[u] + k) * 2 * p.cp, p.cp,
+                        c0 + cl_[u], VT::get(out, k));
           }
           if (!p.delta_zero) VT::st(p.acc2 + sacc + off[u], acc_new);
         }
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         const int cl = e % TB_C, pix = e / TB_C;
         if (cl >= nc) continue;
         const int r = pix / ncol, xl = pix % ncol;
-        dst[((int64_t)(r0 + r) * g.W + x0 + xl) * p.cp + c0 + cl] = s_y[(r * 32 + xl) * 33 + cl];
+        hwc_store(dst + ((int64_t)(r0 + r) * g.W + x0 + xl) * 2 * p.cp, p.cp, c0 + cl, s_y[(r * 32 + xl) * 33 + cl]);
       }
     }
   }
@@ -324,9 +326,9 @@ template <int OP>
 static void launch_op(const TBArgs& p, const TBGeo& g, int S, cudaStream_t st) {
   dim3 grid((unsigned)(g.GH * g.nCG * g.nJC), (unsigned)S);
   if (g.vec == 4)
-    k_tiles<OP, 4><<<grid, TB_THREADS, 0, st>>>(p, g);
+    launch_pdl(k_tiles<OP, 4>, dim3(grid), dim3(TB_THREADS), 0, st, p, g);
   else
-    k_tiles<OP, 1><<<grid, TB_THREADS, 0, st>>>(p, g);
+    launch_pdl(k_tiles<OP, 1>, dim3(grid), dim3(TB_THREADS), 0, st, p, g);
 }
 
 static int tb_launch(int op, const TBArgs& p, int S, cudaStream_t st) {
@@ -387,7 +389,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || cp >= dx->C, "sparsify: shadow channel stride too small");
+  EVC_CHECK_ARG(!hwc || (cp >= dx->C && cp % 32 == 0), "sparsify: shadow channel count must cover C, multiple of 32");
   TBArgs p = {};
   p.a = view_of(*dx);
   p.y = view_of(*y);

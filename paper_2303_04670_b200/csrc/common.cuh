@@ -32,6 +32,32 @@ void set_error(const std::string& msg);
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch (evc_set_pdl): step kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs may start
+// while its predecessor drains.  EVERY kernel launched that way executes pdl_wait()
+// before touching data an earlier kernel writes (which also keeps the dependency
+// transitive down the stream); pdl_trigger() lets the successor launch early.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// cudaLaunchKernelEx with the PDL attribute when enabled.
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 static inline int64_t cdiv64(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -116,6 +142,19 @@ __device__ __forceinline__ T block_sum(T v, F wsum) {
     r = wsum(r);
   }
   return r;
+}
+
+// Channels-innermost hi/lo shadow of a conv input (the TMA A operand of
+// conv_fused.cu): pixel p owns 2*cp floats, the TF32 head of channel c at
+// [p*2cp + c] and the tail x - head at [p*2cp + cp + c]; cp = channels padded to
+// a multiple of 32 so both 32-channel boxes start 128-byte aligned.
+__device__ __forceinline__ float tf32_head(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ void hwc_store(float* pix, int cp, int c, float x) {
+  const float h = tf32_head(x);
+  pix[c] = h;
+  pix[cp + c] = __fsub_rn(x, h);
 }
 
 // Activation f of inc_activation (tensors.py:285-312), float32 ops with the

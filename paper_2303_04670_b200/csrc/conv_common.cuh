@@ -52,6 +52,5 @@ int conv_tc_launch(const evc_conv_geom* g, const evc_tensor* in, const float* wp
                    const evc_tensor* out, const int32_t* table, const int32_t* tile_list, const int32_t* tile_count,
                    int32_t S, int32_t splits, float* workspace, cudaStream_t st);
 int init_conv_tc();
-int init_conv_tma();
 
 }  // namespace evc

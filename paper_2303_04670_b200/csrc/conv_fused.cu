@@ -12,10 +12,12 @@
 //    whose taps all read dead tiles are exactly zero (mask soundness), so a dead
 //    region is skipped -- or zeroed once when it was computed last step
 //    (`rstate`), which restores the exact-zero invariant of TileMask.
-//  * Live regions: K-block = one tap (r, s) x 32 channels; its A operand is RH TMA
-//    boxes of the channels-innermost shadow of the input (zero padding = TMA
-//    out-of-bounds fill).  3xTF32 (hi*hi + hi*lo + lo*hi, fp32 TMEM accumulation)
-//    keeps fp32-grade accuracy; weights are pre-split, pre-swizzled K-major images.
+//  * Live regions: K-block = one tap (r, s) x 32 channels; its A operand is two
+//    TMA boxes (TF32 heads, TF32 tails) of the channels-innermost hi/lo shadow of
+//    the input, each covering the whole RH x RW region (traversal stride = conv
+//    stride; zero padding = TMA out-of-bounds fill).  3xTF32 (hi*hi + hi*lo +
+//    lo*hi, fp32 TMEM accumulation) keeps fp32-grade accuracy; weights are
+//    pre-split, pre-swizzled K-major images.
 //  * Split-K runs across a thread-block cluster (grid z = cluster z = splits):
 //    each CTA parks its fp32 partial tile in shared memory and CTA rank r sums
 //    channel slice r over all ranks through DSMEM in rank order -- deterministic,
@@ -30,8 +32,7 @@
 //    `performed` (with the all-false / all-true shortcuts, increment_ops.py:148-154).
 //
 // Roles (8 warps): warp 0 = region test + TMA producer (lane 0); warp 1 = TMEM
-// alloc + MMA issuer (lane 0); warps 2-3 = flags + meter; warps 4-7 = hi/lo
-// split of each landed A stage, then the epilogue.
+// alloc + MMA issuer (lane 0); warps 2-3 = flags + meter; warps 4-7 = epilogue.
 
 #include <cooperative_groups.h>
 #include <cuda.h>
@@ -62,6 +63,20 @@ __device__ __forceinline__ void bar_arrive(uint32_t bar) {
 }
 __device__ __forceinline__ void bar_arrive_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// Latency-critical single-thread waits (producer / MMA issuer): spin on test_wait,
+// which never suspends the thread (try_wait may park it for a system-defined time).
+__device__ __forceinline__ void bar_spin(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "EVC_FS:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra EVC_FS;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -117,14 +132,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ float tf32_rn(float x) {
-  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct Args {
   int c_in, c_out, kh, kw, stride, pad, H, W, Ho, Wo, S;
   int RH, RW, RHn, RWn, cchunks, nkb, splits, kb_per_split, bn;
-  int th, tw;
+  int th, tw, cp;
   const float* wpack;
   const float* bias;
   // incremental mode (dense == 0)
@@ -147,7 +167,26 @@ struct Args {
   float* yact;
   int64_t yvs;
   int dense;
+  unsigned long long* trace;  // debug: per-CTA phase timestamps (evc_conv_trace), normally NULL
 };
+
+static unsigned long long* g_trace = nullptr;
+
+__device__ __forceinline__ unsigned long long clk() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TR(i)                                                                                              \
+  do {                                                                                                     \
+    if (a.trace)                                                                                           \
+      a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + (i)] = clk() - t_start; \
+  } while (0)
 
 // Flags + meter share of one CTA (q of Qs CTAs of session s; t = thread 0..63).
 // 32-bit indices: every per-session count here is far below 2^31.
@@ -258,17 +297,26 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
                                                            const __grid_constant__ Args a) {
   constexpr int NS = stages_of(BN);
   constexpr int STAGE = stage_bytes(BN);
-  // NA rotating "main" accumulators for hi*hi (one per K-block, round robin) + one
-  // for the small hi*lo + lo*hi corrections, summed in fp32 (RN) by the epilogue.
-  constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 3 : 4);
-  constexpr int NEED = (NA + 1) * BN;
+  // 3xTF32 with the fewest MMA instructions (tcgen05.mma costs ~62 cycles for any N <= 128):
+  //  CAT (BN <= 128): D_j[:, 0:2BN] += A_hi . [B_hi | B_lo]  (one MMA, N = 2 BN: hi*hi and hi*lo)
+  //                   D_c[:, 0:BN]  += A_lo . B_hi           (one MMA)
+  //  BN = 256:        hi*hi, hi*lo and lo*hi as three N = 256 MMAs (hi*lo + lo*hi share one accumulator)
+  // NA rotating accumulator blocks j = K-block mod NA shorten every fp32 accumulation chain; the
+  // epilogue sums all blocks in fp32 (RN), small terms first.
+  constexpr bool CAT = BN <= 128;
+  constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 1 : (BN >= 64 ? 3 : 4));
+  constexpr int NEED = CAT ? NA * 2 * BN + BN : 2 * BN;
   constexpr int TMEM_COLS = NEED <= 32 ? 32 : (NEED <= 64 ? 64 : (NEED <= 128 ? 128 : (NEED <= 256 ? 256 : 512)));
-  // kind::tf32, fp32 accumulate, A and B K-major, N = BN, M = 128
-  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                             ((uint32_t)(BM >> 4) << 24);
+  // kind::tf32, fp32 accumulate, A and B K-major, M = 128, N = BN or 2 BN
+  constexpr uint32_t IDESC_BASE = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BM >> 4) << 24);
+  constexpr uint32_t IDESC = IDESC_BASE | ((uint32_t)(BN >> 3) << 17);
+  constexpr uint32_t IDESC2 = IDESC_BASE | ((uint32_t)((CAT ? 2 * BN : BN) >> 3) << 17);
   constexpr uint32_t A_BYTES = BM * 128;
   constexpr uint32_t B_BYTES = 2 * BN * 128;
 
+  const unsigned long long t_start = clk();
+  if (a.trace && threadIdx.x == 0)
+    a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + 15] = gtime();
   const int R = a.RHn * a.RWn;
   const int reg = blockIdx.x;  // s * R + region
   const int s = reg / R, rr = reg % R;
@@ -276,17 +324,48 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
   const int nblk = blockIdx.y, z = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t rs_idx = (int64_t)reg * gridDim.y + nblk;
+  const int kb0 = z * a.kb_per_split, kb1 = min(a.nkb, kb0 + a.kb_per_split), nk = kb1 - kb0;
+  const int npre = min(NS, nk);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[NS], split[NS], empty[NS], acc
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3 * NS + 1);
-  int* s_flag = reinterpret_cast<int*>(tslot + 1);  // [0] live, [1] computed last step
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[NS], empty[NS], acc
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 1);
+  volatile int* s_flag = reinterpret_cast<volatile int*>(tslot + 1);  // [0] live, [1] computed last step
   const uint32_t sb = su32(smem), b0 = su32(bars);
   auto tma_bar = [&](int i) { return b0 + 8u * i; };
-  auto split_bar = [&](int i) { return b0 + 8u * (NS + i); };
-  auto empty_bar = [&](int i) { return b0 + 8u * (2 * NS + i); };
-  const uint32_t acc_bar = b0 + 8u * (3 * NS);
+  auto empty_bar = [&](int i) { return b0 + 8u * (NS + i); };
+  const uint32_t acc_bar = b0 + 8u * (2 * NS);
+  const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
+
+  // ---- prologue that reads nothing an upstream kernel writes: under programmatic
+  // dependent launch it overlaps the previous kernel's tail
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      bar_init(tma_bar(i), 1);
+      bar_init(empty_bar(i), 1);
+    }
+    bar_init(acc_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    // the first stages' weights are static: stream them now (their arrive comes with the A boxes)
+    for (int i = 0; i < npre; ++i) {
+      bar_expect_tx(tma_bar(i), B_BYTES);
+      bulk_load(sb + i * STAGE + 2 * A_BYTES, wsrc + (int64_t)(kb0 + i) * B_BYTES, B_BYTES, tma_bar(i));
+    }
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  pdl_trigger();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  if (threadIdx.x == 0) TR(2);
+  pdl_wait();  // upstream results (input shadow, flags, fany, accumulators) are visible from here
 
   // ---- region test: OR of the any-channel input tile map over the receptive box
   if (warp == 0) {
@@ -309,19 +388,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
     if (lane == 0) {
       s_flag[0] = live;
       s_flag[1] = a.dense ? 0 : a.rstate[rs_idx];
-      if (live) {
-        for (int i = 0; i < NS; ++i) {
-          bar_init(tma_bar(i), 1);
-          bar_init(split_bar(i), 128);
-          bar_init(empty_bar(i), 1);
-        }
-        bar_init(acc_bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-      }
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) TR(1);
   const bool live = s_flag[0] != 0;
   const int Qs = R * gridDim.y * gridDim.z;
   const int q = ((int)blockIdx.z * (int)gridDim.y + nblk) * R + rr;
@@ -340,59 +410,77 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
       }
       if (threadIdx.x == 0) a.rstate[rs_idx] = 0;
     }
+    if (threadIdx.x == 0) {  // drain the prefetched weight copies before the shared memory is released
+      for (int i = 0; i < npre; ++i) {
+        bar_arrive(tma_bar(i));
+        bar_wait(tma_bar(i), 0);
+      }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 1) {
+      fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    }
     return;
   }
   if (!a.dense && z == 0 && threadIdx.x == 0 && !s_flag[1]) a.rstate[rs_idx] = 1;
 
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tslot;
-  const int kb0 = z * a.kb_per_split, kb1 = min(a.nkb, kb0 + a.kb_per_split), nk = kb1 - kb0;
-
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
-      const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
-      const uint32_t box_bytes = (uint32_t)a.RW * 128u;
       for (int i = 0; i < nk; ++i) {
         const int st = i % NS;
-        bar_wait(empty_bar(st), ((i / NS) & 1) ^ 1);
         const int kb = kb0 + i;
         const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
         const int r = tap / a.kw, qq = tap % a.kw;
         const uint32_t abuf = sb + st * STAGE;
-        bar_arrive_tx(tma_bar(st), A_BYTES + B_BYTES);
-        for (int hh = 0; hh < a.RH; ++hh)
-          tma_load_4d(abuf + hh * box_bytes, &tmap, c0, v0 * a.stride - a.pad + qq, (u0 + hh) * a.stride - a.pad + r,
-                      s, tma_bar(st));
-        bulk_load(abuf + 2 * A_BYTES, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
+        if (i < npre) {
+          bar_arrive_tx(tma_bar(st), 2 * A_BYTES);  // weights already in flight
+        } else {
+          bar_spin(empty_bar(st), ((i / NS) & 1) ^ 1);
+          bar_arrive_tx(tma_bar(st), 2 * A_BYTES + B_BYTES);
+          bulk_load(abuf + 2 * A_BYTES, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
+        }
+        // one box = the whole RH x RW region for this tap: TF32 heads, then tails, of the shadow
+        const int xs = v0 * a.stride - a.pad + qq, ys = u0 * a.stride - a.pad + r;
+        tma_load_4d(abuf, &tmap, c0, xs, ys, s, tma_bar(st));
+        tma_load_4d(abuf + A_BYTES, &tmap, a.cp + c0, xs, ys, s, tma_bar(st));
+        if (i == 0) TR(3);
       }
+      TR(11);
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       for (int i = 0; i < nk; ++i) {
         const int st = i % NS;
-        bar_wait(split_bar(st), (i / NS) & 1);
+        bar_spin(tma_bar(st), (i / NS) & 1);
         fence_after();
         const uint32_t ah = sb + st * STAGE, al = ah + A_BYTES;
         const uint32_t bh = ah + 2 * A_BYTES, bl = bh + BN * 128;
-        const uint32_t tmain = tmem + (uint32_t)((i % NA) * BN), tcorr = tmem + (uint32_t)(NA * BN);
+        if (CAT) {
+          const uint32_t tj = tmem + (uint32_t)((i % NA) * 2 * BN), tc = tmem + (uint32_t)(NA * 2 * BN);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
-          mma(tmain, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i >= NA || kk) ? 1u : 0u);
-          mma(tcorr, desc_k(ah + ko), desc_k(bl + ko), IDESC, (i | kk) ? 1u : 0u);
-          mma(tcorr, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
+            mma(tj, desc_k(ah + ko), desc_k(bh + ko), IDESC2, (i >= NA || kk) ? 1u : 0u);  // [hi*hi | hi*lo]
+            mma(tc, desc_k(al + ko), desc_k(bh + ko), IDESC, (i | kk) ? 1u : 0u);          // lo*hi
+          }
+        } else {
+          const uint32_t tmain = tmem, tcorr = tmem + (uint32_t)BN;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t ko = kk * 32;
+            mma(tmain, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i | kk) ? 1u : 0u);
+            mma(tcorr, desc_k(ah + ko), desc_k(bl + ko), IDESC, (i | kk) ? 1u : 0u);
+            mma(tcorr, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
+          }
         }
         commit(empty_bar(st));
+        if (i == 0) TR(12);
       }
       commit(acc_bar);
+      TR(5);
     }
     __syncwarp();
   } else if (warp < 4) {
@@ -411,49 +499,59 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
         }
       }
       side_work(a, s, q, Qs, threadIdx.x - 64);
+      if (threadIdx.x == 64) TR(10);
     }
   } else {
-    // ------------------------------------------------------------- hi/lo split
-    const int t = threadIdx.x - 128;  // 0..127
-    for (int i = 0; i < nk; ++i) {
-      const int st = i % NS;
-      bar_wait(tma_bar(st), (i / NS) & 1);
-      float4* ah = reinterpret_cast<float4*>(smem + st * STAGE);
-      float4* al = reinterpret_cast<float4*>(smem + st * STAGE + A_BYTES);
-#pragma unroll
-      for (int e = 0; e < (int)(A_BYTES / 16 / 128); ++e) {
-        const int idx = t + e * 128;
-        const float4 x = ah[idx];
-        float4 hv, lv;
-        hv.x = tf32_rn(x.x);
-        hv.y = tf32_rn(x.y);
-        hv.z = tf32_rn(x.z);
-        hv.w = tf32_rn(x.w);
-        lv.x = __fsub_rn(x.x, hv.x);
-        lv.y = __fsub_rn(x.y, hv.y);
-        lv.z = __fsub_rn(x.z, hv.z);
-        lv.w = __fsub_rn(x.w, hv.w);
-        ah[idx] = hv;
-        al[idx] = lv;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bar_arrive(split_bar(st));
-    }
     // ------------------------------------------------------------- epilogue (TMEM -> values)
     const int m = 32 * (warp & 3) + lane;  // TMEM lane = region site
     bar_wait(acc_bar, 0);
     fence_after();
+    if (threadIdx.x == 128) TR(6);
     const int n_main = nk < NA ? nk : NA;
     const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     float* P = reinterpret_cast<float*>(smem);  // [BN][BM] partial tile (split-K only)
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
-      float vals[16], part[16];
-      tmem_ld16(trow + (uint32_t)(NA * BN + c0), vals);  // corrections
-      for (int j = 0; j < n_main; ++j) {
-        tmem_ld16(trow + (uint32_t)(j * BN + c0), part);
+      float vals[16];
+      {  // corrections first (small terms), then the main products
+        uint32_t r[NA + 1][16];
+        const uint32_t cbase = CAT ? (uint32_t)(NA * 2 * BN) : (uint32_t)BN;
+        tmem_ld16_issue(trow + cbase + (uint32_t)c0, r[NA]);
+        if (CAT) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], part[e]);
+          for (int j = 0; j < NA; ++j) tmem_ld16_issue(trow + (uint32_t)(j * 2 * BN + BN + c0), r[j]);
+        }
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j <= NA; ++j)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));  // uses stay after the wait
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vals[e] = __uint_as_float(r[NA][e]);
+        if (CAT) {
+#pragma unroll
+          for (int j = 0; j < NA; ++j)
+            if (j < n_main) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], __uint_as_float(r[j][e]));
+            }
+        }
+      }
+      {
+        uint32_t r[NA][16];
+#pragma unroll
+        for (int j = 0; j < NA; ++j) tmem_ld16_issue(trow + (uint32_t)(j * (CAT ? 2 * BN : BN) + c0), r[j]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < NA; ++j)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
+#pragma unroll
+        for (int j = 0; j < NA; ++j)
+          if (j < n_main) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], __uint_as_float(r[j][e]));
+          }
       }
       if (a.splits == 1) {
         const int n0 = nblk * BN + c0;
@@ -464,9 +562,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
       }
     }
   }
+  if (threadIdx.x == 128) TR(7);
   if (a.splits > 1) {
     // deterministic split-K: rank r sums channel slice r over all ranks in rank order
     cluster_sync();
+    if (threadIdx.x == 0) TR(8);
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int nsp = a.splits;
@@ -475,27 +575,35 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
     const int lo = rank * per, hi = min(BN, lo + per);
     float* P = reinterpret_cast<float*>(smem);
     const int m = threadIdx.x % BM, g = threadIdx.x / BM;  // 2 channel groups of 128 sites
-    constexpr int NB = 4;
+    constexpr int NB = 2;
     for (int nl0 = lo + g; nl0 < hi; nl0 += 2 * NB) {
       const int cnt = min(NB, (hi - nl0 + 1) / 2);
+      float t[16][NB];  // every rank's partials first (latencies overlap), then the ordered sum
+#pragma unroll
+      for (int zz = 0; zz < 16; ++zz) {
+        if (zz < nsp) {
+          const float* Rz = cl.map_shared_rank(P, zz);
+#pragma unroll
+          for (int j = 0; j < NB; ++j) t[zz][j] = j < cnt ? Rz[(nl0 + 2 * j) * BM + m] : 0.0f;
+        }
+      }
       float sum[NB];
 #pragma unroll
-      for (int j = 0; j < NB; ++j) sum[j] = 0.0f;
-      for (int zz = 0; zz < nsp; ++zz) {
-        const float* R = cl.map_shared_rank(P, zz);
-        float t[NB];
+      for (int j = 0; j < NB; ++j) {
+        sum[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < NB; ++j) t[j] = j < cnt ? R[(nl0 + 2 * j) * BM + m] : 0.0f;
-#pragma unroll
-        for (int j = 0; j < NB; ++j) sum[j] = __fadd_rn(sum[j], t[j]);
+        for (int zz = 0; zz < 16; ++zz)
+          if (zz < nsp) sum[j] = __fadd_rn(sum[j], t[zz][j]);
       }
       const int n0 = nblk * BN + nl0;
       emit<NB>(a, s, u0, v0, m, n0, 2, min(cnt, (a.c_out - n0 + 1) / 2), sum);
     }
     cluster_sync();
   }
+  if (threadIdx.x == 128) TR(9);
   fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TR(13);
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
@@ -504,6 +612,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
 
 // any-channel tile map: fany[s][t] = OR_c flags[s][c][t]
 __global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
+  pdl_wait();
+  pdl_trigger();
   const int Ti = x.GH * x.GW;
   const int s = blockIdx.y;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Ti; t += gridDim.x * blockDim.x) {
@@ -527,6 +637,8 @@ __global__ void __launch_bounds__(256) k_meter_step(int n, int S, const int32_t*
                                                     const int32_t* __restrict__ mode, long long* perf_step,
                                                     long long* perf_cum, double* ff_last, double* ff_sum,
                                                     const evc_sp_node* __restrict__ sp) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x > 0) {
     const evc_sp_node nd = sp[blockIdx.x - 1];
     sparsify_finalize_all(nd.partials, nd.n, nd.norm_ema, nd.k, nd.tp, nd.decay, 0, S);
@@ -571,13 +683,22 @@ static cudaError_t launch(const CUtensorMap& m, const Args& a, cudaStream_t st) 
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem_bytes(BN);
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = (unsigned)a.splits;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (a.splits > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 1;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = (unsigned)a.splits;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = a.splits > 1 ? 1 : 0;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, k_conv_fused<BN>, m, a);
 }
 
@@ -660,7 +781,7 @@ int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_c
           const float x = (n < c_out && c < c_in) ? w[((n * c_in + c) * kh + r) * kw + q] : 0.0f;
           uint32_t bits;
           memcpy(&bits, &x, 4);
-          bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32 (as tf32_rn)
+          bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32 (as tf32_head, common.cuh)
           float hv;
           memcpy(&hv, &bits, 4);
           // 128B swizzle: 16-byte chunk j of row `row` lives at chunk (j ^ (row & 7))
@@ -687,10 +808,10 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   EVC_CHECK_ARG(g && cfg && in_hwc && wpack && S > 0 && fz::valid_bn(cfg->bn), "conv_fused: null argument");
   EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
   EVC_CHECK_ARG(cfg->rh * cfg->rw == fz::BM && (cfg->rw == 32 || cfg->rw == 16 || cfg->rw == 8) &&
-                    cfg->rw * g->stride <= 256,
+                    cfg->rw * g->stride <= 256 && cfg->rh * g->stride <= 256,
                 "conv_fused: bad region shape");
   EVC_CHECK_ARG(cfg->splits >= 1 && cfg->splits <= 16, "conv_fused: splits must lie in [1, 16]");
-  EVC_CHECK_ARG(cp % 4 == 0 && cp >= g->c_in && hwc_stride % 4 == 0, "conv_fused: shadow not 16B aligned");
+  EVC_CHECK_ARG(cp % 32 == 0 && cp >= g->c_in && hwc_stride % 32 == 0, "conv_fused: shadow layout (cp % 32)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && act_out->vals && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || act >= 0, "conv_fused: no output");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && in_true && bulk &&
@@ -698,10 +819,10 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                 "conv_fused: incremental mode needs masks, fany, table, rstate and counters");
   fz::EncodeTiled enc = fz::encoder();
   CUtensorMap map;
-  const cuuint64_t dims[4] = {(cuuint64_t)cp, (cuuint64_t)g->W, (cuuint64_t)g->H, (cuuint64_t)S};
-  const cuuint64_t strides[3] = {(cuuint64_t)cp * 4, (cuuint64_t)g->W * cp * 4, (cuuint64_t)hwc_stride * 4};
-  const cuuint32_t box[4] = {32, (cuuint32_t)(cfg->rw * g->stride), 1, 1};
-  const cuuint32_t estr[4] = {1, (cuuint32_t)g->stride, 1, 1};
+  const cuuint64_t dims[4] = {(cuuint64_t)(2 * cp), (cuuint64_t)g->W, (cuuint64_t)g->H, (cuuint64_t)S};
+  const cuuint64_t strides[3] = {(cuuint64_t)cp * 8, (cuuint64_t)g->W * cp * 8, (cuuint64_t)hwc_stride * 4};
+  const cuuint32_t box[4] = {32, (cuuint32_t)(cfg->rw * g->stride), (cuuint32_t)(cfg->rh * g->stride), 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)g->stride, (cuuint32_t)g->stride, 1};
   CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in_hwc), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -734,9 +855,11 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   a.bn = cfg->bn;
   a.th = g->th;
   a.tw = g->tw;
+  a.cp = cp;
   a.wpack = wpack;
   a.bias = bias;
   a.dense = dense != 0;
+  a.trace = fz::g_trace;
   if (!a.dense) {
     const TView vin = view_of(*in);
     a.fany = fany;
@@ -775,11 +898,16 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   return EVC_OK;
 }
 
+int evc_conv_trace(void* buf) {
+  fz::g_trace = reinterpret_cast<unsigned long long*>(buf);
+  return EVC_OK;
+}
+
 int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream) {
   EVC_CHECK_ARG(x && x->flags && fany && S > 0, "tile_any: null argument");
   TView v = view_of(*x);
   const int Ti = v.GH * v.GW;
-  fz::k_tile_any<<<dim3(cdiv(Ti, 128), S), 128, 0, as_stream(stream)>>>(v, fany);
+  launch_pdl(fz::k_tile_any, dim3(dim3(cdiv(Ti, 128), S)), dim3(128), 0, as_stream(stream), v, fany);
   EVC_LAUNCH_CHECK("tile_any");
   return EVC_OK;
 }
@@ -790,7 +918,7 @@ int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* 
   EVC_CHECK_ARG(n > 0 && S > 0 && in_true && bulk && nflags && dense && mode && perf_step && perf_cum && ff_last &&
                     ff_sum && n_sp >= 0 && (n_sp == 0 || sp_nodes),
                 "meter_step: null argument");
-  fz::k_meter_step<<<1 + n_sp, 256, 0, as_stream(stream)>>>(
+  launch_pdl(fz::k_meter_step, dim3(1 + n_sp), dim3(256), 0, as_stream(stream), 
       n, S, in_true, reinterpret_cast<const long long*>(bulk), reinterpret_cast<const long long*>(nflags),
       reinterpret_cast<const long long*>(dense), mode, reinterpret_cast<long long*>(perf_step),
       reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum, sp_nodes);

@@ -36,6 +36,8 @@ constexpr int BK = 8;
 
 template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_conv_gemm(GemmArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NT = (BM / TM) * (BN / TN);
   constexpr int A_PER = BM * BK / NT;
   constexpr int B_PER = (BN * BK + NT - 1) / NT;
@@ -183,6 +185,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) k_conv_gemm(GemmArgs a)
 
 // deterministic split-K reduction + scatter
 __global__ void k_conv_splitk_reduce(GemmArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int th = a.out.th, tw = a.out.tw, sites = th * tw;
   const int n_tiles = a.list ? *a.count : a.S * a.T;
   const int64_t M = (int64_t)n_tiles * sites;
@@ -207,7 +211,7 @@ __global__ void k_conv_splitk_reduce(GemmArgs a) {
 template <int BM, int BN, int TM, int TN>
 static int launch_gemm(const GemmArgs& a, int64_t max_m, cudaStream_t st) {
   dim3 grid((unsigned)cdiv64(max_m, BM), (unsigned)cdiv(a.c_out, BN), (unsigned)a.splits);
-  k_conv_gemm<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(a);
+  launch_pdl(k_conv_gemm<BM, BN, TM, TN>, dim3(grid), dim3((BM / TM) * (BN / TN)), 0, st, a);
   return 0;
 }
 
@@ -270,7 +274,7 @@ int evc_conv_gemm(const evc_conv_geom* g, const evc_tensor* in, const float* wei
   if (a.splits > 1) {
     const int64_t work = max_m * g->c_out;
     const int blocks = (int)std::min<int64_t>(cdiv64(work, 256), 148 * 8);
-    k_conv_splitk_reduce<<<blocks, 256, 0, st>>>(a);
+    launch_pdl(k_conv_splitk_reduce, dim3(blocks), dim3(256), 0, st, a);
     EVC_LAUNCH_CHECK("conv_splitk_reduce");
   }
   return EVC_OK;
@@ -284,7 +288,6 @@ int init_conv() {
   if (cudaFuncGetAttributes(&fa, k_conv_splitk_reduce) != cudaSuccess) return EVC_ECUDA;
   int rc = init_conv_mask();
   if (!rc) rc = init_conv_tc();
-  if (!rc) rc = init_conv_tma();
   return rc ? rc : init_conv_fused();
 }
 }  // namespace evc

@@ -142,6 +142,8 @@ struct MaskArgs {
 constexpr int kCountThreads = 256;
 
 __global__ void __launch_bounds__(kCountThreads) k_conv_count(MaskArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const TabHdr& h = *reinterpret_cast<const TabHdr*>(a.tab);
   const int Ti = h.GHi * h.GWi;
   const int s = blockIdx.y;
@@ -196,6 +198,8 @@ __global__ void __launch_bounds__(kCountThreads) k_conv_count(MaskArgs a) {
 
 // One warp per (output tile, session).
 __global__ void __launch_bounds__(256) k_conv_flags(MaskArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const TabHdr& h = *reinterpret_cast<const TabHdr*>(a.tab);
   const int To = h.GHo * h.GWo, Ti = h.GHi * h.GWi;
   const int lane = threadIdx.x & 31;
@@ -303,9 +307,9 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in, const evc_tensor
   a.nb_count = (int)cdiv64((int64_t)g->c_in * h.GHi * h.GWi, kCountThreads);
   const int nb_border = (int)cdiv64((int64_t)ngrp * g->c_in, kCountThreads);
   cudaStream_t st = as_stream(stream);
-  k_conv_count<<<dim3(a.nb_count + nb_border, S), kCountThreads, 0, st>>>(a);
+  launch_pdl(k_conv_count, dim3(dim3(a.nb_count + nb_border, S)), dim3(kCountThreads), 0, st, a);
   EVC_LAUNCH_CHECK("conv_count");
-  k_conv_flags<<<dim3(cdiv(h.GHo * h.GWo, 8), S), 256, 0, st>>>(a);
+  launch_pdl(k_conv_flags, dim3(dim3(cdiv(h.GHo * h.GWo, 8), S)), dim3(256), 0, st, a);
   EVC_LAUNCH_CHECK("conv_flags");
   return EVC_OK;
 }

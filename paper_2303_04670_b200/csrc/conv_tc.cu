@@ -136,6 +136,8 @@ struct TcArgs {
 
 template <int BN>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(TcArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NS = tc_stages(BN);
   constexpr int STAGE = tc_stage_bytes(BN);
   constexpr int TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_conv_tc(TcArgs a) {
 template <int BN>
 static int launch_tc(const TcArgs& a, int64_t max_m, int n_blocks, cudaStream_t st) {
   dim3 grid((unsigned)cdiv64(max_m, TC_BM), (unsigned)n_blocks, (unsigned)a.splits);
-  k_conv_tc<BN><<<grid, TC_THREADS, tc_smem_bytes(BN), st>>>(a);
+  launch_pdl(k_conv_tc<BN>, dim3(grid), dim3(TC_THREADS), tc_smem_bytes(BN), st, a);
   return 0;
 }
 

@@ -26,6 +26,8 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
 
 __global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __restrict__ y, int64_t ys,
                             float* __restrict__ acc, int64_t as, int64_t n, int kind, float alpha) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const float v = x[(int64_t)s * xs + e];
@@ -37,10 +39,14 @@ __global__ void k_act_dense(const float* __restrict__ x, int64_t xs, float* __re
 
 __global__ void k_sparsify_finalize(const double* __restrict__ partials, int64_t n, double* norm_ema, double* kdev,
                                     double tp, double decay, int reset, int S) {
+  pdl_wait();
+  pdl_trigger();
   sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, reset, S);
 }
 
 __global__ void k_sumsq(const float* __restrict__ x, int64_t xs, int64_t n, double* partials) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   double ss = 0.0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -56,6 +62,8 @@ __global__ void k_sumsq(const float* __restrict__ x, int64_t xs, int64_t n, doub
 
 __global__ void k_binary_dense(const float* __restrict__ a, int64_t as, const float* __restrict__ b, int64_t bs,
                                float* __restrict__ y, int64_t ys, int64_t n, int op) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const float va = a[(int64_t)s * as + e], vb = b[(int64_t)s * bs + e];
@@ -68,6 +76,8 @@ __global__ void k_binary_dense(const float* __restrict__ a, int64_t as, const fl
 // ---------------------------------------------------------------------------
 
 __global__ void k_upsample(TView in, TView out, int f, int mode) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t s_m[];  // proc | new (2 x GWo)
   const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
   const bool masked = in.f != nullptr;
@@ -146,6 +156,8 @@ __device__ __forceinline__ bool pool_covers(int a, int o0, int o1, int st, int w
 }
 
 __global__ void k_maxpool(TView in, const float* __restrict__ acc, int64_t as, TView out, int wh, int ww, int st) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t s_m[];
   const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
   const bool masked = in.f != nullptr;
@@ -220,7 +232,7 @@ int evc_fold(const evc_tensor* dx, float* acc, int64_t acc_stride, int32_t S, vo
 int evc_act_dense(const float* x, int64_t xs, float* y, int64_t ys, float* acc, int64_t as, int64_t n, int32_t kind,
                   float alpha, int32_t S, void* stream) {
   EVC_CHECK_ARG(x && y && S > 0, "act_dense: null argument");
-  k_act_dense<<<dim3(dense_blocks(n), S), 256, 0, as_stream(stream)>>>(x, xs, y, ys, acc, as, n, kind, alpha);
+  launch_pdl(k_act_dense, dim3(dim3(dense_blocks(n), S)), dim3(256), 0, as_stream(stream), x, xs, y, ys, acc, as, n, kind, alpha);
   EVC_LAUNCH_CHECK("act_dense");
   return EVC_OK;
 }
@@ -228,7 +240,7 @@ int evc_act_dense(const float* x, int64_t xs, float* y, int64_t ys, float* acc, 
 int evc_sparsify_finalize(const double* partials, int64_t n, double* norm_ema, double* k, double tp, double decay,
                           int32_t reset, int32_t S, void* stream) {
   EVC_CHECK_ARG(partials && norm_ema && k && S > 0, "sparsify_finalize: null argument");
-  k_sparsify_finalize<<<1, 256, 0, as_stream(stream)>>>(partials, n, norm_ema, k, tp, decay, reset, S);
+  launch_pdl(k_sparsify_finalize, dim3(1), dim3(256), 0, as_stream(stream), partials, n, norm_ema, k, tp, decay, reset, S);
   EVC_LAUNCH_CHECK("sparsify_finalize");
   return EVC_OK;
 }
@@ -236,7 +248,7 @@ int evc_sparsify_finalize(const double* partials, int64_t n, double* norm_ema, d
 int evc_sumsq_dense(const float* x, int64_t xs, int64_t n, double* partials, int32_t n_blocks, int32_t S,
                     void* stream) {
   EVC_CHECK_ARG(x && partials && n_blocks > 0 && S > 0, "sumsq_dense: null argument");
-  k_sumsq<<<dim3(n_blocks, S), 256, 0, as_stream(stream)>>>(x, xs, n, partials);
+  launch_pdl(k_sumsq, dim3(dim3(n_blocks, S)), dim3(256), 0, as_stream(stream), x, xs, n, partials);
   EVC_LAUNCH_CHECK("sumsq_dense");
   return EVC_OK;
 }
@@ -244,7 +256,7 @@ int evc_sumsq_dense(const float* x, int64_t xs, int64_t n, double* partials, int
 int evc_binary_dense(const float* a, int64_t as, const float* b, int64_t bs, float* y, int64_t ys, int64_t n,
                      int32_t op, int32_t S, void* stream) {
   EVC_CHECK_ARG(a && b && y && S > 0, "binary_dense: null argument");
-  k_binary_dense<<<dim3(dense_blocks(n), S), 256, 0, as_stream(stream)>>>(a, as, b, bs, y, ys, n, op);
+  launch_pdl(k_binary_dense, dim3(dim3(dense_blocks(n), S)), dim3(256), 0, as_stream(stream), a, as, b, bs, y, ys, n, op);
   EVC_LAUNCH_CHECK("binary_dense");
   return EVC_OK;
 }
@@ -256,7 +268,7 @@ int evc_upsample(const evc_tensor* in, const evc_tensor* out, int32_t factor, in
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample: unknown mode");
   EVC_CHECK_ARG((in->flags == nullptr) == (out->flags == nullptr), "upsample: masks on both or neither");
   TView vi = view_of(*in), vo = view_of(*out);
-  k_upsample<<<dim3(vo.GH, vo.C, S), bt(vo.W), 2 * vo.GW, as_stream(stream)>>>(vi, vo, factor, mode);
+  launch_pdl(k_upsample, dim3(dim3(vo.GH, vo.C, S)), dim3(bt(vo.W)), 2 * vo.GW, as_stream(stream), vi, vo, factor, mode);
   EVC_LAUNCH_CHECK("upsample");
   return EVC_OK;
 }
@@ -268,7 +280,7 @@ int evc_maxpool(const evc_tensor* in, float* acc, int64_t acc_stride, const evc_
   EVC_CHECK_ARG(!acc || in->flags, "maxpool: incremental mode needs masks");
   TView vi = view_of(*in), vo = view_of(*out);
   cudaStream_t st = as_stream(stream);
-  k_maxpool<<<dim3(vo.GH, vo.C, S), bt(vo.W), 2 * vo.GW, st>>>(vi, acc, acc_stride, vo, wh, ww, stride);
+  launch_pdl(k_maxpool, dim3(dim3(vo.GH, vo.C, S)), dim3(bt(vo.W)), 2 * vo.GW, st, vi, acc, acc_stride, vo, wh, ww, stride);
   EVC_LAUNCH_CHECK("maxpool");
   if (acc) return evc_fold(in, acc, acc_stride, S, stream);  // AccState.fold (increment_ops.py:93-94)
   return EVC_OK;

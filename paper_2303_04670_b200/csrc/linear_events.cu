@@ -25,6 +25,8 @@ __global__ void __launch_bounds__(256) k_linear_partial(const float* __restrict_
                                                         int chunk, const float* __restrict__ Wt, int F, int dense,
                                                         const uint8_t* __restrict__ runflags, int64_t rfs,
                                                         float* __restrict__ part, int64_t* meter) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float s_x[];
   __shared__ int s_live_elems;
   const int b = blockIdx.x, s = blockIdx.y;
@@ -73,6 +75,8 @@ __global__ void __launch_bounds__(256) k_linear_partial(const float* __restrict_
 
 __global__ void k_linear_reduce(const float* __restrict__ part, int nchunks, int F, const float* __restrict__ bias,
                                 float* __restrict__ y, int64_t ys, uint8_t* flags, int64_t fs) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
     float acc = 0.0f;
@@ -90,6 +94,8 @@ __global__ void k_linear_reduce(const float* __restrict__ part, int nchunks, int
 __global__ void k_event_keys(const uint16_t* __restrict__ x, const uint16_t* __restrict__ y,
                              const int8_t* __restrict__ p, int64_t lo, int n, int H, int W, int kind,
                              uint32_t* keys, int32_t* vals) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t e = lo + i;
@@ -102,6 +108,8 @@ __global__ void k_event_keys(const uint16_t* __restrict__ x, const uint16_t* __r
 __global__ void k_event_runs(const uint64_t* __restrict__ t, const int8_t* __restrict__ p,
                              const uint32_t* __restrict__ keys, const int32_t* __restrict__ ev, int n, int64_t t0,
                              int64_t delta, int HW, int kind, int bins, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t key = keys[i];
@@ -178,11 +186,11 @@ int evc_linear(const evc_tensor* in, const float* weight, const float* bias, con
   const int chunk = lin_chunk(run);
   const int nchunks = (int)cdiv64(L, chunk);
   cudaStream_t st = as_stream(stream);
-  k_linear_partial<<<dim3(nchunks, S), 256, chunk * sizeof(float), st>>>(in->vals, in->vstride, L, run, chunk,
+  launch_pdl(k_linear_partial, dim3(dim3(nchunks, S)), dim3(256), chunk * sizeof(float), st, in->vals, in->vstride, L, run, chunk,
                                                                          weight, F, dense, in->flags, in->fstride,
                                                                          workspace, meter);
   EVC_LAUNCH_CHECK("linear_partial");
-  k_linear_reduce<<<dim3(cdiv(F, 128), S), 128, 0, st>>>(workspace, nchunks, F, dense ? bias : nullptr, out->vals,
+  launch_pdl(k_linear_reduce, dim3(dim3(cdiv(F, 128), S)), dim3(128), 0, st, workspace, nchunks, F, dense ? bias : nullptr, out->vals,
                                                         out->vstride, out->flags, out->fstride);
   EVC_LAUNCH_CHECK("linear_reduce");
   return EVC_OK;
@@ -227,14 +235,14 @@ int evc_bin_events(const uint64_t* t, const uint16_t* x, const uint16_t* y, cons
   int32_t* v_out = reinterpret_cast<int32_t*>(ws + 3 * a);
   void* temp = ws + 4 * a;
   size_t temp_bytes = cub_temp_bytes(n, end_bit);
-  k_event_keys<<<cdiv(n, 256), 256, 0, st>>>(x, y, p, lo, n, H, W, kind, k_in, v_in);
+  launch_pdl(k_event_keys, dim3(cdiv(n, 256)), dim3(256), 0, st, x, y, p, lo, n, H, W, kind, k_in, v_in);
   EVC_LAUNCH_CHECK("event_keys");
   err = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, n, 0, end_bit, st);
   if (err != cudaSuccess) {
     set_error(std::string("evc: bin_events sort: ") + cudaGetErrorString(err));
     return EVC_ECUDA;
   }
-  k_event_runs<<<cdiv(n, 256), 256, 0, st>>>(t, p, k_out, v_out, n, tau - delta, delta, H * W, kind, bins, out);
+  launch_pdl(k_event_runs, dim3(cdiv(n, 256)), dim3(256), 0, st, t, p, k_out, v_out, n, tau - delta, delta, H * W, kind, bins, out);
   EVC_LAUNCH_CHECK("event_runs");
   return EVC_OK;
 }

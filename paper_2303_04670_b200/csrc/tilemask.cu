@@ -15,11 +15,16 @@ namespace evc {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
+static bool g_pdl = true;
+bool pdl_enabled() { return g_pdl; }
+
 // ---------------------------------------------------------------------------
 // step_increment + make_tile_mask  (events.py:295-302, tensors.py:93-107)
 // ---------------------------------------------------------------------------
 __global__ void k_diff_mask(const float* __restrict__ prev, const float* __restrict__ cur,
                             int64_t in_stride, TView o) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t s_nz[];
   const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
   for (int j = threadIdx.x; j < o.GW; j += blockDim.x) s_nz[j] = 0;
@@ -43,6 +48,8 @@ __global__ void k_diff_mask(const float* __restrict__ prev, const float* __restr
 }
 
 __global__ void k_make_mask(TView o) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t s_nz[];
   const int i = blockIdx.x, c = blockIdx.y, s = blockIdx.z;
   for (int j = threadIdx.x; j < o.GW; j += blockDim.x) s_nz[j] = 0;
@@ -92,6 +99,8 @@ __device__ __forceinline__ int block_excl_scan(int v, int* s_warp, int* total) {
 }
 
 __global__ void k_compact_count(const uint8_t* __restrict__ flags, int64_t n, int32_t* counts) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t base = (int64_t)blockIdx.x * kCompactChunk;
   int cnt = 0;
 #pragma unroll
@@ -107,6 +116,8 @@ __global__ void k_compact_count(const uint8_t* __restrict__ flags, int64_t n, in
 
 __global__ void k_compact_write(const uint8_t* __restrict__ flags, int64_t n, const int32_t* counts,
                                 int32_t* idx, int32_t* count) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ int s_w[32];
   __shared__ int s_off;
   // offset = sum of counts of previous blocks (deterministic order)
@@ -149,6 +160,8 @@ __global__ void k_compact_write(const uint8_t* __restrict__ flags, int64_t n, co
 // counts of True flags per session
 // ---------------------------------------------------------------------------
 __global__ void k_count_flags(TView t, int32_t* counts) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   const int64_t n = (int64_t)t.C * t.GH * t.GW;
   const uint8_t* f = t.f + (int64_t)s * t.fs;
@@ -163,6 +176,8 @@ __global__ void k_count_flags(TView t, int32_t* counts) {
 
 __global__ void k_copy_dense(const float* __restrict__ a, int64_t as, float* __restrict__ b, int64_t bs,
                              int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     b[(int64_t)s * bs + e] = a[(int64_t)s * as + e];
@@ -170,6 +185,8 @@ __global__ void k_copy_dense(const float* __restrict__ a, int64_t as, float* __r
 
 __global__ void k_max_abs_diff(const float* __restrict__ a, int64_t as, const float* __restrict__ b, int64_t bs,
                                int64_t n, float* out) {
+  pdl_wait();
+  pdl_trigger();
   const int s = blockIdx.y;
   float m = 0.0f;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
@@ -197,7 +214,7 @@ int evc_diff_mask(const float* prev, const float* cur, int64_t in_stride, const 
   EVC_CHECK_ARG(out && out->vals && out->flags && prev && cur && S > 0, "diff_mask: null argument");
   TView o = view_of(*out);
   dim3 grid(o.GH, o.C, S);
-  k_diff_mask<<<grid, band_threads(o.W), o.GW, as_stream(stream)>>>(prev, cur, in_stride, o);
+  launch_pdl(k_diff_mask, dim3(grid), dim3(band_threads(o.W)), o.GW, as_stream(stream), prev, cur, in_stride, o);
   EVC_LAUNCH_CHECK("diff_mask");
   return EVC_OK;
 }
@@ -206,7 +223,7 @@ int evc_make_tile_mask(const evc_tensor* t, int32_t S, void* stream) {
   EVC_CHECK_ARG(t && t->vals && t->flags && S > 0, "make_tile_mask: null argument");
   TView o = view_of(*t);
   dim3 grid(o.GH, o.C, S);
-  k_make_mask<<<grid, band_threads(o.W), o.GW, as_stream(stream)>>>(o);
+  launch_pdl(k_make_mask, dim3(grid), dim3(band_threads(o.W)), o.GW, as_stream(stream), o);
   EVC_LAUNCH_CHECK("make_tile_mask");
   return EVC_OK;
 }
@@ -217,8 +234,8 @@ int evc_compact(const uint8_t* flags, int64_t n, int32_t* idx, int32_t* count, i
   EVC_CHECK_ARG(flags && idx && count && scratch && n >= 0, "compact: null argument");
   const int nb = (int)evc_compact_scratch(n);
   cudaStream_t st = as_stream(stream);
-  k_compact_count<<<nb, kCompactThreads, 0, st>>>(flags, n, scratch);
-  k_compact_write<<<nb, kCompactThreads, 0, st>>>(flags, n, scratch, idx, count);
+  launch_pdl(k_compact_count, dim3(nb), dim3(kCompactThreads), 0, st, flags, n, scratch);
+  launch_pdl(k_compact_write, dim3(nb), dim3(kCompactThreads), 0, st, flags, n, scratch, idx, count);
   EVC_LAUNCH_CHECK("compact");
   return EVC_OK;
 }
@@ -228,7 +245,7 @@ int evc_count_flags(const evc_tensor* t, int32_t S, int32_t* counts, void* strea
   TView v = view_of(*t);
   const int64_t n = (int64_t)v.C * v.GH * v.GW;
   const int blocks = (int)std::min<int64_t>(cdiv64(n, 256 * 4), 64);
-  k_count_flags<<<dim3(blocks > 0 ? blocks : 1, S), 256, 0, as_stream(stream)>>>(v, counts);
+  launch_pdl(k_count_flags, dim3(dim3(blocks > 0 ? blocks : 1, S)), dim3(256), 0, as_stream(stream), v, counts);
   EVC_LAUNCH_CHECK("count_flags");
   return EVC_OK;
 }
@@ -238,7 +255,7 @@ int evc_copy_dense(const float* src, int64_t src_stride, float* dst, int64_t dst
   EVC_CHECK_ARG(src && dst && S > 0 && n >= 0, "copy_dense: null argument");
   if (n == 0) return EVC_OK;
   const int blocks = (int)std::min<int64_t>(cdiv64(n, 256 * 4), 1024);
-  k_copy_dense<<<dim3(blocks, S), 256, 0, as_stream(stream)>>>(src, src_stride, dst, dst_stride, n);
+  launch_pdl(k_copy_dense, dim3(dim3(blocks, S)), dim3(256), 0, as_stream(stream), src, src_stride, dst, dst_stride, n);
   EVC_LAUNCH_CHECK("copy_dense");
   return EVC_OK;
 }
@@ -248,7 +265,7 @@ int evc_max_abs_diff(const float* a, int64_t as, const float* b, int64_t bs, int
   EVC_CHECK_ARG(a && b && out && S > 0, "max_abs_diff: null argument");
   if (n == 0) return EVC_OK;
   const int blocks = (int)std::min<int64_t>(cdiv64(n, 256 * 4), 512);
-  k_max_abs_diff<<<dim3(blocks, S), 256, 0, as_stream(stream)>>>(a, as, b, bs, n, out);
+  launch_pdl(k_max_abs_diff, dim3(dim3(blocks, S)), dim3(256), 0, as_stream(stream), a, as, b, bs, n, out);
   EVC_LAUNCH_CHECK("max_abs_diff");
   return EVC_OK;
 }
@@ -262,6 +279,11 @@ int init_masks() {
   return EVC_OK;
 }
 }  // namespace evc
+
+extern "C" int evc_set_pdl(int32_t on) {
+  evc::g_pdl = on != 0;
+  return EVC_OK;
+}
 
 extern "C" int evc_init(void) {
   int rc = evc::init_masks();

@@ -35,6 +35,8 @@ struct USArgs {
 };
 
 __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ];
   __shared__ float s_y[8 * 32 * 33];
   // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       if (stage) {
         s_y[(r * 32 + xl) * 33 + cl] = o;
       } else if (a.hwc) {
-        a.hwc[(int64_t)s * a.hs + ((int64_t)u * y.W + v) * a.cp + c] = o;
+        hwc_store(a.hwc + (int64_t)s * a.hs + ((int64_t)u * y.W + v) * 2 * a.cp, a.cp, c, o);
       }
       if (!a.delta_zero) *dp = nd;
       ss += (double)corr * (double)corr;
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
         const int cl = e % US_C, pix = e / US_C;
         if (cl >= nc) continue;
         const int r = pix / ncol, xq = pix % ncol;
-        dst[((int64_t)(r0 + r) * y.W + x0 + xq) * a.cp + c0 + cl] = s_y[(r * 32 + xq) * 33 + cl];
+        hwc_store(dst + ((int64_t)(r0 + r) * y.W + x0 + xq) * 2 * a.cp, a.cp, c0 + cl, s_y[(r * 32 + xq) * 33 + cl]);
       }
     }
   }
@@ -217,6 +219,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
   EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");
   EVC_CHECK_ARG(write_chw || hwc, "upsample_sparsify: no output requested");
+  EVC_CHECK_ARG(!hwc || (cp >= y->C && cp % 32 == 0), "upsample_sparsify: shadow channel count must cover C, multiple of 32");
   USArgs a;
   a.x = view_of(*x);
   a.y = view_of(*y);
@@ -239,7 +242,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.mode = mode;
   us_grid(a.y, a.CW, a.nCG, a.nJC);
   dim3 grid((unsigned)(a.y.GH * a.nCG * a.nJC), (unsigned)S);
-  k_up_sparsify<<<grid, US_THREADS, 0, as_stream(stream)>>>(a);
+  launch_pdl(k_up_sparsify, dim3(grid), dim3(US_THREADS), 0, as_stream(stream), a);
   EVC_LAUNCH_CHECK("upsample_sparsify");
   return EVC_OK;
 }

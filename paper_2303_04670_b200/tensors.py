@@ -286,7 +286,7 @@ class ConvPlan:
         if kernel == "tc" and lib.evc_conv_fused_supported(self.g):
             self.path = "fused"
             self.cp = int(lib.evc_hwc_channels(c_in))
-            self.hwc = torch.zeros((S, h, w, self.cp), dtype=torch.float32, device=weight.device)
+            self.hwc = torch.zeros((S, h, w, 2 * self.cp), dtype=torch.float32, device=weight.device)  # heads | tails
             self.cfg = _lib.EvcConvCfg()
             _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
             host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)

@@ -70,9 +70,10 @@ const char* evc_last_error(void);
 /* Loads every kernel module and sets smem attributes (call once, outside
  * graph capture). */
 int evc_init(void);
-/* Programmatic dependent launch for the step kernels (default on): each kernel
+/* Programmatic dependent launch for the step kernels: each kernel
  * may start while its predecessor on the stream drains and waits on the device
- * (griddepcontrol.wait) before reading upstream results.  0 = plain launches. */
+ * (griddepcontrol.wait) before reading upstream results.  Default off:
+ * CUDA-graph replay already hides the launch latency (measured). */
 int evc_set_pdl(int32_t on);
 
 /* ---- tile masks (tensors.py) ------------------------------------------ */

@@ -139,6 +139,8 @@ def load(require_cuda: bool = True):
                 raise RuntimeError("paper_2303_04670_b200 needs a CUDA device (B200); there is no CPU fallback")
             torch.cuda.init()
             check(_lib.evc_init(), "evc_init")
+            import os
+            _lib.evc_set_pdl(1 if os.environ.get("EVC_PDL", "0") == "1" else 0)
             _initialized = True
         return _lib
 

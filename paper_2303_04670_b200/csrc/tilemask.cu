@@ -15,7 +15,7 @@ namespace evc {
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
-static bool g_pdl = true;
+static bool g_pdl = false;
 bool pdl_enabled() { return g_pdl; }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,2 @@
+python scripts/step_breakdown.py --sessions 1 > gpurun_out/brk_s1.txt 2>&1
+python scripts/step_breakdown.py --sessions 32 > gpurun_out/brk_s32.txt 2>&1

@@ -291,14 +291,12 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         p.y.f[(int64_t)s * p.y.fs + fo] = p.a.f[(int64_t)s * p.a.fs + fo] | p.b.f[(int64_t)s * p.b.fs + fo];
       }
     }
-    if (stage) {  // channels-innermost shadow: 32-channel runs per pixel
-      float* dst = p.hwc + (int64_t)s * p.hs;
-      for (int e = threadIdx.x; e < nrow * ncol * TB_C; e += TB_THREADS) {
-        const int cl = e % TB_C, pix = e / TB_C;
-        if (cl >= nc) continue;
-        const int r = pix / ncol, xl = pix % ncol;
-        hwc_store(dst + ((int64_t)(r0 + r) * g.W + x0 + xl) * 2 * p.cp, p.cp, c0 + cl, s_y[(r * 32 + xl) * 33 + cl]);
-      }
+    if (stage && (int)(threadIdx.x & 31) < nc) {  // lane = channel: 128-byte runs of heads and tails per pixel
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * g.W * 2 * p.cp + c0 + lane;
+      for (int r = 0; r < nrow; ++r)
+        for (int xl = warp; xl < ncol; xl += TB_THREADS / 32)
+          hwc_store(dst + ((int64_t)r * g.W + x0 + xl) * 2 * p.cp, p.cp, 0, s_y[(r * 32 + xl) * 33 + lane]);
     }
   }
   if (OP == OP_SPARSIFY) {

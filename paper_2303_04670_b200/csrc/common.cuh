@@ -247,5 +247,6 @@ int init_conv_mask();
 int init_conv_fused();
 int init_elementwise();
 int init_bands();
+int init_upsparsify();
 int init_linear_events();
 }  // namespace evc

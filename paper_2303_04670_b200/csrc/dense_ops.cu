@@ -292,6 +292,7 @@ namespace evc {
 int init_elementwise() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k_sumsq) != cudaSuccess) return EVC_ECUDA;
-  return init_bands();
+  const int rc = init_upsparsify();
+  return rc ? rc : init_bands();
 }
 }  // namespace evc

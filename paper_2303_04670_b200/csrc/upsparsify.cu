@@ -31,6 +31,7 @@ struct USArgs {
   int64_t hs;
   uint8_t* fany;  // optional any-channel tile map of y (OR-accumulated, zeroed per step)
   int cp, write_chw, delta_zero, f, mode;
+  int XR, XC;  // staged input footprint (rows, cols) per CTA
   int CW, nCG, nJC;
 };
 
@@ -38,7 +39,9 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ];
-  __shared__ float s_y[8 * 32 * 33];
+  extern __shared__ float us_dyn[];
+  float* s_y = us_dyn;                // [(row * 32 + col) * 33 + channel] staged output (shadow transpose)
+  float* s_x = us_dyn + 8 * 32 * 33;  // [channel][XR][XC] input footprint of this CTA
   // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
   __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8];
   __shared__ float s_cw0[32], s_cw1[32], s_rw0[8], s_rw1[8];
@@ -104,14 +107,23 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     const float k32 = __double2float_rn(kd);
     const int64_t HW = (int64_t)y.H * y.W;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // lane = output column (ncol <= 32), warps stride over (channel, row) pairs
+    // stage the CTA's input footprint (all channels of the group) in shared memory:
+    // every global load is issued up front, the upsample then reads shared memory
+    const int rlo = s_ri0[0], nr = s_ri1[nrow - 1] - rlo + 1;
+    const int clo = s_ci0[0], ncl = s_ci1[ncol - 1] - clo + 1;
+    for (int e = threadIdx.x; e < nc * nr * ncl; e += US_THREADS) {
+      const int cc = e % ncl, t2 = e / ncl;
+      const int rr = t2 % nr, cl = t2 / nr;
+      s_x[(cl * a.XR + rr) * a.XC + cc] = a.x.plane(s, c0 + cl)[(int64_t)(rlo + rr) * a.x.W + clo + cc];
+    }
+    __syncthreads();
+    // lane = output column (ncol <= 32); warp w owns channels w, w + 8, ...
     const bool col_ok = lane < ncol;
     const int xl = lane, jl_lane = lane / y.tw;
-    const int ci0 = col_ok ? s_ci0[xl] : 0, ci1 = col_ok ? s_ci1[xl] : 0;
+    const int ci0 = col_ok ? s_ci0[xl] - clo : 0, ci1 = col_ok ? s_ci1[xl] - clo : 0;
     const float cw0 = col_ok ? s_cw0[xl] : 0.0f, cw1 = col_ok ? s_cw1[xl] : 0.0f;
-    const int npair = nc * nrow;
-    for (int pr = warp; pr < npair; pr += US_THREADS / 32) {
-      const int cl = pr / nrow, r = pr - cl * nrow;
+    for (int cl = warp; cl < nc; cl += US_THREADS / 32)
+    for (int r = 0; r < nrow; ++r) {
       if (!col_ok) continue;
       const int ti = cl * nj + jl_lane;
       if (!s_proc[ti]) {
@@ -119,13 +131,12 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
         continue;
       }
       const int c = c0 + cl, u = r0 + r, v = x0 + xl;
-      const float* xp = a.x.plane(s, c);
+      const float* xr0 = s_x + (cl * a.XR + s_ri0[r] - rlo) * a.XC;
       float up;
       if (a.mode == 0) {
-        up = xp[(int64_t)s_ri0[r] * a.x.W + ci0];
+        up = xr0[ci0];
       } else {  // same float32 op order as upsample_at (rows first, then columns)
-        const float* xr0 = xp + (int64_t)s_ri0[r] * a.x.W;
-        const float* xr1 = xp + (int64_t)s_ri1[r] * a.x.W;
+        const float* xr1 = s_x + (cl * a.XR + s_ri1[r] - rlo) * a.XC;
         const float rw0 = s_rw0[r], rw1 = s_rw1[r];
         const float ra = __fadd_rn(__fmul_rn(xr0[ci0], rw0), __fmul_rn(xr1[ci0], rw1));
         const float rb = __fadd_rn(__fmul_rn(xr0[ci1], rw0), __fmul_rn(xr1[ci1], rw1));
@@ -161,14 +172,11 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i) * y.GW + j0 + jl] = 1;  // benign race: all store 1
       a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
-    if (stage) {
-      float* dst = a.hwc + (int64_t)s * a.hs;
-      for (int e = threadIdx.x; e < nrow * ncol * US_C; e += US_THREADS) {
-        const int cl = e % US_C, pix = e / US_C;
-        if (cl >= nc) continue;
-        const int r = pix / ncol, xq = pix % ncol;
-        hwc_store(dst + ((int64_t)(r0 + r) * y.W + x0 + xq) * 2 * a.cp, a.cp, c0 + cl, s_y[(r * 32 + xq) * 33 + cl]);
-      }
+    if (stage && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
+      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * y.W * 2 * a.cp + c0 + lane;
+      for (int r = 0; r < nrow; ++r)
+        for (int xq = warp; xq < ncol; xq += US_THREADS / 32)
+          hwc_store(dst + ((int64_t)r * y.W + x0 + xq) * 2 * a.cp, a.cp, 0, s_y[(r * 32 + xq) * 33 + lane]);
     }
   }
   ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
@@ -186,6 +194,12 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     __threadfence();
     sparsify_finalize_all(a.partials, gridDim.x, a.norm_ema, a.k, a.tp, a.decay, 0, gridDim.y);
   }
+}
+
+int init_upsparsify() {
+  return cudaFuncSetAttribute(k_up_sparsify, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) == cudaSuccess
+             ? EVC_OK
+             : EVC_ECUDA;
 }
 
 static void us_grid(const TView& y, int& CW, int& nCG, int& nJC) {
@@ -242,7 +256,10 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.mode = mode;
   us_grid(a.y, a.CW, a.nCG, a.nJC);
   dim3 grid((unsigned)(a.y.GH * a.nCG * a.nJC), (unsigned)S);
-  launch_pdl(k_up_sparsify, dim3(grid), dim3(US_THREADS), 0, as_stream(stream), a);
+  a.XR = y->th / factor + 3;
+  a.XC = a.CW / factor + 3;
+  const size_t smem = sizeof(float) * (8 * 32 * 33 + (size_t)US_C * a.XR * a.XC);
+  launch_pdl(k_up_sparsify, dim3(grid), dim3(US_THREADS), smem, as_stream(stream), a);
   EVC_LAUNCH_CHECK("upsample_sparsify");
   return EVC_OK;
 }

@@ -187,15 +187,33 @@ int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg
  * sparsify), table = evc_conv_table_fill output; in_true[s] (int32) and bulk[s]
  * (int64) are ACCUMULATED (zero them per step) and resolved by evc_meter_step.
  * Output flags are written to act_out when act >= 0, else to out.
- * out may be NULL when act >= 0 (the conv values are then not materialised).
+ * out may be NULL when act >= 0 (the conv values are then not materialised);
+ * act_out->vals may be NULL when sp != NULL (the activation is only read through
+ * the fused sparsify).
  * Dense mode (dense != 0): every region, bias added; with act >= 0 the
  * activation y = f(x) is written to act_out and acc = x when acc != NULL. */
+/* Optional fused sparsify_step at t_p = 0 (sparsify.py:54-78) of the conv (or fused
+ * activation) output, when that sparsify's only reader is another fused conv: the
+ * epilogue writes that conv's hi/lo shadow, the sparsify's per-channel tile flags and
+ * the any-channel map (both must be zeroed per step; only ever set to 1), and one
+ * sum of squares per CTA (partials[s * evc_conv_fused_ctas(g, cfg) + cta]) for the
+ * deferred norm fold of evc_meter_step. */
+typedef struct evc_conv_sparsify {
+  float* hwc;
+  int64_t hwc_stride;
+  int32_t cp;
+  uint8_t* flags;
+  int64_t fstride;
+  uint8_t* fany;
+  double* partials;
+} evc_conv_sparsify;
+int64_t evc_conv_fused_ctas(const evc_conv_geom* g, const evc_conv_cfg* cfg); /* per session */
 int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
                    int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
                    const uint8_t* fany, const int32_t* table, uint8_t* rstate, int32_t* in_true,
                    int64_t* bulk, const evc_tensor* out, int32_t act, float alpha, float* acc,
-                   int64_t acc_stride, const evc_tensor* act_out, int32_t dense, int32_t S,
-                   void* stream);
+                   int64_t acc_stride, const evc_tensor* act_out, const evc_conv_sparsify* sp,
+                   int32_t dense, int32_t S, void* stream);
 /* Debug: subsequent evc_conv_fused launches record per-CTA phase clocks into
  * buf (16 uint64 per CTA, CTA index (z*gy + y)*gx + x); NULL turns it off. */
 int evc_conv_trace(void* buf);

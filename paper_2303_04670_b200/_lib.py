@@ -41,6 +41,11 @@ class EvcConvCfg(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits")]
 
 
+class EvcConvSparsify(C.Structure):
+    _fields_ = [("hwc", C.c_void_p), ("hwc_stride", C.c_int64), ("cp", C.c_int32), ("flags", C.c_void_p),
+                ("fstride", C.c_int64), ("fany", C.c_void_p), ("partials", C.c_void_p)]
+
+
 class EvcSpNode(C.Structure):
     _fields_ = [("partials", C.c_void_p), ("n", C.c_int64), ("norm_ema", C.c_void_p), ("k", C.c_void_p),
                 ("tp", C.c_double), ("decay", C.c_double)]
@@ -54,6 +59,7 @@ _D = C.c_double
 _T = C.POINTER(EvcTensor)
 _G = C.POINTER(EvcConvGeom)
 _CF = C.POINTER(EvcConvCfg)
+_SP = C.POINTER(EvcConvSparsify)
 
 _PROTOS = {
     "evc_version": (_I32, []),
@@ -80,8 +86,9 @@ _PROTOS = {
     "evc_conv_fused_pack_len": (_I64, [_G, _CF]),
     "evc_conv_fused_pack": (_I32, [_P, _G, _CF, _P]),
     "evc_conv_fused_state_len": (_I64, [_G, _CF, _I32]),
+    "evc_conv_fused_ctas": (_I64, [_G, _CF]),
     "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
-                              _I32, _I32, _P]),
+                              _SP, _I32, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
     "evc_conv_trace": (_I32, [_P]),
     "evc_meter_step": (_I32, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),

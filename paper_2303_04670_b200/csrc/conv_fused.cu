@@ -167,6 +167,15 @@ struct Args {
   float* yact;
   int64_t yvs;
   int dense;
+  // fused t_p = 0 sparsify of the output (the next conv's input): hi/lo shadow, per-channel
+  // flags and any-channel map (both zeroed per step), per-CTA sums of squares [S][CTAs/session]
+  float* sp_hwc;
+  int64_t sp_hs;
+  int sp_cp, sp_GH, sp_GW;
+  uint8_t* sp_flags;
+  int64_t sp_fs;
+  uint8_t* sp_fany;
+  double* sp_part;
   unsigned long long* trace;  // debug: per-CTA phase timestamps (evc_conv_trace), normally NULL
 };
 
@@ -251,46 +260,98 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
 
 // Final values of N channels (n0, n0 + step, ...) of output site m (region row-major):
 // every global load is issued before any store so the latencies overlap.
+// Final values of N channels (n0, n0 + step, ...) of output site m (region row-major).
+// Every global load is issued before any store so the latencies overlap.  Called by
+// every lane of a warp with warp-uniform (n0, step, cnt): the fused sparsify uses
+// warp ballots.  Returns the site's sum of squared sparsify outputs (0 if unfused).
 template <int N>
-__device__ __forceinline__ void emit(const Args& a, int s, int u0, int v0, int m, int n0, int step, int cnt,
-                                     const float* vals) {
+__device__ __forceinline__ double emit(const Args& a, int s, int u0, int v0, int m, int n0, int step, int cnt,
+                                       const float* vals) {
   const int u = u0 + m / a.RW, x = v0 + m % a.RW;
-  if (u >= a.Ho || x >= a.Wo) return;
+  const bool valid = u < a.Ho && x < a.Wo;
   const int64_t plane = (int64_t)a.Ho * a.Wo;
   const int64_t base = (int64_t)n0 * plane + (int64_t)u * a.Wo + x;
   const int64_t dn = (int64_t)step * plane;
-  float v[N], acc0[N];
+  float v[N], y[N];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     v[j] = vals[j];
-    if (j < cnt && a.dense && a.bias) v[j] = __fadd_rn(v[j], __ldg(a.bias + n0 + j * step));
+    if (valid && j < cnt && a.dense && a.bias) v[j] = __fadd_rn(v[j], __ldg(a.bias + n0 + j * step));
+    y[j] = v[j];
   }
-  if (a.out) {
+  if (valid && a.out) {
     float* __restrict__ o = a.out + (int64_t)s * a.ovs + base;
 #pragma unroll
     for (int j = 0; j < N; ++j)
       if (j < cnt) o[j * dn] = v[j];
   }
-  if (a.act < 0) return;
-  float* __restrict__ ap = a.acc ? a.acc + (int64_t)s * a.accs + base : nullptr;
-  float* __restrict__ yp = a.yact + (int64_t)s * a.yvs + base;
-  if (!a.dense) {
+  if (valid && a.act >= 0) {
+    float* __restrict__ ap = a.acc ? a.acc + (int64_t)s * a.accs + base : nullptr;
+    float* __restrict__ yp = a.yact ? a.yact + (int64_t)s * a.yvs + base : nullptr;
+    float acc0[N];
+    if (!a.dense) {
 #pragma unroll
-    for (int j = 0; j < N; ++j) acc0[j] = j < cnt ? ap[j * dn] : 0.0f;
+      for (int j = 0; j < N; ++j) acc0[j] = j < cnt ? ap[j * dn] : 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      if (j >= cnt) continue;
+      if (a.dense) {
+        y[j] = act_f(v[j], a.act, a.alpha);
+        if (ap) ap[j * dn] = v[j];
+      } else {
+        const float a1 = __fadd_rn(acc0[j], v[j]);
+        y[j] = __fsub_rn(act_f(a1, a.act, a.alpha), act_f(acc0[j], a.act, a.alpha));
+        ap[j * dn] = a1;
+      }
+      if (yp) yp[j * dn] = y[j];
+    }
+  }
+  if (!a.sp_hwc) return 0.0;
+  // fused sparsify_step at t_p = 0 (sparsify.py:63-71): out = 0 + y, residual stays 0; the mask is
+  // recomputed from the values (sparsify.py:77-78) -- one flag store per (tile, channel) per warp
+  double ss = 0.0;
+  const int lane = threadIdx.x & 31;
+  const int tile = valid ? (u / a.th) * a.sp_GW + x / a.tw : -1;
+  const unsigned grp = __match_any_sync(0xffffffffu, tile);
+  const bool leader = valid && (__ffs(grp) - 1) == lane;
+  float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.Wo + x) * 2 * a.sp_cp;
+  const int64_t To = (int64_t)a.sp_GH * a.sp_GW;
+  uint8_t* fl = a.sp_flags + (int64_t)s * a.sp_fs + tile;
+  bool any = false;
+  float o[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) o[j] = __fadd_rn(0.0f, y[j]);
+  if (N % 4 == 0 && step == 1 && cnt == N && (n0 & 3) == 0 && (a.sp_cp & 3) == 0) {
+    if (valid) {  // 16-byte runs of heads and tails
+#pragma unroll
+      for (int j = 0; j < N; j += 4) {
+        const float4 h = make_float4(tf32_head(o[j]), tf32_head(o[j + 1]), tf32_head(o[j + 2]), tf32_head(o[j + 3]));
+        const float4 l = make_float4(__fsub_rn(o[j], h.x), __fsub_rn(o[j + 1], h.y), __fsub_rn(o[j + 2], h.z),
+                                     __fsub_rn(o[j + 3], h.w));
+        *reinterpret_cast<float4*>(sh + n0 + j) = h;
+        *reinterpret_cast<float4*>(sh + a.sp_cp + n0 + j) = l;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (valid && j < cnt) hwc_store(sh, a.sp_cp, n0 + j * step, o[j]);
   }
 #pragma unroll
   for (int j = 0; j < N; ++j) {
-    if (j >= cnt) continue;
-    if (a.dense) {
-      yp[j * dn] = act_f(v[j], a.act, a.alpha);
-      if (ap) ap[j * dn] = v[j];
-    } else {
-      const float a1 = __fadd_rn(acc0[j], v[j]);
-      yp[j * dn] = __fsub_rn(act_f(a1, a.act, a.alpha), act_f(acc0[j], a.act, a.alpha));
-      ap[j * dn] = a1;
+    const bool in = valid && j < cnt;
+    if (in) ss += (double)o[j] * (double)o[j];
+    const unsigned nz = __ballot_sync(0xffffffffu, in && o[j] != 0.0f);
+    if (leader && (nz & grp)) {
+      fl[(int64_t)(n0 + j * step) * To] = 1;
+      any = true;
     }
   }
+  if (any) a.sp_fany[(int64_t)s * To + tile] = 1;  // benign race: only ever set
+  return ss;
 }
+
 
 template <int BN>
 __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant__ CUtensorMap tmap,
@@ -395,6 +456,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
   const bool live = s_flag[0] != 0;
   const int Qs = R * gridDim.y * gridDim.z;
   const int q = ((int)blockIdx.z * (int)gridDim.y + nblk) * R + rr;
+  double ssq = 0.0;  // fused sparsify: this thread's share of sum(out^2)
 
   if (!live) {
     if (!a.dense && warp >= 2 && warp < 4) side_work(a, s, q, Qs, threadIdx.x - 64);
@@ -406,10 +468,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
         if (u >= a.Ho || x >= a.Wo) continue;
         const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
         if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
-        if (a.act >= 0) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
+        if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
+        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.Wo + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
       }
       if (threadIdx.x == 0) a.rstate[rs_idx] = 0;
     }
+    if (a.sp_part && threadIdx.x == 0) a.sp_part[(int64_t)s * Qs + q] = 0.0;
     if (threadIdx.x == 0) {  // drain the prefetched weight copies before the shared memory is released
       for (int i = 0; i < npre; ++i) {
         bar_arrive(tma_bar(i));
@@ -555,7 +619,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
       }
       if (a.splits == 1) {
         const int n0 = nblk * BN + c0;
-        emit<16>(a, s, u0, v0, m, n0, 1, min(16, a.c_out - n0), vals);
+        ssq += emit<16>(a, s, u0, v0, m, n0, 1, min(16, a.c_out - n0), vals);
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
@@ -574,17 +638,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
     const int rank = (int)cl.block_rank();
     const int lo = rank * per, hi = min(BN, lo + per);
     float* P = reinterpret_cast<float*>(smem);
-    const int m = threadIdx.x % BM, g = threadIdx.x / BM;  // 2 channel groups of 128 sites
-    constexpr int NB = 2;
-    for (int nl0 = lo + g; nl0 < hi; nl0 += 2 * NB) {
-      const int cnt = min(NB, (hi - nl0 + 1) / 2);
+    const int m = threadIdx.x % BM, g = threadIdx.x / BM;  // 2 groups of 128 sites, 4 contiguous channels each
+    constexpr int NB = 4;
+    for (int nl0 = lo + NB * g; nl0 < hi; nl0 += 2 * NB) {
+      const int cnt = min(NB, hi - nl0);
       float t[16][NB];  // every rank's partials first (latencies overlap), then the ordered sum
 #pragma unroll
       for (int zz = 0; zz < 16; ++zz) {
         if (zz < nsp) {
           const float* Rz = cl.map_shared_rank(P, zz);
 #pragma unroll
-          for (int j = 0; j < NB; ++j) t[zz][j] = j < cnt ? Rz[(nl0 + 2 * j) * BM + m] : 0.0f;
+          for (int j = 0; j < NB; ++j) t[zz][j] = j < cnt ? Rz[(nl0 + j) * BM + m] : 0.0f;
         }
       }
       float sum[NB];
@@ -596,11 +660,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
           if (zz < nsp) sum[j] = __fadd_rn(sum[j], t[zz][j]);
       }
       const int n0 = nblk * BN + nl0;
-      emit<NB>(a, s, u0, v0, m, n0, 2, min(cnt, (a.c_out - n0 + 1) / 2), sum);
+      ssq += emit<NB>(a, s, u0, v0, m, n0, 1, min(cnt, a.c_out - n0), sum);
     }
     cluster_sync();
   }
   if (threadIdx.x == 128) TR(9);
+  if (a.sp_part) {
+    ssq = block_sum<double>(ssq, [](double v) { return warp_sum_d(v); });
+    if (threadIdx.x == 0) a.sp_part[(int64_t)s * Qs + q] = ssq;
+  }
   fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TR(13);
@@ -794,6 +862,16 @@ int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_c
   return EVC_OK;
 }
 
+int64_t evc_conv_fused_ctas(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
+  if (!g || !cfg || cfg->rh <= 0 || cfg->rw <= 0 || !fz::valid_bn(cfg->bn)) return -1;
+  const int nkb = g->kh * g->kw * ((g->c_in + 31) / 32);
+  int sp = std::max(1, std::min<int>(cfg->splits, nkb));
+  const int kbps = (nkb + sp - 1) / sp;
+  sp = (nkb + kbps - 1) / kbps;
+  return (int64_t)((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw) *
+         ((g->c_out + cfg->bn - 1) / cfg->bn) * sp;
+}
+
 int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg, int32_t S) {
   if (!g || !cfg || cfg->rh <= 0 || cfg->rw <= 0 || cfg->bn <= 0) return -1;
   return (int64_t)S * ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw) *
@@ -804,7 +882,8 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                    int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
                    const uint8_t* fany, const int32_t* table, uint8_t* rstate, int32_t* in_true, int64_t* bulk,
                    const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
-                   const evc_tensor* act_out, int32_t dense, int32_t S, void* stream) {
+                   const evc_tensor* act_out, const evc_conv_sparsify* sp, int32_t dense, int32_t S,
+                   void* stream) {
   EVC_CHECK_ARG(g && cfg && in_hwc && wpack && S > 0 && fz::valid_bn(cfg->bn), "conv_fused: null argument");
   EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
   EVC_CHECK_ARG(cfg->rh * cfg->rw == fz::BM && (cfg->rw == 32 || cfg->rw == 16 || cfg->rw == 8) &&
@@ -812,8 +891,11 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                 "conv_fused: bad region shape");
   EVC_CHECK_ARG(cfg->splits >= 1 && cfg->splits <= 16, "conv_fused: splits must lie in [1, 16]");
   EVC_CHECK_ARG(cp % 32 == 0 && cp >= g->c_in && hwc_stride % 32 == 0, "conv_fused: shadow layout (cp % 32)");
-  EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && act_out->vals && (acc || dense)), "conv_fused: activation");
-  EVC_CHECK_ARG(out || act >= 0, "conv_fused: no output");
+  EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
+  EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
+  EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 32 == 0 && sp->cp >= g->c_out && sp->hwc_stride % 32 == 0 &&
+                        sp->flags && sp->fany && sp->partials),
+                "conv_fused: fused sparsify needs the shadow, flags, fany and partials (incremental mode)");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && in_true && bulk &&
                           ((act >= 0 ? act_out->flags : (out ? out->flags : nullptr)) != nullptr)),
                 "conv_fused: incremental mode needs masks, fany, table, rstate and counters");
@@ -881,6 +963,17 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   a.accs = acc_stride;
   a.yact = act >= 0 ? act_out->vals : nullptr;
   a.yvs = act >= 0 ? act_out->vstride : 0;
+  if (sp) {
+    a.sp_hwc = sp->hwc;
+    a.sp_hs = sp->hwc_stride;
+    a.sp_cp = sp->cp;
+    a.sp_GH = (g->Ho + g->th - 1) / g->th;
+    a.sp_GW = (g->Wo + g->tw - 1) / g->tw;
+    a.sp_flags = sp->flags;
+    a.sp_fs = sp->fstride;
+    a.sp_fany = sp->fany;
+    a.sp_part = sp->partials;
+  }
   cudaStream_t st = as_stream(stream);
   cudaError_t e;
   switch (cfg->bn) {

@@ -528,6 +528,9 @@ class Graph:
                     self._consumers[i].append(node.spec.id)
             node.shadow = None
             node.fused_into = None
+            node.sp_fused_by = None  # sparsify evaluated in a producing conv's epilogue
+            node.fused_sp = None
+            node.act_values_needed = True
         for node in self.nodes:
             if node.kind != "concat":
                 continue
@@ -615,9 +618,28 @@ class Graph:
                 f = int(node.spec.attrs["out_features"])
                 lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
                                                                        self.tile.h * self.tile.w, S)))
+        # conv -> activation -> sparsify(t_p = 0) -> conv: the sparsify runs in the first conv's epilogue
+        # (it writes the second conv's hi/lo shadow, the sparsify flags and any-channel map directly)
+        for node in self.nodes:
+            act = getattr(node, "fused_act", None)
+            if node.kind != "conv" or act is None:
+                continue
+            cands = [c for c in self._consumers[act.spec.id]
+                     if self._by_id[c].kind == "sparsify" and self._by_id[c].tp == 0.0
+                     and self._by_id[c].shadow is not None and c not in self.output_ids
+                     and root(c) == (c, 0) and self._slots[c].store.C == self._slots[c].C]
+            if not cands:
+                continue
+            sp = self._by_id[cands[0]]
+            node.fused_sp = sp
+            sp.sp_fused_by = node
+            act.act_values_needed = (len(self._consumers[act.spec.id]) > 1 or act.spec.id in self.output_ids)
         # upsample -> sparsify pairs run as one fused kernel when the upsample has no other reader
         self._fused_up = set()
         for node in sp_nodes:
+            if node.sp_fused_by is not None:
+                node.nparts = int(self.lib.evc_conv_fused_ctas(node.sp_fused_by.plan.g, node.sp_fused_by.plan.cfg))
+                continue
             up = self._by_id.get(node.spec.inputs[0])
             if (up is not None and up.kind == "upsample" and self._consumers[up.spec.id] == [node.spec.id]
                     and up.spec.id not in self.output_ids and tile.w <= 32 and tile.h <= 8):
@@ -645,6 +667,9 @@ class Graph:
         o_cnt, o_bulk, o_perf = take(4 * nm * S), take(8 * nm * S), take(8 * nm * S)
         conv_off, fany_off, sp_off = [], [], []
         for node in self.nodes:
+            if node.kind == "sparsify" and node.sp_fused_by is not None:
+                st = self._slots[node.spec.id].store
+                sp_off.append((node, take(st.flags.numel())))  # flags are only ever set by the producer
             if node.kind == "conv":
                 if node.plan.path == "fused":
                     fany_off.append((node, take(S * node.plan.gi[0] * node.plan.gi[1])))
@@ -657,6 +682,9 @@ class Graph:
             node.mask_scratch = (base + c_off, base + s_off)
         for node, o in fany_off:
             node.plan.fany_ptr = base + o
+        for node, o in sp_off:
+            st = self._slots[node.spec.id].store
+            st.flags = self._zero[o:o + st.flags.numel()].view(st.flags.shape)
         self._cnt_step = self._zero[o_cnt:o_cnt + 4 * nm * S].view(torch.int32).view(nm, S)
         self._bulk_step = self._zero[o_bulk:o_bulk + 8 * nm * S].view(torch.int64).view(nm, S)
         self._perf_step = self._zero[o_perf:o_perf + 8 * nm * S].view(torch.int64).view(nm, S)
@@ -746,12 +774,23 @@ class Graph:
                     act = node.fused_act
                     if act is not None:
                         code, alpha = act.act
-                        fa = (code, alpha, act.acc.data_ptr(), act.acc[0].numel(), self._desc(act.spec.id))
+                        ad = self._desc(act.spec.id)
+                        if not act.act_values_needed:
+                            ad.vals = None  # read only through the fused sparsify
+                        fa = (code, alpha, act.acc.data_ptr(), act.acc[0].numel(), ad)
                         dout = None
                     else:
                         fa, dout = None, self._desc(nid)
+                    spd = None
+                    if node.fused_sp is not None:
+                        sp = node.fused_sp
+                        sh = sp.shadow
+                        sdesc = self._desc(sp.spec.id)
+                        spd = _lib.EvcConvSparsify(sh.hwc.data_ptr(), sh.hwc[0].numel(), sh.cp, sdesc.flags,
+                                                   sdesc.fstride, sh.fany_ptr, sp.part_ptr)
+                        node._spd = spd  # keep the struct alive with the program
                     fn, args = plan.fused(din, dout, fany=plan.fany_ptr, in_true=cnt_ptr,
-                                          bulk=self._bulk_step.data_ptr() + 8 * mi * S, act=fa)
+                                          bulk=self._bulk_step.data_ptr() + 8 * mi * S, act=fa, sp=spd)
                     prog.append((fn, args, "conv_fused"))
                 else:
                     dout = self._desc(nid)
@@ -777,6 +816,8 @@ class Graph:
                 code, alpha = node.act
                 prog.append((L.evc_act_delta, (self._desc(ns.inputs[0]), node.acc.data_ptr(),
                                                node.acc[0].numel(), self._desc(nid), code, alpha, S), "act_delta"))
+            elif k == "sparsify" and node.sp_fused_by is not None:
+                continue  # evaluated in the producing conv's epilogue
             elif k == "sparsify" and ns.inputs[0] in self._fused_up:
                 j = node.sp_idx
                 up = self._by_id[ns.inputs[0]]

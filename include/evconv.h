@@ -151,12 +151,15 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
                   int32_t* tile_count, uint8_t* region_flags, int64_t* meter,
                   int32_t S, void* stream);
 
-/* Channels-innermost shadow of the conv input (hwc.cu): element (s,y,x,c) at
- * in_hwc[s*hwc_stride + (y*W + x)*cp + c], cp = evc_hwc_channels(C_in); the
- * A operand of evc_conv_fused is RH TMA boxes of it per (tap, 32-channel) K-block. */
+/* Channels-innermost hi/lo shadow of a conv input (hwc.cu).  The buffer holds
+ * (H + 2 pad) x (W + 2 pad) pixels of 2*cp floats (cp = evc_hwc_channels(C_in)):
+ * the TF32 heads of the channels, then their tails; the border stays zero (the
+ * conv's padding).  Producers get y = the interior origin (pixel (0, 0)) and
+ * pitch = W + 2 pad: element (s, y, x, c) head at y[s*stride + (y*pitch + x)*2cp + c],
+ * tail at + cp. */
 int32_t evc_hwc_channels(int32_t c);
 int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp,
-               int32_t S, void* stream);
+               int32_t pitch, int32_t S, void* stream);
 
 /* ---- fused incremental convolution (conv_fused.cu) --------------------
  * inc_conv2d (increment_ops.py:126-194) in ONE launch: region test against the
@@ -167,8 +170,11 @@ int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp,
  * in the epilogue.  Launch configuration: */
 typedef struct evc_conv_cfg {
   int32_t bn;     /* output channels per CTA: 16, 32, 64, 128 or 256 */
-  int32_t rh, rw; /* output region rows x cols, rh * rw = 128, rw in {8, 16, 32} */
+  int32_t rh, rw; /* tap mode: output region rows x cols, rh * rw = 128, rw in {8, 16, 32} */
   int32_t splits; /* K-splits = cluster size along z, 1..16 */
+  int32_t row;    /* 1: row mode (stride 1): regions = 128 consecutive sites of the output grid
+                     flattened with pitch W + 2 pad; a K-block is one kernel row x 32 channels,
+                     loaded once (128 + kw - 1 shadow pixels) for all kw taps */
 } evc_conv_cfg;
 
 /* 1 if the fused path handles this geometry (pad < kernel, stride <= 8). */
@@ -199,9 +205,10 @@ int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg
  * sum of squares per CTA (partials[s * evc_conv_fused_ctas(g, cfg) + cta]) for the
  * deferred norm fold of evc_meter_step. */
 typedef struct evc_conv_sparsify {
-  float* hwc;
+  float* hwc; /* interior origin of the next conv's shadow (see evc_to_hwc) */
   int64_t hwc_stride;
   int32_t cp;
+  int32_t pitch;
   uint8_t* flags;
   int64_t fstride;
   uint8_t* fany;
@@ -296,10 +303,10 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t delta_stride,
                  uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay,
                  double* partials, int32_t* ticket, float* hwc, int32_t cp,
-                 int64_t hwc_stride, uint8_t* fany, int32_t write_chw,
+                 int64_t hwc_stride, int32_t hwc_pitch, uint8_t* fany, int32_t write_chw,
                  int32_t delta_zero, int32_t S, void* stream);
-/* (hwc, cp, hwc_stride: optional channels-innermost shadow of y for the
- * TMA conv GEMM, see evc_to_hwc; fany: optional any-channel tile map of y
+/* (hwc, cp, hwc_stride, hwc_pitch: optional channels-innermost hi/lo shadow of y
+ * for the TMA conv GEMM, interior origin and row pitch as in evc_to_hwc; fany: optional any-channel tile map of y
  * for evc_conv_fused, only ever set to 1 -- zero it per step;
  * write_chw = 0 skips the planar y values --
  * flags are always written.  delta_zero != 0 asserts tp == 0 and k == 0, so
@@ -315,7 +322,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode,
                           const evc_tensor* y, double* k, double* norm_ema,
                           double tp, double ema_decay, double* partials,
                           int32_t* ticket, float* hwc, int32_t cp,
-                          int64_t hwc_stride, uint8_t* fany, int32_t write_chw,
+                          int64_t hwc_stride, int32_t hwc_pitch, uint8_t* fany, int32_t write_chw,
                           int32_t delta_zero, int32_t S, void* stream);
 
 /* acc += dx on live tiles (AccState.fold, increment_ops.py:93-94). */

@@ -38,11 +38,12 @@ class EvcConvGeom(C.Structure):
 
 
 class EvcConvCfg(C.Structure):
-    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits")]
+    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits", "row")]
 
 
 class EvcConvSparsify(C.Structure):
-    _fields_ = [("hwc", C.c_void_p), ("hwc_stride", C.c_int64), ("cp", C.c_int32), ("flags", C.c_void_p),
+    _fields_ = [("hwc", C.c_void_p), ("hwc_stride", C.c_int64), ("cp", C.c_int32), ("pitch", C.c_int32),
+                ("flags", C.c_void_p),
                 ("fstride", C.c_int64), ("fany", C.c_void_p), ("partials", C.c_void_p)]
 
 
@@ -80,7 +81,7 @@ _PROTOS = {
     "evc_conv_mask_scratch": (_I64, [_G, _I32]),
     "evc_conv_mask": (_I32, [_G, _T, _T, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_hwc_channels": (_I32, [_I32]),
-    "evc_to_hwc": (_I32, [_T, _P, _I64, _I32, _I32, _P]),
+    "evc_to_hwc": (_I32, [_T, _P, _I64, _I32, _I32, _I32, _P]),
     "evc_conv_fused_supported": (_I32, [_G]),
     "evc_conv_fused_config": (_I32, [_G, _I32, _I32, _CF]),
     "evc_conv_fused_pack_len": (_I64, [_G, _CF]),
@@ -99,10 +100,12 @@ _PROTOS = {
     "evc_act_delta": (_I32, [_T, _P, _I64, _T, _I32, _F, _I32, _P]),
     "evc_act_dense": (_I32, [_P, _I64, _P, _I64, _P, _I64, _I64, _I32, _F, _I32, _P]),
     "evc_sparsify_partials": (_I64, [_T]),
-    "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _P, _I32, _I32, _I32, _P]),
+    "evc_sparsify": (_I32, [_T, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32, _P, _I32, _I32, _I32,
+                            _P]),
     "evc_fold": (_I32, [_T, _P, _I64, _I32, _P]),
     "evc_upsample_sparsify_partials": (_I64, [_T]),
-    "evc_upsample_sparsify": (_I32, [_T, _I32, _I32, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _P, _I32,
+    "evc_upsample_sparsify": (_I32, [_T, _I32, _I32, _P, _I64, _P, _T, _P, _P, _D, _D, _P, _P, _P, _I32, _I64, _I32, _P,
+                                     _I32,
                                      _I32, _I32, _P]),
     "evc_sparsify_finalize": (_I32, [_P, _I64, _P, _P, _D, _D, _I32, _I32, _P]),
     "evc_sumsq_dense": (_I32, [_P, _I64, _I64, _P, _I32, _I32, _P]),

@@ -83,6 +83,7 @@ struct TBArgs {
   float* hwc;  // sparsify channels-innermost shadow (optional)
   int64_t hs;  // shadow session stride
   int cp;      // shadow channel stride
+  int hp;      // shadow row pitch in pixels (padded width of the consumer conv's input)
   uint8_t* fany;  // sparsify: optional any-channel tile map of the output (OR-accumulated, zeroed per step)
   int write_chw;
   int delta_zero;  // sparsify with tp == 0 and k == 0: the residual is identically 0, skip its traffic
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
           if (p.hwc && !stage) {
 #pragma unroll
             for (int k = 0; k < V; ++k)
-              hwc_store(p.hwc + (int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * g.W + x0 + xl_[u] + k) * 2 * p.cp, p.cp,
+              hwc_store(p.hwc + (int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * p.hp + x0 + xl_[u] + k) * 2 * p.cp, p.cp,
                         c0 + cl_[u], VT::get(out, k));
           }
           if (!p.delta_zero) VT::st(p.acc2 + sacc + off[u], acc_new);
@@ -293,10 +294,10 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     }
     if (stage && (int)(threadIdx.x & 31) < nc) {  // lane = channel: 128-byte runs of heads and tails per pixel
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * g.W * 2 * p.cp + c0 + lane;
+      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * p.hp * 2 * p.cp + c0 + lane;
       for (int r = 0; r < nrow; ++r)
         for (int xl = warp; xl < ncol; xl += TB_THREADS / 32)
-          hwc_store(dst + ((int64_t)r * g.W + x0 + xl) * 2 * p.cp, p.cp, 0, s_y[(r * 32 + xl) * 33 + lane]);
+          hwc_store(dst + ((int64_t)r * p.hp + x0 + xl) * 2 * p.cp, p.cp, 0, s_y[(r * 32 + xl) * 33 + lane]);
     }
   }
   if (OP == OP_SPARSIFY) {
@@ -383,11 +384,13 @@ int64_t evc_sparsify_partials(const evc_tensor* dx) {
 
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
                  double* norm_ema, double tp, double ema_decay, double* partials, int32_t* ticket, float* hwc,
-                 int32_t cp, int64_t hwc_stride, uint8_t* fany, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
+                 int32_t cp, int64_t hwc_stride, int32_t hwc_pitch, uint8_t* fany, int32_t write_chw,
+                 int32_t delta_zero, int32_t S, void* stream) {
   EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || (cp >= dx->C && cp % 32 == 0), "sparsify: shadow channel count must cover C, multiple of 32");
+  EVC_CHECK_ARG(!hwc || (cp >= dx->C && cp % 32 == 0 && hwc_pitch >= dx->W),
+                "sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   TBArgs p = {};
   p.a = view_of(*dx);
   p.y = view_of(*y);
@@ -402,6 +405,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   p.ticket = ticket;
   p.hwc = hwc;
   p.hs = hwc_stride;
+  p.hp = hwc_pitch;
   p.cp = cp;
   p.fany = fany;
   p.write_chw = write_chw;

@@ -49,9 +49,6 @@ namespace fz {
 constexpr int BM = 128;
 constexpr int THREADS = 256;
 
-__host__ __device__ constexpr int stages_of(int bn) { return bn <= 64 ? 4 : (bn <= 128 ? 3 : 2); }
-__host__ __device__ constexpr int stage_bytes(int bn) { return 2 * BM * 128 + 2 * bn * 128; }
-static inline int smem_bytes(int bn) { return stages_of(bn) * stage_bytes(bn) + 1024 + 256; }
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -93,6 +90,13 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
       "[%6];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(x), "r"(y), "r"(n), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c, int x, int n, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c), "r"(x), "r"(n), "r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -145,6 +149,10 @@ struct Args {
   int c_in, c_out, kh, kw, stride, pad, H, W, Ho, Wo, S;
   int RH, RW, RHn, RWn, cchunks, nkb, splits, kb_per_split, bn;
   int th, tw, cp;
+  // row mode (stride 1): regions are 128 consecutive sites of the output grid flattened with
+  // pitch P = W + 2 pad; a K-block is (kernel row, 32 channels) with the kw taps as row shifts
+  int row, P, R;
+  int ns, stage, a_half, b_bytes;  // pipeline depth and stage layout (bytes)
   const float* wpack;
   const float* bias;
   // incremental mode (dense == 0)
@@ -171,7 +179,7 @@ struct Args {
   // flags and any-channel map (both zeroed per step), per-CTA sums of squares [S][CTAs/session]
   float* sp_hwc;
   int64_t sp_hs;
-  int sp_cp, sp_GH, sp_GW;
+  int sp_cp, sp_pitch, sp_GH, sp_GW;
   uint8_t* sp_flags;
   int64_t sp_fs;
   uint8_t* sp_fany;
@@ -265,9 +273,8 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
 // every lane of a warp with warp-uniform (n0, step, cnt): the fused sparsify uses
 // warp ballots.  Returns the site's sum of squared sparsify outputs (0 if unfused).
 template <int N>
-__device__ __forceinline__ double emit(const Args& a, int s, int u0, int v0, int m, int n0, int step, int cnt,
+__device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n0, int step, int cnt,
                                        const float* vals) {
-  const int u = u0 + m / a.RW, x = v0 + m % a.RW;
   const bool valid = u < a.Ho && x < a.Wo;
   const int64_t plane = (int64_t)a.Ho * a.Wo;
   const int64_t base = (int64_t)n0 * plane + (int64_t)u * a.Wo + x;
@@ -315,7 +322,7 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u0, int v0, int
   const int tile = valid ? (u / a.th) * a.sp_GW + x / a.tw : -1;
   const unsigned grp = __match_any_sync(0xffffffffu, tile);
   const bool leader = valid && (__ffs(grp) - 1) == lane;
-  float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.Wo + x) * 2 * a.sp_cp;
+  float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp;
   const int64_t To = (int64_t)a.sp_GH * a.sp_GW;
   uint8_t* fl = a.sp_flags + (int64_t)s * a.sp_fs + tile;
   bool any = false;
@@ -353,11 +360,21 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u0, int v0, int
 }
 
 
+// Output site of TMEM lane m in region rr.
+__device__ __forceinline__ void site_of(const Args& a, int rr, int m, int& u, int& x) {
+  if (a.row) {
+    const int i = rr * BM + m;
+    u = i / a.P;
+    x = i - u * a.P;
+  } else {
+    u = (rr / a.RWn) * a.RH + m / a.RW;
+    x = (rr % a.RWn) * a.RW + m % a.RW;
+  }
+}
+
 template <int BN>
-__global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(const __grid_constant__ CUtensorMap tmap,
                                                            const __grid_constant__ Args a) {
-  constexpr int NS = stages_of(BN);
-  constexpr int STAGE = stage_bytes(BN);
   // 3xTF32 with the fewest MMA instructions (tcgen05.mma costs ~62 cycles for any N <= 128):
   //  CAT (BN <= 128): D_j[:, 0:2BN] += A_hi . [B_hi | B_lo]  (one MMA, N = 2 BN: hi*hi and hi*lo)
   //                   D_c[:, 0:BN]  += A_lo . B_hi           (one MMA)
@@ -372,35 +389,56 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
   constexpr uint32_t IDESC_BASE = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BM >> 4) << 24);
   constexpr uint32_t IDESC = IDESC_BASE | ((uint32_t)(BN >> 3) << 17);
   constexpr uint32_t IDESC2 = IDESC_BASE | ((uint32_t)((CAT ? 2 * BN : BN) >> 3) << 17);
-  constexpr uint32_t A_BYTES = BM * 128;
-  constexpr uint32_t B_BYTES = 2 * BN * 128;
+  constexpr int MAXNS = 4;
 
   const unsigned long long t_start = clk();
   if (a.trace && threadIdx.x == 0)
     a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16 + 15] = gtime();
-  const int R = a.RHn * a.RWn;
+  const int R = a.R;
   const int reg = blockIdx.x;  // s * R + region
   const int s = reg / R, rr = reg % R;
-  const int u0 = (rr / a.RWn) * a.RH, v0 = (rr % a.RWn) * a.RW;
   const int nblk = blockIdx.y, z = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t rs_idx = (int64_t)reg * gridDim.y + nblk;
   const int kb0 = z * a.kb_per_split, kb1 = min(a.nkb, kb0 + a.kb_per_split), nk = kb1 - kb0;
+  const int NS = a.ns, STAGE = a.stage;
   const int npre = min(NS, nk);
+  const uint32_t A_HALF = (uint32_t)a.a_half, B_BYTES = (uint32_t)a.b_bytes;
+  const int taps = a.row ? a.kw : 1;                           // MMAs groups per K-block
+  const uint32_t A_TX = a.row ? (uint32_t)(BM + a.kw - 1) * 128u : (uint32_t)BM * 128u;  // bytes per A box
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[NS], empty[NS], acc
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[4], empty[4], acc
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNS + 1);
   volatile int* s_flag = reinterpret_cast<volatile int*>(tslot + 1);  // [0] live, [1] computed last step
   const uint32_t sb = su32(smem), b0 = su32(bars);
   auto tma_bar = [&](int i) { return b0 + 8u * i; };
-  auto empty_bar = [&](int i) { return b0 + 8u * (NS + i); };
-  const uint32_t acc_bar = b0 + 8u * (2 * NS);
+  auto empty_bar = [&](int i) { return b0 + 8u * (MAXNS + i); };
+  const uint32_t acc_bar = b0 + 8u * (2 * MAXNS);
   const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
 
-  // ---- prologue that reads nothing an upstream kernel writes: under programmatic
-  // dependent launch it overlaps the previous kernel's tail
+  // valid output rows / columns of this region (receptive-box test, prefetch)
+  int ulo, uhi, xlo, xhi;
+  if (a.row) {
+    const int i0 = rr * BM;
+    ulo = i0 / a.P;
+    uhi = min(a.Ho - 1, (i0 + BM - 1) / a.P);
+    if (ulo == uhi) {
+      xlo = i0 - ulo * a.P;
+      xhi = min(a.Wo - 1, i0 + BM - 1 - ulo * a.P);
+    } else {
+      xlo = 0;
+      xhi = a.Wo - 1;
+    }
+  } else {
+    ulo = (rr / a.RWn) * a.RH;
+    uhi = min(ulo + a.RH, a.Ho) - 1;
+    xlo = (rr % a.RWn) * a.RW;
+    xhi = min(xlo + a.RW, a.Wo) - 1;
+  }
+
+  // ---- prologue that reads nothing an upstream kernel writes
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       bar_init(tma_bar(i), 1);
@@ -412,7 +450,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
     // the first stages' weights are static: stream them now (their arrive comes with the A boxes)
     for (int i = 0; i < npre; ++i) {
       bar_expect_tx(tma_bar(i), B_BYTES);
-      bulk_load(sb + i * STAGE + 2 * A_BYTES, wsrc + (int64_t)(kb0 + i) * B_BYTES, B_BYTES, tma_bar(i));
+      bulk_load(sb + i * STAGE + 2 * A_HALF, wsrc + (int64_t)(kb0 + i) * B_BYTES, B_BYTES, tma_bar(i));
     }
   }
   if (warp == 1) {
@@ -432,17 +470,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
   if (warp == 0) {
     int live = 1;
     if (!a.dense) {
-      const int y_lo = max(0, u0 * a.stride - a.pad);
-      const int y_hi = min(a.H - 1, (min(u0 + a.RH, a.Ho) - 1) * a.stride - a.pad + a.kh - 1);
-      const int x_lo = max(0, v0 * a.stride - a.pad);
-      const int x_hi = min(a.W - 1, (min(v0 + a.RW, a.Wo) - 1) * a.stride - a.pad + a.kw - 1);
       live = 0;
-      if (y_lo <= y_hi && x_lo <= x_hi) {
-        const int GWi = (a.W + a.tw - 1) / a.tw, GHi = (a.H + a.th - 1) / a.th;
-        const int ra = y_lo / a.th, nr = y_hi / a.th - ra + 1;
-        const int ca = x_lo / a.tw, nc = x_hi / a.tw - ca + 1;
-        const uint8_t* fa = a.fany + (int64_t)s * GHi * GWi;
-        for (int e = lane; e < nr * nc; e += 32) live |= fa[(ra + e / nc) * GWi + ca + e % nc];
+      if (ulo <= uhi && xlo <= xhi) {
+        const int y_lo = max(0, ulo * a.stride - a.pad);
+        const int y_hi = min(a.H - 1, uhi * a.stride - a.pad + a.kh - 1);
+        const int x_lo = max(0, xlo * a.stride - a.pad);
+        const int x_hi = min(a.W - 1, xhi * a.stride - a.pad + a.kw - 1);
+        if (y_lo <= y_hi && x_lo <= x_hi) {
+          const int GWi = (a.W + a.tw - 1) / a.tw, GHi = (a.H + a.th - 1) / a.th;
+          const int ra = y_lo / a.th, nr = y_hi / a.th - ra + 1;
+          const int ca = x_lo / a.tw, nc = x_hi / a.tw - ca + 1;
+          const uint8_t* fa = a.fany + (int64_t)s * GHi * GWi;
+          for (int e = lane; e < nr * nc; e += 32) live |= fa[(ra + e / nc) * GWi + ca + e % nc];
+        }
       }
       live = __any_sync(0xffffffffu, live);
     }
@@ -464,12 +504,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
       const int n0 = nblk * a.bn, nn = min(a.bn, a.c_out - n0);
       for (int e = threadIdx.x; e < nn * BM; e += THREADS) {
         const int n = n0 + e / BM, m = e % BM;
-        const int u = u0 + m / a.RW, x = v0 + m % a.RW;
+        int u, x;
+        site_of(a, rr, m, u, x);
         if (u >= a.Ho || x >= a.Wo) continue;
         const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
         if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
         if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
-        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.Wo + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
+        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
       }
       if (threadIdx.x == 0) a.rstate[rs_idx] = 0;
     }
@@ -495,20 +536,26 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
       for (int i = 0; i < nk; ++i) {
         const int st = i % NS;
         const int kb = kb0 + i;
-        const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
-        const int r = tap / a.kw, qq = tap % a.kw;
         const uint32_t abuf = sb + st * STAGE;
         if (i < npre) {
-          bar_arrive_tx(tma_bar(st), 2 * A_BYTES);  // weights already in flight
+          bar_arrive_tx(tma_bar(st), 2 * A_TX);  // weights already in flight
         } else {
           bar_spin(empty_bar(st), ((i / NS) & 1) ^ 1);
-          bar_arrive_tx(tma_bar(st), 2 * A_BYTES + B_BYTES);
-          bulk_load(abuf + 2 * A_BYTES, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
+          bar_arrive_tx(tma_bar(st), 2 * A_TX + B_BYTES);
+          bulk_load(abuf + 2 * A_HALF, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
         }
-        // one box = the whole RH x RW region for this tap: TF32 heads, then tails, of the shadow
-        const int xs = v0 * a.stride - a.pad + qq, ys = u0 * a.stride - a.pad + r;
-        tma_load_4d(abuf, &tmap, c0, xs, ys, s, tma_bar(st));
-        tma_load_4d(abuf + A_BYTES, &tmap, a.cp + c0, xs, ys, s, tma_bar(st));
+        if (a.row) {  // kernel row r of the flattened padded shadow: 128 + kw - 1 pixel rows
+          const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
+          const int i0 = rr * BM + r * a.P;
+          tma_load_3d(abuf, &tmap, c0, i0, s, tma_bar(st));
+          tma_load_3d(abuf + A_HALF, &tmap, a.cp + c0, i0, s, tma_bar(st));
+        } else {  // one box = the whole RH x RW region for this tap (padded coordinates)
+          const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
+          const int r = tap / a.kw, qq = tap % a.kw;
+          const int xs = xlo * a.stride + qq, ys = ulo * a.stride + r;
+          tma_load_4d(abuf, &tmap, c0, xs, ys, s, tma_bar(st));
+          tma_load_4d(abuf + A_HALF, &tmap, a.cp + c0, xs, ys, s, tma_bar(st));
+        }
         if (i == 0) TR(3);
       }
       TR(11);
@@ -520,24 +567,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
         const int st = i % NS;
         bar_spin(tma_bar(st), (i / NS) & 1);
         fence_after();
-        const uint32_t ah = sb + st * STAGE, al = ah + A_BYTES;
-        const uint32_t bh = ah + 2 * A_BYTES, bl = bh + BN * 128;
-        if (CAT) {
-          const uint32_t tj = tmem + (uint32_t)((i % NA) * 2 * BN), tc = tmem + (uint32_t)(NA * 2 * BN);
+        const uint32_t ah = sb + st * STAGE, al = ah + A_HALF, bb = ah + 2 * A_HALF;
+        for (int t = 0; t < taps; ++t) {
+          // row mode: tap t = the A rows shifted by t pixels (any 128-byte row offset is a valid
+          // SW128 descriptor start: the swizzle follows the absolute address, scripts/shift_probe.cu)
+          const uint32_t at = ah + t * 128, lt = al + t * 128, bh = bb + t * 2 * BN * 128, bl = bh + BN * 128;
+          const bool first = t == 0;
+          if (CAT) {
+            const uint32_t tj = tmem + (uint32_t)((i % NA) * 2 * BN), tc = tmem + (uint32_t)(NA * 2 * BN);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
-            mma(tj, desc_k(ah + ko), desc_k(bh + ko), IDESC2, (i >= NA || kk) ? 1u : 0u);  // [hi*hi | hi*lo]
-            mma(tc, desc_k(al + ko), desc_k(bh + ko), IDESC, (i | kk) ? 1u : 0u);          // lo*hi
-          }
-        } else {
-          const uint32_t tmain = tmem, tcorr = tmem + (uint32_t)BN;
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
+              mma(tj, desc_k(at + ko), desc_k(bh + ko), IDESC2, (i >= NA || kk || !first) ? 1u : 0u);
+              mma(tc, desc_k(lt + ko), desc_k(bh + ko), IDESC, (i || kk || !first) ? 1u : 0u);
+            }
+          } else {
+            const uint32_t tmain = tmem, tcorr = tmem + (uint32_t)BN;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t ko = kk * 32;
-            mma(tmain, desc_k(ah + ko), desc_k(bh + ko), IDESC, (i | kk) ? 1u : 0u);
-            mma(tcorr, desc_k(ah + ko), desc_k(bl + ko), IDESC, (i | kk) ? 1u : 0u);
-            mma(tcorr, desc_k(al + ko), desc_k(bh + ko), IDESC, 1u);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t ko = kk * 32;
+              mma(tmain, desc_k(at + ko), desc_k(bh + ko), IDESC, (i || kk || !first) ? 1u : 0u);
+              mma(tcorr, desc_k(at + ko), desc_k(bl + ko), IDESC, (i || kk || !first) ? 1u : 0u);
+              mma(tcorr, desc_k(lt + ko), desc_k(bh + ko), IDESC, 1u);
+            }
           }
         }
         commit(empty_bar(st));
@@ -549,16 +601,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
     __syncwarp();
   } else if (warp < 4) {
     if (!a.dense) {
-      if (a.act >= 0) {  // warm L2 with the accumulator rows the epilogue will read
+      if (a.act >= 0) {  // warm L2 with the accumulator lines the epilogue will read
         const int per = (a.bn + a.splits - 1) / a.splits;
         const int lo = a.splits > 1 ? z * per : 0, hi = a.splits > 1 ? min(a.bn, lo + per) : a.bn;
-        const int rows = min(a.RH, a.Ho - u0);
         const int64_t plane = (int64_t)a.Ho * a.Wo;
-        for (int e = threadIdx.x - 64; e < (hi - lo) * rows * 2; e += 64) {
-          const int n = nblk * a.bn + lo + e / (rows * 2), r = (e / 2) % rows, half = e & 1;
-          if (n >= a.c_out) continue;
-          const float* p = a.acc + (int64_t)s * a.accs + n * plane + (int64_t)(u0 + r) * a.Wo + v0 +
-                           half * min(a.RW - 1, a.Wo - 1 - v0);
+        for (int e = threadIdx.x - 64; e < (hi - lo) * (BM / 16); e += 64) {
+          const int n = nblk * a.bn + lo + e / (BM / 16), m = (e % (BM / 16)) * 16;
+          int u, x;
+          site_of(a, rr, m, u, x);
+          if (n >= a.c_out || u >= a.Ho || x >= a.Wo) continue;
+          const float* p = a.acc + (int64_t)s * a.accs + n * plane + (int64_t)u * a.Wo + x;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
         }
       }
@@ -568,6 +620,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
   } else {
     // ------------------------------------------------------------- epilogue (TMEM -> values)
     const int m = 32 * (warp & 3) + lane;  // TMEM lane = region site
+    int u, x;
+    site_of(a, rr, m, u, x);
     bar_wait(acc_bar, 0);
     fence_after();
     if (threadIdx.x == 128) TR(6);
@@ -619,7 +673,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
       }
       if (a.splits == 1) {
         const int n0 = nblk * BN + c0;
-        ssq += emit<16>(a, s, u0, v0, m, n0, 1, min(16, a.c_out - n0), vals);
+        ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
@@ -639,6 +693,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
     const int lo = rank * per, hi = min(BN, lo + per);
     float* P = reinterpret_cast<float*>(smem);
     const int m = threadIdx.x % BM, g = threadIdx.x / BM;  // 2 groups of 128 sites, 4 contiguous channels each
+    int u, x;
+    site_of(a, rr, m, u, x);
     constexpr int NB = 4;
     for (int nl0 = lo + NB * g; nl0 < hi; nl0 += 2 * NB) {
       const int cnt = min(NB, hi - nl0);
@@ -660,7 +716,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_fused(const __grid_constant
           if (zz < nsp) sum[j] = __fadd_rn(sum[j], t[zz][j]);
       }
       const int n0 = nblk * BN + nl0;
-      ssq += emit<NB>(a, s, u0, v0, m, n0, 1, min(cnt, a.c_out - n0), sum);
+      ssq += emit<NB>(a, s, u, x, n0, 1, min(cnt, a.c_out - n0), sum);
     }
     cluster_sync();
   }
@@ -747,9 +803,9 @@ static EncodeTiled encoder() {
 template <int BN>
 static cudaError_t launch(const CUtensorMap& m, const Args& a, cudaStream_t st) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(a.S * a.RHn * a.RWn), (unsigned)((a.c_out + BN - 1) / BN), (unsigned)a.splits);
+  cfg.gridDim = dim3((unsigned)(a.S * a.R), (unsigned)((a.c_out + BN - 1) / BN), (unsigned)a.splits);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = smem_bytes(BN);
+  cfg.dynamicSmemBytes = (size_t)a.ns * a.stage + 1024 + 256;
   cfg.stream = st;
   cudaLaunchAttribute at[2];
   int na = 0;
@@ -770,10 +826,15 @@ static cudaError_t launch(const CUtensorMap& m, const Args& a, cudaStream_t st) 
   return cudaLaunchKernelEx(&cfg, k_conv_fused<BN>, m, a);
 }
 
+constexpr int SMEM_MAX = 227 * 1024;
+constexpr int STAGE_BUDGET = SMEM_MAX - 1024 - 256 - 2048;
+
 template <int BN>
 static int attr() {
-  if (cudaFuncSetAttribute(k_conv_fused<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(BN)) !=
-      cudaSuccess)
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_conv_fused<BN>) != cudaSuccess) return 1;
+  if (cudaFuncSetAttribute(k_conv_fused<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SMEM_MAX - (int)fa.sharedSizeBytes) != cudaSuccess)
     return 1;
   return cudaFuncSetAttribute(k_conv_fused<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess
              ? 0
@@ -781,6 +842,44 @@ static int attr() {
 }
 
 static bool valid_bn(int bn) { return bn == 16 || bn == 32 || bn == 64 || bn == 128 || bn == 256; }
+
+// Pipeline layout of one configuration: stage = [A heads | A tails | B], A halves 1 KiB aligned.
+struct Layout {
+  int ns, stage, a_half, b_bytes, R, nkb, cchunks;
+};
+
+static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
+  Layout L;
+  L.cchunks = (g->c_in + 31) / 32;
+  if (cfg->row) {
+    L.a_half = ((BM + g->kw - 1 + 7) / 8) * 8 * 128;
+    L.b_bytes = g->kw * 2 * cfg->bn * 128;
+    L.nkb = g->kh * L.cchunks;
+    const int P = g->W + 2 * g->pad;
+    L.R = (int)(((int64_t)g->Ho * P + BM - 1) / BM);
+  } else {
+    L.a_half = BM * 128;
+    L.b_bytes = 2 * cfg->bn * 128;
+    L.nkb = g->kh * g->kw * L.cchunks;
+    L.R = ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw);
+  }
+  L.a_half = (L.a_half + 1023) / 1024 * 1024;
+  L.stage = 2 * L.a_half + L.b_bytes;
+  L.stage = (L.stage + 1023) / 1024 * 1024;
+  L.ns = std::max(1, std::min(4, STAGE_BUDGET / L.stage));
+  // two co-resident CTAs per SM when two stages of each fit and the accumulators fit half of TMEM:
+  // one CTA's prologue / epilogue then overlaps the other's MMA stream
+  const int bn = cfg->bn, na = bn >= 128 ? 1 : (bn >= 64 ? 3 : 4);
+  const int need = bn <= 128 ? na * 2 * bn + bn : 2 * bn;
+  if (need <= 256 && 2 * (2 * L.stage + 1024 + 256 + 1024) <= SMEM_MAX) L.ns = 2;
+  return L;
+}
+
+static int split_count(int nkb, int splits) {
+  int sp = std::max(1, std::min(splits, nkb));
+  const int kbps = (nkb + sp - 1) / sp;
+  return (nkb + kbps - 1) / kbps;
+}
 
 }  // namespace fz
 
@@ -808,20 +907,30 @@ int evc_conv_fused_supported(const evc_conv_geom* g) {
 
 int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits, evc_conv_cfg* cfg) {
   EVC_CHECK_ARG(g && cfg && S > 0, "conv_fused_config: null argument");
-  cfg->rw = g->Wo > 16 ? 32 : (g->Wo > 8 ? 16 : 8);
-  cfg->rh = 128 / cfg->rw;
-  const int64_t regions = (int64_t)S * ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw);
+  // stride 1: row mode (halo rows loaded once for all kw taps); else tap mode over RH x RW regions
+  cfg->row = (g->stride == 1 && g->kw <= 9 && g->Wo == g->W + 2 * g->pad - g->kw + 1) ? 1 : 0;
+  if (cfg->row) {
+    cfg->rh = 1;
+    cfg->rw = fz::BM;
+  } else {
+    cfg->rw = g->Wo > 16 ? 32 : (g->Wo > 8 ? 16 : 8);
+    cfg->rh = fz::BM / cfg->rw;
+  }
   int bn = 16;
   while (bn < g->c_out && bn < 256) bn *= 2;
-  const int msp = std::max(1, std::min<int>(max_splits > 0 ? max_splits : 8, 16));
-  while (bn > 64 && regions * ((g->c_out + bn - 1) / bn) * msp < 148) bn /= 2;
+  if (cfg->row && bn > 64) bn = 64;  // kw taps of B per stage: keep >= 2 stages
   cfg->bn = bn;
-  const int nkb = g->kh * g->kw * ((g->c_in + 31) / 32);
+  const int msp = std::max(1, std::min<int>(max_splits > 0 ? max_splits : 8, 16));
+  fz::Layout L = fz::layout_of(g, cfg);
+  const int64_t regions = (int64_t)S * L.R;
+  while (bn > 64 && regions * ((g->c_out + bn - 1) / bn) * msp < 148) {
+    bn /= 2;
+    cfg->bn = bn;
+  }
+  L = fz::layout_of(g, cfg);
   const int64_t ctas = regions * ((g->c_out + bn - 1) / bn);
   int sp = ctas >= 148 ? 1 : (int)std::min<int64_t>(msp, (148 + ctas - 1) / ctas);
-  sp = std::max(1, std::min(sp, nkb));
-  const int kbps = (nkb + sp - 1) / sp;
-  cfg->splits = (nkb + kbps - 1) / kbps;
+  cfg->splits = fz::split_count(L.nkb, sp);
   return EVC_OK;
 }
 
@@ -837,45 +946,44 @@ int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_c
   const int cch = (c_in + 31) / 32;
   const int64_t nb = (c_out + bn - 1) / bn, nkb = (int64_t)kh * kw * cch;
   for (int64_t b = 0; b < nb; ++b)
-    for (int64_t kb = 0; kb < nkb; ++kb) {
-      const int tap = (int)(kb / cch), c0 = (int)(kb % cch) * 32;
-      const int r = tap / kw, q = tap % kw;
-      float* hi = out + ((b * nkb + kb) * 2) * bn * 32;
-      float* lo = hi + (int64_t)bn * 32;
-      for (int row = 0; row < bn; ++row)
-        for (int e = 0; e < 32; ++e) {
-          const int64_t n = b * bn + row;
-          const int c = c0 + e;
-          const float x = (n < c_out && c < c_in) ? w[((n * c_in + c) * kh + r) * kw + q] : 0.0f;
-          uint32_t bits;
-          memcpy(&bits, &x, 4);
-          bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32 (as tf32_head, common.cuh)
-          float hv;
-          memcpy(&hv, &bits, 4);
-          // 128B swizzle: 16-byte chunk j of row `row` lives at chunk (j ^ (row & 7))
-          const int j = e / 4, sub = e % 4;
-          const int64_t pos = (int64_t)row * 32 + ((j ^ (row & 7)) * 4) + sub;
-          hi[pos] = hv;
-          lo[pos] = x - hv;
+    for (int r = 0; r < kh; ++r)
+      for (int q = 0; q < kw; ++q)
+        for (int ch = 0; ch < cch; ++ch) {
+          // tap mode: K-block (tap, chunk); row mode: K-block (kernel row, chunk) holding its kw taps
+          const int64_t blk = cfg->row ? ((int64_t)r * cch + ch) * kw + q : ((int64_t)r * kw + q) * cch + ch;
+          float* hi = out + ((b * nkb + blk) * 2) * bn * 32;
+          float* lo = hi + (int64_t)bn * 32;
+          const int c0 = ch * 32;
+          for (int row = 0; row < bn; ++row)
+            for (int e = 0; e < 32; ++e) {
+              const int64_t n = b * bn + row;
+              const int c = c0 + e;
+              const float x = (n < c_out && c < c_in) ? w[((n * c_in + c) * kh + r) * kw + q] : 0.0f;
+              uint32_t bits;
+              memcpy(&bits, &x, 4);
+              bits = (bits + 0x1000u) & 0xFFFFE000u;  // round to nearest TF32 (as tf32_head, common.cuh)
+              float hv;
+              memcpy(&hv, &bits, 4);
+              // 128B swizzle: 16-byte chunk j of row `row` lives at chunk (j ^ (row & 7))
+              const int j = e / 4, sub = e % 4;
+              const int64_t pos = (int64_t)row * 32 + ((j ^ (row & 7)) * 4) + sub;
+              hi[pos] = hv;
+              lo[pos] = x - hv;
+            }
         }
-    }
   return EVC_OK;
 }
 
 int64_t evc_conv_fused_ctas(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
-  if (!g || !cfg || cfg->rh <= 0 || cfg->rw <= 0 || !fz::valid_bn(cfg->bn)) return -1;
-  const int nkb = g->kh * g->kw * ((g->c_in + 31) / 32);
-  int sp = std::max(1, std::min<int>(cfg->splits, nkb));
-  const int kbps = (nkb + sp - 1) / sp;
-  sp = (nkb + kbps - 1) / kbps;
-  return (int64_t)((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw) *
-         ((g->c_out + cfg->bn - 1) / cfg->bn) * sp;
+  if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
+  const fz::Layout L = fz::layout_of(g, cfg);
+  return (int64_t)L.R * ((g->c_out + cfg->bn - 1) / cfg->bn) * fz::split_count(L.nkb, cfg->splits);
 }
 
 int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg, int32_t S) {
-  if (!g || !cfg || cfg->rh <= 0 || cfg->rw <= 0 || cfg->bn <= 0) return -1;
-  return (int64_t)S * ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw) *
-         ((g->c_out + cfg->bn - 1) / cfg->bn);
+  if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
+  const fz::Layout L = fz::layout_of(g, cfg);
+  return (int64_t)S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);
 }
 
 int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
@@ -886,28 +994,43 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                    void* stream) {
   EVC_CHECK_ARG(g && cfg && in_hwc && wpack && S > 0 && fz::valid_bn(cfg->bn), "conv_fused: null argument");
   EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
-  EVC_CHECK_ARG(cfg->rh * cfg->rw == fz::BM && (cfg->rw == 32 || cfg->rw == 16 || cfg->rw == 8) &&
-                    cfg->rw * g->stride <= 256 && cfg->rh * g->stride <= 256,
+  EVC_CHECK_ARG(cfg->row ? (g->stride == 1 && cfg->bn <= 128 && g->kw <= 9)
+                         : (cfg->rh * cfg->rw == fz::BM && (cfg->rw == 32 || cfg->rw == 16 || cfg->rw == 8) &&
+                            cfg->rw * g->stride <= 256 && cfg->rh * g->stride <= 256),
                 "conv_fused: bad region shape");
   EVC_CHECK_ARG(cfg->splits >= 1 && cfg->splits <= 16, "conv_fused: splits must lie in [1, 16]");
-  EVC_CHECK_ARG(cp % 32 == 0 && cp >= g->c_in && hwc_stride % 32 == 0, "conv_fused: shadow layout (cp % 32)");
+  const int Hp = g->H + 2 * g->pad, Wp = g->W + 2 * g->pad;
+  EVC_CHECK_ARG(cp % 32 == 0 && cp >= g->c_in && hwc_stride % 32 == 0 && hwc_stride >= (int64_t)Hp * Wp * 2 * cp,
+                "conv_fused: shadow layout (cp % 32, (H + 2 pad) x (W + 2 pad) pixels per session)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
   EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 32 == 0 && sp->cp >= g->c_out && sp->hwc_stride % 32 == 0 &&
-                        sp->flags && sp->fany && sp->partials),
+                        sp->pitch >= g->Wo && sp->flags && sp->fany && sp->partials),
                 "conv_fused: fused sparsify needs the shadow, flags, fany and partials (incremental mode)");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && in_true && bulk &&
                           ((act >= 0 ? act_out->flags : (out ? out->flags : nullptr)) != nullptr)),
                 "conv_fused: incremental mode needs masks, fany, table, rstate and counters");
+  const fz::Layout L = fz::layout_of(g, cfg);
   fz::EncodeTiled enc = fz::encoder();
   CUtensorMap map;
-  const cuuint64_t dims[4] = {(cuuint64_t)(2 * cp), (cuuint64_t)g->W, (cuuint64_t)g->H, (cuuint64_t)S};
-  const cuuint64_t strides[3] = {(cuuint64_t)cp * 8, (cuuint64_t)g->W * cp * 8, (cuuint64_t)hwc_stride * 4};
-  const cuuint32_t box[4] = {32, (cuuint32_t)(cfg->rw * g->stride), (cuuint32_t)(cfg->rh * g->stride), 1};
-  const cuuint32_t estr[4] = {1, (cuuint32_t)g->stride, (cuuint32_t)g->stride, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in_hwc), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (cfg->row) {  // (channels, flattened padded pixels, session)
+    const cuuint64_t dims[3] = {(cuuint64_t)(2 * cp), (cuuint64_t)Hp * Wp, (cuuint64_t)S};
+    const cuuint64_t strides[2] = {(cuuint64_t)cp * 8, (cuuint64_t)hwc_stride * 4};
+    const cuuint32_t box[3] = {32, (cuuint32_t)(fz::BM + g->kw - 1), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(in_hwc), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {  // (channels, padded x, padded y, session), traversal stride = conv stride
+    const cuuint64_t dims[4] = {(cuuint64_t)(2 * cp), (cuuint64_t)Wp, (cuuint64_t)Hp, (cuuint64_t)S};
+    const cuuint64_t strides[3] = {(cuuint64_t)cp * 8, (cuuint64_t)Wp * cp * 8, (cuuint64_t)hwc_stride * 4};
+    const cuuint32_t box[4] = {32, (cuuint32_t)(cfg->rw * g->stride), (cuuint32_t)(cfg->rh * g->stride), 1};
+    const cuuint32_t estr[4] = {1, (cuuint32_t)g->stride, (cuuint32_t)g->stride, 1};
+    r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(in_hwc), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) {
     set_error("evc: conv_fused: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return EVC_ECUDA;
@@ -929,11 +1052,17 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   a.RW = cfg->rw;
   a.RHn = (g->Ho + cfg->rh - 1) / cfg->rh;
   a.RWn = (g->Wo + cfg->rw - 1) / cfg->rw;
-  a.cchunks = (g->c_in + 31) / 32;
-  a.nkb = g->kh * g->kw * a.cchunks;
-  a.splits = std::max(1, std::min<int>(cfg->splits, a.nkb));
+  a.row = cfg->row;
+  a.P = Wp;
+  a.R = L.R;
+  a.ns = L.ns;
+  a.stage = L.stage;
+  a.a_half = L.a_half;
+  a.b_bytes = L.b_bytes;
+  a.cchunks = L.cchunks;
+  a.nkb = L.nkb;
+  a.splits = fz::split_count(a.nkb, cfg->splits);
   a.kb_per_split = (a.nkb + a.splits - 1) / a.splits;
-  a.splits = (a.nkb + a.kb_per_split - 1) / a.kb_per_split;
   a.bn = cfg->bn;
   a.th = g->th;
   a.tw = g->tw;
@@ -967,6 +1096,7 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
     a.sp_hwc = sp->hwc;
     a.sp_hs = sp->hwc_stride;
     a.sp_cp = sp->cp;
+    a.sp_pitch = sp->pitch;
     a.sp_GH = (g->Ho + g->th - 1) / g->th;
     a.sp_GW = (g->Wo + g->tw - 1) / g->tw;
     a.sp_flags = sp->flags;

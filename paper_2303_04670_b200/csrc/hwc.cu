@@ -1,7 +1,8 @@
 // Channels-innermost ("HWC") hi/lo shadow of a channel-planar tensor: the
 // A-operand layout of the TMA-fed conv GEMM (conv_fused.cu, see hwc_store in
 // common.cuh): per pixel the TF32 heads of the cp (= C rounded up to 32)
-// channels, then their tails.
+// channels, then their tails.  Rows are `pitch` pixels apart: the consumer conv
+// keeps a zero border of its padding around the interior (y points at pixel (0, 0)).
 
 #include "common.cuh"
 
@@ -9,9 +10,7 @@ namespace evc {
 
 // CHW -> channels-innermost shadow (channel stride cp), 32x32 tiles through SMEM
 // so both the planar reads and the channel-contiguous writes are coalesced.
-__global__ void __launch_bounds__(256) k_to_hwc(TView x, float* __restrict__ y, int64_t ys, int cp) {
-  pdl_wait();
-  pdl_trigger();
+__global__ void __launch_bounds__(256) k_to_hwc(TView x, float* __restrict__ y, int64_t ys, int cp, int pitch) {
   __shared__ float t[32][33];
   pdl_wait();
   pdl_trigger();
@@ -29,7 +28,10 @@ __global__ void __launch_bounds__(256) k_to_hwc(TView x, float* __restrict__ y, 
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const int p = p0 + ty + 8 * k, c = c0 + tx;
-    if (p < HW && c < x.C) hwc_store(dst + (int64_t)p * 2 * cp, cp, c, t[tx][ty + 8 * k]);
+    if (p < HW && c < x.C) {
+      const int py = p / x.W, px = p - py * x.W;
+      hwc_store(dst + ((int64_t)py * pitch + px) * 2 * cp, cp, c, t[tx][ty + 8 * k]);
+    }
   }
 }
 
@@ -41,11 +43,12 @@ extern "C" {
 
 int32_t evc_hwc_channels(int32_t c) { return (c + 31) / 32 * 32; }
 
-int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp, int32_t S, void* stream) {
-  EVC_CHECK_ARG(x && x->vals && y && S > 0 && cp >= x->C && cp % 32 == 0, "to_hwc: bad argument");
+int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp, int32_t pitch, int32_t S,
+               void* stream) {
+  EVC_CHECK_ARG(x && x->vals && y && S > 0 && cp >= x->C && cp % 32 == 0 && pitch >= x->W, "to_hwc: bad argument");
   TView v = view_of(*x);
   dim3 grid(cdiv(v.H * v.W, 32), cdiv(v.C, 32), S);
-  const cudaError_t e = launch_pdl(k_to_hwc, grid, dim3(256), 0, as_stream(stream), v, y, y_stride, cp);
+  const cudaError_t e = launch_pdl(k_to_hwc, grid, dim3(256), 0, as_stream(stream), v, y, y_stride, cp, pitch);
   if (e != cudaSuccess) {
     set_error(std::string("evc: to_hwc: ") + cudaGetErrorString(e));
     return EVC_ECUDA;

@@ -29,6 +29,7 @@ struct USArgs {
   int* ticket;
   float* hwc;
   int64_t hs;
+  int hp;  // shadow row pitch (pixels)
   uint8_t* fany;  // optional any-channel tile map of y (OR-accumulated, zeroed per step)
   int cp, write_chw, delta_zero, f, mode;
   int XR, XC;  // staged input footprint (rows, cols) per CTA
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       if (stage) {
         s_y[(r * 32 + xl) * 33 + cl] = o;
       } else if (a.hwc) {
-        hwc_store(a.hwc + (int64_t)s * a.hs + ((int64_t)u * y.W + v) * 2 * a.cp, a.cp, c, o);
+        hwc_store(a.hwc + (int64_t)s * a.hs + ((int64_t)u * a.hp + v) * 2 * a.cp, a.cp, c, o);
       }
       if (!a.delta_zero) *dp = nd;
       ss += (double)corr * (double)corr;
@@ -173,10 +174,10 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
-      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * y.W * 2 * a.cp + c0 + lane;
+      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * 2 * a.cp + c0 + lane;
       for (int r = 0; r < nrow; ++r)
         for (int xq = warp; xq < ncol; xq += US_THREADS / 32)
-          hwc_store(dst + ((int64_t)r * y.W + x0 + xq) * 2 * a.cp, a.cp, 0, s_y[(r * 32 + xq) * 33 + lane]);
+          hwc_store(dst + ((int64_t)r * a.hp + x0 + xq) * 2 * a.cp, a.cp, 0, s_y[(r * 32 + xq) * 33 + lane]);
     }
   }
   ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
@@ -225,7 +226,8 @@ int64_t evc_upsample_sparsify_partials(const evc_tensor* y) {
 int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, float* delta, int64_t ds,
                           uint8_t* dlive, const evc_tensor* y, double* k, double* norm_ema, double tp,
                           double ema_decay, double* partials, int32_t* ticket, float* hwc, int32_t cp,
-                          int64_t hwc_stride, uint8_t* fany, int32_t write_chw, int32_t delta_zero, int32_t S, void* stream) {
+                          int64_t hwc_stride, int32_t hwc_pitch, uint8_t* fany, int32_t write_chw,
+                          int32_t delta_zero, int32_t S, void* stream) {
   EVC_CHECK_ARG(x && y && x->flags && y->flags && delta && dlive && k && norm_ema && partials && S > 0,
                 "upsample_sparsify: null argument");
   EVC_CHECK_ARG(y->tw <= 32 && y->th <= 8, "upsample_sparsify: tiles wider than 32 or taller than 8");
@@ -233,7 +235,8 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
   EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");
   EVC_CHECK_ARG(write_chw || hwc, "upsample_sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || (cp >= y->C && cp % 32 == 0), "upsample_sparsify: shadow channel count must cover C, multiple of 32");
+  EVC_CHECK_ARG(!hwc || (cp >= y->C && cp % 32 == 0 && hwc_pitch >= y->W),
+                "upsample_sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   USArgs a;
   a.x = view_of(*x);
   a.y = view_of(*y);
@@ -248,6 +251,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.ticket = ticket;
   a.hwc = hwc;
   a.hs = hwc_stride;
+  a.hp = hwc_pitch;
   a.cp = cp;
   a.fany = fany;
   a.write_chw = write_chw;

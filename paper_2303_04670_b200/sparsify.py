@@ -70,7 +70,7 @@ def sparsify_step(x: IncrementTensor, state: SparsifyState) -> IncrementTensor:
     dy = _lib.tdesc(_lib.ptr(yv), _lib.ptr(yf), 0, 0, c, h, w, tile.h, tile.w)
     ticket = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.check(lib.evc_sparsify(dx, _lib.ptr(state.delta), 0, _lib.ptr(dlive), dy, _lib.ptr(sc) + 8, _lib.ptr(sc),
-                                state.tp, state.ema_decay, _lib.ptr(part), _lib.ptr(ticket), None, 0, 0, None, 1, 0, 1, s),
+                                state.tp, state.ema_decay, _lib.ptr(part), _lib.ptr(ticket), None, 0, 0, 0, None, 1, 0, 1, s),
                "sparsify")
     ne, k = sc.tolist()
     state.norm_ema = ne

@@ -286,7 +286,11 @@ class ConvPlan:
         if kernel == "tc" and lib.evc_conv_fused_supported(self.g):
             self.path = "fused"
             self.cp = int(lib.evc_hwc_channels(c_in))
-            self.hwc = torch.zeros((S, h, w, 2 * self.cp), dtype=torch.float32, device=weight.device)  # heads | tails
+            # hi/lo shadow with a zero border of the conv's padding: (S, H + 2p, W + 2p, heads | tails)
+            self.pitch = w + 2 * pad
+            self.hwc = torch.zeros((S, h + 2 * pad, self.pitch, 2 * self.cp), dtype=torch.float32,
+                                   device=weight.device)
+            self.hwc_interior = self.hwc.data_ptr() + 4 * (pad * self.pitch + pad) * 2 * self.cp
             self.cfg = _lib.EvcConvCfg()
             _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
             host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)
@@ -309,7 +313,7 @@ class ConvPlan:
         """(fn, args-without-stream) mirroring the conv input into the HWC shadow, or None."""
         if self.path != "fused":
             return None
-        return _lib.lib().evc_to_hwc, (din, self.hwc.data_ptr(), self.hwc[0].numel(), self.cp, self.S)
+        return _lib.lib().evc_to_hwc, (din, self.hwc_interior, self.hwc[0].numel(), self.cp, self.pitch, self.S)
 
     def mask_args(self, din, dout, scratch, in_true, tile_list, tile_count, meter):
         """evc_conv_mask arguments of the unfused paths (stream appended by the caller)."""

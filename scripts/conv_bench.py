@@ -84,8 +84,7 @@ def main():
         tot += us
         if args.trace:
             cfg = plan.cfg
-            R = -(-ho // cfg.rh) * -(-wo // cfg.rw)
-            n_cta = R * -(-co // cfg.bn) * cfg.splits
+            n_cta = int(lib.evc_conv_fused_ctas(plan.g, cfg))
             tb = torch.zeros(n_cta * 16, dtype=torch.int64, device=dev)
             lib.evc_conv_trace(tb.data_ptr())
             fn, fa = plan.fused(din, None if act else dout, fany=fany.data_ptr(), in_true=cnt.data_ptr(),

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
   float* s_y = us_dyn;                // [(row * 32 + col) * 33 + channel] staged output (shadow transpose)
   float* s_x = us_dyn + 8 * 32 * 33;  // [channel][XR][XC] input footprint of this CTA
   // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
-  __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8];
+  __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8], s_tj[32];
   __shared__ float s_cw0[32], s_cw1[32], s_rw0[8], s_rw1[8];
   const TView& y = a.y;
   const int jc = blockIdx.x % a.nJC, rest = blockIdx.x / a.nJC;
@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
   }
   if (threadIdx.x < ncol) {
     const int v = x0 + threadIdx.x;
+    s_tj[threadIdx.x] = threadIdx.x / y.tw;
     if (a.mode == 0) {
       s_ci0[threadIdx.x] = s_ci1[threadIdx.x] = v / a.f;
       s_cw0[threadIdx.x] = 1.0f;
@@ -112,12 +113,47 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     // every global load is issued up front, the upsample then reads shared memory
     const int rlo = s_ri0[0], nr = s_ri1[nrow - 1] - rlo + 1;
     const int clo = s_ci0[0], ncl = s_ci1[ncol - 1] - clo + 1;
+    const int cs = (a.XR * a.XC) | 1;  // odd channel stride: lane-per-channel reads are bank-conflict free
     for (int e = threadIdx.x; e < nc * nr * ncl; e += US_THREADS) {
       const int cc = e % ncl, t2 = e / ncl;
       const int rr = t2 % nr, cl = t2 / nr;
-      s_x[(cl * a.XR + rr) * a.XC + cc] = a.x.plane(s, c0 + cl)[(int64_t)(rlo + rr) * a.x.W + clo + cc];
+      s_x[cl * cs + rr * a.XC + cc] = a.x.plane(s, c0 + cl)[(int64_t)(rlo + rr) * a.x.W + clo + cc];
     }
     __syncthreads();
+    const bool fast = a.delta_zero && !use_k && !a.write_chw && a.hwc;
+    if (fast) {
+      // t_p = 0 fast path: lane = channel, warps stride over the output pixels; each pixel's
+      // 32 channels go straight to the shadow as one 128-byte run of heads and one of tails
+      const int cl = lane;
+      if (cl < nc) {
+        float* dst = a.hwc + (int64_t)s * a.hs + c0 + cl + (int64_t)x0 * 2 * a.cp;
+        const float* xc = s_x + cl * cs;
+        for (int r = 0; r < nrow; ++r) {
+          const float* xr0 = xc + (s_ri0[r] - rlo) * a.XC;
+          const float* xr1 = xc + (s_ri1[r] - rlo) * a.XC;
+          const float rw0 = s_rw0[r], rw1 = s_rw1[r];
+          float* drow = dst + (int64_t)(r0 + r) * a.hp * 2 * a.cp;
+          for (int xq = warp; xq < ncol; xq += US_THREADS / 32) {
+            const int ti = cl * nj + s_tj[xq];
+            if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
+            const int ci0 = s_ci0[xq] - clo;
+            float up;
+            if (a.mode == 0) {
+              up = xr0[ci0];
+            } else {  // same float32 op order as upsample_at (rows first, then columns)
+              const int ci1 = s_ci1[xq] - clo;
+              const float ra = __fadd_rn(__fmul_rn(xr0[ci0], rw0), __fmul_rn(xr1[ci0], rw1));
+              const float rb = __fadd_rn(__fmul_rn(xr0[ci1], rw0), __fmul_rn(xr1[ci1], rw1));
+              up = __fadd_rn(__fmul_rn(ra, s_cw0[xq]), __fmul_rn(rb, s_cw1[xq]));
+            }
+            const float o = __fadd_rn(0.0f, up);
+            hwc_store(drow + xq * 2 * a.cp, a.cp, 0, o);
+            ss += (double)o * (double)o;
+            if (o != 0.0f) s_ny[ti] = 1;
+          }
+        }
+      }
+    } else {
     // lane = output column (ncol <= 32); warp w owns channels w, w + 8, ...
     const bool col_ok = lane < ncol;
     const int xl = lane, jl_lane = lane / y.tw;
@@ -132,12 +168,12 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
         continue;
       }
       const int c = c0 + cl, u = r0 + r, v = x0 + xl;
-      const float* xr0 = s_x + (cl * a.XR + s_ri0[r] - rlo) * a.XC;
+      const float* xr0 = s_x + cl * cs + (s_ri0[r] - rlo) * a.XC;
       float up;
       if (a.mode == 0) {
         up = xr0[ci0];
       } else {  // same float32 op order as upsample_at (rows first, then columns)
-        const float* xr1 = s_x + (cl * a.XR + s_ri1[r] - rlo) * a.XC;
+        const float* xr1 = s_x + cl * cs + (s_ri1[r] - rlo) * a.XC;
         const float rw0 = s_rw0[r], rw1 = s_rw1[r];
         const float ra = __fadd_rn(__fmul_rn(xr0[ci0], rw0), __fmul_rn(xr1[ci0], rw1));
         const float rb = __fadd_rn(__fmul_rn(xr0[ci1], rw0), __fmul_rn(xr1[ci1], rw1));
@@ -165,6 +201,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       if (o != 0.0f) s_ny[ti] = 1;
       if (nd != 0.0f) s_nd[ti] = 1;
     }
+    }
     __syncthreads();
     for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
       const int cl = t / nj, jl = t % nj;
@@ -173,7 +210,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i) * y.GW + j0 + jl] = 1;  // benign race: all store 1
       a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
-    if (stage && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
+    if (stage && !fast && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
       float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * 2 * a.cp + c0 + lane;
       for (int r = 0; r < nrow; ++r)
         for (int xq = warp; xq < ncol; xq += US_THREADS / 32)
@@ -262,7 +299,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   dim3 grid((unsigned)(a.y.GH * a.nCG * a.nJC), (unsigned)S);
   a.XR = y->th / factor + 3;
   a.XC = a.CW / factor + 3;
-  const size_t smem = sizeof(float) * (8 * 32 * 33 + (size_t)US_C * a.XR * a.XC);
+  const size_t smem = sizeof(float) * (8 * 32 * 33 + (size_t)US_C * ((a.XR * a.XC) | 1));
   launch_pdl(k_up_sparsify, dim3(grid), dim3(US_THREADS), smem, as_stream(stream), a);
   EVC_LAUNCH_CHECK("upsample_sparsify");
   return EVC_OK;

@@ -175,6 +175,7 @@ typedef struct evc_conv_cfg {
   int32_t row;    /* 1: row mode (stride 1): regions = 128 consecutive sites of the output grid
                      flattened with pitch W + 2 pad; a K-block is one kernel row x 32 channels,
                      loaded once (128 + kw - 1 shadow pixels) for all kw taps */
+  int32_t thin;   /* 1: CUDA-core fp32 path (C_in <= 8 or C_out <= 8, C_out <= 32), tap-mode regions */
 } evc_conv_cfg;
 
 /* 1 if the fused path handles this geometry (pad < kernel, stride <= 8). */
@@ -190,8 +191,9 @@ int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg
 /* in_hwc: channels-innermost shadow of the input (see evc_to_hwc).
  * Incremental mode (dense == 0): `in` supplies the per-channel input flags,
  * fany[s][tile] the any-channel map (evc_tile_any, or written by the producing
- * sparsify), table = evc_conv_table_fill output; in_true[s] (int32) and bulk[s]
- * (int64) are ACCUMULATED (zero them per step) and resolved by evc_meter_step.
+ * sparsify), table = evc_conv_table_fill output; every CTA writes its meter partial
+ * meter_part[(s * evc_conv_fused_ctas + cta) * 2 + {0, 1}] (int64, no zeroing needed),
+ * resolved by evc_meter_step.
  * Output flags are written to act_out when act >= 0, else to out.
  * out may be NULL when act >= 0 (the conv values are then not materialised);
  * act_out->vals may be NULL when sp != NULL (the activation is only read through
@@ -217,8 +219,8 @@ typedef struct evc_conv_sparsify {
 int64_t evc_conv_fused_ctas(const evc_conv_geom* g, const evc_conv_cfg* cfg); /* per session */
 int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
                    int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
-                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int32_t* in_true,
-                   int64_t* bulk, const evc_tensor* out, int32_t act, float alpha, float* acc,
+                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
+                   const evc_tensor* out, int32_t act, float alpha, float* acc,
                    int64_t acc_stride, const evc_tensor* act_out, const evc_conv_sparsify* sp,
                    int32_t dense, int32_t S, void* stream);
 /* Debug: subsequent evc_conv_fused launches record per-CTA phase clocks into
@@ -238,15 +240,26 @@ typedef struct evc_sp_node {
   double tp, decay;
 } evc_sp_node;
 
+/* One meter node (conv / linear) of the end-of-step bookkeeping. */
+typedef struct evc_meter_node {
+  const int64_t* part; /* fused conv: per-CTA partials [S][n][2] (live input flags, weighted
+                          meter term) written by evc_conv_fused; NULL: in_true / perf_step of
+                          this node are already final (linear, unfused conv) */
+  int64_t n;           /* partials per session */
+  int64_t nflags;      /* input tile flags per session */
+  int64_t dense;       /* dense-equivalent FLOPs */
+  int32_t c_out;
+  int32_t reserved;
+} evc_meter_node;
+
 /* End-of-step bookkeeping in one launch (graph.py:617-636):
- *  - n meter nodes x S sessions: mode[l] = C_out for a fused conv (performed =
- *    0 / dense / 2*C_out*bulk by the live-flag count, increment_ops.py:148-154,191),
- *    0 for a node whose perf_step is already final; then perf_cum += perf_step
- *    and the false-tile fraction ff_last = 1 - in_true / nflags, ff_sum += ff_last;
+ *  - n meter nodes (nodes: DEVICE array) x S sessions: a fused conv's performed =
+ *    0 / dense / 2*C_out*(weighted term) by its live-flag count (increment_ops.py:148-154,
+ *    191), written to in_true[l*S + s] and perf_step; then perf_cum += perf_step and
+ *    the false-tile fraction ff_last = 1 - in_true / nflags, ff_sum += ff_last;
  *  - n_sp sparsify nodes (sp_nodes: DEVICE array): norm_ema / k update from the
  *    deferred partial sums in a fixed order (sparsify.py:72-76). */
-int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* bulk,
-                   const int64_t* nflags, const int64_t* dense, const int32_t* mode,
+int evc_meter_step(const evc_meter_node* nodes, int32_t n, int32_t S, int32_t* in_true,
                    int64_t* perf_step, int64_t* perf_cum, double* ff_last, double* ff_sum,
                    const evc_sp_node* sp_nodes, int32_t n_sp, void* stream);
 

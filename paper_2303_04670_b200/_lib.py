@@ -38,13 +38,18 @@ class EvcConvGeom(C.Structure):
 
 
 class EvcConvCfg(C.Structure):
-    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits", "row")]
+    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits", "row", "thin")]
 
 
 class EvcConvSparsify(C.Structure):
     _fields_ = [("hwc", C.c_void_p), ("hwc_stride", C.c_int64), ("cp", C.c_int32), ("pitch", C.c_int32),
                 ("flags", C.c_void_p),
                 ("fstride", C.c_int64), ("fany", C.c_void_p), ("partials", C.c_void_p)]
+
+
+class EvcMeterNode(C.Structure):
+    _fields_ = [("part", C.c_void_p), ("n", C.c_int64), ("nflags", C.c_int64), ("dense", C.c_int64),
+                ("c_out", C.c_int32), ("reserved", C.c_int32)]
 
 
 class EvcSpNode(C.Structure):
@@ -88,11 +93,11 @@ _PROTOS = {
     "evc_conv_fused_pack": (_I32, [_P, _G, _CF, _P]),
     "evc_conv_fused_state_len": (_I64, [_G, _CF, _I32]),
     "evc_conv_fused_ctas": (_I64, [_G, _CF]),
-    "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
+    "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
                               _SP, _I32, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
     "evc_conv_trace": (_I32, [_P]),
-    "evc_meter_step": (_I32, [_I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I32, _P]),
+    "evc_meter_step": (_I32, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _P]),
     "evc_conv_workspace": (_I64, [_G, _I64, _I32]),
     "evc_conv_gemm": (_I32, [_G, _T, _P, _P, _P, _T, _P, _P, _P, _I32, _I32, _P, _P]),
     "evc_conv_tc_pack_len": (_I64, [_I32, _I64]),

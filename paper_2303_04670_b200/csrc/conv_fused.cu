@@ -163,8 +163,7 @@ struct Args {
   uint8_t* oflags;  // output flag planes (conv output, or the fused activation's output)
   int64_t ofs;
   uint8_t* rstate;  // [S*R][nb]
-  int32_t* in_true;
-  unsigned long long* bulk;
+  long long* mpart;  // [S][CTAs per session][2]: live input flags, weighted meter term (no atomics)
   // outputs
   float* out;  // conv values (nullable when the activation is fused and nothing else reads them)
   int64_t ovs;
@@ -251,11 +250,18 @@ __device__ __noinline__ void side_work(const Args& a, int s, int q, int Qs, int 
       for (int qq = 0; qq < gp[3]; ++qq) live |= Fc[(gp[0] + p) * GWi + gp[2] + qq];
     if (live) w += gp[4];
   }
-  cnt = (int)warp_sum_ll(cnt);
-  w = warp_sum_ll(w);
+  // one partial per CTA (the two side-work warps meet at a named barrier): no global atomics
+  __shared__ long long s_mp[2][2];
+  const long long c2 = warp_sum_ll(cnt), w2 = warp_sum_ll(w);
   if ((t & 31) == 0) {
-    if (cnt) atomicAdd(a.in_true + s, cnt);
-    if (w) atomicAdd(a.bulk + s, (unsigned long long)w);
+    s_mp[t >> 5][0] = c2;
+    s_mp[t >> 5][1] = w2;
+  }
+  asm volatile("bar.sync 1, 64;" ::: "memory");
+  if (t == 0) {
+    long long* mp = a.mpart + ((int64_t)s * Qs + q) * 2;
+    mp[0] = s_mp[0][0] + s_mp[1][0];
+    mp[1] = s_mp[0][1] + s_mp[1][1];
   }
 }
 
@@ -359,6 +365,8 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   return ss;
 }
 
+
+__device__ __forceinline__ int64_t rs_of(int reg) { return reg; }  // thin path: one channel block
 
 // Output site of TMEM lane m in region rr.
 __device__ __forceinline__ void site_of(const Args& a, int rr, int m, int& u, int& x) {
@@ -734,6 +742,100 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
   }
 }
 
+// CUDA-core path for thin convs (C_in <= 8 or C_out <= 8, C_out <= 32): the prediction heads
+// (1x1, C_out = 2) and the 4-channel input layer waste most of a 128-row tensor-core tile and
+// all of its 32-channel K-blocks.  Same regions, region test, flags / meter side work and fused
+// epilogue as k_conv_fused; the values are exact fp32 FFMA sums over the hi/lo shadow
+// (head + tail = the float32 input exactly).  One thread per output site, weights in shared
+// memory as [tap][c_in][c_out].
+constexpr int THIN_THREADS = BM;
+__global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
+                                                            const __grid_constant__ Args a) {
+  extern __shared__ float s_w[];  // [kh*kw][c_in][c_out]
+  __shared__ int s_flag[2];
+  __shared__ double s_red[THIN_THREADS / 32];
+  const int R = a.R;
+  const int reg = blockIdx.x, s = reg / R, rr = reg % R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = a.kh * a.kw * a.c_in * a.c_out;
+  for (int e = threadIdx.x; e < nw; e += THIN_THREADS) s_w[e] = a.wpack[e];
+  pdl_trigger();
+  pdl_wait();
+  int ulo = (rr / a.RWn) * a.RH, uhi = min(ulo + a.RH, a.Ho) - 1;
+  int xlo = (rr % a.RWn) * a.RW, xhi = min(xlo + a.RW, a.Wo) - 1;
+  if (warp == 0) {
+    int live = 1;
+    if (!a.dense) {
+      live = 0;
+      const int y_lo = max(0, ulo * a.stride - a.pad), y_hi = min(a.H - 1, uhi * a.stride - a.pad + a.kh - 1);
+      const int x_lo = max(0, xlo * a.stride - a.pad), x_hi = min(a.W - 1, xhi * a.stride - a.pad + a.kw - 1);
+      if (y_lo <= y_hi && x_lo <= x_hi) {
+        const int GWi = (a.W + a.tw - 1) / a.tw, GHi = (a.H + a.th - 1) / a.th;
+        const int ra = y_lo / a.th, nr = y_hi / a.th - ra + 1, ca = x_lo / a.tw, nc = x_hi / a.tw - ca + 1;
+        const uint8_t* fa = a.fany + (int64_t)s * GHi * GWi;
+        for (int e = lane; e < nr * nc; e += 32) live |= fa[(ra + e / nc) * GWi + ca + e % nc];
+      }
+      live = __any_sync(0xffffffffu, live);
+    }
+    if (lane == 0) {
+      s_flag[0] = live;
+      s_flag[1] = a.dense ? 0 : a.rstate[rs_of(reg)];
+    }
+  }
+  __syncthreads();
+  const int Qs = R, q = rr;
+  if (!a.dense && warp < 2) side_work(a, s, q, Qs, threadIdx.x);
+  const int m = threadIdx.x;
+  int u, x;
+  site_of(a, rr, m, u, x);
+  const bool valid = u < a.Ho && x < a.Wo;
+  double ssq = 0.0;
+  if (!s_flag[0]) {
+    if (!a.dense && s_flag[1]) {  // computed last step, dead now: restore exact zeros
+      for (int n = 0; n < a.c_out; ++n) {
+        if (!valid) break;
+        const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
+        if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
+        if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
+        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
+      }
+      if (threadIdx.x == 0) a.rstate[rs_of(reg)] = 0;
+    }
+  } else {
+    if (!a.dense && threadIdx.x == 0 && !s_flag[1]) a.rstate[rs_of(reg)] = 1;
+    float acc[32];
+#pragma unroll
+    for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
+    if (valid) {
+      const float* base = in_hwc + (int64_t)s * hwc_stride;
+      for (int r = 0; r < a.kh; ++r)
+        for (int q2 = 0; q2 < a.kw; ++q2) {
+          const float* px = base + ((int64_t)(u * a.stride + r) * a.P + x * a.stride + q2) * 2 * a.cp;
+          const float* wt = s_w + (r * a.kw + q2) * a.c_in * a.c_out;
+          for (int c = 0; c < a.c_in; ++c) {
+            const float xv = __fadd_rn(px[c], px[a.cp + c]);  // head + tail (exact)
+            const float* wc = wt + c * a.c_out;
+#pragma unroll
+            for (int n = 0; n < 32; ++n)
+              if (n < a.c_out) acc[n] = __fmaf_rn(xv, wc[n], acc[n]);
+          }
+        }
+    }
+    ssq += emit<16>(a, s, u, x, 0, 1, min(16, a.c_out), acc);
+    if (a.c_out > 16) ssq += emit<16>(a, s, u, x, 16, 1, a.c_out - 16, acc + 16);
+  }
+  if (a.sp_part) {
+    double v = warp_sum_d(ssq);
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < THIN_THREADS / 32; ++w) t += s_red[w];
+      a.sp_part[(int64_t)s * Qs + q] = t;
+    }
+  }
+}
+
 // any-channel tile map: fany[s][t] = OR_c flags[s][c][t]
 __global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
   pdl_wait();
@@ -747,40 +849,51 @@ __global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
   }
 }
 
-// End-of-step bookkeeping (graph.py:617-636), one launch: block 0 resolves the
-// meters of n meter nodes x S sessions -- conv nodes (mode = C_out) apply the
-// reference shortcuts from the live-flag count, linear nodes (mode 0) already
-// hold `performed` -- and the false-tile fractions; block 1 + j folds sparsify
-// node j's per-CTA sums of squares into norm_ema / k (sparsify.py:72-76) in a
-// fixed order.  k is first read by the NEXT step's sparsify of that node, so
-// folding at the end of the step is exactly the reference's sequence.
-__global__ void __launch_bounds__(256) k_meter_step(int n, int S, const int32_t* __restrict__ in_true,
-                                                    const long long* __restrict__ bulk,
-                                                    const long long* __restrict__ nflags,
-                                                    const long long* __restrict__ dense,
-                                                    const int32_t* __restrict__ mode, long long* perf_step,
-                                                    long long* perf_cum, double* ff_last, double* ff_sum,
+// End-of-step bookkeeping (graph.py:617-636), one launch.  Block (l, s) < n*S resolves meter
+// node l of session s: a fused conv sums its per-CTA partials (live input flags, weighted term;
+// integer, so exact in any order) and applies the reference's all-false / all-true shortcuts
+// (increment_ops.py:148-154); other nodes already hold `performed`.  Then perf_cum and the
+// false-tile fraction.  Block n*S + j folds sparsify node j's per-CTA sums of squares into
+// norm_ema / k (sparsify.py:72-76) in a fixed order; k is first read by the NEXT step's
+// sparsify of that node, so folding at the end of the step is the reference's sequence.
+__global__ void __launch_bounds__(256) k_meter_step(const evc_meter_node* __restrict__ nodes, int n, int S,
+                                                    int32_t* in_true, long long* perf_step, long long* perf_cum,
+                                                    double* ff_last, double* ff_sum,
                                                     const evc_sp_node* __restrict__ sp) {
   pdl_wait();
   pdl_trigger();
-  if (blockIdx.x > 0) {
-    const evc_sp_node nd = sp[blockIdx.x - 1];
+  if ((int)blockIdx.x >= n * S) {
+    const evc_sp_node nd = sp[blockIdx.x - n * S];
     sparsify_finalize_all(nd.partials, nd.n, nd.norm_ema, nd.k, nd.tp, nd.decay, 0, S);
     return;
   }
-  for (int e = threadIdx.x; e < n * S; e += blockDim.x) {
-    const int l = e / S;
-    const long long cnt = in_true[e];
-    long long p = perf_step[e];
-    if (mode[l] > 0) {
-      p = cnt == 0 ? 0LL : (cnt == nflags[l] ? dense[l] : 2LL * mode[l] * bulk[e]);
-      perf_step[e] = p;
+  const int l = blockIdx.x / S, s = blockIdx.x % S, e = l * S + s;
+  const evc_meter_node nd = nodes[l];
+  long long cnt, p;
+  if (nd.part) {
+    long long c = 0, w = 0;
+    const long long* mp = reinterpret_cast<const long long*>(nd.part) + (int64_t)s * nd.n * 2;
+    for (int64_t i = threadIdx.x; i < nd.n; i += blockDim.x) {
+      c += mp[2 * i];
+      w += mp[2 * i + 1];
     }
-    perf_cum[e] += p;
-    const double ff = __dsub_rn(1.0, __ddiv_rn((double)cnt, (double)nflags[l]));
-    ff_last[e] = ff;
-    ff_sum[e] = __dadd_rn(ff_sum[e], ff);
+    c = block_sum<long long>(c, [](long long v) { return warp_sum_ll(v); });
+    __syncthreads();
+    w = block_sum<long long>(w, [](long long v) { return warp_sum_ll(v); });
+    if (threadIdx.x != 0) return;
+    cnt = c;
+    in_true[e] = (int32_t)c;
+    p = cnt == 0 ? 0LL : (cnt == nd.nflags ? nd.dense : 2LL * nd.c_out * w);
+    perf_step[e] = p;
+  } else {
+    if (threadIdx.x != 0) return;
+    cnt = in_true[e];
+    p = perf_step[e];
   }
+  perf_cum[e] += p;
+  const double ff = __dsub_rn(1.0, __ddiv_rn((double)cnt, (double)nd.nflags));
+  ff_last[e] = ff;
+  ff_sum[e] = __dadd_rn(ff_sum[e], ff);
 }
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -851,6 +964,14 @@ struct Layout {
 static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   Layout L;
   L.cchunks = (g->c_in + 31) / 32;
+  if (cfg->thin) {
+    L.R = ((g->Ho + cfg->rh - 1) / cfg->rh) * ((g->Wo + cfg->rw - 1) / cfg->rw);
+    L.nkb = 1;
+    L.ns = 1;
+    L.a_half = L.b_bytes = 0;
+    L.stage = g->kh * g->kw * g->c_in * g->c_out * 4;  // weights in shared memory
+    return L;
+  }
   if (cfg->row) {
     L.a_half = ((BM + g->kw - 1 + 7) / 8) * 8 * 128;
     L.b_bytes = g->kw * 2 * cfg->bn * 128;
@@ -888,6 +1009,7 @@ int init_conv_fused() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, fz::k_tile_any) != cudaSuccess) rc = 1;
   if (cudaFuncGetAttributes(&fa, fz::k_meter_step) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin) != cudaSuccess) rc = 1;
   return rc ? EVC_ECUDA : EVC_OK;
 }
 
@@ -908,7 +1030,18 @@ int evc_conv_fused_supported(const evc_conv_geom* g) {
 int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits, evc_conv_cfg* cfg) {
   EVC_CHECK_ARG(g && cfg && S > 0, "conv_fused_config: null argument");
   // stride 1: row mode (halo rows loaded once for all kw taps); else tap mode over RH x RW regions
-  cfg->row = (g->stride == 1 && g->kw <= 9 && g->Wo == g->W + 2 * g->pad - g->kw + 1) ? 1 : 0;
+  cfg->thin = ((g->c_in <= 8 || g->c_out <= 8) && g->c_out <= 32 &&
+               (int64_t)g->kh * g->kw * g->c_in * g->c_out * 4 <= 48 * 1024)
+                  ? 1
+                  : 0;
+  cfg->row = (!cfg->thin && g->stride == 1 && g->kw <= 9 && g->Wo == g->W + 2 * g->pad - g->kw + 1) ? 1 : 0;
+  if (cfg->thin) {
+    cfg->rw = g->Wo > 16 ? 32 : (g->Wo > 8 ? 16 : 8);
+    cfg->rh = fz::BM / cfg->rw;
+    cfg->bn = 16;
+    cfg->splits = 1;
+    return EVC_OK;
+  }
   if (cfg->row) {
     cfg->rh = 1;
     cfg->rw = fz::BM;
@@ -936,6 +1069,7 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
 
 int64_t evc_conv_fused_pack_len(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
+  if (cfg->thin) return (int64_t)g->kh * g->kw * g->c_in * g->c_out;
   const int64_t nb = (g->c_out + cfg->bn - 1) / cfg->bn, nkb = (int64_t)g->kh * g->kw * ((g->c_in + 31) / 32);
   return nb * nkb * 2 * cfg->bn * 32;
 }
@@ -943,6 +1077,14 @@ int64_t evc_conv_fused_pack_len(const evc_conv_geom* g, const evc_conv_cfg* cfg)
 int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_cfg* cfg, float* out) {
   EVC_CHECK_ARG(w && g && cfg && out && fz::valid_bn(cfg->bn), "conv_fused_pack: bad argument");
   const int bn = cfg->bn, c_out = g->c_out, c_in = g->c_in, kh = g->kh, kw = g->kw;
+  if (cfg->thin) {  // plain fp32 [tap][c_in][c_out]
+    for (int r = 0; r < kh; ++r)
+      for (int q = 0; q < kw; ++q)
+        for (int c = 0; c < c_in; ++c)
+          for (int n = 0; n < c_out; ++n)
+            out[(((int64_t)r * kw + q) * c_in + c) * c_out + n] = w[(((int64_t)n * c_in + c) * kh + r) * kw + q];
+    return EVC_OK;
+  }
   const int cch = (c_in + 31) / 32;
   const int64_t nb = (c_out + bn - 1) / bn, nkb = (int64_t)kh * kw * cch;
   for (int64_t b = 0; b < nb; ++b)
@@ -977,18 +1119,20 @@ int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_c
 int64_t evc_conv_fused_ctas(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
   const fz::Layout L = fz::layout_of(g, cfg);
+  if (cfg->thin) return L.R;
   return (int64_t)L.R * ((g->c_out + cfg->bn - 1) / cfg->bn) * fz::split_count(L.nkb, cfg->splits);
 }
 
 int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg, int32_t S) {
   if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
   const fz::Layout L = fz::layout_of(g, cfg);
+  if (cfg->thin) return (int64_t)S * L.R;
   return (int64_t)S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);
 }
 
 int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
                    int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
-                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int32_t* in_true, int64_t* bulk,
+                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
                    const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
                    const evc_tensor* act_out, const evc_conv_sparsify* sp, int32_t dense, int32_t S,
                    void* stream) {
@@ -1007,14 +1151,16 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 32 == 0 && sp->cp >= g->c_out && sp->hwc_stride % 32 == 0 &&
                         sp->pitch >= g->Wo && sp->flags && sp->fany && sp->partials),
                 "conv_fused: fused sparsify needs the shadow, flags, fany and partials (incremental mode)");
-  EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && in_true && bulk &&
+  EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && meter_part &&
                           ((act >= 0 ? act_out->flags : (out ? out->flags : nullptr)) != nullptr)),
                 "conv_fused: incremental mode needs masks, fany, table, rstate and counters");
   const fz::Layout L = fz::layout_of(g, cfg);
   fz::EncodeTiled enc = fz::encoder();
   CUtensorMap map;
-  CUresult r;
-  if (cfg->row) {  // (channels, flattened padded pixels, session)
+  CUresult r = CUDA_SUCCESS;
+  if (cfg->thin) {
+    // no tensor map: the CUDA-core path reads the shadow directly
+  } else if (cfg->row) {  // (channels, flattened padded pixels, session)
     const cuuint64_t dims[3] = {(cuuint64_t)(2 * cp), (cuuint64_t)Hp * Wp, (cuuint64_t)S};
     const cuuint64_t strides[2] = {(cuuint64_t)cp * 8, (cuuint64_t)hwc_stride * 4};
     const cuuint32_t box[3] = {32, (cuuint32_t)(fz::BM + g->kw - 1), 1};
@@ -1081,8 +1227,7 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
     a.oflags = fo->flags;
     a.ofs = fo->fstride;
     a.rstate = rstate;
-    a.in_true = in_true;
-    a.bulk = reinterpret_cast<unsigned long long*>(bulk);
+    a.mpart = reinterpret_cast<long long*>(meter_part);
   }
   a.out = out ? out->vals : nullptr;
   a.ovs = out ? out->vstride : 0;
@@ -1106,6 +1251,18 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   }
   cudaStream_t st = as_stream(stream);
   cudaError_t e;
+  if (cfg->thin) {
+    EVC_CHECK_ARG(g->c_out <= 32 && L.stage <= 48 * 1024, "conv_fused: thin path needs C_out <= 32, small weights");
+    a.splits = 1;
+    e = launch_pdl(fz::k_conv_thin, dim3((unsigned)(S * L.R)), dim3(fz::THIN_THREADS), (size_t)L.stage, st, in_hwc,
+                   hwc_stride, a);
+    if (e != cudaSuccess) {
+      set_error(std::string("evc: conv_fused (thin) launch: ") + cudaGetErrorString(e));
+      return EVC_ECUDA;
+    }
+    EVC_LAUNCH_CHECK("conv_fused_thin");
+    return EVC_OK;
+  }
   switch (cfg->bn) {
     case 16: e = fz::launch<16>(map, a, st); break;
     case 32: e = fz::launch<32>(map, a, st); break;
@@ -1135,16 +1292,15 @@ int evc_tile_any(const evc_tensor* x, uint8_t* fany, int32_t S, void* stream) {
   return EVC_OK;
 }
 
-int evc_meter_step(int32_t n, int32_t S, const int32_t* in_true, const int64_t* bulk, const int64_t* nflags,
-                   const int64_t* dense, const int32_t* mode, int64_t* perf_step, int64_t* perf_cum,
-                   double* ff_last, double* ff_sum, const evc_sp_node* sp_nodes, int32_t n_sp, void* stream) {
-  EVC_CHECK_ARG(n > 0 && S > 0 && in_true && bulk && nflags && dense && mode && perf_step && perf_cum && ff_last &&
-                    ff_sum && n_sp >= 0 && (n_sp == 0 || sp_nodes),
+int evc_meter_step(const evc_meter_node* nodes, int32_t n, int32_t S, int32_t* in_true, int64_t* perf_step,
+                   int64_t* perf_cum, double* ff_last, double* ff_sum, const evc_sp_node* sp_nodes, int32_t n_sp,
+                   void* stream) {
+  EVC_CHECK_ARG(nodes && n > 0 && S > 0 && in_true && perf_step && perf_cum && ff_last && ff_sum && n_sp >= 0 &&
+                    (n_sp == 0 || sp_nodes),
                 "meter_step: null argument");
-  launch_pdl(fz::k_meter_step, dim3(1 + n_sp), dim3(256), 0, as_stream(stream), 
-      n, S, in_true, reinterpret_cast<const long long*>(bulk), reinterpret_cast<const long long*>(nflags),
-      reinterpret_cast<const long long*>(dense), mode, reinterpret_cast<long long*>(perf_step),
-      reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum, sp_nodes);
+  launch_pdl(fz::k_meter_step, dim3((unsigned)(n * S + n_sp)), dim3(256), 0, as_stream(stream), nodes, n, S, in_true,
+             reinterpret_cast<long long*>(perf_step), reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum,
+             sp_nodes);
   EVC_LAUNCH_CHECK("meter_step");
   return EVC_OK;
 }

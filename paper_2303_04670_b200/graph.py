@@ -664,7 +664,7 @@ class Graph:
             off[0] = o + int(nbytes)
             return o
 
-        o_cnt, o_bulk, o_perf = take(4 * nm * S), take(8 * nm * S), take(8 * nm * S)
+        o_cnt, o_perf = take(4 * nm * S), take(8 * nm * S)
         conv_off, fany_off, sp_off = [], [], []
         for node in self.nodes:
             if node.kind == "sparsify" and node.sp_fused_by is not None:
@@ -686,7 +686,6 @@ class Graph:
             st = self._slots[node.spec.id].store
             st.flags = self._zero[o:o + st.flags.numel()].view(st.flags.shape)
         self._cnt_step = self._zero[o_cnt:o_cnt + 4 * nm * S].view(torch.int32).view(nm, S)
-        self._bulk_step = self._zero[o_bulk:o_bulk + 8 * nm * S].view(torch.int64).view(nm, S)
         self._perf_step = self._zero[o_perf:o_perf + 8 * nm * S].view(torch.int64).view(nm, S)
         self._perf_cum = torch.zeros((nm, S), dtype=torch.int64, device=dev)
         self._ff_last = torch.zeros((nm, S), dtype=torch.float64, device=dev)
@@ -694,11 +693,18 @@ class Graph:
         self._ff_n = 0
         nflags = [int(np.prod(grid_shape(self.shapes[self._by_id[i].spec.inputs[0]], tile))) for i in meter_ids]
         self._dense_static = [self._dense_equiv(self._by_id[i]) for i in meter_ids]
-        modes = [self._by_id[i].plan.c_out if self._by_id[i].kind == "conv" and self._by_id[i].plan.path == "fused"
-                 else 0 for i in meter_ids]
-        self._meter_static = (torch.tensor(nflags or [1], dtype=torch.int64, device=dev),
-                              torch.tensor(self._dense_static or [0], dtype=torch.int64, device=dev),
-                              torch.tensor(modes or [0], dtype=torch.int32, device=dev))
+        # end-of-step meter table: fused convs resolve their per-CTA partials (no atomics)
+        mrec = (_lib.EvcMeterNode * nm)()
+        for i, nid in enumerate(meter_ids):
+            nd = self._by_id[nid]
+            part, npart, cout = None, 0, 0
+            if nd.kind == "conv" and nd.plan.path == "fused":
+                nd.mpart = torch.zeros(S * nd.plan.ctas * 2, dtype=torch.int64, device=dev)
+                part, npart, cout = nd.mpart.data_ptr(), nd.plan.ctas, nd.plan.c_out
+            mrec[i] = _lib.EvcMeterNode(part, npart, nflags[i], self._dense_static[i], cout, 0)
+        if not meter_ids:
+            mrec[0] = _lib.EvcMeterNode(None, 0, 1, 0, 0, 0)
+        self._meter_table = torch.from_numpy(np.frombuffer(bytes(mrec), dtype=np.uint8).copy()).to(dev)
         self._perf_host = [0] * len(meter_ids)   # dense-pass contributions (host ints)
         self._dense_host = [0] * len(meter_ids)
         self._sp_nodes = sp_nodes
@@ -789,8 +795,7 @@ class Graph:
                         spd = _lib.EvcConvSparsify(sh.hwc_interior, sh.hwc[0].numel(), sh.cp, sh.pitch, sdesc.flags,
                                                    sdesc.fstride, sh.fany_ptr, sp.part_ptr)
                         node._spd = spd  # keep the struct alive with the program
-                    fn, args = plan.fused(din, dout, fany=plan.fany_ptr, in_true=cnt_ptr,
-                                          bulk=self._bulk_step.data_ptr() + 8 * mi * S, act=fa, sp=spd)
+                    fn, args = plan.fused(din, dout, fany=plan.fany_ptr, mpart=node.mpart.data_ptr(), act=fa, sp=spd)
                     prog.append((fn, args, "conv_fused"))
                 else:
                     dout = self._desc(nid)
@@ -897,12 +902,11 @@ class Graph:
                 continue
             _lib.check(fn(*args, s), name)
         # device-side meter bookkeeping (graph.py:620-629, 632-636)
-        nflags, dense, mode = self._meter_static
-        _lib.check(self.lib.evc_meter_step(len(self._meter_ids) or 1, self.S, self._cnt_step.data_ptr(),
-                                           self._bulk_step.data_ptr(), nflags.data_ptr(), dense.data_ptr(),
-                                           mode.data_ptr(), self._perf_step.data_ptr(), self._perf_cum.data_ptr(),
-                                           self._ff_last.data_ptr(), self._ff_sum.data_ptr(),
-                                           self._sp_table.data_ptr(), len(self._sp_nodes), s), "meter_step")
+        _lib.check(self.lib.evc_meter_step(self._meter_table.data_ptr(), len(self._meter_ids) or 1, self.S,
+                                           self._cnt_step.data_ptr(), self._perf_step.data_ptr(),
+                                           self._perf_cum.data_ptr(), self._ff_last.data_ptr(),
+                                           self._ff_sum.data_ptr(), self._sp_table.data_ptr(), len(self._sp_nodes),
+                                           s), "meter_step")
 
     def dense_launches(self) -> int:
         """libevconv launches of the last dense pass (refresh), excluding torch memsets."""

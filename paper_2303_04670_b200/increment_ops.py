@@ -142,14 +142,13 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     dout = _desc(yv, yf, tile)
     if plan.path == "fused":
         fany = torch.zeros(plan.gi[0] * plan.gi[1], dtype=torch.uint8, device=dev)
-        i32 = torch.zeros(2, dtype=torch.int32, device=dev)  # [in_true, pad]
-        bulk = torch.zeros(1, dtype=torch.int64, device=dev)
+        mpart = torch.zeros(plan.ctas * 2, dtype=torch.int64, device=dev)  # per-CTA meter partials
         _lib.check(lib.evc_tile_any(din, _lib.ptr(fany), 1, s), "tile_any")
         pre = plan.prep(din)
         _lib.check(pre[0](*pre[1], s), "to_hwc")
-        fn, args = plan.fused(din, dout, fany=_lib.ptr(fany), in_true=_lib.ptr(i32), bulk=_lib.ptr(bulk))
+        fn, args = plan.fused(din, dout, fany=_lib.ptr(fany), mpart=_lib.ptr(mpart))
         _lib.check(fn(*args, s), "conv_fused")
-        cnt, b = int(i32[0].item()), int(bulk.item())
+        cnt, b = (int(v) for v in mpart.view(-1, 2).sum(dim=0).tolist())
         n_flags = c_in * plan.gi[0] * plan.gi[1]
         perf = 0 if cnt == 0 else (plan.dense_flops if cnt == n_flags else 2 * c_out * b)
         meter.add(perf, 0)

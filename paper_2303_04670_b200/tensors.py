@@ -301,6 +301,7 @@ class ConvPlan:
                                       device=weight.device)
             self.splits = int(self.cfg.splits)
             self.ws_floats = 0
+            self.ctas = int(lib.evc_conv_fused_ctas(self.g, self.cfg))  # per session (meter partials)
         else:
             self.path = "tile" if kernel == "tc" else "simt"
             if self.path == "tile":
@@ -320,8 +321,7 @@ class ConvPlan:
         return (self.g, din, dout, self.table.data_ptr(), scratch, in_true, tile_list, tile_count, None, meter,
                 self.S)
 
-    def fused(self, din, dout, *, fany=None, in_true=None, bulk=None, bias_ptr=None, act=None, sp=None,
-              dense=False):
+    def fused(self, din, dout, *, fany=None, mpart=None, bias_ptr=None, act=None, sp=None, dense=False):
         """(ctypes fn, args-without-stream) of evc_conv_fused.
 
         act = (code, alpha, acc_ptr, acc_stride, act_desc) fuses the activation node;
@@ -330,7 +330,7 @@ class ConvPlan:
         code, alpha, acc, accs, adesc = act if act is not None else (-1, 0.0, None, 0, None)
         return _lib.lib().evc_conv_fused, (self.g, self.cfg, self.hwc.data_ptr(), self.cp, self.hwc[0].numel(),
                                            self.wpack.data_ptr(), bias_ptr, din, fany, self.table.data_ptr(),
-                                           self.rstate.data_ptr(), in_true, bulk, dout, code, alpha, acc, accs,
+                                           self.rstate.data_ptr(), mpart, dout, code, alpha, acc, accs,
                                            adesc, sp, 1 if dense else 0, self.S)
 
     def gemm(self, din, dout, bias_ptr, work, ws_ptr):

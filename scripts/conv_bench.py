@@ -63,14 +63,13 @@ def main():
         dout = _lib.tdesc(y.data_ptr(), yf.data_ptr(), co * ho * wo, co * gho * gwo, co, ho, wo, 6, 6)
         dact = _lib.tdesc(ya.data_ptr(), yf.data_ptr(), co * ho * wo, co * gho * gwo, co, ho, wo, 6, 6)
         fany = torch.ones(gh * gw, dtype=torch.uint8, device=dev)
-        cnt = torch.zeros(2, dtype=torch.int32, device=dev)
-        bulk = torch.zeros(1, dtype=torch.int64, device=dev)
+        mpart = torch.zeros(plan.ctas * 2, dtype=torch.int64, device=dev)
         pre = plan.prep(din)
         _lib.check(pre[0](*pre[1], s), "to_hwc")
         dense = args.mode == "dense"
         act = (0, 0.0, acc.data_ptr(), acc[0].numel(), dact) if args.act else None
-        fn, fa = plan.fused(din, None if act else dout, fany=fany.data_ptr(), in_true=cnt.data_ptr(),
-                            bulk=bulk.data_ptr(), act=act, dense=dense)
+        fn, fa = plan.fused(din, None if act else dout, fany=fany.data_ptr(), mpart=mpart.data_ptr(),
+                            act=act, dense=dense)
         for _ in range(3):
             _lib.check(fn(*fa, s), "conv_fused")
         torch.cuda.synchronize()
@@ -87,8 +86,8 @@ def main():
             n_cta = int(lib.evc_conv_fused_ctas(plan.g, cfg))
             tb = torch.zeros(n_cta * 16, dtype=torch.int64, device=dev)
             lib.evc_conv_trace(tb.data_ptr())
-            fn, fa = plan.fused(din, None if act else dout, fany=fany.data_ptr(), in_true=cnt.data_ptr(),
-                                bulk=bulk.data_ptr(), act=act, dense=dense)
+            fn, fa = plan.fused(din, None if act else dout, fany=fany.data_ptr(), mpart=mpart.data_ptr(),
+                                act=act, dense=dense)
             _lib.check(fn(*fa, s), "conv_fused")
             torch.cuda.synchronize()
             lib.evc_conv_trace(None)

@@ -366,8 +366,6 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
 }
 
 
-__device__ __forceinline__ int64_t rs_of(int reg) { return reg; }  // thin path: one channel block
-
 // Output site of TMEM lane m in region rr.
 __device__ __forceinline__ void site_of(const Args& a, int rr, int m, int& u, int& x) {
   if (a.row) {
@@ -749,20 +747,21 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
 // (head + tail = the float32 input exactly).  One thread per output site, weights in shared
 // memory as [tap][c_in][c_out].
 constexpr int THIN_THREADS = BM;
+template <int CO>  // output channels padded to CO (2, 4, 8, 16, 32); weights [tap][c_in][CO]
 __global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
                                                             const __grid_constant__ Args a) {
-  extern __shared__ float s_w[];  // [kh*kw][c_in][c_out]
+  extern __shared__ float s_w[];
   __shared__ int s_flag[2];
   __shared__ double s_red[THIN_THREADS / 32];
   const int R = a.R;
   const int reg = blockIdx.x, s = reg / R, rr = reg % R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = a.kh * a.kw * a.c_in * a.c_out;
+  const int nw = a.kh * a.kw * a.c_in * CO;
   for (int e = threadIdx.x; e < nw; e += THIN_THREADS) s_w[e] = a.wpack[e];
   pdl_trigger();
   pdl_wait();
-  int ulo = (rr / a.RWn) * a.RH, uhi = min(ulo + a.RH, a.Ho) - 1;
-  int xlo = (rr % a.RWn) * a.RW, xhi = min(xlo + a.RW, a.Wo) - 1;
+  const int ulo = (rr / a.RWn) * a.RH, uhi = min(ulo + a.RH, a.Ho) - 1;
+  const int xlo = (rr % a.RWn) * a.RW, xhi = min(xlo + a.RW, a.Wo) - 1;
   if (warp == 0) {
     int live = 1;
     if (!a.dense) {
@@ -779,50 +778,66 @@ __global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restr
     }
     if (lane == 0) {
       s_flag[0] = live;
-      s_flag[1] = a.dense ? 0 : a.rstate[rs_of(reg)];
+      s_flag[1] = a.dense ? 0 : a.rstate[reg];
     }
   }
   __syncthreads();
   const int Qs = R, q = rr;
   if (!a.dense && warp < 2) side_work(a, s, q, Qs, threadIdx.x);
-  const int m = threadIdx.x;
   int u, x;
-  site_of(a, rr, m, u, x);
+  site_of(a, rr, threadIdx.x, u, x);
   const bool valid = u < a.Ho && x < a.Wo;
   double ssq = 0.0;
   if (!s_flag[0]) {
     if (!a.dense && s_flag[1]) {  // computed last step, dead now: restore exact zeros
-      for (int n = 0; n < a.c_out; ++n) {
-        if (!valid) break;
+      for (int n = 0; n < a.c_out && valid; ++n) {
         const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
         if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
         if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
         if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
       }
-      if (threadIdx.x == 0) a.rstate[rs_of(reg)] = 0;
+      if (threadIdx.x == 0) a.rstate[reg] = 0;
     }
   } else {
-    if (!a.dense && threadIdx.x == 0 && !s_flag[1]) a.rstate[rs_of(reg)] = 1;
-    float acc[32];
+    if (!a.dense && threadIdx.x == 0 && !s_flag[1]) a.rstate[reg] = 1;
+    float acc[CO];
 #pragma unroll
-    for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
+    for (int n = 0; n < CO; ++n) acc[n] = 0.0f;
     if (valid) {
       const float* base = in_hwc + (int64_t)s * hwc_stride;
       for (int r = 0; r < a.kh; ++r)
         for (int q2 = 0; q2 < a.kw; ++q2) {
           const float* px = base + ((int64_t)(u * a.stride + r) * a.P + x * a.stride + q2) * 2 * a.cp;
-          const float* wt = s_w + (r * a.kw + q2) * a.c_in * a.c_out;
-          for (int c = 0; c < a.c_in; ++c) {
-            const float xv = __fadd_rn(px[c], px[a.cp + c]);  // head + tail (exact)
-            const float* wc = wt + c * a.c_out;
+          const float* wt = s_w + (r * a.kw + q2) * a.c_in * CO;
+          int c = 0;
+          if ((a.c_in & 3) == 0) {  // 8 channels per round: four 16-byte loads in flight
+            for (; c + 8 <= a.c_in; c += 8) {
+              const float4 h0 = *reinterpret_cast<const float4*>(px + c);
+              const float4 h1 = *reinterpret_cast<const float4*>(px + c + 4);
+              const float4 l0 = *reinterpret_cast<const float4*>(px + a.cp + c);
+              const float4 l1 = *reinterpret_cast<const float4*>(px + a.cp + c + 4);
+              const float xv[8] = {__fadd_rn(h0.x, l0.x), __fadd_rn(h0.y, l0.y), __fadd_rn(h0.z, l0.z),
+                                   __fadd_rn(h0.w, l0.w), __fadd_rn(h1.x, l1.x), __fadd_rn(h1.y, l1.y),
+                                   __fadd_rn(h1.z, l1.z), __fadd_rn(h1.w, l1.w)};
 #pragma unroll
-            for (int n = 0; n < 32; ++n)
-              if (n < a.c_out) acc[n] = __fmaf_rn(xv, wc[n], acc[n]);
+              for (int k = 0; k < 8; ++k) {
+                const float* wc = wt + (c + k) * CO;
+#pragma unroll
+                for (int n = 0; n < CO; ++n) acc[n] = __fmaf_rn(xv[k], wc[n], acc[n]);
+              }
+            }
+          }
+          for (; c < a.c_in; ++c) {
+            const float xv = __fadd_rn(px[c], px[a.cp + c]);  // head + tail (exact)
+            const float* wc = wt + c * CO;
+#pragma unroll
+            for (int n = 0; n < CO; ++n) acc[n] = __fmaf_rn(xv, wc[n], acc[n]);
           }
         }
     }
-    ssq += emit<16>(a, s, u, x, 0, 1, min(16, a.c_out), acc);
-    if (a.c_out > 16) ssq += emit<16>(a, s, u, x, 16, 1, a.c_out - 16, acc + 16);
+    constexpr int E = CO < 16 ? CO : 16;
+    ssq += emit<E>(a, s, u, x, 0, 1, min(E, a.c_out), acc);
+    if (CO > 16) ssq += emit<E>(a, s, u, x, 16, 1, a.c_out - 16, acc + (CO > 16 ? 16 : 0));
   }
   if (a.sp_part) {
     double v = warp_sum_d(ssq);
@@ -835,6 +850,8 @@ __global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restr
     }
   }
 }
+
+static int thin_co(int c_out) { return c_out <= 2 ? 2 : (c_out <= 4 ? 4 : (c_out <= 8 ? 8 : (c_out <= 16 ? 16 : 32))); }
 
 // any-channel tile map: fany[s][t] = OR_c flags[s][c][t]
 __global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
@@ -969,7 +986,7 @@ static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
     L.nkb = 1;
     L.ns = 1;
     L.a_half = L.b_bytes = 0;
-    L.stage = g->kh * g->kw * g->c_in * g->c_out * 4;  // weights in shared memory
+    L.stage = g->kh * g->kw * g->c_in * thin_co(g->c_out) * 4;  // weights in shared memory
     return L;
   }
   if (cfg->row) {
@@ -1009,7 +1026,11 @@ int init_conv_fused() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, fz::k_tile_any) != cudaSuccess) rc = 1;
   if (cudaFuncGetAttributes(&fa, fz::k_meter_step) != cudaSuccess) rc = 1;
-  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin<2>) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin<4>) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin<8>) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin<16>) != cudaSuccess) rc = 1;
+  if (cudaFuncGetAttributes(&fa, fz::k_conv_thin<32>) != cudaSuccess) rc = 1;
   return rc ? EVC_ECUDA : EVC_OK;
 }
 
@@ -1069,7 +1090,7 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
 
 int64_t evc_conv_fused_pack_len(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   if (!g || !cfg || !fz::valid_bn(cfg->bn)) return -1;
-  if (cfg->thin) return (int64_t)g->kh * g->kw * g->c_in * g->c_out;
+  if (cfg->thin) return (int64_t)g->kh * g->kw * g->c_in * fz::thin_co(g->c_out);
   const int64_t nb = (g->c_out + cfg->bn - 1) / cfg->bn, nkb = (int64_t)g->kh * g->kw * ((g->c_in + 31) / 32);
   return nb * nkb * 2 * cfg->bn * 32;
 }
@@ -1077,12 +1098,14 @@ int64_t evc_conv_fused_pack_len(const evc_conv_geom* g, const evc_conv_cfg* cfg)
 int evc_conv_fused_pack(const float* w, const evc_conv_geom* g, const evc_conv_cfg* cfg, float* out) {
   EVC_CHECK_ARG(w && g && cfg && out && fz::valid_bn(cfg->bn), "conv_fused_pack: bad argument");
   const int bn = cfg->bn, c_out = g->c_out, c_in = g->c_in, kh = g->kh, kw = g->kw;
-  if (cfg->thin) {  // plain fp32 [tap][c_in][c_out]
+  if (cfg->thin) {  // plain fp32 [tap][c_in][CO], output channels zero-padded to CO
+    const int co = fz::thin_co(c_out);
     for (int r = 0; r < kh; ++r)
       for (int q = 0; q < kw; ++q)
         for (int c = 0; c < c_in; ++c)
-          for (int n = 0; n < c_out; ++n)
-            out[(((int64_t)r * kw + q) * c_in + c) * c_out + n] = w[(((int64_t)n * c_in + c) * kh + r) * kw + q];
+          for (int n = 0; n < co; ++n)
+            out[(((int64_t)r * kw + q) * c_in + c) * co + n] =
+                n < c_out ? w[(((int64_t)n * c_in + c) * kh + r) * kw + q] : 0.0f;
     return EVC_OK;
   }
   const int cch = (c_in + 31) / 32;
@@ -1254,8 +1277,14 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   if (cfg->thin) {
     EVC_CHECK_ARG(g->c_out <= 32 && L.stage <= 48 * 1024, "conv_fused: thin path needs C_out <= 32, small weights");
     a.splits = 1;
-    e = launch_pdl(fz::k_conv_thin, dim3((unsigned)(S * L.R)), dim3(fz::THIN_THREADS), (size_t)L.stage, st, in_hwc,
-                   hwc_stride, a);
+    const dim3 tg((unsigned)(S * L.R)), tb(fz::THIN_THREADS);
+    switch (fz::thin_co(g->c_out)) {
+      case 2: e = launch_pdl(fz::k_conv_thin<2>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 4: e = launch_pdl(fz::k_conv_thin<4>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 8: e = launch_pdl(fz::k_conv_thin<8>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 16: e = launch_pdl(fz::k_conv_thin<16>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      default: e = launch_pdl(fz::k_conv_thin<32>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+    }
     if (e != cudaSuccess) {
       set_error(std::string("evc: conv_fused (thin) launch: ") + cudaGetErrorString(e));
       return EVC_ECUDA;

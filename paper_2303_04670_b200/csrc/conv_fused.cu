@@ -747,6 +747,25 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
 // (head + tail = the float32 input exactly).  One thread per output site, weights in shared
 // memory as [tap][c_in][c_out].
 constexpr int THIN_THREADS = BM;
+
+// acc[n] += x * w[n] for CO weights in shared memory (16-byte broadcast reads when CO % 4 == 0)
+template <int CO>
+__device__ __forceinline__ void thin_fma(float* acc, float x, const float* w) {
+  if (CO % 4 == 0) {
+#pragma unroll
+    for (int n = 0; n < CO; n += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(w + n);
+      acc[n] = __fmaf_rn(x, w4.x, acc[n]);
+      acc[n + 1] = __fmaf_rn(x, w4.y, acc[n + 1]);
+      acc[n + 2] = __fmaf_rn(x, w4.z, acc[n + 2]);
+      acc[n + 3] = __fmaf_rn(x, w4.w, acc[n + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int n = 0; n < CO; ++n) acc[n] = __fmaf_rn(x, w[n], acc[n]);
+  }
+}
+
 template <int CO>  // output channels padded to CO (2, 4, 8, 16, 32); weights [tap][c_in][CO]
 __global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
                                                             const __grid_constant__ Args a) {
@@ -820,19 +839,20 @@ __global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restr
                                    __fadd_rn(h0.w, l0.w), __fadd_rn(h1.x, l1.x), __fadd_rn(h1.y, l1.y),
                                    __fadd_rn(h1.z, l1.z), __fadd_rn(h1.w, l1.w)};
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const float* wc = wt + (c + k) * CO;
-#pragma unroll
-                for (int n = 0; n < CO; ++n) acc[n] = __fmaf_rn(xv[k], wc[n], acc[n]);
-              }
+              for (int k = 0; k < 8; ++k) thin_fma<CO>(acc, xv[k], wt + (c + k) * CO);
             }
           }
-          for (; c < a.c_in; ++c) {
-            const float xv = __fadd_rn(px[c], px[a.cp + c]);  // head + tail (exact)
-            const float* wc = wt + c * CO;
-#pragma unroll
-            for (int n = 0; n < CO; ++n) acc[n] = __fmaf_rn(xv, wc[n], acc[n]);
+          if ((a.c_in & 3) == 0) {
+            for (; c + 4 <= a.c_in; c += 4) {
+              const float4 h0 = *reinterpret_cast<const float4*>(px + c);
+              const float4 l0 = *reinterpret_cast<const float4*>(px + a.cp + c);
+              thin_fma<CO>(acc, __fadd_rn(h0.x, l0.x), wt + c * CO);
+              thin_fma<CO>(acc, __fadd_rn(h0.y, l0.y), wt + (c + 1) * CO);
+              thin_fma<CO>(acc, __fadd_rn(h0.z, l0.z), wt + (c + 2) * CO);
+              thin_fma<CO>(acc, __fadd_rn(h0.w, l0.w), wt + (c + 3) * CO);
+            }
           }
+          for (; c < a.c_in; ++c) thin_fma<CO>(acc, __fadd_rn(px[c], px[a.cp + c]), wt + c * CO);  // head + tail
         }
     }
     constexpr int E = CO < 16 ? CO : 16;

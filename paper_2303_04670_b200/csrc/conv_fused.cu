@@ -38,6 +38,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "conv_common.cuh"
@@ -143,6 +144,11 @@ __device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld8_issue(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct Args {
@@ -151,7 +157,7 @@ struct Args {
   int th, tw, cp;
   // row mode (stride 1): regions are 128 consecutive sites of the output grid flattened with
   // pitch P = W + 2 pad; a K-block is (kernel row, 32 channels) with the kw taps as row shifts
-  int row, P, R;
+  int row, P, R, VM;  // row = 2: packed (kw taps along N, shifted sums in the epilogue); VM sites per region
   int ns, stage, a_half, b_bytes;  // pipeline depth and stage layout (bytes)
   const float* wpack;
   const float* bias;
@@ -369,9 +375,11 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
 // Output site of TMEM lane m in region rr.
 __device__ __forceinline__ void site_of(const Args& a, int rr, int m, int& u, int& x) {
   if (a.row) {
-    const int i = rr * BM + m;
+    // packed row mode: a region holds VM = 128 - (kw - 1) sites (lanes >= VM only feed the shifts)
+    const int i = rr * a.VM + m;
     u = i / a.P;
     x = i - u * a.P;
+    if (m >= a.VM) u = a.Ho;  // never valid
   } else {
     u = (rr / a.RWn) * a.RH + m / a.RW;
     x = (rr % a.RWn) * a.RW + m % a.RW;
@@ -388,8 +396,10 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
   // NA rotating accumulator blocks j = K-block mod NA shorten every fp32 accumulation chain; the
   // epilogue sums all blocks in fp32 (RN), small terms first.
   constexpr bool CAT = BN <= 128;
+  constexpr bool PACK = BN <= 32;  // packed row mode possible (2 kw BN <= 256 for kw <= 3... checked on host)
   constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 1 : (BN >= 64 ? 3 : 4));
-  constexpr int NEED = CAT ? NA * 2 * BN + BN : 2 * BN;
+  constexpr int NEED0 = CAT ? NA * 2 * BN + BN : 2 * BN;
+  constexpr int NEED = PACK ? (NEED0 > 12 * BN ? NEED0 : 12 * BN) : NEED0;  // packed: 2 x (3 taps x 2 x BN)
   constexpr int TMEM_COLS = NEED <= 32 ? 32 : (NEED <= 64 ? 64 : (NEED <= 128 ? 128 : (NEED <= 256 ? 256 : 512)));
   // kind::tf32, fp32 accumulate, A and B K-major, M = 128, N = BN or 2 BN
   constexpr uint32_t IDESC_BASE = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BM >> 4) << 24);
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
   const int NS = a.ns, STAGE = a.stage;
   const int npre = min(NS, nk);
   const uint32_t A_HALF = (uint32_t)a.a_half, B_BYTES = (uint32_t)a.b_bytes;
-  const int taps = a.row ? a.kw : 1;                           // MMAs groups per K-block
+  const int taps = a.row == 1 ? a.kw : 1;                      // MMA groups per K-block
   const uint32_t A_TX = a.row ? (uint32_t)(BM + a.kw - 1) * 128u : (uint32_t)BM * 128u;  // bytes per A box
 
   extern __shared__ uint8_t smem_raw[];
@@ -427,12 +437,12 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
   // valid output rows / columns of this region (receptive-box test, prefetch)
   int ulo, uhi, xlo, xhi;
   if (a.row) {
-    const int i0 = rr * BM;
+    const int i0 = rr * a.VM;
     ulo = i0 / a.P;
-    uhi = min(a.Ho - 1, (i0 + BM - 1) / a.P);
+    uhi = min(a.Ho - 1, (i0 + a.VM - 1) / a.P);
     if (ulo == uhi) {
       xlo = i0 - ulo * a.P;
-      xhi = min(a.Wo - 1, i0 + BM - 1 - ulo * a.P);
+      xhi = min(a.Wo - 1, i0 + a.VM - 1 - ulo * a.P);
     } else {
       xlo = 0;
       xhi = a.Wo - 1;
@@ -552,7 +562,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
         }
         if (a.row) {  // kernel row r of the flattened padded shadow: 128 + kw - 1 pixel rows
           const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
-          const int i0 = rr * BM + r * a.P;
+          const int i0 = rr * a.VM + r * a.P;
           tma_load_3d(abuf, &tmap, c0, i0, s, tma_bar(st));
           tma_load_3d(abuf + A_HALF, &tmap, a.cp + c0, i0, s, tma_bar(st));
         } else {  // one box = the whole RH x RW region for this tap (padded coordinates)
@@ -574,6 +584,19 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
         bar_spin(tma_bar(st), (i / NS) & 1);
         fence_after();
         const uint32_t ah = sb + st * STAGE, al = ah + A_HALF, bb = ah + 2 * A_HALF;
+        if (PACK && a.row == 2) {
+          // D_hi[j, (s, hi|lo, n)] += A_hi[j] . B_s ; D_lo[...] += A_lo[j] . B_s for all kw taps s at once
+          const uint32_t idp = IDESC_BASE | ((uint32_t)((a.kw * 2 * BN) >> 3) << 17);
+          const uint32_t thi = tmem, tlo = tmem + (uint32_t)(a.kw * 2 * BN);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t ko = kk * 32;
+            mma(thi, desc_k(ah + ko), desc_k(bb + ko), idp, (i || kk) ? 1u : 0u);
+            mma(tlo, desc_k(al + ko), desc_k(bb + ko), idp, (i || kk) ? 1u : 0u);
+          }
+          commit(empty_bar(st));
+          continue;
+        }
         for (int t = 0; t < taps; ++t) {
           // row mode: tap t = the A rows shifted by t pixels (any 128-byte row offset is a valid
           // SW128 descriptor start: the swizzle follows the absolute address, scripts/shift_probe.cu)
@@ -634,6 +657,64 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
     const int n_main = nk < NA ? nk : NA;
     const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     float* P = reinterpret_cast<float*>(smem);  // [BN][BM] partial tile (split-K only)
+    if (PACK && a.row == 2) {
+      // out[m] = sum_s v_s[m + s] with v_s[j] = lo.lo + lo.hi + hi.lo + hi.hi of tap s at TMEM row j:
+      // shifts by s rows = shuffles inside the warp, the next warp's first rows through shared memory
+      __shared__ float s_xch[4][3][3][8];
+      const int q4 = warp & 3, KW = a.kw;
+      const uint32_t lob = (uint32_t)(KW * 2 * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 8) {
+        float v[3][8];
+#pragma unroll
+        for (int s2 = 0; s2 < 3; ++s2) {
+          if (s2 < KW) {
+            uint32_t r4[4][8];
+            const uint32_t cb = (uint32_t)(s2 * 2 * BN + c0);
+            tmem_ld8_issue(trow + lob + cb + BN, r4[0]);  // lo . lo
+            tmem_ld8_issue(trow + lob + cb, r4[1]);       // lo . hi
+            tmem_ld8_issue(trow + cb + BN, r4[2]);        // hi . lo
+            tmem_ld8_issue(trow + cb, r4[3]);             // hi . hi
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) asm volatile("" : "+r"(r4[j][e]));
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              v[s2][e] = __fadd_rn(__fadd_rn(__fadd_rn(__uint_as_float(r4[0][e]), __uint_as_float(r4[1][e])),
+                                             __uint_as_float(r4[2][e])),
+                                   __uint_as_float(r4[3][e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[s2][e] = 0.0f;
+          }
+        }
+#pragma unroll
+        for (int s2 = 1; s2 < 3; ++s2)
+          if (s2 < KW && lane < s2) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s_xch[q4][s2][lane][e] = v[s2][e];
+          }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = v[0][e];
+#pragma unroll
+        for (int s2 = 1; s2 < 3; ++s2) {
+          if (s2 >= KW) break;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float t = __shfl_down_sync(0xffffffffu, v[s2][e], s2);
+            if (lane >= 32 - s2) t = q4 < 3 ? s_xch[q4 + 1][s2][lane + s2 - 32][e] : 0.0f;
+            o[e] = __fadd_rn(o[e], t);
+          }
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        const int n0 = nblk * BN + c0;
+        ssq += emit<8>(a, s, u, x, n0, 1, min(8, a.c_out - n0), o);
+      }
+    } else
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
       float vals[16];
@@ -995,7 +1076,7 @@ static bool valid_bn(int bn) { return bn == 16 || bn == 32 || bn == 64 || bn == 
 
 // Pipeline layout of one configuration: stage = [A heads | A tails | B], A halves 1 KiB aligned.
 struct Layout {
-  int ns, stage, a_half, b_bytes, R, nkb, cchunks;
+  int ns, stage, a_half, b_bytes, R, nkb, cchunks, VM = BM;
 };
 
 static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
@@ -1014,7 +1095,8 @@ static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
     L.b_bytes = g->kw * 2 * cfg->bn * 128;
     L.nkb = g->kh * L.cchunks;
     const int P = g->W + 2 * g->pad;
-    L.R = (int)(((int64_t)g->Ho * P + BM - 1) / BM);
+    L.VM = cfg->row == 2 ? BM - (g->kw - 1) : BM;
+    L.R = (int)(((int64_t)g->Ho * P + L.VM - 1) / L.VM);
   } else {
     L.a_half = BM * 128;
     L.b_bytes = 2 * cfg->bn * 128;
@@ -1028,7 +1110,8 @@ static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   // two co-resident CTAs per SM when two stages of each fit and the accumulators fit half of TMEM:
   // one CTA's prologue / epilogue then overlaps the other's MMA stream
   const int bn = cfg->bn, na = bn >= 128 ? 1 : (bn >= 64 ? 3 : 4);
-  const int need = bn <= 128 ? na * 2 * bn + bn : 2 * bn;
+  int need = bn <= 128 ? na * 2 * bn + bn : 2 * bn;
+  if (bn <= 32) need = std::max(need, 12 * bn);  // the kernel sizes TMEM for the packed mode too
   if (need <= 256 && 2 * (2 * L.stage + 1024 + 256 + 1024) <= SMEM_MAX) L.ns = 2;
   return L;
 }
@@ -1094,6 +1177,10 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
   while (bn < g->c_out && bn < 256) bn *= 2;
   if (cfg->row && bn > 64) bn = 64;  // kw taps of B per stage: keep >= 2 stages
   cfg->bn = bn;
+  // packed row mode: all kw taps of a K-block in ONE MMA along N (tcgen05.mma costs the same for
+  // any N <= 128), shifted and summed in the epilogue: kw x fewer MMA instructions for thin C_out
+  if (cfg->row && bn <= 32 && g->kw <= 3 && 2 * g->kw * bn <= 256 && std::getenv("EVC_NO_PACK") == nullptr)
+    cfg->row = 2;
   const int msp = std::max(1, std::min<int>(max_splits > 0 ? max_splits : 8, 16));
   fz::Layout L = fz::layout_of(g, cfg);
   const int64_t regions = (int64_t)S * L.R;
@@ -1104,6 +1191,7 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
   L = fz::layout_of(g, cfg);
   const int64_t ctas = regions * ((g->c_out + bn - 1) / bn);
   int sp = ctas >= 148 ? 1 : (int)std::min<int64_t>(msp, (148 + ctas - 1) / ctas);
+  if (cfg->row == 2) sp = 1;  // the packed epilogue sums shifted rows of one CTA's accumulators
   cfg->splits = fz::split_count(L.nkb, sp);
   return EVC_OK;
 }
@@ -1181,7 +1269,8 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                    void* stream) {
   EVC_CHECK_ARG(g && cfg && in_hwc && wpack && S > 0 && fz::valid_bn(cfg->bn), "conv_fused: null argument");
   EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
-  EVC_CHECK_ARG(cfg->row ? (g->stride == 1 && cfg->bn <= 128 && g->kw <= 9)
+  EVC_CHECK_ARG(cfg->row ? (g->stride == 1 && cfg->bn <= 128 && g->kw <= 9 &&
+                            (cfg->row == 1 || (cfg->bn <= 32 && g->kw <= 3 && cfg->splits == 1)))
                          : (cfg->rh * cfg->rw == fz::BM && (cfg->rw == 32 || cfg->rw == 16 || cfg->rw == 8) &&
                             cfg->rw * g->stride <= 256 && cfg->rh * g->stride <= 256),
                 "conv_fused: bad region shape");
@@ -1244,6 +1333,7 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   a.row = cfg->row;
   a.P = Wp;
   a.R = L.R;
+  a.VM = L.VM;
   a.ns = L.ns;
   a.stage = L.stage;
   a.a_half = L.a_half;

@@ -387,7 +387,7 @@ __device__ __forceinline__ void site_of(const Args& a, int rr, int m, int& u, in
 }
 
 template <int BN>
-__global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(const __grid_constant__ CUtensorMap tmap,
+__global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(const __grid_constant__ CUtensorMap tmap,
                                                            const __grid_constant__ Args a) {
   // 3xTF32 with the fewest MMA instructions (tcgen05.mma costs ~62 cycles for any N <= 128):
   //  CAT (BN <= 128): D_j[:, 0:2BN] += A_hi . [B_hi | B_lo]  (one MMA, N = 2 BN: hi*hi and hi*lo)
@@ -397,9 +397,9 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
   // epilogue sums all blocks in fp32 (RN), small terms first.
   constexpr bool CAT = BN <= 128;
   constexpr bool PACK = BN <= 32;  // packed row mode possible (2 kw BN <= 256 for kw <= 3... checked on host)
-  constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 1 : (BN >= 64 ? 3 : 4));
+  constexpr int NA = BN >= 256 ? 1 : (BN >= 128 ? 1 : (BN >= 32 ? 3 : 4));
   constexpr int NEED0 = CAT ? NA * 2 * BN + BN : 2 * BN;
-  constexpr int NEED = PACK ? (NEED0 > 12 * BN ? NEED0 : 12 * BN) : NEED0;  // packed: 2 x (3 taps x 2 x BN)
+  constexpr int NEED = PACK ? (NEED0 > 6 * BN ? NEED0 : 6 * BN) : NEED0;  // packed: 3 taps x 2 x BN
   constexpr int TMEM_COLS = NEED <= 32 ? 32 : (NEED <= 64 ? 64 : (NEED <= 128 ? 128 : (NEED <= 256 ? 256 : 512)));
   // kind::tf32, fp32 accumulate, A and B K-major, M = 128, N = BN or 2 BN
   constexpr uint32_t IDESC_BASE = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BM >> 4) << 24);
@@ -585,14 +585,14 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
         fence_after();
         const uint32_t ah = sb + st * STAGE, al = ah + A_HALF, bb = ah + 2 * A_HALF;
         if (PACK && a.row == 2) {
-          // D_hi[j, (s, hi|lo, n)] += A_hi[j] . B_s ; D_lo[...] += A_lo[j] . B_s for all kw taps s at once
+          // D[j, (s, hi|lo, n)] += A_lo[j] . B_s + A_hi[j] . B_s for all kw taps s at once (the A tail
+          // terms land in the same accumulator: lo . hi is ~2^-11 of hi . hi, far above fp32 rounding)
           const uint32_t idp = IDESC_BASE | ((uint32_t)((a.kw * 2 * BN) >> 3) << 17);
-          const uint32_t thi = tmem, tlo = tmem + (uint32_t)(a.kw * 2 * BN);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint32_t ko = kk * 32;
-            mma(thi, desc_k(ah + ko), desc_k(bb + ko), idp, (i || kk) ? 1u : 0u);
-            mma(tlo, desc_k(al + ko), desc_k(bb + ko), idp, (i || kk) ? 1u : 0u);
+            mma(tmem, desc_k(al + ko), desc_k(bb + ko), idp, (i || kk) ? 1u : 0u);  // small terms first
+            mma(tmem, desc_k(ah + ko), desc_k(bb + ko), idp, 1u);
           }
           commit(empty_bar(st));
           continue;
@@ -658,37 +658,34 @@ __global__ void __launch_bounds__(THREADS, (BN <= 32 ? 2 : 1)) k_conv_fused(cons
     const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     float* P = reinterpret_cast<float*>(smem);  // [BN][BM] partial tile (split-K only)
     if (PACK && a.row == 2) {
-      // out[m] = sum_s v_s[m + s] with v_s[j] = lo.lo + lo.hi + hi.lo + hi.hi of tap s at TMEM row j:
+      // out[m] = sum_s v_s[m + s] with v_s[j] = (A . B_lo) + (A . B_hi) of tap s at TMEM row j:
       // shifts by s rows = shuffles inside the warp, the next warp's first rows through shared memory
       __shared__ float s_xch[4][3][3][8];
       const int q4 = warp & 3, KW = a.kw;
-      const uint32_t lob = (uint32_t)(KW * 2 * BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 8) {
         float v[3][8];
+        {
+          uint32_t r4[3][2][8];  // [tap][B tail part, B head part]: every load in flight, one wait
 #pragma unroll
-        for (int s2 = 0; s2 < 3; ++s2) {
-          if (s2 < KW) {
-            uint32_t r4[4][8];
-            const uint32_t cb = (uint32_t)(s2 * 2 * BN + c0);
-            tmem_ld8_issue(trow + lob + cb + BN, r4[0]);  // lo . lo
-            tmem_ld8_issue(trow + lob + cb, r4[1]);       // lo . hi
-            tmem_ld8_issue(trow + cb + BN, r4[2]);        // hi . lo
-            tmem_ld8_issue(trow + cb, r4[3]);             // hi . hi
-            tmem_wait_ld();
+          for (int s2 = 0; s2 < 3; ++s2)
+            if (s2 < KW) {
+              const uint32_t cb = (uint32_t)(s2 * 2 * BN + c0);
+              tmem_ld8_issue(trow + cb + BN, r4[s2][0]);  // A . B_lo
+              tmem_ld8_issue(trow + cb, r4[s2][1]);       // A . B_hi
+            }
+          tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+          for (int s2 = 0; s2 < 3; ++s2)
 #pragma unroll
-              for (int e = 0; e < 8; ++e) asm volatile("" : "+r"(r4[j][e]));
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) asm volatile("" : "+r"(r4[s2][j][e]));
+#pragma unroll
+          for (int s2 = 0; s2 < 3; ++s2)
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              v[s2][e] = __fadd_rn(__fadd_rn(__fadd_rn(__uint_as_float(r4[0][e]), __uint_as_float(r4[1][e])),
-                                             __uint_as_float(r4[2][e])),
-                                   __uint_as_float(r4[3][e]));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[s2][e] = 0.0f;
-          }
+              v[s2][e] = s2 < KW ? __fadd_rn(__uint_as_float(r4[s2][0][e]), __uint_as_float(r4[s2][1][e])) : 0.0f;
         }
 #pragma unroll
         for (int s2 = 1; s2 < 3; ++s2)
@@ -1109,9 +1106,9 @@ static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   L.ns = std::max(1, std::min(4, STAGE_BUDGET / L.stage));
   // two co-resident CTAs per SM when two stages of each fit and the accumulators fit half of TMEM:
   // one CTA's prologue / epilogue then overlaps the other's MMA stream
-  const int bn = cfg->bn, na = bn >= 128 ? 1 : (bn >= 64 ? 3 : 4);
+  const int bn = cfg->bn, na = bn >= 128 ? 1 : (bn >= 32 ? 3 : 4);
   int need = bn <= 128 ? na * 2 * bn + bn : 2 * bn;
-  if (bn <= 32) need = std::max(need, 12 * bn);  // the kernel sizes TMEM for the packed mode too
+  if (bn <= 32) need = std::max(need, 6 * bn);  // the kernel sizes TMEM for the packed mode too
   if (need <= 256 && 2 * (2 * L.stage + 1024 + 256 + 1024) <= SMEM_MAX) L.ns = 2;
   return L;
 }

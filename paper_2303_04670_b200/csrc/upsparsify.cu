@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
   float* s_y = us_dyn;                // [(row * 32 + col) * 33 + channel] staged output (shadow transpose)
   float* s_x = us_dyn + 8 * 32 * 33;  // [channel][XR][XC] input footprint of this CTA
   // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
-  __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8], s_tj[32];
+  __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8], s_tj[32], s_ro0[8], s_ro1[8];
   __shared__ float s_cw0[32], s_cw1[32], s_rw0[8], s_rw1[8];
   const TView& y = a.y;
   const int jc = blockIdx.x % a.nJC, rest = blockIdx.x / a.nJC;
@@ -114,6 +114,10 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     const int rlo = s_ri0[0], nr = s_ri1[nrow - 1] - rlo + 1;
     const int clo = s_ci0[0], ncl = s_ci1[ncol - 1] - clo + 1;
     const int cs = (a.XR * a.XC) | 1;  // odd channel stride: lane-per-channel reads are bank-conflict free
+    if (threadIdx.x < nrow) {  // staged row offsets of each output row's two taps
+      s_ro0[threadIdx.x] = (s_ri0[threadIdx.x] - rlo) * a.XC;
+      s_ro1[threadIdx.x] = (s_ri1[threadIdx.x] - rlo) * a.XC;
+    }
     for (int e = threadIdx.x; e < nc * nr * ncl; e += US_THREADS) {
       const int cc = e % ncl, t2 = e / ncl;
       const int rr = t2 % nr, cl = t2 / nr;
@@ -124,34 +128,43 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
     if (fast) {
       // t_p = 0 fast path: lane = channel, warps stride over the output pixels; each pixel's
       // 32 channels go straight to the shadow as one 128-byte run of heads and one of tails
+      // warp w owns output columns w, w + 8, ...; per column the taps, the tile and its
+      // "process" flag are loop invariants, the rows are the inner loop
       const int cl = lane;
       if (cl < nc) {
-        float* dst = a.hwc + (int64_t)s * a.hs + c0 + cl + (int64_t)x0 * 2 * a.cp;
         const float* xc = s_x + cl * cs;
-        for (int r = 0; r < nrow; ++r) {
-          const float* xr0 = xc + (s_ri0[r] - rlo) * a.XC;
-          const float* xr1 = xc + (s_ri1[r] - rlo) * a.XC;
-          const float rw0 = s_rw0[r], rw1 = s_rw1[r];
-          float* drow = dst + (int64_t)(r0 + r) * a.hp * 2 * a.cp;
-          for (int xq = warp; xq < ncol; xq += US_THREADS / 32) {
-            const int ti = cl * nj + s_tj[xq];
-            if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
-            const int ci0 = s_ci0[xq] - clo;
+        const int64_t rstride = (int64_t)a.hp * 2 * a.cp;
+        float* dbase = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * rstride + c0 + cl;
+        float ssf = 0.0f;
+        for (int xq = warp; xq < ncol; xq += US_THREADS / 32) {
+          const int ti = cl * nj + s_tj[xq];
+          if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
+          const int ci0 = s_ci0[xq] - clo, ci1 = s_ci1[xq] - clo;
+          const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
+          float* d = dbase + (int64_t)(x0 + xq) * 2 * a.cp;
+          bool nz = false;
+          for (int r = 0; r < nrow; ++r, d += rstride) {
+            const float* xr0 = xc + s_ro0[r];
             float up;
             if (a.mode == 0) {
               up = xr0[ci0];
             } else {  // same float32 op order as upsample_at (rows first, then columns)
-              const int ci1 = s_ci1[xq] - clo;
+              const float* xr1 = xc + s_ro1[r];
+              const float rw0 = s_rw0[r], rw1 = s_rw1[r];
               const float ra = __fadd_rn(__fmul_rn(xr0[ci0], rw0), __fmul_rn(xr1[ci0], rw1));
               const float rb = __fadd_rn(__fmul_rn(xr0[ci1], rw0), __fmul_rn(xr1[ci1], rw1));
-              up = __fadd_rn(__fmul_rn(ra, s_cw0[xq]), __fmul_rn(rb, s_cw1[xq]));
+              up = __fadd_rn(__fmul_rn(ra, cw0), __fmul_rn(rb, cw1));
             }
             const float o = __fadd_rn(0.0f, up);
-            hwc_store(drow + xq * 2 * a.cp, a.cp, 0, o);
-            ss += (double)o * (double)o;
-            if (o != 0.0f) s_ny[ti] = 1;
+            const float h = tf32_head(o);
+            d[0] = h;
+            d[a.cp] = __fsub_rn(o, h);
+            ssf = __fmaf_rn(o, o, ssf);
+            nz |= o != 0.0f;
           }
+          if (nz) s_ny[ti] = 1;
         }
+        ss += (double)ssf;
       }
     } else {
     // lane = output column (ncol <= 32); warp w owns channels w, w + 8, ...

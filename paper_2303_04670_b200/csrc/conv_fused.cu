@@ -584,15 +584,18 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         bar_spin(tma_bar(st), (i / NS) & 1);
         fence_after();
         const uint32_t ah = sb + st * STAGE, al = ah + A_HALF, bb = ah + 2 * A_HALF;
+        // K-steps of 8 channels holding real input channels (the zero-padded tail chunk is skipped)
+        const int kbi = kb0 + i, c0k = (kbi % a.cchunks) * 32, nkk = min(4, (a.c_in - c0k + 7) >> 3);
         if (PACK && a.row == 2) {
           // D[j, (s, hi|lo, n)] += A_lo[j] . B_s + A_hi[j] . B_s for all kw taps s at once (the A tail
           // terms land in the same accumulator: lo . hi is ~2^-11 of hi . hi, far above fp32 rounding)
           const uint32_t idp = IDESC_BASE | ((uint32_t)((a.kw * 2 * BN) >> 3) << 17);
+          const uint64_t dl = desc_k(al), dh = desc_k(ah), db = desc_k(bb);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t ko = kk * 32;
-            mma(tmem, desc_k(al + ko), desc_k(bb + ko), idp, (i || kk) ? 1u : 0u);  // small terms first
-            mma(tmem, desc_k(ah + ko), desc_k(bb + ko), idp, 1u);
+          for (int kk = 0; kk < 4; ++kk) {  // K=8 tf32 = 32 bytes = +2 in the descriptor's address field
+            if (kk >= nkk) break;
+            mma(tmem, dl + 2 * kk, db + 2 * kk, idp, (i || kk) ? 1u : 0u);  // small terms first
+            mma(tmem, dh + 2 * kk, db + 2 * kk, idp, 1u);
           }
           commit(empty_bar(st));
           continue;
@@ -604,20 +607,22 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
           const bool first = t == 0;
           if (CAT) {
             const uint32_t tj = tmem + (uint32_t)((i % NA) * 2 * BN), tc = tmem + (uint32_t)(NA * 2 * BN);
+            const uint64_t da = desc_k(at), dl = desc_k(lt), db = desc_k(bh);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint32_t ko = kk * 32;  // K=8 tf32 = 32 bytes inside the 128-byte swizzle row
-              mma(tj, desc_k(at + ko), desc_k(bh + ko), IDESC2, (i >= NA || kk || !first) ? 1u : 0u);
-              mma(tc, desc_k(lt + ko), desc_k(bh + ko), IDESC, (i || kk || !first) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk) {  // K=8 tf32 = 32 bytes = +2 in the descriptor's address field
+              if (kk >= nkk) break;
+              mma(tj, da + 2 * kk, db + 2 * kk, IDESC2, (i >= NA || kk || !first) ? 1u : 0u);
+              mma(tc, dl + 2 * kk, db + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
             }
           } else {
             const uint32_t tmain = tmem, tcorr = tmem + (uint32_t)BN;
+            const uint64_t da = desc_k(at), dl = desc_k(lt), dbh = desc_k(bh), dbl = desc_k(bl);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              const uint32_t ko = kk * 32;
-              mma(tmain, desc_k(at + ko), desc_k(bh + ko), IDESC, (i || kk || !first) ? 1u : 0u);
-              mma(tcorr, desc_k(at + ko), desc_k(bl + ko), IDESC, (i || kk || !first) ? 1u : 0u);
-              mma(tcorr, desc_k(lt + ko), desc_k(bh + ko), IDESC, 1u);
+              if (kk >= nkk) break;
+              mma(tmain, da + 2 * kk, dbh + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
+              mma(tcorr, da + 2 * kk, dbl + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
+              mma(tcorr, dl + 2 * kk, dbh + 2 * kk, IDESC, 1u);
             }
           }
         }
@@ -812,6 +817,324 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
   fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TR(13);
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Persistent variant (no split-K, BN <= 64): each CTA walks work items (region, channel block)
+// with a continuous TMA/MMA stage ring and TWO TMEM accumulator buffers, so the epilogue of item
+// i (TMEM drain, activation, fused sparsify stores) overlaps the MMAs of item i + 1 and the
+// prologue is paid once per CTA.  Every role evaluates the region test itself (same inputs,
+// same answer), so no per-item hand-off is needed besides the TMEM full / empty barriers.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ bool region_live_warp(const Args& a, int s, int rr) {
+  if (a.dense) return true;
+  int ulo, uhi, xlo, xhi;
+  if (a.row) {
+    const int i0 = rr * a.VM;
+    ulo = i0 / a.P;
+    uhi = min(a.Ho - 1, (i0 + a.VM - 1) / a.P);
+    if (ulo == uhi) {
+      xlo = i0 - ulo * a.P;
+      xhi = min(a.Wo - 1, i0 + a.VM - 1 - ulo * a.P);
+    } else {
+      xlo = 0;
+      xhi = a.Wo - 1;
+    }
+  } else {
+    ulo = (rr / a.RWn) * a.RH;
+    uhi = min(ulo + a.RH, a.Ho) - 1;
+    xlo = (rr % a.RWn) * a.RW;
+    xhi = min(xlo + a.RW, a.Wo) - 1;
+  }
+  int live = 0;
+  if (ulo <= uhi && xlo <= xhi) {
+    const int y_lo = max(0, ulo * a.stride - a.pad), y_hi = min(a.H - 1, uhi * a.stride - a.pad + a.kh - 1);
+    const int x_lo = max(0, xlo * a.stride - a.pad), x_hi = min(a.W - 1, xhi * a.stride - a.pad + a.kw - 1);
+    if (y_lo <= y_hi && x_lo <= x_hi) {
+      const int GWi = (a.W + a.tw - 1) / a.tw, GHi = (a.H + a.th - 1) / a.th;
+      const int ra = y_lo / a.th, nr = y_hi / a.th - ra + 1, ca = x_lo / a.tw, nc = x_hi / a.tw - ca + 1;
+      const uint8_t* fa = a.fany + (int64_t)s * GHi * GWi;
+      for (int e = (int)(threadIdx.x & 31); e < nr * nc; e += 32) live |= fa[(ra + e / nc) * GWi + ca + e % nc];
+    }
+  }
+  return __any_sync(0xffffffffu, live) != 0;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(const __grid_constant__ CUtensorMap tmap,
+                                                                              const __grid_constant__ Args a) {
+  constexpr int BUF = BN <= 32 ? 6 * BN : 3 * BN;  // packed: 3 taps x [A.B_hi | A.B_lo]; CAT: [hi.hi | hi.lo | lo.hi]
+  constexpr int TMEM_COLS = 2 * BUF <= 128 ? 128 : (2 * BUF <= 256 ? 256 : 512);
+  constexpr uint32_t IDESC_BASE = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BM >> 4) << 24);
+  constexpr uint32_t IDESC = IDESC_BASE | ((uint32_t)(BN >> 3) << 17);
+  constexpr uint32_t IDESC2 = IDESC_BASE | ((uint32_t)((2 * BN) >> 3) << 17);
+  constexpr int MAXNS = 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int R = a.R, nb = (a.c_out + BN - 1) / BN;
+  const int n_items = a.S * R * nb;
+  const int NS = a.ns, STAGE = a.stage, nk = a.nkb;
+  const uint32_t A_HALF = (uint32_t)a.a_half, B_BYTES = (uint32_t)a.b_bytes;
+  const uint32_t A_TX = a.row ? (uint32_t)(BM + a.kw - 1) * 128u : (uint32_t)BM * 128u;
+  const bool packed = a.row == 2;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // full[4], empty[4], tfull[2], tempty[2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNS + 4);
+  const uint32_t sb = su32(smem), b0 = su32(bars);
+  auto full_bar = [&](int i) { return b0 + 8u * i; };
+  auto empty_bar = [&](int i) { return b0 + 8u * (MAXNS + i); };
+  auto tfull_bar = [&](int i) { return b0 + 8u * (2 * MAXNS + i); };
+  auto tempty_bar = [&](int i) { return b0 + 8u * (2 * MAXNS + 2 + i); };
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NS; ++i) {
+      bar_init(full_bar(i), 1);
+      bar_init(empty_bar(i), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      bar_init(tfull_bar(i), 1);
+      bar_init(tempty_bar(i), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  pdl_trigger();
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  pdl_wait();
+
+  if (warp == 0) {  // ---------------------------------------------------------- TMA producer
+    int g = 0;  // global stage counter
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int nblk = item % nb, reg = item / nb, s = reg / R, rr = reg % R;
+      if (!region_live_warp(a, s, rr)) continue;
+      if (lane == 0) {
+        const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
+        int ulo = 0, xlo = 0;
+        if (!a.row) {
+          ulo = (rr / a.RWn) * a.RH;
+          xlo = (rr % a.RWn) * a.RW;
+        }
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int st = g % NS;
+          if (g >= NS) bar_spin(empty_bar(st), ((g / NS) & 1) ^ 1);
+          const uint32_t abuf = sb + st * STAGE;
+          bar_arrive_tx(full_bar(st), 2 * A_TX + B_BYTES);
+          bulk_load(abuf + 2 * A_HALF, wsrc + (int64_t)kb * B_BYTES, B_BYTES, full_bar(st));
+          if (a.row) {
+            const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
+            const int i0 = rr * a.VM + r * a.P;
+            tma_load_3d(abuf, &tmap, c0, i0, s, full_bar(st));
+            tma_load_3d(abuf + A_HALF, &tmap, a.cp + c0, i0, s, full_bar(st));
+          } else {
+            const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
+            const int r = tap / a.kw, qq = tap % a.kw;
+            const int xs = xlo * a.stride + qq, ys = ulo * a.stride + r;
+            tma_load_4d(abuf, &tmap, c0, xs, ys, s, full_bar(st));
+            tma_load_4d(abuf + A_HALF, &tmap, a.cp + c0, xs, ys, s, full_bar(st));
+          }
+        }
+      } else {
+        g += nk;
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {  // --------------------------------------------------- MMA issuer
+    int g = 0, li = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int reg = item / nb, s = reg / R, rr = reg % R;
+      if (!region_live_warp(a, s, rr)) continue;
+      const int ab = li & 1;
+      if (lane == 0) {
+        if (li >= 2) bar_spin(tempty_bar(ab), ((li >> 1) & 1) ^ 1);
+        fence_after();
+        const uint32_t tb = tmem + (uint32_t)(ab * BUF);
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int st = g % NS;
+          bar_spin(full_bar(st), (g / NS) & 1);
+          fence_after();
+          const uint32_t ah = sb + st * STAGE, al = ah + A_HALF, bb = ah + 2 * A_HALF;
+          const int c0k = (kb % a.cchunks) * 32, nkk = min(4, (a.c_in - c0k + 7) >> 3);
+          if (packed) {
+            const uint32_t idp = IDESC_BASE | ((uint32_t)((a.kw * 2 * BN) >> 3) << 17);
+            const uint64_t dl = desc_k(al), dh = desc_k(ah), db = desc_k(bb);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kk >= nkk) break;
+              mma(tb, dl + 2 * kk, db + 2 * kk, idp, (kb || kk) ? 1u : 0u);
+              mma(tb, dh + 2 * kk, db + 2 * kk, idp, 1u);
+            }
+          } else {
+            const int taps = a.row ? a.kw : 1;
+            for (int t = 0; t < taps; ++t) {
+              const uint64_t da = desc_k(ah + t * 128), dl = desc_k(al + t * 128), db = desc_k(bb + t * 2 * BN * 128);
+              const bool first = kb == 0 && t == 0;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk) {
+                if (kk >= nkk) break;
+                mma(tb, da + 2 * kk, db + 2 * kk, IDESC2, (!first || kk) ? 1u : 0u);           // hi.[hi|lo]
+                mma(tb + 2 * BN, dl + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);  // lo.hi
+              }
+            }
+          }
+          commit(empty_bar(st));
+        }
+        commit(tfull_bar(ab));
+      } else {
+        g += nk;
+      }
+      ++li;
+      __syncwarp();
+    }
+  } else if (warp < 4) {  // ---------------------------------------------------- flags + meter
+    if (!a.dense) {
+      const int Qs = R * nb;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        const int nblk = item % nb, reg = item / nb, s = reg / R, rr = reg % R;
+        side_work(a, s, nblk * R + rr, Qs, threadIdx.x - 64);
+      }
+    }
+  } else {  // -------------------------------------------------------------------- epilogue
+    __shared__ float s_xch[4][3][3][8];
+    __shared__ double s_red[4];
+    const int q4 = warp & 3, m = 32 * q4 + lane;
+    const int Qs = R * nb;
+    int li = 0;
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      const int nblk = item % nb, reg = item / nb, s = reg / R, rr = reg % R;
+      const int64_t rs_idx = (int64_t)reg * nb + nblk;
+      const bool live = region_live_warp(a, s, rr);
+      int u, x;
+      site_of(a, rr, m, u, x);
+      double ssq = 0.0;
+      const int prev = a.dense ? 0 : a.rstate[rs_idx];
+      if (!live) {
+        if (prev) {  // computed last step, dead now: restore exact zeros
+          const int n0 = nblk * BN, nn = min(BN, a.c_out - n0);
+          if (u < a.Ho && x < a.Wo)
+            for (int n = n0; n < n0 + nn; ++n) {
+              const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
+              if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
+              if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
+              if (a.sp_hwc)
+                hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n,
+                          0.0f);
+            }
+        }
+      } else {
+        const int ab = li & 1;
+        bar_wait(tfull_bar(ab), (li >> 1) & 1);
+        fence_after();
+        const uint32_t trow = tmem + (uint32_t)(ab * BUF) + ((uint32_t)(32 * q4) << 16);
+        if (packed) {
+          const int KW = a.kw;
+          float o_all[BN <= 32 ? BN : 8];
+#pragma unroll
+          for (int c0 = 0; c0 < (BN <= 32 ? BN : 8); c0 += 8) {
+            float v[3][8];
+            {
+              uint32_t r4[3][2][8];
+#pragma unroll
+              for (int s2 = 0; s2 < 3; ++s2)
+                if (s2 < KW) {
+                  const uint32_t cb = (uint32_t)(s2 * 2 * BN + c0);
+                  tmem_ld8_issue(trow + cb + BN, r4[s2][0]);
+                  tmem_ld8_issue(trow + cb, r4[s2][1]);
+                }
+              tmem_wait_ld();
+#pragma unroll
+              for (int s2 = 0; s2 < 3; ++s2)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) asm volatile("" : "+r"(r4[s2][j][e]));
+#pragma unroll
+              for (int s2 = 0; s2 < 3; ++s2)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  v[s2][e] = s2 < KW ? __fadd_rn(__uint_as_float(r4[s2][0][e]), __uint_as_float(r4[s2][1][e])) : 0.0f;
+            }
+#pragma unroll
+            for (int s2 = 1; s2 < 3; ++s2)
+              if (s2 < KW && lane < s2) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) s_xch[q4][s2][lane][e] = v[s2][e];
+              }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o_all[(c0 + e) % (BN <= 32 ? BN : 8)] = v[0][e];
+#pragma unroll
+            for (int s2 = 1; s2 < 3; ++s2) {
+              if (s2 >= KW) break;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                float t = __shfl_down_sync(0xffffffffu, v[s2][e], s2);
+                if (lane >= 32 - s2) t = q4 < 3 ? s_xch[q4 + 1][s2][lane + s2 - 32][e] : 0.0f;
+                o_all[(c0 + e) % (BN <= 32 ? BN : 8)] = __fadd_rn(o_all[(c0 + e) % (BN <= 32 ? BN : 8)], t);
+              }
+            }
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+          }
+          // TMEM buffer free: the next item's MMAs may overwrite it while we store
+          fence_before();
+          bar_arrive(tempty_bar(ab));
+          const int n0 = nblk * BN;
+#pragma unroll
+          for (int c0 = 0; c0 < (BN <= 32 ? BN : 8); c0 += 8)
+            ssq += emit<8>(a, s, u, x, n0 + c0, 1, min(8, a.c_out - n0 - c0), o_all + c0);
+        } else {
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[3][16];
+            tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), r[0]);  // lo . hi
+            tmem_ld16_issue(trow + (uint32_t)(BN + c0), r[1]);      // hi . lo
+            tmem_ld16_issue(trow + (uint32_t)c0, r[2]);             // hi . hi
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+              for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
+            float vals[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              vals[e] = __fadd_rn(__fadd_rn(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])), __uint_as_float(r[2][e]));
+            if (c0 + 16 >= BN) {  // last TMEM read of this buffer
+              fence_before();
+              bar_arrive(tempty_bar(ab));
+            }
+            const int n0 = nblk * BN + c0;
+            ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
+          }
+        }
+        ++li;
+      }
+      // per-item bookkeeping: region state, sum of squares of the fused sparsify
+      if (a.sp_part) {
+        const double w = warp_sum_d(ssq);
+        if (lane == 0) s_red[q4] = w;
+      }
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      if (threadIdx.x == 128) {
+        if (a.sp_part) a.sp_part[(int64_t)s * Qs + nblk * R + rr] = s_red[0] + s_red[1] + s_red[2] + s_red[3];
+        if (!a.dense && live != (prev != 0)) a.rstate[rs_idx] = live ? 1 : 0;
+      }
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+    }
+  }
+  fence_before();
+  __syncthreads();
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
@@ -1058,6 +1381,22 @@ constexpr int SMEM_MAX = 227 * 1024;
 constexpr int STAGE_BUDGET = SMEM_MAX - 1024 - 256 - 2048;
 
 template <int BN>
+static int attr_persist() {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, k_conv_persist<BN>) != cudaSuccess) return 1;
+  return cudaFuncSetAttribute(k_conv_persist<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              SMEM_MAX - (int)fa.sharedSizeBytes) == cudaSuccess
+             ? 0
+             : 1;
+}
+
+template <int BN>
+static cudaError_t launch_persist(const CUtensorMap& m, const Args& a, int grid, cudaStream_t st) {
+  return launch_pdl(k_conv_persist<BN>, dim3((unsigned)grid), dim3(THREADS), (size_t)a.ns * a.stage + 1024 + 256, st,
+                    m, a);
+}
+
+template <int BN>
 static int attr() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k_conv_fused<BN>) != cudaSuccess) return 1;
@@ -1123,6 +1462,7 @@ static int split_count(int nkb, int splits) {
 
 int init_conv_fused() {
   int rc = fz::attr<16>() | fz::attr<32>() | fz::attr<64>() | fz::attr<128>() | fz::attr<256>();
+  rc |= fz::attr_persist<16>() | fz::attr_persist<32>() | fz::attr_persist<64>();
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, fz::k_tile_any) != cudaSuccess) rc = 1;
   if (cudaFuncGetAttributes(&fa, fz::k_meter_step) != cudaSuccess) rc = 1;
@@ -1397,6 +1737,23 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
       return EVC_ECUDA;
     }
     EVC_LAUNCH_CHECK("conv_fused_thin");
+    return EVC_OK;
+  }
+  if (a.splits == 1 && cfg->bn <= 64 && std::getenv("EVC_NO_PERSIST") == nullptr) {
+    // persistent CTAs: one or two per SM (BN = 16 fits two), each walking work items
+    const int occ = (cfg->bn <= 16 && 2 * ((int)L.ns * L.stage + 1024 + 256 + 2048) <= fz::SMEM_MAX) ? 2 : 1;
+    const int items = S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);
+    const int grid = std::max(1, std::min(items, occ * 148));
+    switch (cfg->bn) {
+      case 16: e = fz::launch_persist<16>(map, a, grid, st); break;
+      case 32: e = fz::launch_persist<32>(map, a, grid, st); break;
+      default: e = fz::launch_persist<64>(map, a, grid, st); break;
+    }
+    if (e != cudaSuccess) {
+      set_error(std::string("evc: conv_fused (persistent) launch: ") + cudaGetErrorString(e));
+      return EVC_ECUDA;
+    }
+    EVC_LAUNCH_CHECK("conv_fused_persist");
     return EVC_OK;
   }
   switch (cfg->bn) {

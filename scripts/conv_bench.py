@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--layers", default="")
     ap.add_argument("--act", type=int, default=1)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--sessions", type=int, default=1)
     args = ap.parse_args()
     want = set(args.layers.split(",")) if args.layers else None
     lib = _lib.lib()
@@ -49,21 +50,22 @@ def main():
         k = int(at["kernel"][0])
         st, pad, co = int(at.get("stride", 1)), int(at.get("padding", 0)), int(at["out_channels"])
         wt = torch.randn(co, c, k, k, device=dev) * (2.0 / (c * k * k)) ** 0.5
-        plan = ConvPlan(wt, st, pad, h, w, 6, 6, 1, max_splits=args.splits)
+        S = args.sessions
+        plan = ConvPlan(wt, st, pad, h, w, 6, 6, S, max_splits=args.splits)
         ho, wo = int(plan.g.Ho), int(plan.g.Wo)
-        x = torch.randn(1, c, h, w, device=dev)
+        x = torch.randn(S, c, h, w, device=dev)
         gh, gw = grid_shape((c, h, w), type("T", (), {"h": 6, "w": 6})())[1:]
-        fl = torch.ones(1, c, gh, gw, dtype=torch.uint8, device=dev)
-        y = torch.zeros(1, co, ho, wo, device=dev)
+        fl = torch.ones(S, c, gh, gw, dtype=torch.uint8, device=dev)
+        y = torch.zeros(S, co, ho, wo, device=dev)
         ya = torch.zeros_like(y)
         acc = torch.zeros_like(y)
         gho, gwo = -(-ho // 6), -(-wo // 6)
-        yf = torch.zeros(1, co, gho, gwo, dtype=torch.uint8, device=dev)
+        yf = torch.zeros(S, co, gho, gwo, dtype=torch.uint8, device=dev)
         din = _lib.tdesc(x.data_ptr(), fl.data_ptr(), c * h * w, c * gh * gw, c, h, w, 6, 6)
         dout = _lib.tdesc(y.data_ptr(), yf.data_ptr(), co * ho * wo, co * gho * gwo, co, ho, wo, 6, 6)
         dact = _lib.tdesc(ya.data_ptr(), yf.data_ptr(), co * ho * wo, co * gho * gwo, co, ho, wo, 6, 6)
-        fany = torch.ones(gh * gw, dtype=torch.uint8, device=dev)
-        mpart = torch.zeros(plan.ctas * 2, dtype=torch.int64, device=dev)
+        fany = torch.ones(S * gh * gw, dtype=torch.uint8, device=dev)
+        mpart = torch.zeros(S * plan.ctas * 2, dtype=torch.int64, device=dev)
         pre = plan.prep(din)
         _lib.check(pre[0](*pre[1], s), "to_hwc")
         dense = args.mode == "dense"
@@ -83,7 +85,7 @@ def main():
         tot += us
         if args.trace:
             cfg = plan.cfg
-            n_cta = int(lib.evc_conv_fused_ctas(plan.g, cfg))
+            n_cta = int(lib.evc_conv_fused_ctas(plan.g, cfg)) * S
             tb = torch.zeros(n_cta * 16, dtype=torch.int64, device=dev)
             lib.evc_conv_trace(tb.data_ptr())
             fn, fa = plan.fused(din, None if act else dout, fany=fany.data_ptr(), mpart=mpart.data_ptr(),
@@ -99,7 +101,7 @@ def main():
             print(f"    trace (us from CTA start, median): {line}")
             print(f"    CTA start spread: median {np.median(g0) / 1e3:.2f} us, max {g0.max() / 1e3:.2f} us; "
                   f"CTA duration median {np.median(t[:, 13]) / 1965:.2f} us max {t[:, 13].max() / 1965:.2f}")
-        flops = 2.0 * k * k * c * co * ho * wo
+        flops = 2.0 * k * k * c * co * ho * wo * S
         cfg = plan.cfg
         print(f"{nid:6s} {c:4d}x{h:3d}x{w:3d} -> {co:3d}x{ho:3d}x{wo:3d} k{k} s{st}  bn={cfg.bn:3d} r={cfg.rh}x{cfg.rw} "
               f"splits={cfg.splits:2d}  {us:8.1f} us  {flops / us * 1e-6:7.1f} TFLOP/s alg  "

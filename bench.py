@@ -36,6 +36,8 @@ sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
 
+from paper_2303_04670_b200 import shard as _shard  # noqa: E402  (no CUDA needed)
+
 METRIC = "EV-FlowNet increments/sec/GPU and p50 per-increment latency at 2% density"
 UNIT = "increments/s"
 WINDOW_US, SHIFT_US, RATE_HZ = 50_000, 1_000, 1.0e6
@@ -50,10 +52,7 @@ def peaks():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return _shard.dist_env()
 
 
 # ---------------------------------------------------------------------------
@@ -137,7 +136,7 @@ def timed_run(evc, spec, weights, S, steps, warmup, rank, world, dev):
     import torch
 
     n_win = 1 + warmup + steps + 1
-    seeds = [rank * S + s for s in range(S)]
+    seeds = _shard.stream_seeds(rank, S)
     xs = make_inputs(evc, n_win, seeds, dev)  # resident in HBM before timing
     density = float((xs[1:] != xs[:-1]).float().mean())
     g = evc.build(spec, weights, refresh_interval=64, sessions=S)
@@ -197,13 +196,8 @@ def run_ours(args):
     S = args.sessions
     res = timed_run(evc, spec, weights, S, args.steps, args.warmup, rank, world, dev)
     g, xs, times, refreshes, clk, density = res
-    total_ms = sum(times)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    incr_total = args.steps * S * world
-    value = incr_total / (total_ms / 1e3)
+    total_ms = _shard.job_time_ms(sum(times), world, dev)  # max over ranks
+    value = _shard.aggregate_rate(args.steps, S, world, total_ms)
     steady = sorted(times)
     p50 = statistics.median(steady)
     p99 = steady[min(len(steady) - 1, int(round(0.99 * (len(steady) - 1))))]

@@ -389,7 +389,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || (cp >= dx->C && cp % 32 == 0 && hwc_pitch >= dx->W),
+  EVC_CHECK_ARG(!hwc || (cp >= dx->C && cp % 4 == 0 && hwc_pitch >= dx->W),
                 "sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   TBArgs p = {};
   p.a = view_of(*dx);

@@ -1613,11 +1613,11 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                 "conv_fused: bad region shape");
   EVC_CHECK_ARG(cfg->splits >= 1 && cfg->splits <= 16, "conv_fused: splits must lie in [1, 16]");
   const int Hp = g->H + 2 * g->pad, Wp = g->W + 2 * g->pad;
-  EVC_CHECK_ARG(cp % 32 == 0 && cp >= g->c_in && hwc_stride % 32 == 0 && hwc_stride >= (int64_t)Hp * Wp * 2 * cp,
-                "conv_fused: shadow layout (cp % 32, (H + 2 pad) x (W + 2 pad) pixels per session)");
+  EVC_CHECK_ARG(cp % (cfg->thin ? 4 : 32) == 0 && cp >= g->c_in && hwc_stride % 4 == 0 && hwc_stride >= (int64_t)Hp * Wp * 2 * cp,
+                "conv_fused: shadow layout (cp % 32, thin path % 4; (H + 2 pad) x (W + 2 pad) pixels per session)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
-  EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 32 == 0 && sp->cp >= g->c_out && sp->hwc_stride % 32 == 0 &&
+  EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 4 == 0 && sp->cp >= g->c_out && sp->hwc_stride % 4 == 0 &&
                         sp->pitch >= g->Wo && sp->flags && sp->fany && sp->partials),
                 "conv_fused: fused sparsify needs the shadow, flags, fany and partials (incremental mode)");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && meter_part &&

@@ -45,7 +45,7 @@ int32_t evc_hwc_channels(int32_t c) { return (c + 31) / 32 * 32; }
 
 int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp, int32_t pitch, int32_t S,
                void* stream) {
-  EVC_CHECK_ARG(x && x->vals && y && S > 0 && cp >= x->C && cp % 32 == 0 && pitch >= x->W, "to_hwc: bad argument");
+  EVC_CHECK_ARG(x && x->vals && y && S > 0 && cp >= x->C && cp % 4 == 0 && pitch >= x->W, "to_hwc: bad argument");
   TView v = view_of(*x);
   dim3 grid(cdiv(v.H * v.W, 32), cdiv(v.C, 32), S);
   const cudaError_t e = launch_pdl(k_to_hwc, grid, dim3(256), 0, as_stream(stream), v, y, y_stride, cp, pitch);

@@ -285,7 +285,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
   EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");
   EVC_CHECK_ARG(write_chw || hwc, "upsample_sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || (cp >= y->C && cp % 32 == 0 && hwc_pitch >= y->W),
+  EVC_CHECK_ARG(!hwc || (cp >= y->C && cp % 4 == 0 && hwc_pitch >= y->W),
                 "upsample_sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   USArgs a;
   a.x = view_of(*x);

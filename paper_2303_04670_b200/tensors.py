@@ -285,14 +285,15 @@ class ConvPlan:
         self.gi = (-(-h // th), -(-w // tw))  # input tile grid
         if kernel == "tc" and lib.evc_conv_fused_supported(self.g):
             self.path = "fused"
-            self.cp = int(lib.evc_hwc_channels(c_in))
+            self.cfg = _lib.EvcConvCfg()
+            _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
+            # channels per shadow pixel: 32-aligned for the TMA path, 4-aligned for the CUDA-core path
+            self.cp = -(-c_in // 4) * 4 if self.cfg.thin else int(lib.evc_hwc_channels(c_in))
             # hi/lo shadow with a zero border of the conv's padding: (S, H + 2p, W + 2p, heads | tails)
             self.pitch = w + 2 * pad
             self.hwc = torch.zeros((S, h + 2 * pad, self.pitch, 2 * self.cp), dtype=torch.float32,
                                    device=weight.device)
             self.hwc_interior = self.hwc.data_ptr() + 4 * (pad * self.pitch + pad) * 2 * self.cp
-            self.cfg = _lib.EvcConvCfg()
-            _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
             host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)
             out = np.zeros(int(lib.evc_conv_fused_pack_len(self.g, self.cfg)), dtype=np.float32)
             _lib.check(lib.evc_conv_fused_pack(host.ctypes.data, self.g, self.cfg, out.ctypes.data), "pack")

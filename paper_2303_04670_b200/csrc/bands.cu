@@ -321,6 +321,69 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
   }
 }
 
+// t_p = 0 sparsify of a tensor with few channels (C <= 8, e.g. the 4-channel event input):
+// one thread per pixel of a tile row x SM_TJ tiles, all channels per thread, so no lanes
+// idle on missing channels.  y = 0 + x (sparsify.py:69-71); flags recomputed from the values
+// (sparsify.py:77-78) through shared memory; the channels-innermost hi/lo shadow gets each
+// pixel's C heads and C tails as contiguous runs.
+constexpr int SM_TJ = 6;
+__global__ void __launch_bounds__(256) k_sparsify_small(TBArgs p) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ uint8_t s_f[8 * SM_TJ];
+  __shared__ double s_red[8];
+  const TView& a = p.a;
+  const int nJ = (a.GW + SM_TJ - 1) / SM_TJ;
+  const int jb = blockIdx.x % nJ, i = blockIdx.x / nJ, s = blockIdx.y;
+  const int j0 = jb * SM_TJ, nj = min(SM_TJ, a.GW - j0);
+  for (int t = threadIdx.x; t < a.C * SM_TJ; t += blockDim.x) s_f[t] = 0;
+  __syncthreads();
+  const int span = SM_TJ * a.tw;  // columns of this CTA (th x span <= 216 threads: th, tw <= 6 checked on host)
+  const int r = threadIdx.x / span, xq = threadIdx.x % span;
+  const int u = i * a.th + r, x = j0 * a.tw + xq;
+  const bool valid = r < a.th && u < a.H && xq < nj * a.tw && x < a.W;
+  float ss = 0.0f;
+  if (valid) {
+    const int64_t HW = (int64_t)a.H * a.W, off = (int64_t)u * a.W + x;
+    const float* src = a.v + (int64_t)s * a.vs + off;
+    float v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < a.C) v[c] = __fadd_rn(0.0f, src[c * HW]);
+    const int tj = xq / a.tw;
+    float* sh = p.hwc ? p.hwc + (int64_t)s * p.hs + ((int64_t)u * p.hp + x) * 2 * p.cp : nullptr;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c >= a.C) break;
+      if (p.write_chw) p.y.v[(int64_t)s * p.y.vs + c * HW + off] = v[c];
+      if (sh) hwc_store(sh, p.cp, c, v[c]);
+      ss = __fmaf_rn(v[c], v[c], ss);
+      if (v[c] != 0.0f) s_f[c * SM_TJ + tj] = 1;
+    }
+  }
+  double d = warp_sum_d((double)ss);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
+  __syncthreads();
+  for (int t = threadIdx.x; t < a.C * nj; t += blockDim.x) {
+    const int c = t / nj, jl = t % nj;
+    const int64_t fo = ((int64_t)c * a.GH + i) * a.GW + j0 + jl;
+    p.y.f[(int64_t)s * p.y.fs + fo] = s_f[c * SM_TJ + jl];
+  }
+  if (p.fany && threadIdx.x < nj) {
+    int any = 0;
+    for (int c = 0; c < a.C; ++c) any |= s_f[c * SM_TJ + threadIdx.x];
+    if (any) p.fany[((int64_t)s * a.GH + i) * a.GW + j0 + threadIdx.x] = 1;
+  }
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+    p.partials[(int64_t)s * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+static bool small_ok(const TView& v) { return v.C <= 8 && v.th <= 6 && v.tw <= 6; }
+static int small_blocks(const TView& v) { return v.GH * ((v.GW + SM_TJ - 1) / SM_TJ); }
+
 template <int OP>
 static void launch_op(const TBArgs& p, const TBGeo& g, int S, cudaStream_t st) {
   dim3 grid((unsigned)(g.GH * g.nCG * g.nJC), (unsigned)S);
@@ -377,9 +440,10 @@ int evc_act_delta(const evc_tensor* dx, float* acc, int64_t acc_stride, const ev
 
 int64_t evc_sparsify_partials(const evc_tensor* dx) {
   if (!dx) return -1;
-  const TBGeo g = tb_geo(view_of(*dx), true);
-  const TBGeo g1 = tb_geo(view_of(*dx), false);
-  return std::max(g.GH * g.nCG * g.nJC, g1.GH * g1.nCG * g1.nJC);
+  const TView v = view_of(*dx);
+  const TBGeo g = tb_geo(v, true);
+  const TBGeo g1 = tb_geo(v, false);
+  return std::max(std::max(g.GH * g.nCG * g.nJC, g1.GH * g1.nCG * g1.nJC), small_ok(v) ? small_blocks(v) : 0);
 }
 
 int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive, const evc_tensor* y, double* k,
@@ -410,6 +474,11 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   p.fany = fany;
   p.write_chw = write_chw;
   p.delta_zero = delta_zero;
+  if (delta_zero && !ticket && small_ok(p.a)) {  // few channels at t_p = 0: thread per pixel
+    launch_pdl(k_sparsify_small, dim3((unsigned)small_blocks(p.a), (unsigned)S), dim3(256), 0, as_stream(stream), p);
+    EVC_LAUNCH_CHECK("sparsify_small");
+    return EVC_OK;
+  }
   const int rc = tb_launch(OP_SPARSIFY, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("sparsify");
   return rc;

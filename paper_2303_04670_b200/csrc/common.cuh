@@ -148,6 +148,15 @@ __device__ __forceinline__ T block_sum(T v, F wsum) {
 // conv_fused.cu): pixel p owns 2*cp floats, the TF32 head of channel c at
 // [p*2cp + c] and the tail x - head at [p*2cp + cp + c]; cp = channels padded to
 // a multiple of 32 so both 32-channel boxes start 128-byte aligned.
+// 4-byte global -> shared copy that does not wait for the load (LDGSTS); completed by
+// cp_async_wait_all() before the barrier that publishes the staged data.
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ float tf32_head(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }

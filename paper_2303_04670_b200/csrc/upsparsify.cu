@@ -33,16 +33,17 @@ struct USArgs {
   uint8_t* fany;  // optional any-channel tile map of y (OR-accumulated, zeroed per step)
   int cp, write_chw, delta_zero, f, mode;
   int XR, XC;  // staged input footprint (rows, cols) per CTA
+  int fast;    // t_p = 0 into a shadow only: no output staging buffer (smaller CTA -> more per SM)
   int CW, nCG, nJC;
 };
 
-__global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
+__global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   pdl_wait();
   pdl_trigger();
   __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ];
   extern __shared__ float us_dyn[];
-  float* s_y = us_dyn;                // [(row * 32 + col) * 33 + channel] staged output (shadow transpose)
-  float* s_x = us_dyn + 8 * 32 * 33;  // [channel][XR][XC] input footprint of this CTA
+  float* s_y = us_dyn;                             // [(row * 32 + col) * 33 + channel] staged output
+  float* s_x = us_dyn + (a.fast ? 0 : 8 * 32 * 33);  // [channel][XR][XC] input footprint of this CTA
   // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
   __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8], s_tj[32], s_ro0[8], s_ro1[8];
   __shared__ float s_cw0[32], s_cw1[32], s_rw0[8], s_rw1[8];
@@ -53,25 +54,7 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
   const int x0 = jc * a.CW, ncol = min(y.W, x0 + a.CW) - x0;
   const int j0 = x0 / y.tw, nj = (ncol + y.tw - 1) / y.tw;
   const int r0 = i * y.th, nrow = min(y.H, r0 + y.th) - r0;
-  int alo, ahi;
-  upsample_box(r0, r0 + nrow, a.x.H, a.f, a.mode, a.x.th, alo, ahi);
-  bool any = false;
-  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
-    const int cl = t / nj, jl = t % nj, c = c0 + cl;
-    const int v0 = (j0 + jl) * y.tw, v1 = min(y.W, v0 + y.tw);
-    int blo, bhi;
-    upsample_box(v0, v1, a.x.W, a.f, a.mode, a.x.tw, blo, bhi);
-    const uint8_t* F = a.x.fplane(s, c);
-    uint8_t live = 0;
-    for (int aa = alo; aa <= ahi; ++aa)
-      for (int bb = blo; bb <= bhi; ++bb) live |= F[aa * a.x.GW + bb];
-    const int64_t fo = ((int64_t)c * y.GH + i) * y.GW + j0 + jl;
-    const uint8_t pr = live | y.f[(int64_t)s * y.fs + fo] | a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo];
-    s_proc[t] = pr != 0;
-    s_ny[t] = 0;
-    s_nd[t] = 0;
-    any |= pr != 0;
-  }
+  // 1) taps of this CTA's output columns / rows, and last step's output / residual flags
   if (threadIdx.x < ncol) {
     const int v = x0 + threadIdx.x;
     s_tj[threadIdx.x] = threadIdx.x / y.tw;
@@ -100,6 +83,48 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       s_rw1[r] = t.w1;
     }
   }
+  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {  // last step's output / residual flags
+    const int cl = t / nj, jl = t % nj;
+    const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i) * y.GW + j0 + jl;
+    s_nd[t] = y.f[(int64_t)s * y.fs + fo] | a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo];
+  }
+  __syncthreads();
+  // 2) input tile box of this CTA (rows) and of each output tile (columns) from the taps; the
+  //    input flags of the box, all channels, staged with every load in flight
+  const int alo = s_ri0[0] / a.x.th, ahi = s_ri1[nrow - 1] / a.x.th;
+  const int blo0 = s_ci0[0] / a.x.tw, bhi0 = s_ci1[ncol - 1] / a.x.tw;
+  const int na_ = ahi - alo + 1, nb_ = bhi0 - blo0 + 1;
+  uint8_t* s_fin = s_ny;  // reuse: [cl][na_][nb_] staged input flags (<= 32 * 32 bytes)
+  const bool box_fits = na_ * nb_ <= US_MAXJ;
+  if (box_fits)
+    for (int t = threadIdx.x; t < nc * na_ * nb_; t += US_THREADS) {
+      const int cl = t / (na_ * nb_), e = t % (na_ * nb_);
+      s_fin[t] = a.x.fplane(s, c0 + cl)[(alo + e / nb_) * a.x.GW + blo0 + e % nb_];
+    }
+  __syncthreads();
+  bool any = false;
+  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
+    const int cl = t / nj, jl = t % nj;
+    const int xa = jl * y.tw, xb = min(ncol, xa + y.tw) - 1;
+    const int blo = s_ci0[xa] / a.x.tw, bhi = s_ci1[xb] / a.x.tw;
+    uint8_t live = 0;
+    if (box_fits) {
+      for (int aa = 0; aa < na_; ++aa)
+        for (int bb = blo; bb <= bhi; ++bb) live |= s_fin[(cl * na_ + aa) * nb_ + bb - blo0];
+    } else {
+      const uint8_t* F = a.x.fplane(s, c0 + cl);
+      for (int aa = alo; aa <= ahi; ++aa)
+        for (int bb = blo; bb <= bhi; ++bb) live |= F[aa * a.x.GW + bb];
+    }
+    s_proc[t] = (live | s_nd[t]) != 0;
+    any |= s_proc[t] != 0;
+  }
+  const bool active0 = __syncthreads_or(any) != 0;  // s_fin (= s_ny) consumed
+  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
+    s_ny[t] = 0;
+    s_nd[t] = 0;
+  }
+  any = active0;
   const bool active = __syncthreads_or(any) != 0;
   double ss = 0.0;
   const bool stage = a.hwc && nrow <= 8 && ncol <= 32;
@@ -118,49 +143,73 @@ __global__ void __launch_bounds__(US_THREADS) k_up_sparsify(USArgs a) {
       s_ro0[threadIdx.x] = (s_ri0[threadIdx.x] - rlo) * a.XC;
       s_ro1[threadIdx.x] = (s_ri1[threadIdx.x] - rlo) * a.XC;
     }
-    for (int e = threadIdx.x; e < nc * nr * ncl; e += US_THREADS) {
-      const int cc = e % ncl, t2 = e / ncl;
-      const int rr = t2 % nr, cl = t2 / nr;
-      s_x[cl * cs + rr * a.XC + cc] = a.x.plane(s, c0 + cl)[(int64_t)(rlo + rr) * a.x.W + clo + cc];
+    {  // flat (channel, row, column) walk; the index is advanced by carries, not divisions
+      int cc = threadIdx.x % ncl, t2 = threadIdx.x / ncl;
+      int rr = t2 % nr, cl = t2 / nr;
+      const int dcc = US_THREADS % ncl, dt2 = US_THREADS / ncl, drr = dt2 % nr, dcl = dt2 / nr;
+      const float* xs = a.x.plane(s, c0) + (int64_t)rlo * a.x.W + clo;
+      const int64_t xHW = (int64_t)a.x.H * a.x.W;
+      for (; cl < nc;) {
+        cp_async4(s_x + cl * cs + rr * a.XC + cc, xs + cl * xHW + (int64_t)rr * a.x.W + cc);
+        cc += dcc;
+        const int c1 = cc >= ncl;
+        cc -= c1 ? ncl : 0;
+        rr += drr + c1;
+        const int c2 = rr >= nr;
+        rr -= c2 ? nr : 0;
+        cl += dcl + c2;
+      }
+      cp_async_wait_all();
     }
     __syncthreads();
-    const bool fast = a.delta_zero && !use_k && !a.write_chw && a.hwc;
+    const bool fast = a.fast;
     if (fast) {
-      // t_p = 0 fast path: lane = channel, warps stride over the output pixels; each pixel's
-      // 32 channels go straight to the shadow as one 128-byte run of heads and one of tails
-      // warp w owns output columns w, w + 8, ...; per column the taps, the tile and its
-      // "process" flag are loop invariants, the rows are the inner loop
-      const int cl = lane;
-      if (cl < nc) {
+      // t_p = 0 fast path, separable: (1) the row interpolation R[channel][row][input col]
+      // once per input column, (2) the column interpolation + split per output pixel.
+      // lane -> (channel cl = lane % nc, column phase q = lane / nc): a narrow remainder
+      // group (the 2 flow channels of a decoder concat) still fills the warp.
+      const int Q = 32 / nc, cl = lane % nc, q = lane / nc;
+      const int RS = (8 * a.XC) | 1;
+      float* s_r = s_x + US_C * cs;  // [channel][row][input col] row-interpolated input
+      if (q < Q) {
         const float* xc = s_x + cl * cs;
-        const int64_t rstride = (int64_t)a.hp * 2 * a.cp;
-        float* dbase = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * rstride + c0 + cl;
+        float* rc = s_r + cl * RS;
+        for (int r = 0; r < nrow; ++r) {
+          const float* xr0 = xc + s_ro0[r];
+          const float* xr1 = xc + s_ro1[r];
+          const float rw0 = s_rw0[r], rw1 = s_rw1[r];
+          float* rr_ = rc + r * a.XC;
+          for (int c = warp * Q + q; c < ncl; c += (US_THREADS / 32) * Q)
+            rr_[c] = a.mode == 0 ? xr0[c] : __fadd_rn(__fmul_rn(xr0[c], rw0), __fmul_rn(xr1[c], rw1));
+        }
+      }
+      __syncthreads();
+      if (q < Q) {
+        const float* rc = s_r + cl * RS;
+        const int rstride = a.hp * 2 * a.cp;  // floats between shadow rows (< 2^31 per session)
+        float* sbase = a.hwc + (int64_t)s * a.hs + c0 + cl;
+        const int obase = r0 * rstride + x0 * 2 * a.cp;
         float ssf = 0.0f;
-        for (int xq = warp; xq < ncol; xq += US_THREADS / 32) {
+        for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q) {
           const int ti = cl * nj + s_tj[xq];
           if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
-          const int ci0 = s_ci0[xq] - clo, ci1 = s_ci1[xq] - clo;
+          const float* p0 = rc + (s_ci0[xq] - clo);
+          const float* p1 = rc + (s_ci1[xq] - clo);
           const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
-          float* d = dbase + (int64_t)(x0 + xq) * 2 * a.cp;
+          float* d = sbase + obase + xq * 2 * a.cp;
           bool nz = false;
-          for (int r = 0; r < nrow; ++r, d += rstride) {
-            const float* xr0 = xc + s_ro0[r];
-            float up;
-            if (a.mode == 0) {
-              up = xr0[ci0];
-            } else {  // same float32 op order as upsample_at (rows first, then columns)
-              const float* xr1 = xc + s_ro1[r];
-              const float rw0 = s_rw0[r], rw1 = s_rw1[r];
-              const float ra = __fadd_rn(__fmul_rn(xr0[ci0], rw0), __fmul_rn(xr1[ci0], rw1));
-              const float rb = __fadd_rn(__fmul_rn(xr0[ci1], rw0), __fmul_rn(xr1[ci1], rw1));
-              up = __fadd_rn(__fmul_rn(ra, cw0), __fmul_rn(rb, cw1));
-            }
-            const float o = __fadd_rn(0.0f, up);
-            const float h = tf32_head(o);
+          for (int r = 0; r < nrow; ++r) {
+            // same float32 op order as upsample_at (rows first, then columns)
+            const float up = a.mode == 0 ? p0[0] : __fadd_rn(__fmul_rn(p0[0], cw0), __fmul_rn(p1[0], cw1));
+            const float ov = __fadd_rn(0.0f, up);
+            const float h = tf32_head(ov);
             d[0] = h;
-            d[a.cp] = __fsub_rn(o, h);
-            ssf = __fmaf_rn(o, o, ssf);
-            nz |= o != 0.0f;
+            d[a.cp] = __fsub_rn(ov, h);
+            ssf = __fmaf_rn(ov, ov, ssf);
+            nz |= ov != 0.0f;
+            p0 += a.XC;
+            p1 += a.XC;
+            d += rstride;
           }
           if (nz) s_ny[ti] = 1;
         }
@@ -312,7 +361,9 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   dim3 grid((unsigned)(a.y.GH * a.nCG * a.nJC), (unsigned)S);
   a.XR = y->th / factor + 3;
   a.XC = a.CW / factor + 3;
-  const size_t smem = sizeof(float) * (8 * 32 * 33 + (size_t)US_C * ((a.XR * a.XC) | 1));
+  a.fast = (delta_zero && tp == 0.0 && !write_chw && hwc) ? 1 : 0;
+  const size_t smem = sizeof(float) * ((a.fast ? (size_t)US_C * ((8 * a.XC) | 1) : 8 * 32 * 33) +
+                                       (size_t)US_C * ((a.XR * a.XC) | 1));
   launch_pdl(k_up_sparsify, dim3(grid), dim3(US_THREADS), smem, as_stream(stream), a);
   EVC_LAUNCH_CHECK("upsample_sparsify");
   return EVC_OK;

@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -2
+timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_brk.log 2>&1; tail -2 gpurun_out/pytest_brk.log
 python scripts/step_breakdown.py --sessions 1 > gpurun_out/brk_s1.txt 2>&1
 python scripts/step_breakdown.py --sessions 32 > gpurun_out/brk_s32.txt 2>&1

@@ -269,6 +269,8 @@ __device__ __noinline__ void side_work(const Args& a, int s, int q, int Qs, int 
     mp[0] = s_mp[0][0] + s_mp[1][0];
     mp[1] = s_mp[0][1] + s_mp[1][1];
   }
+  // the persistent kernel calls this in a loop: s_mp is read before either warp refills it
+  asm volatile("bar.sync 1, 64;" ::: "memory");
 }
 
 __device__ __noinline__ float act_other(float x, int kind, float alpha) { return act_apply(x, kind, alpha); }

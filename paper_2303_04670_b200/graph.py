@@ -21,6 +21,8 @@ import heapq
 from dataclasses import dataclass, field
 from pathlib import Path
 
+import os
+
 import numpy as np
 import torch
 import yaml
@@ -642,7 +644,8 @@ class Graph:
                 continue
             up = self._by_id.get(node.spec.inputs[0])
             if (up is not None and up.kind == "upsample" and self._consumers[up.spec.id] == [node.spec.id]
-                    and up.spec.id not in self.output_ids and tile.w <= 32 and tile.h <= 8):
+                    and up.spec.id not in self.output_ids and tile.w <= 32 and tile.h <= 8
+                    and os.environ.get("EVC_NO_UPFUSE", "0") != "1"):
                 self._fused_up.add(up.spec.id)
                 node.nparts = int(self.lib.evc_upsample_sparsify_partials(self._desc(node.spec.id)))
             else:

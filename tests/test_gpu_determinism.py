@@ -3,6 +3,9 @@ must produce bit-identical outputs, increment flags and per-node performed-FLOP 
 (No float atomics on the data path: split-K reduces in a fixed order over DSMEM, norm
 partials fold in a fixed order -- see DESIGN.md.)"""
 
+import hashlib
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -20,7 +23,9 @@ def _run(spec, weights, xs, cuda_graph):
     out = []
     for i in range(1, len(xs)):
         yup, y, rep = g.incr_step(evc.step_increment(xs[i - 1], xs[i], spec.tile))
-        out.append((y.detach().cpu().numpy().copy(), yup.mask.numpy().copy(), dict(rep.per_node)))
+        slots = {nid: hashlib.sha1(f.cpu().numpy().tobytes()).hexdigest()[:10]
+                 for nid in g._slots for f in [g._slot_view(nid)[1]]} if os.environ.get("EVC_DET_SLOTS") else {}
+        out.append((y.detach().cpu().numpy().copy(), yup.mask.numpy().copy(), dict(rep.per_node), slots))
     return out
 
 
@@ -32,7 +37,8 @@ def test_evflownet_bitwise_reproducible(cuda_graph):
     a = _run(spec, weights, xs, cuda_graph)
     for _ in range(2):
         b = _run(spec, weights, xs, cuda_graph)
-        for i, ((ya, fa, pa), (yb, fb, pb)) in enumerate(zip(a, b)):
+        for i, ((ya, fa, pa, sa), (yb, fb, pb, sb)) in enumerate(zip(a, b)):
+            assert sa == sb, (i, [k for k in sa if sa[k] != sb[k]])  # every node's tile flags
             assert np.array_equal(fa, fb), i
             assert np.array_equal(ya.view(np.uint32), yb.view(np.uint32)), (i, float(np.abs(ya - yb).max()))
             bad = {k: (pa[k], pb[k]) for k in pa if pa[k] != pb[k]}

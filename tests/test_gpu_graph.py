@@ -99,10 +99,7 @@ def test_evflownet_64_increments_vs_oracle():
             perf_rel = max(perf_rel, abs(p - orep["per_node"][k][0]) / max(1, orep["per_node"][k][1]))
         worst = max(worst, max_err(np_(y), oy))
     assert worst <= 1e-4, worst
-    # performed FLOPs follow the tile flags, so the rounding-zero flips tolerated above
-    # (their float32 sums differ with the host BLAS the oracle runs on) move a node's
-    # meter by a few tiles' cost: ~3e-5 of the dense count per flipped output tile
-    assert perf_rel <= 5e-4, perf_rel
+    assert perf_rel <= 1e-4, perf_rel
     assert flips <= 8, flips
     assert 0.005 < np.mean(density) < 0.05  # ~2 % increment density
     # drift after 64 chained increments vs a dense recompute on the GPU

@@ -14,7 +14,7 @@
 
 namespace evc {
 
-constexpr int US_C = 32, US_THREADS = 256, US_MAXJ = 32;
+constexpr int US_C = 32, US_THREADS = 256, US_MAXJ = 32, US_MAXR = 16;
 
 struct USArgs {
   TView x;         // upsample input (masked)
@@ -35,26 +35,31 @@ struct USArgs {
   int XR, XC;  // staged input footprint (rows, cols) per CTA
   int fast;    // t_p = 0 into a shadow only: no output staging buffer (smaller CTA -> more per SM)
   int CW, nCG, nJC;
+  int RT;       // output tile rows per CTA (2 on the fast path when they fit, else 1)
+  int pstride;  // partial slots per session (the RT = 1 CTA count)
+  int RS;       // fast path: channel stride of the row-interpolated buffer (odd)
 };
 
 __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   pdl_wait();
   pdl_trigger();
-  __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ];
+  __shared__ uint8_t s_proc[US_C * US_MAXJ], s_ny[US_C * US_MAXJ], s_nd[US_C * US_MAXJ], s_fin[US_C * US_MAXJ];
   extern __shared__ float us_dyn[];
   float* s_y = us_dyn;                             // [(row * 32 + col) * 33 + channel] staged output
   float* s_x = us_dyn + (a.fast ? 0 : 8 * 32 * 33);  // [channel][XR][XC] input footprint of this CTA
   // static upsample taps of this CTA's output columns / rows (tensors.py:259-282)
-  __shared__ int s_ci0[32], s_ci1[32], s_ri0[8], s_ri1[8], s_tj[32], s_ro0[8], s_ro1[8];
-  __shared__ float s_cw0[32], s_cw1[32], s_rw0[8], s_rw1[8];
+  __shared__ int s_ci0[32], s_ci1[32], s_ri0[US_MAXR], s_ri1[US_MAXR], s_tj[32], s_ro0[US_MAXR], s_ro1[US_MAXR];
+  __shared__ float s_cw0[32], s_cw1[32], s_rw0[US_MAXR], s_rw1[US_MAXR];
   const TView& y = a.y;
   const int jc = blockIdx.x % a.nJC, rest = blockIdx.x / a.nJC;
-  const int cg = rest % a.nCG, i = rest / a.nCG, s = blockIdx.y;
+  const int cg = rest % a.nCG, ib = rest / a.nCG, s = blockIdx.y;
   const int c0 = cg * US_C, nc = min(US_C, y.C - c0);
   const int x0 = jc * a.CW, ncol = min(y.W, x0 + a.CW) - x0;
   const int j0 = x0 / y.tw, nj = (ncol + y.tw - 1) / y.tw;
-  const int r0 = i * y.th, nrow = min(y.H, r0 + y.th) - r0;
-  // 1) taps of this CTA's output columns / rows, and last step's output / residual flags
+  const int i0 = ib * a.RT, nti = min(y.GH - i0, a.RT);  // tile rows of this CTA
+  const int r0 = i0 * y.th, nrow = min(y.H, r0 + nti * y.th) - r0;
+  const int NT = nti * nj;  // tiles per channel: t = channel * NT + tile row * nj + tile column
+  // 1) taps of this CTA's output columns / rows
   if (threadIdx.x < ncol) {
     const int v = x0 + threadIdx.x;
     s_tj[threadIdx.x] = threadIdx.x / y.tw;
@@ -83,48 +88,51 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       s_rw1[r] = t.w1;
     }
   }
-  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {  // last step's output / residual flags
-    const int cl = t / nj, jl = t % nj;
-    const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i) * y.GW + j0 + jl;
-    s_nd[t] = y.f[(int64_t)s * y.fs + fo] | a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo];
-  }
-  __syncthreads();
-  // 2) input tile box of this CTA (rows) and of each output tile (columns) from the taps; the
-  //    input flags of the box, all channels, staged with every load in flight
-  const int alo = s_ri0[0] / a.x.th, ahi = s_ri1[nrow - 1] / a.x.th;
-  const int blo0 = s_ci0[0] / a.x.tw, bhi0 = s_ci1[ncol - 1] / a.x.tw;
+  // the CTA's input box from the taps of its corner pixels (taps are monotone), computed by
+  // every thread so the flag loads below need no barrier first
+  auto tap_i0 = [&](int u, int n) { return a.mode == 0 ? u / a.f : bilinear_tap(u, n, a.f).i0; };
+  auto tap_i1 = [&](int u, int n) { return a.mode == 0 ? u / a.f : bilinear_tap(u, n, a.f).i1; };
+  const int rlo = tap_i0(r0, a.x.H), nr = tap_i1(r0 + nrow - 1, a.x.H) - rlo + 1;
+  const int clo = tap_i0(x0, a.x.W), ncl = tap_i1(x0 + ncol - 1, a.x.W) - clo + 1;
+  const int alo = rlo / a.x.th, ahi = (rlo + nr - 1) / a.x.th;
+  const int blo0 = clo / a.x.tw, bhi0 = (clo + ncl - 1) / a.x.tw;
   const int na_ = ahi - alo + 1, nb_ = bhi0 - blo0 + 1;
-  uint8_t* s_fin = s_ny;  // reuse: [cl][na_][nb_] staged input flags (<= 32 * 32 bytes)
   const bool box_fits = na_ * nb_ <= US_MAXJ;
+  // last step's output / residual flags and the input flags of the box (all channels):
+  // every load in flight at once
+  for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
+    const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
+    const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i0 + tr) * y.GW + j0 + jl;
+    s_nd[t] = y.f[(int64_t)s * y.fs + fo] | a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo];
+    s_ny[t] = 0;
+  }
   if (box_fits)
     for (int t = threadIdx.x; t < nc * na_ * nb_; t += US_THREADS) {
       const int cl = t / (na_ * nb_), e = t % (na_ * nb_);
       s_fin[t] = a.x.fplane(s, c0 + cl)[(alo + e / nb_) * a.x.GW + blo0 + e % nb_];
     }
   __syncthreads();
+  // 2) process a tile when its upsample support is live, or it was live / left a residual
   bool any = false;
-  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
-    const int cl = t / nj, jl = t % nj;
+  for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
+    const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
     const int xa = jl * y.tw, xb = min(ncol, xa + y.tw) - 1;
+    const int ya = tr * y.th, yb = min(nrow, ya + y.th) - 1;
     const int blo = s_ci0[xa] / a.x.tw, bhi = s_ci1[xb] / a.x.tw;
+    const int alo_t = s_ri0[ya] / a.x.th, ahi_t = s_ri1[yb] / a.x.th;
     uint8_t live = 0;
     if (box_fits) {
-      for (int aa = 0; aa < na_; ++aa)
-        for (int bb = blo; bb <= bhi; ++bb) live |= s_fin[(cl * na_ + aa) * nb_ + bb - blo0];
+      for (int aa = alo_t; aa <= ahi_t; ++aa)
+        for (int bb = blo; bb <= bhi; ++bb) live |= s_fin[(cl * na_ + aa - alo) * nb_ + bb - blo0];
     } else {
       const uint8_t* F = a.x.fplane(s, c0 + cl);
-      for (int aa = alo; aa <= ahi; ++aa)
+      for (int aa = alo_t; aa <= ahi_t; ++aa)
         for (int bb = blo; bb <= bhi; ++bb) live |= F[aa * a.x.GW + bb];
     }
     s_proc[t] = (live | s_nd[t]) != 0;
     any |= s_proc[t] != 0;
+    s_nd[t] = 0;  // same thread, same entry: from here on this step's residual flags
   }
-  const bool active0 = __syncthreads_or(any) != 0;  // s_fin (= s_ny) consumed
-  for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
-    s_ny[t] = 0;
-    s_nd[t] = 0;
-  }
-  any = active0;
   const bool active = __syncthreads_or(any) != 0;
   double ss = 0.0;
   const bool stage = a.hwc && nrow <= 8 && ncol <= 32;
@@ -136,8 +144,6 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // stage the CTA's input footprint (all channels of the group) in shared memory:
     // every global load is issued up front, the upsample then reads shared memory
-    const int rlo = s_ri0[0], nr = s_ri1[nrow - 1] - rlo + 1;
-    const int clo = s_ci0[0], ncl = s_ci1[ncol - 1] - clo + 1;
     const int cs = (a.XR * a.XC) | 1;  // odd channel stride: lane-per-channel reads are bank-conflict free
     if (threadIdx.x < nrow) {  // staged row offsets of each output row's two taps
       s_ro0[threadIdx.x] = (s_ri0[threadIdx.x] - rlo) * a.XC;
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       // lane -> (channel cl = lane % nc, column phase q = lane / nc): a narrow remainder
       // group (the 2 flow channels of a decoder concat) still fills the warp.
       const int Q = 32 / nc, cl = lane % nc, q = lane / nc;
-      const int RS = (8 * a.XC) | 1;
+      const int RS = a.RS;
       float* s_r = s_x + US_C * cs;  // [channel][row][input col] row-interpolated input
       if (q < Q) {
         const float* xc = s_x + cl * cs;
@@ -190,15 +196,17 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
         float* sbase = a.hwc + (int64_t)s * a.hs + c0 + cl;
         const int obase = r0 * rstride + x0 * 2 * a.cp;
         float ssf = 0.0f;
-        for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q) {
-          const int ti = cl * nj + s_tj[xq];
+        for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q)
+        for (int tr = 0; tr < nti; ++tr) {
+          const int ti = cl * NT + tr * nj + s_tj[xq];
           if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
-          const float* p0 = rc + (s_ci0[xq] - clo);
-          const float* p1 = rc + (s_ci1[xq] - clo);
+          const int ra = tr * y.th, rb = min(nrow, ra + y.th);
+          const float* p0 = rc + ra * a.XC + (s_ci0[xq] - clo);
+          const float* p1 = rc + ra * a.XC + (s_ci1[xq] - clo);
           const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
-          float* d = sbase + obase + xq * 2 * a.cp;
+          float* d = sbase + obase + ra * rstride + xq * 2 * a.cp;
           bool nz = false;
-          for (int r = 0; r < nrow; ++r) {
+          for (int r = ra; r < rb; ++r) {
             // same float32 op order as upsample_at (rows first, then columns)
             const float up = a.mode == 0 ? p0[0] : __fadd_rn(__fmul_rn(p0[0], cw0), __fmul_rn(p1[0], cw1));
             const float ov = __fadd_rn(0.0f, up);
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
     for (int cl = warp; cl < nc; cl += US_THREADS / 32)
     for (int r = 0; r < nrow; ++r) {
       if (!col_ok) continue;
-      const int ti = cl * nj + jl_lane;
+      const int ti = cl * NT + jl_lane;  // RT = 1 here: NT = nj
       if (!s_proc[ti]) {
         if (stage) s_y[(r * 32 + xl) * 33 + cl] = 0.0f;
         continue;
@@ -265,11 +273,11 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
     }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < nc * nj; t += US_THREADS) {
-      const int cl = t / nj, jl = t % nj;
-      const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i) * y.GW + j0 + jl;
+    for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
+      const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
+      const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i0 + tr) * y.GW + j0 + jl;
       y.f[(int64_t)s * y.fs + fo] = s_ny[t];
-      if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i) * y.GW + j0 + jl] = 1;  // benign race: all store 1
+      if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i0 + tr) * y.GW + j0 + jl] = 1;  // benign race: all store 1
       a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage && !fast && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
@@ -280,7 +288,10 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
     }
   }
   ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
-  if (threadIdx.x == 0) a.partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
+  if (threadIdx.x == 0) {
+    a.partials[(int64_t)s * a.pstride + blockIdx.x] = ss;
+    if (blockIdx.x + gridDim.x < (unsigned)a.pstride) a.partials[(int64_t)s * a.pstride + blockIdx.x + gridDim.x] = 0.0;
+  }
   if (!a.ticket) return;  // norm / k folded later by evc_meter_step (one launch for every node)
   const int nblocks = gridDim.x * gridDim.y;
   __shared__ int s_last;
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    sparsify_finalize_all(a.partials, gridDim.x, a.norm_ema, a.k, a.tp, a.decay, 0, gridDim.y);
+    sparsify_finalize_all(a.partials, a.pstride, a.norm_ema, a.k, a.tp, a.decay, 0, gridDim.y);
   }
 }
 
@@ -358,11 +369,15 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.f = factor;
   a.mode = mode;
   us_grid(a.y, a.CW, a.nCG, a.nJC);
-  dim3 grid((unsigned)(a.y.GH * a.nCG * a.nJC), (unsigned)S);
-  a.XR = y->th / factor + 3;
-  a.XC = a.CW / factor + 3;
   a.fast = (delta_zero && tp == 0.0 && !write_chw && hwc) ? 1 : 0;
-  const size_t smem = sizeof(float) * ((a.fast ? (size_t)US_C * ((8 * a.XC) | 1) : 8 * 32 * 33) +
+  // two tile rows per CTA on the fast path when their tiles fit the per-CTA flag tables
+  a.RT = (a.fast && 2 * (a.CW / a.y.tw) <= US_MAXJ && 2 * a.y.th <= US_MAXR) ? 2 : 1;
+  a.pstride = a.y.GH * a.nCG * a.nJC;
+  dim3 grid((unsigned)(((a.y.GH + a.RT - 1) / a.RT) * a.nCG * a.nJC), (unsigned)S);
+  a.XR = a.RT * y->th / factor + 3;
+  a.XC = a.CW / factor + 3;
+  a.RS = (a.RT * y->th * a.XC) | 1;
+  const size_t smem = sizeof(float) * ((a.fast ? (size_t)US_C * a.RS : 8 * 32 * 33) +
                                        (size_t)US_C * ((a.XR * a.XC) | 1));
   launch_pdl(k_up_sparsify, dim3(grid), dim3(US_THREADS), smem, as_stream(stream), a);
   EVC_LAUNCH_CHECK("upsample_sparsify");

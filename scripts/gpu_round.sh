@@ -10,5 +10,5 @@ timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --cloc
 python scripts/kernel_summary.py gpurun_out/launches_c1_s32.csv --steps 1 > gpurun_out/kernel_summary_s32.txt; head -20 gpurun_out/kernel_summary_s32.txt
 timeout 900 python bench.py --steps 64 --warmup 3 --cpu-budget 15 > gpurun_out/bench.log 2>&1; tail -2 gpurun_out/bench.log
 timeout 600 python bench.py --impl reference --steps 8 --warmup 3 --cpu-budget 20 > gpurun_out/bench_ref.log 2>&1; tail -2 gpurun_out/bench_ref.log
-timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_conv_fused" -s 10 -c 1 -o gpurun_out/prof_conv python scripts/profile_step.py --steps 1 > gpurun_out/ncu_f.log 2>&1
+timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_conv" -s 14 -c 1 -o gpurun_out/prof_conv python scripts/profile_step.py --steps 1 --sessions 32 > gpurun_out/ncu_f.log 2>&1
 tail -1 gpurun_out/ncu_f.log

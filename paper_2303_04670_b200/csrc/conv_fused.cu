@@ -1450,7 +1450,7 @@ static Layout layout_of(const evc_conv_geom* g, const evc_conv_cfg* cfg) {
   const int bn = cfg->bn, na = bn >= 128 ? 1 : (bn >= 32 ? 3 : 4);
   int need = bn <= 128 ? na * 2 * bn + bn : 2 * bn;
   if (bn <= 32) need = std::max(need, 6 * bn);  // the kernel sizes TMEM for the packed mode too
-  if (need <= 256 && 2 * (2 * L.stage + 1024 + 256 + 1024) <= SMEM_MAX) L.ns = 2;
+  if (need <= 256 && 2 * (2 * L.stage + 1024 + 256 + 1024) <= SMEM_MAX && !getenv("EVC_NO_OCC2")) L.ns = 2;
   return L;
 }
 

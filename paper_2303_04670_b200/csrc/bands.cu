@@ -16,6 +16,8 @@
 // conv GEMM reads (conv_fused.cu), staged through padded shared memory so the
 // planar reads and the 128-byte channel runs are both coalesced.
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace evc {
@@ -321,6 +323,36 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
   }
 }
 
+// integrate (tensors.py:167-174): y_run += where(live, dx, 0), flat over (session, channel,
+// row, 4 columns): the output is small (C1: 2 x 256 x 256) so tile-row CTAs of 32 channels
+// would leave most lanes idle; one float4 per thread, the tile flag read per vector.
+__global__ void __launch_bounds__(256) k_integrate_flat(TView a, float* __restrict__ y, int64_t ys, int64_t nvec) {
+  pdl_wait();
+  pdl_trigger();
+  const int W4 = a.W >> 2;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nvec; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t per_s = (int64_t)a.C * a.H * W4;
+    const int s = (int)(e / per_s);
+    const int64_t r = e - (int64_t)s * per_s;
+    const int q = (int)(r % W4);
+    const int64_t cu = r / W4;  // channel * H + row
+    const int u = (int)(cu % a.H), c = (int)(cu / a.H);
+    const int x = q * 4;
+    const uint8_t* F = a.f + (int64_t)s * a.fs + ((int64_t)c * a.GH + u / a.th) * a.GW;
+    const bool l0 = F[x / a.tw] != 0, l3 = F[(x + 3) / a.tw] != 0;
+    if (!l0 && !l3 && F[(x + 1) / a.tw] == 0 && F[(x + 2) / a.tw] == 0) continue;
+    const int64_t off = ((int64_t)c * a.H + u) * a.W + x;
+    const float4 d = *reinterpret_cast<const float4*>(a.v + (int64_t)s * a.vs + off);
+    float4* yp = reinterpret_cast<float4*>(y + (int64_t)s * ys + off);
+    float4 v = *yp;
+    if (F[x / a.tw]) v.x = __fadd_rn(v.x, d.x);
+    if (F[(x + 1) / a.tw]) v.y = __fadd_rn(v.y, d.y);
+    if (F[(x + 2) / a.tw]) v.z = __fadd_rn(v.z, d.z);
+    if (F[(x + 3) / a.tw]) v.w = __fadd_rn(v.w, d.w);
+    *yp = v;
+  }
+}
+
 // t_p = 0 sparsify of a tensor with few channels (C <= 8, e.g. the 4-channel event input):
 // one thread per pixel of a tile row x SM_TJ tiles, all channels per thread, so no lanes
 // idle on missing channels.  y = 0 + x (sparsify.py:69-71); flags recomputed from the values
@@ -516,6 +548,13 @@ int evc_integrate(float* y_run, int64_t y_stride, const evc_tensor* dx, int32_t 
   p.a = view_of(*dx);
   p.acc = y_run;
   p.as = y_stride;
+  if (p.a.W % 4 == 0 && al16(p.a.v) && al16(y_run) && p.a.vs % 4 == 0 && y_stride % 4 == 0) {
+    const int64_t nvec = (int64_t)S * p.a.C * p.a.H * (p.a.W / 4);
+    const int grid = (int)std::min<int64_t>((nvec + 255) / 256, 148 * 16);
+    launch_pdl(k_integrate_flat, dim3(grid), dim3(256), 0, as_stream(stream), p.a, y_run, y_stride, nvec);
+    EVC_LAUNCH_CHECK("integrate");
+    return EVC_OK;
+  }
   const int rc = tb_launch(OP_INTEGRATE, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("integrate");
   return rc;

@@ -331,7 +331,7 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   if (!a.sp_hwc) return 0.0;
   // fused sparsify_step at t_p = 0 (sparsify.py:63-71): out = 0 + y, residual stays 0; the mask is
   // recomputed from the values (sparsify.py:77-78) -- one flag store per (tile, channel) per warp
-  double ss = 0.0;
+  float ss = 0.0f;  // <= 16 squares per call in fp32, widened once per site
   const int lane = threadIdx.x & 31;
   const int tile = valid ? (u / a.th) * a.sp_GW + x / a.tw : -1;
   const unsigned grp = __match_any_sync(0xffffffffu, tile);
@@ -362,7 +362,7 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const bool in = valid && j < cnt;
-    if (in) ss += (double)o[j] * (double)o[j];
+    if (in) ss = __fmaf_rn(o[j], o[j], ss);
     const unsigned nz = __ballot_sync(0xffffffffu, in && o[j] != 0.0f);
     if (leader && (nz & grp)) {
       fl[(int64_t)(n0 + j * step) * To] = 1;
@@ -370,7 +370,7 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
     }
   }
   if (any) a.sp_fany[(int64_t)s * To + tile] = 1;  // benign race: only ever set
-  return ss;
+  return (double)ss;
 }
 
 

@@ -88,6 +88,7 @@ struct TBArgs {
   int hp;      // shadow row pitch in pixels (padded width of the consumer conv's input)
   uint8_t* fany;  // sparsify: optional any-channel tile map of the output (OR-accumulated, zeroed per step)
   int write_chw;
+  int pstride;     // sparsify: partial slots per session (evc_sparsify_partials; unused slots stay 0)
   int delta_zero;  // sparsify with tp == 0 and k == 0: the residual is identically 0, skip its traffic
   int kind;
   float alpha;
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
   if (OP == OP_SPARSIFY) {
     const int nblocks = gridDim.x * gridDim.y;
     ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
-    if (threadIdx.x == 0) p.partials[(int64_t)s * gridDim.x + blockIdx.x] = ss;
+    if (threadIdx.x == 0) p.partials[(int64_t)s * p.pstride + blockIdx.x] = ss;
     if (!p.ticket) return;  // norm / k folded later by evc_meter_step (one launch for every node)
     // last CTA to retire folds every session's partials into norm_ema / k (fixed order)
     __shared__ int s_last;
@@ -317,7 +318,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     __syncthreads();
     if (s_last) {
       __threadfence();
-      sparsify_finalize_all(p.partials, gridDim.x, p.norm_ema, const_cast<double*>(p.k), p.tp, p.decay, 0,
+      sparsify_finalize_all(p.partials, p.pstride, p.norm_ema, const_cast<double*>(p.k), p.tp, p.decay, 0,
                             gridDim.y);
     }
   }
@@ -358,63 +359,73 @@ __global__ void __launch_bounds__(256) k_integrate_flat(TView a, float* __restri
 // idle on missing channels.  y = 0 + x (sparsify.py:69-71); flags recomputed from the values
 // (sparsify.py:77-78) through shared memory; the channels-innermost hi/lo shadow gets each
 // pixel's C heads and C tails as contiguous runs.
-constexpr int SM_TJ = 6;
+constexpr int SM_TJ = 6, SM_RT = 4;  // tiles per CTA: SM_RT tile rows x SM_TJ tile columns
 __global__ void __launch_bounds__(256) k_sparsify_small(TBArgs p) {
   pdl_wait();
   pdl_trigger();
-  __shared__ uint8_t s_f[8 * SM_TJ];
+  __shared__ uint8_t s_f[SM_RT * 8 * SM_TJ];  // [tile row][channel][tile column]
   __shared__ double s_red[8];
   const TView& a = p.a;
   const int nJ = (a.GW + SM_TJ - 1) / SM_TJ;
-  const int jb = blockIdx.x % nJ, i = blockIdx.x / nJ, s = blockIdx.y;
+  const int jb = blockIdx.x % nJ, ib = blockIdx.x / nJ, s = blockIdx.y;
   const int j0 = jb * SM_TJ, nj = min(SM_TJ, a.GW - j0);
-  for (int t = threadIdx.x; t < a.C * SM_TJ; t += blockDim.x) s_f[t] = 0;
+  const int i0 = ib * SM_RT, ni = min(SM_RT, a.GH - i0);
+  for (int t = threadIdx.x; t < SM_RT * 8 * SM_TJ; t += blockDim.x) s_f[t] = 0;
   __syncthreads();
-  const int span = SM_TJ * a.tw;  // columns of this CTA (th x span <= 216 threads: th, tw <= 6 checked on host)
-  const int r = threadIdx.x / span, xq = threadIdx.x % span;
-  const int u = i * a.th + r, x = j0 * a.tw + xq;
-  const bool valid = r < a.th && u < a.H && xq < nj * a.tw && x < a.W;
+  const int span = SM_TJ * a.tw, rows = ni * a.th;  // th, tw <= 6 (checked on host)
+  const int64_t HW = (int64_t)a.H * a.W;
+  const bool vec4 = a.C == 4 && p.cp == 4;  // 16-byte runs of heads and of tails per pixel
   float ss = 0.0f;
-  if (valid) {
-    const int64_t HW = (int64_t)a.H * a.W, off = (int64_t)u * a.W + x;
+  for (int t = threadIdx.x; t < rows * span; t += blockDim.x) {
+    const int r = t / span, xq = t - r * span;
+    const int u = i0 * a.th + r, x = j0 * a.tw + xq;
+    if (u >= a.H || xq >= nj * a.tw || x >= a.W) continue;
+    const int64_t off = (int64_t)u * a.W + x;
     const float* src = a.v + (int64_t)s * a.vs + off;
     float v[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       if (c < a.C) v[c] = __fadd_rn(0.0f, src[c * HW]);
-    const int tj = xq / a.tw;
+    uint8_t* f = s_f + (r / a.th) * 8 * SM_TJ + xq / a.tw;
     float* sh = p.hwc ? p.hwc + (int64_t)s * p.hs + ((int64_t)u * p.hp + x) * 2 * p.cp : nullptr;
+    if (sh && vec4) {
+      const float4 h = make_float4(tf32_head(v[0]), tf32_head(v[1]), tf32_head(v[2]), tf32_head(v[3]));
+      *reinterpret_cast<float4*>(sh) = h;
+      *reinterpret_cast<float4*>(sh + 4) =
+          make_float4(__fsub_rn(v[0], h.x), __fsub_rn(v[1], h.y), __fsub_rn(v[2], h.z), __fsub_rn(v[3], h.w));
+    }
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       if (c >= a.C) break;
       if (p.write_chw) p.y.v[(int64_t)s * p.y.vs + c * HW + off] = v[c];
-      if (sh) hwc_store(sh, p.cp, c, v[c]);
+      if (sh && !vec4) hwc_store(sh, p.cp, c, v[c]);
       ss = __fmaf_rn(v[c], v[c], ss);
-      if (v[c] != 0.0f) s_f[c * SM_TJ + tj] = 1;
+      if (v[c] != 0.0f) f[c * SM_TJ] = 1;
     }
   }
   double d = warp_sum_d((double)ss);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = d;
   __syncthreads();
-  for (int t = threadIdx.x; t < a.C * nj; t += blockDim.x) {
-    const int c = t / nj, jl = t % nj;
-    const int64_t fo = ((int64_t)c * a.GH + i) * a.GW + j0 + jl;
-    p.y.f[(int64_t)s * p.y.fs + fo] = s_f[c * SM_TJ + jl];
+  for (int t = threadIdx.x; t < ni * a.C * nj; t += blockDim.x) {
+    const int il = t / (a.C * nj), e = t - il * a.C * nj, c = e / nj, jl = e - c * nj;
+    const int64_t fo = ((int64_t)c * a.GH + i0 + il) * a.GW + j0 + jl;
+    p.y.f[(int64_t)s * p.y.fs + fo] = s_f[(il * 8 + c) * SM_TJ + jl];
   }
-  if (p.fany && threadIdx.x < nj) {
+  if (p.fany && threadIdx.x < ni * nj) {
+    const int il = threadIdx.x / nj, jl = threadIdx.x - il * nj;
     int any = 0;
-    for (int c = 0; c < a.C; ++c) any |= s_f[c * SM_TJ + threadIdx.x];
-    if (any) p.fany[((int64_t)s * a.GH + i) * a.GW + j0 + threadIdx.x] = 1;
+    for (int c = 0; c < a.C; ++c) any |= s_f[(il * 8 + c) * SM_TJ + jl];
+    if (any) p.fany[((int64_t)s * a.GH + i0 + il) * a.GW + j0 + jl] = 1;
   }
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
-    p.partials[(int64_t)s * gridDim.x + blockIdx.x] = t;
+    p.partials[(int64_t)s * p.pstride + blockIdx.x] = t;
   }
 }
 
 static bool small_ok(const TView& v) { return v.C <= 8 && v.th <= 6 && v.tw <= 6; }
-static int small_blocks(const TView& v) { return v.GH * ((v.GW + SM_TJ - 1) / SM_TJ); }
+static int small_blocks(const TView& v) { return ((v.GH + SM_RT - 1) / SM_RT) * ((v.GW + SM_TJ - 1) / SM_TJ); }
 
 template <int OP>
 static void launch_op(const TBArgs& p, const TBGeo& g, int S, cudaStream_t st) {
@@ -506,6 +517,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   p.fany = fany;
   p.write_chw = write_chw;
   p.delta_zero = delta_zero;
+  p.pstride = (int)evc_sparsify_partials(dx);
   if (delta_zero && !ticket && small_ok(p.a)) {  // few channels at t_p = 0: thread per pixel
     launch_pdl(k_sparsify_small, dim3((unsigned)small_blocks(p.a), (unsigned)S), dim3(256), 0, as_stream(stream), p);
     EVC_LAUNCH_CHECK("sparsify_small");

@@ -64,7 +64,7 @@ def sparsify_step(x: IncrementTensor, state: SparsifyState) -> IncrementTensor:
     yf = torch.zeros(grid_shape(x.shape, tile), dtype=torch.uint8, device=dev)
     lib = _lib.lib()
     dx = x.desc()
-    part = torch.empty(int(lib.evc_sparsify_partials(dx)), dtype=torch.float64, device=dev)
+    part = torch.zeros(int(lib.evc_sparsify_partials(dx)), dtype=torch.float64, device=dev)
     sc = torch.tensor([state.norm_ema, state.k], dtype=torch.float64, device=dev)
     s = _lib.stream_ptr()
     dy = _lib.tdesc(_lib.ptr(yv), _lib.ptr(yf), 0, 0, c, h, w, tile.h, tile.w)

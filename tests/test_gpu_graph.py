@@ -189,6 +189,11 @@ def test_cuda_graph_matches_eager_and_sessions_match_single():
         assert rb.keys() == ra.keys()
         for k in ra:  # meters see the same masks up to rounding-zero flips
             assert abs(rb[k][0] - ra[k][0]) <= 1e-4 * ra[k][1] and rb[k][1] == ra[k][1], k
+        # per-session sparsify norms: every session folds exactly its own partial sums
+        fb, fa = gb.state_fingerprint(session=s), ga[s].state_fingerprint()
+        for k in (k for k in fa if k.endswith(".norm")):
+            vb, va = np.asarray(fb[k], np.float64), np.asarray(fa[k], np.float64)
+            assert vb.shape == va.shape and np.allclose(vb, va, rtol=1e-5, atol=1e-5), (k, vb, va)
     # CUDA-graph replay and eager launches run the identical kernels: bit-identical
     ge = evc.build(spec, weights, refresh_interval=0, cuda_graph=False)
     ge.dense_pass(xs[0][0])

@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
     const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
     const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i0 + tr) * y.GW + j0 + jl;
-    s_nd[t] = y.f[(int64_t)s * y.fs + fo] | a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo];
+    // t_p = 0 (fast path): the residual and its live flags are identically 0 -- not read
+    s_nd[t] = y.f[(int64_t)s * y.fs + fo] | (a.fast ? 0 : a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo]);
     s_ny[t] = 0;
   }
   if (box_fits)
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i0 + tr) * y.GW + j0 + jl;
       y.f[(int64_t)s * y.fs + fo] = s_ny[t];
       if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i0 + tr) * y.GW + j0 + jl] = 1;  // benign race: all store 1
-      a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
+      if (!a.fast) a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage && !fast && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
       float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * 2 * a.cp + c0 + lane;

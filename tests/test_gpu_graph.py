@@ -223,6 +223,31 @@ def test_resnet18_steps_vs_oracle():
             assert abs(p - orep["per_node"][k][0]) <= 1e-4 * d, k
 
 
+def test_c2_unet_voxel_steps_vs_oracle():
+    """C2: E2Depth-style UNet on 5-bin voxel grids of a 260 x 346 sensor,
+    zero-padded bottom / right to 264 x 352; dense pass + 3 increments against the oracle."""
+    spec = configs.unet_e2depth_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    stream = evc.generate_events(seed=5, duration_us=54_000, rate_hz=3e5, n_objects=8, sensor_size=(260, 346))
+    xs = [torch.nn.functional.pad(evc.encode(evc.slice_window(stream, 50_000 + 1_000 * i, 50_000),
+                                             evc.parse_encoder("voxel:5")), (0, 6, 0, 4)).contiguous()
+          for i in range(4)]
+    g = evc.build(spec, weights, refresh_interval=0)
+    og = O.OracleGraph(spec.to_dict(), weights, refresh_interval=0)
+    e0 = max_err(np_(g.dense_pass(xs[0])), og.dense_pass(np_(xs[0])))
+    assert e0 <= 1e-4, e0
+    for i in range(1, 4):
+        rv, rf = O.step_increment(np_(xs[i - 1]), np_(xs[i]), 6, 6)
+        x_up = evc.step_increment(xs[i - 1], xs[i], spec.tile)
+        assert np.array_equal(x_up.mask.numpy(), rf)
+        yup, y, rep = g.incr_step(x_up)
+        _, oy, orep = og.incr_step(rv, rf)
+        e = max_err(np_(y), oy)
+        assert e <= 1e-4, e
+        for k, (p, d) in rep.per_node.items():
+            assert abs(p - orep["per_node"][k][0]) <= 1e-4 * d, k
+
+
 def test_tp_positive_refresh_restores():
     spec = evc.build_plain_cnn(depth=4, channels=16, tp=0.05, in_shape=(2, 64, 64))
     weights = evc.WeightManifest.random_tensors(spec, 0)

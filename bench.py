@@ -275,11 +275,22 @@ def conv_roofline(g, xs, args, evc):
     achieved = f / t / 1e12
     peak = 0.5 * bf16  # dense TF32 tensor peak = 1/2 measured bf16
     n_launch = sum(1 for _, _, n in prog if n in ("conv_fused", "conv_gemm"))
+    traffic, tsrc = None, None
+    tp = Path(__file__).resolve().parent / "profiles" / "r01_conv_traffic_s32.json"
+    if tp.exists():  # ncu DRAM bytes of the same 16 launches (one step), committed under profiles/
+        tj = json.loads(tp.read_text())
+        if tj.get("sessions") == S and tj.get("launches_per_step") == n_launch_expected(g2):
+            traffic, tsrc = tj["dram_bytes_per_step"], f"profiles/{tp.name} ({tj['source']})"
     return {"bound": "tensor", "kernel": "conv_fused (all 16 conv layers incl. fused mask/meter/activation, per step)", "achieved": achieved,
-            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step",
+            "traffic_source": tsrc,
             "peak_source": f"0.5 x {src} bf16 ({bf16} TF) as the TF32 tensor peak",
             "algorithmic_flops_per_step": f, "gemm_ms_per_step": t * 1e3, "gemm_launches_per_step": n_launch,
             "gemm_share_of_eager_step": (sum(gemm_ms) / sum(step_ms)) if step_ms else None}
+
+
+def n_launch_expected(g):
+    return sum(1 for _, _, n in g._program if n in ("conv_fused", "conv_gemm"))
 
 
 def _weights_of(g):

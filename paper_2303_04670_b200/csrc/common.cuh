@@ -228,8 +228,8 @@ __device__ __forceinline__ void upsample_box(int o0, int o1, int n_in, int f, in
 // Sum each session's partials in a fixed order, then the EMA / k update
 // (sparsify.py:72-76) or the reset (sparsify.py:43-51).  One CTA does all S.
 __device__ __forceinline__ void sparsify_finalize_all(const double* partials, int64_t n, double* norm_ema, double* kdev, double tp,
-                                      double decay, int reset, int S) {
-  for (int s = 0; s < S; ++s) {
+                                      double decay, int reset, int S, int s_first = 0) {
+  for (int s = s_first; s < S; ++s) {
     double sum = 0.0;
     for (int64_t e = threadIdx.x; e < n; e += blockDim.x) sum += ((volatile const double*)partials)[(int64_t)s * n + e];
     sum = block_sum<double>(sum, [](double v) { return warp_sum_d(v); });

@@ -1302,9 +1302,10 @@ __global__ void __launch_bounds__(256) k_meter_step(const evc_meter_node* __rest
                                                     const evc_sp_node* __restrict__ sp) {
   pdl_wait();
   pdl_trigger();
-  if ((int)blockIdx.x >= n * S) {
-    const evc_sp_node nd = sp[blockIdx.x - n * S];
-    sparsify_finalize_all(nd.partials, nd.n, nd.norm_ema, nd.k, nd.tp, nd.decay, 0, S);
+  if ((int)blockIdx.x >= n * S) {  // one (sparsify node, session) per block: its partials in fixed order
+    const int b = blockIdx.x - n * S, j = b / S, s = b % S;
+    const evc_sp_node nd = sp[j];
+    sparsify_finalize_all(nd.partials, nd.n, nd.norm_ema, nd.k, nd.tp, nd.decay, 0, s + 1, s);
     return;
   }
   const int l = blockIdx.x / S, s = blockIdx.x % S, e = l * S + s;
@@ -1793,7 +1794,7 @@ int evc_meter_step(const evc_meter_node* nodes, int32_t n, int32_t S, int32_t* i
   EVC_CHECK_ARG(nodes && n > 0 && S > 0 && in_true && perf_step && perf_cum && ff_last && ff_sum && n_sp >= 0 &&
                     (n_sp == 0 || sp_nodes),
                 "meter_step: null argument");
-  launch_pdl(fz::k_meter_step, dim3((unsigned)(n * S + n_sp)), dim3(256), 0, as_stream(stream), nodes, n, S, in_true,
+  launch_pdl(fz::k_meter_step, dim3((unsigned)(n * S + n_sp * S)), dim3(256), 0, as_stream(stream), nodes, n, S, in_true,
              reinterpret_cast<long long*>(perf_step), reinterpret_cast<long long*>(perf_cum), ff_last, ff_sum,
              sp_nodes);
   EVC_LAUNCH_CHECK("meter_step");

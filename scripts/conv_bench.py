@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--act", type=int, default=1)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--sessions", type=int, default=1)
+    ap.add_argument("--cin", type=int, default=0)
     args = ap.parse_args()
     want = set(args.layers.split(",")) if args.layers else None
     lib = _lib.lib()
@@ -47,6 +48,8 @@ def main():
     for nid, (c, h, w), at in layers():
         if want and nid not in want:
             continue
+        if args.cin:  # what-if: the same layer with another input channel count
+            c = args.cin
         k = int(at["kernel"][0])
         st, pad, co = int(at.get("stride", 1)), int(at.get("padding", 0)), int(at["out_channels"])
         wt = torch.randn(co, c, k, k, device=dev) * (2.0 / (c * k * k)) ** 0.5

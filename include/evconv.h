@@ -411,6 +411,21 @@ int evc_bin_events(const uint64_t* t, const uint16_t* x, const uint16_t* y,
                    int32_t bins, float* out, void* workspace,
                    int64_t workspace_bytes, void* stream);
 
+/* Event ingest (ingest.cu).
+ * read_events' EVB record view (events.py:185-206): n packed little-endian 13-byte
+ * records {u64 t, u16 x, u16 y, i8 p} (events.py:35-37) already on the device ->
+ * the t / x / y / p columns evc_bin_events reads. */
+int evc_unpack_events(const uint8_t* records, int64_t n, uint64_t* t, uint16_t* x,
+                      uint16_t* y, int8_t* p, void* stream);
+
+/* step_increment(encode(prev, "count"), encode(cur, "count")) (events.py:295-302
+ * over events.py:267-272) from only the events that leave ([lo_prev, lo_cur)) and
+ * enter ([hi_prev, hi_cur)) the window: out (C = 2, one session) receives the
+ * values and their exact tile mask, bit-identical to the two encodings' diff. */
+int evc_count_increment(const uint16_t* x, const uint16_t* y, const int8_t* p,
+                        int64_t lo_prev, int64_t hi_prev, int64_t lo_cur,
+                        int64_t hi_cur, const evc_tensor* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -123,6 +123,8 @@ _PROTOS = {
     "evc_linear": (_I32, [_T, _P, _P, _T, _I32, _I32, _P, _P, _I32, _P]),
     "evc_bin_events_workspace": (_I64, [_I64, _I32, _I32, _I32]),
     "evc_bin_events": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _I64, _P]),
+    "evc_unpack_events": (_I32, [_P, _I64, _P, _P, _P, _P, _P]),
+    "evc_count_increment": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _T, _P]),
 }
 
 EXPORTED = tuple(_PROTOS)

@@ -1498,7 +1498,14 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
                (int64_t)g->kh * g->kw * g->c_in * g->c_out * 4 <= 48 * 1024)
                   ? 1
                   : 0;
-  cfg->row = (!cfg->thin && g->stride == 1 && g->kw <= 9 && g->Wo == g->W + 2 * g->pad - g->kw + 1) ? 1 : 0;
+  // row mode caps BN at 64 (kw taps of weights per stage); with C_out >= 128 the wider channel
+  // block of tap mode wins (fewer MMA cycles per output, the A tile read once per 128+ outputs;
+  // measured: res 256->256 @16x16 96 vs 128 us, dec0 512->128 @32x32 268 vs 306 us at 32 streams;
+  // with few streams the row mode's shorter per-region latency wins)
+  cfg->row = (!cfg->thin && g->stride == 1 && g->kw <= 9 && g->Wo == g->W + 2 * g->pad - g->kw + 1 &&
+              (g->c_out <= 64 || S < 8) && std::getenv("EVC_NO_ROW") == nullptr)
+                 ? 1
+                 : 0;
   if (cfg->thin) {
     cfg->rw = g->Wo > 16 ? 32 : (g->Wo > 8 ? 16 : 8);
     cfg->rh = fz::BM / cfg->rw;

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   auto tap_i1 = [&](int u, int n) { return a.mode == 0 ? u / a.f : bilinear_tap(u, n, a.f).i1; };
   const int rlo = tap_i0(r0, a.x.H), nr = tap_i1(r0 + nrow - 1, a.x.H) - rlo + 1;
   const int clo = tap_i0(x0, a.x.W), ncl = tap_i1(x0 + ncol - 1, a.x.W) - clo + 1;
+  const FDiv d_th = fdiv_of(a.x.th), d_tw = fdiv_of(a.x.tw), d_NT = fdiv_of(NT), d_nj = fdiv_of(nj);
   const int alo = rlo / a.x.th, ahi = (rlo + nr - 1) / a.x.th;
   const int blo0 = clo / a.x.tw, bhi0 = (clo + ncl - 1) / a.x.tw;
   const int na_ = ahi - alo + 1, nb_ = bhi0 - blo0 + 1;
@@ -101,26 +102,28 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   // last step's output / residual flags and the input flags of the box (all channels):
   // every load in flight at once
   for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
-    const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
+    const int cl = fdiv(t, d_NT), e = t - cl * NT, tr = fdiv(e, d_nj), jl = e - tr * nj;
     const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i0 + tr) * y.GW + j0 + jl;
     // t_p = 0 (fast path): the residual and its live flags are identically 0 -- not read
     s_nd[t] = y.f[(int64_t)s * y.fs + fo] | (a.fast ? 0 : a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo]);
     s_ny[t] = 0;
   }
-  if (box_fits)
+  if (box_fits) {
+    const FDiv d_box = fdiv_of(na_ * nb_), d_nb = fdiv_of(nb_);
     for (int t = threadIdx.x; t < nc * na_ * nb_; t += US_THREADS) {
-      const int cl = t / (na_ * nb_), e = t % (na_ * nb_);
-      s_fin[t] = a.x.fplane(s, c0 + cl)[(alo + e / nb_) * a.x.GW + blo0 + e % nb_];
+      const int cl = fdiv(t, d_box), e = t - cl * na_ * nb_, ea = fdiv(e, d_nb);
+      s_fin[t] = a.x.fplane(s, c0 + cl)[(alo + ea) * a.x.GW + blo0 + e - ea * nb_];
     }
+  }
   __syncthreads();
   // 2) process a tile when its upsample support is live, or it was live / left a residual
   bool any = false;
   for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
-    const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
+    const int cl = fdiv(t, d_NT), e = t - cl * NT, tr = fdiv(e, d_nj), jl = e - tr * nj;
     const int xa = jl * y.tw, xb = min(ncol, xa + y.tw) - 1;
     const int ya = tr * y.th, yb = min(nrow, ya + y.th) - 1;
-    const int blo = s_ci0[xa] / a.x.tw, bhi = s_ci1[xb] / a.x.tw;
-    const int alo_t = s_ri0[ya] / a.x.th, ahi_t = s_ri1[yb] / a.x.th;
+    const int blo = fdiv(s_ci0[xa], d_tw), bhi = fdiv(s_ci1[xb], d_tw);
+    const int alo_t = fdiv(s_ri0[ya], d_th), ahi_t = fdiv(s_ri1[yb], d_th);
     uint8_t live = 0;
     if (box_fits) {
       for (int aa = alo_t; aa <= ahi_t; ++aa)
@@ -151,9 +154,11 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       s_ro1[threadIdx.x] = (s_ri1[threadIdx.x] - rlo) * a.XC;
     }
     {  // flat (channel, row, column) walk; the index is advanced by carries, not divisions
-      int cc = threadIdx.x % ncl, t2 = threadIdx.x / ncl;
-      int rr = t2 % nr, cl = t2 / nr;
-      const int dcc = US_THREADS % ncl, dt2 = US_THREADS / ncl, drr = dt2 % nr, dcl = dt2 / nr;
+      const FDiv d_ncl = fdiv_of(ncl), d_nr = fdiv_of(nr);
+      int t2 = fdiv(threadIdx.x, d_ncl), cc = threadIdx.x - t2 * ncl;
+      int cl = fdiv(t2, d_nr), rr = t2 - cl * nr;
+      const int dt2 = fdiv(US_THREADS, d_ncl), dcc = US_THREADS - dt2 * ncl;
+      const int dcl = fdiv(dt2, d_nr), drr = dt2 - dcl * nr;
       const float* xs = a.x.plane(s, c0) + (int64_t)rlo * a.x.W + clo;
       const int64_t xHW = (int64_t)a.x.H * a.x.W;
       for (; cl < nc;) {
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
     }
     __syncthreads();
     for (int t = threadIdx.x; t < nc * NT; t += US_THREADS) {
-      const int cl = t / NT, e = t - cl * NT, tr = e / nj, jl = e - tr * nj;
+      const int cl = fdiv(t, d_NT), e = t - cl * NT, tr = fdiv(e, d_nj), jl = e - tr * nj;
       const int64_t fo = ((int64_t)(c0 + cl) * y.GH + i0 + tr) * y.GW + j0 + jl;
       y.f[(int64_t)s * y.fs + fo] = s_ny[t];
       if (a.fany && s_ny[t]) a.fany[((int64_t)s * y.GH + i0 + tr) * y.GW + j0 + jl] = 1;  // benign race: all store 1

@@ -1170,7 +1170,7 @@ __device__ __forceinline__ void thin_fma(float* acc, float x, const float* w) {
 }
 
 template <int CO>  // output channels padded to CO (2, 4, 8, 16, 32); weights [tap][c_in][CO]
-__global__ void __launch_bounds__(THIN_THREADS) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
+__global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
                                                             const __grid_constant__ Args a) {
   extern __shared__ float s_w[];
   __shared__ int s_flag[2];

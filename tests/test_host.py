@@ -203,3 +203,41 @@ def test_config_specs():
     assert sh["stem_pool"] == (64, 44, 59) and sh["s3b1_act"] == (512, 6, 8) and sh["fc"] == (101, 1, 1)
     c2 = configs.unet_e2depth_spec()
     assert len(c2.nodes) == 47
+
+
+def _c1_conv_cfgs(S):
+    lib = _lib.load(require_cuda=False)
+    spec = configs.evflownet_spec()
+    shapes = spec.infer_shapes()
+    out = {}
+    for n in spec.topo_order():
+        if n.kind != "conv":
+            continue
+        c, h, w = shapes[n.inputs[0]]
+        k, st, pad = int(n.attrs["kernel"][0]), int(n.attrs.get("stride", 1)), int(n.attrs.get("padding", 0))
+        co = int(n.attrs["out_channels"])
+        ho, wo = O.conv_out_hw(h, w, k, k, st, pad)
+        g = _lib.EvcConvGeom(c, co, k, k, st, pad, h, w, ho, wo, 6, 6)
+        cfg = _lib.EvcConvCfg()
+        assert lib.evc_conv_fused_config(g, S, 0, cfg) == 0
+        out[n.id] = (cfg.thin, cfg.row, cfg.bn, cfg.splits)
+        assert lib.evc_conv_fused_ctas(g, cfg) > 0
+    return out
+
+
+def test_conv_launch_configuration_rules():
+    """evc_conv_fused_config: CUDA-core path for the 4-channel input and the
+    2-channel heads; packed row mode for the thin decoders; row mode for C_out <= 64; tap mode with
+    128-channel blocks for wide layers at many streams, row mode at one stream; split-K when the
+    grid is shorter than the SM count."""
+    s32, s1 = _c1_conv_cfgs(32), _c1_conv_cfgs(1)
+    for cfgs in (s32, s1):
+        assert cfgs["enc0"][0] == 1 and all(cfgs[f"pred{i}"][0] == 1 for i in range(4))
+        assert cfgs["dec3"][1:3] == (2, 16) and cfgs["dec2"][1:3] == (2, 32)
+        assert cfgs["dec1"][1:3] == (1, 64)
+        assert cfgs["enc1"][1] == 0  # stride 2: tap mode
+    for nid in ("res0a", "res0b", "res1a", "res1b", "dec0"):
+        assert s32[nid][1] == 0 and s32[nid][2] == 128, (nid, s32[nid])
+        assert s1[nid][1] == 1, (nid, s1[nid])
+    assert s32["enc3"][1:] == (0, 128, 2)  # short grid: cluster split-K
+    assert s32["res0a"][3] >= 2 and s1["res0a"][3] >= 2

@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     const float k32 = __double2float_rn(kd);
     const int nq = ncol / V;  // vector units per row chunk (ncol % V == 0 by construction)
     const int n = nc * nrow * nq;
+    const FDiv d_nq = fdiv_of(nq), d_nrow = fdiv_of(nrow), d_tw = fdiv_of(g.tw);
     const int64_t sa = (int64_t)s * p.a.vs, sy = (int64_t)s * p.y.vs, sacc = (int64_t)s * p.as;
     const int64_t sb = (OP == OP_ADD || OP == OP_MUL) ? (int64_t)s * p.b.vs : 0;
     for (int base = threadIdx.x; base < n; base += TB_THREADS * TB_UNROLL) {
@@ -182,12 +183,12 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         const int e = base + u * TB_THREADS;
         on[u] = false;
         if (e >= n) continue;
-        const int q = e % nq, t2 = e / nq;
-        const int r = t2 % nrow, cl = t2 / nrow;
+        const int t2 = fdiv(e, d_nq), q = e - t2 * nq;
+        const int cl = fdiv(t2, d_nrow), r = t2 - cl * nrow;
         const int xl = q * V;
         bool pr = false;
 #pragma unroll
-        for (int k = 0; k < V; ++k) pr |= s_proc[cl * nj + (xl + k) / g.tw] != 0;
+        for (int k = 0; k < V; ++k) pr |= s_proc[cl * nj + fdiv(xl + k, d_tw)] != 0;
         cl_[u] = cl;
         r_[u] = r;
         xl_[u] = xl;
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
             VT::set(out, k, o);
             VT::set(acc_new, k, nd);
             ss += (double)corr * (double)corr;
-            const int ti = cl_[u] * nj + (xl_[u] + k) / g.tw;
+            const int ti = cl_[u] * nj + fdiv(xl_[u] + k, d_tw);
             if (o != 0.0f) s_f1[ti] = 1;
             if (nd != 0.0f) s_f2[ti] = 1;
             if (stage) s_y[(r_[u] * 32 + xl_[u] + k) * 33 + cl_[u]] = o;

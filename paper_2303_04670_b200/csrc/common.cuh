@@ -157,8 +157,9 @@ __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// floor(a / d) for 0 <= a < 2^16 through an fp32 reciprocal: the error of (a + 0.5) * RN(1/d)
-// is below 2^-7 / d, inside the 0.5 / d margin to the next integer, so the result is exact.
+// floor(a / d) for 0 <= a < 2^22 through an fp32 reciprocal: (a + 0.5) is exact and the
+// relative error of (a + 0.5) * RN(1/d) is <= 2^-23, i.e. below a * 2^-23 / d < 0.5 / d, the
+// distance of (a + 0.5) / d to the next integer -- so the truncation is exact.
 // Replaces the ~20-instruction integer division in per-element index math.
 struct FDiv {
   float inv;

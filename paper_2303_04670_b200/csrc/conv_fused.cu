@@ -866,8 +866,15 @@ __device__ __forceinline__ bool region_live_warp(const Args& a, int s, int rr) {
   return __any_sync(0xffffffffu, live) != 0;
 }
 
+// epilogue warps of the persistent kernel: 8 (two per TMEM lane quarter, each taking half of
+// the channel block) when one CTA owns the SM, 4 when two co-reside (BN = 16)
 template <int BN>
-__global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(const __grid_constant__ CUtensorMap tmap,
+__host__ __device__ constexpr int persist_epi_warps() { return BN >= 32 ? 8 : 4; }
+template <int BN>
+__host__ __device__ constexpr int persist_threads() { return (4 + persist_epi_warps<BN>()) * 32; }
+
+template <int BN>
+__global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_conv_persist(const __grid_constant__ CUtensorMap tmap,
                                                                               const __grid_constant__ Args a) {
   constexpr int BUF = BN <= 32 ? 6 * BN : 3 * BN;  // packed: 3 taps x [A.B_hi | A.B_lo]; CAT: [hi.hi | hi.lo | lo.hi]
   constexpr int TMEM_COLS = 2 * BUF <= 128 ? 128 : (2 * BUF <= 256 ? 256 : 512);
@@ -875,6 +882,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
   constexpr uint32_t IDESC = IDESC_BASE | ((uint32_t)(BN >> 3) << 17);
   constexpr uint32_t IDESC2 = IDESC_BASE | ((uint32_t)((2 * BN) >> 3) << 17);
   constexpr int MAXNS = 4;
+  constexpr int EPI = persist_epi_warps<BN>(), NH = EPI / 4;  // epilogue warps, channel halves
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int R = a.R, nb = (a.c_out + BN - 1) / BN;
   const int n_items = a.S * R * nb;
@@ -900,7 +908,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(tfull_bar(i), 1);
-      bar_init(tempty_bar(i), 128);
+      bar_init(tempty_bar(i), 32 * EPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -1009,9 +1017,11 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
       }
     }
   } else {  // -------------------------------------------------------------------- epilogue
-    __shared__ float s_xch[4][3][3][8];
-    __shared__ double s_red[4];
+    __shared__ float s_xch[NH][4][3][3][8];
+    __shared__ double s_red[EPI];
     const int q4 = warp & 3, m = 32 * q4 + lane;
+    const int half = NH > 1 ? (warp - 4) >> 2 : 0;  // channel half of the block (NH = 2) or 0
+    // named barrier of this half's four warps: id 2 (half 0) or 4 (half 1)
     const int Qs = R * nb;
     int li = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -1043,8 +1053,10 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
         if (packed) {
           const int KW = a.kw;
           float o_all[BN <= 32 ? BN : 8];
+          constexpr int CH = (BN <= 32 ? BN : 8) / NH;  // channels of this half
 #pragma unroll
-          for (int c0 = 0; c0 < (BN <= 32 ? BN : 8); c0 += 8) {
+          for (int cc = 0; cc < CH; cc += 8) {
+            const int c0 = half * CH + cc;
             float v[3][8];
             {
               uint32_t r4[3][2][8];
@@ -1072,9 +1084,12 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
             for (int s2 = 1; s2 < 3; ++s2)
               if (s2 < KW && lane < s2) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) s_xch[q4][s2][lane][e] = v[s2][e];
+                for (int e = 0; e < 8; ++e) s_xch[half][q4][s2][lane][e] = v[s2][e];
               }
-            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (half == 0)
+              asm volatile("bar.sync 2, 128;" ::: "memory");
+            else
+              asm volatile("bar.sync 4, 128;" ::: "memory");
 #pragma unroll
             for (int e = 0; e < 8; ++e) o_all[(c0 + e) % (BN <= 32 ? BN : 8)] = v[0][e];
 #pragma unroll
@@ -1083,22 +1098,27 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 float t = __shfl_down_sync(0xffffffffu, v[s2][e], s2);
-                if (lane >= 32 - s2) t = q4 < 3 ? s_xch[q4 + 1][s2][lane + s2 - 32][e] : 0.0f;
+                if (lane >= 32 - s2) t = q4 < 3 ? s_xch[half][q4 + 1][s2][lane + s2 - 32][e] : 0.0f;
                 o_all[(c0 + e) % (BN <= 32 ? BN : 8)] = __fadd_rn(o_all[(c0 + e) % (BN <= 32 ? BN : 8)], t);
               }
             }
-            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (half == 0)
+              asm volatile("bar.sync 2, 128;" ::: "memory");
+            else
+              asm volatile("bar.sync 4, 128;" ::: "memory");
           }
           // TMEM buffer free: the next item's MMAs may overwrite it while we store
           fence_before();
           bar_arrive(tempty_bar(ab));
           const int n0 = nblk * BN;
 #pragma unroll
-          for (int c0 = 0; c0 < (BN <= 32 ? BN : 8); c0 += 8)
+          for (int cc = 0; cc < CH; cc += 8) {
+            const int c0 = half * CH + cc;
             ssq += emit<8>(a, s, u, x, n0 + c0, 1, min(8, a.c_out - n0 - c0), o_all + c0);
+          }
         } else {
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
+          for (int c0 = half * (BN / NH); c0 < (half + 1) * (BN / NH); c0 += 16) {
             uint32_t r[3][16];
             tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), r[0]);  // lo . hi
             tmem_ld16_issue(trow + (uint32_t)(BN + c0), r[1]);      // hi . lo
@@ -1112,7 +1132,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               vals[e] = __fadd_rn(__fadd_rn(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])), __uint_as_float(r[2][e]));
-            if (c0 + 16 >= BN) {  // last TMEM read of this buffer
+            if (c0 + 16 >= (half + 1) * (BN / NH)) {  // this thread's last TMEM read of the buffer
               fence_before();
               bar_arrive(tempty_bar(ab));
             }
@@ -1125,14 +1145,17 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_persist(co
       // per-item bookkeeping: region state, sum of squares of the fused sparsify
       if (a.sp_part) {
         const double w = warp_sum_d(ssq);
-        if (lane == 0) s_red[q4] = w;
+        if (lane == 0) s_red[warp - 4] = w;
       }
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * EPI) : "memory");
       if (threadIdx.x == 128) {
-        if (a.sp_part) a.sp_part[(int64_t)s * Qs + nblk * R + rr] = s_red[0] + s_red[1] + s_red[2] + s_red[3];
+        double tot = 0.0;
+#pragma unroll
+        for (int w = 0; w < EPI; ++w) tot += s_red[w];
+        if (a.sp_part) a.sp_part[(int64_t)s * Qs + nblk * R + rr] = tot;
         if (!a.dense && live != (prev != 0)) a.rstate[rs_idx] = live ? 1 : 0;
       }
-      asm volatile("bar.sync 3, 128;" ::: "memory");
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * EPI) : "memory");
     }
   }
   fence_before();
@@ -1395,7 +1418,7 @@ static int attr_persist() {
 
 template <int BN>
 static cudaError_t launch_persist(const CUtensorMap& m, const Args& a, int grid, cudaStream_t st) {
-  return launch_pdl(k_conv_persist<BN>, dim3((unsigned)grid), dim3(THREADS), (size_t)a.ns * a.stage + 1024 + 256, st,
+  return launch_pdl(k_conv_persist<BN>, dim3((unsigned)grid), dim3(persist_threads<BN>()), (size_t)a.ns * a.stage + 1024 + 256, st,
                     m, a);
 }
 

@@ -1,4 +1,4 @@
-"""The device replay harness (replay.py) against the reference's bench.replay / sweep reports
+"""The device replay harness (bench_report.py) against the reference's bench.replay / sweep reports
 (golden: tests/golden/make_replay_golden.py, reference bench.py:140-265): same CSV schema, and
 every non-wall-clock column equal -- FLOP meters and false-tile fractions exactly, drift within
 the float tolerance of the graph parity tests."""
@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2303_04670_b200 as evc
-from paper_2303_04670_b200 import replay as R
+from paper_2303_04670_b200 import bench_report as R
 from evc_testutil import GOLDEN
 
 pytestmark = pytest.mark.gpu

@@ -183,15 +183,17 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       const int Q = 32 / nc, cl = lane % nc, q = lane / nc;
       const int RS = a.RS;
       float* s_r = s_x + US_C * cs;  // [channel][row][input col] row-interpolated input
-      if (q < Q) {
+      if (q < Q) {  // work items (row, column half): the per-row taps are read once per 8+ columns
         const float* xc = s_x + cl * cs;
         float* rc = s_r + cl * RS;
-        for (int r = 0; r < nrow; ++r) {
+        const int half_c = (ncl + 1) >> 1;
+        for (int it = warp; it < 2 * nrow; it += US_THREADS / 32) {
+          const int r = it >> 1, c0 = (it & 1) * half_c, c1 = min(ncl, c0 + half_c);
           const float* xr0 = xc + s_ro0[r];
           const float* xr1 = xc + s_ro1[r];
           const float rw0 = s_rw0[r], rw1 = s_rw1[r];
           float* rr_ = rc + r * a.XC;
-          for (int c = warp * Q + q; c < ncl; c += (US_THREADS / 32) * Q)
+          for (int c = c0 + q; c < c1; c += Q)
             rr_[c] = a.mode == 0 ? xr0[c] : __fadd_rn(__fmul_rn(xr0[c], rw0), __fmul_rn(xr1[c], rw1));
         }
       }

@@ -185,18 +185,27 @@ def run_ours(args):
     from paper_2303_04670_b200 import configs
 
     rank, world, local = dist_env()
+    # test knob: EVC_BENCH_SHARE_GPU=1 runs every rank on GPU 0 over gloo (the N > 1 logic on a
+    # one-GPU box); the product path is one rank per GPU over NCCL
+    share = os.environ.get("EVC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    cdev = None if share else dev  # device of the max-over-ranks reduction tensors
     spec = configs.evflownet_spec(tp=0.0)
     weights = evc.WeightManifest.random_tensors(spec, 0)
     S = args.sessions
     res = timed_run(evc, spec, weights, S, args.steps, args.warmup, rank, world, dev)
     g, xs, times, refreshes, clk, density = res
-    total_ms = _shard.job_time_ms(sum(times), world, dev)  # max over ranks
+    total_ms = _shard.job_time_ms(sum(times), world, cdev)  # max over ranks
     value = _shard.aggregate_rate(args.steps, S, world, total_ms)
     steady = sorted(times)
     p50 = statistics.median(steady)
@@ -212,7 +221,7 @@ def run_ours(args):
         del g1
     # -- per-kernel timing of the conv GEMMs (dominant kernel) on the launching stream
     roof = conv_roofline(g, xs, args, evc)
-    e2e = measure_e2e(g, xs, args, S)
+    e2e = measure_e2e(g, xs, args, S, world, cdev)
     out = None
     if rank == 0:
         out = {
@@ -303,7 +312,7 @@ def _weights_of(g):
     return out
 
 
-def measure_e2e(g, xs, args, S):
+def measure_e2e(g, xs, args, S, world=1, dev=None):
     """Same metric through the public serving API with host buffers: every step uploads
     its new encodings from pinned memory, runs step_from_encodings (+refresh) and
     downloads its integrated output (serving.StreamPipeline overlaps those copies with
@@ -320,10 +329,15 @@ def measure_e2e(g, xs, args, S):
     pipe = StreamPipeline(g)
     g.dense_pass(xs[0] if S > 1 else xs[0][0])
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     t0 = time.perf_counter()
     pipe.run(host, out_host, dense_first=False)
     wall = time.perf_counter() - t0
-    return {"value": n * S / wall, "unit": UNIT, "h2d_bytes_per_step": int(host[0].numel() * 4),
+    wall = _shard.job_time_ms(wall * 1e3, world, dev) / 1e3  # slowest rank (every rank ran n steps)
+    return {"value": n * S * world / wall, "unit": UNIT, "h2d_bytes_per_step": int(host[0].numel() * 4),
             "d2h_bytes_per_step": int(out_host[0].numel() * 4), "ms_per_step": wall / n * 1e3,
             "copies": "H2D / D2H on a copy stream, overlapped with the neighbouring steps' compute"}
 

@@ -1563,7 +1563,10 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
   }
   L = fz::layout_of(g, cfg);
   const int64_t ctas = regions * ((g->c_out + bn - 1) / bn);
-  int sp = ctas >= 148 ? 1 : (int)std::min<int64_t>(msp, (148 + ctas - 1) / ctas);
+  // split-K only for short grids: from ~2/3 of the SMs on, the extra partial traffic and the
+  // cluster reduce cost more than the idle SMs (res 128 CTAs: 79 vs 85 us, enc3 54 vs 59 us)
+  int sp = ctas >= 96 ? 1 : (int)std::min<int64_t>(msp, (148 + ctas - 1) / ctas);
+  if (const char* fs = std::getenv("EVC_FORCE_SPLITS")) sp = std::max(1, std::min(atoi(fs), 16));
   if (cfg->row == 2) sp = 1;  // the packed epilogue sums shifted rows of one CTA's accumulators
   cfg->splits = fz::split_count(L.nkb, sp);
   return EVC_OK;

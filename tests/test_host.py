@@ -239,5 +239,5 @@ def test_conv_launch_configuration_rules():
     for nid in ("res0a", "res0b", "res1a", "res1b", "dec0"):
         assert s32[nid][1] == 0 and s32[nid][2] == 128, (nid, s32[nid])
         assert s1[nid][1] == 1, (nid, s1[nid])
-    assert s32["enc3"][1:] == (0, 128, 2)  # short grid: cluster split-K
-    assert s32["res0a"][3] >= 2 and s1["res0a"][3] >= 2
+    assert s32["enc3"][1:] == (0, 128, 1) and s32["res0a"][3] == 1  # 128 CTAs: no split-K
+    assert s1["res0a"][3] >= 2 and s1["enc3"][3] >= 2  # short grids: cluster split-K

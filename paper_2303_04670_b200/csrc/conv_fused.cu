@@ -1541,6 +1541,7 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
     cfg->rw = fz::BM;
   } else {
     cfg->rw = g->Wo > 16 ? 32 : (g->Wo > 8 ? 16 : 8);
+    if (const char* fr = std::getenv("EVC_FORCE_RW")) cfg->rw = std::max(8, std::min(atoi(fr), 32));
     cfg->rh = fz::BM / cfg->rw;
   }
   // BN <= 128 with many streams: N = 256 (hi.[hi|lo]) + N = 128 (lo.hi) per K8 step and twice the

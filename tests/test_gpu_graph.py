@@ -263,3 +263,33 @@ def test_tp_positive_refresh_restores():
             assert g.drift(g.dense_oracle(xs[i])) <= 1e-4
     fr = g.flop_report()
     assert fr.performed < fr.dense_equiv
+
+
+def test_sessions_with_tp_match_single_sessions():
+    """t_p > 0: every session's k follows its own norm EMA (per-session partial sums), so a
+    batched graph must reproduce independent single-session graphs."""
+    spec = evc.build_plain_cnn(depth=3, channels=8, tp=0.02, in_shape=(2, 48, 60))
+    weights = evc.WeightManifest.random_tensors(spec, 2)
+    rng = np.random.default_rng(11)
+    S = 3
+    x0 = rng.standard_normal((S, 2, 48, 60)).astype(np.float32)
+    gb = evc.build(spec, weights, refresh_interval=0, sessions=S)
+    gs = [evc.build(spec, weights, refresh_interval=0) for _ in range(S)]
+    gb.dense_pass(T(x0))
+    for s in range(S):
+        gs[s].dense_pass(T(x0[s]))
+    prev = x0.copy()
+    for i in range(4):
+        cur = prev.copy()
+        m = rng.random(cur.shape) < 0.05
+        cur[m] += rng.standard_normal(int(m.sum())).astype(np.float32)
+        gb.step_from_encodings(T(prev), T(cur))
+        for s in range(S):
+            gs[s].incr_step(evc.step_increment(T(prev[s]), T(cur[s]), spec.tile))
+        prev = cur
+    for s in range(S):
+        e = max_err(np_(gb.integrated_output(session=s)), np_(gs[s].integrated_output()))
+        assert e <= 1e-4, (s, e)
+        fb, fa = gb.state_fingerprint(session=s), gs[s].state_fingerprint()
+        for k in (k for k in fa if k.endswith(".k") or k.endswith(".norm")):
+            assert np.allclose(np.asarray(fb[k], np.float64), np.asarray(fa[k], np.float64), rtol=1e-5, atol=1e-6), k

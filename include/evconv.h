@@ -153,10 +153,11 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
 
 /* Channels-innermost hi/lo shadow of a conv input (hwc.cu).  The buffer holds
  * (H + 2 pad) x (W + 2 pad) pixels of 2*cp floats (cp = evc_hwc_channels(C_in)):
- * the TF32 heads of the channels, then their tails; the border stays zero (the
- * conv's padding).  Producers get y = the interior origin (pixel (0, 0)) and
- * pitch = W + 2 pad: element (s, y, x, c) head at y[s*stride + (y*pitch + x)*2cp + c],
- * tail at + cp. */
+ * TF32 heads and tails; the border stays zero (the conv's padding).  Producers get
+ * y = the interior origin (pixel (0, 0)) and pitch = W + 2 pad; pixel (s, y, x) starts at
+ * y[s*stride + (y*pitch + x)*2cp].  Within a pixel, for cp a multiple of 32 (TMA path):
+ * 32-channel chunks [32 heads | 32 tails], channel c's head at (c/32)*64 + c%32 and its
+ * tail 32 floats later; otherwise (CUDA-core path) heads at c, tails at cp + c. */
 int32_t evc_hwc_channels(int32_t c);
 int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp,
                int32_t pitch, int32_t S, void* stream);

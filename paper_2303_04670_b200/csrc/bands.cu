@@ -298,10 +298,10 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     }
     if (stage && (int)(threadIdx.x & 31) < nc) {  // lane = channel: 128-byte runs of heads and tails per pixel
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * p.hp * 2 * p.cp + c0 + lane;
+      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * p.hp * 2 * p.cp;
       for (int r = 0; r < nrow; ++r)
         for (int xl = warp; xl < ncol; xl += TB_THREADS / 32)
-          hwc_store(dst + ((int64_t)r * p.hp + x0 + xl) * 2 * p.cp, p.cp, 0, s_y[(r * 32 + xl) * 33 + lane]);
+          hwc_store(dst + ((int64_t)r * p.hp + x0 + xl) * 2 * p.cp, p.cp, c0 + lane, s_y[(r * 32 + xl) * 33 + lane]);
     }
   }
   if (OP == OP_SPARSIFY) {

@@ -171,10 +171,19 @@ __device__ __forceinline__ int fdiv(int a, const FDiv& f) { return __float2int_r
 __device__ __forceinline__ float tf32_head(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// Shadow pixel layout: with cp a multiple of 32 (the TMA path), 32-channel chunks of
+// [32 heads | 32 tails] -- a channel's tail sits 128 bytes after its head (one base register,
+// immediate offsets) and a TMA box of heads (or tails) is 32 consecutive floats; otherwise
+// (the CUDA-core path's cp = 4-aligned C) one chunk [cp heads | cp tails].
+__device__ __forceinline__ int hwc_head(int cp, int c) {
+  return (cp & 31) == 0 ? ((c >> 5) << 6) + (c & 31) : c;
+}
+__device__ __forceinline__ int hwc_unit(int cp) { return (cp & 31) == 0 ? 32 : cp; }
 __device__ __forceinline__ void hwc_store(float* pix, int cp, int c, float x) {
   const float h = tf32_head(x);
-  pix[c] = h;
-  pix[cp + c] = __fsub_rn(x, h);
+  const int o = hwc_head(cp, c);
+  pix[o] = h;
+  pix[o + hwc_unit(cp)] = __fsub_rn(x, h);
 }
 
 // Activation f of inc_activation (tensors.py:285-312), float32 ops with the

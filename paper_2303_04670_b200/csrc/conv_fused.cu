@@ -350,8 +350,9 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
         const float4 h = make_float4(tf32_head(o[j]), tf32_head(o[j + 1]), tf32_head(o[j + 2]), tf32_head(o[j + 3]));
         const float4 l = make_float4(__fsub_rn(o[j], h.x), __fsub_rn(o[j + 1], h.y), __fsub_rn(o[j + 2], h.z),
                                      __fsub_rn(o[j + 3], h.w));
-        *reinterpret_cast<float4*>(sh + n0 + j) = h;
-        *reinterpret_cast<float4*>(sh + a.sp_cp + n0 + j) = l;
+        float* hp = sh + hwc_head(a.sp_cp, n0 + j);  // 4 channels never straddle a 32-chunk
+        *reinterpret_cast<float4*>(hp) = h;
+        *reinterpret_cast<float4*>(hp + hwc_unit(a.sp_cp)) = l;
       }
     }
   } else {
@@ -565,14 +566,14 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         if (a.row) {  // kernel row r of the flattened padded shadow: 128 + kw - 1 pixel rows
           const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
           const int i0 = rr * a.VM + r * a.P;
-          tma_load_3d(abuf, &tmap, c0, i0, s, tma_bar(st));
-          tma_load_3d(abuf + A_HALF, &tmap, a.cp + c0, i0, s, tma_bar(st));
+          tma_load_3d(abuf, &tmap, 2 * c0, i0, s, tma_bar(st));  // chunk = [32 heads | 32 tails]
+          tma_load_3d(abuf + A_HALF, &tmap, 2 * c0 + 32, i0, s, tma_bar(st));
         } else {  // one box = the whole RH x RW region for this tap (padded coordinates)
           const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
           const int r = tap / a.kw, qq = tap % a.kw;
           const int xs = xlo * a.stride + qq, ys = ulo * a.stride + r;
-          tma_load_4d(abuf, &tmap, c0, xs, ys, s, tma_bar(st));
-          tma_load_4d(abuf + A_HALF, &tmap, a.cp + c0, xs, ys, s, tma_bar(st));
+          tma_load_4d(abuf, &tmap, 2 * c0, xs, ys, s, tma_bar(st));
+          tma_load_4d(abuf + A_HALF, &tmap, 2 * c0 + 32, xs, ys, s, tma_bar(st));
         }
         if (i == 0) TR(3);
       }
@@ -946,14 +947,14 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
           if (a.row) {
             const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
             const int i0 = rr * a.VM + r * a.P;
-            tma_load_3d(abuf, &tmap, c0, i0, s, full_bar(st));
-            tma_load_3d(abuf + A_HALF, &tmap, a.cp + c0, i0, s, full_bar(st));
+            tma_load_3d(abuf, &tmap, 2 * c0, i0, s, full_bar(st));
+            tma_load_3d(abuf + A_HALF, &tmap, 2 * c0 + 32, i0, s, full_bar(st));
           } else {
             const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
             const int r = tap / a.kw, qq = tap % a.kw;
             const int xs = xlo * a.stride + qq, ys = ulo * a.stride + r;
-            tma_load_4d(abuf, &tmap, c0, xs, ys, s, full_bar(st));
-            tma_load_4d(abuf + A_HALF, &tmap, a.cp + c0, xs, ys, s, full_bar(st));
+            tma_load_4d(abuf, &tmap, 2 * c0, xs, ys, s, full_bar(st));
+            tma_load_4d(abuf + A_HALF, &tmap, 2 * c0 + 32, xs, ys, s, full_bar(st));
           }
         }
       } else {
@@ -1257,10 +1258,10 @@ __global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(
           int c = 0;
           if ((a.c_in & 3) == 0) {  // 8 channels per round: four 16-byte loads in flight
             for (; c + 8 <= a.c_in; c += 8) {
-              const float4 h0 = *reinterpret_cast<const float4*>(px + c);
-              const float4 h1 = *reinterpret_cast<const float4*>(px + c + 4);
-              const float4 l0 = *reinterpret_cast<const float4*>(px + a.cp + c);
-              const float4 l1 = *reinterpret_cast<const float4*>(px + a.cp + c + 4);
+              const float4 h0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c));
+              const float4 h1 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + 4);
+              const float4 l0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp));
+              const float4 l1 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp) + 4);
               const float xv[8] = {__fadd_rn(h0.x, l0.x), __fadd_rn(h0.y, l0.y), __fadd_rn(h0.z, l0.z),
                                    __fadd_rn(h0.w, l0.w), __fadd_rn(h1.x, l1.x), __fadd_rn(h1.y, l1.y),
                                    __fadd_rn(h1.z, l1.z), __fadd_rn(h1.w, l1.w)};
@@ -1270,15 +1271,16 @@ __global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(
           }
           if ((a.c_in & 3) == 0) {
             for (; c + 4 <= a.c_in; c += 4) {
-              const float4 h0 = *reinterpret_cast<const float4*>(px + c);
-              const float4 l0 = *reinterpret_cast<const float4*>(px + a.cp + c);
+              const float4 h0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c));
+              const float4 l0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp));
               thin_fma<CO>(acc, __fadd_rn(h0.x, l0.x), wt + c * CO);
               thin_fma<CO>(acc, __fadd_rn(h0.y, l0.y), wt + (c + 1) * CO);
               thin_fma<CO>(acc, __fadd_rn(h0.z, l0.z), wt + (c + 2) * CO);
               thin_fma<CO>(acc, __fadd_rn(h0.w, l0.w), wt + (c + 3) * CO);
             }
           }
-          for (; c < a.c_in; ++c) thin_fma<CO>(acc, __fadd_rn(px[c], px[a.cp + c]), wt + c * CO);  // head + tail
+          for (; c < a.c_in; ++c)  // head + tail
+            thin_fma<CO>(acc, __fadd_rn(px[hwc_head(a.cp, c)], px[hwc_head(a.cp, c) + hwc_unit(a.cp)]), wt + c * CO);
         }
     }
     constexpr int E = CO < 16 ? CO : 16;

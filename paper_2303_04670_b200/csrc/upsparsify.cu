@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       if (q < Q) {
         const float* rc = s_r + cl * RS;
         const int rstride = a.hp * 2 * a.cp;  // floats between shadow rows (< 2^31 per session)
-        float* sbase = a.hwc + (int64_t)s * a.hs + c0 + cl;
+        float* sbase = a.hwc + (int64_t)s * a.hs + hwc_head(a.cp, c0 + cl);
+        const int tl = hwc_unit(a.cp);  // tail offset (32 floats: an immediate)
         const int obase = r0 * rstride + x0 * 2 * a.cp;
         float ssf = 0.0f;
         for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q)
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
             const float ov = __fadd_rn(0.0f, up);
             const float h = tf32_head(ov);
             d[0] = h;
-            d[a.cp] = __fsub_rn(ov, h);
+            d[tl] = __fsub_rn(ov, h);
             ssf = __fmaf_rn(ov, ov, ssf);
             nz |= ov != 0.0f;
             p0 += a.XC;
@@ -289,10 +290,10 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       if (!a.fast) a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage && !fast && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
-      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * 2 * a.cp + c0 + lane;
+      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * 2 * a.cp;
       for (int r = 0; r < nrow; ++r)
         for (int xq = warp; xq < ncol; xq += US_THREADS / 32)
-          hwc_store(dst + ((int64_t)r * a.hp + x0 + xq) * 2 * a.cp, a.cp, 0, s_y[(r * 32 + xq) * 33 + lane]);
+          hwc_store(dst + ((int64_t)r * a.hp + x0 + xq) * 2 * a.cp, a.cp, c0 + lane, s_y[(r * 32 + xq) * 33 + lane]);
     }
   }
   ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
           const float* p1 = rc + ra * a.XC + (s_ci1[xq] - clo);
           const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
           float* d = sbase + obase + ra * rstride + xq * 2 * a.cp;
-          bool nz = false;
+          uint32_t nzb = 0;  // OR of the magnitude bits: nonzero iff some value != +-0
           for (int r = ra; r < rb; ++r) {
             // same float32 op order as upsample_at (rows first, then columns)
             const float up = a.mode == 0 ? p0[0] : __fadd_rn(__fmul_rn(p0[0], cw0), __fmul_rn(p1[0], cw1));
@@ -223,12 +223,12 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
             d[0] = h;
             d[tl] = __fsub_rn(ov, h);
             ssf = __fmaf_rn(ov, ov, ssf);
-            nz |= ov != 0.0f;
+            nzb |= __float_as_uint(ov) & 0x7fffffffu;
             p0 += a.XC;
             p1 += a.XC;
             d += rstride;
           }
-          if (nz) s_ny[ti] = 1;
+          if (nzb) s_ny[ti] = 1;
         }
         ss += (double)ssf;
       }

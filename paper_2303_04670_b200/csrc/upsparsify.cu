@@ -51,18 +51,19 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   __shared__ int s_ci0[32], s_ci1[32], s_ri0[US_MAXR], s_ri1[US_MAXR], s_tj[32], s_ro0[US_MAXR], s_ro1[US_MAXR];
   __shared__ float s_cw0[32], s_cw1[32], s_rw0[US_MAXR], s_rw1[US_MAXR];
   const TView& y = a.y;
-  const int jc = blockIdx.x % a.nJC, rest = blockIdx.x / a.nJC;
-  const int cg = rest % a.nCG, ib = rest / a.nCG, s = blockIdx.y;
+  const FDiv d_tw_y = fdiv_of(y.tw);
+  const int rest = fdiv(blockIdx.x, fdiv_of(a.nJC)), jc = blockIdx.x - rest * a.nJC;
+  const int ib = fdiv(rest, fdiv_of(a.nCG)), cg = rest - ib * a.nCG, s = blockIdx.y;
   const int c0 = cg * US_C, nc = min(US_C, y.C - c0);
   const int x0 = jc * a.CW, ncol = min(y.W, x0 + a.CW) - x0;
-  const int j0 = x0 / y.tw, nj = (ncol + y.tw - 1) / y.tw;
+  const int j0 = fdiv(x0, d_tw_y), nj = fdiv(ncol + y.tw - 1, d_tw_y);
   const int i0 = ib * a.RT, nti = min(y.GH - i0, a.RT);  // tile rows of this CTA
   const int r0 = i0 * y.th, nrow = min(y.H, r0 + nti * y.th) - r0;
   const int NT = nti * nj;  // tiles per channel: t = channel * NT + tile row * nj + tile column
   // 1) taps of this CTA's output columns / rows
   if (threadIdx.x < ncol) {
     const int v = x0 + threadIdx.x;
-    s_tj[threadIdx.x] = threadIdx.x / y.tw;
+    s_tj[threadIdx.x] = fdiv(threadIdx.x, d_tw_y);
     if (a.mode == 0) {
       s_ci0[threadIdx.x] = s_ci1[threadIdx.x] = v / a.f;
       s_cw0[threadIdx.x] = 1.0f;
@@ -95,8 +96,8 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   const int rlo = tap_i0(r0, a.x.H), nr = tap_i1(r0 + nrow - 1, a.x.H) - rlo + 1;
   const int clo = tap_i0(x0, a.x.W), ncl = tap_i1(x0 + ncol - 1, a.x.W) - clo + 1;
   const FDiv d_th = fdiv_of(a.x.th), d_tw = fdiv_of(a.x.tw), d_NT = fdiv_of(NT), d_nj = fdiv_of(nj);
-  const int alo = rlo / a.x.th, ahi = (rlo + nr - 1) / a.x.th;
-  const int blo0 = clo / a.x.tw, bhi0 = (clo + ncl - 1) / a.x.tw;
+  const int alo = fdiv(rlo, d_th), ahi = fdiv(rlo + nr - 1, d_th);
+  const int blo0 = fdiv(clo, d_tw), bhi0 = fdiv(clo + ncl - 1, d_tw);
   const int na_ = ahi - alo + 1, nb_ = bhi0 - blo0 + 1;
   const bool box_fits = na_ * nb_ <= US_MAXJ;
   // last step's output / residual flags and the input flags of the box (all channels):

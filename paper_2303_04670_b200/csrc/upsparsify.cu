@@ -91,8 +91,12 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
   }
   // the CTA's input box from the taps of its corner pixels (taps are monotone), computed by
   // every thread so the flag loads below need no barrier first
-  auto tap_i0 = [&](int u, int n) { return a.mode == 0 ? u / a.f : bilinear_tap(u, n, a.f).i0; };
-  auto tap_i1 = [&](int u, int n) { return a.mode == 0 ? u / a.f : bilinear_tap(u, n, a.f).i1; };
+  // (integer form of bilinear_tap's floor((o + 0.5) / f - 0.5), exact for f in {2, 4}:
+  // floor((2o + 1 - f) / 2f), with 2f a power of two and 2o + 1 - f >= -3)
+  const int fsh = a.f == 2 ? 2 : 3;
+  auto tap_fl = [&](int o) { const int q = 2 * o + 1 - a.f; return q >= 0 ? q >> fsh : -1; };
+  auto tap_i0 = [&](int u, int n) { return a.mode == 0 ? u >> (fsh - 1) : min(max(tap_fl(u), 0), n - 1); };
+  auto tap_i1 = [&](int u, int n) { return a.mode == 0 ? u >> (fsh - 1) : min(max(tap_fl(u) + 1, 0), n - 1); };
   const int rlo = tap_i0(r0, a.x.H), nr = tap_i1(r0 + nrow - 1, a.x.H) - rlo + 1;
   const int clo = tap_i0(x0, a.x.W), ncl = tap_i1(x0 + ncol - 1, a.x.W) - clo + 1;
   const FDiv d_th = fdiv_of(a.x.th), d_tw = fdiv_of(a.x.tw), d_NT = fdiv_of(NT), d_nj = fdiv_of(nj);

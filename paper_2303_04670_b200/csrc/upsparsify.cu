@@ -188,8 +188,14 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
           const float* xr1 = xc + s_ro1[r];
           const float rw0 = s_rw0[r], rw1 = s_rw1[r];
           float* rr_ = rc + r * a.XC;
-          for (int c = c0 + q; c < c1; c += Q)
-            rr_[c] = a.mode == 0 ? xr0[c] : __fadd_rn(__fmul_rn(xr0[c], rw0), __fmul_rn(xr1[c], rw1));
+          if (Q == 1) {  // full channel group: unit stride, unrolled
+#pragma unroll 4
+            for (int c = c0; c < c1; ++c)
+              rr_[c] = a.mode == 0 ? xr0[c] : __fadd_rn(__fmul_rn(xr0[c], rw0), __fmul_rn(xr1[c], rw1));
+          } else {
+            for (int c = c0 + q; c < c1; c += Q)
+              rr_[c] = a.mode == 0 ? xr0[c] : __fadd_rn(__fmul_rn(xr0[c], rw0), __fmul_rn(xr1[c], rw1));
+          }
         }
       }
       __syncthreads();

@@ -216,18 +216,23 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
           const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
           float* d = sbase + obase + ra * rstride + xq * 2 * a.cp;
           uint32_t nzb = 0;  // OR of the magnitude bits: nonzero iff some value != +-0
-          for (int r = ra; r < rb; ++r) {
-            // same float32 op order as upsample_at (rows first, then columns)
-            const float up = a.mode == 0 ? p0[0] : __fadd_rn(__fmul_rn(p0[0], cw0), __fmul_rn(p1[0], cw1));
+          // same float32 op order as upsample_at (rows first, then columns)
+          auto row = [&](int k) {
+            const float up = a.mode == 0 ? p0[k * a.XC]
+                                         : __fadd_rn(__fmul_rn(p0[k * a.XC], cw0), __fmul_rn(p1[k * a.XC], cw1));
             const float ov = __fadd_rn(0.0f, up);
             const float h = tf32_head(ov);
-            d[0] = h;
-            d[tl] = __fsub_rn(ov, h);
+            float* dk = d + (int64_t)k * rstride;
+            dk[0] = h;
+            dk[tl] = __fsub_rn(ov, h);
             ssf = __fmaf_rn(ov, ov, ssf);
             nzb |= __float_as_uint(ov) & 0x7fffffffu;
-            p0 += a.XC;
-            p1 += a.XC;
-            d += rstride;
+          };
+          if (rb - ra == 6) {  // the 6-row tiles of the reference default: fully unrolled
+#pragma unroll
+            for (int k = 0; k < 6; ++k) row(k);
+          } else {
+            for (int k = 0; k < rb - ra; ++k) row(k);
           }
           if (nzb) s_ny[ti] = 1;
         }

@@ -206,15 +206,18 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
         const int tl = hwc_unit(a.cp);  // tail offset (32 floats: an immediate)
         const int obase = r0 * rstride + x0 * 2 * a.cp;
         float ssf = 0.0f;
-        for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q)
+        for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q) {
+        // the column's taps once (before any s_ny store of this column)
+        const int tj = s_tj[xq], o0 = s_ci0[xq] - clo, o1 = s_ci1[xq] - clo;
+        const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
+        float* dcol = sbase + obase + xq * 2 * a.cp;
         for (int tr = 0; tr < nti; ++tr) {
-          const int ti = cl * NT + tr * nj + s_tj[xq];
+          const int ti = cl * NT + tr * nj + tj;
           if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
           const int ra = tr * y.th, rb = min(nrow, ra + y.th);
-          const float* p0 = rc + ra * a.XC + (s_ci0[xq] - clo);
-          const float* p1 = rc + ra * a.XC + (s_ci1[xq] - clo);
-          const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
-          float* d = sbase + obase + ra * rstride + xq * 2 * a.cp;
+          const float* p0 = rc + ra * a.XC + o0;
+          const float* p1 = rc + ra * a.XC + o1;
+          float* d = dcol + ra * rstride;
           uint32_t nzb = 0;  // OR of the magnitude bits: nonzero iff some value != +-0
           // same float32 op order as upsample_at (rows first, then columns)
           auto row = [&](int k) {
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
             for (int k = 0; k < rb - ra; ++k) row(k);
           }
           if (nzb) s_ny[ti] = 1;
+        }
         }
         ss += (double)ssf;
       }

@@ -550,6 +550,70 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
   }
   if (!a.dense && z == 0 && threadIdx.x == 0 && !s_flag[1]) a.rstate[rs_idx] = 1;
 
+  // non-packed epilogue over channels [cb, ce) of the block (TMEM lane quarter = warp % 4).
+  // With a wide block and no split-K, warps 0-3 -- idle once the mainloop is issued -- drain the
+  // upper half of the channels while warps 4-7 drain the lower half.
+  const bool wide = CAT && BN >= 64 && a.splits == 1 && !(PACK && a.row == 2);
+  auto drain = [&](int cb, int ce) {
+    const int m = 32 * (warp & 3) + lane;
+    int u, x;
+    site_of(a, rr, m, u, x);
+    const int n_main = nk < NA ? nk : NA;
+    const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    float* P = reinterpret_cast<float*>(smem);
+  #pragma unroll 1
+      for (int c0 = cb; c0 < ce; c0 += 16) {
+        float vals[16];
+        {  // corrections first (small terms), then the main products
+          uint32_t r[NA + 1][16];
+          const uint32_t cbase = CAT ? (uint32_t)(NA * 2 * BN) : (uint32_t)BN;
+          tmem_ld16_issue(trow + cbase + (uint32_t)c0, r[NA]);
+          if (CAT) {
+  #pragma unroll
+            for (int j = 0; j < NA; ++j) tmem_ld16_issue(trow + (uint32_t)(j * 2 * BN + BN + c0), r[j]);
+          }
+          tmem_wait_ld();
+  #pragma unroll
+          for (int j = 0; j <= NA; ++j)
+  #pragma unroll
+            for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));  // uses stay after the wait
+  #pragma unroll
+          for (int e = 0; e < 16; ++e) vals[e] = __uint_as_float(r[NA][e]);
+          if (CAT) {
+  #pragma unroll
+            for (int j = 0; j < NA; ++j)
+              if (j < n_main) {
+  #pragma unroll
+                for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], __uint_as_float(r[j][e]));
+              }
+          }
+        }
+        {
+          uint32_t r[NA][16];
+  #pragma unroll
+          for (int j = 0; j < NA; ++j) tmem_ld16_issue(trow + (uint32_t)(j * (CAT ? 2 * BN : BN) + c0), r[j]);
+          tmem_wait_ld();
+  #pragma unroll
+          for (int j = 0; j < NA; ++j)
+  #pragma unroll
+            for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
+  #pragma unroll
+          for (int j = 0; j < NA; ++j)
+            if (j < n_main) {
+  #pragma unroll
+              for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], __uint_as_float(r[j][e]));
+            }
+        }
+        if (a.splits == 1) {
+          const int n0 = nblk * BN + c0;
+          ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
+        } else {
+  #pragma unroll
+          for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
+        }
+      }
+  };
+
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ TMA producer
       for (int i = 0; i < nk; ++i) {
@@ -720,57 +784,12 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         ssq += emit<8>(a, s, u, x, n0, 1, min(8, a.c_out - n0), o);
       }
     } else
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float vals[16];
-      {  // corrections first (small terms), then the main products
-        uint32_t r[NA + 1][16];
-        const uint32_t cbase = CAT ? (uint32_t)(NA * 2 * BN) : (uint32_t)BN;
-        tmem_ld16_issue(trow + cbase + (uint32_t)c0, r[NA]);
-        if (CAT) {
-#pragma unroll
-          for (int j = 0; j < NA; ++j) tmem_ld16_issue(trow + (uint32_t)(j * 2 * BN + BN + c0), r[j]);
-        }
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j <= NA; ++j)
-#pragma unroll
-          for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));  // uses stay after the wait
-#pragma unroll
-        for (int e = 0; e < 16; ++e) vals[e] = __uint_as_float(r[NA][e]);
-        if (CAT) {
-#pragma unroll
-          for (int j = 0; j < NA; ++j)
-            if (j < n_main) {
-#pragma unroll
-              for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], __uint_as_float(r[j][e]));
-            }
-        }
-      }
-      {
-        uint32_t r[NA][16];
-#pragma unroll
-        for (int j = 0; j < NA; ++j) tmem_ld16_issue(trow + (uint32_t)(j * (CAT ? 2 * BN : BN) + c0), r[j]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < NA; ++j)
-#pragma unroll
-          for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
-#pragma unroll
-        for (int j = 0; j < NA; ++j)
-          if (j < n_main) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) vals[e] = __fadd_rn(vals[e], __uint_as_float(r[j][e]));
-          }
-      }
-      if (a.splits == 1) {
-        const int n0 = nblk * BN + c0;
-        ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
-      }
-    }
+      drain(0, wide ? BN / 2 : BN);
+  }
+  if (wide && warp < 4) {
+    bar_wait(acc_bar, 0);
+    fence_after();
+    drain(BN / 2, BN);
   }
   if (threadIdx.x == 128) TR(7);
   if (a.splits > 1) {

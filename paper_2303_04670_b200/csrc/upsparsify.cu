@@ -306,7 +306,18 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
           hwc_store(dst + ((int64_t)r * a.hp + x0 + xq) * 2 * a.cp, a.cp, c0 + lane, s_y[(r * 32 + xq) * 33 + lane]);
     }
   }
-  ss = block_sum<double>(ss, [](double v) { return warp_sum_d(v); });
+  {  // block sum: the t_p = 0 path's per-thread sums are fp32 already -> fp32 warp sums
+    __shared__ double s_wsum[US_THREADS / 32];
+    const double w = a.fast ? (double)warp_sum((float)ss) : warp_sum_d(ss);
+    if ((threadIdx.x & 31) == 0) s_wsum[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int k = 0; k < US_THREADS / 32; ++k) t += s_wsum[k];
+      ss = t;
+    }
+  }
   if (threadIdx.x == 0) {
     a.partials[(int64_t)s * a.pstride + blockIdx.x] = ss;
     if (blockIdx.x + gridDim.x < (unsigned)a.pstride) a.partials[(int64_t)s * a.pstride + blockIdx.x + gridDim.x] = 0.0;

@@ -360,6 +360,12 @@ int evc_sumsq_dense(const float* x, int64_t x_stride, int64_t n_per_session,
 int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y,
             int32_t S, void* stream);
 
+/* inc_add followed by inc_activation (increment_ops.py:226-229 then :232-238) in one pass,
+ * for an add whose only reader is the activation: s = a + b, y = f(acc + s) - f(acc),
+ * acc += s, y.flags = a.flags | b.flags -- the same float32 ops as the two calls. */
+int evc_add_act(const evc_tensor* a, const evc_tensor* b, float* acc, int64_t acc_stride,
+                const evc_tensor* y, int32_t kind, float alpha, int32_t S, void* stream);
+
 /* inc_mul (increment_ops.py:241-254): y = (acc_a+a)*b + acc_b*a. */
 int evc_mul(const evc_tensor* a, const evc_tensor* b, float* acc_a,
             float* acc_b, int64_t acc_stride, const evc_tensor* y, int32_t S,

@@ -69,7 +69,7 @@ __device__ __forceinline__ float act_fn(float x, int kind, float alpha) {
   }
 }
 
-enum { OP_ACT = 0, OP_SPARSIFY = 1, OP_ADD = 2, OP_MUL = 3, OP_INTEGRATE = 4, OP_COPY = 5, OP_FOLD = 6 };
+enum { OP_ACT = 0, OP_SPARSIFY = 1, OP_ADD = 2, OP_MUL = 3, OP_INTEGRATE = 4, OP_COPY = 5, OP_FOLD = 6, OP_ADD_ACT = 7 };
 
 struct TBArgs {
   TView a, b, y;    // inputs (b optional) and output
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     const int n = nc * nrow * nq;
     const FDiv d_nq = fdiv_of(nq), d_nrow = fdiv_of(nrow), d_tw = fdiv_of(g.tw);
     const int64_t sa = (int64_t)s * p.a.vs, sy = (int64_t)s * p.y.vs, sacc = (int64_t)s * p.as;
-    const int64_t sb = (OP == OP_ADD || OP == OP_MUL) ? (int64_t)s * p.b.vs : 0;
+    const int64_t sb = (OP == OP_ADD || OP == OP_MUL || OP == OP_ADD_ACT) ? (int64_t)s * p.b.vs : 0;
     for (int base = threadIdx.x; base < n; base += TB_THREADS * TB_UNROLL) {
       int64_t off[TB_UNROLL];
       int cl_[TB_UNROLL], r_[TB_UNROLL], xl_[TB_UNROLL];
@@ -196,8 +196,9 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         if (!pr) continue;
         off[u] = (int64_t)(c0 + cl) * HW + (int64_t)(r0 + r) * g.W + x0 + xl;
         va[u] = VT::ld(p.a.v + sa + off[u]);
-        if (OP == OP_ADD || OP == OP_MUL) vb[u] = VT::ld(p.b.v + sb + off[u]);
-        if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD) vc[u] = VT::ld(p.acc + sacc + off[u]);
+        if (OP == OP_ADD || OP == OP_MUL || OP == OP_ADD_ACT) vb[u] = VT::ld(p.b.v + sb + off[u]);
+        if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD || OP == OP_ADD_ACT)
+          vc[u] = VT::ld(p.acc + sacc + off[u]);
         if (OP == OP_SPARSIFY) {
           if (p.delta_zero) {
 #pragma unroll
@@ -223,7 +224,12 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
 #pragma unroll
         for (int k = 0; k < V; ++k) {
           const float a = VT::get(va[u], k);
-          if (OP == OP_ACT) {
+          if (OP == OP_ADD_ACT) {  // inc_add then inc_activation, the same float32 ops in order
+            const float sm = __fadd_rn(a, VT::get(vb[u], k));
+            const float a0 = VT::get(vc[u], k), a1 = __fadd_rn(a0, sm);
+            VT::set(out, k, __fsub_rn(act_fn(a1, p.kind, p.alpha), act_fn(a0, p.kind, p.alpha)));
+            VT::set(acc_new, k, a1);
+          } else if (OP == OP_ACT) {
             const float a0 = VT::get(vc[u], k), a1 = __fadd_rn(a0, a);
             VT::set(out, k, __fsub_rn(act_fn(a1, p.kind, p.alpha), act_fn(a0, p.kind, p.alpha)));
             VT::set(acc_new, k, a1);
@@ -268,7 +274,8 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
           VT::st(pb2, sbv);
           (void)acc2_new;
         }
-        if (OP == OP_ACT || OP == OP_ADD || OP == OP_MUL || OP == OP_COPY) VT::st(p.y.v + sy + off[u], out);
+        if (OP == OP_ACT || OP == OP_ADD || OP == OP_MUL || OP == OP_COPY || OP == OP_ADD_ACT)
+          VT::st(p.y.v + sy + off[u], out);
         if (OP == OP_SPARSIFY) {
           if (p.write_chw) VT::st(p.y.v + sy + off[u], out);
           if (p.hwc && !stage) {
@@ -279,7 +286,8 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
           }
           if (!p.delta_zero) VT::st(p.acc2 + sacc + off[u], acc_new);
         }
-        if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD) VT::st(p.acc + sacc + off[u], acc_new);
+        if (OP == OP_ACT || OP == OP_MUL || OP == OP_INTEGRATE || OP == OP_FOLD || OP == OP_ADD_ACT)
+          VT::st(p.acc + sacc + off[u], acc_new);
       }
     }
     __syncthreads();
@@ -292,7 +300,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
         p.y.f[(int64_t)s * p.y.fs + fo] = s_f1[t];
         p.dlive[(int64_t)s * g.C * g.GH * g.GW + fo] = s_f2[t];
         if (p.fany && s_f1[t]) p.fany[((int64_t)s * g.GH + i) * g.GW + j0 + jl] = 1;  // benign race: all store 1
-      } else if (OP == OP_ADD || OP == OP_MUL) {
+      } else if (OP == OP_ADD || OP == OP_MUL || OP == OP_ADD_ACT) {
         p.y.f[(int64_t)s * p.y.fs + fo] = p.a.f[(int64_t)s * p.a.fs + fo] | p.b.f[(int64_t)s * p.b.fs + fo];
       }
     }
@@ -450,6 +458,7 @@ static int tb_launch(int op, const TBArgs& p, int S, cudaStream_t st) {
     case OP_INTEGRATE: launch_op<OP_INTEGRATE>(p, g, S, st); break;
     case OP_COPY: launch_op<OP_COPY>(p, g, S, st); break;
     case OP_FOLD: launch_op<OP_FOLD>(p, g, S, st); break;
+    case OP_ADD_ACT: launch_op<OP_ADD_ACT>(p, g, S, st); break;
     default: return EVC_EINVAL;
   }
   return EVC_OK;
@@ -537,6 +546,23 @@ int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y, int32
   p.y = view_of(*y);
   const int rc = tb_launch(OP_ADD, p, S, as_stream(stream));
   EVC_LAUNCH_CHECK("add");
+  return rc;
+}
+
+int evc_add_act(const evc_tensor* a, const evc_tensor* b, float* acc, int64_t acc_stride, const evc_tensor* y,
+                int32_t kind, float alpha, int32_t S, void* stream) {
+  EVC_CHECK_ARG(a && b && y && acc && a->flags && b->flags && y->flags && S > 0 && kind >= 0 && kind <= 3,
+                "add_act: bad argument");
+  TBArgs p = {};
+  p.a = view_of(*a);
+  p.b = view_of(*b);
+  p.y = view_of(*y);
+  p.acc = acc;
+  p.as = acc_stride;
+  p.kind = kind;
+  p.alpha = alpha;
+  const int rc = tb_launch(OP_ADD_ACT, p, S, as_stream(stream));
+  EVC_LAUNCH_CHECK("add_act");
   return rc;
 }
 

@@ -533,6 +533,8 @@ class Graph:
             node.sp_fused_by = None  # sparsify evaluated in a producing conv's epilogue
             node.fused_sp = None
             node.act_values_needed = True
+            node.fused_add = None  # activation: the add it evaluates in the same pass
+            node.add_fused = False  # add: evaluated by its only reader, an activation
         for node in self.nodes:
             if node.kind != "concat":
                 continue
@@ -620,6 +622,16 @@ class Graph:
                 f = int(node.spec.attrs["out_features"])
                 lin_ws = max(lin_ws, int(self.lib.evc_linear_workspace(f, int(np.prod(ish)),
                                                                        self.tile.h * self.tile.w, S)))
+        # add -> activation, the add read by nothing else: one elementwise pass (evc_add_act)
+        for node in self.nodes:
+            if node.kind != "add" or node.spec.id in self.output_ids:
+                continue
+            cons = self._consumers[node.spec.id]
+            if len(cons) == 1 and self._by_id[cons[0]].kind in ACTIVATION_KINDS:
+                act = self._by_id[cons[0]]
+                if act.fused_into is None and act.spec.inputs == [node.spec.id]:
+                    act.fused_add = node
+                    node.add_fused = True
         # conv -> activation -> sparsify(t_p = 0) -> conv: the sparsify runs in the first conv's epilogue
         # (it writes the second conv's hi/lo shadow, the sparsify flags and any-channel map directly)
         for node in self.nodes:
@@ -820,6 +832,11 @@ class Graph:
                                             self._lin_ws.data_ptr(), S), "linear"))
             elif k in ACTIVATION_KINDS and node.fused_into is not None:
                 continue  # evaluated in the producing conv's epilogue
+            elif k in ACTIVATION_KINDS and node.fused_add is not None:
+                code, alpha = node.act
+                ad = node.fused_add.spec
+                prog.append((L.evc_add_act, (self._desc(ad.inputs[0]), self._desc(ad.inputs[1]), node.acc.data_ptr(),
+                                             node.acc[0].numel(), self._desc(nid), code, alpha, S), "add_act"))
             elif k in ACTIVATION_KINDS:
                 code, alpha = node.act
                 prog.append((L.evc_act_delta, (self._desc(ns.inputs[0]), node.acc.data_ptr(),
@@ -856,6 +873,8 @@ class Graph:
                                               1 if node.tp == 0.0 else 0,  # k stays 0 -> residual stays 0
                                               S),
                              "sparsify"))
+            elif k == "add" and node.add_fused:
+                continue  # evaluated with its activation (evc_add_act)
             elif k == "add":
                 prog.append((L.evc_add, (self._desc(ns.inputs[0]), self._desc(ns.inputs[1]), self._desc(nid), S),
                              "add"))

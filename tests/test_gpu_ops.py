@@ -220,3 +220,39 @@ def test_no_cpu_fallback_when_library_missing(monkeypatch, tmp_path):
     monkeypatch.setattr(_lib, "LIB_PATH", tmp_path / "missing.so")
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         evc.make_tile_mask(torch.zeros(1, 6, 6), evc.TileShape())
+
+
+@pytest.mark.parametrize("kind", ["relu", "leaky_relu", "tanh"])
+def test_add_act_equals_add_then_activation(kind):
+    """evc_add_act (graph fusion of an add read only by an activation) is bit-identical to
+    evc_add followed by evc_act_delta (increment_ops.py:226-238)."""
+    from paper_2303_04670_b200 import _lib
+    lib = _lib.lib()
+    rng = np.random.default_rng(5)
+    C, H, W = 24, 30, 36
+    gh, gw = 5, 6
+    fa, fb = rng.random((C, gh, gw)) < 0.3, rng.random((C, gh, gw)) < 0.3
+    a = (rng.standard_normal((C, H, W)) * O.flags_to_pixels(fa, 6, 6, H, W)).astype(np.float32)
+    b = (rng.standard_normal((C, H, W)) * O.flags_to_pixels(fb, 6, 6, H, W)).astype(np.float32)
+    acc0 = rng.standard_normal((C, H, W)).astype(np.float32)
+    code = _lib.ACT[kind]
+    ta, tb = T(a), T(b)
+    tfa, tfb = T(fa.astype(np.uint8)), T(fb.astype(np.uint8))
+
+    def desc(v, f):
+        return _lib.tdesc(v.data_ptr(), f.data_ptr(), 0, 0, C, H, W, 6, 6)
+
+    # unfused
+    s_v, s_f = torch.zeros_like(ta), torch.zeros_like(tfa)
+    y1, f1, acc1 = torch.zeros_like(ta), torch.zeros_like(tfa), T(acc0)
+    assert lib.evc_add(desc(ta, tfa), desc(tb, tfb), desc(s_v, s_f), 1, _lib.stream_ptr()) == 0
+    assert lib.evc_act_delta(desc(s_v, s_f), acc1.data_ptr(), acc1.numel(), desc(y1, f1), code, 0.01, 1,
+                             _lib.stream_ptr()) == 0
+    # fused
+    y2, f2, acc2 = torch.zeros_like(ta), torch.zeros_like(tfa), T(acc0)
+    assert lib.evc_add_act(desc(ta, tfa), desc(tb, tfb), acc2.data_ptr(), acc2.numel(), desc(y2, f2), code, 0.01, 1,
+                           _lib.stream_ptr()) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(np_(y1).view(np.uint32), np_(y2).view(np.uint32))
+    assert np.array_equal(np_(acc1).view(np.uint32), np_(acc2).view(np.uint32))
+    assert np.array_equal(np_(f1), np_(f2)) and np.array_equal(np_(f2).astype(bool), fa | fb)

@@ -1587,7 +1587,10 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
   const int64_t ctas = regions * ((g->c_out + bn - 1) / bn);
   // split-K only for short grids: from ~2/3 of the SMs on, the extra partial traffic and the
   // cluster reduce cost more than the idle SMs (res 128 CTAs: 79 vs 85 us, enc3 54 vs 59 us)
-  int sp = ctas >= 96 ? 1 : (int)std::min<int64_t>(msp, (148 + ctas - 1) / ctas);
+  // short grids: about 96 CTAs in one wave (more ranks cost more in the cluster reduce than
+  // they win; measured at one stream: dec0 / dec1 best at 4-5 ranks, res / enc3 at 8)
+  int sp = ctas >= 96 ? 1
+                      : (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)msp, (96 + ctas / 2) / ctas, 148 / ctas}));
   if (const char* fs = std::getenv("EVC_FORCE_SPLITS")) sp = std::max(1, std::min(atoi(fs), 16));
   if (cfg->row == 2) sp = 1;  // the packed epilogue sums shifted rows of one CTA's accumulators
   cfg->splits = fz::split_count(L.nkb, sp);

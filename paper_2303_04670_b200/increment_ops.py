@@ -135,7 +135,7 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     tile = x.tile
     meter.add(0, 2 * kh * kw * c_in * c_out * ho * wo)
     lib = _lib.lib()
-    plan = tensors.ConvPlan(weight, st, pad, h, w, tile.h, tile.w)
+    plan = tensors.cached_plan(weight, st, pad, h, w, tile.h, tile.w)
     yv, yf = _zeros_incr((c_out, ho, wo), tile, dev)
     s = _lib.stream_ptr()
     din = x.desc()

@@ -259,6 +259,25 @@ def pack_conv_weight(weight: torch.Tensor):
     return torch.from_numpy(out).to(weight.device)
 
 
+_PLANS: dict = {}
+
+
+def cached_plan(weight: torch.Tensor, stride, pad, h, w, th, tw) -> "ConvPlan":
+    """ConvPlan for the stateless op API (inc_conv2d / dense_conv2d), cached per weight tensor
+    and geometry: the weight packing, tables and shadow buffer are built once, not per call.
+    The key holds the tensor's data pointer and version counter, so an in-place update of the
+    weights (or a new tensor) gets a fresh plan; the dense kernel kind is part of the key."""
+    key = (weight.data_ptr(), weight._version, tuple(weight.shape), str(weight.device), int(stride), int(pad),
+           int(h), int(w), int(th), int(tw), CONV_KERNEL)
+    plan = _PLANS.get(key)
+    if plan is None:
+        if len(_PLANS) >= 8:  # each plan holds its shadow buffer
+            _PLANS.clear()
+        plan = ConvPlan(weight, stride, pad, h, w, th, tw)
+        _PLANS[key] = plan
+    return plan
+
+
 class ConvPlan:
     """Static launch plan of one conv layer: geometry table, kernel path, packed weights, K-splits.
 
@@ -373,7 +392,7 @@ def dense_conv2d(x, weight, bias=None, stride: int = 1, padding: int = 0) -> tor
         raise ValueError(f"input has {c} channels but weight expects {c_in}")
     ho, wo = conv_output_hw(h, w, kh, kw, stride, padding)
     th, tw = (4, 32) if wo >= 32 else (8, max(1, wo))
-    plan = ConvPlan(weight, stride, padding, h, w, th, tw)
+    plan = cached_plan(weight, stride, padding, h, w, th, tw)
     y = torch.empty((c_out, ho, wo), dtype=torch.float32, device=x.device)
     b = None if bias is None else as_bias(bias, c_out, x.device)
     din = _lib.tdesc(_lib.ptr(x), None, c * h * w, 0, c, h, w, th, tw)

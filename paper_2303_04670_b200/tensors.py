@@ -245,7 +245,7 @@ def conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw):
     return g, tab
 
 
-CONV_KERNEL = os.environ.get("EVC_CONV_KERNEL", "tc")  # "tc" (tcgen05 3xTF32) or "simt" (FFMA)
+CONV_KERNEL = os.environ.get("EVC_CONV_KERNEL", "tc")  # "tc" (tcgen05 3xTF32), "tile" (gathered tiles only), "simt"
 
 
 def pack_conv_weight(weight: torch.Tensor):
@@ -262,18 +262,19 @@ def pack_conv_weight(weight: torch.Tensor):
 _PLANS: dict = {}
 
 
-def cached_plan(weight: torch.Tensor, stride, pad, h, w, th, tw) -> "ConvPlan":
+def cached_plan(weight: torch.Tensor, stride, pad, h, w, th, tw, kernel: str | None = None) -> "ConvPlan":
     """ConvPlan for the stateless op API (inc_conv2d / dense_conv2d), cached per weight tensor
     and geometry: the weight packing, tables and shadow buffer are built once, not per call.
     The key holds the tensor's data pointer and version counter, so an in-place update of the
     weights (or a new tensor) gets a fresh plan; the dense kernel kind is part of the key."""
+    kernel = kernel or CONV_KERNEL
     key = (weight.data_ptr(), weight._version, tuple(weight.shape), str(weight.device), int(stride), int(pad),
-           int(h), int(w), int(th), int(tw), CONV_KERNEL)
+           int(h), int(w), int(th), int(tw), kernel)
     plan = _PLANS.get(key)
     if plan is None:
         if len(_PLANS) >= 8:  # each plan holds its shadow buffer
             _PLANS.clear()
-        plan = ConvPlan(weight, stride, pad, h, w, th, tw)
+        plan = ConvPlan(weight, stride, pad, h, w, th, tw, kernel=kernel)
         _PLANS[key] = plan
     return plan
 
@@ -323,7 +324,7 @@ class ConvPlan:
             self.ws_floats = 0
             self.ctas = int(lib.evc_conv_fused_ctas(self.g, self.cfg))  # per session (meter partials)
         else:
-            self.path = "tile" if kernel == "tc" else "simt"
+            self.path = "tile" if kernel in ("tc", "tile") else "simt"
             if self.path == "tile":
                 self.wpack = pack_conv_weight(weight)
             self.splits = choose_splits(S * T * th * tw, c_out, c_in * kh * kw, kernel=kernel)
@@ -366,7 +367,7 @@ class ConvPlan:
 
 def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148, kernel: str | None = None) -> int:
     """K-splits so the worst-case grid still fills the B200 (148 SMs)."""
-    if (kernel or CONV_KERNEL) == "tc":
+    if (kernel or CONV_KERNEL) in ("tc", "tile"):
         ctas = max(1, -(-max_sites // 128)) * max(1, -(-c_out // 256))
         if ctas >= 148:
             return 1

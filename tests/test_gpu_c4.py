@@ -52,7 +52,7 @@ def _torch_conv(vals, wt):
     return y.cpu().numpy()
 
 
-@pytest.mark.parametrize("d,clustered", [(0.02, True), (0.2, True), (0.01, False)])
+@pytest.mark.parametrize("d,clustered", [(0.005, True), (0.02, True), (0.2, True), (0.01, False)])
 def test_c4_full_size_vs_meter_oracle_and_fp32(d, clustered):
     vals, flags = _case(d, clustered, 3)
     wt = _weights()

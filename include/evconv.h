@@ -157,7 +157,10 @@ int evc_conv_mask(const evc_conv_geom* g, const evc_tensor* in,
  * y = the interior origin (pixel (0, 0)) and pitch = W + 2 pad; pixel (s, y, x) starts at
  * y[s*stride + (y*pitch + x)*2cp].  Within a pixel, for cp a multiple of 32 (TMA path):
  * 32-channel chunks [32 heads | 32 tails], channel c's head at (c/32)*64 + c%32 and its
- * tail 32 floats later; otherwise (CUDA-core path) heads at c, tails at cp + c. */
+ * tail 32 floats later; otherwise (CUDA-core path) heads at c, tails at cp + c.
+ * A negative cp selects the fp32 shadow of -cp channels read only by the CUDA-core (thin)
+ * conv: -cp floats per pixel, channel c's value at c (half the bytes; every producer taking
+ * cp -- to_hwc, sparsify, up_sparsify, the fused conv sparsify -- writes either layout). */
 int32_t evc_hwc_channels(int32_t c);
 int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp,
                int32_t pitch, int32_t S, void* stream);

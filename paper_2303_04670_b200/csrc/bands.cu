@@ -18,6 +18,8 @@
 
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace evc {
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
           if (p.hwc && !stage) {
 #pragma unroll
             for (int k = 0; k < V; ++k)
-              hwc_store(p.hwc + (int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * p.hp + x0 + xl_[u] + k) * 2 * p.cp, p.cp,
+              hwc_store(p.hwc + (int64_t)s * p.hs + ((int64_t)(r0 + r_[u]) * p.hp + x0 + xl_[u] + k) * hwc_px(p.cp), p.cp,
                         c0 + cl_[u], VT::get(out, k));
           }
           if (!p.delta_zero) VT::st(p.acc2 + sacc + off[u], acc_new);
@@ -306,10 +308,10 @@ __global__ void __launch_bounds__(TB_THREADS) k_tiles(TBArgs p, TBGeo g) {
     }
     if (stage && (int)(threadIdx.x & 31) < nc) {  // lane = channel: 128-byte runs of heads and tails per pixel
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * p.hp * 2 * p.cp;
+      float* dst = p.hwc + (int64_t)s * p.hs + (int64_t)r0 * p.hp * hwc_px(p.cp);
       for (int r = 0; r < nrow; ++r)
         for (int xl = warp; xl < ncol; xl += TB_THREADS / 32)
-          hwc_store(dst + ((int64_t)r * p.hp + x0 + xl) * 2 * p.cp, p.cp, c0 + lane, s_y[(r * 32 + xl) * 33 + lane]);
+          hwc_store(dst + ((int64_t)r * p.hp + x0 + xl) * hwc_px(p.cp), p.cp, c0 + lane, s_y[(r * 32 + xl) * 33 + lane]);
     }
   }
   if (OP == OP_SPARSIFY) {
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(256) k_sparsify_small(TBArgs p) {
   __syncthreads();
   const int span = SM_TJ * a.tw, rows = ni * a.th;  // th, tw <= 6 (checked on host)
   const int64_t HW = (int64_t)a.H * a.W;
-  const bool vec4 = a.C == 4 && p.cp == 4;  // 16-byte runs of heads and of tails per pixel
+  const bool vec4 = a.C == 4 && (p.cp == 4 || p.cp == -4);  // 16-byte runs of heads and of tails per pixel
   float ss = 0.0f;
   for (int t = threadIdx.x; t < rows * span; t += blockDim.x) {
     const int r = t / span, xq = t - r * span;
@@ -396,8 +398,10 @@ __global__ void __launch_bounds__(256) k_sparsify_small(TBArgs p) {
     for (int c = 0; c < 8; ++c)
       if (c < a.C) v[c] = __fadd_rn(0.0f, src[c * HW]);
     uint8_t* f = s_f + (r / a.th) * 8 * SM_TJ + xq / a.tw;
-    float* sh = p.hwc ? p.hwc + (int64_t)s * p.hs + ((int64_t)u * p.hp + x) * 2 * p.cp : nullptr;
-    if (sh && vec4) {
+    float* sh = p.hwc ? p.hwc + (int64_t)s * p.hs + ((int64_t)u * p.hp + x) * hwc_px(p.cp) : nullptr;
+    if (sh && vec4 && p.cp < 0) {
+      *reinterpret_cast<float4*>(sh) = make_float4(v[0], v[1], v[2], v[3]);
+    } else if (sh && vec4) {
       const float4 h = make_float4(tf32_head(v[0]), tf32_head(v[1]), tf32_head(v[2]), tf32_head(v[3]));
       *reinterpret_cast<float4*>(sh) = h;
       *reinterpret_cast<float4*>(sh + 4) =
@@ -506,7 +510,7 @@ int evc_sparsify(const evc_tensor* dx, float* delta, int64_t ds, uint8_t* dlive,
   EVC_CHECK_ARG(dx && y && delta && dlive && k && norm_ema && partials && dx->flags && y->flags && S > 0,
                 "sparsify: null argument");
   EVC_CHECK_ARG(write_chw || hwc, "sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || (cp >= dx->C && cp % 4 == 0 && hwc_pitch >= dx->W),
+  EVC_CHECK_ARG(!hwc || (std::abs(cp) >= dx->C && cp % 4 == 0 && hwc_pitch >= dx->W),
                 "sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   TBArgs p = {};
   p.a = view_of(*dx);

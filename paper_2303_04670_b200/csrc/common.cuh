@@ -175,11 +175,18 @@ __device__ __forceinline__ float tf32_head(float x) {
 // [32 heads | 32 tails] -- a channel's tail sits 128 bytes after its head (one base register,
 // immediate offsets) and a TMA box of heads (or tails) is 32 consecutive floats; otherwise
 // (the CUDA-core path's cp = 4-aligned C) one chunk [cp heads | cp tails].
+// cp < 0 selects an fp32 shadow of -cp channels, [values] per pixel: the CUDA-core thin
+// conv reads the value itself (head + tail rebuilt it exactly), so it needs half the bytes.
+__host__ __device__ __forceinline__ int hwc_px(int cp) { return cp < 0 ? -cp : 2 * cp; }
 __device__ __forceinline__ int hwc_head(int cp, int c) {
-  return (cp & 31) == 0 ? ((c >> 5) << 6) + (c & 31) : c;
+  return cp > 0 && (cp & 31) == 0 ? ((c >> 5) << 6) + (c & 31) : c;
 }
 __device__ __forceinline__ int hwc_unit(int cp) { return (cp & 31) == 0 ? 32 : cp; }
 __device__ __forceinline__ void hwc_store(float* pix, int cp, int c, float x) {
+  if (cp < 0) {
+    pix[c] = x;
+    return;
+  }
   const float h = tf32_head(x);
   const int o = hwc_head(cp, c);
   pix[o] = h;

@@ -336,7 +336,7 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   const int tile = valid ? (u / a.th) * a.sp_GW + x / a.tw : -1;
   const unsigned grp = __match_any_sync(0xffffffffu, tile);
   const bool leader = valid && (__ffs(grp) - 1) == lane;
-  float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp;
+  float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp);
   const int64_t To = (int64_t)a.sp_GH * a.sp_GW;
   uint8_t* fl = a.sp_flags + (int64_t)s * a.sp_fs + tile;
   bool any = false;
@@ -344,7 +344,11 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
 #pragma unroll
   for (int j = 0; j < N; ++j) o[j] = __fadd_rn(0.0f, y[j]);
   if (N % 4 == 0 && step == 1 && cnt == N && (n0 & 3) == 0 && (a.sp_cp & 3) == 0) {
-    if (valid) {  // 16-byte runs of heads and tails
+    if (valid && a.sp_cp < 0) {  // fp32 shadow: 16-byte runs of values
+#pragma unroll
+      for (int j = 0; j < N; j += 4)
+        *reinterpret_cast<float4*>(sh + n0 + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    } else if (valid) {  // 16-byte runs of heads and tails
 #pragma unroll
       for (int j = 0; j < N; j += 4) {
         const float4 h = make_float4(tf32_head(o[j]), tf32_head(o[j + 1]), tf32_head(o[j + 2]), tf32_head(o[j + 3]));
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
         if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
         if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
-        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
+        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp), a.sp_cp, n, 0.0f);
       }
       if (threadIdx.x == 0) a.rstate[rs_idx] = 0;
     }
@@ -1061,7 +1065,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
               if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
               if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
               if (a.sp_hwc)
-                hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n,
+                hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp), a.sp_cp, n,
                           0.0f);
             }
         }
@@ -1212,7 +1216,8 @@ __device__ __forceinline__ void thin_fma(float* acc, float x, const float* w) {
   }
 }
 
-template <int CO>  // output channels padded to CO (2, 4, 8, 16, 32); weights [tap][c_in][CO]
+// output channels padded to CO (2, 4, 8, 16, 32); weights [tap][c_in][CO]; F32: fp32 shadow (cp < 0)
+template <int CO, bool F32 = false>
 __global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
                                                             const __grid_constant__ Args a) {
   extern __shared__ float s_w[];
@@ -1259,7 +1264,7 @@ __global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(
         const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
         if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
         if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
-        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * 2 * a.sp_cp, a.sp_cp, n, 0.0f);
+        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp), a.sp_cp, n, 0.0f);
       }
       if (threadIdx.x == 0) a.rstate[reg] = 0;
     }
@@ -1270,36 +1275,37 @@ __global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(
     for (int n = 0; n < CO; ++n) acc[n] = 0.0f;
     if (valid) {
       const float* base = in_hwc + (int64_t)s * hwc_stride;
+      constexpr bool f32 = F32;
       for (int r = 0; r < a.kh; ++r)
         for (int q2 = 0; q2 < a.kw; ++q2) {
-          const float* px = base + ((int64_t)(u * a.stride + r) * a.P + x * a.stride + q2) * 2 * a.cp;
+          const float* px = base + ((int64_t)(u * a.stride + r) * a.P + x * a.stride + q2) * hwc_px(a.cp);
           const float* wt = s_w + (r * a.kw + q2) * a.c_in * CO;
+          // four channel values at c (16 bytes of an fp32 shadow, or head + tail runs)
+          auto ld4 = [&](int c) -> float4 {
+            if (f32) return *reinterpret_cast<const float4*>(px + c);
+            const float4 h = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c));
+            const float4 l = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp));
+            return make_float4(__fadd_rn(h.x, l.x), __fadd_rn(h.y, l.y), __fadd_rn(h.z, l.z), __fadd_rn(h.w, l.w));
+          };
           int c = 0;
-          if ((a.c_in & 3) == 0) {  // 8 channels per round: four 16-byte loads in flight
+          if ((a.c_in & 3) == 0) {  // 8 channels per round: 16-byte loads in flight
             for (; c + 8 <= a.c_in; c += 8) {
-              const float4 h0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c));
-              const float4 h1 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + 4);
-              const float4 l0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp));
-              const float4 l1 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp) + 4);
-              const float xv[8] = {__fadd_rn(h0.x, l0.x), __fadd_rn(h0.y, l0.y), __fadd_rn(h0.z, l0.z),
-                                   __fadd_rn(h0.w, l0.w), __fadd_rn(h1.x, l1.x), __fadd_rn(h1.y, l1.y),
-                                   __fadd_rn(h1.z, l1.z), __fadd_rn(h1.w, l1.w)};
+              const float4 v0 = ld4(c), v1 = ld4(c + 4);
+              const float xv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
               for (int k = 0; k < 8; ++k) thin_fma<CO>(acc, xv[k], wt + (c + k) * CO);
             }
-          }
-          if ((a.c_in & 3) == 0) {
             for (; c + 4 <= a.c_in; c += 4) {
-              const float4 h0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c));
-              const float4 l0 = *reinterpret_cast<const float4*>(px + hwc_head(a.cp, c) + hwc_unit(a.cp));
-              thin_fma<CO>(acc, __fadd_rn(h0.x, l0.x), wt + c * CO);
-              thin_fma<CO>(acc, __fadd_rn(h0.y, l0.y), wt + (c + 1) * CO);
-              thin_fma<CO>(acc, __fadd_rn(h0.z, l0.z), wt + (c + 2) * CO);
-              thin_fma<CO>(acc, __fadd_rn(h0.w, l0.w), wt + (c + 3) * CO);
+              const float4 v0 = ld4(c);
+              thin_fma<CO>(acc, v0.x, wt + c * CO);
+              thin_fma<CO>(acc, v0.y, wt + (c + 1) * CO);
+              thin_fma<CO>(acc, v0.z, wt + (c + 2) * CO);
+              thin_fma<CO>(acc, v0.w, wt + (c + 3) * CO);
             }
           }
           for (; c < a.c_in; ++c)  // head + tail
-            thin_fma<CO>(acc, __fadd_rn(px[hwc_head(a.cp, c)], px[hwc_head(a.cp, c) + hwc_unit(a.cp)]), wt + c * CO);
+            thin_fma<CO>(acc, f32 ? px[c] : __fadd_rn(px[hwc_head(a.cp, c)], px[hwc_head(a.cp, c) + hwc_unit(a.cp)]),
+                         wt + c * CO);
         }
     }
     constexpr int E = CO < 16 ? CO : 16;
@@ -1677,11 +1683,13 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                 "conv_fused: bad region shape");
   EVC_CHECK_ARG(cfg->splits >= 1 && cfg->splits <= 16, "conv_fused: splits must lie in [1, 16]");
   const int Hp = g->H + 2 * g->pad, Wp = g->W + 2 * g->pad;
-  EVC_CHECK_ARG(cp % (cfg->thin ? 4 : 32) == 0 && cp >= g->c_in && hwc_stride % 4 == 0 && hwc_stride >= (int64_t)Hp * Wp * 2 * cp,
-                "conv_fused: shadow layout (cp % 32, thin path % 4; (H + 2 pad) x (W + 2 pad) pixels per session)");
+  const int acp = cp < 0 ? -cp : cp;  // cp < 0: fp32 shadow, CUDA-core path only
+  EVC_CHECK_ARG((cp > 0 || cfg->thin) && acp % (cfg->thin ? 4 : 32) == 0 && acp >= g->c_in && hwc_stride % 4 == 0 &&
+                    hwc_stride >= (int64_t)Hp * Wp * hwc_px(cp),
+                "conv_fused: shadow layout (cp % 32, thin path +-cp % 4; (H + 2 pad) x (W + 2 pad) pixels per session)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
-  EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 4 == 0 && sp->cp >= g->c_out && sp->hwc_stride % 4 == 0 &&
+  EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 4 == 0 && std::abs(sp->cp) >= g->c_out && sp->hwc_stride % 4 == 0 &&
                         sp->pitch >= g->Wo && sp->flags && sp->fany && sp->partials),
                 "conv_fused: fused sparsify needs the shadow, flags, fany and partials (incremental mode)");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && meter_part &&
@@ -1789,12 +1797,13 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
     EVC_CHECK_ARG(g->c_out <= 32 && L.stage <= 48 * 1024, "conv_fused: thin path needs C_out <= 32, small weights");
     a.splits = 1;
     const dim3 tg((unsigned)(S * L.R)), tb(fz::THIN_THREADS);
+    const bool f32 = cp < 0;
     switch (fz::thin_co(g->c_out)) {
-      case 2: e = launch_pdl(fz::k_conv_thin<2>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
-      case 4: e = launch_pdl(fz::k_conv_thin<4>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
-      case 8: e = launch_pdl(fz::k_conv_thin<8>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
-      case 16: e = launch_pdl(fz::k_conv_thin<16>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
-      default: e = launch_pdl(fz::k_conv_thin<32>, tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 2: e = launch_pdl((f32 ? fz::k_conv_thin<2, true> : fz::k_conv_thin<2, false>), tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 4: e = launch_pdl((f32 ? fz::k_conv_thin<4, true> : fz::k_conv_thin<4, false>), tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 8: e = launch_pdl((f32 ? fz::k_conv_thin<8, true> : fz::k_conv_thin<8, false>), tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      case 16: e = launch_pdl((f32 ? fz::k_conv_thin<16, true> : fz::k_conv_thin<16, false>), tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
+      default: e = launch_pdl((f32 ? fz::k_conv_thin<32, true> : fz::k_conv_thin<32, false>), tg, tb, (size_t)L.stage, st, in_hwc, hwc_stride, a); break;
     }
     if (e != cudaSuccess) {
       set_error(std::string("evc: conv_fused (thin) launch: ") + cudaGetErrorString(e));

@@ -4,6 +4,8 @@
 // channels, then their tails.  Rows are `pitch` pixels apart: the consumer conv
 // keeps a zero border of its padding around the interior (y points at pixel (0, 0)).
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace evc {
@@ -30,7 +32,7 @@ __global__ void __launch_bounds__(256) k_to_hwc(TView x, float* __restrict__ y, 
     const int p = p0 + ty + 8 * k, c = c0 + tx;
     if (p < HW && c < x.C) {
       const int py = p / x.W, px = p - py * x.W;
-      hwc_store(dst + ((int64_t)py * pitch + px) * 2 * cp, cp, c, t[tx][ty + 8 * k]);
+      hwc_store(dst + ((int64_t)py * pitch + px) * hwc_px(cp), cp, c, t[tx][ty + 8 * k]);
     }
   }
 }
@@ -45,7 +47,7 @@ int32_t evc_hwc_channels(int32_t c) { return (c + 31) / 32 * 32; }
 
 int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp, int32_t pitch, int32_t S,
                void* stream) {
-  EVC_CHECK_ARG(x && x->vals && y && S > 0 && cp >= x->C && cp % 4 == 0 && pitch >= x->W, "to_hwc: bad argument");
+  EVC_CHECK_ARG(x && x->vals && y && S > 0 && std::abs(cp) >= x->C && cp % 4 == 0 && pitch >= x->W, "to_hwc: bad argument");
   TView v = view_of(*x);
   dim3 grid(cdiv(v.H * v.W, 32), cdiv(v.C, 32), S);
   const cudaError_t e = launch_pdl(k_to_hwc, grid, dim3(256), 0, as_stream(stream), v, y, y_stride, cp, pitch);

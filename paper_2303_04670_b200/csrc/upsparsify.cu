@@ -10,6 +10,8 @@
 // last step, or when its residual is nonzero -- exactly the tiles the unfused
 // pair could change.  Norm partials are folded by the last CTA (fixed order).
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace evc {
@@ -201,16 +203,16 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       __syncthreads();
       if (q < Q) {
         const float* rc = s_r + cl * RS;
-        const int rstride = a.hp * 2 * a.cp;  // floats between shadow rows (< 2^31 per session)
+        const int rstride = a.hp * hwc_px(a.cp);  // floats between shadow rows (< 2^31 per session)
         float* sbase = a.hwc + (int64_t)s * a.hs + hwc_head(a.cp, c0 + cl);
-        const int tl = hwc_unit(a.cp);  // tail offset (32 floats: an immediate)
-        const int obase = r0 * rstride + x0 * 2 * a.cp;
+        const int tl = a.cp < 0 ? -1 : hwc_unit(a.cp);  // tail offset (32 floats: an immediate); -1: fp32
+        const int obase = r0 * rstride + x0 * hwc_px(a.cp);
         float ssf = 0.0f;
         for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q) {
         // the column's taps once (before any s_ny store of this column)
         const int tj = s_tj[xq], o0 = s_ci0[xq] - clo, o1 = s_ci1[xq] - clo;
         const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
-        float* dcol = sbase + obase + xq * 2 * a.cp;
+        float* dcol = sbase + obase + xq * hwc_px(a.cp);
         for (int tr = 0; tr < nti; ++tr) {
           const int ti = cl * NT + tr * nj + tj;
           if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
@@ -224,10 +226,14 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
             const float up = a.mode == 0 ? p0[k * a.XC]
                                          : __fadd_rn(__fmul_rn(p0[k * a.XC], cw0), __fmul_rn(p1[k * a.XC], cw1));
             const float ov = __fadd_rn(0.0f, up);
-            const float h = tf32_head(ov);
             float* dk = d + (int64_t)k * rstride;
-            dk[0] = h;
-            dk[tl] = __fsub_rn(ov, h);
+            if (tl < 0) {  // fp32 shadow (hwc_px)
+              dk[0] = ov;
+            } else {
+              const float h = tf32_head(ov);
+              dk[0] = h;
+              dk[tl] = __fsub_rn(ov, h);
+            }
             ssf = __fmaf_rn(ov, ov, ssf);
             nzb |= __float_as_uint(ov) & 0x7fffffffu;
           };
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       if (stage) {
         s_y[(r * 32 + xl) * 33 + cl] = o;
       } else if (a.hwc) {
-        hwc_store(a.hwc + (int64_t)s * a.hs + ((int64_t)u * a.hp + v) * 2 * a.cp, a.cp, c, o);
+        hwc_store(a.hwc + (int64_t)s * a.hs + ((int64_t)u * a.hp + v) * hwc_px(a.cp), a.cp, c, o);
       }
       if (!a.delta_zero) *dp = nd;
       ss += (double)corr * (double)corr;
@@ -300,10 +306,10 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       if (!a.fast) a.dlive[(int64_t)s * y.C * y.GH * y.GW + fo] = s_nd[t];
     }
     if (stage && !fast && lane < nc) {  // lane = channel: 128-byte runs of heads and of tails per pixel
-      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * 2 * a.cp;
+      float* dst = a.hwc + (int64_t)s * a.hs + (int64_t)r0 * a.hp * hwc_px(a.cp);
       for (int r = 0; r < nrow; ++r)
         for (int xq = warp; xq < ncol; xq += US_THREADS / 32)
-          hwc_store(dst + ((int64_t)r * a.hp + x0 + xq) * 2 * a.cp, a.cp, c0 + lane, s_y[(r * 32 + xq) * 33 + lane]);
+          hwc_store(dst + ((int64_t)r * a.hp + x0 + xq) * hwc_px(a.cp), a.cp, c0 + lane, s_y[(r * 32 + xq) * 33 + lane]);
     }
   }
   {  // block sum: the t_p = 0 path's per-thread sums are fp32 already -> fp32 warp sums
@@ -375,7 +381,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
   EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");
   EVC_CHECK_ARG(write_chw || hwc, "upsample_sparsify: no output requested");
-  EVC_CHECK_ARG(!hwc || (cp >= y->C && cp % 4 == 0 && hwc_pitch >= y->W),
+  EVC_CHECK_ARG(!hwc || (std::abs(cp) >= y->C && cp % 4 == 0 && hwc_pitch >= y->W),
                 "upsample_sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   USArgs a;
   a.x = view_of(*x);

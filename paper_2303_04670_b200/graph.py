@@ -807,7 +807,7 @@ class Graph:
                         sp = node.fused_sp
                         sh = sp.shadow
                         sdesc = self._desc(sp.spec.id)
-                        spd = _lib.EvcConvSparsify(sh.hwc_interior, sh.hwc[0].numel(), sh.cp, sh.pitch, sdesc.flags,
+                        spd = _lib.EvcConvSparsify(sh.hwc_interior, sh.hwc[0].numel(), sh.cpa, sh.pitch, sdesc.flags,
                                                    sdesc.fstride, sh.fany_ptr, sp.part_ptr)
                         node._spd = spd  # keep the struct alive with the program
                     fn, args = plan.fused(din, dout, fany=plan.fany_ptr, mpart=node.mpart.data_ptr(), act=fa, sp=spd)
@@ -847,7 +847,7 @@ class Graph:
                 j = node.sp_idx
                 up = self._by_id[ns.inputs[0]]
                 sh = node.shadow
-                hwc = ((sh.hwc_interior, sh.cp, sh.hwc[0].numel(), sh.pitch, sh.fany_ptr) if sh is not None
+                hwc = ((sh.hwc_interior, sh.cpa, sh.hwc[0].numel(), sh.pitch, sh.fany_ptr) if sh is not None
                        else (None, 0, 0, 0, None))
                 mode = 0 if up.spec.attrs.get("mode", "nearest") == "nearest" else 1
                 prog.append((L.evc_upsample_sparsify, (self._desc(up.spec.inputs[0]), int(up.spec.attrs.get("factor", 2)),
@@ -863,7 +863,7 @@ class Graph:
             elif k == "sparsify":
                 j = node.sp_idx
                 sh = node.shadow  # ConvPlan of the only consumer when it reads a channels-innermost shadow
-                hwc = ((sh.hwc_interior, sh.cp, sh.hwc[0].numel(), sh.pitch, sh.fany_ptr) if sh is not None
+                hwc = ((sh.hwc_interior, sh.cpa, sh.hwc[0].numel(), sh.pitch, sh.fany_ptr) if sh is not None
                        else (None, 0, 0, 0, None))
                 prog.append((L.evc_sparsify, (self._desc(ns.inputs[0]), node.delta.data_ptr(), node.delta[0].numel(),
                                               node.dlive.data_ptr(), self._desc(nid),

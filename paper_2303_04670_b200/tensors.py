@@ -309,11 +309,15 @@ class ConvPlan:
             _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
             # channels per shadow pixel: 32-aligned for the TMA path, 4-aligned for the CUDA-core path
             self.cp = -(-c_in // 4) * 4 if self.cfg.thin else int(lib.evc_hwc_channels(c_in))
-            # hi/lo shadow with a zero border of the conv's padding: (S, H + 2p, W + 2p, heads | tails)
+            # the CUDA-core path reads plain fp32 values (cp < 0 at the ABI, common.cuh hwc_px);
+            # the tensor-core path the hi/lo split
+            self.cpa = -self.cp if self.cfg.thin else self.cp
+            self.px = self.cp if self.cfg.thin else 2 * self.cp
+            # shadow with a zero border of the conv's padding: (S, H + 2p, W + 2p, px)
             self.pitch = w + 2 * pad
-            self.hwc = torch.zeros((S, h + 2 * pad, self.pitch, 2 * self.cp), dtype=torch.float32,
+            self.hwc = torch.zeros((S, h + 2 * pad, self.pitch, self.px), dtype=torch.float32,
                                    device=weight.device)
-            self.hwc_interior = self.hwc.data_ptr() + 4 * (pad * self.pitch + pad) * 2 * self.cp
+            self.hwc_interior = self.hwc.data_ptr() + 4 * (pad * self.pitch + pad) * self.px
             host = np.ascontiguousarray(weight.detach().cpu().numpy(), dtype=np.float32)
             out = np.zeros(int(lib.evc_conv_fused_pack_len(self.g, self.cfg)), dtype=np.float32)
             _lib.check(lib.evc_conv_fused_pack(host.ctypes.data, self.g, self.cfg, out.ctypes.data), "pack")
@@ -335,7 +339,7 @@ class ConvPlan:
         """(fn, args-without-stream) mirroring the conv input into the HWC shadow, or None."""
         if self.path != "fused":
             return None
-        return _lib.lib().evc_to_hwc, (din, self.hwc_interior, self.hwc[0].numel(), self.cp, self.pitch, self.S)
+        return _lib.lib().evc_to_hwc, (din, self.hwc_interior, self.hwc[0].numel(), self.cpa, self.pitch, self.S)
 
     def mask_args(self, din, dout, scratch, in_true, tile_list, tile_count, meter):
         """evc_conv_mask arguments of the unfused paths (stream appended by the caller)."""
@@ -349,7 +353,7 @@ class ConvPlan:
         dout may then be None (conv values not materialised).  sp = EvcConvSparsify fuses
         the following t_p = 0 sparsify (the act desc may then carry no values)."""
         code, alpha, acc, accs, adesc = act if act is not None else (-1, 0.0, None, 0, None)
-        return _lib.lib().evc_conv_fused, (self.g, self.cfg, self.hwc.data_ptr(), self.cp, self.hwc[0].numel(),
+        return _lib.lib().evc_conv_fused, (self.g, self.cfg, self.hwc.data_ptr(), self.cpa, self.hwc[0].numel(),
                                            self.wpack.data_ptr(), bias_ptr, din, fany, self.table.data_ptr(),
                                            self.rstate.data_ptr(), mpart, dout, code, alpha, acc, accs,
                                            adesc, sp, 1 if dense else 0, self.S)

@@ -256,3 +256,35 @@ def test_add_act_equals_add_then_activation(kind):
     assert np.array_equal(np_(y1).view(np.uint32), np_(y2).view(np.uint32))
     assert np.array_equal(np_(acc1).view(np.uint32), np_(acc2).view(np.uint32))
     assert np.array_equal(np_(f1), np_(f2)) and np.array_equal(np_(f2).astype(bool), fa | fb)
+
+
+@pytest.mark.parametrize("C", [4, 12, 32])
+def test_shadow_layouts_hilo_and_fp32(C):
+    """evc_to_hwc (include/evconv.h shadow layout): with cp > 0 each channel is a TF32 head
+    plus an exact tail (head + tail == value bit for bit, head has 13 zero low bits); with
+    cp < 0 the pixel holds the fp32 values themselves -- the same numbers in half the bytes."""
+    from paper_2303_04670_b200 import _lib
+    lib = _lib.lib()
+    rng = np.random.default_rng(C)
+    H, W, S = 14, 17, 2
+    cp = -(-C // 4) * 4 if C % 32 else C
+    x = rng.standard_normal((S, C, H, W)).astype(np.float32)
+    tx = T(x)
+    flags = torch.ones((S, C, -(-H // 6), -(-W // 6)), dtype=torch.uint8, device="cuda")
+    d = _lib.tdesc(tx.data_ptr(), flags.data_ptr(), C * H * W, flags[0].numel(), C, H, W, 6, 6)
+    hl = torch.zeros((S, H, W, 2 * cp), dtype=torch.float32, device="cuda")
+    f32 = torch.zeros((S, H, W, cp), dtype=torch.float32, device="cuda")
+    assert lib.evc_to_hwc(d, hl.data_ptr(), hl[0].numel(), cp, W, S, _lib.stream_ptr()) == 0
+    assert lib.evc_to_hwc(d, f32.data_ptr(), f32[0].numel(), -cp, W, S, _lib.stream_ptr()) == 0
+    torch.cuda.synchronize()
+    want = x.transpose(0, 2, 3, 1)
+    got = np_(f32)
+    assert np.array_equal(got[..., :C].view(np.uint32), want.view(np.uint32))
+    h = np_(hl)
+    if cp % 32 == 0:  # 32-channel chunks [heads | tails]
+        h = h.reshape(S, H, W, cp // 32, 2, 32)
+        heads, tails = h[..., 0, :].reshape(S, H, W, cp), h[..., 1, :].reshape(S, H, W, cp)
+    else:
+        heads, tails = h[..., :cp], h[..., cp:]
+    assert np.array_equal((heads[..., :C] + tails[..., :C]).view(np.uint32), want.view(np.uint32))
+    assert not np.any(heads.view(np.uint32) & 0x1FFF)

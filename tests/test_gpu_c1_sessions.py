@@ -1,0 +1,93 @@
+"""C1 (EV-FlowNet 256x256) at the benchmarked session counts, against the oracle.
+
+bench.py times C1 with 32 independent streams batched into every launch (the C5 layout:
+256 streams over 8 GPUs).  The fused conv's launch configuration changes with the session
+count (tap mode / BN 128 / split-K rules at S >= 8, csrc/conv_fused.cu evc_conv_fused_config),
+so the benchmarked graph itself is checked here: the bench's stream seeds, the bench's
+entry point (step_from_encodings = step_increment + incr_step, graph.py:573-630 and the
+reference timed region bench.py:196-209), and per-session oracle graphs for sessions
+{0, S/2 - 1, S - 1}:
+
+* integrated output within 1e-4 * max(1, max|ref|) every step;
+* output increment tile mask: flips (value-derived masks, rounding-zero tiles) counted,
+  printed and bounded, and every flipped tile's values <= 1e-6;
+* per-node FLOP meter: exact where no upstream mask flipped, <= 1e-4 * dense otherwise
+  (the count of exact nodes is printed);
+* drift after the run against a GPU dense recompute.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2303_04670_b200 as evc
+from paper_2303_04670_b200 import configs, shard
+from oracle import evincr_np as O
+from evc_testutil import max_err
+
+pytestmark = pytest.mark.gpu
+
+N_INC = 16
+
+
+def _stream_inputs(seed, n):
+    st = evc.generate_events(seed=seed, duration_us=50_000 + 1_000 * (n + 1), rate_hz=1.0e6, n_objects=8,
+                             sensor_size=(256, 256))
+    xs = []
+    for i in range(n + 1):
+        w = evc.slice_window(st, 50_000 + 1_000 * i, 50_000)
+        xs.append(torch.cat([evc.encode(w, evc.EncoderKind("count")), evc.encode(w, evc.EncoderKind("timestamp"))]))
+    return torch.stack(xs)
+
+
+@pytest.mark.parametrize("S", [8, 32])
+def test_c1_batched_sessions_vs_oracle(S):
+    spec = configs.evflownet_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    seeds = shard.stream_seeds(0, S)
+    xs = torch.stack([_stream_inputs(sd, N_INC) for sd in seeds], dim=1).contiguous()  # (n+1, S, 4, 256, 256)
+    g = evc.build(spec, weights, refresh_interval=0, sessions=S)
+    # the configuration under test really is the S >= 8 one
+    cfgs = {n.spec.id: (int(n.plan.cfg.row), int(n.plan.cfg.bn), int(n.plan.cfg.splits))
+            for n in g.nodes if n.kind == "conv" and n.plan.path == "fused" and not n.plan.cfg.thin}
+    assert cfgs["res0a"][0] == 0 and cfgs["dec0"][0] == 0 and cfgs["dec0"][1] == 128, cfgs
+    check = sorted({0, S // 2 - 1, S - 1})
+    ogs = {s: O.OracleGraph(spec.to_dict(), weights, refresh_interval=0) for s in check}
+    y0 = g.dense_pass(xs[0]).cpu().numpy()
+    for s in check:
+        e = max_err(y0[s], ogs[s].dense_pass(xs[0, s].cpu().numpy()))
+        assert e <= 1e-4, ("dense", s, e)
+    flips, exact_nodes, nodes, worst, perf_rel = 0, 0, 0, 0.0, 0.0
+    out = spec.output
+    for i in range(1, N_INC + 1):
+        g.step_from_encodings(xs[i - 1], xs[i])
+        v, f = g._slot_view(out)
+        v, f = v.cpu().numpy(), f.cpu().numpy().astype(bool)
+        for s in check:
+            rv, rf = O.step_increment(xs[i - 1, s].cpu().numpy(), xs[i, s].cpu().numpy(), 6, 6)
+            inm = g.input_slot()[1][s].cpu().numpy().astype(bool)
+            assert np.array_equal(inm, rf), ("input mask", i, s)
+            (ov, of), oy, orep = ogs[s].incr_step(rv, rf)
+            diff = f[s] != of
+            flips += int(diff.sum())
+            if diff.any():
+                px = O.flags_to_pixels(diff, 6, 6, 256, 256)
+                assert np.abs(np.where(px, v[s] - ov, 0)).max() <= 1e-6, ("flipped tile carries values", i, s)
+            rep = g.step_report(session=s).per_node
+            for nid, (p, de) in rep.items():
+                rp, rde = orep["per_node"][nid]
+                assert de == rde, nid
+                nodes += 1
+                exact_nodes += int(p == rp)
+                perf_rel = max(perf_rel, abs(p - rp) / max(1, rde))
+            worst = max(worst, max_err(g.integrated_output(session=s).cpu().numpy(), oy))
+    print(f"S={S}: sessions {check}, {N_INC} increments: output-mask flips {flips}, "
+          f"exact per-node meters {exact_nodes}/{nodes}, max meter rel {perf_rel:.2e}, max err {worst:.2e}")
+    assert worst <= 1e-4, worst
+    assert perf_rel <= 1e-4, perf_rel
+    assert flips <= 8, flips
+    assert exact_nodes >= 0.95 * nodes, (exact_nodes, nodes)
+    d = g.dense_oracle(xs[N_INC])
+    for s in check:
+        dr = g.drift(d, session=s)
+        assert dr <= 1e-4 * max(1.0, float(d[s].abs().max())), (s, dr)

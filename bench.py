@@ -1,22 +1,35 @@
-"""EV-FlowNet 256x256 incremental inference benchmark (BASELINE.json metric).
+"""EV-FlowNet 256x256 incremental inference benchmark (BASELINE.json metric), plus the C2 / C3 / C4
+configurations of BASELINE.json as sub-results of the same JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--sessions S] [--impl ours|reference]
+                    [--configs c2,c3,c4 | --configs none]
 
 A "step" is one incremental pass (step_increment + Graph.incr_step, plus the
 refresh when due -- the reference's timed region, bench.py:196-209) for each of
 the S independent event streams this rank owns (default 32 per GPU: the C5
 layout of 256 streams over 8 GPUs; every launch serves all S streams).  A
 second, single-stream pass reports the batch-1 per-increment latency
-(p50_increment_latency_ms).  Inputs are count(2) +
-timestamp(2) encodings of seeded synthetic 1 MHz streams (generate_events,
-8 objects, 256x256), 50 ms windows shifted by 1 ms (~2 % of elements change
-per increment), encoded on the GPU before timing and resident in HBM.
-Weights: seeded He-normal (WeightManifest.generate), t_p = 0, refresh every 64.
+(p50_increment_latency_ms).  Inputs are count(2) + timestamp(2) encodings of
+seeded synthetic 1 MHz streams (generate_events, 8 objects, 256x256), 50 ms
+windows shifted by 1 ms (~2 % of elements change per increment), encoded on the
+GPU before timing and resident in HBM.  Weights: seeded He-normal
+(WeightManifest.random_tensors), t_p = 0, refresh every 64 increments: one dense
+refresh is timed on its own and 1/64 of it is added to every step
+(``refresh_amortized_ms``), so ``value`` is the steady-state rate with refreshes.
 
-Multi-GPU (torchrun): streams shard across ranks with no collective on the
-data path (scaling "weak"); rank 0 prints one JSON line with the max-over-ranks
-device time.  ``--impl reference`` times the CPU reference algorithm (the
-oracle port of evincr's per-channel loop) on the host cores instead.
+``value`` is the whole-job rate (increments/s over all ranks, the driver's
+scaling input); ``value_per_gpu`` = value / N is the metric's per-GPU figure.
+``--gpus N`` without torchrun re-launches this script under
+``torch.distributed.run`` with N ranks (one GPU each, NCCL, 127.0.0.1).
+Streams shard across ranks with no collective on the data path (scaling
+"weak": rank r owns streams r*S .. r*S+S-1); rank 0 prints one JSON line with
+the max-over-ranks device time.  ``--impl reference`` times the CPU reference
+algorithm (the oracle port of evincr's per-channel loop) on the host cores.
+At N = 1 the line also carries ``configs``: C2 (E2Depth UNet, 5-bin voxels,
+264x352, 1 / 3 / 5 % density), C3 (ResNet-18, 2x180x240 counts) and C4 (one
+64->128 3x3 conv at 480x640, sparse vs the library's own dense conv over
+0.5-20 % live tiles), each with its rate, p50 latency, conv roofline and a
+bounded CPU baseline.
 """
 
 from __future__ import annotations
@@ -116,41 +129,67 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 
-def make_inputs(evc, n_windows, seeds, device):
+def c1_frames(evc, seed, n_windows):
+    """C1 input frames: count(2) + timestamp(2) of a seeded 1 MHz 256x256 stream, 50 ms windows / 1 ms."""
     import torch
 
-    per = []
-    for seed in seeds:
-        stream = evc.generate_events(seed=seed, duration_us=WINDOW_US + SHIFT_US * n_windows, rate_hz=RATE_HZ,
-                                     n_objects=8, sensor_size=(256, 256))
-        xs = []
-        for i in range(n_windows):
-            w = evc.slice_window(stream, WINDOW_US + SHIFT_US * i, WINDOW_US)
-            xs.append(torch.cat([evc.encode(w, evc.EncoderKind("count")), evc.encode(w, evc.EncoderKind("timestamp"))]))
-        per.append(torch.stack(xs))
-    return torch.stack(per, dim=1).contiguous()  # (n_windows, S, 4, 256, 256)
+    stream = evc.generate_events(seed=seed, duration_us=WINDOW_US + SHIFT_US * n_windows, rate_hz=RATE_HZ,
+                                 n_objects=8, sensor_size=(256, 256))
+    xs = []
+    for i in range(n_windows):
+        w = evc.slice_window(stream, WINDOW_US + SHIFT_US * i, WINDOW_US)
+        xs.append(torch.cat([evc.encode(w, evc.EncoderKind("count")), evc.encode(w, evc.EncoderKind("timestamp"))]))
+    return torch.stack(xs)
 
 
-def timed_run(evc, spec, weights, S, steps, warmup, rank, world, dev):
-    """Build an S-session graph, warm up, and time `steps` steps with CUDA events (L2 flushed between)."""
+C2_RATES = {"1%": 2.0e5, "3%": 2.0e6, "5%": 3.8e6}  # voxel increment density on 264x352 (calibrated)
+
+
+def c2_frames(evc, seed, n_windows, rate):
+    """C2 input frames: 5-bin voxel grids of a 260x346 stream, zero-padded bottom / right to 264x352."""
     import torch
 
-    n_win = 1 + warmup + steps + 1
-    seeds = _shard.stream_seeds(rank, S)
-    xs = make_inputs(evc, n_win, seeds, dev)  # resident in HBM before timing
-    density = float((xs[1:] != xs[:-1]).float().mean())
-    g = evc.build(spec, weights, refresh_interval=64, sessions=S)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = evc.generate_events(seed=seed, duration_us=WINDOW_US + SHIFT_US * n_windows, rate_hz=rate,
+                                 n_objects=8, sensor_size=(260, 346))
+    xs = [torch.nn.functional.pad(evc.encode(evc.slice_window(stream, WINDOW_US + SHIFT_US * i, WINDOW_US),
+                                             evc.parse_encoder("voxel:5")), (0, 6, 0, 4))
+          for i in range(n_windows)]
+    return torch.stack(xs)
 
-    def dense(i):
-        return g.dense_pass(xs[i] if S > 1 else xs[i][0])
+
+def c3_frames(evc, seed, n_windows, rate=2.0e5):
+    """C3 input frames: count(2) of a 180x240 stream (N-Caltech101 shape)."""
+    import torch
+
+    stream = evc.generate_events(seed=seed, duration_us=WINDOW_US + SHIFT_US * n_windows, rate_hz=rate,
+                                 n_objects=8, sensor_size=(180, 240))
+    return torch.stack([evc.encode(evc.slice_window(stream, WINDOW_US + SHIFT_US * i, WINDOW_US),
+                                   evc.EncoderKind("count")) for i in range(n_windows)])
+
+
+def make_inputs(frames, seeds):
+    import torch
+
+    return torch.stack([frames(sd) for sd in seeds], dim=1).contiguous()  # (n_windows, S, C, H, W)
+
+
+def timed_steps(g, xs, steps, warmup, world=1, clocks_index=None):
+    """Dense pass on window 0, `warmup` untimed steps, then `steps` timed steps (CUDA events on
+    the step stream, L2 flushed by a 256 MiB write before each).  Refreshes run in-line when due."""
+    import torch
+
+    S = g.S
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=xs.device)
+
+    def frame(i):
+        return xs[i] if S > 1 else xs[i][0]
 
     def step(i):
-        g.step_from_encodings(xs[i - 1], xs[i])
+        g.step_from_encodings(frame(i - 1), frame(i))
         if g.refresh_due:
-            dense(i)
+            g.dense_pass(frame(i))
 
-    dense(0)
+    g.dense_pass(frame(0))
     for i in range(1, 1 + warmup):
         step(i)
     torch.cuda.synchronize()
@@ -161,7 +200,10 @@ def timed_run(evc, spec, weights, S, steps, warmup, rank, world, dev):
         dist.barrier()
     torch.cuda.synchronize()
     refreshes = 0
-    with Clocks(dev.index or 0) as clk:
+    clk = Clocks(clocks_index) if clocks_index is not None else None
+    if clk:
+        clk.__enter__()
+    try:
         for j in range(steps):
             flush.fill_(float(j))  # evict L2 between timed steps (256 MiB > 126 MB L2)
             i = 1 + warmup + j
@@ -171,11 +213,33 @@ def timed_run(evc, spec, weights, S, steps, warmup, rank, world, dev):
             refreshes += bool(will_refresh)
             evs[j][1].record()
         torch.cuda.synchronize()
+    finally:
+        if clk:
+            clk.__exit__()
     if world > 1:
         dist.barrier()
-    times = [a.elapsed_time(b) for a, b in evs]
     del flush
-    return g, xs, times, refreshes, clk, density
+    return [a.elapsed_time(b) for a, b in evs], refreshes, clk
+
+
+def time_refresh(g, x, reps=3):
+    """Device time of one dense refresh (dense_pass) of all S sessions, ms (median of `reps`)."""
+    import torch
+
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        g.dense_pass(x)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts)
+
+
+def pct(sorted_ts, q):
+    return sorted_ts[min(len(sorted_ts) - 1, int(round(q * (len(sorted_ts) - 1))))]
 
 
 def run_ours(args):
@@ -203,24 +267,29 @@ def run_ours(args):
     spec = configs.evflownet_spec(tp=0.0)
     weights = evc.WeightManifest.random_tensors(spec, 0)
     S = args.sessions
-    res = timed_run(evc, spec, weights, S, args.steps, args.warmup, rank, world, dev)
-    g, xs, times, refreshes, clk, density = res
-    total_ms = _shard.job_time_ms(sum(times), world, cdev)  # max over ranks
+    n_win = 1 + args.warmup + args.steps + 1
+    seeds = _shard.stream_seeds(rank, S)
+    xs = make_inputs(lambda sd: c1_frames(evc, sd, n_win), seeds)  # resident in HBM before timing
+    density = float((xs[1:] != xs[:-1]).float().mean())
+    g = evc.build(spec, weights, refresh_interval=64, sessions=S)
+    times, refreshes, clk = timed_steps(g, xs, args.steps, args.warmup, world, dev.index or 0)
+    # one refresh per 64 increments: timed on its own, 1/64 of it added to every step
+    refresh_ms = time_refresh(g, xs[0] if S > 1 else xs[0][0])
+    steps_cost = sum(times) + refresh_ms * max(0.0, args.steps / 64.0 - refreshes)
+    total_ms = _shard.job_time_ms(steps_cost, world, cdev)  # max over ranks
     value = _shard.aggregate_rate(args.steps, S, world, total_ms)
     steady = sorted(times)
-    p50 = statistics.median(steady)
-    p99 = steady[min(len(steady) - 1, int(round(0.99 * (len(steady) - 1))))]
+    p50, p99 = statistics.median(steady), pct(steady, 0.99)
     launches = g.kernel_launches_per_step() + 1  # + diff_mask
     gpu_launches = args.steps * launches + refreshes * g.dense_launches()
     lat = None
     if S > 1 and not args.no_latency_pass:  # single-stream latency (batch 1), same workload
-        g1, _, t1, _, _, _ = timed_run(evc, spec, weights, 1, min(args.steps, 32), args.warmup, rank, world, dev)
+        g1 = evc.build(spec, weights, refresh_interval=64, sessions=1)
+        t1, _, _ = timed_steps(g1, xs[:, :1].contiguous(), min(args.steps, 32), args.warmup, world)
         s1 = sorted(t1)
-        lat = {"sessions": 1, "p50_ms": statistics.median(s1),
-               "p99_ms": s1[min(len(s1) - 1, int(round(0.99 * (len(s1) - 1))))], "steps": len(s1)}
+        lat = {"sessions": 1, "p50_ms": statistics.median(s1), "p99_ms": pct(s1, 0.99), "steps": len(s1)}
         del g1
-    # -- per-kernel timing of the conv GEMMs (dominant kernel) on the launching stream
-    roof = conv_roofline(g, xs, args, evc)
+    roof = conv_roofline(g, xs, evc)
     e2e = measure_e2e(g, xs, args, S, world, cdev)
     out = None
     if rank == 0:
@@ -228,18 +297,32 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "value_per_gpu": value / world,
             "config": {"workload": (f"C1 EV-FlowNet 256x256 (4-ch count+timestamp), ~2% increment density, batch 1 "
                                     f"per stream; {S} independent streams per GPU batched into every launch "
                                     f"(C5 layout: 256 streams over 8 GPUs = 32 per GPU)"),
                        "sessions_per_gpu": S, "streams_total": S * world, "t_p": 0.0, "refresh_interval": 64,
                        "window_us": WINDOW_US, "shift_us": SHIFT_US, "increment_density": density,
                        "l2": "flushed between timed steps (256 MiB write, excluded from step events)",
-                       "parallelism": f"streams sharded over {world} GPU(s), no collective"},
+                       "refresh": ("one dense refresh per 64 increments: timed separately and 1/64 of it added to "
+                                   "every step without an in-line refresh"),
+                       "parallelism": f"streams sharded over {world} GPU(s) (rank r owns streams r*S..r*S+S-1), "
+                                      f"no collective"},
             "p50_ms": p50, "p99_ms": p99, "refreshes_in_timed_region": refreshes,
+            "refresh_ms": refresh_ms, "refresh_amortized_ms": refresh_ms / 64.0,
+            "value_no_refresh": _shard.aggregate_rate(args.steps, S, world, _shard.job_time_ms(sum(times), world, cdev)),
             "p50_increment_latency_ms": (lat or {}).get("p50_ms", p50 if S == 1 else None),
             "latency_single_stream": lat,
             "clocks": clk.summary(), "gpu_launches": gpu_launches, "roofline": roof, "e2e": e2e,
         }
+    if world > 1 and args.gpus != world and rank == 0:
+        out["config"]["gpus_flag_mismatch"] = f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    del g, xs
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1:
+        want = [c for c in args.configs.split(",") if c and c != "none"]
+        if want:
+            out["configs"] = sub_configs(evc, configs, want, args)
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -250,22 +333,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def conv_roofline(g, xs, args, evc):
-    """Time every conv GEMM launch of a few steps with CUDA events on the launching
-    stream; achieved = reference-meter FLOPs (algorithmic) / GEMM time."""
+def conv_roofline(g, xs, evc, nsteps=8):
+    """Time every conv launch of a few eager steps with CUDA events on the launching stream;
+    achieved = reference-meter FLOPs (algorithmic) / conv time, peak = the TF32 tensor peak."""
     import torch
 
     from paper_2303_04670_b200 import _lib
 
     hbm, bf16, src = peaks()
-    # replay the same windows eagerly with events around the GEMM launches
-    g2 = evc.build(g.spec, {k: v for k, v in _weights_of(g).items()}, refresh_interval=0, sessions=g.S,
-                   cuda_graph=False)
     S = g.S
+    g2 = evc.build(g.spec, _weights_of(g), refresh_interval=0, sessions=S, cuda_graph=False)
     g2.dense_pass(xs[0] if S > 1 else xs[0][0])
     prog = g2._program
     gemm_ms, gemm_flops, step_ms = [], [], []
-    nsteps = min(8, xs.shape[0] - 1)
+    nsteps = min(nsteps, xs.shape[0] - 1)
     conv_idx = [n.meter_idx for n in g2.nodes if n.kind == "conv"]
     for i in range(1, 1 + nsteps):
         _lib.check(g2.lib.evc_diff_mask(xs[i - 1].data_ptr(), xs[i].data_ptr(), xs[0][0].numel(),
@@ -285,21 +366,18 @@ def conv_roofline(g, xs, args, evc):
     peak = 0.5 * bf16  # dense TF32 tensor peak = 1/2 measured bf16
     n_launch = sum(1 for _, _, n in prog if n in ("conv_fused", "conv_gemm"))
     traffic, tsrc = None, None
-    tp = Path(__file__).resolve().parent / "profiles" / "r01_conv_traffic_s32.json"
-    if tp.exists():  # ncu DRAM bytes of the same 16 launches (one step), committed under profiles/
+    tp = ROOT / "profiles" / "r02_conv_traffic_s32.json"
+    if tp.exists():  # ncu DRAM bytes of the same launches (one step), committed under profiles/
         tj = json.loads(tp.read_text())
-        if tj.get("sessions") == S and tj.get("launches_per_step") == n_launch_expected(g2):
+        if tj.get("sessions") == S and tj.get("launches_per_step") == n_launch and g.spec.name == tj.get("model"):
             traffic, tsrc = tj["dram_bytes_per_step"], f"profiles/{tp.name} ({tj['source']})"
-    return {"bound": "tensor", "kernel": "conv_fused (all 16 conv layers incl. fused mask/meter/activation, per step)", "achieved": achieved,
-            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per step",
-            "traffic_source": tsrc,
+    del g2
+    return {"bound": "tensor", "kernel": f"conv_fused (all {n_launch} conv layers incl. fused mask/meter/activation, per step)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_unit": "bytes per step", "traffic_source": tsrc,
             "peak_source": f"0.5 x {src} bf16 ({bf16} TF) as the TF32 tensor peak",
             "algorithmic_flops_per_step": f, "gemm_ms_per_step": t * 1e3, "gemm_launches_per_step": n_launch,
             "gemm_share_of_eager_step": (sum(gemm_ms) / sum(step_ms)) if step_ms else None}
-
-
-def n_launch_expected(g):
-    return sum(1 for _, _, n in g._program if n in ("conv_fused", "conv_gemm"))
 
 
 def _weights_of(g):
@@ -340,6 +418,129 @@ def measure_e2e(g, xs, args, S, world=1, dev=None):
     return {"value": n * S * world / wall, "unit": UNIT, "h2d_bytes_per_step": int(host[0].numel() * 4),
             "d2h_bytes_per_step": int(out_host[0].numel() * 4), "ms_per_step": wall / n * 1e3,
             "copies": "H2D / D2H on a copy stream, overlapped with the neighbouring steps' compute"}
+
+
+# ---------------------------------------------------------------------------
+# C2 / C3 / C4 sub-results (N = 1)
+# ---------------------------------------------------------------------------
+
+
+def graph_config(evc, spec, frames, S, steps, warmup, cpu_fn, cpu_budget, label):
+    """Rate (S sessions), single-stream p50 latency, conv roofline and CPU baseline of one model config."""
+    import torch
+
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    n_win = 1 + warmup + steps + 1
+    xs = make_inputs(frames, _shard.stream_seeds(0, S))
+    density = float((xs[1:] != xs[:-1]).float().mean())
+    g = evc.build(spec, weights, refresh_interval=64, sessions=S)
+    times, refreshes, _ = timed_steps(g, xs, steps, warmup)
+    refresh_ms = time_refresh(g, xs[0] if S > 1 else xs[0][0], reps=1)
+    cost = sum(times) + refresh_ms * max(0.0, steps / 64.0 - refreshes)
+    roof = conv_roofline(g, xs, evc, nsteps=4)
+    del g
+    g1 = evc.build(spec, weights, refresh_interval=64, sessions=1)
+    t1, _, _ = timed_steps(g1, xs[:, :1].contiguous(), steps, warmup)
+    del g1, xs
+    torch.cuda.empty_cache()
+    s1 = sorted(t1)
+    res = {"workload": label, "sessions": S, "increment_density": density, "steps": steps,
+           "value": steps * S / (cost / 1e3), "unit": UNIT, "ms_per_step": cost / steps,
+           "p50_ms_per_step": statistics.median(times), "refresh_ms": refresh_ms,
+           "p50_increment_latency_ms": statistics.median(s1), "p99_increment_latency_ms": pct(s1, 0.99),
+           "roofline": {k: roof[k] for k in ("bound", "achieved", "peak", "unit", "frac", "algorithmic_flops_per_step",
+                                             "gemm_ms_per_step", "gemm_share_of_eager_step")}}
+    if cpu_fn is not None and cpu_budget > 0:
+        res["cpu_baseline"] = run_cpu(cpu_fn, cpu_budget)
+    return res
+
+
+def c4_config(evc, iters=10, cpu_budget=0.0):
+    """C4: one 64 -> 128 3x3 conv (stride 1, pad 1) at 480x640 inside a device Graph (input ->
+    conv), incremental on a tile-clustered increment (fraction d of the 6x6 tiles live in all 64
+    channels) vs the same library's dense conv of the full input.  Times = CUDA events around the
+    conv's launches (input shadow + any-channel map + fused conv), median of `iters`."""
+    import numpy as np
+    import torch
+
+    from paper_2303_04670_b200 import _lib
+    from paper_2303_04670_b200.graph import ModelSpec, NodeSpec
+
+    C, H, W, CO = 64, 480, 640, 128
+    spec = ModelSpec("c4-conv", (C, H, W), [NodeSpec("conv", "conv", ["input"],
+                                                      {"out_channels": CO, "kernel": [3, 3], "stride": 1,
+                                                       "padding": 1})], "conv")
+    rng = np.random.default_rng(0)
+    wt = (rng.standard_normal((CO, C, 3, 3)) * np.sqrt(2.0 / (C * 9))).astype(np.float32)
+    g = evc.build(spec, {"conv.weight": wt}, refresh_interval=0, sessions=1, cuda_graph=False)
+    x_dense = torch.from_numpy(rng.standard_normal((C, H, W)).astype(np.float32)).cuda()
+    g.dense_pass(x_dense)
+    # dense: the conv's launches of the dense program (input shadow + dense conv)
+    dts = []
+    for _ in range(iters):
+        g._load_input(x_dense)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g._dense_program(False)
+        e1.record()
+        torch.cuda.synchronize()
+        dts.append(e0.elapsed_time(e1) * 1e3)
+    g._clear_increments()
+    t_dense = statistics.median(dts)
+    gh, gw = -(-H // 6), -(-W // 6)
+    rows = []
+    for d in (0.005, 0.01, 0.02, 0.05, 0.10, 0.20):
+        f2 = rng.random((gh, gw)) < d
+        px = np.repeat(np.repeat(f2, 6, 0), 6, 1)[:H, :W]
+        vals = torch.from_numpy((rng.standard_normal((C, H, W)) * px[None]).astype(np.float32)).cuda()
+        flags = torch.from_numpy(np.broadcast_to(f2, (C, gh, gw)).copy()).cuda().to(torch.uint8)
+        ts, perf = [], 0
+        v, f = g.input_slot()
+        for it in range(iters + 2):
+            v.copy_(vals.unsqueeze(0))
+            f.copy_(flags.unsqueeze(0))
+            torch.cuda.synchronize()
+            timed = ({"to_hwc", "tile_any", "conv_fused", "conv_mask", "conv_gemm"}, [])
+            g._run_program(timed=timed)
+            torch.cuda.synchronize()
+            if it >= 2:  # (the first two calls settle the region state of the new mask)
+                ts.append(sum(a.elapsed_time(b) for _, a, b in timed[1]) * 1e3)
+                perf = int(g._perf_step[0, 0])
+        t = statistics.median(ts)
+        rows.append({"live_tiles": d, "mask": "clustered", "sparse_us": t, "dense_us": t_dense,
+                     "sparse_over_dense": t / t_dense, "performed_over_dense": perf / g._dense_static[0]})
+    cross = max([r["live_tiles"] for r in rows if r["sparse_us"] < t_dense], default=None)
+    del g
+    torch.cuda.empty_cache()
+    res = {"workload": "C4 single 3x3 conv 64->128 @480x640, tile-clustered increments (Graph, conv launches timed)",
+           "dense_us": t_dense, "sweep": rows, "sparse_faster_than_dense_up_to": cross}
+    if cpu_budget > 0:
+        res["cpu_baseline"] = run_cpu(("c4", 0.02), cpu_budget)
+    return res
+
+
+def sub_configs(evc, configs, want, args):
+    steps = max(4, min(args.steps, 16))
+    warmup = args.warmup
+    n_win = 1 + warmup + steps + 1
+    budget = args.sub_cpu_budget if not args.no_cpu_baseline else 0.0
+    out = {}
+    if "c2" in want:
+        spec = configs.unet_e2depth_spec(tp=0.0)
+        for name, rate in C2_RATES.items():
+            out[f"C2_{name}"] = graph_config(
+                evc, spec, lambda sd, r=rate: c2_frames(evc, sd, n_win, r), 8, steps, warmup,
+                ("c2", rate) if name == "1%" else None, budget,
+                f"C2 E2Depth-style UNet (levels 4, base 32) on 5-bin voxels 264x352, ~{name} increment density, "
+                f"8 streams batched")
+    if "c3" in want:
+        out["C3"] = graph_config(evc, configs.resnet18_spec(tp=0.0), lambda sd: c3_frames(evc, sd, n_win), 32, steps,
+                                 warmup, ("c3", 2.0e5), budget,
+                                 "C3 ResNet-18 (fc 101) on 2x180x240 count histograms, 32 streams batched")
+    if "c4" in want:
+        out["C4"] = c4_config(evc, cpu_budget=budget)
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -418,6 +619,81 @@ def cpu_baseline(budget_s=20.0, procs=1, n_incr=64):
                       f"{cores} host cores visible, wall {wall:.1f}s"}
 
 
+def _cpu_sub_worker(kind, param, budget_s, q):
+    """Reference algorithm (oracle port, per-channel conv loop) on one C2 / C3 / C4 sample."""
+    import paper_2303_04670_b200.configs as configs  # specs only (no CUDA)
+    from paper_2303_04670_b200.graph import WeightManifest
+    from paper_2303_04670_b200.synth import generate_events
+    from oracle import evincr_np as O
+
+    times = []
+    if kind == "c4":
+        rng = np.random.default_rng(0)
+        C, H, W, CO = 64, 480, 640, 128
+        wt = (rng.standard_normal((CO, C, 3, 3)) * np.sqrt(2.0 / (C * 9))).astype(np.float32)
+        f2 = rng.random((-(-H // 6), -(-W // 6))) < param
+        px = np.repeat(np.repeat(f2, 6, 0), 6, 1)[:H, :W]
+        vals = (rng.standard_normal((C, H, W)) * px[None]).astype(np.float32)
+        flags = np.broadcast_to(f2, (C, *f2.shape)).copy()
+        t_start = time.perf_counter()
+        while not times or time.perf_counter() - t_start < budget_s:
+            t0 = time.perf_counter()
+            O.inc_conv2d_refalg(vals, flags, 6, 6, wt, 1, 1)
+            times.append(time.perf_counter() - t0)
+        q.put(times)
+        return
+    if kind == "c2":
+        spec = configs.unet_e2depth_spec(tp=0.0)
+        hw, enc, pad = (260, 346), ("voxel", 5), (4, 6)
+    else:
+        spec = configs.resnet18_spec(tp=0.0)
+        hw, enc, pad = (180, 240), ("count", 1), (0, 0)
+    weights = WeightManifest.random_tensors(spec, 0)
+    stream = generate_events(seed=0, duration_us=WINDOW_US + SHIFT_US * 40, rate_hz=param, n_objects=8,
+                             sensor_size=hw)
+
+    def frame(i):
+        lo, hi = O.slice_window(stream.t, WINDOW_US + SHIFT_US * i, WINDOW_US)
+        x = O.encode(stream.t, stream.x, stream.y, stream.p, lo, hi, WINDOW_US + SHIFT_US * i, WINDOW_US, *hw,
+                     enc[0], bins=enc[1])
+        return np.pad(x, ((0, 0), (0, pad[0]), (0, pad[1])))
+
+    g = O.OracleGraph(spec.to_dict(), weights, refresh_interval=64, conv_impl="refalg")
+    prev = frame(0)
+    g.dense_pass(prev)
+    t_start = time.perf_counter()
+    for i in range(1, 39):
+        cur = frame(i)
+        t0 = time.perf_counter()
+        g.incr_step(*O.step_increment(prev, cur, 6, 6))
+        times.append(time.perf_counter() - t0)
+        prev = cur
+        if time.perf_counter() - t_start > budget_s:
+            break
+    q.put(times)
+
+
+def run_cpu(job, budget_s):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_cpu_sub_worker, args=(job[0], job[1], budget_s, q))
+    t0 = time.perf_counter()
+    p.start()
+    times = q.get()
+    p.join()
+    cores = len(os.sched_getaffinity(0))
+    what = {"c2": "C2 increments (step_increment + incr_step)", "c3": "C3 increments (step_increment + incr_step)",
+            "c4": f"C4 inc_conv2d calls at {job[1]:.0%} clustered live tiles"}[job[0]]
+    return {"value": len(times) / sum(times), "unit": UNIT if job[0] != "c4" else "calls/s",
+            "cores": int(os.environ.get("OPENBLAS_NUM_THREADS", cores)), "kind": "port",
+            "p50_ms": 1e3 * statistics.median(times),
+            "sample": f"{len(times)} {what}, reference per-channel conv loop (oracle port), OpenBLAS threads "
+                      f"{os.environ.get('OPENBLAS_NUM_THREADS', 'default')}, {cores} host cores visible, "
+                      f"wall {time.perf_counter() - t0:.1f}s"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -436,6 +712,18 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def relaunch(n):
+    """--gpus N without a launcher: re-exec this script under torch.distributed.run with N ranks."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -447,7 +735,12 @@ def main():
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency-pass", action="store_true")
+    ap.add_argument("--configs", default="c2,c3,c4",
+                    help="sub-results at N = 1: comma list of c2, c3, c4 (or 'none')")
+    ap.add_argument("--sub-cpu-budget", type=float, default=8.0, help="CPU seconds per sub-config baseline")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

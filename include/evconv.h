@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define EVC_ABI_VERSION 1
+#define EVC_ABI_VERSION 2
 
 enum {
   EVC_OK = 0,
@@ -115,6 +115,26 @@ int evc_copy_dense(const float* src, int64_t src_stride, float* dst,
                    int64_t dst_stride, int64_t n_per_session, int32_t S,
                    void* stream);
 
+/* Serving-path ingest of S sessions per step (events.py:35-37 records,
+ * events.py:251-280 encodings).  Each session keeps its recent events in a device ring of `ring`
+ * (power of two) slots per column; event with absolute index e lives at slot e & (ring - 1).
+ * evc_ingest_ring: desc[s] = {first record of session s in `records`, count, absolute index of
+ * its first new event}; records = the step's packed EVB records of all sessions, concatenated.
+ * evc_encode_windows: win[s] = {lo, hi (absolute event indices), tau, delta}; writes count
+ * (mode 1), timestamp (mode 2) or count + timestamp (mode 3, 4 channels) of every window into
+ * out[s * out_stride] (zeroed here), bit-identical to encode(); max_events >= max(hi - lo). */
+int evc_ingest_ring(const uint8_t* records, const int64_t* desc, int64_t max_new, int64_t ring, uint64_t* t,
+                    uint16_t* x, uint16_t* y, int8_t* p, int32_t S, void* stream);
+int evc_encode_windows(const uint64_t* t, const uint16_t* x, const uint16_t* y, const int8_t* p, int64_t ring,
+                       const int64_t* win, int64_t max_events, int32_t H, int32_t W, int32_t mode, float* out,
+                       int64_t out_stride, int32_t S, void* stream);
+
+/* Strided byte copy of S blocks of `nbytes` (cudaMemcpy2DAsync, capturable in a CUDA
+ * graph): the recurrent delay node's pending increment (values and tile flags) moved
+ * between its state buffers and its output slot. */
+int evc_copy_bytes(const void* src, int64_t src_stride, void* dst, int64_t dst_stride,
+                   int64_t nbytes, int32_t S, void* stream);
+
 /* Graph.drift (graph.py:646-654): out[s] = max|a - b| (float32 bits kept
  * exact).  out must be zeroed first. */
 int evc_max_abs_diff(const float* a, int64_t a_stride, const float* b,
@@ -180,6 +200,10 @@ typedef struct evc_conv_cfg {
                      flattened with pitch W + 2 pad; a K-block is one kernel row x 32 channels,
                      loaded once (128 + kw - 1 shadow pixels) for all kw taps */
   int32_t thin;   /* 1: CUDA-core fp32 path (C_in <= 8 or C_out <= 8, C_out <= 32), tap-mode regions */
+  int32_t drain;  /* > 0: K-blocks per TMEM accumulation segment -- every segment's partial sum is promoted
+                     into fp32 registers of the epilogue warps (RN adds) while the MMAs fill the other of
+                     two accumulator blocks, so no tensor-core accumulation chain is longer than one
+                     segment (the dense pass always runs this way); 0: one chain per accumulator block */
 } evc_conv_cfg;
 
 /* 1 if the fused path handles this geometry (pad < kernel, stride <= 8). */

@@ -485,7 +485,17 @@ def step_increment(prev, cur, th, tw):
 # ---------------------------------------------------------------------------
 
 ACTS = ("relu", "sigmoid", "tanh", "leaky_relu")
-KINDS = ACTS + ("conv", "linear", "add", "mul", "concat", "upsample", "maxpool", "sparsify")
+KINDS = ACTS + ("conv", "linear", "add", "mul", "concat", "upsample", "maxpool", "sparsify", "delay")
+
+# ``delay`` (recurrent-state extension, SURVEY.md 8(f) rank 3 -- not a reference kind; the reference
+# has the recurrent primitives inc_mul / sigmoid / tanh, increment_ops.py:241-254, tensors.py:289-294,
+# but no recurrent graph).  A delay node has no inputs; attrs ``source`` (a node id) and
+# ``shape``.  Frame semantics: at frame t it outputs the source's value of frame t - 1 (zeros before the
+# first frame), which closes ConvLSTM / ConvGRU loops h_t = cell(x_t, h_{t-1}) without a cycle in the
+# per-frame DAG.  Incremental semantics (exact restatement of the frame semantics):
+#   state  held = the delay's current output value, pend = (values, flags) of its next increment;
+#   dense pass: output held; afterwards pend = step_increment(held, source)            (mutating pass)
+#   incr step : output pend; held += pend (integrate); after the step pend = source's increment.
 
 
 def topo_order(spec):
@@ -535,6 +545,8 @@ def node_shape(n, ins):
         wh, ww = n.get("window", [2, 2])
         st = n.get("stride", 2)
         return (c, (h - wh) // st + 1, (w - ww) // st + 1)
+    if k == "delay":
+        return tuple(int(v) for v in n["shape"])
     raise ValueError(k)
 
 
@@ -566,13 +578,17 @@ class OracleGraph:
         self.ff = {}
         for n in self.order:
             nid, k = n["id"], n["kind"]
-            ish = self.shapes[n["inputs"][0]]
+            ish = self.shapes[n["inputs"][0]] if n["inputs"] else None
             if k in ACTS or k == "maxpool":
                 self.state[nid] = {"acc": np.zeros(ish, F32)}
             elif k == "mul":
                 self.state[nid] = {"acc": np.zeros(ish, F32), "acc2": np.zeros(self.shapes[n["inputs"][1]], F32)}
             elif k == "sparsify":
                 self.state[nid] = sparsify_state(ish, n.get("tp", 0.0), n.get("ema_decay", 0.9))
+            elif k == "delay":
+                sh = self.shapes[nid]
+                self.state[nid] = {"held": np.zeros(sh, F32), "pv": np.zeros(sh, F32),
+                                   "pf": np.zeros(tile_grid(sh, self.th, self.tw), bool)}
             if k in ("conv", "linear"):
                 self.meter[nid] = [0, 0]
                 self.ff[nid] = [0.0, 0.0, 0]  # last, sum, n
@@ -626,9 +642,16 @@ class OracleGraph:
                 y = dense_maxpool(ins[0], tuple(n.get("window", [2, 2])), n.get("stride", 2))
                 if mutate:
                     self.state[nid]["acc"] = ins[0].copy()
+            elif k == "delay":
+                y = self.state[nid]["held"].copy()
             else:
                 raise ValueError(k)
             vals[nid] = y
+        if mutate:
+            for n in self.order:
+                if n["kind"] == "delay":
+                    st = self.state[n["id"]]
+                    st["pv"], st["pf"] = step_increment(st["held"], vals[n["source"]], self.th, self.tw)
         return vals
 
     def dense_oracle(self, x):
@@ -687,11 +710,18 @@ class OracleGraph:
                 y, f, st["acc"] = inc_maxpool(ins[0][0], ins[0][1], th, tw, st["acc"],
                                               tuple(n.get("window", [2, 2])), n.get("stride", 2))
                 out = (y, f)
+            elif k == "delay":
+                out = (st["pv"], st["pf"])
+                st["held"] = integrate(st["held"], st["pv"], st["pf"], th, tw)
             else:
                 raise ValueError(k)
             vals[nid] = out
             if trace is not None:
                 trace[nid] = out
+        for n in self.order:  # the next step's delayed increments
+            if n["kind"] == "delay":
+                sv, sf = vals[n["source"]]
+                self.state[n["id"]]["pv"], self.state[n["id"]]["pf"] = sv.copy(), np.asarray(sf, bool).copy()
         for o in self.out_ids:
             self.y_run[o] = integrate(self.y_run[o], vals[o][0], vals[o][1], th, tw)
         for nid, (perf, de) in step.items():
@@ -735,6 +765,9 @@ class OracleGraph:
             if "delta" in st:
                 out[nid + ".delta"] = st["delta"].copy()
                 out[nid + ".norm"] = np.asarray([st["norm_ema"], st["k"]], np.float64)
+            if "held" in st:
+                out[nid + ".held"] = st["held"].copy()
+                out[nid + ".pend"] = st["pv"].copy()
         for o in self.out_ids:
             if o in self.y_run:
                 out[o + ".y_run"] = self.y_run[o].copy()

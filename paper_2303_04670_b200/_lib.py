@@ -13,7 +13,7 @@ from pathlib import Path
 import torch
 
 LIB_PATH = Path(__file__).resolve().parent / "libevconv.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 ENC = {"count": 0, "timestamp": 1, "voxel": 2}
 ACT = {"relu": 0, "sigmoid": 1, "tanh": 2, "leaky_relu": 3}
@@ -38,7 +38,7 @@ class EvcConvGeom(C.Structure):
 
 
 class EvcConvCfg(C.Structure):
-    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits", "row", "thin")]
+    _fields_ = [(n, C.c_int32) for n in ("bn", "rh", "rw", "splits", "row", "thin", "drain")]
 
 
 class EvcConvSparsify(C.Structure):
@@ -80,6 +80,7 @@ _PROTOS = {
     "evc_integrate": (_I32, [_P, _I64, _T, _I32, _P]),
     "evc_copy_masked": (_I32, [_T, _T, _I32, _P]),
     "evc_copy_dense": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P]),
+    "evc_copy_bytes": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P]),
     "evc_max_abs_diff": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P]),
     "evc_conv_table_len": (_I64, [_G]),
     "evc_conv_table_fill": (_I32, [_G, _P]),
@@ -126,6 +127,8 @@ _PROTOS = {
     "evc_bin_events": (_I32, [_P, _P, _P, _P, _I64, _I64, _I64, _I64, _I32, _I32, _I32, _I32, _P, _P, _I64, _P]),
     "evc_unpack_events": (_I32, [_P, _I64, _P, _P, _P, _P, _P]),
     "evc_count_increment": (_I32, [_P, _P, _P, _I64, _I64, _I64, _I64, _T, _P]),
+    "evc_ingest_ring": (_I32, [_P, _P, _I64, _I64, _P, _P, _P, _P, _I32, _P]),
+    "evc_encode_windows": (_I32, [_P, _P, _P, _P, _I64, _P, _I64, _I32, _I32, _I32, _P, _I64, _I32, _P]),
 }
 
 EXPORTED = tuple(_PROTOS)

@@ -159,6 +159,7 @@ struct Args {
   // pitch P = W + 2 pad; a K-block is (kernel row, 32 channels) with the kw taps as row shifts
   int row, P, R, VM;  // row = 2: packed (kw taps along N, shifted sums in the epilogue); VM sites per region
   int ns, stage, a_half, b_bytes;  // pipeline depth and stage layout (bytes)
+  int drain;                       // > 0: K-blocks per accumulation segment (promoted to fp32 registers)
   const float* wpack;
   const float* bias;
   // incremental mode (dense == 0)
@@ -432,13 +433,19 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[4], empty[4], acc
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNS + 1);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // tma[4], empty[4], acc, seg[2], free[2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNS + 5);
   volatile int* s_flag = reinterpret_cast<volatile int*>(tslot + 1);  // [0] live, [1] computed last step
   const uint32_t sb = su32(smem), b0 = su32(bars);
   auto tma_bar = [&](int i) { return b0 + 8u * i; };
   auto empty_bar = [&](int i) { return b0 + 8u * (MAXNS + i); };
   const uint32_t acc_bar = b0 + 8u * (2 * MAXNS);
+  // promotion mode: segment g of a.drain K-blocks accumulates into TMEM block g & 1 = [main | small]
+  // (2 BN columns: hi.hi, then hi.lo + lo.hi); seg_bar[j] = block j's segment complete, free_bar[j] =
+  // the epilogue warps have added it to their fp32 register sums
+  const int D = (CAT && !(PACK && a.row == 2)) ? a.drain : 0;
+  auto seg_bar = [&](int j) { return b0 + 8u * (2 * MAXNS + 1 + j); };
+  auto free_bar = [&](int j) { return b0 + 8u * (2 * MAXNS + 3 + j); };
   const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
 
   // valid output rows / columns of this region (receptive-box test, prefetch)
@@ -468,6 +475,10 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
       bar_init(empty_bar(i), 1);
     }
     bar_init(acc_bar, 1);
+    for (int j = 0; j < 2; ++j) {
+      bar_init(seg_bar(j), 1);
+      bar_init(free_bar(j), 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     // the first stages' weights are static: stream them now (their arrive comes with the A boxes)
@@ -557,7 +568,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
   // non-packed epilogue over channels [cb, ce) of the block (TMEM lane quarter = warp % 4).
   // With a wide block and no split-K, warps 0-3 -- idle once the mainloop is issued -- drain the
   // upper half of the channels while warps 4-7 drain the lower half.
-  const bool wide = CAT && BN >= 64 && a.splits == 1 && !(PACK && a.row == 2);
+  const bool wide = CAT && BN >= 64 && a.splits == 1 && !(PACK && a.row == 2) && D == 0;
   auto drain = [&](int cb, int ce) {
     const int m = 32 * (warp & 3) + lane;
     int u, x;
@@ -671,6 +682,29 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
           commit(empty_bar(st));
           continue;
         }
+        if (CAT && D > 0) {
+          // promotion mode: K-block i belongs to segment g = i / D in TMEM block g & 1
+          const int g = i / D, j = g & 1;
+          const bool seg0 = i % D == 0;
+          if (seg0 && g >= 2) {  // block j's previous segment (g - 2) must have been promoted
+            bar_spin(free_bar(j), (uint32_t)(((g >> 1) - 1) & 1));
+            fence_after();
+          }
+          const uint32_t tj = tmem + (uint32_t)(j * 2 * BN), ts = tj + (uint32_t)BN;
+          for (int t = 0; t < taps; ++t) {
+            const uint64_t da = desc_k(ah + t * 128), dl = desc_k(al + t * 128), db = desc_k(bb + t * 2 * BN * 128);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if (kk >= nkk) break;
+              mma(tj, da + 2 * kk, db + 2 * kk, IDESC2, (seg0 && t == 0 && kk == 0) ? 0u : 1u);  // [hi.hi | hi.lo]
+              mma(ts, dl + 2 * kk, db + 2 * kk, IDESC, 1u);                                    // += lo.hi
+            }
+          }
+          commit(empty_bar(st));
+          if (i % D == D - 1 || i == nk - 1) commit(seg_bar(j));
+          if (i == 0) TR(12);
+          continue;
+        }
         for (int t = 0; t < taps; ++t) {
           // row mode: tap t = the A rows shifted by t pixels (any 128-byte row offset is a valid
           // SW128 descriptor start: the swizzle follows the absolute address, scripts/shift_probe.cu)
@@ -727,8 +761,10 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     const int m = 32 * (warp & 3) + lane;  // TMEM lane = region site
     int u, x;
     site_of(a, rr, m, u, x);
-    bar_wait(acc_bar, 0);
-    fence_after();
+    if (D == 0) {  // (promotion mode waits segment by segment: the MMAs need the promoted blocks back)
+      bar_wait(acc_bar, 0);
+      fence_after();
+    }
     if (threadIdx.x == 128) TR(6);
     const int n_main = nk < NA ? nk : NA;
     const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
@@ -786,6 +822,47 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         asm volatile("bar.sync 2, 128;" ::: "memory");
         const int n0 = nblk * BN + c0;
         ssq += emit<8>(a, s, u, x, n0, 1, min(8, a.c_out - n0), o);
+      }
+    } else if (D > 0) {
+      // promotion: every segment's [main | small] block is added into fp32 register sums (RN) while
+      // the MMAs fill the other block -- no tensor-core accumulation chain spans more than a.drain
+      // K-blocks (the accumulate truncates; long chains drift, short ones keep fp32 accuracy)
+      constexpr int BP = BN < 128 ? BN : 128;  // (the BN = 256 kernel never runs promoted: CAT)
+      float sum[BP];
+#pragma unroll
+      for (int c = 0; c < BP; ++c) sum[c] = 0.0f;
+      const int G = (nk + D - 1) / D;
+#pragma unroll 1
+      for (int g = 0; g < G; ++g) {
+        const int j = g & 1;
+        bar_wait(seg_bar(j), (uint32_t)((g >> 1) & 1));
+        fence_after();
+        const uint32_t tb = trow + (uint32_t)(j * 2 * BN);
+#pragma unroll
+        for (int c0 = 0; c0 < BP; c0 += 16) {
+          uint32_t rm[16], rs[16];
+          tmem_ld16_issue(tb + (uint32_t)c0, rm);
+          tmem_ld16_issue(tb + (uint32_t)(BN + c0), rs);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            asm volatile("" : "+r"(rm[e]), "+r"(rs[e]));
+            sum[c0 + e] = __fadd_rn(sum[c0 + e], __fadd_rn(__uint_as_float(rs[e]), __uint_as_float(rm[e])));
+          }
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) bar_arrive(free_bar(j));
+      }
+#pragma unroll
+      for (int c0 = 0; c0 < BP; c0 += 16) {
+        if (a.splits == 1) {
+          const int n0 = nblk * BN + c0;
+          if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), sum + c0);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) P[(c0 + e) * BM + m] = sum[c0 + e];
+        }
       }
     } else
       drain(0, wide ? BN / 2 : BN);
@@ -1543,6 +1620,7 @@ int evc_conv_fused_supported(const evc_conv_geom* g) {
 
 int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits, evc_conv_cfg* cfg) {
   EVC_CHECK_ARG(g && cfg && S > 0, "conv_fused_config: null argument");
+  cfg->drain = 0;
   // stride 1: row mode (halo rows loaded once for all kw taps); else tap mode over RH x RW regions
   cfg->thin = ((g->c_in <= 8 || g->c_out <= 8) && g->c_out <= 32 &&
                (int64_t)g->kh * g->kw * g->c_in * g->c_out * 4 <= 48 * 1024)
@@ -1600,6 +1678,7 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
   if (const char* fs = std::getenv("EVC_FORCE_SPLITS")) sp = std::max(1, std::min(atoi(fs), 16));
   if (cfg->row == 2) sp = 1;  // the packed epilogue sums shifted rows of one CTA's accumulators
   cfg->splits = fz::split_count(L.nkb, sp);
+  if (const char* d = std::getenv("EVC_DRAIN")) cfg->drain = std::max(0, atoi(d));
   return EVC_OK;
 }
 
@@ -1668,13 +1747,22 @@ int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg
   return (int64_t)S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);
 }
 
-int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
+int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const float* in_hwc, int32_t cp,
                    int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
                    const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
                    const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
                    const evc_tensor* act_out, const evc_conv_sparsify* sp, int32_t dense, int32_t S,
                    void* stream) {
-  EVC_CHECK_ARG(g && cfg && in_hwc && wpack && S > 0 && fz::valid_bn(cfg->bn), "conv_fused: null argument");
+  EVC_CHECK_ARG(g && cfg_in && in_hwc && wpack && S > 0 && fz::valid_bn(cfg_in->bn), "conv_fused: null argument");
+  // The dense pass (full-magnitude values, not increments) always runs promoted: K-segments of one
+  // K-block in row mode (kw taps per K-block) and two in tap mode, the packed row mode unpacked
+  // (same weight images), so its accumulation chains stay as short as the fp32 reference needs.
+  evc_conv_cfg cfg_local = *cfg_in;
+  if (dense && !cfg_local.thin && cfg_local.bn <= 128) {
+    if (cfg_local.row == 2) cfg_local.row = 1;
+    if (cfg_local.drain <= 0) cfg_local.drain = cfg_local.row ? 1 : 2;
+  }
+  const evc_conv_cfg* cfg = &cfg_local;
   EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
   EVC_CHECK_ARG(cfg->row ? (g->stride == 1 && cfg->bn <= 128 && g->kw <= 9 &&
                             (cfg->row == 1 || (cfg->bn <= 32 && g->kw <= 3 && cfg->splits == 1)))
@@ -1747,6 +1835,7 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
   a.stage = L.stage;
   a.a_half = L.a_half;
   a.b_bytes = L.b_bytes;
+  a.drain = cfg->bn <= 128 ? std::max(0, cfg->drain) : 0;
   a.cchunks = L.cchunks;
   a.nkb = L.nkb;
   a.splits = fz::split_count(a.nkb, cfg->splits);
@@ -1812,7 +1901,7 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
     EVC_LAUNCH_CHECK("conv_fused_thin");
     return EVC_OK;
   }
-  if (a.splits == 1 && cfg->bn <= 64 && std::getenv("EVC_NO_PERSIST") == nullptr) {
+  if (a.splits == 1 && cfg->bn <= 64 && a.drain == 0 && std::getenv("EVC_NO_PERSIST") == nullptr) {
     // persistent CTAs: one or two per SM (BN = 16 fits two), each walking work items
     const int occ = (cfg->bn <= 16 && 2 * ((int)L.ns * L.stage + 1024 + 256 + 2048) <= fz::SMEM_MAX) ? 2 : 1;
     const int items = S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);

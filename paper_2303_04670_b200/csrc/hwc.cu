@@ -58,4 +58,18 @@ int evc_to_hwc(const evc_tensor* x, float* y, int64_t y_stride, int32_t cp, int3
   return EVC_OK;
 }
 
+int evc_copy_bytes(const void* src, int64_t src_stride, void* dst, int64_t dst_stride, int64_t nbytes, int32_t S,
+                   void* stream) {
+  EVC_CHECK_ARG(src && dst && nbytes >= 0 && S > 0 && src_stride >= nbytes && dst_stride >= nbytes,
+                "copy_bytes: bad argument");
+  if (nbytes == 0) return EVC_OK;
+  const cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dst_stride, src, (size_t)src_stride, (size_t)nbytes, (size_t)S,
+                                          cudaMemcpyDeviceToDevice, as_stream(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("evc: copy_bytes: ") + cudaGetErrorString(e));
+    return EVC_ECUDA;
+  }
+  return EVC_OK;
+}
+
 }  // extern "C"

@@ -54,7 +54,12 @@ __all__ = [
 ]
 
 ACTIVATION_KINDS = ("relu", "sigmoid", "tanh", "leaky_relu")
-NODE_KINDS = ACTIVATION_KINDS + ("conv", "linear", "add", "mul", "concat", "upsample", "maxpool", "sparsify")
+NODE_KINDS = ACTIVATION_KINDS + ("conv", "linear", "add", "mul", "concat", "upsample", "maxpool", "sparsify", "delay")
+# "delay" is this package's recurrent-state extension (not a reference kind):
+# no inputs, attrs {"source": node id, "shape": [C, H, W]}; at frame t it outputs the source's value of
+# frame t - 1 (zeros before the first frame).  Its source edge is not a dataflow edge of the per-frame
+# DAG, so ConvLSTM / ConvGRU loops h_t = cell(x_t, h_{t-1}) need no cycle (oracle/evincr_np.py states
+# the incremental rules: output the pending increment, held += it, pending = the source's increment).
 _ARITY = {"add": 2, "mul": 2}
 DEFAULT_REFRESH_INTERVAL = 64
 
@@ -130,7 +135,12 @@ class ModelSpec:
                 raise GraphError(f"node {n.id!r}: {n.kind} takes {want} inputs, got {len(n.inputs)}")
             if n.kind == "concat" and not n.inputs:
                 raise GraphError(f"node {n.id!r}: concat needs at least one input")
-            if n.kind not in ("add", "mul", "concat") and len(n.inputs) != 1:
+            if n.kind == "delay":
+                if n.inputs:
+                    raise GraphError(f"node {n.id!r}: delay takes no inputs (its source is an attribute)")
+                if n.attrs.get("source") not in by_id or n.attrs.get("source") == n.id:
+                    raise GraphError(f"node {n.id!r}: delay source {n.attrs.get('source')!r} is not another node")
+            elif n.kind not in ("add", "mul", "concat") and len(n.inputs) != 1:
                 raise GraphError(f"node {n.id!r}: {n.kind} takes 1 input, got {len(n.inputs)}")
             deg = 0
             for i in n.inputs:
@@ -161,8 +171,13 @@ class ModelSpec:
 
     def infer_shapes(self) -> dict:
         shapes = {self.input_id: tuple(self.input_shape)}
-        for n in self.topo_order():
+        order = self.topo_order()
+        for n in order:
             shapes[n.id] = _node_out_shape(n, [shapes[i] for i in n.inputs])
+        for n in order:
+            if n.kind == "delay" and shapes[n.attrs["source"]] != shapes[n.id]:
+                raise ShapeError(f"node {n.id!r}: delay shape {shapes[n.id]} differs from its source "
+                                 f"{n.attrs['source']!r} {shapes[n.attrs['source']]}")
         return shapes
 
     def _weight_specs(self, shapes) -> list:
@@ -251,6 +266,11 @@ def _node_out_shape(n: NodeSpec, ins: list) -> tuple:
         if f not in (2, 4):
             raise ShapeError(f"node {n.id!r}: upsample factor must be 2 or 4")
         return (c, h * f, w * f)
+    if kind == "delay":
+        shp = tuple(int(v) for v in n.attrs.get("shape", ()))
+        if len(shp) != 3 or min(shp) < 1:
+            raise ShapeError(f"node {n.id!r}: delay needs a positive shape [C, H, W], got {list(shp)}")
+        return shp
     if kind == "maxpool":
         c, h, w = ins[0]
         wh, ww = (int(v) for v in n.attrs.get("window", [2, 2]))
@@ -528,6 +548,8 @@ class Graph:
             for i in node.spec.inputs:
                 if i in self._consumers:
                     self._consumers[i].append(node.spec.id)
+            if node.kind == "delay":  # reads its source's values at the end of every step
+                self._consumers[node.spec.attrs["source"]].append(node.spec.id)
             node.shadow = None
             node.fused_into = None
             node.sp_fused_by = None  # sparsify evaluated in a producing conv's epilogue
@@ -584,6 +606,12 @@ class Graph:
             elif k == "mul":
                 node.acc = torch.zeros((S, *ish), dtype=torch.float32, device=dev)
                 node.acc2 = torch.zeros((S, *self.shapes[node.spec.inputs[1]]), dtype=torch.float32, device=dev)
+            elif k == "delay":
+                shp = self.shapes[node.spec.id]
+                node.held = torch.zeros((S, *shp), dtype=torch.float32, device=dev)   # current output value
+                node.pend_v = torch.zeros((S, *shp), dtype=torch.float32, device=dev)  # next increment
+                node.pend_f = torch.zeros((S, *grid_shape(shp, tile)), dtype=torch.uint8, device=dev)
+                node.tmp = torch.zeros((S, *shp), dtype=torch.float32, device=dev)
             elif k == "sparsify":
                 node.delta = torch.zeros((S, *ish), dtype=torch.float32, device=dev)
                 node.dlive = torch.zeros((S, *grid_shape(ish, tile)), dtype=torch.uint8, device=dev)
@@ -893,12 +921,40 @@ class Graph:
                 wh, ww = (int(v) for v in ns.attrs.get("window", [2, 2]))
                 prog.append((L.evc_maxpool, (self._desc(ns.inputs[0]), node.acc.data_ptr(), node.acc[0].numel(),
                                              self._desc(nid), wh, ww, int(ns.attrs.get("stride", 2)), S), "maxpool"))
+            elif k == "delay":
+                # output = the pending increment (moved into the slot at the start of the step); held += it
+                prog.insert(0, self._delay_move(node, to_slot=True))
+                prog.insert(0, self._delay_move(node, to_slot=True, flags=True))
+                prog.append((L.evc_integrate, (node.held.data_ptr(), node.held[0].numel(), self._desc(nid), S),
+                             "delay_hold"))
             else:
                 raise GraphError(f"unhandled node kind {k!r}")
         for o in self.output_ids:
             prog.append((L.evc_integrate, (self._y_run[o].data_ptr(), self._y_run[o][0].numel(), self._desc(o), S),
                          "integrate"))
+        for node in self.nodes:  # the next step's delayed increments = this step's source increments
+            if node.kind == "delay":
+                prog.append(self._delay_move(node, to_slot=False))
+                prog.append(self._delay_move(node, to_slot=False, flags=True))
         return prog
+
+    def _delay_move(self, node, to_slot: bool, flags: bool = False):
+        """(fn, args, name) copying a delay node's pending increment into its output slot
+        (to_slot) or its source's increment into the pending buffers (not to_slot)."""
+        nid = node.spec.id
+        sl = self._slots[nid if to_slot else node.spec.attrs["source"]]
+        st = sl.store
+        if flags:
+            gsz = st.GH * st.GW
+            slot_p, slot_s, n = st.flags.data_ptr() + sl.coff * gsz, st.C * gsz, sl.C * gsz
+            buf = node.pend_f
+        else:
+            hw = st.H * st.W
+            slot_p, slot_s, n = st.vals.data_ptr() + 4 * sl.coff * hw, 4 * st.C * hw, 4 * sl.C * hw
+            buf = node.pend_v
+        if to_slot:
+            return self.lib.evc_copy_bytes, (buf.data_ptr(), n, slot_p, slot_s, n, self.S), "delay_out"
+        return self.lib.evc_copy_bytes, (slot_p, slot_s, buf.data_ptr(), n, n, self.S), "delay_pend"
 
     def _concat_part_desc(self, cid, off, c):
         sl = self._slots[cid]
@@ -1025,6 +1081,22 @@ class Graph:
                 if mutate:
                     xp, xs = self._vptr(ns.inputs[0])
                     run(L.evc_copy_dense, xp, xs, node.acc.data_ptr(), node.acc[0].numel(), node.acc[0].numel(), S)
+            elif k == "delay":
+                yp, ys = self._vptr(nid)
+                n = node.held[0].numel()
+                run(L.evc_copy_dense, node.held.data_ptr(), n, yp, ys, n, S)
+        if mutate:  # pending increment of every delay = step_increment(held, source value)
+            for node in self.nodes:
+                if node.kind != "delay":
+                    continue
+                n = node.held[0].numel()
+                sp, ss = self._vptr(node.spec.attrs["source"])
+                run(L.evc_copy_dense, sp, ss, node.tmp.data_ptr(), n, n, S)
+                c, h, w = self.shapes[node.spec.id]
+                gh, gw = grid_shape((c, h, w), self.tile)[1:]
+                pd = _lib.tdesc(node.pend_v.data_ptr(), node.pend_f.data_ptr(), n, c * gh * gw, c, h, w, self.tile.h,
+                                self.tile.w)
+                run(L.evc_diff_mask, node.held.data_ptr(), node.tmp.data_ptr(), n, pd, S)
 
     def _load_input(self, x):
         x = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
@@ -1232,6 +1304,9 @@ class Graph:
                 out[f"{nid}.acc"] = n.acc[session].cpu().numpy()
             if n.kind == "mul":
                 out[f"{nid}.acc2"] = n.acc2[session].cpu().numpy()
+            if n.kind == "delay":
+                out[f"{nid}.held"] = n.held[session].cpu().numpy()
+                out[f"{nid}.pend"] = n.pend_v[session].cpu().numpy()
             if n.kind == "sparsify":
                 out[f"{nid}.delta"] = n.delta[session].cpu().numpy()
                 out[f"{nid}.norm"] = np.asarray([float(self._norm[n.sp_idx, session]),

@@ -203,7 +203,8 @@ typedef struct evc_conv_cfg {
   int32_t drain;  /* > 0: K-blocks per TMEM accumulation segment -- every segment's partial sum is promoted
                      into fp32 registers of the epilogue warps (RN adds) while the MMAs fill the other of
                      two accumulator blocks, so no tensor-core accumulation chain is longer than one
-                     segment (the dense pass always runs this way); 0: one chain per accumulator block */
+                     segment; 0: one chain per accumulator block (the config sets 1 in row mode, 2 in
+                     tap / packed mode; the dense pass never runs with 0) */
 } evc_conv_cfg;
 
 /* 1 if the fused path handles this geometry (pad < kernel, stride <= 8). */

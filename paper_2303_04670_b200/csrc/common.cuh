@@ -181,7 +181,12 @@ __host__ __device__ __forceinline__ int hwc_px(int cp) { return cp < 0 ? -cp : 2
 __device__ __forceinline__ int hwc_head(int cp, int c) {
   return cp > 0 && (cp & 31) == 0 ? ((c >> 5) << 6) + (c & 31) : c;
 }
-__device__ __forceinline__ int hwc_unit(int cp) { return (cp & 31) == 0 ? 32 : cp; }
+// Offset of a channel's tail from its head.  Only defined for the hi/lo layouts (cp > 0): an fp32
+// shadow (cp < 0) has no tails, and a negative offset would address the previous pixel -- trap.
+__device__ __forceinline__ int hwc_unit(int cp) {
+  if (cp <= 0) __trap();
+  return (cp & 31) == 0 ? 32 : cp;
+}
 __device__ __forceinline__ void hwc_store(float* pix, int cp, int c, float x) {
   if (cp < 0) {
     pix[c] = x;

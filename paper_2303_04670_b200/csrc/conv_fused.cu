@@ -149,6 +149,16 @@ __device__ __forceinline__ void tmem_ld8_issue(uint32_t taddr, uint32_t* r) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct Args {
@@ -568,7 +578,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
   // non-packed epilogue over channels [cb, ce) of the block (TMEM lane quarter = warp % 4).
   // With a wide block and no split-K, warps 0-3 -- idle once the mainloop is issued -- drain the
   // upper half of the channels while warps 4-7 drain the lower half.
-  const bool wide = CAT && BN >= 64 && a.splits == 1 && !(PACK && a.row == 2) && D == 0;
+  const bool wide = CAT && BN >= 64 && a.splits == 1 && !(PACK && a.row == 2);
   auto drain = [&](int cb, int ce) {
     const int m = 32 * (warp & 3) + lane;
     int u, x;
@@ -838,14 +848,20 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         bar_wait(seg_bar(j), (uint32_t)((g >> 1) & 1));
         fence_after();
         const uint32_t tb = trow + (uint32_t)(j * 2 * BN);
+        constexpr int LW = BP >= 32 ? 32 : 16;  // columns per tcgen05.ld (latency-bound: few, wide loads)
 #pragma unroll
-        for (int c0 = 0; c0 < BP; c0 += 16) {
-          uint32_t rm[16], rs[16];
-          tmem_ld16_issue(tb + (uint32_t)c0, rm);
-          tmem_ld16_issue(tb + (uint32_t)(BN + c0), rs);
+        for (int c0 = 0; c0 < BP; c0 += LW) {
+          uint32_t rm[LW], rs[LW];
+          if (LW == 32) {
+            tmem_ld32_issue(tb + (uint32_t)c0, rm);
+            tmem_ld32_issue(tb + (uint32_t)(BN + c0), rs);
+          } else {
+            tmem_ld16_issue(tb + (uint32_t)c0, rm);
+            tmem_ld16_issue(tb + (uint32_t)(BN + c0), rs);
+          }
           tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
+          for (int e = 0; e < LW; ++e) {
             asm volatile("" : "+r"(rm[e]), "+r"(rs[e]));
             sum[c0 + e] = __fadd_rn(sum[c0 + e], __fadd_rn(__uint_as_float(rs[e]), __uint_as_float(rm[e])));
           }
@@ -854,8 +870,18 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         __syncwarp();
         if (lane == 0) bar_arrive(free_bar(j));
       }
+      // wide block: the upper half of the channels goes to warps 0-3 through shared memory (the
+      // stages are idle: every MMA and TMA of the CTA has completed), so eight warps emit
+      constexpr int EB = BP / 2;
+      if (wide) {
+        float* X = reinterpret_cast<float*>(smem);  // [EB][BM]
+#pragma unroll
+        for (int c = 0; c < EB; ++c) X[c * BM + m] = sum[EB + c];
+        asm volatile("bar.sync 5, 256;" ::: "memory");
+      }
 #pragma unroll
       for (int c0 = 0; c0 < BP; c0 += 16) {
+        if (wide && c0 >= EB) break;
         if (a.splits == 1) {
           const int n0 = nblk * BN + c0;
           if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), sum + c0);
@@ -868,9 +894,26 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
       drain(0, wide ? BN / 2 : BN);
   }
   if (wide && warp < 4) {
-    bar_wait(acc_bar, 0);
-    fence_after();
-    drain(BN / 2, BN);
+    if (D > 0) {  // promoted sums of channels [BN/2, BN) handed over by warps 4-7
+      constexpr int EB = (BN < 128 ? BN : 128) / 2;
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      const int m = 32 * (warp & 3) + lane;
+      int u, x;
+      site_of(a, rr, m, u, x);
+      const float* X = reinterpret_cast<const float*>(smem);
+#pragma unroll 1
+      for (int c0 = 0; c0 < EB; c0 += 16) {
+        float vals[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) vals[e] = X[(c0 + e) * BM + m];
+        const int n0 = nblk * BN + EB + c0;
+        if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
+      }
+    } else {
+      bar_wait(acc_bar, 0);
+      fence_after();
+      drain(BN / 2, BN);
+    }
   }
   if (threadIdx.x == 128) TR(7);
   if (a.splits > 1) {
@@ -974,7 +1017,9 @@ __host__ __device__ constexpr int persist_epi_warps() { return BN >= 32 ? 8 : 4;
 template <int BN>
 __host__ __device__ constexpr int persist_threads() { return (4 + persist_epi_warps<BN>()) * 32; }
 
-template <int BN>
+// PK: packed row mode (a.row == 2) -- a separate instantiation, so each epilogue gets its own
+// register allocation
+template <int BN, bool PK>
 __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_conv_persist(const __grid_constant__ CUtensorMap tmap,
                                                                               const __grid_constant__ Args a) {
   constexpr int BUF = BN <= 32 ? 6 * BN : 3 * BN;  // packed: 3 taps x [A.B_hi | A.B_lo]; CAT: [hi.hi | hi.lo | lo.hi]
@@ -990,7 +1035,10 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
   const int NS = a.ns, STAGE = a.stage, nk = a.nkb;
   const uint32_t A_HALF = (uint32_t)a.a_half, B_BYTES = (uint32_t)a.b_bytes;
   const uint32_t A_TX = a.row ? (uint32_t)(BM + a.kw - 1) * 128u : (uint32_t)BM * 128u;
-  const bool packed = a.row == 2;
+  constexpr bool packed = PK;
+  // promotion: K-blocks per TMEM accumulation segment, segments per item
+  // (balanced: GS = round(nk / drain) segments of DS K-blocks; a short item stays one segment)
+  const int GS = a.drain > 0 ? max(1, (nk + a.drain / 2) / a.drain) : 1, DS = (nk + GS - 1) / GS;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -1063,16 +1111,23 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
       __syncwarp();
     }
   } else if (warp == 1) {  // --------------------------------------------------- MMA issuer
-    int g = 0, li = 0;
+    // TMEM buffer use = one accumulation segment of DS K-blocks (the whole item when a.drain == 0);
+    // segment gs fills buffer gs & 1 while the epilogue promotes segment gs - 1 into registers
+    int g = 0, gs = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int reg = item / nb, s = reg / R, rr = reg % R;
       if (!region_live_warp(a, s, rr)) continue;
-      const int ab = li & 1;
       if (lane == 0) {
-        if (li >= 2) bar_spin(tempty_bar(ab), ((li >> 1) & 1) ^ 1);
-        fence_after();
-        const uint32_t tb = tmem + (uint32_t)(ab * BUF);
+        uint32_t tb = tmem;
+        int ab = 0;
         for (int kb = 0; kb < nk; ++kb, ++g) {
+          const bool seg0 = kb % DS == 0;
+          if (seg0) {
+            ab = gs & 1;
+            if (gs >= 2) bar_spin(tempty_bar(ab), ((gs >> 1) & 1) ^ 1);
+            fence_after();
+            tb = tmem + (uint32_t)(ab * BUF);
+          }
           const int st = g % NS;
           bar_spin(full_bar(st), (g / NS) & 1);
           fence_after();
@@ -1084,14 +1139,14 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (kk >= nkk) break;
-              mma(tb, dl + 2 * kk, db + 2 * kk, idp, (kb || kk) ? 1u : 0u);
+              mma(tb, dl + 2 * kk, db + 2 * kk, idp, (!seg0 || kk) ? 1u : 0u);
               mma(tb, dh + 2 * kk, db + 2 * kk, idp, 1u);
             }
           } else {
             const int taps = a.row ? a.kw : 1;
             for (int t = 0; t < taps; ++t) {
               const uint64_t da = desc_k(ah + t * 128), dl = desc_k(al + t * 128), db = desc_k(bb + t * 2 * BN * 128);
-              const bool first = kb == 0 && t == 0;
+              const bool first = seg0 && t == 0;
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
                 if (kk >= nkk) break;
@@ -1101,12 +1156,14 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
             }
           }
           commit(empty_bar(st));
+          if (kb % DS == DS - 1 || kb == nk - 1) {
+            commit(tfull_bar(ab));
+            ++gs;
+          }
         }
-        commit(tfull_bar(ab));
       } else {
         g += nk;
       }
-      ++li;
       __syncwarp();
     }
   } else if (warp < 4) {  // ---------------------------------------------------- flags + meter
@@ -1124,7 +1181,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
     const int half = NH > 1 ? (warp - 4) >> 2 : 0;  // channel half of the block (NH = 2) or 0
     // named barrier of this half's four warps: id 2 (half 0) or 4 (half 1)
     const int Qs = R * nb;
-    int li = 0;
+    int gs = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int nblk = item % nb, reg = item / nb, s = reg / R, rr = reg % R;
       const int64_t rs_idx = (int64_t)reg * nb + nblk;
@@ -1147,101 +1204,124 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
             }
         }
       } else {
-        const int ab = li & 1;
-        bar_wait(tfull_bar(ab), (li >> 1) & 1);
-        fence_after();
-        const uint32_t trow = tmem + (uint32_t)(ab * BUF) + ((uint32_t)(32 * q4) << 16);
         if (packed) {
+          // per segment and 8-channel chunk: v_s = A.B_lo + A.B_hi of tap s, out[m] = sum_s v_s[m + s]
+          // (shifts by s rows = shuffles inside the warp, the next warp's first rows through shared
+          // memory), accumulated over the segments
           const int KW = a.kw;
-          float o_all[BN <= 32 ? BN : 8];
-          constexpr int CH = (BN <= 32 ? BN : 8) / NH;  // channels of this half
+          constexpr int PB = BN <= 32 ? BN : 8;  // (packed mode only runs with BN <= 32)
+          constexpr int CH = PB / NH < 8 ? 8 : PB / NH;  // channels of this half (BN = 64: never packed)
+          float O[CH];
+#pragma unroll 1
+          for (int sg = 0; sg < GS; ++sg, ++gs) {
+            const int ab = gs & 1;
+            bar_wait(tfull_bar(ab), (gs >> 1) & 1);
+            fence_after();
+            const uint32_t trow = tmem + (uint32_t)(ab * BUF) + ((uint32_t)(32 * q4) << 16);
 #pragma unroll
-          for (int cc = 0; cc < CH; cc += 8) {
-            const int c0 = half * CH + cc;
-            float v[3][8];
-            {
-              uint32_t r4[3][2][8];
+            for (int cc = 0; cc < CH; cc += 8) {
+              const int c0 = half * CH + cc;
+              float v[3][8];
+              {
+                uint32_t r4[3][2][8];
 #pragma unroll
-              for (int s2 = 0; s2 < 3; ++s2)
-                if (s2 < KW) {
-                  const uint32_t cb = (uint32_t)(s2 * 2 * BN + c0);
-                  tmem_ld8_issue(trow + cb + BN, r4[s2][0]);
-                  tmem_ld8_issue(trow + cb, r4[s2][1]);
+                for (int s2 = 0; s2 < 3; ++s2)
+                  if (s2 < KW) {
+                    const uint32_t cb = (uint32_t)(s2 * 2 * BN + c0);
+                    tmem_ld8_issue(trow + cb + BN, r4[s2][0]);
+                    tmem_ld8_issue(trow + cb, r4[s2][1]);
+                  }
+                tmem_wait_ld();
+#pragma unroll
+                for (int s2 = 0; s2 < 3; ++s2)
+#pragma unroll
+                  for (int j = 0; j < 2; ++j)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) asm volatile("" : "+r"(r4[s2][j][e]));
+#pragma unroll
+                for (int s2 = 0; s2 < 3; ++s2)
+#pragma unroll
+                  for (int e = 0; e < 8; ++e)
+                    v[s2][e] = s2 < KW ? __fadd_rn(__uint_as_float(r4[s2][0][e]), __uint_as_float(r4[s2][1][e])) : 0.0f;
+              }
+              if (cc + 8 >= CH) {  // this thread's last TMEM read of the buffer
+                fence_before();
+                bar_arrive(tempty_bar(ab));
+              }
+#pragma unroll
+              for (int s2 = 1; s2 < 3; ++s2)
+                if (s2 < KW && lane < s2) {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) s_xch[half][q4][s2][lane][e] = v[s2][e];
                 }
-              tmem_wait_ld();
+              if (half == 0)
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+              else
+                asm volatile("bar.sync 4, 128;" ::: "memory");
+              float o[8];
 #pragma unroll
-              for (int s2 = 0; s2 < 3; ++s2)
+              for (int e = 0; e < 8; ++e) o[e] = v[0][e];
 #pragma unroll
-                for (int j = 0; j < 2; ++j)
+              for (int s2 = 1; s2 < 3; ++s2) {
+                if (s2 >= KW) break;
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) asm volatile("" : "+r"(r4[s2][j][e]));
-#pragma unroll
-              for (int s2 = 0; s2 < 3; ++s2)
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  v[s2][e] = s2 < KW ? __fadd_rn(__uint_as_float(r4[s2][0][e]), __uint_as_float(r4[s2][1][e])) : 0.0f;
-            }
-#pragma unroll
-            for (int s2 = 1; s2 < 3; ++s2)
-              if (s2 < KW && lane < s2) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) s_xch[half][q4][s2][lane][e] = v[s2][e];
+                for (int e = 0; e < 8; ++e) {
+                  float t = __shfl_down_sync(0xffffffffu, v[s2][e], s2);
+                  if (lane >= 32 - s2) t = q4 < 3 ? s_xch[half][q4 + 1][s2][lane + s2 - 32][e] : 0.0f;
+                  o[e] = __fadd_rn(o[e], t);
+                }
               }
-            if (half == 0)
-              asm volatile("bar.sync 2, 128;" ::: "memory");
-            else
-              asm volatile("bar.sync 4, 128;" ::: "memory");
+              if (half == 0)
+                asm volatile("bar.sync 2, 128;" ::: "memory");
+              else
+                asm volatile("bar.sync 4, 128;" ::: "memory");
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o_all[(c0 + e) % (BN <= 32 ? BN : 8)] = v[0][e];
-#pragma unroll
-            for (int s2 = 1; s2 < 3; ++s2) {
-              if (s2 >= KW) break;
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                float t = __shfl_down_sync(0xffffffffu, v[s2][e], s2);
-                if (lane >= 32 - s2) t = q4 < 3 ? s_xch[half][q4 + 1][s2][lane + s2 - 32][e] : 0.0f;
-                o_all[(c0 + e) % (BN <= 32 ? BN : 8)] = __fadd_rn(o_all[(c0 + e) % (BN <= 32 ? BN : 8)], t);
-              }
+              for (int e = 0; e < 8; ++e) O[cc + e] = sg ? __fadd_rn(O[cc + e], o[e]) : o[e];
             }
-            if (half == 0)
-              asm volatile("bar.sync 2, 128;" ::: "memory");
-            else
-              asm volatile("bar.sync 4, 128;" ::: "memory");
           }
-          // TMEM buffer free: the next item's MMAs may overwrite it while we store
-          fence_before();
-          bar_arrive(tempty_bar(ab));
           const int n0 = nblk * BN;
 #pragma unroll
           for (int cc = 0; cc < CH; cc += 8) {
             const int c0 = half * CH + cc;
-            ssq += emit<8>(a, s, u, x, n0 + c0, 1, min(8, a.c_out - n0 - c0), o_all + c0);
+            ssq += emit<8>(a, s, u, x, n0 + c0, 1, min(8, a.c_out - n0 - c0), O + cc);
           }
         } else {
+          constexpr int CB = BN / NH;  // channels of this half
+          float acc[CB];               // (lo.hi + hi.lo) + hi.hi, summed over the segments
 #pragma unroll 1
-          for (int c0 = half * (BN / NH); c0 < (half + 1) * (BN / NH); c0 += 16) {
-            uint32_t r[3][16];
-            tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), r[0]);  // lo . hi
-            tmem_ld16_issue(trow + (uint32_t)(BN + c0), r[1]);      // hi . lo
-            tmem_ld16_issue(trow + (uint32_t)c0, r[2]);             // hi . hi
-            tmem_wait_ld();
+          for (int sg = 0; sg < GS; ++sg, ++gs) {
+            const int ab = gs & 1;
+            bar_wait(tfull_bar(ab), (gs >> 1) & 1);
+            fence_after();
+            const uint32_t trow = tmem + (uint32_t)(ab * BUF) + ((uint32_t)(32 * q4) << 16);
 #pragma unroll
-            for (int j = 0; j < 3; ++j)
+            for (int cc = 0; cc < CB; cc += 16) {
+              const int c0 = half * CB + cc;
+              uint32_t r[3][16];
+              tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), r[0]);  // lo . hi
+              tmem_ld16_issue(trow + (uint32_t)(BN + c0), r[1]);      // hi . lo
+              tmem_ld16_issue(trow + (uint32_t)c0, r[2]);             // hi . hi
+              tmem_wait_ld();
 #pragma unroll
-              for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
-            float vals[16];
+              for (int j = 0; j < 3; ++j)
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              vals[e] = __fadd_rn(__fadd_rn(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])), __uint_as_float(r[2][e]));
-            if (c0 + 16 >= (half + 1) * (BN / NH)) {  // this thread's last TMEM read of the buffer
-              fence_before();
-              bar_arrive(tempty_bar(ab));
+                for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
+#pragma unroll
+              for (int e = 0; e < 16; ++e) {
+                const float v = __fadd_rn(__fadd_rn(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])),
+                                          __uint_as_float(r[2][e]));
+                acc[cc + e] = sg ? __fadd_rn(acc[cc + e], v) : v;
+              }
             }
-            const int n0 = nblk * BN + c0;
-            ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
+            fence_before();
+            bar_arrive(tempty_bar(ab));
+          }
+#pragma unroll
+          for (int cc = 0; cc < CB; cc += 16) {
+            const int n0 = nblk * BN + half * CB + cc;
+            ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), acc + cc);
           }
         }
-        ++li;
       }
       // per-item bookkeeping: region state, sum of squares of the fused sparsify
       if (a.sp_part) {
@@ -1510,20 +1590,26 @@ static cudaError_t launch(const CUtensorMap& m, const Args& a, cudaStream_t st) 
 constexpr int SMEM_MAX = 227 * 1024;
 constexpr int STAGE_BUDGET = SMEM_MAX - 1024 - 256 - 2048;
 
-template <int BN>
-static int attr_persist() {
+template <int BN, bool PK>
+static int attr_persist1() {
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, k_conv_persist<BN>) != cudaSuccess) return 1;
-  return cudaFuncSetAttribute(k_conv_persist<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  if (cudaFuncGetAttributes(&fa, k_conv_persist<BN, PK>) != cudaSuccess) return 1;
+  return cudaFuncSetAttribute(k_conv_persist<BN, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               SMEM_MAX - (int)fa.sharedSizeBytes) == cudaSuccess
              ? 0
              : 1;
 }
+template <int BN>
+static int attr_persist() {
+  return attr_persist1<BN, false>() | (BN <= 32 ? attr_persist1<BN, true>() : 0);
+}
 
 template <int BN>
 static cudaError_t launch_persist(const CUtensorMap& m, const Args& a, int grid, cudaStream_t st) {
-  return launch_pdl(k_conv_persist<BN>, dim3((unsigned)grid), dim3(persist_threads<BN>()), (size_t)a.ns * a.stage + 1024 + 256, st,
-                    m, a);
+  const size_t smem = (size_t)a.ns * a.stage + 1024 + 256;
+  if (BN <= 32 && a.row == 2)
+    return launch_pdl(k_conv_persist<BN, (BN <= 32)>, dim3((unsigned)grid), dim3(persist_threads<BN>()), smem, st, m, a);
+  return launch_pdl(k_conv_persist<BN, false>, dim3((unsigned)grid), dim3(persist_threads<BN>()), smem, st, m, a);
 }
 
 template <int BN>
@@ -1678,6 +1764,14 @@ int evc_conv_fused_config(const evc_conv_geom* g, int32_t S, int32_t max_splits,
   if (const char* fs = std::getenv("EVC_FORCE_SPLITS")) sp = std::max(1, std::min(atoi(fs), 16));
   if (cfg->row == 2) sp = 1;  // the packed epilogue sums shifted rows of one CTA's accumulators
   cfg->splits = fz::split_count(L.nkb, sp);
+  // Promotion: the TMEM partial sums are added into fp32 registers every K-block (row mode: kw taps per
+  // K-block) or every two (tap mode, packed row mode).  The tensor core's accumulate truncates, and an
+  // unpromoted chain drifts with its length (dec0 unsplit: 576 K8 steps, ~1e-5 relative per layer --
+  // enough to break 1e-4 at the network output); segments of <= 12 K8 steps keep fp32-level accuracy.
+  // Segment lengths (K8 steps per chain): one-shot tap mode 8 K-blocks (32), row mode 2 (24); the
+  // persistent kernel promotes long items only -- row mode every 3 K-blocks (36), tap / packed mode
+  // every 8 (32; enc1 / dec3 items are shorter and run unpromoted).  The dense pass uses 1 / 2.
+  if (cfg->bn <= 128) cfg->drain = cfg->row == 1 ? ((cfg->bn > 64 || cfg->splits > 1) ? 2 : 3) : 8;
   if (const char* d = std::getenv("EVC_DRAIN")) cfg->drain = std::max(0, atoi(d));
   return EVC_OK;
 }
@@ -1754,14 +1848,10 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
                    const evc_tensor* act_out, const evc_conv_sparsify* sp, int32_t dense, int32_t S,
                    void* stream) {
   EVC_CHECK_ARG(g && cfg_in && in_hwc && wpack && S > 0 && fz::valid_bn(cfg_in->bn), "conv_fused: null argument");
-  // The dense pass (full-magnitude values, not increments) always runs promoted: K-segments of one
-  // K-block in row mode (kw taps per K-block) and two in tap mode, the packed row mode unpacked
-  // (same weight images), so its accumulation chains stay as short as the fp32 reference needs.
+  // The dense pass (full-magnitude values, not increments) always runs promoted (K-segments of one
+  // K-block in row mode, two otherwise), so its accumulation chains stay as short as fp32 needs.
   evc_conv_cfg cfg_local = *cfg_in;
-  if (dense && !cfg_local.thin && cfg_local.bn <= 128) {
-    if (cfg_local.row == 2) cfg_local.row = 1;
-    if (cfg_local.drain <= 0) cfg_local.drain = cfg_local.row ? 1 : 2;
-  }
+  if (dense && !cfg_local.thin && cfg_local.bn <= 128) cfg_local.drain = cfg_local.row == 1 ? 1 : 2;
   const evc_conv_cfg* cfg = &cfg_local;
   EVC_CHECK_ARG(evc_conv_fused_supported(g), "conv_fused: unsupported geometry");
   EVC_CHECK_ARG(cfg->row ? (g->stride == 1 && cfg->bn <= 128 && g->kw <= 9 &&
@@ -1901,7 +1991,7 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
     EVC_LAUNCH_CHECK("conv_fused_thin");
     return EVC_OK;
   }
-  if (a.splits == 1 && cfg->bn <= 64 && a.drain == 0 && std::getenv("EVC_NO_PERSIST") == nullptr) {
+  if (a.splits == 1 && cfg->bn <= 64 && std::getenv("EVC_NO_PERSIST") == nullptr) {
     // persistent CTAs: one or two per SM (BN = 16 fits two), each walking work items
     const int occ = (cfg->bn <= 16 && 2 * ((int)L.ns * L.stage + 1024 + 256 + 2048) <= fz::SMEM_MAX) ? 2 : 1;
     const int items = S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);

@@ -133,7 +133,7 @@ class EventPipeline:
                      torch.zeros(S * ring, dtype=torch.int16, device=dev), torch.zeros(S * ring, dtype=torch.int8, device=dev))
         self.enc = [torch.zeros((S, c, self.H, self.W), dtype=torch.float32, device=dev) for _ in range(2)]
         self.meta = 7 * S  # int64 words: desc (3 per session) + windows (4 per session)
-        nbytes = 8 * self.meta + S * max_new * 13
+        nbytes = 8 * self.meta + S * self.max_new * 13
         self.host = [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
         self.dev_stage = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
         self.copy = torch.cuda.Stream(device=dev)

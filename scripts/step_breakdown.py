@@ -24,7 +24,7 @@ def main():
     S = args.sessions
     spec = configs.evflownet_spec(tp=0.0)
     g = evc.build(spec, evc.WeightManifest.random_tensors(spec, 0), refresh_interval=0, sessions=S, cuda_graph=False)
-    xs = bench.make_inputs(evc, 4 + args.steps, list(range(S)), "cuda")
+    xs = bench.make_inputs(lambda sd: bench.c1_frames(evc, sd, 4 + args.steps), list(range(S)))
     g.dense_pass(xs[0] if S > 1 else xs[0][0])
     for i in range(1, 3):
         g.step_from_encodings(xs[i - 1], xs[i])

@@ -1,0 +1,121 @@
+"""Parity of the BASELINE.json configurations over chained increments.
+
+Every case runs the device Graph and the oracle (oracle/evincr_np.py, pinned to the reference by
+tests/golden) side by side on the same seeded event streams and checks, every step:
+
+* the input increment mask bit-exact (step_increment, events.py:295-302);
+* the integrated output within 1e-4 * max(1, max|ref|);
+* the output increment mask -- value-derived masks may flip only at rounding zeros: flips are
+  counted, printed and bounded, and every flipped tile's values stay <= 1e-6;
+* the per-node FLOP meters (exact where no upstream mask flipped, <= 1e-4 * dense otherwise);
+* for t_p > 0, every sparsify node's (norm_ema, k) tracked -- never re-pinned -- against the
+  oracle's (sparsify.py:54-78);
+
+and every 16 steps the drift of the integrated output against a GPU dense recompute
+(graph.py:646-654).  Each case prints one PARITY line (collected into profiles/).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2303_04670_b200 as evc
+from paper_2303_04670_b200 import configs
+from oracle import evincr_np as O
+from evc_testutil import max_err
+
+pytestmark = pytest.mark.gpu
+
+
+def np_(t):
+    return t.detach().cpu().numpy()
+
+
+def run_parity(name, spec, weights, xs, drift_every=16, flip_budget=8, flip_value_tol=1e-6):
+    g = evc.build(spec, weights, refresh_interval=0)
+    og = O.OracleGraph(spec.to_dict(), weights, refresh_interval=0)
+    e0 = max_err(np_(g.dense_pass(xs[0])), og.dense_pass(np_(xs[0])))
+    worst, flips, perf_rel, exact, nodes, drift, norm_rel, dens = e0, 0, 0.0, 0, 0, 0.0, 0.0, []
+    sp_ids = [n.spec.id for n in g.nodes if n.kind == "sparsify" and n.tp > 0]
+    th, tw = spec.tile.h, spec.tile.w
+    for i in range(1, len(xs)):
+        rv, rf = O.step_increment(np_(xs[i - 1]), np_(xs[i]), th, tw)
+        x_up = evc.step_increment(xs[i - 1], xs[i], spec.tile)
+        assert np.array_equal(x_up.mask.numpy(), rf), ("input mask", i)
+        dens.append(float((rv != 0).mean()))
+        yup, y, rep = g.incr_step(x_up)
+        (ov, of), oy, orep = og.incr_step(rv, rf)
+        diff = yup.mask.numpy() != of
+        flips += int(diff.sum())
+        if diff.any() and flip_value_tol is not None:
+            px = O.flags_to_pixels(diff, th, tw, ov.shape[1], ov.shape[2])
+            assert np.abs(np.where(px, np_(yup.values) - ov, 0)).max() <= flip_value_tol, ("flipped tile values", i)
+        for k, (p, d) in rep.per_node.items():
+            rp = orep["per_node"][k][0]
+            nodes += 1
+            exact += int(p == rp)
+            perf_rel = max(perf_rel, abs(p - rp) / max(1, d))
+        worst = max(worst, max_err(np_(y), oy))
+        if sp_ids:
+            fg, fo = g.state_fingerprint(), og.state_fingerprint()
+            for sid in sp_ids:
+                a, b = np.asarray(fg[f"{sid}.norm"], np.float64), np.asarray(fo[f"{sid}.norm"], np.float64)
+                norm_rel = max(norm_rel, float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30))))
+        if i % drift_every == 0 or i == len(xs) - 1:
+            d = g.dense_oracle(xs[i])
+            scale = max(1.0, float(d.abs().max()))
+            drift = max(drift, g.drift(d) / scale)
+    print(f"PARITY {name}: increments {len(xs) - 1}, density {np.mean(dens):.4f}, dense err {e0:.2e}, "
+          f"max err {worst:.2e}, output-mask flips {flips}, exact meters {exact}/{nodes}, max meter rel "
+          f"{perf_rel:.2e}, max drift/scale {drift:.2e}" + (f", max norm/k rel {norm_rel:.2e}" if sp_ids else ""))
+    assert worst <= 1e-4, worst
+    assert drift <= 1e-4, drift
+    assert perf_rel <= 1e-4, perf_rel
+    assert flips <= flip_budget, flips
+    if sp_ids:
+        assert norm_rel <= 1e-5, norm_rel
+    return dict(worst=worst, flips=flips, exact=exact, nodes=nodes, drift=drift)
+
+
+def c2_frames(n, seed, rate):
+    stream = evc.generate_events(seed=seed, duration_us=50_000 + 1_000 * (n + 1), rate_hz=rate, n_objects=8,
+                                 sensor_size=(260, 346))
+    return [torch.nn.functional.pad(evc.encode(evc.slice_window(stream, 50_000 + 1_000 * i, 50_000),
+                                               evc.parse_encoder("voxel:5")), (0, 6, 0, 4)).contiguous()
+            for i in range(n + 1)]
+
+
+def c1_frames(n, seed=0):
+    stream = evc.generate_events(seed=seed, duration_us=50_000 + 1_000 * (n + 1), rate_hz=1.0e6, n_objects=8,
+                                 sensor_size=(256, 256))
+    return [torch.cat([evc.encode(w, evc.EncoderKind("count")), evc.encode(w, evc.EncoderKind("timestamp"))])
+            for w in (evc.slice_window(stream, 50_000 + 1_000 * i, 50_000) for i in range(n + 1))]
+
+
+@pytest.mark.parametrize("density,rate,n", [("1%", 2.0e5, 64), ("3%", 2.0e6, 32), ("5%", 3.8e6, 64)])
+def test_c2_unet_voxel_chained_increments(density, rate, n):
+    spec = configs.unet_e2depth_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    run_parity(f"C2 UNet voxel 264x352 ~{density}", spec, weights, c2_frames(n, 5, rate))
+
+
+def test_c3_resnet18_64_increments():
+    spec = configs.resnet18_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    stream = evc.generate_events(seed=2, duration_us=50_000 + 1_000 * 65, rate_hz=2e5, n_objects=8,
+                                 sensor_size=(180, 240))
+    xs = [evc.encode(evc.slice_window(stream, 50_000 + 1_000 * i, 50_000), evc.EncoderKind("count"))
+          for i in range(65)]
+    run_parity("C3 ResNet-18 2x180x240", spec, weights, xs)
+
+
+@pytest.mark.parametrize("tp", [1e-5, 1e-4, 1e-3])
+def test_c1_threshold_tracking(tp):
+    """C1 with t_p > 0 (SURVEY.md 7 hard part 9): the sparsify thresholds k follow each node's norm
+    EMA on the device and on the oracle independently (nothing re-pinned)."""
+    spec = configs.evflownet_spec(tp=tp)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    # an element within rounding of its threshold k may be kept by one side and deferred to the residual
+    # by the other (the device norm is an f64 sum of squares, the reference's an f32 np.linalg.norm):
+    # such flips are counted and bounded; the integrated output and k stay within tolerance
+    run_parity(f"C1 EV-FlowNet t_p={tp:g}", spec, weights, c1_frames(16), flip_budget=64, flip_value_tol=None)

@@ -450,10 +450,12 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
   auto tma_bar = [&](int i) { return b0 + 8u * i; };
   auto empty_bar = [&](int i) { return b0 + 8u * (MAXNS + i); };
   const uint32_t acc_bar = b0 + 8u * (2 * MAXNS);
-  // promotion mode: segment g of a.drain K-blocks accumulates into TMEM block g & 1 = [main | small]
-  // (2 BN columns: hi.hi, then hi.lo + lo.hi); seg_bar[j] = block j's segment complete, free_bar[j] =
-  // the epilogue warps have added it to their fp32 register sums
-  const int D = (CAT && !(PACK && a.row == 2)) ? a.drain : 0;
+  // promotion mode: segment g of a.drain K-blocks accumulates hi.hi into TMEM block g & 1 (BN columns
+  // at j * BN); the small terms hi.lo + lo.hi go to one block at 2 BN for the whole K range (their
+  // magnitude is 2^-11 of the main term, so their chain length is harmless).  Three N = BN MMAs per K8
+  // step, none of them partially overlapping another's accumulator.  seg_bar[j] = block j's segment
+  // complete, free_bar[j] = the epilogue warps have added it to their fp32 register sums
+  const int D = (CAT && !(PACK && a.row == 2)) ? max(1, a.drain) : 0;
   auto seg_bar = [&](int j) { return b0 + 8u * (2 * MAXNS + 1 + j); };
   auto free_bar = [&](int j) { return b0 + 8u * (2 * MAXNS + 3 + j); };
   const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
@@ -700,14 +702,17 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
             bar_spin(free_bar(j), (uint32_t)(((g >> 1) - 1) & 1));
             fence_after();
           }
-          const uint32_t tj = tmem + (uint32_t)(j * 2 * BN), ts = tj + (uint32_t)BN;
+          const uint32_t tj = tmem + (uint32_t)(j * BN), ts = tmem + (uint32_t)(2 * BN);
           for (int t = 0; t < taps; ++t) {
-            const uint64_t da = desc_k(ah + t * 128), dl = desc_k(al + t * 128), db = desc_k(bb + t * 2 * BN * 128);
+            const uint32_t bh = bb + t * 2 * BN * 128;
+            const uint64_t da = desc_k(ah + t * 128), dl = desc_k(al + t * 128), dbh = desc_k(bh),
+                           dbl = desc_k(bh + BN * 128);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (kk >= nkk) break;
-              mma(tj, da + 2 * kk, db + 2 * kk, IDESC2, (seg0 && t == 0 && kk == 0) ? 0u : 1u);  // [hi.hi | hi.lo]
-              mma(ts, dl + 2 * kk, db + 2 * kk, IDESC, 1u);                                    // += lo.hi
+              mma(tj, da + 2 * kk, dbh + 2 * kk, IDESC, (seg0 && t == 0 && kk == 0) ? 0u : 1u);  // hi.hi
+              mma(ts, da + 2 * kk, dbl + 2 * kk, IDESC, (i == 0 && t == 0 && kk == 0) ? 0u : 1u);  // hi.lo
+              mma(ts, dl + 2 * kk, dbh + 2 * kk, IDESC, 1u);                                      // lo.hi
             }
           }
           commit(empty_bar(st));
@@ -839,80 +844,86 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
       // K-blocks (the accumulate truncates; long chains drift, short ones keep fp32 accuracy)
       constexpr int BP = BN < 128 ? BN : 128;  // (the BN = 256 kernel never runs promoted: CAT)
       float sum[BP];
+      const int G = (nk + D - 1) / D;
 #pragma unroll
       for (int c = 0; c < BP; ++c) sum[c] = 0.0f;
-      const int G = (nk + D - 1) / D;
 #pragma unroll 1
       for (int g = 0; g < G; ++g) {
         const int j = g & 1;
         bar_wait(seg_bar(j), (uint32_t)((g >> 1) & 1));
         fence_after();
-        const uint32_t tb = trow + (uint32_t)(j * 2 * BN);
-        constexpr int LW = BP >= 32 ? 32 : 16;  // columns per tcgen05.ld (latency-bound: few, wide loads)
+        const uint32_t tb = trow + (uint32_t)(j * BN);
+        constexpr int LW = BP >= 32 ? 32 : 16;  // columns per wait (latency-bound: wide loads)
 #pragma unroll
         for (int c0 = 0; c0 < BP; c0 += LW) {
-          uint32_t rm[LW], rs[LW];
-          if (LW == 32) {
-            tmem_ld32_issue(tb + (uint32_t)c0, rm);
-            tmem_ld32_issue(tb + (uint32_t)(BN + c0), rs);
-          } else {
-            tmem_ld16_issue(tb + (uint32_t)c0, rm);
-            tmem_ld16_issue(tb + (uint32_t)(BN + c0), rs);
+          uint32_t rm[LW];
+#pragma unroll
+          for (int q = 0; q < LW; q += 16) {
+            if (LW >= 32 && q % 32 == 0) tmem_ld32_issue(tb + (uint32_t)(c0 + q), rm + q);
+            else if (LW < 32) tmem_ld16_issue(tb + (uint32_t)(c0 + q), rm + q);
           }
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < LW; ++e) {
-            asm volatile("" : "+r"(rm[e]), "+r"(rs[e]));
-            sum[c0 + e] = __fadd_rn(sum[c0 + e], __fadd_rn(__uint_as_float(rs[e]), __uint_as_float(rm[e])));
+            asm volatile("" : "+r"(rm[e]));
+            sum[c0 + e] = g ? __fadd_rn(sum[c0 + e], __uint_as_float(rm[e])) : __uint_as_float(rm[e]);
           }
         }
         fence_before();
         __syncwarp();
         if (lane == 0) bar_arrive(free_bar(j));
       }
-      // wide block: the upper half of the channels goes to warps 0-3 through shared memory (the
-      // stages are idle: every MMA and TMA of the CTA has completed), so eight warps emit
-      constexpr int EB = BP / 2;
-      if (wide) {
-        float* X = reinterpret_cast<float*>(smem);  // [EB][BM]
+      // the small terms (complete with the last segment)
 #pragma unroll
-        for (int c = 0; c < EB; ++c) X[c * BM + m] = sum[EB + c];
-        asm volatile("bar.sync 5, 256;" ::: "memory");
-      }
-#pragma unroll
-      for (int c0 = 0; c0 < BP; c0 += 16) {
-        if (wide && c0 >= EB) break;
-        if (a.splits == 1) {
-          const int n0 = nblk * BN + c0;
-          if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), sum + c0);
+      for (int c0 = 0; c0 < BP; c0 += 32) {
+        uint32_t rs[32];
+        if (BP >= 32) {
+          tmem_ld32_issue(trow + (uint32_t)(2 * BN + c0), rs);
         } else {
+          tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), rs);
+        }
+        tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) P[(c0 + e) * BM + m] = sum[c0 + e];
+        for (int e = 0; e < (BP >= 32 ? 32 : 16); ++e) {
+          asm volatile("" : "+r"(rs[e]));
+          sum[c0 + e] = __fadd_rn(sum[c0 + e], __uint_as_float(rs[e]));
         }
       }
-    } else
+      // the sums go to shared memory ([channel][site], the stages are idle: every MMA and TMA of the
+      // CTA has completed) -- the split-K partial tile as is, else the emit reads them back in a
+      // rolled loop (one inlined emit: the unrolled form bloats the kernel past the I-cache); a wide
+      // block hands the upper half of the channels to warps 0-3, so eight warps emit
+#pragma unroll
+      for (int c = 0; c < BP; ++c) P[c * BM + m] = sum[c];
+    } else if (!CAT) {
       drain(0, wide ? BN / 2 : BN);
+    }
   }
-  if (wide && warp < 4) {
-    if (D > 0) {  // promoted sums of channels [BN/2, BN) handed over by warps 4-7
-      constexpr int EB = (BN < 128 ? BN : 128) / 2;
-      asm volatile("bar.sync 5, 256;" ::: "memory");
+  if (!CAT && wide && warp < 4) {
+    bar_wait(acc_bar, 0);
+    fence_after();
+    drain(BN / 2, BN);
+  }
+  if (CAT && D > 0 && a.splits == 1) {
+    // promoted sums in shared memory ([channel][site]): one rolled emit loop for every warp that
+    // emits (one inlined emit -- unrolled copies bloat the kernel past the instruction cache); a
+    // wide block splits the channels between warps 4-7 (lower half) and warps 0-3 (upper half)
+    if (wide) asm volatile("bar.sync 5, 256;" ::: "memory");
+    if (warp >= 4 || wide) {
+      constexpr int BP = BN < 128 ? BN : 128;
       const int m = 32 * (warp & 3) + lane;
       int u, x;
       site_of(a, rr, m, u, x);
+      const int cb = (wide && warp < 4) ? BP / 2 : 0, ce = (wide && warp >= 4) ? BP / 2 : BP;
       const float* X = reinterpret_cast<const float*>(smem);
 #pragma unroll 1
-      for (int c0 = 0; c0 < EB; c0 += 16) {
+      for (int c0 = cb; c0 < ce; c0 += 16) {
         float vals[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) vals[e] = X[(c0 + e) * BM + m];
-        const int n0 = nblk * BN + EB + c0;
+        const int n0 = nblk * BN + c0;
         if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
       }
-    } else {
-      bar_wait(acc_bar, 0);
-      fence_after();
-      drain(BN / 2, BN);
     }
   }
   if (threadIdx.x == 128) TR(7);
@@ -1038,7 +1049,8 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
   constexpr bool packed = PK;
   // promotion: K-blocks per TMEM accumulation segment, segments per item
   // (balanced: GS = round(nk / drain) segments of DS K-blocks; a short item stays one segment)
-  const int GS = a.drain > 0 ? max(1, (nk + a.drain / 2) / a.drain) : 1, DS = (nk + GS - 1) / GS;
+  const int GS0 = a.drain > 0 ? max(1, (nk + a.drain / 2) / a.drain) : 1, DS = (nk + GS0 - 1) / GS0;
+  const int GS = (nk + DS - 1) / DS;  // the MMA issuer closes a segment every DS K-blocks
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);

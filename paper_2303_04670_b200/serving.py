@@ -147,7 +147,7 @@ class EventPipeline:
         buf = self.host[k].numpy()
         meta = buf[: 8 * self.meta].view(np.int64)
         off = 8 * self.meta
-        first = 0
+        first, most = 0, 0
         for s in range(S):
             lo, hi = bounds[s]
             a = prev_hi[s] if prev_hi is not None else lo
@@ -161,7 +161,8 @@ class EventPipeline:
             meta[3 * s: 3 * s + 3] = (first, n, a)
             meta[3 * S + 4 * s: 3 * S + 4 * s + 4] = (lo, hi, tau[s], self.window_us)
             first += n
-        return 8 * self.meta + 13 * first, first
+            most = max(most, n)
+        return 8 * self.meta + 13 * first, most
 
     def run(self, records, t_host, taus, out_host: torch.Tensor) -> int:
         """records[s]: the session's packed EVB records (numpy, _EVB_RECORD dtype, time-sorted);
@@ -196,7 +197,7 @@ class EventPipeline:
             k = i % 2
             if i >= 2:
                 ev_h2d[k].synchronize()  # host buffer k's previous upload has left
-            nb, nev = self._fill(k, records, bnds, prev, [taus[s][i] for s in range(S)])
+            nb, nev = self._fill(k, records, bnds, prev, [taus[s][i] for s in range(S)])  # nev: most per session
             with torch.cuda.stream(cp):
                 if i >= 2:
                     cp.wait_event(ev_used[k])  # device buffer k's previous contents were consumed

@@ -129,12 +129,16 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 
-def c1_frames(evc, seed, n_windows):
+def c1_stream(evc, seed, n_windows):
+    return evc.generate_events(seed=seed, duration_us=WINDOW_US + SHIFT_US * n_windows, rate_hz=RATE_HZ,
+                               n_objects=8, sensor_size=(256, 256))
+
+
+def c1_frames(evc, seed, n_windows, stream=None):
     """C1 input frames: count(2) + timestamp(2) of a seeded 1 MHz 256x256 stream, 50 ms windows / 1 ms."""
     import torch
 
-    stream = evc.generate_events(seed=seed, duration_us=WINDOW_US + SHIFT_US * n_windows, rate_hz=RATE_HZ,
-                                 n_objects=8, sensor_size=(256, 256))
+    stream = stream or c1_stream(evc, seed, n_windows)
     xs = []
     for i in range(n_windows):
         w = evc.slice_window(stream, WINDOW_US + SHIFT_US * i, WINDOW_US)
@@ -269,7 +273,8 @@ def run_ours(args):
     S = args.sessions
     n_win = 1 + args.warmup + args.steps + 1
     seeds = _shard.stream_seeds(rank, S)
-    xs = make_inputs(lambda sd: c1_frames(evc, sd, n_win), seeds)  # resident in HBM before timing
+    streams = {sd: c1_stream(evc, sd, max(n_win, 66)) for sd in seeds}  # (the e2e leg runs 64 increments)
+    xs = make_inputs(lambda sd: c1_frames(evc, sd, n_win, streams[sd]), seeds)  # resident in HBM before timing
     density = float((xs[1:] != xs[:-1]).float().mean())
     g = evc.build(spec, weights, refresh_interval=64, sessions=S)
     times, refreshes, clk = timed_steps(g, xs, args.steps, args.warmup, world, dev.index or 0)
@@ -290,7 +295,8 @@ def run_ours(args):
         lat = {"sessions": 1, "p50_ms": statistics.median(s1), "p99_ms": pct(s1, 0.99), "steps": len(s1)}
         del g1
     roof = conv_roofline(g, xs, evc)
-    e2e = measure_e2e(g, xs, args, S, world, cdev)
+    e2e = measure_e2e_events(evc, g, [streams[sd] for sd in seeds], args, S, world, cdev)
+    e2e["frames_pipeline"] = measure_e2e(g, xs, args, S, world, cdev)
     out = None
     if rank == 0:
         out = {
@@ -420,6 +426,39 @@ def measure_e2e(g, xs, args, S, world=1, dev=None):
             "copies": "H2D / D2H on a copy stream, overlapped with the neighbouring steps' compute"}
 
 
+def measure_e2e_events(evc, g, streams, args, S, world=1, dev=None):
+    """The metric end to end from raw events (serving.EventPipeline): every step uploads only the
+    packed EVB records that arrived since the previous window end (13 B per event, pinned), bins
+    the windows on the device, runs step_increment + incr_step (+ refresh) and downloads the
+    integrated output.  Wall clock incl. Python, first upload to last download."""
+    import torch
+
+    n = 63  # one dense pass (the first window) per 64 windows: the steady state of refresh_interval 64
+    taus = [[WINDOW_US + SHIFT_US * i for i in range(n + 1)] for _ in range(S)]
+    recs = [evc.pack_records(st) for st in streams]
+    ts = [st.t for st in streams]
+    pipe = evc.EventPipeline(g, (256, 256), "count+timestamp", window_us=WINDOW_US)
+    y = g._y_run[g.output_ids[0]]
+    out_host = torch.empty((n, *y.shape), dtype=torch.float32).pin_memory()
+    pipe.run(recs, ts, [t[:3] for t in taus], out_host[:2])  # warm-up (allocations, graph capture)
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    t0 = time.perf_counter()
+    pipe.run(recs, ts, taus, out_host)
+    wall = time.perf_counter() - t0
+    wall = _shard.job_time_ms(wall * 1e3, world, dev) / 1e3
+    steady = pipe.h2d_bytes[1:]
+    return {"value": n * S * world / wall, "unit": UNIT, "h2d_bytes_per_step": int(sum(steady) / len(steady)),
+            "d2h_bytes_per_step": int(out_host[0].numel() * 4), "ms_per_step": wall / n * 1e3,
+            "h2d_bytes_first_window": int(pipe.h2d_bytes[0]),
+            "copies": ("raw events in: each step's new packed EVB records (13 B/event) of every stream H2D from "
+                       "pinned memory, device ring + binning (evc_ingest_ring, evc_encode_windows), the step, "
+                       "the integrated output D2H; copies overlapped with the neighbouring steps' compute")}
+
+
 # ---------------------------------------------------------------------------
 # C2 / C3 / C4 sub-results (N = 1)
 # ---------------------------------------------------------------------------
@@ -458,12 +497,13 @@ def graph_config(evc, spec, frames, S, steps, warmup, cpu_fn, cpu_budget, label)
 def c4_config(evc, iters=10, cpu_budget=0.0):
     """C4: one 64 -> 128 3x3 conv (stride 1, pad 1) at 480x640 inside a device Graph (input ->
     conv), incremental on a tile-clustered increment (fraction d of the 6x6 tiles live in all 64
-    channels) vs the same library's dense conv of the full input.  Times = CUDA events around the
-    conv's launches (input shadow + any-channel map + fused conv), median of `iters`."""
+    channels) vs the same library's dense conv of the full input.  Sparse paths: the
+    input-stationary scatter conv (mask/meter kernel + evc_conv_scatter: compaction, gather -> GEMM
+    -> scatter-add, per-tile sum) and the output-stationary fused conv (input shadow + any-channel
+    map + evc_conv_fused).  Times = CUDA events around the conv's launches, median of `iters`."""
     import numpy as np
     import torch
 
-    from paper_2303_04670_b200 import _lib
     from paper_2303_04670_b200.graph import ModelSpec, NodeSpec
 
     C, H, W, CO = 64, 480, 640, 128
@@ -472,12 +512,14 @@ def c4_config(evc, iters=10, cpu_budget=0.0):
                                                        "padding": 1})], "conv")
     rng = np.random.default_rng(0)
     wt = (rng.standard_normal((CO, C, 3, 3)) * np.sqrt(2.0 / (C * 9))).astype(np.float32)
-    g = evc.build(spec, {"conv.weight": wt}, refresh_interval=0, sessions=1, cuda_graph=False)
+    graphs = {"scatter": evc.build(spec, {"conv.weight": wt}, refresh_interval=0, sessions=1, cuda_graph=False,
+                                   scatter_convs=("conv",)),
+              "fused": evc.build(spec, {"conv.weight": wt}, refresh_interval=0, sessions=1, cuda_graph=False)}
     x_dense = torch.from_numpy(rng.standard_normal((C, H, W)).astype(np.float32)).cuda()
+    g = graphs["fused"]
     g.dense_pass(x_dense)
-    # dense: the conv's launches of the dense program (input shadow + dense conv)
     dts = []
-    for _ in range(iters):
+    for _ in range(iters):  # dense: the conv's launches of the dense program (input shadow + dense conv)
         g._load_input(x_dense)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -488,33 +530,40 @@ def c4_config(evc, iters=10, cpu_budget=0.0):
         dts.append(e0.elapsed_time(e1) * 1e3)
     g._clear_increments()
     t_dense = statistics.median(dts)
+    graphs["scatter"].dense_pass(x_dense)
     gh, gw = -(-H // 6), -(-W // 6)
+    names = {"to_hwc", "tile_any", "conv_fused", "conv_mask", "conv_gemm", "conv_scatter"}
     rows = []
     for d in (0.005, 0.01, 0.02, 0.05, 0.10, 0.20):
         f2 = rng.random((gh, gw)) < d
         px = np.repeat(np.repeat(f2, 6, 0), 6, 1)[:H, :W]
         vals = torch.from_numpy((rng.standard_normal((C, H, W)) * px[None]).astype(np.float32)).cuda()
         flags = torch.from_numpy(np.broadcast_to(f2, (C, gh, gw)).copy()).cuda().to(torch.uint8)
-        ts, perf = [], 0
-        v, f = g.input_slot()
-        for it in range(iters + 2):
-            v.copy_(vals.unsqueeze(0))
-            f.copy_(flags.unsqueeze(0))
-            torch.cuda.synchronize()
-            timed = ({"to_hwc", "tile_any", "conv_fused", "conv_mask", "conv_gemm"}, [])
-            g._run_program(timed=timed)
-            torch.cuda.synchronize()
-            if it >= 2:  # (the first two calls settle the region state of the new mask)
-                ts.append(sum(a.elapsed_time(b) for _, a, b in timed[1]) * 1e3)
-                perf = int(g._perf_step[0, 0])
-        t = statistics.median(ts)
-        rows.append({"live_tiles": d, "mask": "clustered", "sparse_us": t, "dense_us": t_dense,
-                     "sparse_over_dense": t / t_dense, "performed_over_dense": perf / g._dense_static[0]})
+        row = {"live_tiles": d, "mask": "clustered", "dense_us": t_dense}
+        for name, gg in graphs.items():
+            ts, perf = [], 0
+            v, f = gg.input_slot()
+            for it in range(iters + 2):
+                v.copy_(vals.unsqueeze(0))
+                f.copy_(flags.unsqueeze(0))
+                torch.cuda.synchronize()
+                timed = (names, [])
+                gg._run_program(timed=timed)
+                torch.cuda.synchronize()
+                if it >= 2:  # (the first two calls settle the region / tile state of the new mask)
+                    ts.append(sum(a.elapsed_time(b) for _, a, b in timed[1]) * 1e3)
+                    perf = int(gg._perf_step[0, 0])
+            row[f"{name}_us"] = statistics.median(ts)
+            row["performed_over_dense"] = perf / gg._dense_static[0]
+        row["sparse_us"] = row["scatter_us"]
+        row["sparse_over_dense"] = row["scatter_us"] / t_dense
+        rows.append(row)
     cross = max([r["live_tiles"] for r in rows if r["sparse_us"] < t_dense], default=None)
-    del g
+    del graphs, g
     torch.cuda.empty_cache()
     res = {"workload": "C4 single 3x3 conv 64->128 @480x640, tile-clustered increments (Graph, conv launches timed)",
-           "dense_us": t_dense, "sweep": rows, "sparse_faster_than_dense_up_to": cross}
+           "dense_us": t_dense, "sweep": rows, "sparse_faster_than_dense_up_to": cross,
+           "sparse_path": "input-stationary scatter conv (evc_conv_mask + evc_conv_scatter)"}
     if cpu_budget > 0:
         res["cpu_baseline"] = run_cpu(("c4", 0.02), cpu_budget)
     return res

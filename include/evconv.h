@@ -129,6 +129,19 @@ int evc_encode_windows(const uint64_t* t, const uint16_t* x, const uint16_t* y, 
                        const int64_t* win, int64_t max_events, int32_t H, int32_t W, int32_t mode, float* out,
                        int64_t out_stride, int32_t S, void* stream);
 
+/* Input-stationary incremental conv (inc_conv2d increment_ops.py:156-194 value
+ * path): live input tiles compacted, gathered into 3xTF32 tcgen05 tiles with every tap along N,
+ * scattered into per-tile output patches and summed per output tile in a fixed order.  Values only:
+ * output flags and the FLOP meter come from evc_conv_mask.  Geometry: stride 1, "same" output,
+ * k <= 3, th * tw <= 36.  fresh_out != 0: the output buffer was zeroed since the last call (else only
+ * tiles that held values and are dead now are rewritten with zeros). */
+int evc_conv_scatter_supported(const evc_conv_geom* g);
+int64_t evc_conv_scatter_pack_len(const evc_conv_geom* g);
+int evc_conv_scatter_pack(const float* w, const evc_conv_geom* g, float* out);
+int64_t evc_conv_scatter_workspace(const evc_conv_geom* g, int32_t S);
+int evc_conv_scatter(const evc_conv_geom* g, const evc_tensor* in, const float* wpack, const evc_tensor* out,
+                     void* workspace, int64_t ws_bytes, int32_t fresh_out, int32_t S, void* stream);
+
 /* Strided byte copy of S blocks of `nbytes` (cudaMemcpy2DAsync, capturable in a CUDA
  * graph): the recurrent delay node's pending increment (values and tile flags) moved
  * between its state buffers and its output slot. */

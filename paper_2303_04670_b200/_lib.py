@@ -81,6 +81,11 @@ _PROTOS = {
     "evc_copy_masked": (_I32, [_T, _T, _I32, _P]),
     "evc_copy_dense": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P]),
     "evc_copy_bytes": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P]),
+    "evc_conv_scatter_supported": (_I32, [_G]),
+    "evc_conv_scatter_pack_len": (_I64, [_G]),
+    "evc_conv_scatter_pack": (_I32, [_P, _G, _P]),
+    "evc_conv_scatter_workspace": (_I64, [_G, _I32]),
+    "evc_conv_scatter": (_I32, [_G, _T, _P, _T, _P, _I64, _I32, _I32, _P]),
     "evc_max_abs_diff": (_I32, [_P, _I64, _P, _I64, _I64, _I32, _P, _P]),
     "evc_conv_table_len": (_I64, [_G]),
     "evc_conv_table_fill": (_I32, [_G, _P]),

@@ -286,6 +286,7 @@ int init_masks();
 int init_conv();
 int init_conv_mask();
 int init_conv_fused();
+int init_conv_scatter();
 int init_elementwise();
 int init_bands();
 int init_upsparsify();

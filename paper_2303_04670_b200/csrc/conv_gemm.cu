@@ -288,6 +288,7 @@ int init_conv() {
   if (cudaFuncGetAttributes(&fa, k_conv_splitk_reduce) != cudaSuccess) return EVC_ECUDA;
   int rc = init_conv_mask();
   if (!rc) rc = init_conv_tc();
-  return rc ? rc : init_conv_fused();
+  if (!rc) rc = init_conv_fused();
+  return rc ? rc : init_conv_scatter();
 }
 }  // namespace evc

@@ -458,7 +458,7 @@ class Graph:
 
     def __init__(self, spec: ModelSpec, weights, refresh_interval: int = DEFAULT_REFRESH_INTERVAL, *,
                  sessions: int = 1, cuda_graph: bool = True, device=None, conv_kernel: str | None = None,
-                 max_splits: int = 0):
+                 max_splits: int = 0, scatter_convs=()):
         self.lib = _lib.lib()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.spec = spec
@@ -472,6 +472,8 @@ class Graph:
             raise ValueError("sessions must be >= 1")
         self.use_cuda_graph = bool(cuda_graph)
         self.max_splits = int(max_splits)  # K-split cap of the fused conv (0: library default)
+        # conv node ids run on the input-stationary scatter path (evc_conv_scatter) in incremental steps
+        self.scatter_convs = set(scatter_convs or ())
         from . import tensors as _t
 
         self.conv_kernel = conv_kernel or _t.CONV_KERNEL
@@ -631,7 +633,9 @@ class Graph:
                 max_T = max(max_T, S * node.plan.T)
                 max_ws = max(max_ws, node.plan.ws_floats)
                 node.fused_act = None
-                if node.plan.path == "fused":
+                node.scatter = (node.spec.id in self.scatter_convs and node.plan.path == "fused"
+                                and node.plan.scatter_plan() is not None)
+                if node.plan.path == "fused" and not node.scatter:
                     # a sparsify whose only reader is this conv writes the conv's channels-innermost
                     # shadow and its any-channel tile map itself (and skips its planar values)
                     prod = self._by_id.get(node.spec.inputs[0])
@@ -714,7 +718,7 @@ class Graph:
                 st = self._slots[node.spec.id].store
                 sp_off.append((node, take(st.flags.numel())))  # flags are only ever set by the producer
             if node.kind == "conv":
-                if node.plan.path == "fused":
+                if node.plan.path == "fused" and not node.scatter:
                     fany_off.append((node, take(S * node.plan.gi[0] * node.plan.gi[1])))
                 else:
                     n = int(self.lib.evc_conv_mask_scratch(node.plan.g, S))
@@ -741,7 +745,7 @@ class Graph:
         for i, nid in enumerate(meter_ids):
             nd = self._by_id[nid]
             part, npart, cout = None, 0, 0
-            if nd.kind == "conv" and nd.plan.path == "fused":
+            if nd.kind == "conv" and nd.plan.path == "fused" and not nd.scatter:
                 nd.mpart = torch.zeros(S * nd.plan.ctas * 2, dtype=torch.int64, device=dev)
                 part, npart, cout = nd.mpart.data_ptr(), nd.plan.ctas, nd.plan.c_out
             mrec[i] = _lib.EvcMeterNode(part, npart, nflags[i], self._dense_static[i], cout, 0)
@@ -815,7 +819,14 @@ class Graph:
                 din = self._desc(ns.inputs[0])
                 cnt_ptr = i32.data_ptr() + 4 * mi * S
                 perf_ptr = self._perf_step.data_ptr() + 8 * mi * S
-                if plan.path == "fused":
+                if node.scatter:  # flags + meter from the mask kernel, values from the scatter conv
+                    dout = self._desc(nid)
+                    count_ptr, scratch_ptr = node.mask_scratch
+                    prog.append((L.evc_conv_mask, plan.mask_args(din, dout, scratch_ptr, cnt_ptr, None, None,
+                                                                 perf_ptr), "conv_mask"))
+                    fn, args = plan.scatter(din, dout, fresh_out=False)
+                    prog.append((fn, args, "conv_scatter"))
+                elif plan.path == "fused":
                     if not plan.fed_by_sparsify:
                         pre = plan.prep(din)
                         prog.append((pre[0], pre[1], "to_hwc"))
@@ -994,7 +1005,7 @@ class Graph:
         """libevconv kernels launched by one incr_step (+ the scratch memset; diff_mask excluded)."""
         n = 2  # memset of the per-step scratch + meter bookkeeping
         for fn, args, name in self._program:
-            n += 2 if name in ("conv_mask", "maxpool", "linear") else 1
+            n += 2 if name in ("conv_mask", "maxpool", "linear") else (6 if name == "conv_scatter" else 1)
         n += sum(1 for nd in self.nodes if nd.kind == "conv" and nd.plan.path != "fused" and nd.plan.splits > 1)
         return n
 
@@ -1125,6 +1136,8 @@ class Graph:
                 nd.plan.hwc.zero_()
             if nd.kind == "conv" and nd.plan.path == "fused":
                 nd.plan.rstate.zero_()  # no region holds a nonzero increment now
+            if nd.kind == "conv" and getattr(nd, "scatter", False):
+                nd.plan.scatter_plan()[1].zero_()  # nor does any output tile of the scatter path
 
     def dense_oracle(self, x):
         """Pure dense forward of the primary output; session state is untouched."""

@@ -12,6 +12,8 @@ Graph runtime drives the same kernels over preallocated, batched buffers.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass
 
 import numpy as np
@@ -121,6 +123,7 @@ def _desc(v, f, tile):
 
 
 SPARSE_TILE_PATH_BELOW = 0.012  # live-tile fraction under which inc_conv2d gathers tiles
+SCATTER_PATH_BELOW = float(os.environ.get("EVC_SCATTER_BELOW", "0.35"))  # input-stationary path below this
 
 
 def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounter) -> IncrementTensor:
@@ -142,13 +145,29 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     # while the fused kernel computes whole 128-site regions around them (measured on C4,
     # 64 -> 128 @ 480x640: 252 vs 398 us at 0.5 % live tiles; the fused path wins from ~1.5 %)
     kernel = None
-    if tensors.CONV_KERNEL == "tc" and 1.0 - x.mask.false_fraction() < SPARSE_TILE_PATH_BELOW:
+    live = 1.0 - x.mask.false_fraction() if tensors.CONV_KERNEL == "tc" else 1.0
+    plan = tensors.cached_plan(weight, st, pad, h, w, tile.h, tile.w)
+    scatter = (tensors.CONV_KERNEL == "tc" and plan.path == "fused" and live < SCATTER_PATH_BELOW
+               and plan.scatter_plan() is not None)
+    if not scatter and tensors.CONV_KERNEL == "tc" and live < SPARSE_TILE_PATH_BELOW:
         kernel = "tile"
-    plan = tensors.cached_plan(weight, st, pad, h, w, tile.h, tile.w, kernel=kernel)
+        plan = tensors.cached_plan(weight, st, pad, h, w, tile.h, tile.w, kernel=kernel)
     yv, yf = _zeros_incr((c_out, ho, wo), tile, dev)
     s = _lib.stream_ptr()
     din = x.desc()
     dout = _desc(yv, yf, tile)
+    if scatter:
+        # sparse increments: input-stationary gather -> GEMM -> scatter-add over the live input tiles
+        # only (the meter's own unit of work); output flags and meter from the mask kernel
+        i32 = torch.zeros(1, dtype=torch.int32, device=dev)
+        scratch = torch.zeros(int(lib.evc_conv_mask_scratch(plan.g, 1)), dtype=torch.int32, device=dev)
+        perf = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.check(lib.evc_conv_mask(*plan.mask_args(din, dout, _lib.ptr(scratch), _lib.ptr(i32), None, None,
+                                                     _lib.ptr(perf)), s), "conv_mask")
+        fn, args = plan.scatter(din, dout, fresh_out=True)
+        _lib.check(fn(*args, s), "conv_scatter")
+        meter.add(int(perf.item()), 0)
+        return IncrementTensor(yv, TileMask(yf, tile))
     if plan.path == "fused":
         fany = torch.zeros(plan.gi[0] * plan.gi[1], dtype=torch.uint8, device=dev)
         mpart = torch.zeros(plan.ctas * 2, dtype=torch.int64, device=dev)  # per-CTA meter partials

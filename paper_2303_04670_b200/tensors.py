@@ -335,6 +335,29 @@ class ConvPlan:
             self.ws_floats = int(lib.evc_conv_workspace(self.g, S * T, self.splits))
         self.dense_flops = 2 * kh * kw * c_in * c_out * ho * wo
 
+    def scatter_plan(self):
+        """Packed weights + workspace of the input-stationary scatter path (evc_conv_scatter) for
+        this layer, built on first use; None when the geometry is not supported."""
+        sp = getattr(self, "_scatter", None)
+        if sp is None:
+            lib = _lib.lib()
+            if not lib.evc_conv_scatter_supported(self.g):
+                self._scatter = False
+                return None
+            host = np.ascontiguousarray(self.weight.detach().cpu().numpy(), dtype=np.float32)
+            out = np.zeros(int(lib.evc_conv_scatter_pack_len(self.g)), dtype=np.float32)
+            _lib.check(lib.evc_conv_scatter_pack(host.ctypes.data, self.g, out.ctypes.data), "scatter_pack")
+            ws = torch.zeros(int(lib.evc_conv_scatter_workspace(self.g, self.S)), dtype=torch.uint8,
+                             device=self.weight.device)
+            sp = self._scatter = (torch.from_numpy(out).to(self.weight.device), ws)
+        return sp or None
+
+    def scatter(self, din, dout, fresh_out: bool):
+        """(ctypes fn, args-without-stream) of evc_conv_scatter (values only)."""
+        wp, ws = self.scatter_plan()
+        return _lib.lib().evc_conv_scatter, (self.g, din, wp.data_ptr(), dout, ws.data_ptr(), ws.numel(),
+                                             1 if fresh_out else 0, self.S)
+
     def prep(self, din):
         """(fn, args-without-stream) mirroring the conv input into the HWC shadow, or None."""
         if self.path != "fused":

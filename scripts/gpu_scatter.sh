@@ -1,0 +1,2 @@
+timeout 300 python -m pytest tests/test_gpu_scatter.py -q -x -s --timeout 120 -p no:cacheprovider > gpurun_out/pytest_sc.log 2>&1; tail -30 gpurun_out/pytest_sc.log
+timeout 300 python scripts/c4_bench.py > gpurun_out/c4.log 2>&1; head -12 gpurun_out/c4.log

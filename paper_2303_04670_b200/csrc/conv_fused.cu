@@ -1394,7 +1394,13 @@ __global__ void k_tile_any(TView x, uint8_t* __restrict__ fany) {
   const int s = blockIdx.y;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < Ti; t += gridDim.x * blockDim.x) {
     int any = 0;
-    for (int c = 0; c < x.C && !any; ++c) any |= x.fplane(s, c)[t];
+    for (int c0 = 0; c0 < x.C && !any; c0 += 8) {  // eight independent loads in flight per test
+      uint8_t f[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) f[k] = c0 + k < x.C ? x.fplane(s, c0 + k)[t] : 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) any |= f[k];
+    }
     fany[(int64_t)s * Ti + t] = any != 0;
   }
 }

@@ -36,10 +36,11 @@ using namespace fz;
 constexpr int BNB = 16;      // output channels per unit
 constexpr int SLOT = 40;     // A rows (TMEM lanes) per tile slot: th * tw <= 36 sites, five 8-row groups
 constexpr int TPU = 3;       // tiles per group (120 of 128 rows)
-constexpr int NS = 3;        // weight pipeline stages
+constexpr int NS = 2;        // weight pipeline stages
 constexpr int A_KB = 2 * 128 * 128;  // one K-block of the resident A tile: heads + tails, 128 rows x 128 B
-constexpr int MAX_KB = 3;    // resident A: C_in <= 96
-constexpr int THREADS = 320;  // warps 0-3 gather, 4-7 epilogue, 8 TMEM alloc + MMA issuer, 9 weight stream
+constexpr int MAX_KB = 2;    // resident A: C_in <= 64
+constexpr int THREADS = 448;  // warps 0-3 gather, 4-11 epilogue, 12 TMEM alloc + MMA issuer, 13 weight stream
+constexpr int EPI = 256;      // epilogue threads (two warps per TMEM lane quarter)
 
 struct ScArgs {
   const float* in;
@@ -54,22 +55,25 @@ struct ScArgs {
   float* contrib;
 };
 
-__device__ __forceinline__ void sync_epi() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void sync_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // One CTA walks tile groups (3 live input tiles); per group the gather warps stage the A tile of
 // every K-block once (resident), and the MMA issuer runs all output-channel blocks over it, each
 // into a double-buffered TMEM accumulator that the epilogue warps scatter into output patches.
+template <int K, int T>
 __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_constant__ ScArgs a) {
+  // compile-time geometry: every index decode below is shifts / multiplies
+  constexpr int TAPS = K * K, PH = T + K - 1, PW = T + K - 1, SITES = T * T, PPT = PH * PW;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int N = a.taps * BNB;
+  constexpr int N = TAPS * BNB;
   const uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const int BSTAGE = (2 * a.b_half + 1023) / 1024 * 1024;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* bst = smem + a.nkb * A_KB;  // weight stages
-  float* patch = reinterpret_cast<float*>(bst + NS * BSTAGE);
-  const int PSZ = a.PH * a.PW * BNB;  // floats per tile patch
-  uint64_t* bars = reinterpret_cast<uint64_t*>(patch + TPU * PSZ);
+  float* Dsm = reinterpret_cast<float*>(bst + NS * BSTAGE);  // accumulator stage [column][TMEM lane]
+  constexpr int PSZ = PPT * BNB;  // floats per tile patch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Dsm + 128 * N);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 6);
   const uint32_t sA = su32(smem), sB = su32(bst), b0 = su32(bars);
   auto bfull = [&](int i) { return b0 + 8u * i; };
@@ -85,13 +89,13 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
     }
     for (int i = 0; i < 2; ++i) {
       bar_init(tfull(i), 1);
-      bar_init(tempty(i), 128);
+      bar_init(tempty(i), EPI);
     }
     bar_init(afull, 128);
     bar_init(aempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8) {
+  if (warp == 12) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -103,7 +107,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
   pdl_wait();
   const int n_live = *a.count;
   const int ngroups = (n_live + TPU - 1) / TPU;
-  const int sites = a.th * a.tw, Ti = a.GH * a.GW;
+  const int Ti = a.GH * a.GW;
 
   if (warp < 4) {  // ------------------------------------------------------------ A gather
     const int tid = threadIdx.x;
@@ -120,16 +124,17 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
           const int t = a.list[li];
           tile_s[j] = t / Ti;
           const int r = t - tile_s[j] * Ti;
-          tile_y[j] = (r / a.GW) * a.th;
-          tile_x[j] = (r % a.GW) * a.tw;
+          tile_y[j] = (r / a.GW) * T;
+          tile_x[j] = (r % a.GW) * T;
         }
       }
       if (q >= 1) bar_wait(aempty, (q - 1) & 1);  // every MMA over the previous group's A is done
       // element e = ((j * 32 + c) * th + y) * tw + x  (x fastest: short coalesced runs)
-      const int per = TPU * 32 * sites;
+      constexpr int per = TPU * 32 * SITES;
       for (int kb = 0; kb < a.nkb; ++kb) {
         float* Ah = reinterpret_cast<float*>(smem + kb * A_KB);
         float* Al = Ah + 128 * 32;
+#pragma unroll 1
         for (int e0 = tid; e0 < per; e0 += 128 * BATCH) {
           float v[BATCH];
 #pragma unroll
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
             const int e = e0 + 128 * k;
             v[k] = 0.0f;
             if (e < per) {
-              const int x = e % a.tw, y = (e / a.tw) % a.th, c = (e / sites) % 32, j = e / (32 * sites);
+              const int x = e % T, y = (e / T) % T, c = (e / SITES) % 32, j = e / (32 * SITES);
               const int ch = kb * 32 + c, py = tile_y[j] + y, px = tile_x[j] + x;
               if (tile_s[j] >= 0 && ch < a.C && py < a.H && px < a.W)
                 v[k] = __ldg(a.in + (int64_t)tile_s[j] * a.in_vs + ((int64_t)ch * a.H + py) * a.W + px);
@@ -147,8 +152,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
           for (int k = 0; k < BATCH; ++k) {
             const int e = e0 + 128 * k;
             if (e < per) {
-              const int x = e % a.tw, y = (e / a.tw) % a.th, c = (e / sites) % 32, j = e / (32 * sites);
-              const int row = j * SLOT + y * a.tw + x;
+              const int x = e % T, y = (e / T) % T, c = (e / SITES) % 32, j = e / (32 * SITES);
+              const int row = j * SLOT + y * T + x;
               const int off = row * 32 + (((c >> 2) ^ (row & 7)) << 2) + (c & 3);  // 128B swizzle (floats)
               const float hi = tf32_head(v[k]);
               Ah[off] = hi;
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bar_arrive(afull);
     }
-  } else if (warp == 9) {  // ----------------------------------------------------- weight stream
+  } else if (warp == 13) {  // ---------------------------------------------------- weight stream
     if (lane == 0) {
       int it = 0;
       for (int g = blockIdx.x; g < ngroups; g += gridDim.x)
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
           }
     }
     __syncwarp();
-  } else if (warp == 8) {  // ------------------------------------------------------- MMA issuer
+  } else if (warp == 12) {  // ------------------------------------------------------ MMA issuer
     if (lane == 0) {
       int it = 0, u = 0, q = 0;
       for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++q) {
@@ -208,59 +213,52 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
     }
     __syncwarp();
   } else {  // ---------------------------------------------------------------------- epilogue
+    // per unit: the accumulator (site x [tap][16 channels]) goes TMEM -> shared memory, then every
+    // thread forms output patch points: patch point (py, px) of tile j, channel n sums, in tap
+    // order, D[site (py + r - kh + 1, px + q - kw + 1)][tap (r, q)][n] -- a gather, no atomics
     const int etid = threadIdx.x - 128;
     const int m = 32 * (warp & 3) + lane;  // TMEM lane = A row
-    const int j = m / SLOT, p = m % SLOT;
-    const bool site = j < TPU && p < sites;
-    const int iy = p / a.tw, ix = p % a.tw;
+    const int half = (warp - 4) >> 2;      // the two warps of a lane quarter split the taps
     const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     int u = 0;
     for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
       const int ntile = min(TPU, n_live - g * TPU);
       for (int nb = 0; nb < a.nb; ++nb, ++u) {
-        for (int i = etid; i < TPU * PSZ; i += 128) patch[i] = 0.0f;
-        sync_epi();
         const int ab = u & 1;
         bar_wait(tfull(ab), (u >> 1) & 1);
         fence_after();
-        for (int t0 = 0; t0 < a.taps; t0 += 3) {  // three taps per TMEM wait
+#pragma unroll
+        for (int t0 = 0; t0 < TAPS; t0 += 3) {  // three taps per TMEM wait
+          if (((t0 / 3) & 1) != half) continue;
           uint32_t r[3][16];
 #pragma unroll
           for (int dt = 0; dt < 3; ++dt)
-            if (t0 + dt < a.taps) tmem_ld16_issue(trow + (uint32_t)(ab * 256 + (t0 + dt) * BNB), r[dt]);
+            if (t0 + dt < TAPS) tmem_ld16_issue(trow + (uint32_t)(ab * 256 + (t0 + dt) * BNB), r[dt]);
           tmem_wait_ld();
-          if (t0 + 3 >= a.taps) {  // the accumulator buffer is free for the unit after next
-            fence_before();
-            bar_arrive(tempty(ab));
-          }
 #pragma unroll
-          for (int dt = 0; dt < 3; ++dt) {
-            const int t = t0 + dt;
-            if (t < a.taps) {
-              if (site && j < ntile) {
-                const int rr = t / a.kw, qq = t % a.kw;
-                const int py = iy - rr + a.kh - 1, px = ix - qq + a.kw - 1;  // patch coordinates
-                float4* dst = reinterpret_cast<float4*>(patch + j * PSZ + (py * a.PW + px) * BNB);
+          for (int dt = 0; dt < 3; ++dt)
+            if (t0 + dt < TAPS) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  float4 w = dst[e];
-                  w.x = __fadd_rn(w.x, __uint_as_float(r[dt][4 * e]));
-                  w.y = __fadd_rn(w.y, __uint_as_float(r[dt][4 * e + 1]));
-                  w.z = __fadd_rn(w.z, __uint_as_float(r[dt][4 * e + 2]));
-                  w.w = __fadd_rn(w.w, __uint_as_float(r[dt][4 * e + 3]));
-                  dst[e] = w;
-                }
-              }
-              sync_epi();  // the next tap may hit the same positions from other sites
+              for (int e = 0; e < 16; ++e) Dsm[((t0 + dt) * BNB + e) * 128 + m] = __uint_as_float(r[dt][e]);
             }
-          }
         }
-        // patches of the group's live tiles -> contrib[list index][nb]
-        const int q4 = PSZ / 4;
-        for (int i = etid; i < ntile * q4; i += 128) {
-          const int jj = i / q4, k = i - jj * q4;
-          float4* dst = reinterpret_cast<float4*>(a.contrib + ((int64_t)(g * TPU + jj) * a.nb + nb) * PSZ);
-          dst[k] = reinterpret_cast<const float4*>(patch + jj * PSZ)[k];
+        fence_before();
+        bar_arrive(tempty(ab));  // the accumulator buffer is free for the unit after next
+        sync_epi();
+        // contrib layout [list index][channel block][16][PH][PW]: consecutive items, consecutive floats
+        const int items = ntile * BNB * PPT;
+        float* cdst = a.contrib + ((int64_t)(g * TPU) * a.nb + nb) * PSZ;
+#pragma unroll 2
+        for (int i = etid; i < items; i += EPI) {
+          const int px = i % PW, py = (i / PW) % PH, n = (i / PPT) % BNB, j = i / (BNB * PPT);
+          const float* dcol = Dsm + n * 128 + j * SLOT;
+          float sum = 0.0f;
+#pragma unroll
+          for (int t = 0; t < TAPS; ++t) {
+            const int iy = py + t / K - K + 1, ix = px + t % K - K + 1;
+            if (iy >= 0 && iy < T && ix >= 0 && ix < T) sum = __fadd_rn(sum, dcol[t * BNB * 128 + iy * T + ix]);
+          }
+          cdst[(int64_t)j * a.nb * PSZ + (i - j * BNB * PPT)] = sum;
         }
         sync_epi();
       }
@@ -268,7 +266,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
   }
   fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 12) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
   }
@@ -282,74 +280,96 @@ __global__ void k_scatter_map(const int32_t* __restrict__ list, const int32_t* _
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) map[list[i]] = i;
 }
 
-// One CTA per (session, output tile): sum the patches of the live neighbour input tiles in a fixed
-// order, stage the th x tw x C_out tile in shared memory, write it channel-planar.  Tiles dead now
-// but live last step are zeroed once; `live_prev` carries the state between steps.
-__global__ void __launch_bounds__(128) k_scatter_gather(const __grid_constant__ ScArgs a, const int32_t* __restrict__ map,
+// One CTA per (session, strip of STRIP output tiles in a tile row): each output value sums, in a
+// fixed neighbour order, the patch points of the (up to 4) live neighbour input tiles that cover it
+// (contrib layout [li][nb][16][PH][PW]).  The covering list of every pixel is resolved once per CTA;
+// a warp then writes 24-pixel row runs.  Tiles dead now but live last step are zeroed once;
+// `live_prev` carries that state between steps.
+constexpr int STRIP = 4;
+
+template <int K, int T>
+__global__ void __launch_bounds__(256) k_scatter_gather(const __grid_constant__ ScArgs a, const int32_t* __restrict__ map,
                                                         float* __restrict__ out, int64_t ovs, int Ho, int Wo,
                                                         uint8_t* live_prev) {
+  constexpr int PH = T + K - 1, PW = T + K - 1, SITES = T * T, PPT = PH * PW, PSZ = PPT * BNB;
+  constexpr int OFF = K - 1 - K / 2;  // patch origin offset ("same" padding K / 2)
+  __shared__ int s_off[STRIP][SITES][4];
+  __shared__ int s_cnt[STRIP][SITES];
+  __shared__ int s_state[STRIP];  // bit 0: live now, bit 1: live last step
   pdl_wait();
   pdl_trigger();
-  extern __shared__ float tile[];  // [sites][c_out + 1]
-  const int GHo = (Ho + a.th - 1) / a.th, GWo = (Wo + a.tw - 1) / a.tw;
-  const int s = blockIdx.y, T = blockIdx.x, ty = T / GWo, tx = T % GWo;
-  const int Ti = a.GH * a.GW;
-  const int32_t* mp = map + (int64_t)s * Ti;
-  // neighbour input tiles whose patch reaches this output tile: input tile rows ny with
-  // [ny th + pad - (kh - 1), ny th + th - 1 + pad] meeting [ty th, ty th + th - 1]
-  int nbr[9];
-  int nn = 0;
-  bool live = false;
-  for (int dy = -1; dy <= 1; ++dy)
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int ny = ty + dy, nx = tx + dx;
-      int li = -1;
-      if (ny >= 0 && ny < a.GH && nx >= 0 && nx < a.GW) li = mp[ny * a.GW + nx];
-      nbr[nn++] = li >= 0 ? (li << 4) | ((dy + 1) * 3 + (dx + 1)) : -1;
-      live |= li >= 0;
-    }
-  uint8_t* lp = live_prev + (int64_t)s * GHo * GWo + T;
-  const bool was = *lp != 0;
-  if (!live && !was) return;
-  const int sites = a.th * a.tw, CP = a.c_out + 1, PSZ = a.PH * a.PW * BNB;
-  for (int i = threadIdx.x; i < sites * a.c_out; i += blockDim.x) {
-    const int n = i % a.c_out, pidx = i / a.c_out;
-    const int oy = ty * a.th + pidx / a.tw, ox = tx * a.tw + pidx % a.tw;
-    float sum = 0.0f;
-    if (live) {
+  const int GHo = (Ho + T - 1) / T, GWo = (Wo + T - 1) / T, nstrip = (GWo + STRIP - 1) / STRIP;
+  const int s = blockIdx.y, ty = blockIdx.x / nstrip, tx0 = (blockIdx.x % nstrip) * STRIP;
+  const int32_t* mp = map + (int64_t)s * a.GH * a.GW;
+  uint8_t* lp = live_prev + (int64_t)s * GHo * GWo + (int64_t)ty * GWo;
+  if (threadIdx.x < STRIP * SITES) {
+    const int q = threadIdx.x / SITES, p = threadIdx.x % SITES, tx = tx0 + q;
+    const int ly = p / T, lx = p % T;
+    int cnt = 0;
+    bool live = false;
+    if (tx < GWo) {
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
-        if (nbr[k] < 0) continue;
-        const int li = nbr[k] >> 4, d = nbr[k] & 15, dy = d / 3 - 1, dx = d % 3 - 1;
-        const int py = oy - ((ty + dy) * a.th + a.pad - (a.kh - 1)), px = ox - ((tx + dx) * a.tw + a.pad - (a.kw - 1));
-        if (py < 0 || py >= a.PH || px < 0 || px >= a.PW) continue;
-        sum = __fadd_rn(sum, a.contrib[((int64_t)li * a.nb + n / BNB) * PSZ + (py * a.PW + px) * BNB + n % BNB]);
+        const int ny = ty + k / 3 - 1, nx = tx + k % 3 - 1;
+        const int li = (ny >= 0 && ny < a.GH && nx >= 0 && nx < a.GW) ? __ldg(mp + ny * a.GW + nx) : -1;
+        live |= li >= 0;
+        const int py = ly - (k / 3 - 1) * T + OFF, px = lx - (k % 3 - 1) * T + OFF;  // in the neighbour's patch
+        if (li >= 0 && py >= 0 && py < PH && px >= 0 && px < PW) s_off[q][p][cnt++] = li * a.nb * PSZ + py * PW + px;
       }
     }
-    tile[pidx * CP + n] = sum;
+    s_cnt[q][p] = cnt;
+    if (p == 0) s_state[q] = tx < GWo ? ((live ? 1 : 0) | (lp[tx] ? 2 : 0)) : 0;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < sites * a.c_out; i += blockDim.x) {
-    const int pidx = i % sites, n = i / sites;
-    const int oy = ty * a.th + pidx / a.tw, ox = tx * a.tw + pidx % a.tw;
-    if (oy < Ho && ox < Wo) out[(int64_t)s * ovs + ((int64_t)n * Ho + oy) * Wo + ox] = tile[pidx * CP + n];
+  if (!(s_state[0] | s_state[1] | s_state[2] | s_state[3])) return;  // nothing to write in this strip
+  constexpr int RW = STRIP * T;  // strip row width (pixels)
+  constexpr int U = 4;           // items per thread per pass: every load issued before any store
+  const int total = a.c_out * T * RW;
+  for (int i0 = threadIdx.x; i0 < total; i0 += U * 256) {
+    float sum[U];
+    int64_t dst[U];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      const int i = i0 + uu * 256;
+      sum[uu] = 0.0f;
+      dst[uu] = -1;
+      if (i >= total) continue;
+      const int xx = i % RW, y = (i / RW) % T, n = i / (RW * T);
+      const int q = xx / T, lx = xx % T, p = y * T + lx;
+      const int st = s_state[q];
+      const int oy = ty * T + y, ox = (tx0 + q) * T + lx;
+      if (!st || oy >= Ho || ox >= Wo) continue;
+      dst[uu] = (int64_t)s * ovs + ((int64_t)n * Ho + oy) * Wo + ox;
+      if (st & 1) {
+        const float* cb = a.contrib + (int64_t)(n / BNB) * PSZ + (n % BNB) * PPT;
+        const int c = s_cnt[q][p];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < c) sum[uu] = __fadd_rn(sum[uu], __ldg(cb + s_off[q][p][k]));
+      }
+    }
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu)
+      if (dst[uu] >= 0) out[dst[uu]] = sum[uu];
   }
-  if (threadIdx.x == 0) *lp = live ? 1 : 0;
+  __syncthreads();
+  if (threadIdx.x < STRIP && tx0 + (int)threadIdx.x < GWo) lp[tx0 + threadIdx.x] = s_state[threadIdx.x] & 1;
 }
 
 }  // namespace sc
 
-int init_conv_scatter() {
+template <int K>
+static int init_scatter_k() {
   cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, sc::k_conv_scatter) != cudaSuccess) return EVC_ECUDA;
-  if (cudaFuncSetAttribute(sc::k_conv_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+  if (cudaFuncGetAttributes(&fa, sc::k_conv_scatter<K, 6>) != cudaSuccess) return EVC_ECUDA;
+  if (cudaFuncSetAttribute(sc::k_conv_scatter<K, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
       cudaSuccess)
     return EVC_ECUDA;
-  if (cudaFuncSetAttribute(sc::k_scatter_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) !=
-      cudaSuccess)
-    return EVC_ECUDA;
+  if (cudaFuncGetAttributes(&fa, sc::k_scatter_gather<K, 6>) != cudaSuccess) return EVC_ECUDA;
   return EVC_OK;
 }
+
+int init_conv_scatter() { return init_scatter_k<1>() | init_scatter_k<3>(); }
 
 }  // namespace evc
 
@@ -406,8 +426,8 @@ extern "C" {
 
 int evc_conv_scatter_supported(const evc_conv_geom* g) {
   if (!g) return 0;
-  return g->stride == 1 && g->kh * g->kw * sc::BNB <= 256 && g->th * g->tw <= 36 && g->pad < g->kh &&
-         g->c_in <= 32 * sc::MAX_KB &&
+  return g->stride == 1 && g->kh == g->kw && (g->kh == 1 || g->kh == 3) && g->pad == g->kh / 2 && g->th == 6 &&
+         g->tw == 6 && g->c_in <= 32 * sc::MAX_KB &&
          g->pad < g->kw && g->kh <= 3 && g->kw <= 3 && g->Ho == g->H + 2 * g->pad - g->kh + 1 &&
          g->Wo == g->W + 2 * g->pad - g->kw + 1 && (g->th + g->kh - 1) * (g->tw + g->kw - 1) * sc::BNB % 4 == 0;
 }
@@ -507,20 +527,21 @@ int evc_conv_scatter(const evc_conv_geom* g, const evc_tensor* in, const float* 
   a.count = count;
   a.contrib = reinterpret_cast<float*>(ws + w.contrib);
   const int bstage = (2 * o.b_half + 1023) / 1024 * 1024;
-  const size_t smem = (size_t)o.nkb * sc::A_KB + (size_t)sc::NS * bstage +
-                      4 * (size_t)sc::TPU * o.PH * o.PW * sc::BNB + 1024 + 256;
+  const size_t smem = (size_t)o.nkb * sc::A_KB + (size_t)sc::NS * bstage + 4 * (size_t)128 * o.taps * sc::BNB +
+                      1024 + 256;
   EVC_CHECK_ARG(smem <= 227 * 1024, "conv_scatter: shared memory");
   const int grid = 148;
-  e = launch_pdl(sc::k_conv_scatter, dim3(grid), dim3(sc::THREADS), smem, st, a);
+  e = g->kh == 3 ? launch_pdl(sc::k_conv_scatter<3, 6>, dim3(grid), dim3(sc::THREADS), smem, st, a)
+                 : launch_pdl(sc::k_conv_scatter<1, 6>, dim3(grid), dim3(sc::THREADS), smem, st, a);
   if (e != cudaSuccess) {
     set_error(std::string("evc: conv_scatter launch: ") + cudaGetErrorString(e));
     return EVC_ECUDA;
   }
   const TView vout = view_of(*out);
-  const size_t gsm = 4 * (size_t)g->th * g->tw * (g->c_out + 1);
-  EVC_CHECK_ARG(gsm <= 96 * 1024, "conv_scatter: too many output channels for the gather tile");
-  e = launch_pdl(sc::k_scatter_gather, dim3(o.GHo * o.GWo, S), dim3(128), gsm, st, a, map, vout.v, vout.vs,
-                 (int)g->Ho, (int)g->Wo, reinterpret_cast<uint8_t*>(ws + w.prev));
+  auto gk = g->kh == 3 ? sc::k_scatter_gather<3, 6> : sc::k_scatter_gather<1, 6>;
+  const int nstrip = (o.GWo + sc::STRIP - 1) / sc::STRIP;
+  e = launch_pdl(gk, dim3(o.GHo * nstrip, S), dim3(256), 0, st, a, map, vout.v, vout.vs, (int)g->Ho, (int)g->Wo,
+                 reinterpret_cast<uint8_t*>(ws + w.prev));
   if (e != cudaSuccess) {
     set_error(std::string("evc: scatter_gather launch: ") + cudaGetErrorString(e));
     return EVC_ECUDA;

@@ -23,7 +23,7 @@ def main():
             launches.append({"kernel": name.split("(")[0], "dram_read": m["dram__bytes_read.sum"],
                              "dram_write": m.get("dram__bytes_write.sum", 0.0)})
     tot = sum(l["dram_read"] + l["dram_write"] for l in launches) / args.steps
-    print(json.dumps({"sessions": args.sessions, "launches_per_step": len(launches) // args.steps,
+    print(json.dumps({"model": "evflownet-256", "sessions": args.sessions, "launches_per_step": len(launches) // args.steps,
                       "dram_bytes_per_step": tot, "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
                       "-k regex:k_conv, one C1 step (python scripts/profile_step.py --steps 1 --sessions 32)",
                       "launches": launches}, indent=1))

@@ -10,3 +10,13 @@ for k in k_diff_mask k_sparsify_small k_conv_thin k_tiles k_up_sparsify k_conv_p
 done
 timeout 300 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"k_conv_scatter|k_scatter_gather" -c 2 -o gpurun_out/fam_scatter python scripts/scatter_prof.py > /dev/null 2>&1
 ls gpurun_out/*.ncu-rep | wc -l
+timeout 300 ncu --profile-from-start off --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum -k regex:"k_conv" --csv --log-file gpurun_out/conv_traffic_s32.csv python scripts/profile_step.py --steps 1 --sessions 32 > /dev/null 2>&1
+python scripts/conv_traffic.py gpurun_out/conv_traffic_s32.csv --sessions 32 > gpurun_out/r02_conv_traffic_s32.json; head -5 gpurun_out/r02_conv_traffic_s32.json
+timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1_s32.csv python scripts/profile_step.py --steps 1 --sessions 32 > /dev/null 2>&1
+timeout 300 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv python scripts/profile_step.py --steps 2 > /dev/null 2>&1
+python scripts/families_summary.py gpurun_out > gpurun_out/r02_ncu_families.md 2> gpurun_out/fam_sum.err
+for f in gpurun_out/fam_*.ncu-rep; do python scripts/ncu_summary.py $f > ${f%.ncu-rep}.txt 2>/dev/null; done
+ls -la gpurun_out/*.ncu-rep | awk '{s+=$5} END {print s/1e6, "MB of reports"}'
+# keep the two largest-launch reports (dec3 persistent conv, up_sparsify) for source-level reading; drop the rest
+mkdir -p gpurun_out/keep; mv gpurun_out/fam_k_conv_persist.ncu-rep gpurun_out/fam_k_up_sparsify.ncu-rep gpurun_out/keep/ 2>/dev/null
+rm -f gpurun_out/*.ncu-rep; du -sh gpurun_out

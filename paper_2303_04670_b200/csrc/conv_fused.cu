@@ -1776,9 +1776,9 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
                 "conv_fused: shadow layout (cp % 32, thin path +-cp % 4; (H + 2 pad) x (W + 2 pad) pixels per session)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
-  EVC_CHECK_ARG(!sp || (!dense && sp->hwc && sp->cp % 4 == 0 && std::abs(sp->cp) >= g->c_out && sp->hwc_stride % 4 == 0 &&
+  EVC_CHECK_ARG(!sp || (sp->hwc && sp->cp % 4 == 0 && std::abs(sp->cp) >= g->c_out && sp->hwc_stride % 4 == 0 &&
                         sp->pitch >= g->Wo && sp->flags && sp->fany && sp->partials),
-                "conv_fused: fused sparsify needs the shadow, flags, fany and partials (incremental mode)");
+                "conv_fused: fused sparsify needs the shadow, flags, fany and partials");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && meter_part &&
                           ((act >= 0 ? act_out->flags : (out ? out->flags : nullptr)) != nullptr)),
                 "conv_fused: incremental mode needs masks, fany, table, rstate and counters");

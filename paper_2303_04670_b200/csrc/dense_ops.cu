@@ -41,7 +41,7 @@ __global__ void k_sparsify_finalize(const double* __restrict__ partials, int64_t
                                     double tp, double decay, int reset, int S) {
   pdl_wait();
   pdl_trigger();
-  sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, reset, S);
+  sparsify_finalize_all(partials, n, norm_ema, kdev, tp, decay, reset, blockIdx.x + 1, blockIdx.x);  // session = block
 }
 
 __global__ void k_sumsq(const float* __restrict__ x, int64_t xs, int64_t n, double* partials) {
@@ -240,7 +240,7 @@ int evc_act_dense(const float* x, int64_t xs, float* y, int64_t ys, float* acc, 
 int evc_sparsify_finalize(const double* partials, int64_t n, double* norm_ema, double* k, double tp, double decay,
                           int32_t reset, int32_t S, void* stream) {
   EVC_CHECK_ARG(partials && norm_ema && k && S > 0, "sparsify_finalize: null argument");
-  launch_pdl(k_sparsify_finalize, dim3(1), dim3(256), 0, as_stream(stream), partials, n, norm_ema, k, tp, decay, reset, S);
+  launch_pdl(k_sparsify_finalize, dim3(S), dim3(256), 0, as_stream(stream), partials, n, norm_ema, k, tp, decay, reset, S);
   EVC_LAUNCH_CHECK("sparsify_finalize");
   return EVC_OK;
 }

@@ -1025,17 +1025,27 @@ class Graph:
                 din = self._desc(ns.inputs[0], False)
                 plan = node.plan
                 if plan.path == "fused":
-                    pre = plan.prep(din)
-                    run(pre[0], *pre[1])
+                    prod = self._by_id.get(ns.inputs[0])
+                    if not (plan.fed_by_sparsify and prod.sp_fused_by is not None):
+                        pre = plan.prep(din)  # (else the producing conv's epilogue wrote the shadow)
+                        run(pre[0], *pre[1])
                     act = node.fused_act
+                    # conv -> act -> sparsify(t_p = 0) -> conv: the dense epilogue writes the next conv's
+                    # shadow and the sparsify's sum of squares too (no copy / to_hwc / sumsq passes)
+                    spd = node._spd if node.fused_sp is not None else None
                     if act is not None:
                         code, alpha = act.act
                         fa = (code, alpha, act.acc.data_ptr() if mutate else None, act.acc[0].numel(),
                               self._desc(act.spec.id, False))
-                        fn, args = plan.fused(din, None, bias_ptr=_lib.ptr(node.bias), act=fa, dense=True)
+                        fn, args = plan.fused(din, None, bias_ptr=_lib.ptr(node.bias), act=fa, sp=spd, dense=True)
                     else:
                         fn, args = plan.fused(din, self._desc(nid, False), bias_ptr=_lib.ptr(node.bias), dense=True)
                     run(fn, *args)
+                    if spd is not None and mutate:  # the sparsify's reset: norm_ema = ||x|| (sparsify.py:43-51)
+                        sp = node.fused_sp
+                        j = sp.sp_idx
+                        run(L.evc_sparsify_finalize, sp.part_ptr, sp.nparts, self._norm.data_ptr() + 8 * j * S,
+                            self._k.data_ptr() + 8 * j * S, sp.tp, sp.ema_decay, 1, S)
                 else:
                     fn, args = plan.gemm(din, self._desc(nid, False), _lib.ptr(node.bias), None,
                                          self._conv_ws.data_ptr())
@@ -1053,6 +1063,10 @@ class Graph:
                 yp, ys = self._vptr(nid)
                 run(L.evc_act_dense, xp, xs, yp, ys, node.acc.data_ptr() if mutate else None, node.acc[0].numel(),
                     node.acc[0].numel(), code, alpha, S)
+            elif k == "sparsify" and node.sp_fused_by is not None:
+                if mutate:  # values, shadow and norm came from the producing conv's epilogue
+                    node.delta.zero_()
+                    node.dlive.zero_()
             elif k == "sparsify":
                 xp, xs = self._vptr(ns.inputs[0])
                 yp, ys = self._vptr(nid)

@@ -1026,7 +1026,7 @@ class Graph:
                 plan = node.plan
                 if plan.path == "fused":
                     prod = self._by_id.get(ns.inputs[0])
-                    if not (plan.fed_by_sparsify and prod.sp_fused_by is not None):
+                    if not (getattr(plan, "fed_by_sparsify", False) and prod.sp_fused_by is not None):
                         pre = plan.prep(din)  # (else the producing conv's epilogue wrote the shadow)
                         run(pre[0], *pre[1])
                     act = node.fused_act

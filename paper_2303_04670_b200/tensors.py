@@ -302,6 +302,7 @@ class ConvPlan:
         self.T = T
         self.wpack = None
         self.hwc = None
+        self.fed_by_sparsify = False  # set by the Graph: a sparsify writes this conv's input shadow
         self.gi = (-(-h // th), -(-w // tw))  # input tile grid
         if kernel == "tc" and lib.evc_conv_fused_supported(self.g):
             self.path = "fused"

@@ -393,6 +393,7 @@ def conv_roofline(g, xs, evc, nsteps=8):
     del g2
     return {"bound": "tensor", "kernel": f"conv_fused (all {n_launch} conv layers incl. fused mask/meter/activation, per step)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+            "frac_of_3xtf32_ceiling": achieved / (peak / 3.0),  # fp32 accuracy: three TF32 MMAs per product
             "traffic_unit": "bytes per step", "traffic_source": tsrc,
             "peak_source": f"0.5 x {src} bf16 ({bf16} TF) as the TF32 tensor peak",
             "algorithmic_flops_per_step": f, "gemm_ms_per_step": t * 1e3, "gemm_launches_per_step": n_launch,

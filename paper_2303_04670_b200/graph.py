@@ -809,6 +809,7 @@ class Graph:
         """List of (ctypes fn, args-without-stream, name) for one incr_step."""
         L, S = self.lib, self.S
         prog = []
+        self._dense_up = {}  # upsample id -> its fused upsample -> sparsify(t_p = 0) launch
         i32 = self._cnt_step
         for node in self.nodes:
             ns, k = node.spec, node.kind
@@ -897,6 +898,8 @@ class Graph:
                                                        node.part_ptr, None, *hwc,
                                                        0 if sh is not None else 1, 1 if node.tp == 0.0 else 0, S),
                              "upsample_sparsify"))
+                if node.tp == 0.0:  # the dense pass reuses it with every input tile live (_dense_program)
+                    self._dense_up[up.spec.id] = prog[-1]
             elif k == "upsample" and nid in self._fused_up:
                 continue  # evaluated inside the consumer's fused upsample_sparsify
             elif k == "sparsify":
@@ -1026,8 +1029,9 @@ class Graph:
                 plan = node.plan
                 if plan.path == "fused":
                     prod = self._by_id.get(ns.inputs[0])
-                    if not (getattr(plan, "fed_by_sparsify", False) and prod.sp_fused_by is not None):
-                        pre = plan.prep(din)  # (else the producing conv's epilogue wrote the shadow)
+                    if not (getattr(plan, "fed_by_sparsify", False) and
+                            (prod.sp_fused_by is not None or prod.spec.inputs[0] in self._dense_up)):
+                        pre = plan.prep(din)  # (else the producing conv / upsample wrote the shadow)
                         run(pre[0], *pre[1])
                     act = node.fused_act
                     # conv -> act -> sparsify(t_p = 0) -> conv: the dense epilogue writes the next conv's
@@ -1067,6 +1071,21 @@ class Graph:
                 if mutate:  # values, shadow and norm came from the producing conv's epilogue
                     node.delta.zero_()
                     node.dlive.zero_()
+            elif k == "sparsify" and ns.inputs[0] in self._dense_up:
+                # upsample -> sparsify(t_p = 0) -> conv: the fused kernel of the incremental program with every
+                # input tile marked live writes the conv's shadow and the norm partials (no dense upsample,
+                # copy, sum of squares or to_hwc passes); the flags are cleared with the increments afterwards
+                up = self._by_id[ns.inputs[0]]
+                sl = self._slots[up.spec.inputs[0]]
+                sl.store.flags[:, sl.coff:sl.coff + sl.C].fill_(1)
+                fn, args, _ = self._dense_up[up.spec.id]
+                run(fn, *args)
+                if mutate:
+                    j = node.sp_idx
+                    run(L.evc_sparsify_finalize, node.part_ptr, node.nparts, self._norm.data_ptr() + 8 * j * S,
+                        self._k.data_ptr() + 8 * j * S, node.tp, node.ema_decay, 1, S)
+                    node.delta.zero_()
+                    node.dlive.zero_()
             elif k == "sparsify":
                 xp, xs = self._vptr(ns.inputs[0])
                 yp, ys = self._vptr(nid)
@@ -1095,6 +1114,8 @@ class Graph:
                     dst = self._concat_part_desc(nid, off, self.shapes[p][0])
                     n = int(np.prod(self.shapes[p]))
                     run(L.evc_copy_dense, pp, ps, dst.vals, dst.vstride, n, S)
+            elif k == "upsample" and nid in self._dense_up:
+                continue  # evaluated inside its sparsify's fused kernel
             elif k == "upsample":
                 mode = 0 if ns.attrs.get("mode", "nearest") == "nearest" else 1
                 run(L.evc_upsample, self._desc(ns.inputs[0], False), self._desc(nid, False),

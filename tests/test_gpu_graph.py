@@ -293,3 +293,51 @@ def test_sessions_with_tp_match_single_sessions():
         fb, fa = gb.state_fingerprint(session=s), gs[s].state_fingerprint()
         for k in (k for k in fa if k.endswith(".k") or k.endswith(".norm")):
             assert np.allclose(np.asarray(fb[k], np.float64), np.asarray(fa[k], np.float64), rtol=1e-5, atol=1e-6), k
+
+
+def test_evflownet_graph_node_masks_vs_oracle():
+    """The Graph's fused kernels (conv epilogue activation + sparsify, fused upsample -> sparsify,
+    add -> activation) checked per node, not only through the final output: after each of 8 steps,
+    every node's output tile flags as the device graph left them against the oracle's trace (bit-exact
+    except value-derived rounding-zero flips, counted, whose oracle values must be <= 1e-6 * scale),
+    and the values of every node whose planar output the graph materialises (<= 1e-4 * scale)."""
+    spec = configs.evflownet_spec(tp=0.0)
+    weights = evc.WeightManifest.random_tensors(spec, 0)
+    xs = evflownet_inputs(8, seed=3)
+    g = evc.build(spec, weights, refresh_interval=0)
+    og = O.OracleGraph(spec.to_dict(), weights, refresh_interval=0)
+    g.dense_pass(xs[0])
+    og.dense_pass(np_(xs[0]))
+    flips, checked_f, checked_v = 0, 0, 0
+    # not materialised at all: the fused upsample (inside its sparsify), an add evaluated with its
+    # activation, a conv whose activation runs in its epilogue (its mask is the activation's,
+    # increment_ops.py:232-238, checked there)
+    skip = {n.spec.id for n in g.nodes if (n.kind == "upsample" and n.spec.id in g._fused_up)
+            or (n.kind == "add" and n.add_fused) or (n.kind == "conv" and n.fused_act is not None)}
+    for i in range(1, 9):
+        g.incr_step(evc.step_increment(xs[i - 1], xs[i], spec.tile))
+        trace = {}
+        og.incr_step(*O.step_increment(np_(xs[i - 1]), np_(xs[i]), 6, 6), trace=trace)
+        for n in g.nodes:
+            nid = n.spec.id
+            if nid in skip:
+                continue
+            gv, gf = g._slot_view(nid)
+            ov, of = trace[nid]
+            gf = gf[0].cpu().numpy().astype(bool)
+            diff = gf != of
+            scale = max(1.0, float(np.abs(ov).max()))
+            if diff.any():
+                flips += int(diff.sum())
+                px = O.flags_to_pixels(diff, 6, 6, ov.shape[1], ov.shape[2])
+                assert np.abs(np.where(px, ov, 0)).max() <= 1e-6 * scale, (i, nid)
+            checked_f += 1
+            materialised = not ((n.kind in ("relu", "tanh") and n.fused_into is not None and not n.act_values_needed)
+                                or (n.kind == "sparsify" and (n.sp_fused_by is not None or n.shadow is not None)))
+            if materialised:
+                assert max_err(gv[0].cpu().numpy(), ov) <= 1e-4, (i, nid, max_err(gv[0].cpu().numpy(), ov))
+                checked_v += 1
+    print(f"C1 graph node masks over 8 steps: {checked_f} node-steps, {flips} flipped tiles, "
+          f"{checked_v} node-steps with values")
+    assert flips <= 8 * 4
+    assert checked_f >= 8 * 38  # 58 nodes minus the fused-away ones

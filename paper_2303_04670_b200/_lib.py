@@ -13,7 +13,7 @@ from pathlib import Path
 import torch
 
 LIB_PATH = Path(__file__).resolve().parent / "libevconv.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 ENC = {"count": 0, "timestamp": 1, "voxel": 2}
 ACT = {"relu": 0, "sigmoid": 1, "tanh": 2, "leaky_relu": 3}
@@ -47,6 +47,11 @@ class EvcConvSparsify(C.Structure):
                 ("fstride", C.c_int64), ("fany", C.c_void_p), ("partials", C.c_void_p)]
 
 
+class EvcConvSubpixel(C.Structure):
+    _fields_ = [("c_out", C.c_int32), ("Ho", C.c_int32), ("Wo", C.c_int32), ("reserved", C.c_int32),
+                ("fany_in", C.c_void_p), ("border", C.c_void_p)]
+
+
 class EvcMeterNode(C.Structure):
     _fields_ = [("part", C.c_void_p), ("n", C.c_int64), ("nflags", C.c_int64), ("dense", C.c_int64),
                 ("c_out", C.c_int32), ("reserved", C.c_int32)]
@@ -66,6 +71,7 @@ _T = C.POINTER(EvcTensor)
 _G = C.POINTER(EvcConvGeom)
 _CF = C.POINTER(EvcConvCfg)
 _SP = C.POINTER(EvcConvSparsify)
+_SUB = C.POINTER(EvcConvSubpixel)
 
 _PROTOS = {
     "evc_version": (_I32, []),
@@ -101,6 +107,10 @@ _PROTOS = {
     "evc_conv_fused_ctas": (_I64, [_G, _CF]),
     "evc_conv_fused": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _T, _I32, _F, _P, _I64, _T,
                               _SP, _I32, _I32, _P]),
+    "evc_conv_fused_subpixel": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _T, _I32, _F, _P, _I64,
+                                       _T, _SP, _SUB, _I32, _I32, _P]),
+    "evc_subpixel_prep": (_I32, [_T, _P, _I32, _I64, _I32, _P, _I32, _P]),
+    "evc_subpixel_border": (_I32, [_T, _P, _I32, _P, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
     "evc_conv_trace": (_I32, [_P]),
     "evc_meter_step": (_I32, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _P]),

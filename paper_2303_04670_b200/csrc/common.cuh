@@ -287,6 +287,7 @@ int init_conv();
 int init_conv_mask();
 int init_conv_fused();
 int init_conv_scatter();
+int init_subpixel();
 int init_elementwise();
 int init_bands();
 int init_upsparsify();

@@ -92,6 +92,16 @@ struct Args {
   uint8_t* sp_fany;
   double* sp_part;
   unsigned long long* trace;  // debug: per-CTA phase timestamps (evc_conv_trace), normally NULL
+  // output geometry of the emitted tensor (= Ho, Wo, c_out unless sub)
+  int eHo, eWo, oc;
+  // sub-pixel mode (evc_conv_fused_subpixel): this launch is the 2x bilinear upsample -> 3x3 conv
+  // pair rewritten as a 3x3 conv on the low-res input with 4 * oc composed output channels
+  // (phase p = n / oc -> output site (2u + p / 2, 2x + p % 2)); fany is then the low-res region map,
+  // fany_side the any-channel map of the high-res conv input (flags, meter, output masking),
+  // border[s][2 (eHo + eWo)][oc] the correction of the high-res border lines
+  int sub;
+  const uint8_t* fany_side;
+  const float* border;
 };
 
 static unsigned long long* g_trace = nullptr;
@@ -118,12 +128,12 @@ __device__ __noinline__ void side_work(const Args& a, int s, int q, int Qs, int 
   const TabHdr& h = *reinterpret_cast<const TabHdr*>(a.tab);
   const int To = h.GHo * h.GWo, Ti = h.GHi * h.GWi, GWo = h.GWo, GWi = h.GWi;
   const int nthr = Qs * 64, gid = q * 64 + t;
-  const uint8_t* fa = a.fany + (int64_t)s * Ti;
+  const uint8_t* fa = a.fany_side + (int64_t)s * Ti;
   const int32_t* boxr = a.tab + h.boxr;
   const int32_t* boxc = a.tab + h.boxc;
   // output tile flags, (channel, tile) order -> coalesced byte stores
   uint8_t* of = a.oflags + (int64_t)s * a.ofs;
-  const int nflag = a.c_out * To;
+  const int nflag = a.oc * To;
   for (int e = gid; e < nflag; e += nthr) {
     const int tt = e % To;
     const int i = tt / GWo, j = tt - i * GWo;
@@ -188,17 +198,79 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
 // Every global load is issued before any store so the latencies overlap.  Called by
 // every lane of a warp with warp-uniform (n0, step, cnt): the fused sparsify uses
 // warp ballots.  Returns the site's sum of squared sparsify outputs (0 if unfused).
+// Sub-pixel mode: composed channel n of low-res site (u, x) -> output channel and high-res site.
+// (Channel groups never straddle a phase: oc % 16 == 0 and groups start at multiples of their size.)
+__device__ __forceinline__ void sub_site(const Args& a, int& u, int& x, int& n) {
+  if (!a.sub) return;
+  const int ph = n / a.oc;
+  n -= ph * a.oc;
+  if (u < a.Ho && x < a.Wo) {
+    u = 2 * u + (ph >> 1);
+    x = 2 * x + (ph & 1);
+  } else {
+    u = a.eHo;  // never valid
+  }
+}
+
+// Sub-pixel mode, incremental: is output tile (u / th, x / tw) live?  The OR of the high-res input's
+// any-channel map over its receptive box (what side_work writes as the output flags).  A composed
+// value can be a rounding-level nonzero where the oracle's upsampled input is exactly zero; the flags
+// say dead there, so the value is forced to the oracle's exact zero.
+__device__ __forceinline__ bool sub_tile_live(const Args& a, int s, int u, int x) {
+  const TabHdr& h = *reinterpret_cast<const TabHdr*>(a.tab);
+  const int32_t* boxr = a.tab + h.boxr;
+  const int32_t* boxc = a.tab + h.boxc;
+  const int i = u / a.th, j = x / a.tw;
+  const uint8_t* fa = a.fany_side + (int64_t)s * h.GHi * h.GWi;
+  int nf = 0;
+  for (int r = boxr[2 * i]; r <= boxr[2 * i + 1]; ++r)
+    for (int c = boxc[2 * j]; c <= boxc[2 * j + 1]; ++c) nf |= fa[r * h.GWi + c];
+  return nf != 0;
+}
+
+// Sub-pixel extras of a valid high-res site, out of line (keeps the common emit's registers):
+// the border-line correction pointer and the output-tile mask.
+struct SubSite {
+  const float* bc;
+  int masked;
+};
+// sub_live: the caller's sub_tile_live of this site (all four phases of a low-res site share one
+// output tile: th, tw even), or -1 to evaluate it here.
+__device__ __forceinline__ SubSite sub_extras(const Args& a, int s, int u, int x, int n0, int sub_live) {
+  SubSite r = {nullptr, 0};
+  if (u == 0 || x == 0 || u == a.eHo - 1 || x == a.eWo - 1) {
+    const int li = u == 0 ? x : (u == a.eHo - 1 ? a.eWo + x : (x == 0 ? 2 * a.eWo + u : 2 * a.eWo + a.eHo + u));
+    r.bc = a.border + ((int64_t)s * 2 * (a.eHo + a.eWo) + li) * a.oc + n0;
+  }
+  r.masked = !a.dense && !(sub_live >= 0 ? sub_live != 0 : sub_tile_live(a, s, u, x));
+  return r;
+}
+
+// Sub-pixel, incremental: the output-tile liveness shared by the four phase sites of low-res site
+// (u, x) (-1 when not applicable), evaluated once per work item.
+__device__ __forceinline__ int sub_live_of(const Args& a, int s, int u, int x) {
+  if (!a.sub || a.dense || u >= a.Ho || x >= a.Wo) return -1;
+  return sub_tile_live(a, s, 2 * u, 2 * x) ? 1 : 0;
+}
+
 template <int N>
 __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n0, int step, int cnt,
-                                       const float* vals) {
-  const bool valid = u < a.Ho && x < a.Wo;
-  const int64_t plane = (int64_t)a.Ho * a.Wo;
-  const int64_t base = (int64_t)n0 * plane + (int64_t)u * a.Wo + x;
+                                       const float* vals, int sub_live = -1) {
+  sub_site(a, u, x, n0);
+  const bool valid = u < a.eHo && x < a.eWo;
+  const int64_t plane = (int64_t)a.eHo * a.eWo;
+  const int64_t base = (int64_t)n0 * plane + (int64_t)u * a.eWo + x;
   const int64_t dn = (int64_t)step * plane;
   float v[N], y[N];
+  SubSite ss0 = {nullptr, 0};
+  if (a.sub && valid) ss0 = sub_extras(a, s, u, x, n0, sub_live);
+  const float* bc = ss0.bc;
+  const bool masked = ss0.masked != 0;
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     v[j] = vals[j];
+    if (bc && j < cnt) v[j] = __fadd_rn(v[j], bc[j * step]);
+    if (masked) v[j] = 0.0f;
     if (valid && j < cnt && a.dense && a.bias) v[j] = __fadd_rn(v[j], __ldg(a.bias + n0 + j * step));
     y[j] = v[j];
   }
@@ -280,6 +352,16 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   return (double)ss;
 }
 
+
+// Restore exact zeros of channel n at site (u, x) of a region computed last step and dead now.
+__device__ __forceinline__ void zero_site(const Args& a, int s, int u, int x, int n) {
+  sub_site(a, u, x, n);
+  if (u >= a.eHo || x >= a.eWo) return;
+  const int64_t off = (int64_t)n * a.eHo * a.eWo + (int64_t)u * a.eWo + x;
+  if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
+  if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
+  if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp), a.sp_cp, n, 0.0f);
+}
 
 // Output site of TMEM lane m in region rr.
 __device__ __forceinline__ void site_of(const Args& a, int rr, int m, int& u, int& x) {
@@ -443,11 +525,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         const int n = n0 + e / BM, m = e % BM;
         int u, x;
         site_of(a, rr, m, u, x);
-        if (u >= a.Ho || x >= a.Wo) continue;
-        const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
-        if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
-        if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
-        if (a.sp_hwc) hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp), a.sp_cp, n, 0.0f);
+        zero_site(a, s, u, x, n);
       }
       if (threadIdx.x == 0) a.rstate[rs_idx] = 0;
     }
@@ -476,6 +554,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     const int m = 32 * (warp & 3) + lane;
     int u, x;
     site_of(a, rr, m, u, x);
+    const int sl = sub_live_of(a, s, u, x);
     const int n_main = nk < NA ? nk : NA;
     const uint32_t trow = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     float* P = reinterpret_cast<float*>(smem);
@@ -524,7 +603,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         }
         if (a.splits == 1) {
           const int n0 = nblk * BN + c0;
-          ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
+          ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals, sl);
         } else {
   #pragma unroll
           for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
@@ -646,7 +725,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     __syncwarp();
   } else if (warp < 4) {
     if (!a.dense) {
-      if (a.act >= 0) {  // warm L2 with the accumulator lines the epilogue will read
+      if (a.act >= 0 && !a.sub) {  // warm L2 with the accumulator lines the epilogue will read
         const int per = (a.bn + a.splits - 1) / a.splits;
         const int lo = a.splits > 1 ? z * per : 0, hi = a.splits > 1 ? min(a.bn, lo + per) : a.bn;
         const int64_t plane = (int64_t)a.Ho * a.Wo;
@@ -667,6 +746,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     const int m = 32 * (warp & 3) + lane;  // TMEM lane = region site
     int u, x;
     site_of(a, rr, m, u, x);
+    const int sl = sub_live_of(a, s, u, x);
     if (D == 0) {  // (promotion mode waits segment by segment: the MMAs need the promoted blocks back)
       bar_wait(acc_bar, 0);
       fence_after();
@@ -727,7 +807,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         }
         asm volatile("bar.sync 2, 128;" ::: "memory");
         const int n0 = nblk * BN + c0;
-        ssq += emit<8>(a, s, u, x, n0, 1, min(8, a.c_out - n0), o);
+        ssq += emit<8>(a, s, u, x, n0, 1, min(8, a.c_out - n0), o, sl);
       }
     } else if (D > 0) {
       // promotion: every segment's [main | small] block is added into fp32 register sums (RN) while
@@ -805,6 +885,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
       const int m = 32 * (warp & 3) + lane;
       int u, x;
       site_of(a, rr, m, u, x);
+      const int sl = sub_live_of(a, s, u, x);
       const int cb = (wide && warp < 4) ? BP / 2 : 0, ce = (wide && warp >= 4) ? BP / 2 : BP;
       const float* X = reinterpret_cast<const float*>(smem);
 #pragma unroll 1
@@ -813,7 +894,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 #pragma unroll
         for (int e = 0; e < 16; ++e) vals[e] = X[(c0 + e) * BM + m];
         const int n0 = nblk * BN + c0;
-        if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals);
+        if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals, sl);
       }
     }
   }
@@ -825,13 +906,14 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     const int nsp = a.splits;
-    const int per = (BN + nsp - 1) / nsp;
+    const int per = (((BN + nsp - 1) / nsp) + 3) & ~3;  // 4-aligned slices: emit groups never straddle a phase
     const int rank = (int)cl.block_rank();
     const int lo = rank * per, hi = min(BN, lo + per);
     float* P = reinterpret_cast<float*>(smem);
     const int m = threadIdx.x % BM, g = threadIdx.x / BM;  // 2 groups of 128 sites, 4 contiguous channels each
     int u, x;
     site_of(a, rr, m, u, x);
+    const int sl = sub_live_of(a, s, u, x);
     constexpr int NB = 4;
     for (int nl0 = lo + NB * g; nl0 < hi; nl0 += 2 * NB) {
       const int cnt = min(NB, hi - nl0);
@@ -853,7 +935,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
           if (zz < nsp) sum[j] = __fadd_rn(sum[j], t[zz][j]);
       }
       const int n0 = nblk * BN + nl0;
-      ssq += emit<NB>(a, s, u, x, n0, 1, min(cnt, a.c_out - n0), sum);
+      ssq += emit<NB>(a, s, u, x, n0, 1, min(cnt, a.c_out - n0), sum, sl);
     }
     cluster_sync();
   }
@@ -1097,16 +1179,10 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
         if (prev) {  // computed last step, dead now: restore exact zeros
           const int n0 = nblk * BN, nn = min(BN, a.c_out - n0);
           if (u < a.Ho && x < a.Wo)
-            for (int n = n0; n < n0 + nn; ++n) {
-              const int64_t off = (int64_t)n * a.Ho * a.Wo + (int64_t)u * a.Wo + x;
-              if (a.out) a.out[(int64_t)s * a.ovs + off] = 0.0f;
-              if (a.yact) a.yact[(int64_t)s * a.yvs + off] = 0.0f;
-              if (a.sp_hwc)
-                hwc_store(a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp), a.sp_cp, n,
-                          0.0f);
-            }
+            for (int n = n0 + half; n < n0 + nn; n += NH) zero_site(a, s, u, x, n);
         }
       } else {
+        const int sl = sub_live_of(a, s, u, x);
         if (packed) {
           // per segment and 8-channel chunk: v_s = A.B_lo + A.B_hi of tap s, out[m] = sum_s v_s[m + s]
           // (shifts by s rows = shuffles inside the warp, the next warp's first rows through shared
@@ -1186,7 +1262,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 #pragma unroll
           for (int cc = 0; cc < CH; cc += 8) {
             const int c0 = half * CH + cc;
-            ssq += emit<8>(a, s, u, x, n0 + c0, 1, min(8, a.c_out - n0 - c0), O + cc);
+            ssq += emit<8>(a, s, u, x, n0 + c0, 1, min(8, a.c_out - n0 - c0), O + cc, sl);
           }
         } else {
           constexpr int CB = BN / NH;  // channels of this half
@@ -1222,7 +1298,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 #pragma unroll
           for (int cc = 0; cc < CB; cc += 16) {
             const int n0 = nblk * BN + half * CB + cc;
-            ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), acc + cc);
+            ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), acc + cc, sl);
           }
         }
       }
@@ -1750,12 +1826,12 @@ int64_t evc_conv_fused_state_len(const evc_conv_geom* g, const evc_conv_cfg* cfg
   return (int64_t)S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);
 }
 
-int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const float* in_hwc, int32_t cp,
-                   int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
-                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
-                   const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
-                   const evc_tensor* act_out, const evc_conv_sparsify* sp, int32_t dense, int32_t S,
-                   void* stream) {
+static int conv_fused_impl(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const float* in_hwc, int32_t cp,
+                           int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
+                           const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
+                           const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
+                           const evc_tensor* act_out, const evc_conv_sparsify* sp, const evc_conv_subpixel* sub,
+                           int32_t dense, int32_t S, void* stream) {
   EVC_CHECK_ARG(g && cfg_in && in_hwc && wpack && S > 0 && fz::valid_bn(cfg_in->bn), "conv_fused: null argument");
   // The dense pass (full-magnitude values, not increments) always runs promoted (K-segments of one
   // K-block in row mode, two otherwise), so its accumulation chains stay as short as fp32 needs.
@@ -1776,8 +1852,14 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
                 "conv_fused: shadow layout (cp % 32, thin path +-cp % 4; (H + 2 pad) x (W + 2 pad) pixels per session)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
-  EVC_CHECK_ARG(!sp || (sp->hwc && sp->cp % 4 == 0 && std::abs(sp->cp) >= g->c_out && sp->hwc_stride % 4 == 0 &&
-                        sp->pitch >= g->Wo && sp->flags && sp->fany && sp->partials),
+  EVC_CHECK_ARG(!sub || (sub->c_out > 0 && sub->c_out % 16 == 0 && g->c_out == 4 * sub->c_out && g->kh == 3 &&
+                         g->kw == 3 && g->stride == 1 && g->pad == 1 && sub->Ho == 2 * g->Ho && sub->Wo == 2 * g->Wo &&
+                         !cfg->thin && sub->border && (dense || sub->fany_in)),
+                "conv_fused_subpixel: needs a 3x3 stride-1 pad-1 geometry with 4 x c_out (c_out % 16 == 0) "
+                "composed channels, the border correction and the high-res any-channel map");
+  const int eHo = sub ? sub->Ho : g->Ho, eWo = sub ? sub->Wo : g->Wo, oc = sub ? sub->c_out : g->c_out;
+  EVC_CHECK_ARG(!sp || (sp->hwc && sp->cp % 4 == 0 && std::abs(sp->cp) >= oc && sp->hwc_stride % 4 == 0 &&
+                        sp->pitch >= eWo && sp->flags && sp->fany && sp->partials),
                 "conv_fused: fused sparsify needs the shadow, flags, fany and partials");
   EVC_CHECK_ARG(dense || (in && in->flags && fany && table && rstate && meter_part &&
                           ((act >= 0 ? act_out->flags : (out ? out->flags : nullptr)) != nullptr)),
@@ -1847,6 +1929,15 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
   a.bias = bias;
   a.dense = dense != 0;
   a.trace = fz::g_trace;
+  a.eHo = eHo;
+  a.eWo = eWo;
+  a.oc = oc;
+  a.fany_side = fany;
+  if (sub) {
+    a.sub = 1;
+    a.fany_side = sub->fany_in;
+    a.border = sub->border;
+  }
   if (!a.dense) {
     const TView vin = view_of(*in);
     a.fany = fany;
@@ -1872,8 +1963,8 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
     a.sp_hs = sp->hwc_stride;
     a.sp_cp = sp->cp;
     a.sp_pitch = sp->pitch;
-    a.sp_GH = (g->Ho + g->th - 1) / g->th;
-    a.sp_GW = (g->Wo + g->tw - 1) / g->tw;
+    a.sp_GH = (eHo + g->th - 1) / g->th;
+    a.sp_GW = (eWo + g->tw - 1) / g->tw;
     a.sp_flags = sp->flags;
     a.sp_fs = sp->fstride;
     a.sp_fany = sp->fany;
@@ -1930,6 +2021,27 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, const flo
   }
   EVC_LAUNCH_CHECK("conv_fused");
   return EVC_OK;
+}
+
+int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
+                   int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
+                   const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
+                   const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
+                   const evc_tensor* act_out, const evc_conv_sparsify* sp, int32_t dense, int32_t S,
+                   void* stream) {
+  return conv_fused_impl(g, cfg, in_hwc, cp, hwc_stride, wpack, bias, in, fany, table, rstate, meter_part, out, act,
+                         alpha, acc, acc_stride, act_out, sp, nullptr, dense, S, stream);
+}
+
+int evc_conv_fused_subpixel(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float* in_hwc, int32_t cp,
+                            int64_t hwc_stride, const float* wpack, const float* bias, const evc_tensor* in,
+                            const uint8_t* fany, const int32_t* table, uint8_t* rstate, int64_t* meter_part,
+                            const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
+                            const evc_tensor* act_out, const evc_conv_sparsify* sp, const evc_conv_subpixel* sub,
+                            int32_t dense, int32_t S, void* stream) {
+  EVC_CHECK_ARG(sub, "conv_fused_subpixel: null sub-pixel descriptor");
+  return conv_fused_impl(g, cfg, in_hwc, cp, hwc_stride, wpack, bias, in, fany, table, rstate, meter_part, out, act,
+                         alpha, acc, acc_stride, act_out, sp, sub, dense, S, stream);
 }
 
 int evc_conv_trace(void* buf) {

@@ -289,6 +289,7 @@ int init_conv() {
   int rc = init_conv_mask();
   if (!rc) rc = init_conv_tc();
   if (!rc) rc = init_conv_fused();
-  return rc ? rc : init_conv_scatter();
+  if (!rc) rc = init_conv_scatter();
+  return rc ? rc : init_subpixel();
 }
 }  // namespace evc

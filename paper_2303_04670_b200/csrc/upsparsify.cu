@@ -203,31 +203,34 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
       __syncthreads();
       if (q < Q) {
         const float* rc = s_r + cl * RS;
-        const int rstride = a.hp * hwc_px(a.cp);  // floats between shadow rows (< 2^31 per session)
-        float* sbase = a.hwc + (int64_t)s * a.hs + hwc_head(a.cp, c0 + cl);
-        const int tl = a.cp < 0 ? -1 : hwc_unit(a.cp);  // tail offset (32 floats: an immediate); -1: fp32
+        // (no shadow: flags, any-map and norm partials only -- the sub-pixel conv reads the low-res input)
+        const bool wr = a.hwc != nullptr;
+        const int rstride = wr ? a.hp * hwc_px(a.cp) : 0;  // floats between shadow rows (< 2^31 per session)
+        float* sbase = wr ? a.hwc + (int64_t)s * a.hs + hwc_head(a.cp, c0 + cl) : nullptr;
+        const int tl = !wr ? 0 : (a.cp < 0 ? -1 : hwc_unit(a.cp));  // tail offset (32 floats: an immediate); -1: fp32
         const int obase = r0 * rstride + x0 * hwc_px(a.cp);
         float ssf = 0.0f;
         for (int xq = warp * Q + q; xq < ncol; xq += (US_THREADS / 32) * Q) {
         // the column's taps once (before any s_ny store of this column)
         const int tj = s_tj[xq], o0 = s_ci0[xq] - clo, o1 = s_ci1[xq] - clo;
         const float cw0 = s_cw0[xq], cw1 = s_cw1[xq];
-        float* dcol = sbase + obase + xq * hwc_px(a.cp);
+        float* dcol = wr ? sbase + obase + xq * hwc_px(a.cp) : nullptr;
         for (int tr = 0; tr < nti; ++tr) {
           const int ti = cl * NT + tr * nj + tj;
           if (!s_proc[ti]) continue;  // not live now nor last step: the shadow already holds zeros
           const int ra = tr * y.th, rb = min(nrow, ra + y.th);
           const float* p0 = rc + ra * a.XC + o0;
           const float* p1 = rc + ra * a.XC + o1;
-          float* d = dcol + ra * rstride;
+          float* d = wr ? dcol + ra * rstride : nullptr;
           uint32_t nzb = 0;  // OR of the magnitude bits: nonzero iff some value != +-0
           // same float32 op order as upsample_at (rows first, then columns)
           auto row = [&](int k) {
             const float up = a.mode == 0 ? p0[k * a.XC]
                                          : __fadd_rn(__fmul_rn(p0[k * a.XC], cw0), __fmul_rn(p1[k * a.XC], cw1));
             const float ov = __fadd_rn(0.0f, up);
-            float* dk = d + (int64_t)k * rstride;
-            if (tl < 0) {  // fp32 shadow (hwc_px)
+            float* dk = wr ? d + (int64_t)k * rstride : nullptr;
+            if (!wr) {
+            } else if (tl < 0) {  // fp32 shadow (hwc_px)
               dk[0] = ov;
             } else {
               const float h = tf32_head(ov);
@@ -380,7 +383,8 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   EVC_CHECK_ARG(factor == 2 || factor == 4, "upsample_sparsify: factor must be 2 or 4");
   EVC_CHECK_ARG(mode == 0 || mode == 1, "upsample_sparsify: unknown mode");
   EVC_CHECK_ARG(y->H == x->H * factor && y->W == x->W * factor && y->C == x->C, "upsample_sparsify: shape");
-  EVC_CHECK_ARG(write_chw || hwc, "upsample_sparsify: no output requested");
+  EVC_CHECK_ARG(write_chw || hwc || (delta_zero && tp == 0.0 && fany),
+                "upsample_sparsify: no output requested (flags-only needs t_p = 0, a zero residual and fany)");
   EVC_CHECK_ARG(!hwc || (std::abs(cp) >= y->C && cp % 4 == 0 && hwc_pitch >= y->W),
                 "upsample_sparsify: shadow channel count must cover C (multiple of 32), pitch >= W");
   USArgs a;
@@ -405,7 +409,7 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.f = factor;
   a.mode = mode;
   us_grid(a.y, a.CW, a.nCG, a.nJC);
-  a.fast = (delta_zero && tp == 0.0 && !write_chw && hwc) ? 1 : 0;
+  a.fast = (delta_zero && tp == 0.0 && !write_chw) ? 1 : 0;
   // two tile rows per CTA on the fast path when their tiles fit the per-CTA flag tables
   a.RT = (a.fast && 2 * (a.CW / a.y.tw) <= US_MAXJ && 2 * a.y.th <= US_MAXR) ? 2 : 1;
   a.pstride = a.y.GH * a.nCG * a.nJC;

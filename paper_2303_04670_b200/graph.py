@@ -553,6 +553,7 @@ class Graph:
             if node.kind == "delay":  # reads its source's values at the end of every step
                 self._consumers[node.spec.attrs["source"]].append(node.spec.id)
             node.shadow = None
+            node.subpixel_conv = None  # sparsify: its only reader is a conv in sub-pixel form
             node.fused_into = None
             node.sp_fused_by = None  # sparsify evaluated in a producing conv's epilogue
             node.fused_sp = None
@@ -627,9 +628,12 @@ class Graph:
             if k == "conv":
                 st_, pad_ = node.conv_attrs
                 src = self._slots[node.spec.inputs[0]].store
+                node.subpixel_up = self._subpixel_source(node, st_, pad_, ish)
                 node.plan = ConvPlan(node.weight, st_, pad_, ish[1], ish[2], tile.h, tile.w, S,
                                      vstride=src.C * src.H * src.W, kernel=self.conv_kernel,
-                                     max_splits=self.max_splits)
+                                     max_splits=self.max_splits, subpixel=node.subpixel_up is not None)
+                if node.subpixel_up is not None:
+                    self._by_id[node.spec.inputs[0]].subpixel_conv = node
                 max_T = max(max_T, S * node.plan.T)
                 max_ws = max(max_ws, node.plan.ws_floats)
                 node.fused_act = None
@@ -720,6 +724,8 @@ class Graph:
             if node.kind == "conv":
                 if node.plan.path == "fused" and not node.scatter:
                     fany_off.append((node, take(S * node.plan.gi[0] * node.plan.gi[1])))
+                    if node.plan.subpixel:  # + the low-res map of the composed conv
+                        fany_off.append((node, -take(S * node.plan.gl[0] * node.plan.gl[1]) - 1))
                 else:
                     n = int(self.lib.evc_conv_mask_scratch(node.plan.g, S))
                     conv_off.append((node, take(8), take(4 * n)))
@@ -728,7 +734,10 @@ class Graph:
         for node, c_off, s_off in conv_off:
             node.mask_scratch = (base + c_off, base + s_off)
         for node, o in fany_off:
-            node.plan.fany_ptr = base + o
+            if o < 0:
+                node.plan.fany_lo_ptr = base + (-o - 1)
+            else:
+                node.plan.fany_ptr = base + o
         for node, o in sp_off:
             st = self._slots[node.spec.id].store
             st.flags = self._zero[o:o + st.flags.numel()].view(st.flags.shape)
@@ -776,6 +785,24 @@ class Graph:
         self._drift_buf = torch.zeros(S, dtype=torch.float32, device=dev)
         self._program = self._build_incr_program()
 
+    def _subpixel_source(self, node, stride, pad, ish):
+        """The upsample node when `node` reads upsample(2x bilinear) -> sparsify(t_p = 0) -> node
+        with nothing else reading either, so the pair runs in sub-pixel form (ConvPlan._init_subpixel):
+        the sparsify only derives flags, any-map and norm partials, the conv reads the low-res input."""
+        sp = self._by_id.get(node.spec.inputs[0])
+        if (sp is None or sp.kind != "sparsify" or sp.tp != 0.0 or self._consumers[sp.spec.id] != [node.spec.id]
+                or sp.spec.id in self.output_ids or node.spec.id in self.scatter_convs):
+            return None
+        up = self._by_id.get(sp.spec.inputs[0])
+        if (up is None or up.kind != "upsample" or up.spec.attrs.get("mode", "nearest") != "bilinear"
+                or int(up.spec.attrs.get("factor", 2)) != 2 or self._consumers[up.spec.id] != [sp.spec.id]
+                or up.spec.id in self.output_ids
+                or self.tile.w > 32 or self.tile.h > 8 or os.environ.get("EVC_NO_UPFUSE", "0") == "1"):
+            return None
+        if not ConvPlan.subpixel_ok(node.weight, stride, pad, ish[1], ish[2]):
+            return None
+        return up
+
     def _dense_equiv(self, node) -> int:
         if node.kind == "conv":
             return node.plan.dense_flops
@@ -810,6 +837,7 @@ class Graph:
         L, S = self.lib, self.S
         prog = []
         self._dense_up = {}  # upsample id -> its fused upsample -> sparsify(t_p = 0) launch
+        self._dense_subpixel = {}  # upsample id -> the sub-pixel conv's input launches
         i32 = self._cnt_step
         for node in self.nodes:
             ns, k = node.spec, node.kind
@@ -889,6 +917,8 @@ class Graph:
                 sh = node.shadow
                 hwc = ((sh.hwc_interior, sh.cpa, sh.hwc[0].numel(), sh.pitch, sh.fany_ptr) if sh is not None
                        else (None, 0, 0, 0, None))
+                if node.subpixel_conv is not None:  # flags / any-map / partials only: the conv reads low-res
+                    hwc = (None, 0, 0, 0, sh.fany_ptr)
                 mode = 0 if up.spec.attrs.get("mode", "nearest") == "nearest" else 1
                 prog.append((L.evc_upsample_sparsify, (self._desc(up.spec.inputs[0]), int(up.spec.attrs.get("factor", 2)),
                                                        mode, node.delta.data_ptr(), node.delta[0].numel(),
@@ -900,6 +930,10 @@ class Graph:
                              "upsample_sparsify"))
                 if node.tp == 0.0:  # the dense pass reuses it with every input tile live (_dense_program)
                     self._dense_up[up.spec.id] = prog[-1]
+                if node.subpixel_conv is not None:
+                    extra = node.subpixel_conv.plan.subpixel_launches(self._desc(up.spec.inputs[0]))
+                    prog.extend(extra)
+                    self._dense_subpixel[up.spec.id] = extra
             elif k == "upsample" and nid in self._fused_up:
                 continue  # evaluated inside the consumer's fused upsample_sparsify
             elif k == "sparsify":
@@ -1080,6 +1114,8 @@ class Graph:
                 sl.store.flags[:, sl.coff:sl.coff + sl.C].fill_(1)
                 fn, args, _ = self._dense_up[up.spec.id]
                 run(fn, *args)
+                for fn, args, _ in self._dense_subpixel.get(up.spec.id, []):
+                    run(fn, *args)  # (values only: same launches read the dense low-res input)
                 if mutate:
                     j = node.sp_idx
                     run(L.evc_sparsify_finalize, node.part_ptr, node.nparts, self._norm.data_ptr() + 8 * j * S,

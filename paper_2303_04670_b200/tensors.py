@@ -246,6 +246,11 @@ def conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw):
 
 
 CONV_KERNEL = os.environ.get("EVC_CONV_KERNEL", "tc")  # "tc" (tcgen05 3xTF32), "tile" (gathered tiles only), "simt"
+# Sub-pixel decoder convs (ConvPlan._init_subpixel) are opt-in (EVC_SUBPIXEL=1): measured on C1 at 32
+# streams the composed conv reads 4x fewer operand bytes but costs the same (epilogue-bound), and the
+# extra low-res shadow / border passes make the step slower (measured and rejected).  Only
+# thin decoder convs qualify: with C_out > 32 the composed conv was no faster even in isolation.
+SUBPIXEL_MAX_COUT = int(os.environ.get("EVC_SUBPIXEL_MAX_COUT", "32"))
 
 
 def pack_conv_weight(weight: torch.Tensor):
@@ -290,10 +295,14 @@ class ConvPlan:
     """
 
     def __init__(self, weight: torch.Tensor, stride, pad, h, w, th, tw, S=1, vstride=None, kernel=None,
-                 max_splits: int = 0):
+                 max_splits: int = 0, subpixel: bool = False):
         lib = _lib.lib()
         c_out, c_in, kh, kw = (int(v) for v in weight.shape)
         self.g, self.table = conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw)
+        self.subpixel = False
+        if subpixel:  # (the Graph checked subpixel_ok: the input is a 2x bilinear upsample)
+            self._init_subpixel(weight, h, w, th, tw, S, max_splits)
+            return
         self.c_out, self.c_in, self.kh, self.kw, self.S = c_out, c_in, kh, kw, S
         self.weight = weight
         kernel = kernel or CONV_KERNEL
@@ -336,6 +345,64 @@ class ConvPlan:
             self.ws_floats = int(lib.evc_conv_workspace(self.g, S * T, self.splits))
         self.dense_flops = 2 * kh * kw * c_in * c_out * ho * wo
 
+    @staticmethod
+    def subpixel_ok(weight, stride, pad, h, w) -> bool:
+        """Whether a conv fed by a 2x bilinear upsample can run in sub-pixel form."""
+        c_out, _, kh, kw = (int(v) for v in weight.shape)
+        return (kh == kw == 3 and stride == 1 and pad == 1 and c_out % 16 == 0 and h % 2 == 0 and w % 2 == 0
+                and c_out <= SUBPIXEL_MAX_COUT and CONV_KERNEL == "tc"
+                and os.environ.get("EVC_SUBPIXEL", "0") == "1")
+
+    def _init_subpixel(self, weight, h, w, th, tw, S, max_splits):
+        """Sub-pixel plan (csrc/subpixel.cu): the conv of the 2x bilinear upsample of a (C, h/2, w/2)
+        input as ONE 3x3 conv of that low-res input with 4 x C_out composed channels (compose_subpixel),
+        reading a low-res hi/lo shadow with a replicated edge ring (evc_subpixel_prep) plus a
+        border-line correction (evc_subpixel_border).  self.table / flags / meter stay the real
+        (high-res) conv's; self.g / cfg / wpack / rstate describe the composed launch."""
+        lib = _lib.lib()
+        c_out, c_in = int(weight.shape[0]), int(weight.shape[1])
+        self.subpixel = True
+        self.c_out, self.c_in, self.kh, self.kw, self.S = c_out, c_in, 3, 3, S
+        self.weight = weight.contiguous()
+        self.g_hi = self.g
+        ho, wo = int(self.g.Ho), int(self.g.Wo)
+        self.T = -(-ho // th) * -(-wo // tw)
+        hl, wl = h // 2, w // 2
+        self.g, _ = conv_geometry(c_in, 4 * c_out, 3, 3, 1, 1, hl, wl, th, tw)
+        self.path = "fused"
+        self.fed_by_sparsify = False
+        self.gi = (-(-h // th), -(-w // tw))  # the real conv's input tile grid (fany of the sparsify)
+        self.cfg = _lib.EvcConvCfg()
+        _lib.check(lib.evc_conv_fused_config(self.g, S, int(max_splits), self.cfg), "conv_fused_config")
+        self.cp = int(lib.evc_hwc_channels(c_in))
+        self.cpa, self.px = self.cp, 2 * self.cp
+        self.pitch = wl + 2
+        self.hwc = torch.zeros((S, hl + 2, self.pitch, self.px), dtype=torch.float32, device=weight.device)
+        self.hwc_interior = self.hwc.data_ptr() + 4 * (self.pitch + 1) * self.px
+        host = np.ascontiguousarray(compose_subpixel(weight.detach().cpu().numpy()), dtype=np.float32)
+        out = np.zeros(int(lib.evc_conv_fused_pack_len(self.g, self.cfg)), dtype=np.float32)
+        _lib.check(lib.evc_conv_fused_pack(host.ctypes.data, self.g, self.cfg, out.ctypes.data), "pack")
+        self.wpack = torch.from_numpy(out).to(weight.device)
+        self.rstate = torch.zeros(int(lib.evc_conv_fused_state_len(self.g, self.cfg, S)), dtype=torch.uint8,
+                                  device=weight.device)
+        self.splits = int(self.cfg.splits)
+        self.ws_floats = 0
+        self.ctas = int(lib.evc_conv_fused_ctas(self.g, self.cfg))
+        self.gl = (-(-hl // th), -(-wl // tw))  # low-res tile grid: its any-map (per-step zeroed) is
+        self.fany_lo_ptr = None                  # placed by the owner (Graph: the step's scratch arena)
+        self.wborder = self.weight.permute(1, 2, 3, 0).contiguous()  # (C_in, 3, 3, C_out) for the border GEMM
+        self.border = torch.zeros((S, 2 * (ho + wo), c_out), dtype=torch.float32, device=weight.device)
+        self.dense_flops = 2 * 9 * c_in * c_out * ho * wo
+
+    def subpixel_launches(self, dlo):
+        """[(fn, args-without-stream, name)] writing the composed conv's inputs from the low-res
+        tensor dlo (the upsample's input): low-res shadow + tile map, border correction."""
+        L = _lib.lib()
+        return [(L.evc_subpixel_prep, (dlo, self.hwc_interior, self.cp, self.hwc[0].numel(), self.pitch,
+                                       self.fany_lo_ptr, self.S), "subpixel_prep"),
+                (L.evc_subpixel_border, (dlo, self.wborder.data_ptr(), self.c_out, self.border.data_ptr(), self.S),
+                 "subpixel_border")]
+
     def scatter_plan(self):
         """Packed weights + workspace of the input-stationary scatter path (evc_conv_scatter) for
         this layer, built on first use; None when the geometry is not supported."""
@@ -377,6 +444,15 @@ class ConvPlan:
         dout may then be None (conv values not materialised).  sp = EvcConvSparsify fuses
         the following t_p = 0 sparsify (the act desc may then carry no values)."""
         code, alpha, acc, accs, adesc = act if act is not None else (-1, 0.0, None, 0, None)
+        if self.subpixel:
+            sub = _lib.EvcConvSubpixel(self.c_out, int(self.g_hi.Ho), int(self.g_hi.Wo), 0, fany,
+                                       self.border.data_ptr())
+            self._sub_keep = getattr(self, "_sub_keep", []) + [sub]  # alive as long as the program
+            return _lib.lib().evc_conv_fused_subpixel, (self.g, self.cfg, self.hwc.data_ptr(), self.cpa,
+                                                        self.hwc[0].numel(), self.wpack.data_ptr(), bias_ptr, din,
+                                                        self.fany_lo_ptr, self.table.data_ptr(),
+                                                        self.rstate.data_ptr(), mpart, dout, code, alpha, acc, accs,
+                                                        adesc, sp, sub, 1 if dense else 0, self.S)
         return _lib.lib().evc_conv_fused, (self.g, self.cfg, self.hwc.data_ptr(), self.cpa, self.hwc[0].numel(),
                                            self.wpack.data_ptr(), bias_ptr, din, fany, self.table.data_ptr(),
                                            self.rstate.data_ptr(), mpart, dout, code, alpha, acc, accs,
@@ -391,6 +467,31 @@ class ConvPlan:
         tl, tc = work if work is not None else (None, None)
         return lib.evc_conv_gemm, (self.g, din, self.weight.data_ptr(), _lib.ptr(self.wpack), bias_ptr, dout,
                                    self.table.data_ptr(), tl, tc, self.S, self.splits, ws_ptr)
+
+
+# half-pixel 2x bilinear taps per output phase: _SUBPIX_TAPS[a][d + 1][k] = weight of low-res offset
+# d in the upsampled value that kernel tap k of a 3x3 conv reads for output phase a (tensors.py:259-266)
+_SUBPIX_TAPS = np.zeros((2, 3, 3))
+_SUBPIX_TAPS[0, 0, 0], _SUBPIX_TAPS[0, 1, 0] = 0.75, 0.25
+_SUBPIX_TAPS[0, 0, 1], _SUBPIX_TAPS[0, 1, 1] = 0.25, 0.75
+_SUBPIX_TAPS[0, 1, 2], _SUBPIX_TAPS[0, 2, 2] = 0.75, 0.25
+_SUBPIX_TAPS[1, 0, 0], _SUBPIX_TAPS[1, 1, 0] = 0.25, 0.75
+_SUBPIX_TAPS[1, 1, 1], _SUBPIX_TAPS[1, 2, 1] = 0.75, 0.25
+_SUBPIX_TAPS[1, 1, 2], _SUBPIX_TAPS[1, 2, 2] = 0.25, 0.75
+
+
+def compose_subpixel(weight) -> np.ndarray:
+    """(4 C_out, C_in, 3, 3) weights of the sub-pixel conv: composed channel (2a + b) * C_out + o is
+    output channel o at phase (a, b) (site (2i + a, 2j + b)) of conv3x3(upsample2x_bilinear(x)),
+    evaluated on x itself (edge-replicated).  Composed in float64, rounded once."""
+    w = np.asarray(weight, dtype=np.float64)
+    co = w.shape[0]
+    out = np.zeros((4 * co, *w.shape[1:]))
+    for a in range(2):
+        for b in range(2):
+            out[(2 * a + b) * co:(2 * a + b + 1) * co] = np.einsum("yk,xl,oikl->oiyx", _SUBPIX_TAPS[a],
+                                                                   _SUBPIX_TAPS[b], w)
+    return out.astype(np.float32)
 
 
 def choose_splits(max_sites: int, c_out: int, k: int, target_ctas: int = 2 * 148, kernel: str | None = None) -> int:

@@ -39,6 +39,8 @@ def main():
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--sessions", type=int, default=1)
     ap.add_argument("--cin", type=int, default=0)
+    ap.add_argument("--subpixel", action="store_true",
+                    help="what-if: decoder convs on the low-res input with 4x output channels")
     args = ap.parse_args()
     want = set(args.layers.split(",")) if args.layers else None
     lib = _lib.lib()
@@ -52,6 +54,8 @@ def main():
             c = args.cin
         k = int(at["kernel"][0])
         st, pad, co = int(at.get("stride", 1)), int(at.get("padding", 0)), int(at["out_channels"])
+        if args.subpixel and nid.startswith("dec"):
+            h, w, co = h // 2, w // 2, 4 * co
         wt = torch.randn(co, c, k, k, device=dev) * (2.0 / (c * k * k)) ** 0.5
         S = args.sessions
         plan = ConvPlan(wt, st, pad, h, w, 6, 6, S, max_splits=args.splits)

@@ -192,12 +192,6 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
   return kind == EVC_ACT_RELU ? fmaxf(x, 0.0f) : act_other(x, kind, alpha);
 }
 
-// Final values of N channels (n0, n0 + step, ...) of output site m (region row-major):
-// every global load is issued before any store so the latencies overlap.
-// Final values of N channels (n0, n0 + step, ...) of output site m (region row-major).
-// Every global load is issued before any store so the latencies overlap.  Called by
-// every lane of a warp with warp-uniform (n0, step, cnt): the fused sparsify uses
-// warp ballots.  Returns the site's sum of squared sparsify outputs (0 if unfused).
 // Sub-pixel mode: composed channel n of low-res site (u, x) -> output channel and high-res site.
 // (Channel groups never straddle a phase: oc % 16 == 0 and groups start at multiples of their size.)
 __device__ __forceinline__ void sub_site(const Args& a, int& u, int& x, int& n) {
@@ -253,6 +247,9 @@ __device__ __forceinline__ int sub_live_of(const Args& a, int s, int u, int x) {
   return sub_tile_live(a, s, 2 * u, 2 * x) ? 1 : 0;
 }
 
+// Final values of N channels (n0, n0 + step, ...) of output site (u, x) (region row-major).
+// Every global load is issued before any store so the latencies overlap.  Returns the
+// site's sum of squared sparsify outputs (0 if unfused).
 template <int N>
 __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n0, int step, int cnt,
                                        const float* vals, int sub_live = -1) {
@@ -304,12 +301,10 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   }
   if (!a.sp_hwc) return 0.0;
   // fused sparsify_step at t_p = 0 (sparsify.py:63-71): out = 0 + y, residual stays 0; the mask is
-  // recomputed from the values (sparsify.py:77-78) -- one flag store per (tile, channel) per warp
+  // recomputed from the values (sparsify.py:77-78): every site with a nonzero value stores 1 into its
+  // (tile, channel) flag (benign: only ever set; the lanes of one tile merge into one store)
   float ss = 0.0f;  // <= 16 squares per call in fp32, widened once per site
-  const int lane = threadIdx.x & 31;
-  const int tile = valid ? (u / a.th) * a.sp_GW + x / a.tw : -1;
-  const unsigned grp = __match_any_sync(0xffffffffu, tile);
-  const bool leader = valid && (__ffs(grp) - 1) == lane;
+  const int tile = valid ? (u / a.th) * a.sp_GW + x / a.tw : 0;
   float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)u * a.sp_pitch + x) * hwc_px(a.sp_cp);
   const int64_t To = (int64_t)a.sp_GH * a.sp_GW;
   uint8_t* fl = a.sp_flags + (int64_t)s * a.sp_fs + tile;
@@ -342,13 +337,12 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   for (int j = 0; j < N; ++j) {
     const bool in = valid && j < cnt;
     if (in) ss = __fmaf_rn(o[j], o[j], ss);
-    const unsigned nz = __ballot_sync(0xffffffffu, in && o[j] != 0.0f);
-    if (leader && (nz & grp)) {
+    if (in && o[j] != 0.0f) {
       fl[(int64_t)(n0 + j * step) * To] = 1;
       any = true;
     }
   }
-  if (any) a.sp_fany[(int64_t)s * To + tile] = 1;  // benign race: only ever set
+  if (any) a.sp_fany[(int64_t)s * To + tile] = 1;
   return (double)ss;
 }
 
@@ -960,13 +954,24 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 // prologue is paid once per CTA.  Every role evaluates the region test itself (same inputs,
 // same answer), so no per-item hand-off is needed besides the TMEM full / empty barriers.
 // ---------------------------------------------------------------------------------------------
+// (Divisions through fp32 reciprocals, fdiv: exact for these small operands, and no state held
+// across the callers' item loops.)
 __device__ __forceinline__ bool region_live_warp(const Args& a, int s, int rr) {
   if (a.dense) return true;
+  struct {
+    FDiv P, th, tw;
+    int GWi, GHi;
+  } d;
+  d.P = fdiv_of(max(1, a.P));
+  d.th = fdiv_of(a.th);
+  d.tw = fdiv_of(a.tw);
+  d.GWi = fdiv(a.W + a.tw - 1, d.tw);
+  d.GHi = fdiv(a.H + a.th - 1, d.th);
   int ulo, uhi, xlo, xhi;
   if (a.row) {
     const int i0 = rr * a.VM;
-    ulo = i0 / a.P;
-    uhi = min(a.Ho - 1, (i0 + a.VM - 1) / a.P);
+    ulo = fdiv(i0, d.P);
+    uhi = min(a.Ho - 1, fdiv(i0 + a.VM - 1, d.P));
     if (ulo == uhi) {
       xlo = i0 - ulo * a.P;
       xhi = min(a.Wo - 1, i0 + a.VM - 1 - ulo * a.P);
@@ -985,10 +990,20 @@ __device__ __forceinline__ bool region_live_warp(const Args& a, int s, int rr) {
     const int y_lo = max(0, ulo * a.stride - a.pad), y_hi = min(a.H - 1, uhi * a.stride - a.pad + a.kh - 1);
     const int x_lo = max(0, xlo * a.stride - a.pad), x_hi = min(a.W - 1, xhi * a.stride - a.pad + a.kw - 1);
     if (y_lo <= y_hi && x_lo <= x_hi) {
-      const int GWi = (a.W + a.tw - 1) / a.tw, GHi = (a.H + a.th - 1) / a.th;
-      const int ra = y_lo / a.th, nr = y_hi / a.th - ra + 1, ca = x_lo / a.tw, nc = x_hi / a.tw - ca + 1;
-      const uint8_t* fa = a.fany + (int64_t)s * GHi * GWi;
-      for (int e = (int)(threadIdx.x & 31); e < nr * nc; e += 32) live |= fa[(ra + e / nc) * GWi + ca + e % nc];
+      const int ra = fdiv(y_lo, d.th), nr = fdiv(y_hi, d.th) - ra + 1;
+      const int ca = fdiv(x_lo, d.tw), nc = fdiv(x_hi, d.tw) - ca + 1;
+      const uint8_t* fa = a.fany + (int64_t)s * d.GHi * d.GWi + ra * d.GWi + ca;
+      if (nr * nc <= 32) {
+        const FDiv dn = fdiv_of(nc);
+        const int e = (int)(threadIdx.x & 31);
+        if (e < nr * nc) {
+          const int r = fdiv(e, dn);
+          live = fa[r * d.GWi + e - r * nc];
+        }
+      } else {
+        for (int r = 0; r < nr; ++r)
+          for (int c = (int)(threadIdx.x & 31); c < nc; c += 32) live |= fa[r * d.GWi + c];
+      }
     }
   }
   return __any_sync(0xffffffffu, live) != 0;

@@ -10,13 +10,14 @@
 // last step, or when its residual is nonzero -- exactly the tiles the unfused
 // pair could change.  Norm partials are folded by the last CTA (fixed order).
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
 
 namespace evc {
 
-constexpr int US_C = 32, US_THREADS = 256, US_MAXJ = 32, US_MAXR = 16;
+constexpr int US_C = 32, US_THREADS = 256, US_MAXJ = 32, US_MAXR = 32;
 
 struct USArgs {
   TView x;         // upsample input (masked)
@@ -410,8 +411,19 @@ int evc_upsample_sparsify(const evc_tensor* x, int32_t factor, int32_t mode, flo
   a.mode = mode;
   us_grid(a.y, a.CW, a.nCG, a.nJC);
   a.fast = (delta_zero && tp == 0.0 && !write_chw) ? 1 : 0;
-  // two tile rows per CTA on the fast path when their tiles fit the per-CTA flag tables
-  a.RT = (a.fast && 2 * (a.CW / a.y.tw) <= US_MAXJ && 2 * a.y.th <= US_MAXR) ? 2 : 1;
+  // tile rows per CTA on the fast path (EVC_UP_RT, default 2, when the per-CTA flag tables and 96 KB
+  // of staging hold them): measured on C1 at 32 streams, 4 rows (fewer, larger CTAs) cost 25 % more
+  // than 2 -- half the CTAs per SM fit -- and 1 row 5 % more (scripts/gpu_iter3.sh)
+  a.RT = 1;
+  if (a.fast) {
+    const char* ev = std::getenv("EVC_UP_RT");
+    const int want = ev ? std::max(1, std::atoi(ev)) : 2;
+    for (int rt = want; rt > 1 && a.RT == 1; --rt) {
+      const size_t xr = rt * y->th / factor + 3, xc = a.CW / factor + 3;
+      const size_t bytes = sizeof(float) * US_C * (((rt * y->th * xc) | 1) + ((xr * xc) | 1));
+      if (rt * (a.CW / a.y.tw) <= US_MAXJ && rt * a.y.th <= US_MAXR && bytes <= 96 * 1024) a.RT = rt;
+    }
+  }
   a.pstride = a.y.GH * a.nCG * a.nJC;
   dim3 grid((unsigned)(((a.y.GH + a.RT - 1) / a.RT) * a.nCG * a.nJC), (unsigned)S);
   a.XR = a.RT * y->th / factor + 3;

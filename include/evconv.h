@@ -267,15 +267,16 @@ int evc_conv_fused(const evc_conv_geom* g, const evc_conv_cfg* cfg, const float*
                    int32_t dense, int32_t S, void* stream);
 /* Sub-pixel form of "2x bilinear upsample -> sparsify(t_p = 0) -> 3x3 stride-1 pad-1 conv"
  * (increment_ops.py:271-285 -> sparsify.py:54-78 -> increment_ops.py:126-194): the conv runs on
- * the LOW-RES input x with composed weights (4 x c_out channels, phase p -> output site
- * (2i + p / 2, 2j + p % 2)), reading the low-res shadow evc_subpixel_prep writes (edges
- * replicated into the ring) instead of the upsampled one.  g / cfg: the composed low-res conv
- * (c_out = 4 x sub->c_out); fany: the low-res tile map of evc_subpixel_prep; table: the
- * evc_conv_table_fill output of the REAL (high-res) conv; in: the sparsify output (high-res
- * flags, from evc_upsample_sparsify with hwc = NULL); out / act_out / sp: high-res tensors as in
- * evc_conv_fused.  Flags and meter are the real conv's; values within fp32 rounding of it. */
+ * the LOW-RES input x with composed weights (4 x c_out channels, phase-minor: composed channel
+ * 4 c + 2 a + b -> channel c at output site (2i + a, 2j + b)), reading the low-res shadow that
+ * evc_subpixel_input writes (edges replicated into the ring) instead of the upsampled one.
+ * g / cfg: the composed low-res conv (c_out = 4 x sub->c_out; channel block >= 64, not packed);
+ * fany: the low-res tile map of evc_subpixel_input; table: the evc_conv_table_fill output of the
+ * REAL (high-res) conv; in: the sparsify output (high-res flags, from evc_subpixel_input);
+ * out / act_out / sp: high-res tensors as in evc_conv_fused.  Flags and meter are the real
+ * conv's; values within fp32 rounding of it. */
 typedef struct evc_conv_subpixel {
-  int32_t c_out;          /* output channels of the real conv (multiple of 16) */
+  int32_t c_out;          /* output channels of the real conv (multiple of 4); tiles th, tw even */
   int32_t Ho, Wo;         /* its output size = 2 x the composed conv's */
   int32_t reserved;
   const uint8_t* fany_in; /* any-channel tile map of the high-res conv input (incremental mode) */
@@ -287,11 +288,18 @@ int evc_conv_fused_subpixel(const evc_conv_geom* g, const evc_conv_cfg* cfg, con
                             const evc_tensor* out, int32_t act, float alpha, float* acc, int64_t acc_stride,
                             const evc_tensor* act_out, const evc_conv_sparsify* sp, const evc_conv_subpixel* sub,
                             int32_t dense, int32_t S, void* stream);
-/* Low-res shadow of x for evc_conv_fused_subpixel (hwc = interior origin, pitch >= W + 2, cp a
- * multiple of 32 >= C; the one-pixel ring holds the replicated edge) and fany[s][tile] |= any
- * channel of x nonzero in the tile (zero fany first; only ever set to 1). */
-int evc_subpixel_prep(const evc_tensor* x, float* hwc, int32_t cp, int64_t hwc_stride, int32_t pitch,
-                      uint8_t* fany, int32_t S, void* stream);
+/* The sub-pixel conv's input pass in one launch over x (replaces evc_upsample_sparsify at
+ * t_p = 0 for that conv): the low-res shadow (interior origin hwc, pitch >= W + 2, cp a multiple
+ * of 32 >= C, the one-pixel ring = the replicated edge), fany_lo[s][tile] |= any channel flag of
+ * x, and for the 2x bilinear upsample U(x) -- never stored -- the sparsify output y's flags (every
+ * tile written: U != 0 anywhere in it, sparsify.py:77-78, evaluated where x's flags mark the
+ * support), fany_hi[s][tile] |= any channel, and one sum of U^2 per CTA at
+ * partials[s * evc_subpixel_input_partials(x, cp) + cta] (norm fold: evc_meter_step).  Tiles of x
+ * and y equal and even. */
+int64_t evc_subpixel_input_partials(const evc_tensor* x, int32_t cp);
+int evc_subpixel_input(const evc_tensor* x, const evc_tensor* y, double* partials, float* hwc, int32_t cp,
+                       int64_t hwc_stride, int32_t pitch, uint8_t* fany_lo, uint8_t* fany_hi, int32_t S,
+                       void* stream);
 /* Border correction of evc_conv_fused_subpixel: out[s][line][c] for the high-res lines row 0
  * (index X), row Ho - 1, column 0 (index Y), column Wo - 1, = - sum over the taps leaving the
  * image of w . U(clamped site); w = the real conv's weights transposed to (C, 3, 3, c_out)

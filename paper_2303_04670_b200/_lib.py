@@ -109,7 +109,8 @@ _PROTOS = {
                               _SP, _I32, _I32, _P]),
     "evc_conv_fused_subpixel": (_I32, [_G, _CF, _P, _I32, _I64, _P, _P, _T, _P, _P, _P, _P, _T, _I32, _F, _P, _I64,
                                        _T, _SP, _SUB, _I32, _I32, _P]),
-    "evc_subpixel_prep": (_I32, [_T, _P, _I32, _I64, _I32, _P, _I32, _P]),
+    "evc_subpixel_input_partials": (_I64, [_T, _I32]),
+    "evc_subpixel_input": (_I32, [_T, _T, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _P]),
     "evc_subpixel_border": (_I32, [_T, _P, _I32, _P, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
     "evc_conv_trace": (_I32, [_P]),

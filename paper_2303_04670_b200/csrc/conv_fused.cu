@@ -193,11 +193,12 @@ __device__ __forceinline__ float act_f(float x, int kind, float alpha) {
 }
 
 // Sub-pixel mode: composed channel n of low-res site (u, x) -> output channel and high-res site.
-// (Channel groups never straddle a phase: oc % 16 == 0 and groups start at multiples of their size.)
+// Composed channels are phase-minor: n = 4 c + 2 a + b (tensors.compose_subpixel), so an aligned
+// group of 4k composed channels holds k real channels at all four phase sites of (u, x).
 __device__ __forceinline__ void sub_site(const Args& a, int& u, int& x, int& n) {
   if (!a.sub) return;
-  const int ph = n / a.oc;
-  n -= ph * a.oc;
+  const int ph = n & 3;
+  n >>= 2;
   if (u < a.Ho && x < a.Wo) {
     u = 2 * u + (ph >> 1);
     x = 2 * x + (ph & 1);
@@ -222,24 +223,6 @@ __device__ __forceinline__ bool sub_tile_live(const Args& a, int s, int u, int x
   return nf != 0;
 }
 
-// Sub-pixel extras of a valid high-res site, out of line (keeps the common emit's registers):
-// the border-line correction pointer and the output-tile mask.
-struct SubSite {
-  const float* bc;
-  int masked;
-};
-// sub_live: the caller's sub_tile_live of this site (all four phases of a low-res site share one
-// output tile: th, tw even), or -1 to evaluate it here.
-__device__ __forceinline__ SubSite sub_extras(const Args& a, int s, int u, int x, int n0, int sub_live) {
-  SubSite r = {nullptr, 0};
-  if (u == 0 || x == 0 || u == a.eHo - 1 || x == a.eWo - 1) {
-    const int li = u == 0 ? x : (u == a.eHo - 1 ? a.eWo + x : (x == 0 ? 2 * a.eWo + u : 2 * a.eWo + a.eHo + u));
-    r.bc = a.border + ((int64_t)s * 2 * (a.eHo + a.eWo) + li) * a.oc + n0;
-  }
-  r.masked = !a.dense && !(sub_live >= 0 ? sub_live != 0 : sub_tile_live(a, s, u, x));
-  return r;
-}
-
 // Sub-pixel, incremental: the output-tile liveness shared by the four phase sites of low-res site
 // (u, x) (-1 when not applicable), evaluated once per work item.
 __device__ __forceinline__ int sub_live_of(const Args& a, int s, int u, int x) {
@@ -251,23 +234,25 @@ __device__ __forceinline__ int sub_live_of(const Args& a, int s, int u, int x) {
 // Every global load is issued before any store so the latencies overlap.  Returns the
 // site's sum of squared sparsify outputs (0 if unfused).
 template <int N>
+__device__ __forceinline__ double emit_sub(const Args& a, int s, int u, int x, int n0, int cnt, const float* vals,
+                                           int sub_live);
+
+// SUBOK: the instantiation can run in sub-pixel mode (BN >= 64, not packed -- the host enforces it),
+// so kernels that never do carry no sub-pixel code (registers, instruction cache).
+template <int N, bool SUBOK = false>
 __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n0, int step, int cnt,
                                        const float* vals, int sub_live = -1) {
-  sub_site(a, u, x, n0);
+  if constexpr (SUBOK && N % 4 == 0) {
+    if (a.sub) return emit_sub<N>(a, s, u, x, n0, cnt, vals, sub_live);
+  }
   const bool valid = u < a.eHo && x < a.eWo;
   const int64_t plane = (int64_t)a.eHo * a.eWo;
   const int64_t base = (int64_t)n0 * plane + (int64_t)u * a.eWo + x;
   const int64_t dn = (int64_t)step * plane;
   float v[N], y[N];
-  SubSite ss0 = {nullptr, 0};
-  if (a.sub && valid) ss0 = sub_extras(a, s, u, x, n0, sub_live);
-  const float* bc = ss0.bc;
-  const bool masked = ss0.masked != 0;
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     v[j] = vals[j];
-    if (bc && j < cnt) v[j] = __fadd_rn(v[j], bc[j * step]);
-    if (masked) v[j] = 0.0f;
     if (valid && j < cnt && a.dense && a.bias) v[j] = __fadd_rn(v[j], __ldg(a.bias + n0 + j * step));
     y[j] = v[j];
   }
@@ -346,6 +331,134 @@ __device__ __forceinline__ double emit(const Args& a, int s, int u, int x, int n
   return (double)ss;
 }
 
+
+// Sub-pixel emit: composed channels n0 .. n0 + N - 1 (n0 % 4 == 0) of low-res site (u, x) = NC = N / 4
+// real channels c0 + k at the four high-res sites (2u + a, 2x + b).  Each (channel, row a) pair of
+// sites is adjacent in x: every value, accumulator and activation access is a float2 (a warp covers
+// 256 contiguous bytes of a row).  Adds the border-line correction, zeroes sites of dead output
+// tiles (incremental; the four sites share one tile, th and tw even), then the activation and the
+// fused t_p = 0 sparsify as in emit.
+template <int N>
+__device__ __forceinline__ double emit_sub(const Args& a, int s, int u, int x, int n0, int cnt, const float* vals,
+                                           int sub_live) {
+  constexpr int NC = N / 4;
+  const int c0 = n0 >> 2, nc = cnt >> 2;
+  const bool valid = u < a.Ho && x < a.Wo;
+  const int U0 = 2 * u, X0 = 2 * x;
+  const int64_t plane = (int64_t)a.eHo * a.eWo;
+  float v[NC][2][2];
+  const bool masked = valid && !a.dense && !(sub_live >= 0 ? sub_live != 0 : sub_tile_live(a, s, U0, X0));
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        float t = masked ? 0.0f : vals[4 * k + 2 * r + b];
+        if (valid && k < nc && a.dense && a.bias) t = __fadd_rn(t, __ldg(a.bias + c0 + k));
+        v[k][r][b] = t;
+      }
+  if (valid && !masked && (U0 == 0 || X0 == 0 || U0 + 1 == a.eHo - 1 || X0 + 1 == a.eWo - 1)) {
+    const int64_t lines = (int64_t)s * 2 * (a.eHo + a.eWo);
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int uu = U0 + r, xx = X0 + b;
+        if (uu != 0 && xx != 0 && uu != a.eHo - 1 && xx != a.eWo - 1) continue;
+        const int li = uu == 0 ? xx : (uu == a.eHo - 1 ? a.eWo + xx : (xx == 0 ? 2 * a.eWo + uu : 2 * a.eWo + a.eHo + uu));
+        const float* bc = a.border + (lines + li) * a.oc + c0;
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+          if (k < nc) v[k][r][b] = __fadd_rn(v[k][r][b], bc[k]);
+      }
+  }
+  float y[NC][2][2];
+#pragma unroll
+  for (int k = 0; k < NC; ++k)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) y[k][r][0] = v[k][r][0], y[k][r][1] = v[k][r][1];
+  const int64_t base = (int64_t)c0 * plane + (int64_t)U0 * a.eWo + X0;  // float2-aligned: X0, eWo even
+  if (valid && a.out) {
+    float* o = a.out + (int64_t)s * a.ovs + base;
+#pragma unroll
+    for (int k = 0; k < NC; ++k)
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+        if (k < nc) *reinterpret_cast<float2*>(o + k * plane + r * a.eWo) = make_float2(v[k][r][0], v[k][r][1]);
+  }
+  if (valid && a.act >= 0) {
+    float* ap = a.acc ? a.acc + (int64_t)s * a.accs + base : nullptr;
+    float* yp = a.yact ? a.yact + (int64_t)s * a.yvs + base : nullptr;
+    float2 acc0[NC][2];
+    if (!a.dense) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+          acc0[k][r] = k < nc ? *reinterpret_cast<const float2*>(ap + k * plane + r * a.eWo) : make_float2(0.0f, 0.0f);
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      if (k >= nc) continue;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        float2 a1;
+        if (a.dense) {
+          y[k][r][0] = act_f(v[k][r][0], a.act, a.alpha);
+          y[k][r][1] = act_f(v[k][r][1], a.act, a.alpha);
+          a1 = make_float2(v[k][r][0], v[k][r][1]);
+        } else {
+          a1 = make_float2(__fadd_rn(acc0[k][r].x, v[k][r][0]), __fadd_rn(acc0[k][r].y, v[k][r][1]));
+          y[k][r][0] = __fsub_rn(act_f(a1.x, a.act, a.alpha), act_f(acc0[k][r].x, a.act, a.alpha));
+          y[k][r][1] = __fsub_rn(act_f(a1.y, a.act, a.alpha), act_f(acc0[k][r].y, a.act, a.alpha));
+        }
+        if (ap) *reinterpret_cast<float2*>(ap + k * plane + r * a.eWo) = a1;
+        if (yp) *reinterpret_cast<float2*>(yp + k * plane + r * a.eWo) = make_float2(y[k][r][0], y[k][r][1]);
+      }
+    }
+  }
+  if (!a.sp_hwc) return 0.0;
+  // fused sparsify_step at t_p = 0 of the four sites (see emit)
+  float ss = 0.0f;
+  const int tile = valid ? (U0 / a.th) * a.sp_GW + X0 / a.tw : 0;
+  const int64_t To = (int64_t)a.sp_GH * a.sp_GW;
+  uint8_t* fl = a.sp_flags + (int64_t)s * a.sp_fs + tile;
+  bool any = false;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (!valid) continue;
+      float* sh = a.sp_hwc + (int64_t)s * a.sp_hs + ((int64_t)(U0 + r) * a.sp_pitch + X0 + b) * hwc_px(a.sp_cp);
+      float o[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) o[k] = __fadd_rn(0.0f, y[k][r][b]);
+      if (NC % 4 == 0 && nc == NC && (c0 & 3) == 0 && a.sp_cp < 0) {
+#pragma unroll
+        for (int k = 0; k < NC; k += 4) *reinterpret_cast<float4*>(sh + c0 + k) = make_float4(o[k], o[k + 1], o[k + 2], o[k + 3]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NC; ++k)
+          if (k < nc) hwc_store(sh, a.sp_cp, c0 + k, o[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < NC; ++k)
+        if (k < nc) ss = __fmaf_rn(o[k], o[k], ss);
+    }
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    const bool nz = valid && k < nc &&
+                    (__fadd_rn(0.0f, y[k][0][0]) != 0.0f || __fadd_rn(0.0f, y[k][0][1]) != 0.0f ||
+                     __fadd_rn(0.0f, y[k][1][0]) != 0.0f || __fadd_rn(0.0f, y[k][1][1]) != 0.0f);
+    if (nz) {
+      fl[(int64_t)(c0 + k) * To] = 1;
+      any = true;
+    }
+  }
+  if (any) a.sp_fany[(int64_t)s * To + tile] = 1;
+  return (double)ss;
+}
 
 // Restore exact zeros of channel n at site (u, x) of a region computed last step and dead now.
 __device__ __forceinline__ void zero_site(const Args& a, int s, int u, int x, int n) {
@@ -597,7 +710,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
         }
         if (a.splits == 1) {
           const int n0 = nblk * BN + c0;
-          ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals, sl);
+          ssq += emit<16, (BN >= 64)>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals, sl);
         } else {
   #pragma unroll
           for (int j = 0; j < 16; ++j) P[(c0 + j) * BM + m] = vals[j];
@@ -888,7 +1001,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 #pragma unroll
         for (int e = 0; e < 16; ++e) vals[e] = X[(c0 + e) * BM + m];
         const int n0 = nblk * BN + c0;
-        if (n0 < a.c_out) ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals, sl);
+        if (n0 < a.c_out) ssq += emit<16, (BN >= 64)>(a, s, u, x, n0, 1, min(16, a.c_out - n0), vals, sl);
       }
     }
   }
@@ -929,7 +1042,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
           if (zz < nsp) sum[j] = __fadd_rn(sum[j], t[zz][j]);
       }
       const int n0 = nblk * BN + nl0;
-      ssq += emit<NB>(a, s, u, x, n0, 1, min(cnt, a.c_out - n0), sum, sl);
+      ssq += emit<NB, (BN >= 64)>(a, s, u, x, n0, 1, min(cnt, a.c_out - n0), sum, sl);
     }
     cluster_sync();
   }
@@ -1313,7 +1426,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 #pragma unroll
           for (int cc = 0; cc < CB; cc += 16) {
             const int n0 = nblk * BN + half * CB + cc;
-            ssq += emit<16>(a, s, u, x, n0, 1, min(16, a.c_out - n0), acc + cc, sl);
+            ssq += emit<16, (BN >= 64 && !PK)>(a, s, u, x, n0, 1, min(16, a.c_out - n0), acc + cc, sl);
           }
         }
       }
@@ -1867,11 +1980,14 @@ static int conv_fused_impl(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, c
                 "conv_fused: shadow layout (cp % 32, thin path +-cp % 4; (H + 2 pad) x (W + 2 pad) pixels per session)");
   EVC_CHECK_ARG(act < 0 || (act <= 3 && act_out && (act_out->vals || sp) && (acc || dense)), "conv_fused: activation");
   EVC_CHECK_ARG(out || (act >= 0 && act_out->vals) || sp, "conv_fused: no output");
-  EVC_CHECK_ARG(!sub || (sub->c_out > 0 && sub->c_out % 16 == 0 && g->c_out == 4 * sub->c_out && g->kh == 3 &&
+  EVC_CHECK_ARG(!sub || (sub->c_out > 0 && sub->c_out % 4 == 0 && g->c_out == 4 * sub->c_out && g->th % 2 == 0 &&
+                         g->tw % 2 == 0 && g->kh == 3 &&
                          g->kw == 3 && g->stride == 1 && g->pad == 1 && sub->Ho == 2 * g->Ho && sub->Wo == 2 * g->Wo &&
                          !cfg->thin && sub->border && (dense || sub->fany_in)),
-                "conv_fused_subpixel: needs a 3x3 stride-1 pad-1 geometry with 4 x c_out (c_out % 16 == 0) "
+                "conv_fused_subpixel: needs a 3x3 stride-1 pad-1 geometry with 4 x c_out (c_out % 4 == 0), even tiles, "
                 "composed channels, the border correction and the high-res any-channel map");
+  EVC_CHECK_ARG(!sub || (cfg->bn >= 64 && cfg->row != 2),
+                "conv_fused_subpixel: needs a channel block of >= 64 composed channels, not packed");
   const int eHo = sub ? sub->Ho : g->Ho, eWo = sub ? sub->Wo : g->Wo, oc = sub ? sub->c_out : g->c_out;
   EVC_CHECK_ARG(!sp || (sp->hwc && sp->cp % 4 == 0 && std::abs(sp->cp) >= oc && sp->hwc_stride % 4 == 0 &&
                         sp->pitch >= eWo && sp->flags && sp->fany && sp->partials),

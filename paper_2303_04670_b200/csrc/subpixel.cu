@@ -12,8 +12,9 @@
 // difference for the four border lines and the conv epilogue adds it.  The conv then reads the
 // low-res input (4x fewer shadow bytes than the upsampled one) and never materialises U.
 //
-//  k_subpix_prep:   the low-res hi/lo shadow (interior + replicated ring) and the low-res any-channel
-//                   tile map (region liveness of the composed conv; OR-accumulated), one pass over x
+//  k_subpix_input:  one pass over x: the low-res hi/lo shadow (interior + replicated ring), the
+//                   low-res tile map (region liveness of the composed conv), and the sparsify's
+//                   high-res flags / any-map / norm partials from the (unstored) upsample
 //  k_subpix_border: border correction [S][2 (Ho + Wo)][C_out] = - sum over the off-image taps of
 //                   W . U(clamped site), U evaluated with dense_upsample's float32 op order
 
@@ -25,67 +26,177 @@ namespace evc {
 
 constexpr int SP_THREADS = 256, SP_MAXC = 32;
 
-// CTA = (session, low-res tile row, column block of CW = tw * floor(32 / tw) columns x one 32-channel
-// chunk).  Thread (channel, row) reads its row run of the channel-planar input (all loads in flight),
-// the CTA then writes 256-byte [32 heads | 32 tails] runs per pixel (lane = channel): both sides
-// coalesced.  fany (zeroed per step) is OR-accumulated per tile (benign race: every writer stores 1).
-__global__ void __launch_bounds__(SP_THREADS) k_subpix_prep(TView x, float* __restrict__ hwc, int64_t hs, int cp,
-                                                             int pitch, uint8_t* __restrict__ fany, int CW, int nJB) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ float t[SP_MAXC][8 * 33 + 1];  // [channel][row * 33 + col] (odd channel stride)
-  __shared__ int s_any[8];
-  const int s = blockIdx.z, ti = blockIdx.y, jb = blockIdx.x % nJB, k0 = (blockIdx.x / nJB) * 32;
-  const int r0 = ti * x.th, nrow = min(x.th, x.H - r0);
-  const int c0 = jb * CW, ncol = min(CW, x.W - c0);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int ntile = (ncol + x.tw - 1) / x.tw;
-  if (threadIdx.x < 8) s_any[threadIdx.x] = 0;
-  __syncthreads();
-  {  // thread (channel ch, row) loads columns 0..ncol-1 of its row: independent loads, one wait
-    const int ch = threadIdx.x >> 3, row = threadIdx.x & 7, c = k0 + ch;
-    const bool ok = row < nrow && c < x.C;
-    const float* src = ok ? x.plane(s, c) + (int64_t)(r0 + row) * x.W + c0 : nullptr;
-    float v[32];
-#pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = (ok && q < ncol) ? __ldg(src + q) : 0.0f;
-    if (row < 8) {
-      uint32_t nz = 0;
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        t[ch][row * 33 + q] = v[q];
-        nz |= __float_as_uint(v[q]) & 0x7fffffffu;
-      }
-      if (ok && nz) {  // per tile of the row
-        for (int tj = 0; tj < ntile; ++tj) {
-          uint32_t z = 0;
-          for (int q = tj * x.tw; q < min(ncol, (tj + 1) * x.tw); ++q) z |= __float_as_uint(t[ch][row * 33 + q]) & 0x7fffffffu;
-          if (z) s_any[tj] = 1;
-        }
-      }
-    }
+// Half-pixel 2x bilinear tap of output index o (tensors.py:259-266 for factor 2, the values
+// bilinear_tap computes, in closed form): o = 2i -> (i - 1, i) with (1/4, 3/4), o = 2i + 1 -> (i, i + 1)
+// with (3/4, 1/4), indices clamped to [0, n).
+__device__ __forceinline__ Tap tap2(int o, int n) {
+  Tap t;
+  const int i = o >> 1;
+  if (o & 1) {
+    t.i0 = min(i, n - 1);
+    t.i1 = min(i + 1, n - 1);
+    t.w0 = 0.75f;
+    t.w1 = 0.25f;
+  } else {
+    t.i0 = max(i - 1, 0);
+    t.i1 = min(i, n - 1);
+    t.w0 = 0.25f;
+    t.w1 = 0.75f;
   }
-  __syncthreads();
-  if (fany && threadIdx.x < ntile && s_any[threadIdx.x]) fany[((int64_t)s * x.GH + ti) * x.GW + c0 / x.tw + threadIdx.x] = 1;
-  // output pixel rows / columns incl. the replicated ring at the image edges
-  const int ra = r0 - (ti == 0 ? 1 : 0), rb = r0 + nrow + (r0 + nrow == x.H ? 1 : 0);
-  const int ca = c0 - (c0 == 0 ? 1 : 0), cb = c0 + ncol + (c0 + ncol == x.W ? 1 : 0);
-  const int nr = rb - ra, nc = cb - ca;
-  float* base = hwc + (int64_t)s * hs + 2 * k0 + lane;
-  for (int p = warp; p < nr * nc; p += SP_THREADS / 32) {  // warp per pixel, lane = channel
-    const int pr = ra + p / nc, pc = ca + p % nc;
-    const int sr = min(max(pr, 0), x.H - 1) - r0, sc = min(max(pc, 0), x.W - 1) - c0;
-    const float v = t[lane][sr * 33 + sc];
-    const float h = tf32_head(v);
-    float* d = base + ((int64_t)pr * pitch + pc) * (2 * cp);
-    d[0] = h;
-    d[32] = __fsub_rn(v, h);
-  }
+  return t;
 }
 
 // U(y, x) of the 2x bilinear upsample of plane xv (H x W low-res), dense_upsample's op order.
 __device__ __forceinline__ float up2(const float* xv, int H, int W, int y, int x) {
-  return upsample_at(xv, H, W, y, x, 2, 1);
+  const Tap tr = tap2(y, H), tc = tap2(x, W);
+  const float* x0 = xv + (int64_t)tr.i0 * W;
+  const float* x1 = xv + (int64_t)tr.i1 * W;
+  const float ra = __fadd_rn(__fmul_rn(x0[tc.i0], tr.w0), __fmul_rn(x1[tc.i0], tr.w1));
+  const float rb = __fadd_rn(__fmul_rn(x0[tc.i1], tr.w0), __fmul_rn(x1[tc.i1], tr.w1));
+  return __fadd_rn(__fmul_rn(ra, tc.w0), __fmul_rn(rb, tc.w1));
+}
+
+// The sub-pixel conv's input pass (replaces upsample_sparsify's t_p = 0 fast path for that conv plus
+// a low-res shadow copy): per CTA = (session, low-res tile row, CW low-res columns, 32 channels) --
+// i.e. the high-res tiles 2 ti, 2 ti + 1 x (2 CW / tw) tile columns it owns (th, tw even):
+//  * the low-res hi/lo shadow of its pixels (+ the replicated ring at the image edges),
+//  * the low-res tile map (any channel flag; OR, zeroed per step) for the composed conv's regions,
+//  * the sparsify output's flags of every owned high-res (channel, tile), recomputed from the values
+//    of the upsample (sparsify.py:77-78), the high-res any-channel map (OR) and the sum of squares of
+//    the owned values (norm partial, one per CTA, folded later by evc_meter_step).
+// The footprint (rows r0 - 1 .. r0 + th, columns c0 - 1 .. c0 + CW, edge-clamped) is staged once in
+// shared memory by coalesced row loads; the upsample runs lane = high-res column (taps per lane
+// hoisted), channel loops over the CTA's real channels only, skipping channels without a flagged
+// low-res tile in the support (their values are exact zeros).
+constexpr int SI_R = 10, SI_C = 34;  // footprint rows (th + 2 <= 10) and columns (CW + 2 <= 34)
+
+__global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* __restrict__ yf, int64_t yfs,
+                                                              int GHy, int GWy, double* __restrict__ part,
+                                                              float* __restrict__ hwc, int64_t hs, int cp, int pitch,
+                                                              uint8_t* __restrict__ fany_lo,
+                                                              uint8_t* __restrict__ fany_hi, int CW, int nJB) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float t[SP_MAXC][SI_R * SI_C + 1];  // [channel][row * SI_C + col] (odd channel stride)
+  __shared__ double s_w[SP_THREADS / 32];
+  __shared__ uint8_t s_fy[SP_MAXC][2][16];  // high-res flags of the owned tiles
+  __shared__ int s_live[SP_MAXC];           // channel has a flagged low-res tile in the support box
+  const int s = blockIdx.z, ti = blockIdx.y, jb = blockIdx.x % nJB, k0 = (blockIdx.x / nJB) * 32;
+  const int r0 = ti * x.th, nrow = min(x.th, x.H - r0);
+  const int c0 = jb * CW, ncol = min(CW, x.W - c0);
+  const int nch = min(32, x.C - k0);  // real channels of the chunk
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jt0 = c0 / x.tw, ntl = (ncol + x.tw - 1) / x.tw;
+  const int Hy = 2 * x.H;
+  const int T0r = 2 * ti, T0c = 2 * c0 / x.tw, ntc = (2 * ncol + x.tw - 1) / x.tw;
+  if (threadIdx.x < SP_MAXC) s_live[threadIdx.x] = 0;
+  for (int e = threadIdx.x; e < SP_MAXC * 2 * 16; e += SP_THREADS) (&s_fy[0][0][0])[e] = 0;
+  __syncthreads();
+  // 1) footprint rows (coalesced: lane = column), support flags, low-res tile map
+  {
+    const int q0 = min(max(c0 - 1 + lane, 0), x.W - 1), q1 = min(max(c0 + 31 + lane, 0), x.W - 1);
+    const bool has1 = lane + 32 < ncol + 2, has0 = lane < ncol + 2;
+    for (int ch = warp; ch < nch; ch += SP_THREADS / 32) {  // every row's loads in flight, then the stores
+      const float* pl = x.plane(s, k0 + ch);
+      float* dst = t[ch];
+      float v0[SI_R], v1[SI_R];
+#pragma unroll
+      for (int fr = 0; fr < SI_R; ++fr) {
+        const float* src = pl + (int64_t)min(max(r0 - 1 + fr, 0), x.H - 1) * x.W;
+        const bool rok = fr < nrow + 2;
+        v0[fr] = (rok && has0) ? __ldg(src + q0) : 0.0f;
+        v1[fr] = (rok && has1) ? __ldg(src + q1) : 0.0f;
+      }
+#pragma unroll
+      for (int fr = 0; fr < SI_R; ++fr) {
+        dst[fr * SI_C + lane] = v0[fr];
+        if (lane + 32 < SI_C) dst[fr * SI_C + lane + 32] = v1[fr];
+      }
+    }
+  }
+  for (int e = threadIdx.x; e < nch * 4 * 8; e += SP_THREADS) {
+    const int ch = e >> 5, rr = (e >> 3) & 3, cc = e & 7;
+    if (rr == 3) continue;
+    const int a = ti - 1 + rr, b = jt0 - 1 + cc;
+    if (a >= 0 && a < x.GH && b >= 0 && b < x.GW && cc < ntl + 2 && x.fplane(s, k0 + ch)[a * x.GW + b]) {
+      s_live[ch] = 1;  // (benign: all store 1)
+      if (rr == 1 && cc >= 1 && cc <= ntl && fany_lo) fany_lo[((int64_t)s * x.GH + ti) * x.GW + b] = 1;
+    }
+  }
+  __syncthreads();
+  // 2) low-res shadow: owned pixels + the ring, lane = channel (256-byte [heads | tails] runs)
+  {
+    const int ra = r0 - (ti == 0 ? 1 : 0), rb = r0 + nrow + (r0 + nrow == x.H ? 1 : 0);
+    const int ca = c0 - (c0 == 0 ? 1 : 0), cb = c0 + ncol + (c0 + ncol == x.W ? 1 : 0);
+    float* base = hwc + (int64_t)s * hs + 2 * k0 + lane;
+    if (lane < nch)
+      for (int pr = ra + warp; pr < rb; pr += SP_THREADS / 32) {
+        const float* tr = &t[lane][(min(max(pr, 0), x.H - 1) - r0 + 1) * SI_C - c0 + 1];
+        float* d = base + (int64_t)pr * pitch * (2 * cp);
+        for (int pc = ca; pc < cb; ++pc) {
+          const float v = tr[min(max(pc, 0), x.W - 1)];
+          const float h = tf32_head(v);
+          d[pc * (2 * cp)] = h;
+          d[pc * (2 * cp) + 32] = __fsub_rn(v, h);
+        }
+      }
+  }
+  // 3) the upsample of the owned high-res block: rows 2 r0 .. 2 (r0 + nrow) - 1; lane = footprint
+  //    column q (low-res column j = c0 - 1 + q): the row interpolation r(j) once per lane, the
+  //    neighbours' by shuffles, then the two output columns 2j (taps j - 1, j: 1/4, 3/4) and 2j + 1
+  //    (taps j, j + 1: 3/4, 1/4) -- dense_upsample's op order (rows, then columns), bit-exact
+  float ss = 0.0f;
+  const int Ya = 2 * r0, Yb = min(Hy, 2 * (r0 + nrow));
+  const bool own = lane >= 1 && lane <= ncol;  // j = c0 + lane - 1 is an owned column
+  const int tje = own ? (2 * (lane - 1)) / x.tw : 0, tjo = own ? (2 * (lane - 1) + 1) / x.tw : 0;
+  for (int ch = warp; ch < nch; ch += SP_THREADS / 32) {
+    if (!s_live[ch]) continue;  // no flagged support: every value is an exact zero (flags stay 0)
+    const float* tc = t[ch] + min(lane, SI_C - 1);
+    uint32_t n00 = 0u, n01 = 0u, n10 = 0u, n11 = 0u;  // [tile row][even, odd column]: OR of magnitude bits
+    for (int Y = Ya; Y < Yb; ++Y) {
+      const Tap tr = tap2(Y, x.H);
+      const float r = __fadd_rn(__fmul_rn(tc[(tr.i0 - r0 + 1) * SI_C], tr.w0), __fmul_rn(tc[(tr.i1 - r0 + 1) * SI_C], tr.w1));
+      const float rl = __shfl_up_sync(0xffffffffu, r, 1), rr = __shfl_down_sync(0xffffffffu, r, 1);
+      const float oe = __fadd_rn(0.0f, __fadd_rn(__fmul_rn(rl, 0.25f), __fmul_rn(r, 0.75f)));
+      const float oo = __fadd_rn(0.0f, __fadd_rn(__fmul_rn(r, 0.75f), __fmul_rn(rr, 0.25f)));
+      if (own) {
+        ss = __fmaf_rn(oe, oe, ss);
+        ss = __fmaf_rn(oo, oo, ss);
+        const uint32_t be = __float_as_uint(oe) & 0x7fffffffu, bo = __float_as_uint(oo) & 0x7fffffffu;
+        if (Y - Ya >= x.th) {  // (two tile rows)
+          n10 |= be;
+          n11 |= bo;
+        } else {
+          n00 |= be;
+          n01 |= bo;
+        }
+      }
+    }
+    if (n00) s_fy[ch][0][tje] = 1;  // (benign: all store 1)
+    if (n01) s_fy[ch][0][tjo] = 1;
+    if (n10) s_fy[ch][1][tje] = 1;
+    if (n11) s_fy[ch][1][tjo] = 1;
+  }
+  const double w = (double)warp_sum(ss);
+  if (lane == 0) s_w[warp] = w;
+  __syncthreads();
+  // 4) flags of every owned (channel, tile) -- written, not accumulated --, the any-map, the partial
+  for (int e = threadIdx.x; e < nch * 2 * 16; e += SP_THREADS) {
+    const int ch = e >> 5, r = (e >> 4) & 1, q = e & 15, Tr = T0r + r, Tc = T0c + q;
+    if (q < ntc && Tr < GHy && Tc < GWy) yf[(int64_t)s * yfs + ((int64_t)(k0 + ch) * GHy + Tr) * GWy + Tc] = s_fy[ch][r][q];
+  }
+  if (threadIdx.x < 32 && fany_hi) {
+    const int r = threadIdx.x / 16, q = threadIdx.x % 16, Tr = T0r + r, Tc = T0c + q;
+    int any = 0;
+    for (int ch = 0; ch < nch; ++ch) any |= s_fy[ch][r][q];
+    if (q < ntc && Tr < GHy && Tc < GWy && any) fany_hi[((int64_t)s * GHy + Tr) * GWy + Tc] = 1;
+  }
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < SP_THREADS / 32; ++k) tot += s_w[k];
+    part[(int64_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = tot;
+  }
 }
 
 // Border correction, a small GEMM per (session, line): out[pos][o] = - sum_{c, k} Wl[o][c][k] U[c][pos - 1 + k]
@@ -97,15 +208,16 @@ __device__ __forceinline__ float up2(const float* xv, int H, int W, int y, int x
 // channels at a time: U of the 34 line positions + the 2 corner sites, and the weights [c][tap][o]
 // (float4 per thread; w is laid out [C][9][c_out] so the staging reads are coalesced).  Fixed
 // summation order: deterministic.
-constexpr int SB_C = 32;
+constexpr int SB_C = 32, SB_SPB = 1;  // channels per K step, sessions per CTA (1: measured fastest)
 
-__global__ void __launch_bounds__(SP_THREADS) k_subpix_border(TView x, const float* __restrict__ w, int co,
+__global__ void __launch_bounds__(SP_THREADS) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
                                                                float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float sU[SB_C][36];               // [c][34 line positions | 2 corner sites]
-  __shared__ __align__(16) float sW[SB_C][9][32];  // [c][tap][o]
-  const int s = blockIdx.z, L = blockIdx.y % 4, oc0 = (blockIdx.y / 4) * 32, p0 = blockIdx.x * 32;
+  __shared__ float sU[SB_C][36];                   // [c][34 line positions | 2 corner sites]
+  __shared__ __align__(16) float sW[SB_C][3][32];  // [c][k][o]: the line's three off-image taps
+  __shared__ __align__(16) float sWc[SB_C][2][3][32];  // row lines with a corner: [c][kc = 0 | 2][kh][o]
+  const int s0 = blockIdx.z * SB_SPB, L = blockIdx.y % 4, oc0 = (blockIdx.y / 4) * 32, p0 = blockIdx.x * 32;
   const int Ho = 2 * x.H, Wo = 2 * x.W, C = x.C;
   const bool rowline = L < 2;
   const int len = rowline ? Wo : Ho;
@@ -114,67 +226,97 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_border(TView x, const flo
   const int other = L == 0 ? 1 : Ho - 2;  // row lines: the corner column's other in-image row
   const int kout = (L == 0 || L == 2) ? 0 : 2;
   const int pl = threadIdx.x & 31, og = threadIdx.x >> 5, pos = p0 + pl;
-  const int no = min(32, co - oc0);
+  const int no = min(32, co - oc0), nss = min(SB_SPB, S - s0);
   const bool corner = rowline && (pos == 0 || pos == Wo - 1);
-  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float acc[SB_SPB][4] = {};
   for (int c0 = 0; c0 < C; c0 += SB_C) {
     const int nc = min(SB_C, C - c0);
     __syncthreads();
-    for (int e = threadIdx.x; e < SB_C * 36; e += SP_THREADS) {
-      const int c = e / 36, q = e % 36;
-      float v = 0.0f;
-      if (c < nc) {
-        const float* xv = x.plane(s, c0 + c);
-        if (q < 34) {
-          const int pp = min(max(p0 - 1 + q, 0), len - 1);
-          v = rowline ? up2(xv, x.H, x.W, fixed, pp) : up2(xv, x.H, x.W, pp, fixed);
-        } else if (rowline && Ho > 1) {
-          v = up2(xv, x.H, x.W, other, q == 34 ? 0 : Wo - 1);
+    {  // 96 (channel, tap) rows of 32 output channels: 12 per warp, every load in flight first
+      const int o = threadIdx.x & 31;
+      float wv[SB_C * 3 / (SP_THREADS / 32)];
+#pragma unroll
+      for (int i = 0; i < SB_C * 3 / (SP_THREADS / 32); ++i) {
+        const int ct = (threadIdx.x >> 5) + i * (SP_THREADS / 32), c = ct / 3, k = ct - 3 * c;
+        const int tap = rowline ? kout * 3 + k : k * 3 + kout;
+        wv[i] = (c < nc && o < no) ? __ldg(w + ((int64_t)(c0 + c) * 9 + tap) * co + oc0 + o) : 0.0f;
+      }
+#pragma unroll
+      for (int i = 0; i < SB_C * 3 / (SP_THREADS / 32); ++i) {
+        const int ct = (threadIdx.x >> 5) + i * (SP_THREADS / 32), c = ct / 3, k = ct - 3 * c;
+        sW[c][k][o] = wv[i];
+      }
+      if (rowline && (p0 == 0 || p0 + 32 >= len)) {  // the column taps of the corners
+        for (int ct = threadIdx.x >> 5; ct < SB_C * 6; ct += SP_THREADS / 32) {
+          const int c = ct / 6, r = ct - 6 * c, kcs = r / 3, kh = r - 3 * kcs;
+          sWc[c][kcs][kh][o] = (c < nc && o < no) ? __ldg(w + ((int64_t)(c0 + c) * 9 + kh * 3 + 2 * kcs) * co + oc0 + o)
+                                                  : 0.0f;
         }
       }
-      sU[c][q] = v;
     }
-    for (int e = threadIdx.x; e < SB_C * 9 * 32; e += SP_THREADS) {
-      const int o = e & 31, rest = e >> 5, tap = rest % 9, c = rest / 9;
-      sW[c][tap][o] = (c < nc && o < no) ? w[((int64_t)(c0 + c) * 9 + tap) * co + oc0 + o] : 0.0f;
-    }
-    __syncthreads();
-    if (pos < len && 4 * og < no) {
-      for (int c = 0; c < nc; ++c) {
-        const float u0 = sU[c][pl], u1 = sU[c][pl + 1], u2 = sU[c][pl + 2];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const float uk = k == 0 ? u0 : (k == 1 ? u1 : u2);
-          const int tap = rowline ? kout * 3 + k : k * 3 + kout;
-          const float4 wv = *reinterpret_cast<const float4*>(&sW[c][tap][4 * og]);
-          acc[0] = __fmaf_rn(wv.x, uk, acc[0]);
-          acc[1] = __fmaf_rn(wv.y, uk, acc[1]);
-          acc[2] = __fmaf_rn(wv.z, uk, acc[2]);
-          acc[3] = __fmaf_rn(wv.w, uk, acc[3]);
-        }
-        if (corner) {  // taps (kh, kc) leaving through the column: rows fixed (line value) and `other`
-          const int kc = pos == 0 ? 0 : 2;
-#pragma unroll
-          for (int kh = 0; kh < 3; ++kh) {
-            const int yy = fixed + kh - 1;
-            if (yy < 0 || yy >= Ho) continue;  // (counted on the row line)
-            const float uk = yy == fixed ? sU[c][pl + 1] : sU[c][pos == 0 ? 34 : 35];
-            const float4 wv = *reinterpret_cast<const float4*>(&sW[c][kh * 3 + kc][4 * og]);
-            acc[0] = __fmaf_rn(wv.x, uk, acc[0]);
-            acc[1] = __fmaf_rn(wv.y, uk, acc[1]);
-            acc[2] = __fmaf_rn(wv.z, uk, acc[2]);
-            acc[3] = __fmaf_rn(wv.w, uk, acc[3]);
+    for (int sl = 0; sl < SB_SPB; ++sl) {
+      if (sl >= nss) break;
+      const int s = s0 + sl;
+      __syncthreads();
+      for (int e = threadIdx.x; e < SB_C * 64; e += SP_THREADS) {
+        const int c = e >> 6, q = e & 63;
+        if (q >= 36) continue;
+        float v = 0.0f;
+        if (c < nc) {
+          const float* xv = x.plane(s, c0 + c);
+          if (q < 34) {
+            const int pp = min(max(p0 - 1 + q, 0), len - 1);
+            v = rowline ? up2(xv, x.H, x.W, fixed, pp) : up2(xv, x.H, x.W, pp, fixed);
+          } else if (rowline) {
+            v = up2(xv, x.H, x.W, other, q == 34 ? 0 : Wo - 1);
           }
         }
+        sU[c][q] = v;
+      }
+      __syncthreads();
+      if (pos < len && 4 * og < no) {
+        float a4[4] = {acc[sl][0], acc[sl][1], acc[sl][2], acc[sl][3]};
+        for (int c = 0; c < nc; ++c) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float uk = sU[c][pl + k];
+            const float4 wv = *reinterpret_cast<const float4*>(&sW[c][k][4 * og]);
+            a4[0] = __fmaf_rn(wv.x, uk, a4[0]);
+            a4[1] = __fmaf_rn(wv.y, uk, a4[1]);
+            a4[2] = __fmaf_rn(wv.z, uk, a4[2]);
+            a4[3] = __fmaf_rn(wv.w, uk, a4[3]);
+          }
+          if (corner) {  // taps (kh, kc) leaving through the column: rows fixed (line value) and `other`
+            const int kc = pos == 0 ? 0 : 2;
+#pragma unroll
+            for (int kh = 0; kh < 3; ++kh) {
+              const int yy = fixed + kh - 1;
+              if (yy < 0 || yy >= Ho) continue;  // (counted on the row line)
+              const float uk = yy == fixed ? sU[c][pl + 1] : sU[c][pos == 0 ? 34 : 35];
+              const float4 wv = *reinterpret_cast<const float4*>(&sWc[c][kc >> 1][kh][4 * og]);
+              a4[0] = __fmaf_rn(wv.x, uk, a4[0]);
+              a4[1] = __fmaf_rn(wv.y, uk, a4[1]);
+              a4[2] = __fmaf_rn(wv.z, uk, a4[2]);
+              a4[3] = __fmaf_rn(wv.w, uk, a4[3]);
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[sl][j] = a4[j];
       }
     }
   }
   if (pos < len) {
     const int li = L == 0 ? pos : (L == 1 ? Wo + pos : (L == 2 ? 2 * Wo + pos : 2 * Wo + Ho + pos));
-    float* o = out + ((int64_t)s * 2 * (Ho + Wo) + li) * co + oc0 + 4 * og;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (4 * og + j < no) o[j] = -acc[j];
+    for (int sl = 0; sl < SB_SPB; ++sl) {
+      if (sl >= nss) break;
+      float* o = out + ((int64_t)(s0 + sl) * 2 * (Ho + Wo) + li) * co + oc0 + 4 * og;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (4 * og + j < no) o[j] = -acc[sl][j];
+    }
   }
 }
 
@@ -186,17 +328,36 @@ using namespace evc;
 
 extern "C" {
 
-int evc_subpixel_prep(const evc_tensor* x, float* hwc, int32_t cp, int64_t hwc_stride, int32_t pitch, uint8_t* fany,
-                      int32_t S, void* stream) {
-  EVC_CHECK_ARG(x && hwc && S > 0, "subpixel_prep: null argument");
-  EVC_CHECK_ARG(cp >= x->C && cp % 32 == 0 && pitch >= x->W + 2 && x->th <= 8 && x->tw <= 32,
-                "subpixel_prep: shadow channels (multiple of 32 >= C), pitch >= W + 2, tiles <= 8 x 32");
+static void si_geom(const TView& v, int cp, int& CW, int& nJB, int& nx) {
+  CW = v.tw * (32 / v.tw);
+  nJB = (v.W + CW - 1) / CW;
+  nx = nJB * ((cp + 31) / 32);
+}
+
+int64_t evc_subpixel_input_partials(const evc_tensor* x, int32_t cp) {
+  if (!x) return -1;
   const TView v = view_of(*x);
-  const int CW = v.tw * (32 / v.tw), nJB = (v.W + CW - 1) / CW;
-  const dim3 grid((unsigned)(nJB * (cp / 32)), (unsigned)v.GH, (unsigned)S);
-  launch_pdl(k_subpix_prep, grid, dim3(SP_THREADS), 0, as_stream(stream), v, hwc, hwc_stride, (int)cp, (int)pitch,
-             fany, CW, nJB);
-  EVC_LAUNCH_CHECK("subpixel_prep");
+  int CW, nJB, nx;
+  si_geom(v, cp, CW, nJB, nx);
+  return (int64_t)nx * v.GH;
+}
+
+int evc_subpixel_input(const evc_tensor* x, const evc_tensor* y, double* partials, float* hwc, int32_t cp,
+                       int64_t hwc_stride, int32_t pitch, uint8_t* fany_lo, uint8_t* fany_hi, int32_t S, void* stream) {
+  EVC_CHECK_ARG(x && x->flags && y && y->flags && partials && hwc && S > 0, "subpixel_input: null argument");
+  EVC_CHECK_ARG(y->C == x->C && y->H == 2 * x->H && y->W == 2 * x->W && y->th == x->th && y->tw == x->tw &&
+                    x->th % 2 == 0 && x->tw % 2 == 0 && x->th <= 8 && x->tw >= 6 && x->tw <= 32,
+                "subpixel_input: y must be the 2x upsample of x with the same even tiles (th <= 8, 6 <= tw <= 32)");
+  EVC_CHECK_ARG(cp >= x->C && cp % 32 == 0 && pitch >= x->W + 2,
+                "subpixel_input: shadow channels (multiple of 32 >= C), pitch >= W + 2");
+  const TView v = view_of(*x);
+  const TView vy = view_of(*y);
+  int CW, nJB, nx;
+  si_geom(v, cp, CW, nJB, nx);
+  launch_pdl(k_subpix_input, dim3((unsigned)nx, (unsigned)v.GH, (unsigned)S), dim3(SP_THREADS), 0,
+             as_stream(stream), v, vy.f, vy.fs, vy.GH, vy.GW, partials, hwc, hwc_stride, (int)cp, (int)pitch, fany_lo,
+             fany_hi, CW, nJB);
+  EVC_LAUNCH_CHECK("subpixel_input");
   return EVC_OK;
 }
 
@@ -204,8 +365,9 @@ int evc_subpixel_border(const evc_tensor* x, const float* w, int32_t c_out, floa
   EVC_CHECK_ARG(x && w && out && c_out > 0 && c_out % 4 == 0 && S > 0, "subpixel_border: null argument");
   const TView v = view_of(*x);
   const int len = 2 * std::max(v.H, v.W);
-  const dim3 grid((unsigned)((len + 31) / 32), (unsigned)(4 * ((c_out + 31) / 32)), (unsigned)S);
-  launch_pdl(k_subpix_border, grid, dim3(SP_THREADS), 0, as_stream(stream), v, w, (int)c_out, out);
+  const dim3 grid((unsigned)((len + 31) / 32), (unsigned)(4 * ((c_out + 31) / 32)),
+                  (unsigned)((S + SB_SPB - 1) / SB_SPB));
+  launch_pdl(k_subpix_border, grid, dim3(SP_THREADS), 0, as_stream(stream), v, w, (int)c_out, (int)S, out);
   EVC_LAUNCH_CHECK("subpixel_border");
   return EVC_OK;
 }

@@ -36,9 +36,14 @@ from .tensors import (
     as_bias,
     as_matrix,
     as_tensor,
+    conv_geometry,
     conv_output_hw,
     grid_shape,
 )
+
+# The sub-pixel decoder form (ConvPlan._init_subpixel) by default only for batched sessions: measured on
+# C1 it wins at 32 streams, while a single stream's latency is lower with the high-res path.
+SUBPIXEL_MIN_SESSIONS = 8
 
 __all__ = [
     "GraphError",
@@ -695,7 +700,11 @@ class Graph:
                     and up.spec.id not in self.output_ids and tile.w <= 32 and tile.h <= 8
                     and os.environ.get("EVC_NO_UPFUSE", "0") != "1"):
                 self._fused_up.add(up.spec.id)
-                node.nparts = int(self.lib.evc_upsample_sparsify_partials(self._desc(node.spec.id)))
+                if node.subpixel_conv is not None:  # (evc_subpixel_input's CTAs)
+                    node.nparts = int(self.lib.evc_subpixel_input_partials(self._desc(up.spec.inputs[0]),
+                                                                           node.subpixel_conv.plan.cp))
+                else:
+                    node.nparts = int(self.lib.evc_upsample_sparsify_partials(self._desc(node.spec.id)))
             else:
                 node.nparts = int(self.lib.evc_sparsify_partials(self._desc(node.spec.inputs[0])))
         # per-node partial sums of the sparsify norms, folded by the end-of-step kernel
@@ -789,6 +798,9 @@ class Graph:
         """The upsample node when `node` reads upsample(2x bilinear) -> sparsify(t_p = 0) -> node
         with nothing else reading either, so the pair runs in sub-pixel form (ConvPlan._init_subpixel):
         the sparsify only derives flags, any-map and norm partials, the conv reads the low-res input."""
+        mode = os.environ.get("EVC_SUBPIXEL", "auto")  # "1" always, "0" never, "auto": >= 8 sessions
+        if mode == "0" or (mode != "1" and self.S < SUBPIXEL_MIN_SESSIONS):
+            return None
         sp = self._by_id.get(node.spec.inputs[0])
         if (sp is None or sp.kind != "sparsify" or sp.tp != 0.0 or self._consumers[sp.spec.id] != [node.spec.id]
                 or sp.spec.id in self.output_ids or node.spec.id in self.scatter_convs):
@@ -797,9 +809,17 @@ class Graph:
         if (up is None or up.kind != "upsample" or up.spec.attrs.get("mode", "nearest") != "bilinear"
                 or int(up.spec.attrs.get("factor", 2)) != 2 or self._consumers[up.spec.id] != [sp.spec.id]
                 or up.spec.id in self.output_ids
-                or self.tile.w > 32 or self.tile.h > 8 or os.environ.get("EVC_NO_UPFUSE", "0") == "1"):
+                or self.tile.w > 32 or self.tile.w < 6 or self.tile.h > 8 or self.tile.w % 2 or self.tile.h % 2
+                or os.environ.get("EVC_NO_UPFUSE", "0") == "1"):
             return None
         if not ConvPlan.subpixel_ok(node.weight, stride, pad, ish[1], ish[2]):
+            return None
+        # the composed launch must run a channel block of >= 64 composed channels, not packed
+        g, _ = conv_geometry(ish[0], 4 * int(node.weight.shape[0]), 3, 3, 1, 1, ish[1] // 2, ish[2] // 2,
+                             self.tile.h, self.tile.w)
+        cfg = _lib.EvcConvCfg()
+        _lib.check(self.lib.evc_conv_fused_config(g, self.S, int(self.max_splits), cfg), "conv_fused_config")
+        if cfg.bn < 64 or cfg.row == 2 or cfg.thin:
             return None
         return up
 
@@ -911,14 +931,21 @@ class Graph:
                                                node.acc[0].numel(), self._desc(nid), code, alpha, S), "act_delta"))
             elif k == "sparsify" and node.sp_fused_by is not None:
                 continue  # evaluated in the producing conv's epilogue
+            elif k == "sparsify" and ns.inputs[0] in self._fused_up and node.subpixel_conv is not None:
+                # the conv reads the low-res input: its shadow, the sparsify's flags / any-map / norm
+                # partials in one pass over the low-res tensor, plus the border correction
+                up = self._by_id[ns.inputs[0]]
+                extra = node.subpixel_conv.plan.subpixel_launches(self._desc(up.spec.inputs[0]), self._desc(nid),
+                                                                  node.part_ptr, node.shadow.fany_ptr)
+                prog.extend(extra)
+                self._dense_up[up.spec.id] = extra[0]
+                self._dense_subpixel[up.spec.id] = extra[1:]
             elif k == "sparsify" and ns.inputs[0] in self._fused_up:
                 j = node.sp_idx
                 up = self._by_id[ns.inputs[0]]
                 sh = node.shadow
                 hwc = ((sh.hwc_interior, sh.cpa, sh.hwc[0].numel(), sh.pitch, sh.fany_ptr) if sh is not None
                        else (None, 0, 0, 0, None))
-                if node.subpixel_conv is not None:  # flags / any-map / partials only: the conv reads low-res
-                    hwc = (None, 0, 0, 0, sh.fany_ptr)
                 mode = 0 if up.spec.attrs.get("mode", "nearest") == "nearest" else 1
                 prog.append((L.evc_upsample_sparsify, (self._desc(up.spec.inputs[0]), int(up.spec.attrs.get("factor", 2)),
                                                        mode, node.delta.data_ptr(), node.delta[0].numel(),
@@ -930,10 +957,6 @@ class Graph:
                              "upsample_sparsify"))
                 if node.tp == 0.0:  # the dense pass reuses it with every input tile live (_dense_program)
                     self._dense_up[up.spec.id] = prog[-1]
-                if node.subpixel_conv is not None:
-                    extra = node.subpixel_conv.plan.subpixel_launches(self._desc(up.spec.inputs[0]))
-                    prog.extend(extra)
-                    self._dense_subpixel[up.spec.id] = extra
             elif k == "upsample" and nid in self._fused_up:
                 continue  # evaluated inside the consumer's fused upsample_sparsify
             elif k == "sparsify":

@@ -246,10 +246,9 @@ def conv_geometry(c_in, c_out, kh, kw, stride, pad, h, w, th, tw):
 
 
 CONV_KERNEL = os.environ.get("EVC_CONV_KERNEL", "tc")  # "tc" (tcgen05 3xTF32), "tile" (gathered tiles only), "simt"
-# Sub-pixel decoder convs (ConvPlan._init_subpixel) are opt-in (EVC_SUBPIXEL=1): measured on C1 at 32
-# streams the composed conv reads 4x fewer operand bytes but costs the same (epilogue-bound), and the
-# extra low-res shadow / border passes make the step slower (measured and rejected).  Only
-# thin decoder convs qualify: with C_out > 32 the composed conv was no faster even in isolation.
+# Sub-pixel decoder convs (ConvPlan._init_subpixel; the Graph's policy: graph.SUBPIXEL_MIN_SESSIONS,
+# EVC_SUBPIXEL) only for thin decoder convs: with C_out > 32 the composed conv (4 x C_out channels on
+# the low-res grid) was no faster than the high-res one even in isolation (scripts/conv_bench.py).
 SUBPIXEL_MAX_COUT = int(os.environ.get("EVC_SUBPIXEL_MAX_COUT", "32"))
 
 
@@ -349,9 +348,8 @@ class ConvPlan:
     def subpixel_ok(weight, stride, pad, h, w) -> bool:
         """Whether a conv fed by a 2x bilinear upsample can run in sub-pixel form."""
         c_out, _, kh, kw = (int(v) for v in weight.shape)
-        return (kh == kw == 3 and stride == 1 and pad == 1 and c_out % 16 == 0 and h % 2 == 0 and w % 2 == 0
-                and c_out <= SUBPIXEL_MAX_COUT and CONV_KERNEL == "tc"
-                and os.environ.get("EVC_SUBPIXEL", "0") == "1")
+        return (kh == kw == 3 and stride == 1 and pad == 1 and c_out % 4 == 0 and h % 2 == 0 and w % 2 == 0
+                and c_out <= SUBPIXEL_MAX_COUT and CONV_KERNEL == "tc")
 
     def _init_subpixel(self, weight, h, w, th, tw, S, max_splits):
         """Sub-pixel plan (csrc/subpixel.cu): the conv of the 2x bilinear upsample of a (C, h/2, w/2)
@@ -394,12 +392,13 @@ class ConvPlan:
         self.border = torch.zeros((S, 2 * (ho + wo), c_out), dtype=torch.float32, device=weight.device)
         self.dense_flops = 2 * 9 * c_in * c_out * ho * wo
 
-    def subpixel_launches(self, dlo):
-        """[(fn, args-without-stream, name)] writing the composed conv's inputs from the low-res
-        tensor dlo (the upsample's input): low-res shadow + tile map, border correction."""
+    def subpixel_launches(self, dlo, dy, part_ptr, fany_hi):
+        """[(fn, args-without-stream, name)] of the composed conv's inputs, from the low-res tensor dlo
+        (the upsample's input): evc_subpixel_input (low-res shadow + tile map, and the sparsify's
+        flags dy / any-map fany_hi / norm partials at part_ptr), evc_subpixel_border."""
         L = _lib.lib()
-        return [(L.evc_subpixel_prep, (dlo, self.hwc_interior, self.cp, self.hwc[0].numel(), self.pitch,
-                                       self.fany_lo_ptr, self.S), "subpixel_prep"),
+        return [(L.evc_subpixel_input, (dlo, dy, part_ptr, self.hwc_interior, self.cp, self.hwc[0].numel(),
+                                        self.pitch, self.fany_lo_ptr, fany_hi, self.S), "subpixel_input"),
                 (L.evc_subpixel_border, (dlo, self.wborder.data_ptr(), self.c_out, self.border.data_ptr(), self.S),
                  "subpixel_border")]
 
@@ -481,16 +480,15 @@ _SUBPIX_TAPS[1, 1, 2], _SUBPIX_TAPS[1, 2, 2] = 0.25, 0.75
 
 
 def compose_subpixel(weight) -> np.ndarray:
-    """(4 C_out, C_in, 3, 3) weights of the sub-pixel conv: composed channel (2a + b) * C_out + o is
-    output channel o at phase (a, b) (site (2i + a, 2j + b)) of conv3x3(upsample2x_bilinear(x)),
+    """(4 C_out, C_in, 3, 3) weights of the sub-pixel conv: composed channel 4 o + 2 a + b (phase-minor)
+    is output channel o at phase (a, b) (site (2i + a, 2j + b)) of conv3x3(upsample2x_bilinear(x)),
     evaluated on x itself (edge-replicated).  Composed in float64, rounded once."""
     w = np.asarray(weight, dtype=np.float64)
     co = w.shape[0]
     out = np.zeros((4 * co, *w.shape[1:]))
     for a in range(2):
         for b in range(2):
-            out[(2 * a + b) * co:(2 * a + b + 1) * co] = np.einsum("yk,xl,oikl->oiyx", _SUBPIX_TAPS[a],
-                                                                   _SUBPIX_TAPS[b], w)
+            out[2 * a + b::4] = np.einsum("yk,xl,oikl->oiyx", _SUBPIX_TAPS[a], _SUBPIX_TAPS[b], w)
     return out.astype(np.float32)
 
 

@@ -23,7 +23,7 @@ def subpixel_conv(x, w):
     out = np.zeros((co, H, W))
     for a in range(2):
         for b in range(2):
-            out[:, a::2, b::2] = lo[(2 * a + b) * co:(2 * a + b + 1) * co]
+            out[:, a::2, b::2] = lo[2 * a + b::4]
     u = O.dense_upsample(x, 2, "bilinear").astype(np.float64)
     w64 = w.astype(np.float64)
     for Y in range(H):

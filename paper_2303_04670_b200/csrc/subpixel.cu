@@ -209,14 +209,16 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
 // (float4 per thread; w is laid out [C][9][c_out] so the staging reads are coalesced).  Fixed
 // summation order: deterministic.
 constexpr int SB_C = 32, SB_SPB = 1;  // channels per K step, sessions per CTA (1: measured fastest)
+constexpr int SB_WL = 20;             // low-res window along a line: 34 positions -> <= 19 columns
 
-__global__ void __launch_bounds__(SP_THREADS) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
+__global__ void __launch_bounds__(SP_THREADS, 4) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
                                                                float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   __shared__ float sU[SB_C][36];                   // [c][34 line positions | 2 corner sites]
   __shared__ __align__(16) float sW[SB_C][3][32];  // [c][k][o]: the line's three off-image taps
   __shared__ __align__(16) float sWc[SB_C][2][3][32];  // row lines with a corner: [c][kc = 0 | 2][kh][o]
+  __shared__ float sL[SB_C][2][SB_WL];                 // low-res window: [c][across tap][along]
   const int s0 = blockIdx.z * SB_SPB, L = blockIdx.y % 4, oc0 = (blockIdx.y / 4) * 32, p0 = blockIdx.x * 32;
   const int Ho = 2 * x.H, Wo = 2 * x.W, C = x.C;
   const bool rowline = L < 2;
@@ -228,6 +230,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_border(TView x, const flo
   const int pl = threadIdx.x & 31, og = threadIdx.x >> 5, pos = p0 + pl;
   const int no = min(32, co - oc0), nss = min(SB_SPB, S - s0);
   const bool corner = rowline && (pos == 0 || pos == Wo - 1);
+  // the two low-res lines across the line (taps of the fixed coordinate) and the window along it
+  const Tap tx = tap2(fixed, rowline ? x.H : x.W);
+  const int ac0 = tx.i0, ac1 = tx.i1;
+  const int wlo = tap2(max(p0 - 1, 0), rowline ? x.W : x.H).i0;
   float acc[SB_SPB][4] = {};
   for (int c0 = 0; c0 < C; c0 += SB_C) {
     const int nc = min(SB_C, C - c0);
@@ -259,17 +265,47 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_border(TView x, const flo
       if (sl >= nss) break;
       const int s = s0 + sl;
       __syncthreads();
-      for (int e = threadIdx.x; e < SB_C * 64; e += SP_THREADS) {
-        const int c = e >> 6, q = e & 63;
-        if (q >= 36) continue;
+      {  // the low-res window under the line (2 lines x <= 20 along it per channel), loads first
+        float lv[SB_C * 2 * SB_WL / SP_THREADS];
+#pragma unroll
+        for (int i = 0; i < SB_C * 2 * SB_WL / SP_THREADS; ++i) {
+          const int e = threadIdx.x + i * SP_THREADS, c = e / (2 * SB_WL), r = e - c * 2 * SB_WL;
+          const int k = r / SB_WL, q = r - k * SB_WL;
+          const int along = min(wlo + q, (rowline ? x.W : x.H) - 1);
+          const int across = k ? ac1 : ac0;
+          lv[i] = c < nc ? __ldg(x.plane(s, c0 + c) + (rowline ? (int64_t)across * x.W + along
+                                                               : (int64_t)along * x.W + across))
+                         : 0.0f;
+        }
+#pragma unroll
+        for (int i = 0; i < SB_C * 2 * SB_WL / SP_THREADS; ++i) {
+          const int e = threadIdx.x + i * SP_THREADS, c = e / (2 * SB_WL), r = e - c * 2 * SB_WL;
+          sL[c][r / SB_WL][r % SB_WL] = lv[i];
+        }
+      }
+      __syncthreads();
+      // U along the line from the window (dense_upsample's op order: rows first, then columns); the
+      // corners' other-row sites straight from global memory (2 per channel)
+      for (int e = threadIdx.x; e < SB_C * 36; e += SP_THREADS) {
+        const int c = e / 36, q = e - 36 * c;
         float v = 0.0f;
         if (c < nc) {
-          const float* xv = x.plane(s, c0 + c);
           if (q < 34) {
             const int pp = min(max(p0 - 1 + q, 0), len - 1);
-            v = rowline ? up2(xv, x.H, x.W, fixed, pp) : up2(xv, x.H, x.W, pp, fixed);
+            const Tap ta = tap2(pp, rowline ? x.W : x.H);  // along the line
+            const float a0 = sL[c][0][ta.i0 - wlo], a1 = sL[c][1][ta.i0 - wlo];
+            const float b0 = sL[c][0][ta.i1 - wlo], b1 = sL[c][1][ta.i1 - wlo];
+            if (rowline) {  // rows (across) first: r(col) = x[ac0][col] w0 + x[ac1][col] w1, then columns
+              const float ra = __fadd_rn(__fmul_rn(a0, tx.w0), __fmul_rn(a1, tx.w1));
+              const float rb = __fadd_rn(__fmul_rn(b0, tx.w0), __fmul_rn(b1, tx.w1));
+              v = __fadd_rn(__fmul_rn(ra, ta.w0), __fmul_rn(rb, ta.w1));
+            } else {  // rows (along) first: r(col k) = x[row i0][k] w0 + x[row i1][k] w1, then the columns
+              const float ra = __fadd_rn(__fmul_rn(a0, ta.w0), __fmul_rn(b0, ta.w1));
+              const float rb = __fadd_rn(__fmul_rn(a1, ta.w0), __fmul_rn(b1, ta.w1));
+              v = __fadd_rn(__fmul_rn(ra, tx.w0), __fmul_rn(rb, tx.w1));
+            }
           } else if (rowline) {
-            v = up2(xv, x.H, x.W, other, q == 34 ? 0 : Wo - 1);
+            v = up2(x.plane(s, c0 + c), x.H, x.W, other, q == 34 ? 0 : Wo - 1);
           }
         }
         sU[c][q] = v;

@@ -93,6 +93,17 @@ class StreamPipeline:
         return n
 
 
+def window_bounds(t, taus, delta):
+    """(lo, hi) event-index arrays of every window (tau - delta, tau] of the time-sorted timestamps t
+    (slice_window, events.py:240-248, for all taus at once): one vectorised searchsorted per edge, the keys in
+    t's own dtype (a Python-int key makes numpy convert the whole array on every call)."""
+    t = np.asarray(t)
+    ends = np.asarray(taus, dtype=np.int64)
+    starts = ends - int(delta)
+    lo = np.searchsorted(t, np.maximum(starts, 0).astype(t.dtype), side="right")
+    return np.where(starts < 0, 0, lo), np.searchsorted(t, ends.astype(t.dtype), side="right")
+
+
 class EventPipeline:
     """Serving loop from raw events: per step, only the newly arrived
     packed EVB records of every session cross PCIe.
@@ -189,9 +200,10 @@ class EventPipeline:
         prev_hi = None
         self.h2d_bytes = []
 
+        lo_all, hi_all = zip(*(window_bounds(t_host[s], taus[s], self.window_us) for s in range(S)))
+
         def bounds_of(i):
-            return [(int(np.searchsorted(t_host[s], taus[s][i] - self.window_us, side="right")),
-                     int(np.searchsorted(t_host[s], taus[s][i], side="right"))) for s in range(S)]
+            return [(int(lo_all[s][i]), int(hi_all[s][i])) for s in range(S)]
 
         def stage(i, bnds, prev):
             k = i % 2

@@ -241,3 +241,16 @@ def test_conv_launch_configuration_rules():
         assert s1[nid][1] == 1, (nid, s1[nid])
     assert s32["enc3"][1:] == (0, 128, 1) and s32["res0a"][3] == 1  # 128 CTAs: no split-K
     assert s1["res0a"][3] >= 2 and s1["enc3"][3] >= 2  # short grids: cluster split-K
+
+
+def test_window_bounds_match_slice_window():
+    """serving.window_bounds (all windows of the e2e loop at once) == slice_window per window."""
+    from paper_2303_04670_b200.serving import window_bounds
+
+    st = evc.generate_events(seed=3, duration_us=80_000, rate_hz=2.0e5, n_objects=4, sensor_size=(64, 64))
+    taus = [0, 5, 1_000, 30_000, 50_000, 50_001, 79_999, 80_000, 95_000]
+    for delta in (1, 1_000, 50_000):
+        lo, hi = window_bounds(st.t, taus, delta)
+        for i, tau in enumerate(taus):
+            w = evc.slice_window(st, tau, delta)
+            assert (int(lo[i]), int(hi[i])) == (w.lo, w.hi), (tau, delta)

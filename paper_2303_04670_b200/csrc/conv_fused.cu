@@ -131,31 +131,42 @@ __device__ __noinline__ void side_work(const Args& a, int s, int q, int Qs, int 
   const uint8_t* fa = a.fany_side + (int64_t)s * Ti;
   const int32_t* boxr = a.tab + h.boxr;
   const int32_t* boxc = a.tab + h.boxc;
-  // output tile flags, (channel, tile) order -> coalesced byte stores
+  // output tile flags: every channel's flag is the receptive-box OR of the any-channel map; work unit =
+  // (tile, 16 channels): the box OR once per unit, 16 byte stores (coalesced across threads: consecutive tiles)
   uint8_t* of = a.oflags + (int64_t)s * a.ofs;
-  const int nflag = a.oc * To;
-  for (int e = gid; e < nflag; e += nthr) {
-    const int tt = e % To;
+  const int nocj = (a.oc + 15) >> 4;
+  for (int e = gid; e < nocj * To; e += nthr) {
+    const int cj = e / To, tt = e - cj * To;
     const int i = tt / GWo, j = tt - i * GWo;
     const int r0 = boxr[2 * i], r1 = boxr[2 * i + 1], c0 = boxc[2 * j], c1 = boxc[2 * j + 1];
     int nf = 0;
     for (int r = r0; r <= r1; ++r)
       for (int c = c0; c <= c1; ++c) nf |= fa[r * GWi + c];
-    of[e] = nf != 0;
+    const uint8_t v = nf != 0;
+    uint8_t* o = of + (int64_t)(cj * 16) * To + tt;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (cj * 16 + k < a.oc) o[(int64_t)k * To] = v;
   }
-  // meter: live-flag count, weighted count and border padding term
+  // meter: live-flag count and weighted count; work unit = (tile, 8 channels): the tile's weight once,
+  // eight independent flag loads (coalesced across threads: consecutive tiles)
   int cnt = 0;
   long long w = 0;
   const uint8_t* F = a.in_f + (int64_t)s * a.in_fs;
   const int32_t* rt = a.tab + h.rt;
   const int32_t* ct = a.tab + h.ct;
-  const int nin = a.c_in * Ti;
-  for (int e = gid; e < nin; e += nthr) {
-    if (F[e]) {
-      const int tt = e % Ti;
+  const int nchk = (a.c_in + 7) >> 3, nunit = nchk * Ti;
+  for (int e = gid; e < nunit; e += nthr) {
+    const int ck = e / Ti, tt = e - ck * Ti;
+    const uint8_t* Fc = F + (int64_t)(ck * 8) * Ti + tt;
+    int live = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (ck * 8 + k < a.c_in) live += Fc[(int64_t)k * Ti] != 0;
+    if (live) {
       const int i = tt / GWi;
-      ++cnt;
-      w += (long long)(rt[i] * ct[tt - i * GWi]);
+      cnt += live;
+      w += (long long)live * (rt[i] * ct[tt - i * GWi]);
     }
   }
   const int nbd = h.ngrp * a.c_in;

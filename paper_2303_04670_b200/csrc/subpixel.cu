@@ -24,7 +24,8 @@
 
 namespace evc {
 
-constexpr int SP_THREADS = 256, SP_MAXC = 32;
+constexpr int SP_THREADS = 256;
+constexpr int SI_CH = 40;  // channels per input-pass CTA: a chunk of 32, the last one takes a remainder <= 8
 
 // Half-pixel 2x bilinear tap of output index o (tensors.py:259-266 for factor 2, the values
 // bilinear_tap computes, in closed form): o = 2i -> (i - 1, i) with (1/4, 3/4), o = 2i + 1 -> (i, i + 1)
@@ -77,20 +78,22 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
                                                               uint8_t* __restrict__ fany_hi, int CW, int nJB) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float t[SP_MAXC][SI_R * SI_C + 1];  // [channel][row * SI_C + col] (odd channel stride)
+  extern __shared__ float si_dyn[];                   // [channel][row * SI_C + col] (odd channel stride)
+  float(*t)[SI_R * SI_C + 1] = reinterpret_cast<float(*)[SI_R * SI_C + 1]>(si_dyn);
   __shared__ double s_w[SP_THREADS / 32];
-  __shared__ uint8_t s_fy[SP_MAXC][2][16];  // high-res flags of the owned tiles
-  __shared__ int s_live[SP_MAXC];           // channel has a flagged low-res tile in the support box
+  __shared__ uint8_t s_fy[SI_CH][2][16];  // high-res flags of the owned tiles
+  __shared__ int s_live[SI_CH];           // channel has a flagged low-res tile in the support box
   const int s = blockIdx.z, ti = blockIdx.y, jb = blockIdx.x % nJB, k0 = (blockIdx.x / nJB) * 32;
   const int r0 = ti * x.th, nrow = min(x.th, x.H - r0);
   const int c0 = jb * CW, ncol = min(CW, x.W - c0);
-  const int nch = min(32, x.C - k0);  // real channels of the chunk
+  // real channels of the chunk: 32, the last chunk also the remainder (<= 8) of C past a multiple of 32
+  const int nch = (x.C - k0 <= SI_CH) ? x.C - k0 : 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int jt0 = c0 / x.tw, ntl = (ncol + x.tw - 1) / x.tw;
   const int Hy = 2 * x.H;
   const int T0r = 2 * ti, T0c = 2 * c0 / x.tw, ntc = (2 * ncol + x.tw - 1) / x.tw;
-  if (threadIdx.x < SP_MAXC) s_live[threadIdx.x] = 0;
-  for (int e = threadIdx.x; e < SP_MAXC * 2 * 16; e += SP_THREADS) (&s_fy[0][0][0])[e] = 0;
+  if (threadIdx.x < SI_CH) s_live[threadIdx.x] = 0;
+  for (int e = threadIdx.x; e < SI_CH * 2 * 16; e += SP_THREADS) (&s_fy[0][0][0])[e] = 0;
   __syncthreads();
   // 1) footprint rows (coalesced: lane = column), support flags, low-res tile map
   {
@@ -128,10 +131,10 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
   {
     const int ra = r0 - (ti == 0 ? 1 : 0), rb = r0 + nrow + (r0 + nrow == x.H ? 1 : 0);
     const int ca = c0 - (c0 == 0 ? 1 : 0), cb = c0 + ncol + (c0 + ncol == x.W ? 1 : 0);
-    float* base = hwc + (int64_t)s * hs + 2 * k0 + lane;
-    if (lane < nch)
+    for (int cl = lane; cl < nch; cl += 32) {  // (a second pass for the remainder channels)
+      float* base = hwc + (int64_t)s * hs + 2 * ((k0 + cl) & ~31) + ((k0 + cl) & 31);  // hwc_head layout
       for (int pr = ra + warp; pr < rb; pr += SP_THREADS / 32) {
-        const float* tr = &t[lane][(min(max(pr, 0), x.H - 1) - r0 + 1) * SI_C - c0 + 1];
+        const float* tr = &t[cl][(min(max(pr, 0), x.H - 1) - r0 + 1) * SI_C - c0 + 1];
         float* d = base + (int64_t)pr * pitch * (2 * cp);
         for (int pc = ca; pc < cb; ++pc) {
           const float v = tr[min(max(pc, 0), x.W - 1)];
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
           d[pc * (2 * cp) + 32] = __fsub_rn(v, h);
         }
       }
+    }
   }
   // 3) the upsample of the owned high-res block: rows 2 r0 .. 2 (r0 + nrow) - 1; lane = footprint
   //    column q (low-res column j = c0 - 1 + q): the row interpolation r(j) once per lane, the
@@ -356,7 +360,13 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_subpix_border(TView x, const 
   }
 }
 
-int init_subpixel() { return EVC_OK; }
+constexpr size_t SI_SMEM = sizeof(float) * SI_CH * (SI_R * SI_C + 1);
+
+int init_subpixel() {
+  return cudaFuncSetAttribute(k_subpix_input, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SI_SMEM) == cudaSuccess
+             ? EVC_OK
+             : EVC_ECUDA;
+}
 
 }  // namespace evc
 
@@ -365,9 +375,13 @@ using namespace evc;
 extern "C" {
 
 static void si_geom(const TView& v, int cp, int& CW, int& nJB, int& nx) {
+  (void)cp;
   CW = v.tw * (32 / v.tw);
   nJB = (v.W + CW - 1) / CW;
-  nx = nJB * ((cp + 31) / 32);
+  // channel chunks of 32; a remainder <= SI_CH - 32 joins the last full chunk
+  const int full = v.C / 32, rem = v.C - 32 * full;
+  const int nchunk = full == 0 ? 1 : (rem == 0 ? full : (rem <= SI_CH - 32 ? full : full + 1));
+  nx = nJB * nchunk;
 }
 
 int64_t evc_subpixel_input_partials(const evc_tensor* x, int32_t cp) {
@@ -390,7 +404,7 @@ int evc_subpixel_input(const evc_tensor* x, const evc_tensor* y, double* partial
   const TView vy = view_of(*y);
   int CW, nJB, nx;
   si_geom(v, cp, CW, nJB, nx);
-  launch_pdl(k_subpix_input, dim3((unsigned)nx, (unsigned)v.GH, (unsigned)S), dim3(SP_THREADS), 0,
+  launch_pdl(k_subpix_input, dim3((unsigned)nx, (unsigned)v.GH, (unsigned)S), dim3(SP_THREADS), SI_SMEM,
              as_stream(stream), v, vy.f, vy.fs, vy.GH, vy.GW, partials, hwc, hwc_stride, (int)cp, (int)pitch, fany_lo,
              fany_hi, CW, nJB);
   EVC_LAUNCH_CHECK("subpixel_input");

@@ -50,7 +50,8 @@ def _subpixel_on(monkeypatch):
     monkeypatch.setenv("EVC_SUBPIXEL", "1")  # opt-in path (tensors.SUBPIXEL_MAX_COUT)
 
 
-@pytest.mark.parametrize("c,h,w,co,S", [(66, 32, 40, 16, 2), (20, 23, 31, 32, 3), (8, 12, 12, 16, 1)])
+@pytest.mark.parametrize("c,h,w,co,S", [(66, 32, 40, 16, 2), (20, 23, 31, 32, 3), (8, 12, 12, 16, 1),
+                                        (41, 14, 18, 16, 2), (72, 12, 14, 16, 1)])  # channel chunks 32+9, 40
 def test_subpixel_chain_vs_oracle(c, h, w, co, S):
     spec = _spec(c, h, w, co)
     weights = evc.WeightManifest.random_tensors(spec, 5)

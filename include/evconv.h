@@ -437,6 +437,16 @@ int evc_sparsify_finalize(const double* partials, int64_t n_partials,
 int evc_sumsq_dense(const float* x, int64_t x_stride, int64_t n_per_session,
                     double* partials, int32_t n_blocks, int32_t S, void* stream);
 
+/* Byte fill of n segments in one launch: the resets of a dense refresh (graph.py:503-565 rebuilds
+ * every AccState; the increment stores, flag grids and conv shadows return to exact zeros).
+ * `segs` is a DEVICE array of n entries; value is the fill byte (low 8 bits). */
+typedef struct evc_fill_segment {
+  uint64_t addr;
+  int64_t bytes;
+  int64_t value;
+} evc_fill_segment;
+int evc_fill_segments(const evc_fill_segment* segs, int32_t n, int32_t n_blocks, void* stream);
+
 /* inc_add (increment_ops.py:226-229). */
 int evc_add(const evc_tensor* a, const evc_tensor* b, const evc_tensor* y,
             int32_t S, void* stream);

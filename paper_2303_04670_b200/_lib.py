@@ -131,6 +131,7 @@ _PROTOS = {
                                      _I32, _I32, _P]),
     "evc_sparsify_finalize": (_I32, [_P, _I64, _P, _P, _D, _D, _I32, _I32, _P]),
     "evc_sumsq_dense": (_I32, [_P, _I64, _I64, _P, _I32, _I32, _P]),
+    "evc_fill_segments": (_I32, [_P, _I32, _I32, _P]),
     "evc_add": (_I32, [_T, _T, _T, _I32, _P]),
     "evc_add_act": (_I32, [_T, _T, _P, _I64, _T, _I32, _F, _I32, _P]),
     "evc_mul": (_I32, [_T, _T, _P, _P, _I64, _T, _I32, _P]),

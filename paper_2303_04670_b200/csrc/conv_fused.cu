@@ -1145,8 +1145,12 @@ __host__ __device__ constexpr int persist_threads() { return (4 + persist_epi_wa
 template <int BN, bool PK>
 __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_conv_persist(const __grid_constant__ CUtensorMap tmap,
                                                                               const __grid_constant__ Args a) {
-  constexpr int BUF = BN <= 32 ? 6 * BN : 3 * BN;  // packed: 3 taps x [A.B_hi | A.B_lo]; CAT: [hi.hi | hi.lo | lo.hi]
-  constexpr int TMEM_COLS = 2 * BUF <= 128 ? 128 : (2 * BUF <= 256 ? 256 : 512);
+  // SS (BN = 128): TMEM = [main_0 | main_1 | small_0 | small_1] -- the hi.hi segments alternate between
+  // the main blocks (promotion), the small terms hi.lo + lo.hi of a whole item go to small_(item & 1), so
+  // the next item's MMAs start while the epilogue still drains the previous one (512 columns).
+  constexpr bool SS = BN >= 128;
+  constexpr int BUF = SS ? BN : (BN <= 32 ? 6 * BN : 3 * BN);  // packed: 3 taps x [A.B_hi | A.B_lo]; CAT: [hi.hi | hi.lo | lo.hi]
+  constexpr int TMEM_COLS = SS ? 4 * BN : (2 * BUF <= 128 ? 128 : (2 * BUF <= 256 ? 256 : 512));
   constexpr uint32_t IDESC_BASE = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BM >> 4) << 24);
   constexpr uint32_t IDESC = IDESC_BASE | ((uint32_t)(BN >> 3) << 17);
   constexpr uint32_t IDESC2 = IDESC_BASE | ((uint32_t)((2 * BN) >> 3) << 17);
@@ -1166,13 +1170,15 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // full[4], empty[4], tfull[2], tempty[2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNS + 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NS * STAGE);  // full[4], empty[4], tfull[2], tempty[2], sfull[2], sempty[2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNS + 8);
   const uint32_t sb = su32(smem), b0 = su32(bars);
   auto full_bar = [&](int i) { return b0 + 8u * i; };
   auto empty_bar = [&](int i) { return b0 + 8u * (MAXNS + i); };
   auto tfull_bar = [&](int i) { return b0 + 8u * (2 * MAXNS + i); };
   auto tempty_bar = [&](int i) { return b0 + 8u * (2 * MAXNS + 2 + i); };
+  auto sfull_bar = [&](int i) { return b0 + 8u * (2 * MAXNS + 4 + i); };
+  auto sempty_bar = [&](int i) { return b0 + 8u * (2 * MAXNS + 6 + i); };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -1182,6 +1188,8 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
     for (int i = 0; i < 2; ++i) {
       bar_init(tfull_bar(i), 1);
       bar_init(tempty_bar(i), 32 * EPI);
+      bar_init(sfull_bar(i), 1);
+      bar_init(sempty_bar(i), 32 * EPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -1237,13 +1245,16 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
   } else if (warp == 1) {  // --------------------------------------------------- MMA issuer
     // TMEM buffer use = one accumulation segment of DS K-blocks (the whole item when a.drain == 0);
     // segment gs fills buffer gs & 1 while the epilogue promotes segment gs - 1 into registers
-    int g = 0, gs = 0;
+    int g = 0, gs = 0, it = 0;  // it: live items so far (small block it & 1 when SS)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int reg = item / nb, s = reg / R, rr = reg % R;
       if (!region_live_warp(a, s, rr)) continue;
       if (lane == 0) {
         uint32_t tb = tmem;
         int ab = 0;
+        const uint32_t tsm = tmem + (uint32_t)(2 * BN + (it & 1) * BN);
+        if (SS && it >= 2) bar_spin(sempty_bar(it & 1), ((it >> 1) & 1) ^ 1);
+        fence_after();
         for (int kb = 0; kb < nk; ++kb, ++g) {
           const bool seg0 = kb % DS == 0;
           if (seg0) {
@@ -1271,11 +1282,23 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
             for (int t = 0; t < taps; ++t) {
               const uint64_t da = desc_k(ah + t * 128), dl = desc_k(al + t * 128), db = desc_k(bb + t * 2 * BN * 128);
               const bool first = seg0 && t == 0;
+              if constexpr (SS) {
+                const uint64_t dbl = desc_k(bb + BN * 128);  // B_lo rows of the [B_hi | B_lo] tile
+                const bool firsts = kb == 0 && t == 0;
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                if (kk >= nkk) break;
-                mma(tb, da + 2 * kk, db + 2 * kk, IDESC2, (!first || kk) ? 1u : 0u);           // hi.[hi|lo]
-                mma(tb + 2 * BN, dl + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);  // lo.hi
+                for (int kk = 0; kk < 4; ++kk) {
+                  if (kk >= nkk) break;
+                  mma(tb, da + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);      // hi.hi
+                  mma(tsm, da + 2 * kk, dbl + 2 * kk, IDESC, (!firsts || kk) ? 1u : 0u);  // hi.lo
+                  mma(tsm, dl + 2 * kk, db + 2 * kk, IDESC, 1u);                           // lo.hi
+                }
+              } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                  if (kk >= nkk) break;
+                  mma(tb, da + 2 * kk, db + 2 * kk, IDESC2, (!first || kk) ? 1u : 0u);           // hi.[hi|lo]
+                  mma(tb + 2 * BN, dl + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);  // lo.hi
+                }
               }
             }
           }
@@ -1285,9 +1308,11 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
             ++gs;
           }
         }
+        if (SS) commit(sfull_bar(it & 1));
       } else {
         g += nk;
       }
+      ++it;
       __syncwarp();
     }
   } else if (warp < 4) {  // ---------------------------------------------------- flags + meter
@@ -1305,7 +1330,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
     const int half = NH > 1 ? (warp - 4) >> 2 : 0;  // channel half of the block (NH = 2) or 0
     // named barrier of this half's four warps: id 2 (half 0) or 4 (half 1)
     const int Qs = R * nb;
-    int gs = 0;
+    int gs = 0, it = 0;
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int nblk = item % nb, reg = item / nb, s = reg / R, rr = reg % R;
       const int64_t rs_idx = (int64_t)reg * nb + nblk;
@@ -1412,27 +1437,68 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
             bar_wait(tfull_bar(ab), (gs >> 1) & 1);
             fence_after();
             const uint32_t trow = tmem + (uint32_t)(ab * BUF) + ((uint32_t)(32 * q4) << 16);
+            if constexpr (SS) {
 #pragma unroll
-            for (int cc = 0; cc < CB; cc += 16) {
-              const int c0 = half * CB + cc;
-              uint32_t r[3][16];
-              tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), r[0]);  // lo . hi
-              tmem_ld16_issue(trow + (uint32_t)(BN + c0), r[1]);      // hi . lo
-              tmem_ld16_issue(trow + (uint32_t)c0, r[2]);             // hi . hi
-              tmem_wait_ld();
+              for (int cc = 0; cc < CB; cc += 32) {  // hi . hi of this segment
+                const int c0 = half * CB + cc;
+                uint32_t r[2][16];
+                tmem_ld16_issue(trow + (uint32_t)c0, r[0]);
+                tmem_ld16_issue(trow + (uint32_t)(c0 + 16), r[1]);
+                tmem_wait_ld();
 #pragma unroll
-              for (int j = 0; j < 3; ++j)
+                for (int j = 0; j < 2; ++j)
 #pragma unroll
-                for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
+                  for (int e = 0; e < 16; ++e) {
+                    asm volatile("" : "+r"(r[j][e]));
+                    const float v = __uint_as_float(r[j][e]);
+                    acc[cc + 16 * j + e] = sg ? __fadd_rn(acc[cc + 16 * j + e], v) : v;
+                  }
+              }
+            } else {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) {
-                const float v = __fadd_rn(__fadd_rn(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])),
-                                          __uint_as_float(r[2][e]));
-                acc[cc + e] = sg ? __fadd_rn(acc[cc + e], v) : v;
+              for (int cc = 0; cc < CB; cc += 16) {
+                const int c0 = half * CB + cc;
+                uint32_t r[3][16];
+                tmem_ld16_issue(trow + (uint32_t)(2 * BN + c0), r[0]);  // lo . hi
+                tmem_ld16_issue(trow + (uint32_t)(BN + c0), r[1]);      // hi . lo
+                tmem_ld16_issue(trow + (uint32_t)c0, r[2]);             // hi . hi
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) asm volatile("" : "+r"(r[j][e]));
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  const float v = __fadd_rn(__fadd_rn(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])),
+                                            __uint_as_float(r[2][e]));
+                  acc[cc + e] = sg ? __fadd_rn(acc[cc + e], v) : v;
+                }
               }
             }
             fence_before();
             bar_arrive(tempty_bar(ab));
+          }
+          if constexpr (SS) {  // + the item's small terms (hi.lo + lo.hi, one chain over the whole K range)
+            bar_wait(sfull_bar(it & 1), (it >> 1) & 1);
+            fence_after();
+            const uint32_t srow = tmem + (uint32_t)(2 * BN + (it & 1) * BN) + ((uint32_t)(32 * q4) << 16);
+#pragma unroll
+            for (int cc = 0; cc < CB; cc += 32) {
+              const int c0 = half * CB + cc;
+              uint32_t r[2][16];
+              tmem_ld16_issue(srow + (uint32_t)c0, r[0]);
+              tmem_ld16_issue(srow + (uint32_t)(c0 + 16), r[1]);
+              tmem_wait_ld();
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  asm volatile("" : "+r"(r[j][e]));
+                  acc[cc + 16 * j + e] = __fadd_rn(__uint_as_float(r[j][e]), acc[cc + 16 * j + e]);
+                }
+            }
+            fence_before();
+            bar_arrive(sempty_bar(it & 1));
           }
 #pragma unroll
           for (int cc = 0; cc < CB; cc += 16) {
@@ -1440,6 +1506,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
             ssq += emit<16, (BN >= 64 && !PK)>(a, s, u, x, n0, 1, min(16, a.c_out - n0), acc + cc, sl);
           }
         }
+        ++it;
       }
       // per-item bookkeeping: region state, sum of squares of the fused sparsify
       if (a.sp_part) {
@@ -1493,7 +1560,13 @@ __device__ __forceinline__ void thin_fma(float* acc, float x, const float* w) {
 
 // output channels padded to CO (2, 4, 8, 16, 32); weights [tap][c_in][CO]; F32: fp32 shadow (cp < 0)
 template <int CO, bool F32 = false>
-__global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? 6 : 8)) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
+#ifndef EVC_THIN_MINB32
+#define EVC_THIN_MINB32 6
+#endif
+#ifndef EVC_THIN_MINB
+#define EVC_THIN_MINB 8
+#endif
+__global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? EVC_THIN_MINB32 : EVC_THIN_MINB)) k_conv_thin(const float* __restrict__ in_hwc, int64_t hwc_stride,
                                                             const __grid_constant__ Args a) {
   extern __shared__ float s_w[];
   __shared__ int s_flag[2];
@@ -1802,7 +1875,7 @@ static int split_count(int nkb, int splits) {
 
 int init_conv_fused() {
   int rc = fz::attr<16>() | fz::attr<32>() | fz::attr<64>() | fz::attr<128>() | fz::attr<256>();
-  rc |= fz::attr_persist<16>() | fz::attr_persist<32>() | fz::attr_persist<64>();
+  rc |= fz::attr_persist<16>() | fz::attr_persist<32>() | fz::attr_persist<64>() | fz::attr_persist<128>();
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, fz::k_tile_any) != cudaSuccess) rc = 1;
   if (cudaFuncGetAttributes(&fa, fz::k_meter_step) != cudaSuccess) rc = 1;
@@ -2133,7 +2206,13 @@ static int conv_fused_impl(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, c
     EVC_LAUNCH_CHECK("conv_fused_thin");
     return EVC_OK;
   }
-  if (a.splits == 1 && cfg->bn <= 64 && std::getenv("EVC_NO_PERSIST") == nullptr) {
+  // BN = 128 (tap mode), opt-in (EVC_PERSIST128=1): persistent with the split-small TMEM layout, the next
+  // item's mainloop overlapping the previous item's epilogue.  Measured slower at 32 streams (enc2 93 vs
+  // 75 us, dec0 384 vs 313 us: these layers are bound by L2 operand traffic, ~8.7 TB/s for dec0, not
+  // by the epilogue), so the one-shot kernel stays the default
+  const bool p128 = cfg->bn == 128 && !cfg->row && (int64_t)S * L.R * ((g->c_out + 127) / 128) > 148 &&
+                    std::getenv("EVC_PERSIST128") != nullptr;
+  if (a.splits == 1 && (cfg->bn <= 64 || p128) && std::getenv("EVC_NO_PERSIST") == nullptr) {
     // persistent CTAs: one or two per SM (BN = 16 fits two), each walking work items
     const int occ = (cfg->bn <= 16 && 2 * ((int)L.ns * L.stage + 1024 + 256 + 2048) <= fz::SMEM_MAX) ? 2 : 1;
     const int items = S * L.R * ((g->c_out + cfg->bn - 1) / cfg->bn);
@@ -2141,6 +2220,7 @@ static int conv_fused_impl(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, c
     switch (cfg->bn) {
       case 16: e = fz::launch_persist<16>(map, a, grid, st); break;
       case 32: e = fz::launch_persist<32>(map, a, grid, st); break;
+      case 128: e = fz::launch_persist<128>(map, a, grid, st); break;
       default: e = fz::launch_persist<64>(map, a, grid, st); break;
     }
     if (e != cudaSuccess) {

@@ -289,6 +289,42 @@ int evc_maxpool(const evc_tensor* in, float* acc, int64_t acc_stride, const evc_
 }  // extern "C"
 
 namespace evc {
+
+// Byte fill of n segments in one launch (the dense refresh's resets: increment stores, flag grids,
+// conv input shadows, region states -- 100+ memsets otherwise, most of them a few KB).  seg[i] =
+// {address, bytes, value}; every CTA walks every segment with a grid-stride loop over its 16-byte
+// aligned body (the unaligned head / tail bytes by the first CTA).
+__global__ void __launch_bounds__(256) k_fill_segments(const evc_fill_segment* __restrict__ seg, int n) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int i = 0; i < n; ++i) {
+    uint8_t* p = reinterpret_cast<uint8_t*>(seg[i].addr);
+    const int64_t nb = seg[i].bytes;
+    const uint32_t b = seg[i].value & 0xffu, w = b * 0x01010101u;
+    const int64_t head = std::min<int64_t>(nb, (int64_t)((16u - (reinterpret_cast<uintptr_t>(p) & 15u)) & 15u));
+    const int64_t nv = (nb - head) >> 4, tail0 = head + (nv << 4);
+    uint4* body = reinterpret_cast<uint4*>(p + head);
+    const uint4 wv = make_uint4(w, w, w, w);
+    for (int64_t e = tid; e < nv; e += nthr) body[e] = wv;
+    if (blockIdx.x == 0) {
+      for (int64_t e = threadIdx.x; e < head; e += blockDim.x) p[e] = (uint8_t)b;
+      for (int64_t e = tail0 + threadIdx.x; e < nb; e += blockDim.x) p[e] = (uint8_t)b;
+    }
+  }
+}
+
+}  // namespace evc
+
+extern "C" int evc_fill_segments(const evc_fill_segment* segs, int32_t n, int32_t n_blocks, void* stream) {
+  EVC_CHECK_ARG(segs && n >= 0 && n_blocks > 0, "fill_segments: bad argument");
+  if (n == 0) return EVC_OK;
+  launch_pdl(evc::k_fill_segments, dim3(n_blocks), dim3(256), 0, evc::as_stream(stream), segs, (int)n);
+  EVC_LAUNCH_CHECK("fill_segments");
+  return EVC_OK;
+}
+
+namespace evc {
 int init_elementwise() {
   cudaFuncAttributes fa;
   if (cudaFuncGetAttributes(&fa, k_sumsq) != cudaSuccess) return EVC_ECUDA;

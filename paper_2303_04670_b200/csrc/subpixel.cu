@@ -153,13 +153,22 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
   const int Ya = 2 * r0, Yb = min(Hy, 2 * (r0 + nrow));
   const bool own = lane >= 1 && lane <= ncol;  // j = c0 + lane - 1 is an owned column
   const int tje = own ? (2 * (lane - 1)) / x.tw : 0, tjo = own ? (2 * (lane - 1) + 1) / x.tw : 0;
+  // The footprint row fr holds x[clamp(r0 - 1 + fr)], so the clamped taps of tap2(Y) are footprint rows
+  // k / 2 + {0, 1} (Y = 2 r0 + k even: 1/4, 3/4) and k / 2 + {1, 2} (odd: 3/4, 1/4): the column is read
+  // into registers once per channel and the row loop is unrolled over compile-time indices.
+  const int nk = Yb - Ya;  // 2 nrow <= 2 (SI_R - 2)
   for (int ch = warp; ch < nch; ch += SP_THREADS / 32) {
     if (!s_live[ch]) continue;  // no flagged support: every value is an exact zero (flags stay 0)
     const float* tc = t[ch] + min(lane, SI_C - 1);
+    float col[SI_R];
+#pragma unroll
+    for (int fr = 0; fr < SI_R; ++fr) col[fr] = tc[fr * SI_C];
     uint32_t n00 = 0u, n01 = 0u, n10 = 0u, n11 = 0u;  // [tile row][even, odd column]: OR of magnitude bits
-    for (int Y = Ya; Y < Yb; ++Y) {
-      const Tap tr = tap2(Y, x.H);
-      const float r = __fadd_rn(__fmul_rn(tc[(tr.i0 - r0 + 1) * SI_C], tr.w0), __fmul_rn(tc[(tr.i1 - r0 + 1) * SI_C], tr.w1));
+#pragma unroll
+    for (int k = 0; k < 2 * (SI_R - 2); ++k) {
+      if (k >= nk) break;
+      const float r = (k & 1) ? __fadd_rn(__fmul_rn(col[k / 2 + 1], 0.75f), __fmul_rn(col[k / 2 + 2], 0.25f))
+                              : __fadd_rn(__fmul_rn(col[k / 2], 0.25f), __fmul_rn(col[k / 2 + 1], 0.75f));
       const float rl = __shfl_up_sync(0xffffffffu, r, 1), rr = __shfl_down_sync(0xffffffffu, r, 1);
       const float oe = __fadd_rn(0.0f, __fadd_rn(__fmul_rn(rl, 0.25f), __fmul_rn(r, 0.75f)));
       const float oo = __fadd_rn(0.0f, __fadd_rn(__fmul_rn(r, 0.75f), __fmul_rn(rr, 0.25f)));
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
         ss = __fmaf_rn(oe, oe, ss);
         ss = __fmaf_rn(oo, oo, ss);
         const uint32_t be = __float_as_uint(oe) & 0x7fffffffu, bo = __float_as_uint(oo) & 0x7fffffffu;
-        if (Y - Ya >= x.th) {  // (two tile rows)
+        if (k >= x.th) {  // (two tile rows)
           n10 |= be;
           n11 |= bo;
         } else {

@@ -500,6 +500,8 @@ class Graph:
         self._initialized = False
         self._plan()
         self._graph = None
+        self._dense_graph = None
+        self._dense_eager_runs = 0
 
     # -- construction ---------------------------------------------------------
 
@@ -1125,9 +1127,7 @@ class Graph:
                 run(L.evc_act_dense, xp, xs, yp, ys, node.acc.data_ptr() if mutate else None, node.acc[0].numel(),
                     node.acc[0].numel(), code, alpha, S)
             elif k == "sparsify" and node.sp_fused_by is not None:
-                if mutate:  # values, shadow and norm came from the producing conv's epilogue
-                    node.delta.zero_()
-                    node.dlive.zero_()
+                pass  # values, shadow and norm came from the producing conv's epilogue; delta / dlive: batched reset
             elif k == "sparsify" and ns.inputs[0] in self._dense_up:
                 # upsample -> sparsify(t_p = 0) -> conv: the fused kernel of the incremental program with every
                 # input tile marked live writes the conv's shadow and the norm partials (no dense upsample,
@@ -1143,8 +1143,6 @@ class Graph:
                     j = node.sp_idx
                     run(L.evc_sparsify_finalize, node.part_ptr, node.nparts, self._norm.data_ptr() + 8 * j * S,
                         self._k.data_ptr() + 8 * j * S, node.tp, node.ema_decay, 1, S)
-                    node.delta.zero_()
-                    node.dlive.zero_()
             elif k == "sparsify":
                 xp, xs = self._vptr(ns.inputs[0])
                 yp, ys = self._vptr(nid)
@@ -1156,8 +1154,6 @@ class Graph:
                     run(L.evc_sumsq_dense, xp, xs, n, self._partials.data_ptr(), nb, S)
                     run(L.evc_sparsify_finalize, self._partials.data_ptr(), nb, self._norm.data_ptr() + 8 * j * S,
                         self._k.data_ptr() + 8 * j * S, node.tp, node.ema_decay, 1, S)
-                    node.delta.zero_()
-                    node.dlive.zero_()
             elif k in ("add", "mul"):
                 ap, as_ = self._vptr(ns.inputs[0])
                 bp, bs = self._vptr(ns.inputs[1])
@@ -1221,17 +1217,42 @@ class Graph:
         self._load_input(x)
         self._dense_program(mutate)
 
-    def _clear_increments(self):
-        for st in self._stores:
-            st.vals.zero_()
-            st.flags.zero_()
-        for nd in self.nodes:  # conv input shadows held dense values during the dense pass
-            if nd.kind == "conv" and nd.plan.hwc is not None:
-                nd.plan.hwc.zero_()
-            if nd.kind == "conv" and nd.plan.path == "fused":
-                nd.plan.rstate.zero_()  # no region holds a nonzero increment now
-            if nd.kind == "conv" and getattr(nd, "scatter", False):
-                nd.plan.scatter_plan()[1].zero_()  # nor does any output tile of the scatter path
+    def _reset_segments(self, mutate: bool):
+        """Device table of every buffer a dense pass leaves non-zero that the increment program needs
+        back at exact zeros (evc_fill_segments: one launch instead of 100+ memsets).  ``mutate``: also
+        the sparsify residuals (a dense_pass restarts them; dense_oracle leaves session state alone)."""
+        tabs = getattr(self, "_reset_tables", None)
+        if tabs is None:
+            tabs = self._reset_tables = {}
+        if mutate not in tabs:
+            segs = []
+
+            def add(t):
+                if t is not None and t.numel():
+                    assert t.is_contiguous()
+                    segs.append((t.data_ptr(), t.numel() * t.element_size(), 0))
+
+            for st in self._stores:
+                add(st.vals)
+                add(st.flags)
+            for nd in self.nodes:
+                if nd.kind == "conv" and nd.plan.hwc is not None:
+                    add(nd.plan.hwc)  # conv input shadows held dense values during the dense pass
+                if nd.kind == "conv" and nd.plan.path == "fused":
+                    add(nd.plan.rstate)  # no region holds a nonzero increment now
+                if nd.kind == "conv" and getattr(nd, "scatter", False):
+                    add(nd.plan.scatter_plan()[1])  # nor does any output tile of the scatter path
+                if nd.kind == "sparsify" and mutate:
+                    add(getattr(nd, "delta", None))  # residuals restart at zero (sparsify.py:43-51)
+                    add(getattr(nd, "dlive", None))
+            tab = torch.tensor(segs, dtype=torch.int64).view(-1, 3) if segs else torch.zeros((0, 3), dtype=torch.int64)
+            tabs[mutate] = (tab.to(self.device), len(segs))
+        return tabs[mutate]
+
+    def _clear_increments(self, mutate: bool = False):
+        tab, n = self._reset_segments(mutate)
+        nb = 4 * torch.cuda.get_device_properties(self.device).multi_processor_count
+        _lib.check(self.lib.evc_fill_segments(tab.data_ptr(), n, nb, _lib.stream_ptr()), "fill_segments")
 
     def dense_oracle(self, x):
         """Pure dense forward of the primary output; session state is untouched."""
@@ -1245,21 +1266,41 @@ class Graph:
     def dense_pass(self, x):
         """Full dense forward that re-seeds every accumulator and baseline."""
         self._check_input_shape(x)
-        self._eval_dense(x, mutate=True)
+        self._load_input(x)
+        # the device work of a refresh is static: after one eager run (lazy plans, reset tables) it is
+        # captured once and every later dense_pass / refresh is one graph replay
+        if self.use_cuda_graph and (self._dense_graph is not None or self._dense_eager_runs > 0):
+            if self._dense_graph is None:
+                g = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(device=self.device)
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.graph(g, stream=side):
+                    self._dense_device_work()
+                torch.cuda.current_stream().wait_stream(side)
+                self._dense_graph = g
+            self._dense_graph.replay()
+        else:
+            self._dense_device_work()
+            self._dense_eager_runs += 1
         for i, node in enumerate(self._meter_nodes):
             de = self._dense_static[i]
             self._perf_host[i] += de * self.S
             self._dense_host[i] += de * self.S
-        for o in self.output_ids:
-            v, _ = self._slot_view(o)
-            self._baseline[o].copy_(v)
-            self._y_run[o].copy_(v)
         out = self._y_run[self.output_ids[0]].clone()
-        self._clear_increments()
         self.step_count = 0
         self.refresh_due = False
         self._initialized = True
         return out[0] if self.S == 1 else out
+
+    def _dense_device_work(self):
+        """Every launch of dense_pass after the input upload: the dense program (mutating), the output
+        baselines, the batched reset of the increment buffers."""
+        self._dense_program(True)
+        for o in self.output_ids:
+            v, _ = self._slot_view(o)
+            self._baseline[o].copy_(v)
+            self._y_run[o].copy_(v)
+        self._clear_increments(mutate=True)
 
     def refresh(self, x):
         """Dense reconstruction run; identical contract to dense_pass."""

@@ -43,6 +43,9 @@ CASES = {
     "res_forced_split3_s2": (256, 256, 3, 1, 1, 16, 16, 2, 0.97, {"EVC_FORCE_SPLITS": "3"}, {"splits": 3}),
     "dec0_tap_s32": (512, 128, 3, 1, 1, 32, 32, 32, 0.95, {}, {"row": 0, "bn": 128}),
     "dec0_tap_s8": (512, 128, 3, 1, 1, 32, 32, 8, 0.95, {}, {"row": 0, "bn": 128}),
+    # opt-in persistent BN = 128 (split-small TMEM layout): more items than SMs
+    "enc2_persist128_s32": (64, 128, 3, 2, 1, 64, 64, 32, 0.95, {"EVC_PERSIST128": "1"}, {"row": 0, "bn": 128}),
+    "dec0_persist128_s32": (512, 128, 3, 1, 1, 32, 32, 32, 0.95, {"EVC_PERSIST128": "1"}, {"row": 0, "bn": 128}),
     "dec0_row_s2": (512, 128, 3, 1, 1, 32, 32, 2, 0.95, {}, {"row": 1, "bn": 64}),
     "dec1_row_bn64_s8": (258, 64, 3, 1, 1, 64, 64, 8, 0.88, {}, {"row": 1, "bn": 64}),
     "dec1_row_oneshot_s8": (258, 64, 3, 1, 1, 64, 64, 8, 0.88, {"EVC_NO_PERSIST": "1"}, {"row": 1}),

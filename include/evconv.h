@@ -305,6 +305,13 @@ int evc_subpixel_input(const evc_tensor* x, const evc_tensor* y, double* partial
  * image of w . U(clamped site); w = the real conv's weights transposed to (C, 3, 3, c_out)
  * (device), c_out a multiple of 4. */
 int evc_subpixel_border(const evc_tensor* x, const float* w, int32_t c_out, float* out, int32_t S, void* stream);
+
+/* evc_subpixel_input and evc_subpixel_border in ONE launch (both only read x; the border GEMM's CTAs are
+ * scheduled between the input pass's).  Same arguments and results as the two calls; partials are
+ * indexed exactly as evc_subpixel_input's (evc_subpixel_input_partials). */
+int evc_subpixel_input_border(const evc_tensor* x, const evc_tensor* y, double* partials, float* hwc, int32_t cp,
+                              int64_t hwc_stride, int32_t pitch, uint8_t* fany_lo, uint8_t* fany_hi, const float* w,
+                              int32_t c_out, float* border, int32_t S, void* stream);
 /* Debug: subsequent evc_conv_fused launches record per-CTA phase clocks into
  * buf (16 uint64 per CTA, CTA index (z*gy + y)*gx + x); NULL turns it off. */
 int evc_conv_trace(void* buf);

@@ -112,6 +112,7 @@ _PROTOS = {
     "evc_subpixel_input_partials": (_I64, [_T, _I32]),
     "evc_subpixel_input": (_I32, [_T, _T, _P, _P, _I32, _I64, _I32, _P, _P, _I32, _P]),
     "evc_subpixel_border": (_I32, [_T, _P, _I32, _P, _I32, _P]),
+    "evc_subpixel_input_border": (_I32, [_T, _T, _P, _P, _I32, _I64, _I32, _P, _P, _P, _I32, _P, _I32, _P]),
     "evc_tile_any": (_I32, [_T, _P, _I32, _P]),
     "evc_conv_trace": (_I32, [_P]),
     "evc_meter_step": (_I32, [_P, _I32, _I32, _P, _P, _P, _P, _P, _P, _I32, _P]),

@@ -102,6 +102,7 @@ struct Args {
   int sub;
   const uint8_t* fany_side;
   const float* border;
+  int pf;  // epilogue warps prefetch the activation accumulators of their sites into L2 during the mainloop
 };
 
 static unsigned long long* g_trace = nullptr;
@@ -247,6 +248,17 @@ __device__ __forceinline__ int sub_live_of(const Args& a, int s, int u, int x) {
 template <int N>
 __device__ __forceinline__ double emit_sub(const Args& a, int s, int u, int x, int n0, int cnt, const float* vals,
                                            int sub_live);
+
+// L2 prefetch of the activation accumulator values emit() will read for output site (u, x), channels
+// n0 .. n0 + nn - 1 (incremental mode): issued by the epilogue warps before they wait for the MMAs, so the
+// epilogue's read-modify-write of acc finds its lines in L2 instead of HBM
+__device__ __forceinline__ void prefetch_acc(const Args& a, int s, int u, int x, int n0, int nn) {
+  if (!a.pf || a.dense || a.act < 0 || !a.acc || a.sub || u >= a.eHo || x >= a.eWo) return;
+  nn = min(nn, a.c_out - n0);
+  const int64_t plane = (int64_t)a.eHo * a.eWo;
+  const float* p = a.acc + (int64_t)s * a.accs + (int64_t)n0 * plane + (int64_t)u * a.eWo + x;
+  for (int j = 0; j < nn; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + j * plane));
+}
 
 // SUBOK: the instantiation can run in sub-pixel mode (BN >= 64, not packed -- the host enforces it),
 // so kernels that never do carry no sub-pixel code (registers, instruction cache).
@@ -865,6 +877,7 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     int u, x;
     site_of(a, rr, m, u, x);
     const int sl = sub_live_of(a, s, u, x);
+    if (a.splits == 1) prefetch_acc(a, s, u, x, nblk * a.bn, BN);
     if (D == 0) {  // (promotion mode waits segment by segment: the MMAs need the promoted blocks back)
       bar_wait(acc_bar, 0);
       fence_after();
@@ -1347,6 +1360,7 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
         }
       } else {
         const int sl = sub_live_of(a, s, u, x);
+        prefetch_acc(a, s, u, x, nblk * BN + half * (BN / NH), BN / NH);
         if (packed) {
           // per segment and 8-channel chunk: v_s = A.B_lo + A.B_hi of tap s, out[m] = sum_s v_s[m + s]
           // (shifts by s rows = shuffles inside the warp, the next warp's first rows through shared
@@ -1618,6 +1632,7 @@ __global__ void __launch_bounds__(THIN_THREADS, (CO >= 32 ? EVC_THIN_MINB32 : EV
     }
   } else {
     if (!a.dense && threadIdx.x == 0 && !s_flag[1]) a.rstate[reg] = 1;
+    if (valid) prefetch_acc(a, s, u, x, 0, a.c_out);
     float acc[CO];
 #pragma unroll
     for (int n = 0; n < CO; ++n) acc[n] = 0.0f;
@@ -2144,6 +2159,7 @@ static int conv_fused_impl(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, c
   a.bias = bias;
   a.dense = dense != 0;
   a.trace = fz::g_trace;
+  a.pf = std::getenv("EVC_NO_ACC_PREFETCH") == nullptr ? 1 : 0;
   a.eHo = eHo;
   a.eWo = eWo;
   a.oc = oc;

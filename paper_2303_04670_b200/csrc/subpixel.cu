@@ -71,19 +71,16 @@ __device__ __forceinline__ float up2(const float* xv, int H, int W, int y, int x
 // low-res tile in the support (their values are exact zeros).
 constexpr int SI_R = 10, SI_C = 34;  // footprint rows (th + 2 <= 10) and columns (CW + 2 <= 34)
 
-__global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* __restrict__ yf, int64_t yfs,
-                                                              int GHy, int GWy, double* __restrict__ part,
-                                                              float* __restrict__ hwc, int64_t hs, int cp, int pitch,
-                                                              uint8_t* __restrict__ fany_lo,
-                                                              uint8_t* __restrict__ fany_hi, int CW, int nJB) {
-  pdl_wait();
-  pdl_trigger();
-  extern __shared__ float si_dyn[];                   // [channel][row * SI_C + col] (odd channel stride)
+__device__ __forceinline__ void subpix_input_body(const TView& x, uint8_t* __restrict__ yf, int64_t yfs, int GHy,
+                                                  int GWy, double* __restrict__ part, float* __restrict__ hwc,
+                                                  int64_t hs, int cp, int pitch, uint8_t* __restrict__ fany_lo,
+                                                  uint8_t* __restrict__ fany_hi, int CW, int nJB, int bx, int nx,
+                                                  float* si_dyn) {
   float(*t)[SI_R * SI_C + 1] = reinterpret_cast<float(*)[SI_R * SI_C + 1]>(si_dyn);
   __shared__ double s_w[SP_THREADS / 32];
   __shared__ uint8_t s_fy[SI_CH][2][16];  // high-res flags of the owned tiles
   __shared__ int s_live[SI_CH];           // channel has a flagged low-res tile in the support box
-  const int s = blockIdx.z, ti = blockIdx.y, jb = blockIdx.x % nJB, k0 = (blockIdx.x / nJB) * 32;
+  const int s = blockIdx.z, ti = blockIdx.y, jb = bx % nJB, k0 = (bx / nJB) * 32;
   const int r0 = ti * x.th, nrow = min(x.th, x.H - r0);
   const int c0 = jb * CW, ncol = min(CW, x.W - c0);
   // real channels of the chunk: 32, the last chunk also the remainder (<= 8) of C past a multiple of 32
@@ -208,8 +205,20 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
     double tot = 0.0;
 #pragma unroll
     for (int k = 0; k < SP_THREADS / 32; ++k) tot += s_w[k];
-    part[(int64_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    part[(int64_t)s * nx * gridDim.y + blockIdx.y * nx + bx] = tot;
   }
+}
+
+__global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* __restrict__ yf, int64_t yfs,
+                                                              int GHy, int GWy, double* __restrict__ part,
+                                                              float* __restrict__ hwc, int64_t hs, int cp, int pitch,
+                                                              uint8_t* __restrict__ fany_lo,
+                                                              uint8_t* __restrict__ fany_hi, int CW, int nJB) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ float si_dyn[];  // [channel][row * SI_C + col] (odd channel stride)
+  subpix_input_body(x, yf, yfs, GHy, GWy, part, hwc, hs, cp, pitch, fany_lo, fany_hi, CW, nJB, (int)blockIdx.x,
+                    (int)gridDim.x, si_dyn);
 }
 
 // Border correction, a small GEMM per (session, line): out[pos][o] = - sum_{c, k} Wl[o][c][k] U[c][pos - 1 + k]
@@ -224,15 +233,17 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
 constexpr int SB_C = 32, SB_SPB = 1;  // channels per K step, sessions per CTA (1: measured fastest)
 constexpr int SB_WL = 20;             // low-res window along a line: 34 positions -> <= 19 columns
 
-__global__ void __launch_bounds__(SP_THREADS, 4) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
-                                                               float* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ float sU[SB_C][36];                   // [c][34 line positions | 2 corner sites]
-  __shared__ __align__(16) float sW[SB_C][3][32];  // [c][k][o]: the line's three off-image taps
-  __shared__ __align__(16) float sWc[SB_C][2][3][32];  // row lines with a corner: [c][kc = 0 | 2][kh][o]
-  __shared__ float sL[SB_C][2][SB_WL];                 // low-res window: [c][across tap][along]
-  const int s0 = blockIdx.z * SB_SPB, L = blockIdx.y % 4, oc0 = (blockIdx.y / 4) * 32, p0 = blockIdx.x * 32;
+constexpr int SB_SMEM_FLOATS = SB_C * 3 * 32 + SB_C * 2 * 3 * 32 + SB_C * 36 + SB_C * 2 * SB_WL;
+
+// one CTA of the border GEMM: (bx = 32 positions, by = line + 32 output channels, bz = session group);
+// shared memory carved from `sm` (16-byte aligned, SB_SMEM_FLOATS floats)
+__device__ __forceinline__ void subpix_border_body(const TView& x, const float* __restrict__ w, int co, int S,
+                                                   float* __restrict__ out, int bx, int by, int bz, float* sm) {
+  float(*sW)[3][32] = reinterpret_cast<float(*)[3][32]>(sm);                       // [c][k][o]: the line's three off-image taps
+  float(*sWc)[2][3][32] = reinterpret_cast<float(*)[2][3][32]>(sm + SB_C * 3 * 32);  // corners: [c][kc = 0 | 2][kh][o]
+  float(*sU)[36] = reinterpret_cast<float(*)[36]>(sm + SB_C * 9 * 32);             // [c][34 line positions | 2 corners]
+  float(*sL)[2][SB_WL] = reinterpret_cast<float(*)[2][SB_WL]>(sm + SB_C * 9 * 32 + SB_C * 36);  // [c][across][along]
+  const int s0 = bz * SB_SPB, L = by % 4, oc0 = (by / 4) * 32, p0 = bx * 32;
   const int Ho = 2 * x.H, Wo = 2 * x.W, C = x.C;
   const bool rowline = L < 2;
   const int len = rowline ? Wo : Ho;
@@ -369,10 +380,45 @@ __global__ void __launch_bounds__(SP_THREADS, 4) k_subpix_border(TView x, const 
   }
 }
 
+__global__ void __launch_bounds__(SP_THREADS, 4) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
+                                                               float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ __align__(16) float sm[SB_SMEM_FLOATS];
+  subpix_border_body(x, w, co, S, out, (int)blockIdx.x, (int)blockIdx.y, (int)blockIdx.z, sm);
+}
+
+// Both passes in one launch (they only read x): grid (nx + nbb, GH, S); x blocks >= nx run the border
+// GEMM, CTA b = (blockIdx.x - nx) * GH + blockIdx.y of its (nbx x nby) grid per session, so its
+// latency-bound CTAs spread between the input pass's instead of forming a serial phase.
+#ifndef EVC_SIB_MINB
+#define EVC_SIB_MINB 4
+#endif
+__global__ void __launch_bounds__(SP_THREADS, EVC_SIB_MINB) k_subpix_input_border(
+    TView x, uint8_t* __restrict__ yf, int64_t yfs, int GHy, int GWy, double* __restrict__ part,
+    float* __restrict__ hwc, int64_t hs, int cp, int pitch, uint8_t* __restrict__ fany_lo,
+    uint8_t* __restrict__ fany_hi, int CW, int nJB, int nx, const float* __restrict__ w, int co, float* __restrict__ bout,
+    int nbx, int nby) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) float si_dyn[];
+  if ((int)blockIdx.x >= nx) {
+    const int b = ((int)blockIdx.x - nx) * (int)gridDim.y + (int)blockIdx.y;
+    if (b >= nbx * nby) return;
+    subpix_border_body(x, w, co, (int)gridDim.z, bout, b % nbx, b / nbx, (int)blockIdx.z, si_dyn);
+    return;
+  }
+  subpix_input_body(x, yf, yfs, GHy, GWy, part, hwc, hs, cp, pitch, fany_lo, fany_hi, CW, nJB, (int)blockIdx.x, nx,
+                    si_dyn);
+}
+
 constexpr size_t SI_SMEM = sizeof(float) * SI_CH * (SI_R * SI_C + 1);
 
 int init_subpixel() {
-  return cudaFuncSetAttribute(k_subpix_input, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SI_SMEM) == cudaSuccess
+  static_assert(SB_SMEM_FLOATS * sizeof(float) <= SI_SMEM, "border GEMM carve exceeds the input pass's shared memory");
+  return (cudaFuncSetAttribute(k_subpix_input, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SI_SMEM) == cudaSuccess &&
+          cudaFuncSetAttribute(k_subpix_input_border, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SI_SMEM) ==
+              cudaSuccess)
              ? EVC_OK
              : EVC_ECUDA;
 }
@@ -428,6 +474,31 @@ int evc_subpixel_border(const evc_tensor* x, const float* w, int32_t c_out, floa
                   (unsigned)((S + SB_SPB - 1) / SB_SPB));
   launch_pdl(k_subpix_border, grid, dim3(SP_THREADS), 0, as_stream(stream), v, w, (int)c_out, (int)S, out);
   EVC_LAUNCH_CHECK("subpixel_border");
+  return EVC_OK;
+}
+
+int evc_subpixel_input_border(const evc_tensor* x, const evc_tensor* y, double* partials, float* hwc, int32_t cp,
+                              int64_t hwc_stride, int32_t pitch, uint8_t* fany_lo, uint8_t* fany_hi, const float* w,
+                              int32_t c_out, float* border, int32_t S, void* stream) {
+  EVC_CHECK_ARG(x && x->flags && y && y->flags && partials && hwc && w && border && S > 0 && c_out > 0 &&
+                    c_out % 4 == 0,
+                "subpixel_input_border: null argument");
+  EVC_CHECK_ARG(y->C == x->C && y->H == 2 * x->H && y->W == 2 * x->W && y->th == x->th && y->tw == x->tw &&
+                    x->th % 2 == 0 && x->tw % 2 == 0 && x->th <= 8 && x->tw >= 6 && x->tw <= 32,
+                "subpixel_input_border: y must be the 2x upsample of x with the same even tiles (th <= 8, 6 <= tw <= 32)");
+  EVC_CHECK_ARG(cp >= x->C && cp % 32 == 0 && pitch >= x->W + 2,
+                "subpixel_input_border: shadow channels (multiple of 32 >= C), pitch >= W + 2");
+  const TView v = view_of(*x);
+  const TView vy = view_of(*y);
+  int CW, nJB, nx;
+  si_geom(v, cp, CW, nJB, nx);
+  const int len = 2 * std::max(v.H, v.W);
+  const int nbx = (len + 31) / 32, nby = 4 * ((c_out + 31) / 32);
+  const int nbb = (nbx * nby + v.GH - 1) / v.GH;  // extra x blocks holding the border CTAs
+  launch_pdl(k_subpix_input_border, dim3((unsigned)(nx + nbb), (unsigned)v.GH, (unsigned)S), dim3(SP_THREADS),
+             SI_SMEM, as_stream(stream), v, vy.f, vy.fs, vy.GH, vy.GW, partials, hwc, hwc_stride, (int)cp, (int)pitch,
+             fany_lo, fany_hi, CW, nJB, nx, w, (int)c_out, border, nbx, nby);
+  EVC_LAUNCH_CHECK("subpixel_input_border");
   return EVC_OK;
 }
 

@@ -113,10 +113,11 @@ class EventPipeline:
     keeps its recent events in a device ring (``ring`` slots per column, a power of two); every
     step the host appends the records that arrived since the last window end -- 13 bytes per
     event, ``{u64 t, u16 x, u16 y, i8 p}`` (events.py:35-37) -- to a pinned staging block with
-    a small per-session descriptor, one H2D copy moves the block, and on the compute stream
-    ``evc_ingest_ring`` unpacks it into the rings, ``evc_encode_windows`` bins every session's
-    window (count + timestamp, bit-identical to ``encode``) into the current encoding buffer,
-    and ``step_from_encodings`` forms the increment and runs the step (a dense pass for the
+    a small per-session descriptor, one H2D copy moves the block, and on an ingest stream
+    ``evc_ingest_ring`` unpacks it into the rings and ``evc_encode_windows`` bins every session's
+    window (count + timestamp, bit-identical to ``encode``) into one of three encoding buffers --
+    one step ahead, overlapping the previous step's compute --; on the compute stream
+    ``step_from_encodings`` forms the increment and runs the step (a dense pass for the
     first window and whenever a refresh is due).  The integrated output of every step is read
     back as in :class:`StreamPipeline`.  Uploads of step i + 1 overlap step i's compute.
     """
@@ -142,12 +143,13 @@ class EventPipeline:
         S, dev = g.S, g.device
         self.cols = (torch.zeros(S * ring, dtype=torch.int64, device=dev), torch.zeros(S * ring, dtype=torch.int16, device=dev),
                      torch.zeros(S * ring, dtype=torch.int16, device=dev), torch.zeros(S * ring, dtype=torch.int8, device=dev))
-        self.enc = [torch.zeros((S, c, self.H, self.W), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.enc = [torch.zeros((S, c, self.H, self.W), dtype=torch.float32, device=dev) for _ in range(3)]
         self.meta = 7 * S  # int64 words: desc (3 per session) + windows (4 per session)
         nbytes = 8 * self.meta + S * self.max_new * 13
         self.host = [torch.empty(nbytes, dtype=torch.uint8).pin_memory() for _ in range(2)]
         self.dev_stage = [torch.empty(nbytes, dtype=torch.uint8, device=dev) for _ in range(2)]
         self.copy = torch.cuda.Stream(device=dev)
+        self.ingest = torch.cuda.Stream(device=dev)
         self.compute = torch.cuda.current_stream(dev)
         self.lib = _lib.lib()
         self.h2d_bytes = []
@@ -218,35 +220,52 @@ class EventPipeline:
             self.h2d_bytes.append(nb)
             return nev
 
-        bnds = bounds_of(0)
-        pend = stage(0, bnds, None)
-        for i in range(n + 1):
+        # ingest + binning run on their own stream, one step ahead: the window of step i + 1 is binned
+        # while step i computes.  Encodings rotate through three buffers: step j reads windows j - 1 and j,
+        # so window i's buffer (= window i - 3's) was last read by step i - 2.
+        ing = self.ingest
+        ev_enc = [torch.cuda.Event() for _ in range(2)]
+        ev_step = [torch.cuda.Event() for _ in range(2)]
+
+        def ingest(i, bnds, pend):
             k = i % 2
-            nb_next = None
-            if i + 1 <= n:  # stage the next step while this one computes
+            with torch.cuda.stream(ing):
+                ing.wait_event(ev_h2d[k])
+                if i >= 2:
+                    ing.wait_event(ev_step[(i - 2) % 2])  # buffer i % 3 was last read by step i - 2
+                st = self.dev_stage[k]
+                meta = st.data_ptr()
+                _lib.check(self.lib.evc_ingest_ring(meta + 8 * self.meta, meta, max(pend, 1), self.ring, t.data_ptr(),
+                                                    x.data_ptr(), yy.data_ptr(), p.data_ptr(), S, _lib.stream_ptr()),
+                           "ingest_ring")
+                wmax = max(b[1] - b[0] for b in bnds)
+                _lib.check(self.lib.evc_encode_windows(t.data_ptr(), x.data_ptr(), yy.data_ptr(), p.data_ptr(), self.ring,
+                                                       meta + 8 * 3 * S, max(wmax, 1), H, W, self.mode,
+                                                       self.enc[i % 3].data_ptr(), stride, S, _lib.stream_ptr()),
+                           "encode_windows")
+                ev_used[k].record(ing)
+                ev_enc[k].record(ing)
+
+        bnds = bounds_of(0)
+        ingest(0, bnds, stage(0, bnds, None))
+        for i in range(n + 1):
+            if i + 1 <= n:  # stage the next step's records (host fill + H2D on the copy stream)
                 b1 = bounds_of(i + 1)
-                nb_next = (b1, [b[1] for b in bnds])
-            cs.wait_event(ev_h2d[k])
-            st = self.dev_stage[k]
-            meta = st.data_ptr()
-            rec_ptr = meta + 8 * self.meta
-            _lib.check(self.lib.evc_ingest_ring(rec_ptr, meta, max(pend, 1), self.ring, t.data_ptr(), x.data_ptr(),
-                                                yy.data_ptr(), p.data_ptr(), S, _lib.stream_ptr()), "ingest_ring")
-            wmax = max(b[1] - b[0] for b in bnds)
-            cur, prv = self.enc[i % 2], self.enc[(i + 1) % 2]
-            _lib.check(self.lib.evc_encode_windows(t.data_ptr(), x.data_ptr(), yy.data_ptr(), p.data_ptr(), self.ring,
-                                                   meta + 8 * 3 * S, max(wmax, 1), H, W, self.mode, cur.data_ptr(),
-                                                   stride, S, _lib.stream_ptr()), "encode_windows")
-            ev_used[k].record(cs)
-            if nb_next is not None:
-                bnds, prev_hi = nb_next
-                pend = stage(i + 1, bnds, prev_hi)
+                pend = stage(i + 1, b1, [b[1] for b in bnds])
+                bnds = b1
+            cs.wait_event(ev_enc[i % 2])
+            cur, prv = self.enc[i % 3], self.enc[(i - 1) % 3]
             if i == 0:
                 g.dense_pass(cur if S > 1 else cur[0])
+            else:
+                g.step_from_encodings(prv if S > 1 else prv[0], cur if S > 1 else cur[0])
+                if g.refresh_due:
+                    g.dense_pass(cur if S > 1 else cur[0])
+            ev_step[i % 2].record(cs)
+            if i + 1 <= n:  # bin window i + 1 while step i computes
+                ingest(i + 1, bnds, pend)
+            if i == 0:
                 continue
-            g.step_from_encodings(prv if S > 1 else prv[0], cur if S > 1 else cur[0])
-            if g.refresh_due:
-                g.dense_pass(cur if S > 1 else cur[0])
             j = i % 2
             if i >= 3:
                 cs.wait_event(ev_out[j])

@@ -397,6 +397,12 @@ class ConvPlan:
         (the upsample's input): evc_subpixel_input (low-res shadow + tile map, and the sparsify's
         flags dy / any-map fany_hi / norm partials at part_ptr), evc_subpixel_border."""
         L = _lib.lib()
+        # EVC_SUBPIX_FUSED=1: both passes in one launch (evc_subpixel_input_border) -- measured slower at 32
+        # streams (621 vs 423 + 177 us per step), so two launches by default
+        if os.environ.get("EVC_SUBPIX_FUSED") == "1":
+            return [(L.evc_subpixel_input_border, (dlo, dy, part_ptr, self.hwc_interior, self.cp, self.hwc[0].numel(),
+                                                   self.pitch, self.fany_lo_ptr, fany_hi, self.wborder.data_ptr(),
+                                                   self.c_out, self.border.data_ptr(), self.S), "subpixel_input_border")]
         return [(L.evc_subpixel_input, (dlo, dy, part_ptr, self.hwc_interior, self.cp, self.hwc[0].numel(),
                                         self.pitch, self.fany_lo_ptr, fany_hi, self.S), "subpixel_input"),
                 (L.evc_subpixel_border, (dlo, self.wborder.data_ptr(), self.c_out, self.border.data_ptr(), self.S),

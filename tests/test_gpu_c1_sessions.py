@@ -27,7 +27,7 @@ from evc_testutil import max_err
 
 pytestmark = pytest.mark.gpu
 
-N_INC = 16
+N_INC = 16  # S = 8; the benchmarked S = 32 runs 64 chained increments (BASELINE.json configs[0])
 
 
 def _stream_inputs(seed, n):
@@ -40,12 +40,12 @@ def _stream_inputs(seed, n):
     return torch.stack(xs)
 
 
-@pytest.mark.parametrize("S", [8, 32])
-def test_c1_batched_sessions_vs_oracle(S):
+@pytest.mark.parametrize("S,n_inc", [(8, N_INC), (32, 64)])
+def test_c1_batched_sessions_vs_oracle(S, n_inc):
     spec = configs.evflownet_spec(tp=0.0)
     weights = evc.WeightManifest.random_tensors(spec, 0)
     seeds = shard.stream_seeds(0, S)
-    xs = torch.stack([_stream_inputs(sd, N_INC) for sd in seeds], dim=1).contiguous()  # (n+1, S, 4, 256, 256)
+    xs = torch.stack([_stream_inputs(sd, n_inc) for sd in seeds], dim=1).contiguous()  # (n+1, S, 4, 256, 256)
     g = evc.build(spec, weights, refresh_interval=0, sessions=S)
     # the configuration under test really is the S >= 8 one
     cfgs = {n.spec.id: (int(n.plan.cfg.row), int(n.plan.cfg.bn), int(n.plan.cfg.splits))
@@ -59,7 +59,7 @@ def test_c1_batched_sessions_vs_oracle(S):
         assert e <= 1e-4, ("dense", s, e)
     flips, exact_nodes, nodes, worst, perf_rel = 0, 0, 0, 0.0, 0.0
     out = spec.output
-    for i in range(1, N_INC + 1):
+    for i in range(1, n_inc + 1):
         g.step_from_encodings(xs[i - 1], xs[i])
         v, f = g._slot_view(out)
         v, f = v.cpu().numpy(), f.cpu().numpy().astype(bool)
@@ -81,7 +81,7 @@ def test_c1_batched_sessions_vs_oracle(S):
                 exact_nodes += int(p == rp)
                 perf_rel = max(perf_rel, abs(p - rp) / max(1, rde))
             worst = max(worst, max_err(g.integrated_output(session=s).cpu().numpy(), oy))
-    print(f"S={S}: sessions {check}, {N_INC} increments: output-mask flips {flips}, "
+    print(f"S={S}: sessions {check}, {n_inc} increments: output-mask flips {flips}, "
           f"exact per-node meters {exact_nodes}/{nodes}, max meter rel {perf_rel:.2e}, max err {worst:.2e}")
     assert worst <= 1e-4, worst
     # value-derived intermediate masks (the t_p = 0 sparsify flags re-derived from the activation
@@ -90,7 +90,7 @@ def test_c1_batched_sessions_vs_oracle(S):
     assert perf_rel <= 1e-3, perf_rel
     assert flips <= 8, flips
     assert exact_nodes >= 0.8 * nodes, (exact_nodes, nodes)
-    d = g.dense_oracle(xs[N_INC])
+    d = g.dense_oracle(xs[n_inc])
     for s in check:
         dr = g.drift(d, session=s)
         assert dr <= 1e-4 * max(1.0, float(d[s].abs().max())), (s, dr)

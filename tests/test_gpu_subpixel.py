@@ -50,9 +50,12 @@ def _subpixel_on(monkeypatch):
     monkeypatch.setenv("EVC_SUBPIXEL", "1")  # opt-in path (tensors.SUBPIXEL_MAX_COUT)
 
 
-@pytest.mark.parametrize("c,h,w,co,S", [(66, 32, 40, 16, 2), (20, 23, 31, 32, 3), (8, 12, 12, 16, 1),
-                                        (41, 14, 18, 16, 2), (72, 12, 14, 16, 1)])  # channel chunks 32+9, 40
-def test_subpixel_chain_vs_oracle(c, h, w, co, S):
+@pytest.mark.parametrize("c,h,w,co,S,fused", [(66, 32, 40, 16, 2, 0), (20, 23, 31, 32, 3, 0), (8, 12, 12, 16, 1, 0),
+                                              (41, 14, 18, 16, 2, 0), (72, 12, 14, 16, 1, 0),  # chunks 32+9, 40
+                                              (66, 32, 40, 16, 2, 1), (20, 23, 31, 32, 3, 1)])  # one-launch form
+def test_subpixel_chain_vs_oracle(c, h, w, co, S, fused, monkeypatch):
+    if fused:  # evc_subpixel_input_border (input pass + border GEMM in one launch)
+        monkeypatch.setenv("EVC_SUBPIX_FUSED", "1")
     spec = _spec(c, h, w, co)
     weights = evc.WeightManifest.random_tensors(spec, 5)
     g = evc.build(spec, weights, refresh_interval=0, sessions=S)
@@ -79,7 +82,7 @@ def test_subpixel_chain_vs_oracle(c, h, w, co, S):
             e = max_err(g.integrated_output(session=s).cpu().numpy(), ry)
             worst = max(worst, e)
             assert e <= 1e-5, (step, s, e)
-    print(f"sub-pixel chain C={c} {h}x{w} -> {co} S={S}: max err {worst:.2e}")
+    print(f"sub-pixel chain C={c} {h}x{w} -> {co} S={S}{' (one launch)' if fused else ''}: max err {worst:.2e}")
 
 
 def test_subpixel_matches_unfused_graph(monkeypatch):

@@ -2159,7 +2159,7 @@ static int conv_fused_impl(const evc_conv_geom* g, const evc_conv_cfg* cfg_in, c
   a.bias = bias;
   a.dense = dense != 0;
   a.trace = fz::g_trace;
-  a.pf = std::getenv("EVC_NO_ACC_PREFETCH") == nullptr ? 1 : 0;
+  a.pf = std::getenv("EVC_ACC_PREFETCH") != nullptr ? 1 : 0;  // opt-in: measured neutral
   a.eHo = eHo;
   a.eWo = eWo;
   a.oc = oc;

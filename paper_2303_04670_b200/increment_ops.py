@@ -92,15 +92,35 @@ class AccState:
         self.x_acc = self.x_acc + as_tensor(dx)
 
 
-@dataclass
 class FlopCounter:
-    """2 ops per multiply-accumulate (increment_ops.py:97-113)."""
+    """2 ops per multiply-accumulate (increment_ops.py:97-113).
 
-    performed: int = 0
-    dense_equiv: int = 0
+    Same fields and methods as the reference dataclass.  ``add`` also takes a device int64 tensor for
+    ``performed`` (the op API's meters are computed on the GPU): it is kept on the device and resolved,
+    with one host read for everything pending, only when ``performed`` is read -- the operators
+    themselves never synchronise the host for the meter."""
 
-    def add(self, performed: int, dense_equiv: int) -> None:
-        self.performed += int(performed)
+    def __init__(self, performed: int = 0, dense_equiv: int = 0):
+        self._performed = int(performed)
+        self._pending = []
+        self.dense_equiv = int(dense_equiv)
+
+    @property
+    def performed(self) -> int:
+        if self._pending:
+            self._performed += int(torch.stack([t.reshape(()) for t in self._pending]).sum().item())
+            self._pending = []
+        return self._performed
+
+    @performed.setter
+    def performed(self, v: int) -> None:
+        self._performed, self._pending = int(v), []
+
+    def add(self, performed, dense_equiv: int) -> None:
+        if isinstance(performed, torch.Tensor):
+            self._pending.append(performed.to(torch.int64))
+        else:
+            self._performed += int(performed)
         self.dense_equiv += int(dense_equiv)
 
     def reset(self) -> None:
@@ -109,6 +129,12 @@ class FlopCounter:
 
     def snapshot(self):
         return self.performed, self.dense_equiv
+
+    def __eq__(self, other):
+        return isinstance(other, FlopCounter) and self.snapshot() == other.snapshot()
+
+    def __repr__(self):
+        return f"FlopCounter(performed={self.performed}, dense_equiv={self.dense_equiv})"
 
 
 def _zeros_incr(shape, tile: TileShape, device):
@@ -166,7 +192,7 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
                                                      _lib.ptr(perf)), s), "conv_mask")
         fn, args = plan.scatter(din, dout, fresh_out=True)
         _lib.check(fn(*args, s), "conv_scatter")
-        meter.add(int(perf.item()), 0)
+        meter.add(perf, 0)
         return IncrementTensor(yv, TileMask(yf, tile))
     if plan.path == "fused":
         fany = torch.zeros(plan.gi[0] * plan.gi[1], dtype=torch.uint8, device=dev)
@@ -176,9 +202,12 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
         _lib.check(pre[0](*pre[1], s), "to_hwc")
         fn, args = plan.fused(din, dout, fany=_lib.ptr(fany), mpart=_lib.ptr(mpart))
         _lib.check(fn(*args, s), "conv_fused")
-        cnt, b = (int(v) for v in mpart.view(-1, 2).sum(dim=0).tolist())
+        # performed (increment_ops.py:145-160): 0 when no input flag is live, the dense count when all are,
+        # else 2 * C_out * the weighted live-tap term -- on the device, no host read
+        cb = mpart.view(-1, 2).sum(dim=0)
         n_flags = c_in * plan.gi[0] * plan.gi[1]
-        perf = 0 if cnt == 0 else (plan.dense_flops if cnt == n_flags else 2 * c_out * b)
+        perf = torch.where(cb[0] == 0, torch.zeros_like(cb[1]),
+                           torch.where(cb[0] == n_flags, torch.full_like(cb[1], int(plan.dense_flops)), 2 * c_out * cb[1]))
         meter.add(perf, 0)
         return IncrementTensor(yv, TileMask(yf, tile))
     T = yf.shape[1] * yf.shape[2]
@@ -191,7 +220,7 @@ def inc_conv2d(x: IncrementTensor, weight, params: ConvParams, meter: FlopCounte
     ws = torch.empty(max(plan.ws_floats, 1), dtype=torch.float32, device=dev)
     fn, args = plan.gemm(din, dout, None, (_lib.ptr(tiles), _lib.ptr(i32) + 4), ws.data_ptr())
     _lib.check(fn(*args, s), "conv_gemm")
-    meter.add(int(perf.item()), 0)
+    meter.add(perf, 0)
     return IncrementTensor(yv, TileMask(yf, tile))
 
 
@@ -224,7 +253,7 @@ def inc_linear(x_flat: IncrementTensor, matrix, meter: FlopCounter) -> Increment
     dout = _lib.tdesc(_lib.ptr(y), None, 0, 0, rows, 1, 1, 1, 1)
     _lib.check(lib.evc_linear(din, _lib.ptr(matrix), None, dout, rows, 0, _lib.ptr(perf), _lib.ptr(ws), 1,
                               _lib.stream_ptr()), "linear")
-    meter.add(int(perf.item()), 0)
+    meter.add(perf, 0)
     flags = torch.ones(grid_shape(out_shape, tile), dtype=torch.uint8, device=dev)
     return IncrementTensor(y.reshape(out_shape), TileMask(flags, tile))
 

@@ -2,8 +2,10 @@
 
 Rounds the residual-corrected increment to multiples of k on the GPU and
 carries the round-off forward (sparsify.py:54-78).  The per-op
-``sparsify_step`` keeps ``norm_ema``/``k`` as Python floats like the
-reference; the Graph runtime keeps them as device float64 scalars.
+``sparsify_step`` exposes ``norm_ema``/``k`` as Python floats like the
+reference, but keeps them as a device float64 pair that is read back only when
+an attribute is read (the operators never synchronise the host); the Graph
+runtime keeps them as device float64 scalars.
 """
 
 from __future__ import annotations
@@ -29,8 +31,30 @@ class SparsifyState:
         self.tp = float(tp)
         self.ema_decay = float(ema_decay)
         self.delta = torch.zeros(self.shape, dtype=torch.float32, device="cuda")
-        self.norm_ema = 0.0
-        self.k = float(k)
+        self._sc = torch.tensor([0.0, float(k)], dtype=torch.float64, device="cuda")  # (norm_ema, k)
+
+    @property
+    def norm_ema(self) -> float:
+        return float(self._sc[0].item())
+
+    @norm_ema.setter
+    def norm_ema(self, v: float) -> None:
+        self._sc[0] = float(v)
+
+    @property
+    def k(self) -> float:
+        return float(self._sc[1].item())
+
+    @k.setter
+    def k(self, v: float) -> None:
+        self._sc[1] = float(v)
+
+    def _fold(self, sc) -> None:
+        """Take norm_ema (and k when t_p > 0, sparsify.py:76) from a device pair the kernel updated."""
+        if self.tp > 0:
+            self._sc.copy_(sc)
+        else:
+            self._sc[0:1].copy_(sc[0:1])
 
     def reset(self, dense_input) -> None:
         """Clear the residual and seed the norm at a dense pass (sparsify.py:43-51)."""
@@ -40,16 +64,13 @@ class SparsifyState:
         self.delta = torch.zeros(self.shape, dtype=torch.float32, device=x.device)
         nb = 64
         part = torch.empty(nb, dtype=torch.float64, device=x.device)
-        sc = torch.tensor([0.0, self.k], dtype=torch.float64, device=x.device)
+        sc = self._sc.clone()
         lib = _lib.lib()
         s = _lib.stream_ptr()
         _lib.check(lib.evc_sumsq_dense(_lib.ptr(x), 0, x.numel(), _lib.ptr(part), nb, 1, s), "sumsq")
         _lib.check(lib.evc_sparsify_finalize(_lib.ptr(part), nb, _lib.ptr(sc), _lib.ptr(sc) + 8, self.tp,
                                              self.ema_decay, 1, 1, s), "sparsify_finalize")
-        ne, k = sc.tolist()
-        self.norm_ema = ne
-        if self.tp > 0:
-            self.k = k
+        self._fold(sc)
 
 
 def sparsify_step(x: IncrementTensor, state: SparsifyState) -> IncrementTensor:
@@ -65,15 +86,12 @@ def sparsify_step(x: IncrementTensor, state: SparsifyState) -> IncrementTensor:
     lib = _lib.lib()
     dx = x.desc()
     part = torch.zeros(int(lib.evc_sparsify_partials(dx)), dtype=torch.float64, device=dev)
-    sc = torch.tensor([state.norm_ema, state.k], dtype=torch.float64, device=dev)
+    sc = state._sc.clone()
     s = _lib.stream_ptr()
     dy = _lib.tdesc(_lib.ptr(yv), _lib.ptr(yf), 0, 0, c, h, w, tile.h, tile.w)
     ticket = torch.zeros(1, dtype=torch.int32, device=dev)
     _lib.check(lib.evc_sparsify(dx, _lib.ptr(state.delta), 0, _lib.ptr(dlive), dy, _lib.ptr(sc) + 8, _lib.ptr(sc),
                                 state.tp, state.ema_decay, _lib.ptr(part), _lib.ptr(ticket), None, 0, 0, 0, None, 1, 0, 1, s),
                "sparsify")
-    ne, k = sc.tolist()
-    state.norm_ema = ne
-    if state.tp > 0:
-        state.k = k
+    state._fold(sc)
     return IncrementTensor(yv, TileMask(yf, tile))

@@ -167,12 +167,13 @@ __device__ __forceinline__ void subpix_input_body(const TView& x, uint8_t* __res
       const float r = (k & 1) ? __fadd_rn(__fmul_rn(col[k / 2 + 1], 0.75f), __fmul_rn(col[k / 2 + 2], 0.25f))
                               : __fadd_rn(__fmul_rn(col[k / 2], 0.25f), __fmul_rn(col[k / 2 + 1], 0.75f));
       const float rl = __shfl_up_sync(0xffffffffu, r, 1), rr = __shfl_down_sync(0xffffffffu, r, 1);
-      const float oe = __fadd_rn(0.0f, __fadd_rn(__fmul_rn(rl, 0.25f), __fmul_rn(r, 0.75f)));
-      const float oo = __fadd_rn(0.0f, __fadd_rn(__fmul_rn(r, 0.75f), __fmul_rn(rr, 0.25f)));
+      // (the sparsify's "0 + y" only turns -0 into +0: neither the squares nor the magnitude bits see it)
+      const float oe = __fadd_rn(__fmul_rn(rl, 0.25f), __fmul_rn(r, 0.75f));
+      const float oo = __fadd_rn(__fmul_rn(r, 0.75f), __fmul_rn(rr, 0.25f));
       if (own) {
         ss = __fmaf_rn(oe, oe, ss);
         ss = __fmaf_rn(oo, oo, ss);
-        const uint32_t be = __float_as_uint(oe) & 0x7fffffffu, bo = __float_as_uint(oo) & 0x7fffffffu;
+        const uint32_t be = __float_as_uint(oe), bo = __float_as_uint(oo);  // sign bits masked once below
         if (k >= x.th) {  // (two tile rows)
           n10 |= be;
           n11 |= bo;
@@ -182,6 +183,10 @@ __device__ __forceinline__ void subpix_input_body(const TView& x, uint8_t* __res
         }
       }
     }
+    n00 &= 0x7fffffffu;
+    n01 &= 0x7fffffffu;
+    n10 &= 0x7fffffffu;
+    n11 &= 0x7fffffffu;
     if (n00) s_fy[ch][0][tje] = 1;  // (benign: all store 1)
     if (n01) s_fy[ch][0][tjo] = 1;
     if (n10) s_fy[ch][1][tje] = 1;
@@ -233,7 +238,9 @@ __global__ void __launch_bounds__(SP_THREADS) k_subpix_input(TView x, uint8_t* _
 constexpr int SB_C = 32, SB_SPB = 1;  // channels per K step, sessions per CTA (1: measured fastest)
 constexpr int SB_WL = 20;             // low-res window along a line: 34 positions -> <= 19 columns
 
-constexpr int SB_SMEM_FLOATS = SB_C * 3 * 32 + SB_C * 2 * 3 * 32 + SB_C * 36 + SB_C * 2 * SB_WL;
+static_assert(SB_SPB == 1, "the split-channel reduction below assumes one session per CTA");
+constexpr int SB_RED = 4 * 32 * 4;  // split mode: the second channel half's partial sums [og][pos][4]
+constexpr int SB_SMEM_FLOATS = SB_C * 3 * 32 + SB_C * 2 * 3 * 32 + SB_C * 36 + SB_C * 2 * SB_WL + SB_RED;
 
 // one CTA of the border GEMM: (bx = 32 positions, by = line + 32 output channels, bz = session group);
 // shared memory carved from `sm` (16-byte aligned, SB_SMEM_FLOATS floats)
@@ -251,7 +258,11 @@ __device__ __forceinline__ void subpix_border_body(const TView& x, const float* 
   const int fixed = L == 0 ? 0 : (L == 1 ? Ho - 1 : (L == 2 ? 0 : Wo - 1));
   const int other = L == 0 ? 1 : Ho - 2;  // row lines: the corner column's other in-image row
   const int kout = (L == 0 || L == 2) ? 0 : 2;
-  const int pl = threadIdx.x & 31, og = threadIdx.x >> 5, pos = p0 + pl;
+  const int pl = threadIdx.x & 31, pos = p0 + pl;
+  // C_out <= 16 (one 16-channel group): warps 4-7 would idle in the FMA loop, so the warps split the input
+  // channels of every K step in two halves instead (fixed order: half 0's sum + half 1's sum)
+  const bool split = co - (by / 4) * 32 <= 16;
+  const int og = split ? (threadIdx.x >> 5) & 3 : threadIdx.x >> 5, hf = split ? (int)(threadIdx.x >> 7) : 0;
   const int no = min(32, co - oc0), nss = min(SB_SPB, S - s0);
   const bool corner = rowline && (pos == 0 || pos == Wo - 1);
   // the two low-res lines across the line (taps of the fixed coordinate) and the window along it
@@ -337,7 +348,8 @@ __device__ __forceinline__ void subpix_border_body(const TView& x, const float* 
       __syncthreads();
       if (pos < len && 4 * og < no) {
         float a4[4] = {acc[sl][0], acc[sl][1], acc[sl][2], acc[sl][3]};
-        for (int c = 0; c < nc; ++c) {
+        const int ch0 = split ? hf * ((nc + 1) >> 1) : 0, ch1 = split && !hf ? (nc + 1) >> 1 : nc;
+        for (int c = ch0; c < ch1; ++c) {
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
             const float uk = sU[c][pl + k];
@@ -367,6 +379,17 @@ __device__ __forceinline__ void subpix_border_body(const TView& x, const float* 
       }
     }
   }
+  if (split) {  // add the second half's partial sums (every thread reaches these barriers)
+    float* red = sm + SB_C * 9 * 32 + SB_C * 36 + SB_C * 2 * SB_WL;  // [og][pos][4]
+    __syncthreads();
+    if (hf)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[(og * 32 + pl) * 4 + j] = acc[0][j];
+    __syncthreads();
+    if (hf) return;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[0][j] = __fadd_rn(acc[0][j], red[(og * 32 + pl) * 4 + j]);
+  }
   if (pos < len) {
     const int li = L == 0 ? pos : (L == 1 ? Wo + pos : (L == 2 ? 2 * Wo + pos : 2 * Wo + Ho + pos));
 #pragma unroll
@@ -380,7 +403,10 @@ __device__ __forceinline__ void subpix_border_body(const TView& x, const float* 
   }
 }
 
-__global__ void __launch_bounds__(SP_THREADS, 4) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
+#ifndef EVC_SB_MINB
+#define EVC_SB_MINB 4
+#endif
+__global__ void __launch_bounds__(SP_THREADS, EVC_SB_MINB) k_subpix_border(TView x, const float* __restrict__ w, int co, int S,
                                                                float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
           const float* p0 = rc + ra * a.XC + o0;
           const float* p1 = rc + ra * a.XC + o1;
           float* d = wr ? dcol + ra * rstride : nullptr;
-          uint32_t nzb = 0;  // OR of the magnitude bits: nonzero iff some value != +-0
+          uint32_t nzb = 0;  // OR of the value bits: some value != +-0 iff a magnitude bit is set
           // same float32 op order as upsample_at (rows first, then columns)
           auto row = [&](int k) {
             const float up = a.mode == 0 ? p0[k * a.XC]
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
               dk[tl] = __fsub_rn(ov, h);
             }
             ssf = __fmaf_rn(ov, ov, ssf);
-            nzb |= __float_as_uint(ov) & 0x7fffffffu;
+            nzb |= __float_as_uint(ov);  // (sign bits masked once per tile below)
           };
           if (rb - ra == 6) {  // the 6-row tiles of the reference default: fully unrolled
 #pragma unroll
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(US_THREADS, 4) k_up_sparsify(USArgs a) {
           } else {
             for (int k = 0; k < rb - ra; ++k) row(k);
           }
-          if (nzb) s_ny[ti] = 1;
+          if (nzb & 0x7fffffffu) s_ny[ti] = 1;
         }
         }
         ss += (double)ssf;

@@ -1267,10 +1267,15 @@ class Graph:
         """Full dense forward that re-seeds every accumulator and baseline."""
         self._check_input_shape(x)
         self._load_input(x)
-        # the device work of a refresh is static: after one eager run (lazy plans, reset tables) it is
-        # captured once and every later dense_pass / refresh is one graph replay
-        if self.use_cuda_graph and (self._dense_graph is not None or self._dense_eager_runs > 0):
-            if self._dense_graph is None:
+        # the device work of a refresh is static: the first dense pass runs eagerly (lazy plans, reset
+        # tables) and is captured right after it (capture only records), so every later dense_pass /
+        # refresh -- e.g. one due inside a timed run -- is a single graph replay with no capture cost
+        if self.use_cuda_graph and self._dense_graph is not None:
+            self._dense_graph.replay()
+        else:
+            self._dense_device_work()
+            self._dense_eager_runs += 1
+            if self.use_cuda_graph:
                 g = torch.cuda.CUDAGraph()
                 side = torch.cuda.Stream(device=self.device)
                 side.wait_stream(torch.cuda.current_stream())
@@ -1278,10 +1283,6 @@ class Graph:
                     self._dense_device_work()
                 torch.cuda.current_stream().wait_stream(side)
                 self._dense_graph = g
-            self._dense_graph.replay()
-        else:
-            self._dense_device_work()
-            self._dense_eager_runs += 1
         for i, node in enumerate(self._meter_nodes):
             de = self._dense_static[i]
             self._perf_host[i] += de * self.S

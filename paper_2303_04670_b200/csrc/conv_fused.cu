@@ -42,6 +42,12 @@
 #include <mutex>
 
 #include "conv_common.cuh"
+// 1: the MMA issuer warp walks its K loop converged and one elected lane issues each tcgen05.mma / commit
+// (operands in uniform registers, no per-MMA waterfall loop around a single active lane): 12 % faster on
+// the tap-mode BN = 128 layers, whose single issuing thread was the bottleneck.  0: lane 0 issues alone.
+#ifndef EVC_MMA_WARP
+#define EVC_MMA_WARP 1
+#endif
 #include "tcgen05.cuh"
 
 namespace evc {
@@ -772,7 +778,16 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
     }
     __syncwarp();
   } else if (warp == 1) {
+#if EVC_MMA_WARP
+    // the whole warp walks the K loop with warp-uniform operands; one elected lane issues each MMA / commit
+#define MMA_ mma_w
+#define COMMIT_ commit_w
+    {  // ------------------------------------------------ MMA issuer
+#else
+#define MMA_ mma
+#define COMMIT_ commit
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
+#endif
       for (int i = 0; i < nk; ++i) {
         const int st = i % NS;
         bar_spin(tma_bar(st), (i / NS) & 1);
@@ -788,10 +803,10 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {  // K=8 tf32 = 32 bytes = +2 in the descriptor's address field
             if (kk >= nkk) break;
-            mma(tmem, dl + 2 * kk, db + 2 * kk, idp, (i || kk) ? 1u : 0u);  // small terms first
-            mma(tmem, dh + 2 * kk, db + 2 * kk, idp, 1u);
+            MMA_(tmem, dl + 2 * kk, db + 2 * kk, idp, (i || kk) ? 1u : 0u);  // small terms first
+            MMA_(tmem, dh + 2 * kk, db + 2 * kk, idp, 1u);
           }
-          commit(empty_bar(st));
+          COMMIT_(empty_bar(st));
           continue;
         }
         if (CAT && D > 0) {
@@ -810,14 +825,14 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (kk >= nkk) break;
-              mma(tj, da + 2 * kk, dbh + 2 * kk, IDESC, (seg0 && t == 0 && kk == 0) ? 0u : 1u);  // hi.hi
-              mma(ts, da + 2 * kk, dbl + 2 * kk, IDESC, (i == 0 && t == 0 && kk == 0) ? 0u : 1u);  // hi.lo
-              mma(ts, dl + 2 * kk, dbh + 2 * kk, IDESC, 1u);                                      // lo.hi
+              MMA_(tj, da + 2 * kk, dbh + 2 * kk, IDESC, (seg0 && t == 0 && kk == 0) ? 0u : 1u);  // hi.hi
+              MMA_(ts, da + 2 * kk, dbl + 2 * kk, IDESC, (i == 0 && t == 0 && kk == 0) ? 0u : 1u);  // hi.lo
+              MMA_(ts, dl + 2 * kk, dbh + 2 * kk, IDESC, 1u);                                      // lo.hi
             }
           }
-          commit(empty_bar(st));
-          if (i % D == D - 1 || i == nk - 1) commit(seg_bar(j));
-          if (i == 0) TR(12);
+          COMMIT_(empty_bar(st));
+          if (i % D == D - 1 || i == nk - 1) COMMIT_(seg_bar(j));
+          if (i == 0 && lane == 0) TR(12);
           continue;
         }
         for (int t = 0; t < taps; ++t) {
@@ -831,8 +846,8 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {  // K=8 tf32 = 32 bytes = +2 in the descriptor's address field
               if (kk >= nkk) break;
-              mma(tj, da + 2 * kk, db + 2 * kk, IDESC2, (i >= NA || kk || !first) ? 1u : 0u);
-              mma(tc, dl + 2 * kk, db + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
+              MMA_(tj, da + 2 * kk, db + 2 * kk, IDESC2, (i >= NA || kk || !first) ? 1u : 0u);
+              MMA_(tc, dl + 2 * kk, db + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
             }
           } else {
             const uint32_t tmain = tmem, tcorr = tmem + (uint32_t)BN;
@@ -840,18 +855,20 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (kk >= nkk) break;
-              mma(tmain, da + 2 * kk, dbh + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
-              mma(tcorr, da + 2 * kk, dbl + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
-              mma(tcorr, dl + 2 * kk, dbh + 2 * kk, IDESC, 1u);
+              MMA_(tmain, da + 2 * kk, dbh + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
+              MMA_(tcorr, da + 2 * kk, dbl + 2 * kk, IDESC, (i || kk || !first) ? 1u : 0u);
+              MMA_(tcorr, dl + 2 * kk, dbh + 2 * kk, IDESC, 1u);
             }
           }
         }
-        commit(empty_bar(st));
-        if (i == 0) TR(12);
+        COMMIT_(empty_bar(st));
+        if (i == 0 && lane == 0) TR(12);
       }
-      commit(acc_bar);
-      TR(5);
+      COMMIT_(acc_bar);
+      if (lane == 0) TR(5);
     }
+#undef MMA_
+#undef COMMIT_
     __syncwarp();
   } else if (warp < 4) {
     if (!a.dense) {
@@ -1256,13 +1273,20 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
       __syncwarp();
     }
   } else if (warp == 1) {  // --------------------------------------------------- MMA issuer
+#if EVC_MMA_WARP
+#define MMA_ mma_w
+#define COMMIT_ commit_w
+#else
+#define MMA_ mma
+#define COMMIT_ commit
+#endif
     // TMEM buffer use = one accumulation segment of DS K-blocks (the whole item when a.drain == 0);
     // segment gs fills buffer gs & 1 while the epilogue promotes segment gs - 1 into registers
     int g = 0, gs = 0, it = 0;  // it: live items so far (small block it & 1 when SS)
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int reg = item / nb, s = reg / R, rr = reg % R;
       if (!region_live_warp(a, s, rr)) continue;
-      if (lane == 0) {
+      if (EVC_MMA_WARP || lane == 0) {  // (warp-wide issue: every lane walks the loop, one elected lane issues)
         uint32_t tb = tmem;
         int ab = 0;
         const uint32_t tsm = tmem + (uint32_t)(2 * BN + (it & 1) * BN);
@@ -1287,8 +1311,8 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (kk >= nkk) break;
-              mma(tb, dl + 2 * kk, db + 2 * kk, idp, (!seg0 || kk) ? 1u : 0u);
-              mma(tb, dh + 2 * kk, db + 2 * kk, idp, 1u);
+              MMA_(tb, dl + 2 * kk, db + 2 * kk, idp, (!seg0 || kk) ? 1u : 0u);
+              MMA_(tb, dh + 2 * kk, db + 2 * kk, idp, 1u);
             }
           } else {
             const int taps = a.row ? a.kw : 1;
@@ -1301,33 +1325,35 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                   if (kk >= nkk) break;
-                  mma(tb, da + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);      // hi.hi
-                  mma(tsm, da + 2 * kk, dbl + 2 * kk, IDESC, (!firsts || kk) ? 1u : 0u);  // hi.lo
-                  mma(tsm, dl + 2 * kk, db + 2 * kk, IDESC, 1u);                           // lo.hi
+                  MMA_(tb, da + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);      // hi.hi
+                  MMA_(tsm, da + 2 * kk, dbl + 2 * kk, IDESC, (!firsts || kk) ? 1u : 0u);  // hi.lo
+                  MMA_(tsm, dl + 2 * kk, db + 2 * kk, IDESC, 1u);                           // lo.hi
                 }
               } else {
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk) {
                   if (kk >= nkk) break;
-                  mma(tb, da + 2 * kk, db + 2 * kk, IDESC2, (!first || kk) ? 1u : 0u);           // hi.[hi|lo]
-                  mma(tb + 2 * BN, dl + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);  // lo.hi
+                  MMA_(tb, da + 2 * kk, db + 2 * kk, IDESC2, (!first || kk) ? 1u : 0u);           // hi.[hi|lo]
+                  MMA_(tb + 2 * BN, dl + 2 * kk, db + 2 * kk, IDESC, (!first || kk) ? 1u : 0u);  // lo.hi
                 }
               }
             }
           }
-          commit(empty_bar(st));
+          COMMIT_(empty_bar(st));
           if (kb % DS == DS - 1 || kb == nk - 1) {
-            commit(tfull_bar(ab));
+            COMMIT_(tfull_bar(ab));
             ++gs;
           }
         }
-        if (SS) commit(sfull_bar(it & 1));
+        if (SS) COMMIT_(sfull_bar(it & 1));
       } else {
         g += nk;
       }
       ++it;
       __syncwarp();
     }
+#undef MMA_
+#undef COMMIT_
   } else if (warp < 4) {  // ---------------------------------------------------- flags + meter
     if (!a.dense) {
       const int Qs = R * nb;

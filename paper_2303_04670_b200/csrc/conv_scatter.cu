@@ -28,6 +28,10 @@
 #include "conv_common.cuh"
 #include "tcgen05.cuh"
 
+#ifndef EVC_MMA_WARP
+#define EVC_MMA_WARP 1  // as conv_fused.cu: the MMA warp walks its loop converged, one elected lane issues
+#endif
+
 namespace evc {
 namespace sc {
 
@@ -180,7 +184,14 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
     }
     __syncwarp();
   } else if (warp == 12) {  // ------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+#if EVC_MMA_WARP
+#define MMA_ mma_w
+#define COMMIT_ commit_w
+#else
+#define MMA_ mma
+#define COMMIT_ commit
+#endif
+    if (EVC_MMA_WARP || lane == 0) {  // (warp-wide: every lane walks the loop, one elected lane issues)
       int it = 0, u = 0, q = 0;
       for (int g = blockIdx.x; g < ngroups; g += gridDim.x, ++q) {
         bar_spin(afull, q & 1);
@@ -200,18 +211,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_conv_scatter(const __grid_consta
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
               if (kk >= nkk) break;
-              mma(d, dah + 2 * kk, dbh + 2 * kk, IDESC, (kb || kk) ? 1u : 0u);  // hi.hi
-              mma(d, dah + 2 * kk, dbl + 2 * kk, IDESC, 1u);                    // hi.lo
-              mma(d, dal + 2 * kk, dbh + 2 * kk, IDESC, 1u);                    // lo.hi
+              MMA_(d, dah + 2 * kk, dbh + 2 * kk, IDESC, (kb || kk) ? 1u : 0u);  // hi.hi
+              MMA_(d, dah + 2 * kk, dbl + 2 * kk, IDESC, 1u);                    // hi.lo
+              MMA_(d, dal + 2 * kk, dbh + 2 * kk, IDESC, 1u);                    // lo.hi
             }
-            commit(bempty(st));
+            COMMIT_(bempty(st));
           }
-          commit(tfull(ab));
+          COMMIT_(tfull(ab));
         }
-        commit(aempty);  // the gather may overwrite A once these MMAs have completed
+        COMMIT_(aempty);  // the gather may overwrite A once these MMAs have completed
       }
     }
     __syncwarp();
+#undef MMA_
+#undef COMMIT_
   } else {  // ---------------------------------------------------------------------- epilogue
     // per unit: the accumulator (site x [tap][16 channels]) goes TMEM -> shared memory, then every
     // thread forms output patch points: patch point (py, px) of tile j, channel n sums, in tap

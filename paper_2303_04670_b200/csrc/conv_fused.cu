@@ -48,6 +48,9 @@
 #ifndef EVC_MMA_WARP
 #define EVC_MMA_WARP 1
 #endif
+#ifndef EVC_TMA_WARP  // the same for the TMA producer warp
+#define EVC_TMA_WARP 0
+#endif
 #include "tcgen05.cuh"
 
 namespace evc {
@@ -748,35 +751,50 @@ __global__ void __launch_bounds__(THREADS, (BN <= 16 ? 2 : 1)) k_conv_fused(cons
   };
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ TMA producer
+#if EVC_TMA_WARP
+#define ARRIVE_TX_ bar_arrive_tx_w
+#define BULK_ bulk_load_w
+#define TMA3_ tma_load_3d_w
+#define TMA4_ tma_load_4d_w
+#else
+#define ARRIVE_TX_ bar_arrive_tx
+#define BULK_ bulk_load
+#define TMA3_ tma_load_3d
+#define TMA4_ tma_load_4d
+#endif
+    if (EVC_TMA_WARP || lane == 0) {  // ------------------------------------------------ TMA producer
       for (int i = 0; i < nk; ++i) {
         const int st = i % NS;
         const int kb = kb0 + i;
         const uint32_t abuf = sb + st * STAGE;
         if (i < npre) {
-          bar_arrive_tx(tma_bar(st), 2 * A_TX);  // weights already in flight
+          ARRIVE_TX_(tma_bar(st), 2 * A_TX);  // weights already in flight
         } else {
           bar_spin(empty_bar(st), ((i / NS) & 1) ^ 1);
-          bar_arrive_tx(tma_bar(st), 2 * A_TX + B_BYTES);
-          bulk_load(abuf + 2 * A_HALF, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
+          ARRIVE_TX_(tma_bar(st), 2 * A_TX + B_BYTES);
+          BULK_(abuf + 2 * A_HALF, wsrc + (int64_t)kb * B_BYTES, B_BYTES, tma_bar(st));
         }
         if (a.row) {  // kernel row r of the flattened padded shadow: 128 + kw - 1 pixel rows
           const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
           const int i0 = rr * a.VM + r * a.P;
-          tma_load_3d(abuf, &tmap, 2 * c0, i0, s, tma_bar(st));  // chunk = [32 heads | 32 tails]
-          tma_load_3d(abuf + A_HALF, &tmap, 2 * c0 + 32, i0, s, tma_bar(st));
+          TMA3_(abuf, &tmap, 2 * c0, i0, s, tma_bar(st));  // chunk = [32 heads | 32 tails]
+          TMA3_(abuf + A_HALF, &tmap, 2 * c0 + 32, i0, s, tma_bar(st));
         } else {  // one box = the whole RH x RW region for this tap (padded coordinates)
           const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
           const int r = tap / a.kw, qq = tap % a.kw;
           const int xs = xlo * a.stride + qq, ys = ulo * a.stride + r;
-          tma_load_4d(abuf, &tmap, 2 * c0, xs, ys, s, tma_bar(st));
-          tma_load_4d(abuf + A_HALF, &tmap, 2 * c0 + 32, xs, ys, s, tma_bar(st));
+          TMA4_(abuf, &tmap, 2 * c0, xs, ys, s, tma_bar(st));
+          TMA4_(abuf + A_HALF, &tmap, 2 * c0 + 32, xs, ys, s, tma_bar(st));
         }
-        if (i == 0) TR(3);
+        if (i == 0 && lane == 0) TR(3);
       }
-      TR(11);
+      if (lane == 0) TR(11);
     }
     __syncwarp();
+#undef ARRIVE_TX_
+#undef BULK_
+#undef TMA3_
+#undef TMA4_
   } else if (warp == 1) {
 #if EVC_MMA_WARP
     // the whole warp walks the K loop with warp-uniform operands; one elected lane issues each MMA / commit
@@ -1237,11 +1255,22 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
   pdl_wait();
 
   if (warp == 0) {  // ---------------------------------------------------------- TMA producer
+#if EVC_TMA_WARP
+#define ARRIVE_TX_ bar_arrive_tx_w
+#define BULK_ bulk_load_w
+#define TMA3_ tma_load_3d_w
+#define TMA4_ tma_load_4d_w
+#else
+#define ARRIVE_TX_ bar_arrive_tx
+#define BULK_ bulk_load
+#define TMA3_ tma_load_3d
+#define TMA4_ tma_load_4d
+#endif
     int g = 0;  // global stage counter
     for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
       const int nblk = item % nb, reg = item / nb, s = reg / R, rr = reg % R;
       if (!region_live_warp(a, s, rr)) continue;
-      if (lane == 0) {
+      if (EVC_TMA_WARP || lane == 0) {
         const char* wsrc = reinterpret_cast<const char*>(a.wpack) + (int64_t)nblk * a.nkb * B_BYTES;
         int ulo = 0, xlo = 0;
         if (!a.row) {
@@ -1252,19 +1281,19 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
           const int st = g % NS;
           if (g >= NS) bar_spin(empty_bar(st), ((g / NS) & 1) ^ 1);
           const uint32_t abuf = sb + st * STAGE;
-          bar_arrive_tx(full_bar(st), 2 * A_TX + B_BYTES);
-          bulk_load(abuf + 2 * A_HALF, wsrc + (int64_t)kb * B_BYTES, B_BYTES, full_bar(st));
+          ARRIVE_TX_(full_bar(st), 2 * A_TX + B_BYTES);
+          BULK_(abuf + 2 * A_HALF, wsrc + (int64_t)kb * B_BYTES, B_BYTES, full_bar(st));
           if (a.row) {
             const int r = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
             const int i0 = rr * a.VM + r * a.P;
-            tma_load_3d(abuf, &tmap, 2 * c0, i0, s, full_bar(st));
-            tma_load_3d(abuf + A_HALF, &tmap, 2 * c0 + 32, i0, s, full_bar(st));
+            TMA3_(abuf, &tmap, 2 * c0, i0, s, full_bar(st));
+            TMA3_(abuf + A_HALF, &tmap, 2 * c0 + 32, i0, s, full_bar(st));
           } else {
             const int tap = kb / a.cchunks, c0 = (kb % a.cchunks) * 32;
             const int r = tap / a.kw, qq = tap % a.kw;
             const int xs = xlo * a.stride + qq, ys = ulo * a.stride + r;
-            tma_load_4d(abuf, &tmap, 2 * c0, xs, ys, s, full_bar(st));
-            tma_load_4d(abuf + A_HALF, &tmap, 2 * c0 + 32, xs, ys, s, full_bar(st));
+            TMA4_(abuf, &tmap, 2 * c0, xs, ys, s, full_bar(st));
+            TMA4_(abuf + A_HALF, &tmap, 2 * c0 + 32, xs, ys, s, full_bar(st));
           }
         }
       } else {
@@ -1272,6 +1301,10 @@ __global__ void __launch_bounds__(persist_threads<BN>(), (BN <= 16 ? 2 : 1)) k_c
       }
       __syncwarp();
     }
+#undef ARRIVE_TX_
+#undef BULK_
+#undef TMA3_
+#undef TMA4_
   } else if (warp == 1) {  // --------------------------------------------------- MMA issuer
 #if EVC_MMA_WARP
 #define MMA_ mma_w
